@@ -1,0 +1,164 @@
+"""Generate the golden parity fixtures from the REAL reference.
+
+Runs only in the build container (imports /root/reference/pkg/src).  For
+each case it builds the reference dependence graph (optionally transformed
+by the reference's own passes), serialises it with
+`paper_2501_05408_b200.ir.from_pdg(...).to_json()`, runs the reference
+oracle `recten.runtime.reference_execute`, and writes
+
+    tests/golden/cases/<case>.json   graph + bounds + seed + meta
+    tests/golden/cases/<case>.npz    inputs (in_*) and reference outputs (out_*)
+
+Cases the reference itself cannot evaluate (eager-fold hazard on
+transformed graphs) are recorded with their error text, not skipped
+silently.  Also writes the benchmark graphs under tests/golden/graphs/.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
+
+import programs as P  # noqa: E402
+from paper_2501_05408_b200 import ir  # noqa: E402
+
+CASES = os.path.join(HERE, "cases")
+GRAPHS = os.path.join(HERE, "graphs")
+
+
+def variants():
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+
+    def plain(g):
+        return g
+
+    def vec(g):
+        tr.vectorize_all(g)
+        return g
+
+    def vec_fuse(g):
+        tr.vectorize_all(g)
+        tr.fuse(g)
+        return g
+
+    def lift(g):
+        tr.lift_incremental_patterns(g)
+        return g
+
+    return {"plain": plain, "vec": vec, "vecfuse": vec_fuse, "lift": lift}
+
+
+def bind(g, bounds):
+    for d, b in g.dim_bound.items():
+        if bounds and b.name in bounds:
+            g.bindings[b] = bounds[b.name]
+
+
+def write_case(name, g, bounds, inputs, seed, meta):
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+    doc = {"name": name, "bounds": bounds, "seed": seed, "meta": meta}
+    arrays = {}
+    for k, v in (inputs or {}).items():
+        arrays[f"in_{k}"] = np.asarray(v)
+    doc["inputs"] = sorted((inputs or {}).keys())
+    t0 = time.time()
+    try:
+        outs, rb = rt.reference_execute(g, bounds=bounds, inputs=inputs, seed=seed,
+                                        return_bounds=True)
+        doc["error"] = None
+        doc["resolved_bounds"] = rb
+        for k, v in outs.items():
+            arrays[f"out_{k}"] = v
+        doc["outputs"] = sorted(outs.keys())
+    except Exception as exc:  # the reference's own failure is the fixture
+        doc["error"] = f"{type(exc).__name__}: {exc}"
+        doc["outputs"] = []
+    doc["ref_seconds"] = round(time.time() - t0, 4)
+    doc["graph"] = json.loads(ir.from_pdg(g).to_json())
+    with open(os.path.join(CASES, f"{name}.json"), "w") as fh:
+        json.dump(doc, fh)
+    np.savez_compressed(os.path.join(CASES, f"{name}.npz"), **arrays)
+    print(f"{name:40s} {'ERR ' + doc['error'][:60] if doc['error'] else 'ok'} "
+          f"{doc['ref_seconds']}s")
+
+
+def main():
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+    os.makedirs(CASES, exist_ok=True)
+    os.makedirs(GRAPHS, exist_ok=True)
+    V = variants()
+
+    # corpus x variants x seeds (reference pkg/tests/test_dsl.py:240-248)
+    for name, (bounds, inp) in sorted(P.CORPUS_BINDS.items()):
+        inputs = {k: P.make_input(v) for k, v in (inp or {}).items()}
+        for vname, fn in V.items():
+            for seed in (3, 0):
+                g = pdg.build(dsl.load_text(P.corpus_text(name)))
+                bind(g, bounds)  # transforms read static bindings
+                fn(g)
+                write_case(f"corpus_{name}_{vname}_s{seed}", g, bounds, inputs, seed,
+                           {"program": name, "variant": vname})
+    # wider reinforce (more points through the per-point executor)
+    for (I, B, T) in ((2, 8, 16), (3, 4, 32)):
+        g = pdg.build(dsl.load_text(P.corpus_text("reinforce")))
+        write_case(f"reinforce_I{I}B{B}T{T}", g, {"I": I, "B": B, "T": T},
+                   {"winit": 0.1}, 3, {"program": "reinforce"})
+
+    # KAT programs (reference pkg/tests/test_dsl.py:106-188) and appendices
+    for name, (text, bounds, inp) in P.KAT_TEXTS.items():
+        inputs = {k: P.make_input(v) for k, v in (inp or {}).items()}
+        for vname in ("plain", "vec"):
+            g = pdg.build(dsl.load_text(text))
+            V[vname](g)
+            write_case(f"{name}_{vname}", g, bounds, inputs, 0,
+                       {"program": name, "variant": vname})
+
+    # transform-test programs (reference pkg/tests/test_transforms.py)
+    for name, mk in (("gated", P.ctx_gated), ("reverse_scan", P.ctx_reverse_scan)):
+        for vname in ("plain", "lift", "vec"):
+            g = pdg.build(mk())
+            V[vname](g)
+            write_case(f"tr_{name}_{vname}", g, None, None, 5,
+                       {"program": name, "variant": vname})
+    for bs in (10, 7):
+        g = pdg.build(P.ctx_widesum())
+        (tgt,) = [n for n in g.sorted_nodes()
+                  if n.kind == "sum" and n.params["dims"] == (0,)
+                  and g.nodes[g.in_edges(n.id)[0].src].kind == "mul"]
+        tr.incrementalize(g, tgt, bs=bs)
+        write_case(f"tr_widesum_inc{bs}", g, None, None, 7,
+                   {"program": "widesum", "variant": f"incrementalize bs={bs}"})
+    g = pdg.build(P.ctx_widesum())
+    write_case("tr_widesum_plain", g, None, None, 7, {"program": "widesum"})
+
+    # the benchmark program at parity scale, f32 and f64
+    for dt in ("f32", "f64"):
+        for I, B, T in ((1, 4, 6), (2, 3, 5)):
+            ctx = P.ctx_reinforce_mlp(B=B, T=T, I=I, d_o=4, H=8, d_a=2, dtype=dt,
+                                      lr=0.05)
+            g = pdg.build(ctx)
+            pdg.eliminate_dead(g)
+            inputs = P.mlp_inputs(d_o=4, H=8, d_a=2, dtype=dt, seed=1234)
+            write_case(f"mlp_{dt}_I{I}B{B}T{T}", g, None, inputs, 0,
+                       {"program": "reinforce_mlp", "dtype": dt})
+
+    # benchmark graphs (too large for the oracle; structure only)
+    ctx = P.ctx_reinforce_mlp()
+    g = pdg.build(ctx)
+    pdg.eliminate_dead(g)
+    with open(os.path.join(GRAPHS, "reinforce_mlp_c2.json"), "w") as fh:
+        fh.write(ir.from_pdg(g).to_json())
+    print("wrote graphs/reinforce_mlp_c2.json")
+
+
+if __name__ == "__main__":
+    main()
