@@ -1,0 +1,231 @@
+"""Benchmark: REINFORCE training iterations of a 2-layer 256-wide MLP policy
+on E=1024 synthetic envs x T=1000 steps (BASELINE.json configs[1], SURVEY
+§8(d) C2), through the B200 executor.
+
+One step = one call of the program at I=1: roll out E envs for T steps,
+discounted returns-to-go (suffix scan), surrogate backward through the MLP,
+and the SGD update of all six parameters (outputs `*_next`, fed back as the
+next step's inputs).  env-steps per step = E*T.
+
+  value : device-resident (weights already in HBM, outputs left in HBM)
+  e2e   : public API `execute()` with host numpy weights in and updated
+          weights + objective out (H2D/D2H inside the timed region)
+
+`--impl reference` times the reference CPU implementation of the same
+program (the oracle port of reference_execute, oracle/pdg_oracle.py) on a
+bounded sample on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+E_PER_GPU = 1024
+T_STEPS = 1000
+GRAPH = "reinforce_mlp_c2"
+
+
+def load_graph():
+    from paper_2501_05408_b200 import ir
+    with open(os.path.join(ROOT, "tests", "golden", "graphs", f"{GRAPH}.json")) as fh:
+        return ir.Graph.from_json(fh.read())
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    def __init__(self):
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,"
+                         "clocks_event_reasons.hw_slowdown,"
+                         "clocks_event_reasons.hw_thermal_slowdown,"
+                         "clocks_event_reasons.sw_thermal_slowdown,"
+                         "clocks_event_reasons.sw_power_cap",
+                         "--format=csv,noheader,nounits", "-i", "0"],
+                        capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(seconds=12.0):
+    """Oracle port (reference_execute restated) on a bounded sample of the
+    same program: E=4 envs, T=32 steps at full width (H=256)."""
+    from oracle.pdg_oracle import oracle_execute
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    g = load_graph()
+    inputs = mlp_inputs()
+    B, T = 4, 32
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        oracle_execute(g, bounds={"I": 1, "B": B, "T": T}, inputs=inputs, seed=n)
+        n += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n * B * T / dt, "unit": "env-steps/s", "cores": 1, "kind": "port",
+            "sample": f"{n} x oracle_execute(E={B}, T={T}, H=256) of the C2 program, "
+                      f"{dt:.1f}s, single-threaded Python+numpy (reference_execute restated)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps_total = args.warmup + args.steps
+    base = cpu_baseline(seconds=max(5.0, 2.0 * steps_total))
+    line = {"impl": "reference", "metric": "env-steps/s per train iter",
+            "value": base["value"], "unit": "env-steps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "reinforce_mlp_c2 (bounded CPU sample)", "E": 4, "T": 32,
+                       "hidden": [256, 256], "obs": 16, "act": 4},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    from paper_2501_05408_b200 import execute, get_executable
+    from paper_2501_05408_b200.workloads import mlp_inputs, next_inputs, PARAMS
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    g = load_graph()
+    B = E_PER_GPU
+    bounds = {"I": 1, "B": B, "T": T_STEPS}
+    host = mlp_inputs()
+    dev_in = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
+    exe, _ = get_executable(g, bounds, dev_in, seed=rank)
+
+    def step_dev(inp, seed):
+        exe.run(inp)
+        outs = exe.outputs(device_outputs=True)
+        return next_inputs(outs)
+
+    # warmup (device path)
+    inp = dev_in
+    for w in range(args.warmup):
+        inp = step_dev(inp, w)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = Clocks()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    for s in range(args.steps):
+        inp = step_dev(inp, s)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * T_STEPS / (ms / 1e3)
+
+    # e2e through the public API with host buffers
+    exe_h, _ = get_executable(g, bounds, host, seed=rank)
+    hin = host
+    for w in range(max(1, args.warmup)):
+        outs = execute(g, bounds=bounds, inputs=hin, seed=rank)
+        hin = next_inputs(outs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        outs = execute(g, bounds=bounds, inputs=hin, seed=rank)
+        hin = next_inputs(outs)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    h2d = sum(v.nbytes for v in host.values())
+    d2h = sum(np.asarray(v).nbytes for v in outs.values())
+    e2e = world * B * T_STEPS / (e2e_ms / 1e3)
+
+    line = {"metric": "env-steps/s per train iter", "value": value, "unit": "env-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "reinforce_mlp_c2", "E_per_gpu": B, "T": T_STEPS,
+                       "hidden": [256, 256], "obs": 16, "act": 4, "iters_per_step": 1,
+                       "l2": "activations (GBs) exceed L2 every step",
+                       "parallelism": f"env-shard x{world}"},
+            "e2e": {"value": e2e, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": exe.launch_count * args.steps,
+            "peak_hbm_bytes": exe.peak_bytes,
+            "clocks": clk}
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,296 @@
+/*
+ * rtb200 — B200 execution backend for recurrent-tensor / PDG programs.
+ *
+ * C ABI (plain pointers, sizes and POD descriptors; no torch types).  The
+ * host side (paper_2501_05408_b200/) lowers a dependence graph into a
+ * program of kernel launches over "boxes" (slab of a node's domain x its
+ * payload) and loops over the dims the dependence structure serialises;
+ * this library runs that program on one CUDA stream.
+ *
+ * Reference interfaces each entry replaces (paths relative to the
+ * reference root, pkg/src/recten/):
+ *   rt_run            runtime.py:460-475 reference_execute (the executor
+ *                     loop _Oracle.value/read, runtime.py:344-425) — runs a
+ *                     lowered program: loops + launches + memory ops
+ *   rt_launch         runtime.py:37-44, 236-271 the KERNELS table ABI
+ *                     fn(node, vals, env, rng): one kernel family per call
+ *   rt_status_read    runtime.py:25-30, 176-177, 186-188 error reporting
+ *                     (RuntimeError_/OracleError) via a device status word
+ *   rt_memcpy_*       SPEC.md:558-561 Backend move-between-tiers (the
+ *                     offload/fetch of polysched.py:936-1105, realised as
+ *                     pinned cudaMemcpyAsync on a side stream)
+ *   rt_rng_fill       runtime.py:50-55, 391-394 per-point
+ *                     default_rng((seed, tag, *point)) draws, bit-exact
+ *   rt_scan_ref       runtime.py:133-146 discounted_cumsum (standalone)
+ */
+#ifndef RTB200_H
+#define RTB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RT_MAXD 10    /* max rank of an iteration box (slab dims + payload dims) */
+#define RT_MAXENV 8   /* max loop dims visible to a launch                        */
+#define RT_MAXIN 8    /* max operand views of one elementwise launch             */
+#define RT_MAXCHK 3   /* max range checks per view                               */
+#define RT_CODE 256   /* program words per launch                                */
+#define RT_KONST 32   /* float constants per launch                              */
+
+enum rt_dtype { RT_F64 = 0, RT_F32 = 1, RT_I64 = 2, RT_BOOL = 3 };
+
+enum rt_kernel {
+  RT_K_EW = 1,       /* fused elementwise/layout/merge/gather program        */
+  RT_K_REDUCE = 2,   /* sum / discounted sum over (possibly ragged) ranges   */
+  RT_K_SCAN = 3,     /* linear recurrence y = x + g*y_prev along one dim      */
+  RT_K_GEMM = 4,     /* strided/batched/contracting fp32|fp64 matmul          */
+  RT_K_RNG = 5,      /* SeedSequence->PCG64->{normal,uniform} per point       */
+  RT_K_UDF = 6,      /* synthetic environment (dsl.py:288-307) per point      */
+  RT_K_SPLITK = 7,   /* split-K partial reduction for RT_K_GEMM               */
+  RT_K_POLICY = 8    /* fused acting step: MLP policy + sample + env          */
+};
+
+enum rt_status_code {
+  RT_OK = 0,
+  RT_ERR_ROW_RANGE = 1,     /* index_select row outside 0..n-1 (runtime.py:186-188) */
+  RT_ERR_SLICE_RANGE = 2,   /* index_select rows lo:hi outside (runtime.py:176-177) */
+  RT_ERR_CUDA = 3,
+  RT_ERR_BAD_ARG = 4,
+  RT_ERR_UNKNOWN_KERNEL = 5
+};
+
+/* A flat index over a box, decomposed row-major. */
+typedef struct {
+  int32_t nd;
+  int32_t _pad;
+  int64_t ext[RT_MAXD];
+} rt_box;
+
+/* An operand's addressing over a box: element offset
+ *   off + sum_e env[e]*off_env[e] + sum_d idx[d]*stride[d]
+ * valid iff every check  0 <= c0 + sum_e env[e]*c_env[e] + sum_d idx[d]*a[d] < hi
+ * (an invalid load yields 0; the planner guarantees invalid loads are never
+ * selected where the reference would have read them). */
+typedef struct {
+  uint64_t ptr;
+  int32_t dtype;
+  int32_t nchk;
+  int64_t off;
+  int64_t off_env[RT_MAXENV];
+  int64_t stride[RT_MAXD];
+  int64_t chk_c0[RT_MAXCHK];
+  int64_t chk_hi[RT_MAXCHK];
+  int32_t chk_env[RT_MAXCHK][RT_MAXENV];
+  int32_t chk_a[RT_MAXCHK][RT_MAXD];
+} rt_view;
+
+/* Every parameter block starts with this header; rt_run patches env[]
+ * before each launch. */
+typedef struct {
+  int64_t env[RT_MAXENV];
+  int32_t node;        /* graph node id, for error reports */
+  int32_t status_slot; /* unused: status word is global   */
+  uint64_t status;     /* device pointer to int32[4] status word */
+} rt_hdr;
+
+/* RT_K_EW: out[idx] = program(views)(idx) for idx over box. */
+typedef struct {
+  rt_hdr h;
+  rt_box box;
+  int64_t total;
+  int32_t nin;
+  int32_t f64;         /* compute in double (else float) */
+  rt_view out;
+  rt_view in[RT_MAXIN];
+  int32_t code[RT_CODE];
+  double konst[RT_KONST];
+} rt_ew_params;
+
+/* RT_K_REDUCE: out[p] = sum_{k in ranges(p)} w(k) * in[p, k]
+ * box = output points (nd_out dims); red = reduced dims with extents given
+ * as affine forms (lo fixed at the view, len per point) or int programs. */
+typedef struct {
+  rt_hdr h;
+  rt_box box;          /* output box */
+  int64_t total;
+  int32_t nred;        /* number of reduced dims (<= 4) */
+  int32_t op;          /* 0 = sum, 1 = discounted sum along red dim 0 */
+  double gamma;
+  int32_t reverse;     /* dsum weights reversed */
+  int32_t f64;
+  int32_t len_prog[4]; /* -1: len = len0 + sum a*idx + env; else program entry */
+  int64_t len0[4];
+  int64_t len_env[4][RT_MAXENV];
+  int64_t len_a[4][RT_MAXD];
+  int64_t red_stride[4];   /* input element stride per reduced dim */
+  int32_t lo_prog[4];      /* -1 none; else program computing the start offset shift */
+  int32_t threads_per_out; /* 1 or a power of two <= 1024 */
+  int32_t _pad;
+  rt_view in;          /* strides over the output box; lo folded in */
+  rt_view out;
+  int32_t code[RT_CODE];
+  double konst[RT_KONST];
+} rt_reduce_params;
+
+/* RT_K_SCAN: along dim `sdim` of box: y[j] = x[j] + gamma*y[j-1] (or j+1). */
+typedef struct {
+  rt_hdr h;
+  rt_box box;          /* full box including the scan dim */
+  int64_t total_lines; /* prod of extents except the scan dim */
+  int32_t sdim;
+  int32_t reverse;
+  double gamma;
+  int32_t f64;
+  int32_t chunk;       /* elements per chunk along the line (0 = whole line) */
+  rt_view in;
+  rt_view out;
+  /* window form: y[j] = S[lo(j)] - gamma^(hi-lo) * S[hi(j)], unused if win=0 */
+  int32_t win;
+  int32_t _pad2;
+} rt_scan_params;
+
+/* RT_K_GEMM: for z in Z, C[z,m,n] (+)= sum_k A[z,m,k] * B[z,k,n].
+ * Each of Z, M, N, K is a flat index decomposed over its own small box;
+ * every operand carries strides for each decomposed coordinate. */
+typedef struct {
+  int32_t nd;
+  int32_t _pad;
+  int64_t ext[4];
+} rt_gbox;
+
+typedef struct {
+  uint64_t ptr;
+  int32_t dtype;
+  int32_t _pad;
+  int64_t off;
+  int64_t off_env[RT_MAXENV];
+  int64_t sz[4];   /* strides for the Z coordinates  */
+  int64_t s1[4];   /* strides for the M (A,C) or K (B) coordinates */
+  int64_t s2[4];   /* strides for the K (A) or N (B,C) coordinates */
+} rt_gop;
+
+typedef struct {
+  rt_hdr h;
+  rt_gbox Z, M, N, K;
+  int64_t z, m, n, k;  /* flat sizes */
+  int32_t f64;
+  int32_t splits;      /* split-K factor (partials to `part` when > 1) */
+  int32_t accumulate;  /* C += result */
+  int32_t epilogue;    /* 0 none, 1 tanh */
+  rt_gop A, B, C;
+  uint64_t part;       /* device scratch [splits, z, m, n] when splits > 1 */
+  rt_gop bias;         /* added when bias.ptr != 0 (strides over Z,M: s1 for M? uses s2 over N) */
+} rt_gemm_params;
+
+/* RT_K_SPLITK: C[z,m,n] = sum_s part[s,z,m,n] */
+typedef struct {
+  rt_hdr h;
+  rt_gbox Z, M, N;
+  int64_t z, m, n;
+  int32_t splits;
+  int32_t f64;
+  int32_t accumulate;
+  int32_t epilogue;
+  uint64_t part;
+  rt_gop C;
+  rt_gop bias;
+} rt_splitk_params;
+
+/* Point coordinates for per-point entropy: coordinate j of the node's
+ * domain point is box index coord_src[j] when >= 0, else env[-1-coord_src[j]]. */
+
+/* RT_K_RNG: per point of box, draw `count` values from
+ * default_rng((prefix words..., *coords)) in C order (runtime.py:50-55). */
+typedef struct {
+  rt_hdr h;
+  rt_box box;            /* slab box (points) */
+  int64_t total;
+  int32_t nprefix;       /* entropy words before the point coordinates */
+  int32_t ncoord;        /* number of point coordinates (full node domain) */
+  uint32_t prefix[8];
+  int32_t coord_src[RT_MAXD];
+  int32_t dist;          /* 0 normal, 1 uniform */
+  int32_t count;         /* values per point */
+  rt_view out;           /* strides over box; `count` contiguous values per point */
+} rt_rng_params;
+
+/* RT_K_UDF: synthetic env body of dsl.make_udf_fn per point (dsl.py:288-307):
+ * base = salt + sum_k mean(in_k); out_j ~ tanh(base + 0.3 N) | bool | i64. */
+typedef struct {
+  rt_hdr h;
+  rt_box box;
+  int64_t total;
+  int32_t nprefix;
+  int32_t ncoord;
+  uint32_t prefix[8];
+  int32_t coord_src[RT_MAXD];
+  double salt;
+  int32_t nin;
+  int32_t nout;
+  int32_t in_count[4];   /* payload elements per input (mean over them) */
+  int32_t out_count[4];
+  int32_t out_kind[4];   /* rt_dtype of each output */
+  rt_view in[4];         /* strides over box; payload contiguous after */
+  rt_view out[4];
+} rt_udf_params;
+
+/* Launch record: one kernel family + its parameter block. */
+typedef struct {
+  int32_t kernel;
+  int32_t param_bytes;
+  uint64_t params;     /* host pointer to the parameter block */
+  int32_t grid[3];
+  int32_t block[3];
+  int32_t smem;
+  int32_t _pad;
+} rt_launch_rec;
+
+/* Program instructions for rt_run. */
+enum rt_op {
+  RT_OP_LAUNCH = 1,    /* a = launch record index                          */
+  RT_OP_FOR = 2,       /* a = env slot, b = start, c = end (exclusive for  */
+                       /*     step +1; for step -1 runs b down to c+1),    */
+                       /*     d = step, e = pc after matching END          */
+  RT_OP_END = 3,       /* a = pc of matching FOR                           */
+  RT_OP_EVENT = 4,     /* a = event slot: record on the stream             */
+  RT_OP_COPY = 5       /* device copy: a = rec idx of an rt_copy record    */
+};
+
+typedef struct {
+  int32_t op;
+  int32_t a;
+  int64_t b, c, d;
+  int32_t e;
+  int32_t _pad;
+} rt_instr;
+
+/* ---- entry points ------------------------------------------------------ */
+
+int rt_version(void);
+/* Launch one kernel family with `rec`, patching env[0..nenv) into its header. */
+int rt_launch(const rt_launch_rec* rec, const int64_t* env, int32_t nenv, uint64_t stream);
+/* Run a lowered program (loops + launches) on `stream`.  events: optional
+ * cudaEvent_t handles for RT_OP_EVENT. */
+int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,
+           int64_t* env, int32_t nenv, uint64_t stream, const uint64_t* events, int32_t nevents);
+/* Device status word: int32[4] = {code, node, aux0, aux1}; allocate/clear/read. */
+int rt_status_alloc(uint64_t* dev_ptr);
+int rt_status_read(uint64_t dev_ptr, int32_t* host4, uint64_t stream);
+int rt_status_clear(uint64_t dev_ptr, uint64_t stream);
+int rt_status_free(uint64_t dev_ptr);
+/* Pinned-host tier moves (offload / fetch) on a side stream with an event. */
+int rt_memcpy_d2h_async(void* host_pinned, uint64_t dev, uint64_t bytes, uint64_t stream);
+int rt_memcpy_h2d_async(uint64_t dev, const void* host_pinned, uint64_t bytes, uint64_t stream);
+/* Standalone bit-exact RNG fill (numpy default_rng((words..., *coords)) per
+ * row): rows x count values of dist into dev (f64).  For tests/tools. */
+int rt_rng_fill(uint64_t dev_out, const uint32_t* prefix, int32_t nprefix,
+                const int64_t* coords, int32_t ncoord, int64_t rows, int32_t count,
+                int32_t dist, uint64_t stream);
+const char* rt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTB200_H */

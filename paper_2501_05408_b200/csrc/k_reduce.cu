@@ -1,0 +1,109 @@
+// RT_K_REDUCE — sums and discounted sums over payload axes and over gathered
+// (possibly ragged) index ranges.  Replaces the reference's per-point
+// `_k_sum` (runtime.py:95-96), `_k_discounted_sum` (runtime.py:108-122),
+// `_k_window_reduce` (runtime.py:192-211, direct form for short windows) and
+// the slice gather of `_Oracle.read` (runtime.py:414-425) feeding them: the
+// gathered range is never materialised, the reduction walks it in place.
+// Accumulation is in fp64 for every input type.
+#include "common.cuh"
+
+template <typename T>
+RT_DEV double red_weight(const rt_reduce_params& p, int64_t k, int64_t n) {
+  if (p.op == 0) return 1.0;
+  int64_t e = p.reverse ? (n - 1 - k) : k;
+  // runtime.py:108-112: f64 gamma**arange, cast to the input dtype
+  return (double)(T)pow(p.gamma, (double)e);
+}
+
+template <typename T>
+RT_DEV void red_setup(const rt_reduce_params& p, const int64_t* idx, int64_t* len,
+                      int64_t* base, int64_t* total) {
+  const int nd = p.box.nd;
+  int64_t off = view_off(p.in, nd, idx);
+  int64_t tot = 1;
+  for (int j = 0; j < p.nred; ++j) {
+    int64_t L;
+    if (p.len_prog[j] < 0) {
+      L = p.len0[j];
+      for (int d = 0; d < nd; ++d) L += p.len_a[j][d] * idx[d];
+    } else {
+      T dv;
+      vm_run<T>(p.code, p.len_prog[j], p.konst, p.h, idx, nd, &p.in, &dv, &L);
+    }
+    if (L < 0) L = 0;
+    len[j] = L;
+    tot *= L;
+    if (p.lo_prog[j] >= 0) {
+      int64_t lo = 0;
+      T dv;
+      vm_run<T>(p.code, p.lo_prog[j], p.konst, p.h, idx, nd, &p.in, &dv, &lo);
+      off += lo * p.red_stride[j];
+    }
+  }
+  *base = off;
+  *total = tot;
+}
+
+template <typename T>
+RT_DEV double red_term(const rt_reduce_params& p, int64_t base, const int64_t* len, int64_t k) {
+  int64_t off = base;
+  int64_t r = k, k0 = 0;
+  for (int j = p.nred - 1; j >= 0; --j) {
+    int64_t q = r / len[j];
+    int64_t kj = r - q * len[j];
+    r = q;
+    off += kj * p.red_stride[j];
+    if (j == 0) k0 = kj;
+  }
+  T x = load_as<T>((const void*)p.in.ptr, p.in.dtype, off);
+  if (p.op == 0) return (double)x;
+  T w = (T)red_weight<T>(p, k0, len[0]);
+  return (double)(T)(x * w);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_thread(const __grid_constant__ rt_reduce_params p) {
+  int64_t idx[RT_MAXD];
+  int64_t len[4];
+  const int nd = p.box.nd;
+  for (int64_t flat = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; flat < p.total;
+       flat += (int64_t)gridDim.x * blockDim.x) {
+    decompose(p.box, flat, idx);
+    int64_t base, tot;
+    red_setup<T>(p, idx, len, &base, &tot);
+    double acc = 0.0;
+    for (int64_t k = 0; k < tot; ++k) acc += red_term<T>(p, base, len, k);
+    store_as<double>((void*)p.out.ptr, p.out.dtype, view_off(p.out, nd, idx), acc);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_reduce_block(const __grid_constant__ rt_reduce_params p) {
+  __shared__ double sh[32];
+  int64_t idx[RT_MAXD];
+  int64_t len[4];
+  const int nd = p.box.nd;
+  for (int64_t flat = blockIdx.x; flat < p.total; flat += gridDim.x) {
+    decompose(p.box, flat, idx);
+    int64_t base, tot;
+    red_setup<T>(p, idx, len, &base, &tot);
+    double acc = 0.0;
+    for (int64_t k = threadIdx.x; k < tot; k += blockDim.x) acc += red_term<T>(p, base, len, k);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = acc;
+    __syncthreads();
+    if (w == 0) {
+      int nw = blockDim.x >> 5;
+      double v = l < nw ? sh[l] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (l == 0) store_as<double>((void*)p.out.ptr, p.out.dtype, view_off(p.out, nd, idx), v);
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" void* rt_kernel_reduce(int f64, int block) {
+  if (block) return f64 ? (void*)k_reduce_block<double> : (void*)k_reduce_block<float>;
+  return f64 ? (void*)k_reduce_thread<double> : (void*)k_reduce_thread<float>;
+}

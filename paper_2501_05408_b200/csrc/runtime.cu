@@ -1,0 +1,258 @@
+// C-ABI runtime: kernel table, launch with env patching, the loop-nest
+// program interpreter (the executor loop that replaces the reference's
+// demand-driven recursion, runtime.py:285-475), status word, tier moves.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+#include <string>
+#include <vector>
+#include "../../include/rtb200.h"
+
+extern "C" void* rt_kernel_ew(int f64);
+extern "C" void* rt_kernel_reduce(int f64, int block);
+extern "C" void* rt_kernel_scan(int f64, int warp);
+extern "C" void* rt_kernel_gemm(int f64);
+extern "C" void* rt_kernel_splitk(int f64);
+extern "C" void* rt_kernel_rng();
+extern "C" void* rt_kernel_udf();
+extern "C" void* rt_kernel_rng_fill();
+extern "C" void* rt_kernel_policy(const void* params);
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+
+static int cuda_check(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return RT_OK;
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s: %s", where, cudaGetErrorString(e));
+  g_err = buf;
+  return RT_ERR_CUDA;
+}
+
+extern "C" const char* rt_last_error(void) { return g_err.c_str(); }
+extern "C" int rt_version(void) { return 1; }
+
+// ------------------------------------------------------------ env folding
+
+static void fold_view(rt_view& v, const int64_t* env, int nenv) {
+  for (int e = 0; e < nenv && e < RT_MAXENV; ++e) {
+    int64_t x = env[e];
+    if (!x) continue;
+    v.off += x * v.off_env[e];
+    for (int c = 0; c < v.nchk; ++c) v.chk_c0[c] += x * (int64_t)v.chk_env[c][e];
+  }
+}
+
+static void fold_gop(rt_gop& g, const int64_t* env, int nenv) {
+  for (int e = 0; e < nenv && e < RT_MAXENV; ++e) g.off += env[e] * g.off_env[e];
+}
+
+static void patch_env(rt_hdr* h, const int64_t* env, int nenv) {
+  for (int e = 0; e < RT_MAXENV; ++e) h->env[e] = e < nenv ? env[e] : 0;
+}
+
+// Fold the launch's env into a private copy of the parameter block and pick
+// the kernel variant.  Returns the kernel function or null.
+static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
+  patch_env((rt_hdr*)blk, env, nenv);
+  switch (kernel) {
+    case RT_K_EW: {
+      rt_ew_params* p = (rt_ew_params*)blk;
+      fold_view(p->out, env, nenv);
+      for (int i = 0; i < p->nin; ++i) fold_view(p->in[i], env, nenv);
+      return rt_kernel_ew(p->f64);
+    }
+    case RT_K_REDUCE: {
+      rt_reduce_params* p = (rt_reduce_params*)blk;
+      fold_view(p->in, env, nenv);
+      fold_view(p->out, env, nenv);
+      for (int j = 0; j < p->nred; ++j)
+        for (int e = 0; e < nenv && e < RT_MAXENV; ++e) p->len0[j] += env[e] * p->len_env[j][e];
+      return rt_kernel_reduce(p->f64, p->threads_per_out > 1);
+    }
+    case RT_K_SCAN: {
+      rt_scan_params* p = (rt_scan_params*)blk;
+      fold_view(p->in, env, nenv);
+      fold_view(p->out, env, nenv);
+      int warp = p->in.stride[p->sdim] == 1 && p->out.stride[p->sdim] == 1;
+      return rt_kernel_scan(p->f64, warp);
+    }
+    case RT_K_GEMM: {
+      rt_gemm_params* p = (rt_gemm_params*)blk;
+      fold_gop(p->A, env, nenv);
+      fold_gop(p->B, env, nenv);
+      fold_gop(p->C, env, nenv);
+      if (p->bias.ptr) fold_gop(p->bias, env, nenv);
+      return rt_kernel_gemm(p->f64);
+    }
+    case RT_K_SPLITK: {
+      rt_splitk_params* p = (rt_splitk_params*)blk;
+      fold_gop(p->C, env, nenv);
+      if (p->bias.ptr) fold_gop(p->bias, env, nenv);
+      return rt_kernel_splitk(p->f64);
+    }
+    case RT_K_RNG: {
+      rt_rng_params* p = (rt_rng_params*)blk;
+      fold_view(p->out, env, nenv);
+      return rt_kernel_rng();
+    }
+    case RT_K_UDF: {
+      rt_udf_params* p = (rt_udf_params*)blk;
+      for (int i = 0; i < p->nin; ++i) fold_view(p->in[i], env, nenv);
+      for (int i = 0; i < p->nout; ++i) fold_view(p->out[i], env, nenv);
+      return rt_kernel_udf();
+    }
+    case RT_K_POLICY:
+      return rt_kernel_policy(blk);
+    default:
+      return nullptr;
+  }
+}
+
+static int launch_one(const rt_launch_rec* rec, const int64_t* env, int nenv, cudaStream_t s) {
+  alignas(16) static thread_local unsigned char blk[32768];
+  if (rec->param_bytes <= 0 || rec->param_bytes > (int)sizeof blk)
+    return fail(RT_ERR_BAD_ARG, "parameter block size out of range");
+  memcpy(blk, (const void*)rec->params, rec->param_bytes);
+  void* fn = prepare(rec->kernel, blk, env, nenv);
+  if (!fn) return fail(RT_ERR_UNKNOWN_KERNEL, "unknown kernel family");
+  if (rec->grid[0] <= 0) return RT_OK;  // empty box
+  void* args[1] = {blk};
+  dim3 g(rec->grid[0], rec->grid[1] > 0 ? rec->grid[1] : 1, rec->grid[2] > 0 ? rec->grid[2] : 1);
+  dim3 b(rec->block[0], rec->block[1] > 0 ? rec->block[1] : 1, rec->block[2] > 0 ? rec->block[2] : 1);
+  if (rec->smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, rec->smem);
+    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
+  }
+  return cuda_check(cudaLaunchKernel(fn, g, b, args, rec->smem, s), "cudaLaunchKernel");
+}
+
+extern "C" int rt_launch(const rt_launch_rec* rec, const int64_t* env, int32_t nenv, uint64_t stream) {
+  return launch_one(rec, env, nenv, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------ programs
+
+extern "C" int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,
+                      int64_t* env, int32_t nenv, uint64_t stream, const uint64_t* events,
+                      int32_t nevents) {
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int64_t> ends(nprog, 0);
+  int pc = 0;
+  while (pc < nprog) {
+    const rt_instr& in = prog[pc];
+    switch (in.op) {
+      case RT_OP_LAUNCH: {
+        if (in.a < 0 || in.a >= nrec) return fail(RT_ERR_BAD_ARG, "launch record out of range");
+        int rc = launch_one(&recs[in.a], env, nenv, s);
+        if (rc) return rc;
+        ++pc;
+        break;
+      }
+      case RT_OP_FOR: {
+        // b = first value, c = bound (exclusive in the direction of d), d = step
+        if (in.a < 0 || in.a >= nenv) return fail(RT_ERR_BAD_ARG, "loop slot out of range");
+        bool empty = in.d > 0 ? (in.b >= in.c) : (in.b <= in.c);
+        if (empty) {
+          pc = in.e;
+        } else {
+          env[in.a] = in.b;
+          ++pc;
+        }
+        break;
+      }
+      case RT_OP_END: {
+        const rt_instr& f = prog[in.a];
+        int64_t v = env[f.a] + f.d;
+        bool more = f.d > 0 ? (v < f.c) : (v > f.c);
+        if (more) {
+          env[f.a] = v;
+          pc = in.a + 1;
+        } else {
+          ++pc;
+        }
+        break;
+      }
+      case RT_OP_EVENT: {
+        if (in.a < 0 || in.a >= nevents) return fail(RT_ERR_BAD_ARG, "event slot out of range");
+        int rc = cuda_check(cudaEventRecord((cudaEvent_t)events[in.a], s), "cudaEventRecord");
+        if (rc) return rc;
+        ++pc;
+        break;
+      }
+      default:
+        return fail(RT_ERR_BAD_ARG, "bad program instruction");
+    }
+  }
+  return RT_OK;
+}
+
+// ------------------------------------------------------------ status word
+
+extern "C" int rt_status_alloc(uint64_t* dev_ptr) {
+  void* p = nullptr;
+  int rc = cuda_check(cudaMalloc(&p, 4 * sizeof(int)), "cudaMalloc(status)");
+  if (rc) return rc;
+  rc = cuda_check(cudaMemset(p, 0, 4 * sizeof(int)), "cudaMemset(status)");
+  *dev_ptr = (uint64_t)p;
+  return rc;
+}
+
+extern "C" int rt_status_read(uint64_t dev_ptr, int32_t* host4, uint64_t stream) {
+  int rc = cuda_check(cudaMemcpyAsync(host4, (void*)dev_ptr, 4 * sizeof(int), cudaMemcpyDeviceToHost,
+                                      (cudaStream_t)stream), "status read");
+  if (rc) return rc;
+  return cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "status sync");
+}
+
+extern "C" int rt_status_clear(uint64_t dev_ptr, uint64_t stream) {
+  return cuda_check(cudaMemsetAsync((void*)dev_ptr, 0, 4 * sizeof(int), (cudaStream_t)stream),
+                    "status clear");
+}
+
+extern "C" int rt_status_free(uint64_t dev_ptr) {
+  return cuda_check(cudaFree((void*)dev_ptr), "status free");
+}
+
+// ------------------------------------------------------------ tier moves
+
+extern "C" int rt_memcpy_d2h_async(void* host_pinned, uint64_t dev, uint64_t bytes, uint64_t stream) {
+  return cuda_check(cudaMemcpyAsync(host_pinned, (void*)dev, bytes, cudaMemcpyDeviceToHost,
+                                    (cudaStream_t)stream), "d2h");
+}
+
+extern "C" int rt_memcpy_h2d_async(uint64_t dev, const void* host_pinned, uint64_t bytes, uint64_t stream) {
+  return cuda_check(cudaMemcpyAsync((void*)dev, host_pinned, bytes, cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream), "h2d");
+}
+
+// ------------------------------------------------------------ rng fill
+
+extern "C" int rt_rng_fill(uint64_t dev_out, const uint32_t* prefix, int32_t nprefix,
+                           const int64_t* coords, int32_t ncoord, int64_t rows, int32_t count,
+                           int32_t dist, uint64_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t* dpre = nullptr;
+  int64_t* dco = nullptr;
+  int rc = cuda_check(cudaMalloc(&dpre, 8 * sizeof(uint32_t)), "malloc");
+  if (rc) return rc;
+  size_t cb = (size_t)(rows * (ncoord > 0 ? ncoord : 1)) * sizeof(int64_t);
+  rc = cuda_check(cudaMalloc(&dco, cb), "malloc");
+  if (rc) return rc;
+  cudaMemcpyAsync(dpre, prefix, nprefix * sizeof(uint32_t), cudaMemcpyHostToDevice, s);
+  if (ncoord > 0) cudaMemcpyAsync(dco, coords, rows * ncoord * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+  void* fn = rt_kernel_rng_fill();
+  void* args[] = {&dev_out, &dpre, &nprefix, &dco, &ncoord, &rows, &count, &dist};
+  int blocks = (int)((rows + 127) / 128);
+  if (blocks > 65535) blocks = 65535;
+  if (blocks < 1) blocks = 1;
+  rc = cuda_check(cudaLaunchKernel(fn, dim3(blocks), dim3(128), args, 0, s), "rng_fill");
+  cudaStreamSynchronize(s);
+  cudaFree(dpre);
+  cudaFree(dco);
+  return rc;
+}

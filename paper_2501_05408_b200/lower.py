@@ -1,0 +1,1242 @@
+"""Lowering: planned steps -> parameter blocks for the C-ABI kernel families
+plus the loop program `rt_run` interprets.
+
+Each bulk step of node n with enclosing loop dims F evaluates n over
+box = (free dims of n's domain) x (payload).  Every in-edge becomes an
+operand view: the edge's index expression phi (reference pdg.py:58-68,
+evaluated per point by runtime.py:396-425) is folded at compile time into
+element strides over the box, offsets linear in the loop variables, and
+range checks for components that may leave the source domain; index
+expressions that are not affine compile to small int programs (Euclidean
+// and %, reference symexpr.py:491-506).  Slice components become value
+axes: reduced in place by RT_K_REDUCE / RT_K_SCAN, or walked as payload
+axes when their length is constant.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import zlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import ir
+from . import native as N
+from .planner import INF, Bulk, Loop, interval, subst_bounds
+
+
+class LowerError(Exception):
+    pass
+
+
+def prod(xs):
+    out = 1
+    for x in xs:
+        out *= x
+    return out
+
+
+def cstrides(shape):
+    st, acc = [], 1
+    for s in reversed(shape):
+        st.append(acc)
+        acc *= s
+    return list(reversed(st))
+
+
+# ---------------------------------------------------------------------------
+# buffers
+
+
+@dataclass
+class Buf:
+    key: tuple            # (nid, oid)
+    dims: tuple           # domain dims
+    dshape: tuple         # domain extents
+    pshape: tuple         # payload shape
+    dtype: str
+    alias: tuple | None = None   # (nid, oid) whose storage this is
+    host: np.ndarray | None = None  # constant/input contents
+    ptr: int = 0
+
+    @property
+    def shape(self):
+        return tuple(self.dshape) + tuple(self.pshape)
+
+    @property
+    def strides(self):
+        return cstrides(self.shape)
+
+    def dim_stride(self, d):
+        return self.strides[self.dims.index(d)]
+
+    def payload_strides(self):
+        return self.strides[len(self.dims):]
+
+    @property
+    def nbytes(self):
+        return prod(self.shape) * ir.ITEMSIZE[self.dtype]
+
+
+# ---------------------------------------------------------------------------
+# VM programs
+
+
+OPC = {"ICOORD": 1, "IENV": 2, "ICONST": 3, "IADD": 4, "ISUB": 5, "IMUL": 6, "IFDIV": 7,
+       "IMOD": 8, "IMIN": 9, "IMAX": 10, "INEG": 11, "IEQ": 12, "ILT": 13, "ILE": 14,
+       "IGT": 15, "IGE": 16, "INE": 17, "IAND": 18, "IOR": 19, "INOT": 20, "JZ": 21,
+       "JMP": 22, "LOAD": 30, "LOADX": 31, "VCONST": 32, "VITOF": 33, "VADD": 34,
+       "VSUB": 35, "VMUL": 36, "VDIV": 37, "VNEG": 38, "VEXP": 39, "VLOG": 40,
+       "VTANH": 41, "VSQRT": 42, "VPOW": 43, "VEQ": 44, "VNE": 45, "VLT": 46, "VLE": 47,
+       "VGT": 48, "VGE": 49, "VWHERE": 50, "VCAST": 51, "VMOV": 52, "VTOI": 53,
+       "VALID": 54, "STORE": 60, "ERROR": 62, "ISTORE": 63}
+
+IBIN = {"add": "IADD", "sub": "ISUB", "mul": "IMUL", "floordiv": "IFDIV", "mod": "IMOD",
+        "eq": "IEQ", "lt": "ILT", "le": "ILE", "gt": "IGT", "ge": "IGE", "and": "IAND",
+        "or": "IOR"}
+
+
+class Prog:
+    """Builder for the two-word VM code (csrc/common.cuh)."""
+
+    def __init__(self):
+        self.code: list[int] = []
+        self.konst: list[float] = []
+        self.ifree = list(range(8))
+        self.vfree = list(range(8))
+
+    def emit(self, op, d=0, a=0, b=0, c=0, imm=0):
+        self.code += [OPC[op] | (d << 8) | (a << 12) | (b << 16) | (c << 20), int(imm)]
+        if len(self.code) > N.RT_CODE:
+            raise LowerError("program too long")
+        return len(self.code) - 1  # index of the imm word (for patching jumps)
+
+    def pc(self):
+        return len(self.code)
+
+    def ireg(self):
+        if not self.ifree:
+            raise LowerError("out of int registers")
+        return self.ifree.pop(0)
+
+    def vreg(self):
+        if not self.vfree:
+            raise LowerError("out of value registers")
+        return self.vfree.pop(0)
+
+    def ifree_(self, r):
+        self.ifree.insert(0, r)
+
+    def vfree_(self, r):
+        self.vfree.insert(0, r)
+
+    def k(self, v):
+        v = float(v)
+        for i, x in enumerate(self.konst):
+            if x == v and math.copysign(1, x) == math.copysign(1, v):
+                return i
+        self.konst.append(v)
+        if len(self.konst) > N.RT_KONST:
+            raise LowerError("too many constants")
+        return len(self.konst) - 1
+
+    def int_expr(self, e, dimmap):
+        """Compile an integer/bool expression; returns the result register.
+        dimmap: (name, kind) -> ("coord", i) | ("env", slot) | ("const", v)."""
+        k = e[0]
+        if k in ("int", "bool"):
+            r = self.ireg()
+            v = int(e[1])
+            if not -(1 << 31) <= v < (1 << 31):
+                raise LowerError("integer constant out of range")
+            self.emit("ICONST", d=r, imm=v)
+            return r
+        if k == "sym":
+            m = dimmap.get((e[1], e[2]))
+            if m is None:
+                raise LowerError(f"unbound symbol {e[1]} in index expression")
+            r = self.ireg()
+            if m[0] == "coord":
+                self.emit("ICOORD", d=r, imm=m[1])
+            elif m[0] == "env":
+                self.emit("IENV", d=r, imm=m[1])
+            else:
+                self.emit("ICONST", d=r, imm=m[1])
+            return r
+        if k == "neg":
+            a = self.int_expr(e[1], dimmap)
+            self.emit("INEG", d=a, a=a)
+            return a
+        if k == "not":
+            a = self.int_expr(e[1], dimmap)
+            self.emit("INOT", d=a, a=a)
+            return a
+        if k in ("min", "max"):
+            a = self.int_expr(e[1], dimmap)
+            for x in e[2:]:
+                b = self.int_expr(x, dimmap)
+                self.emit("IMIN" if k == "min" else "IMAX", d=a, a=a, b=b)
+                self.ifree_(b)
+            return a
+        if k in IBIN:
+            a = self.int_expr(e[1], dimmap)
+            b = self.int_expr(e[2], dimmap)
+            self.emit(IBIN[k], d=a, a=a, b=b)
+            self.ifree_(b)
+            return a
+        raise LowerError(f"cannot compile index expression kind {k}")
+
+
+# ---------------------------------------------------------------------------
+# operand views
+
+
+@dataclass
+class Axis:
+    ext: int | None        # None: ragged (length varies per point)
+    stride: int
+    len_expr: object = None  # ragged slice: hi - lo (bounds substituted)
+    lo_expr: object = None   # slice lower endpoint (bounds substituted)
+
+
+@dataclass
+class EdgeVal:
+    buf: Buf
+    off: int = 0
+    coef: dict = field(default_factory=dict)      # sink dim -> element stride
+    checks: list = field(default_factory=list)    # (k, {sink dim: a}, hi)
+    axes: list = field(default_factory=list)      # value axes (slices then payload)
+    nslices: int = 0
+    progs: list = field(default_factory=list)     # (expr, stride, hi) non-affine comps
+    psi: object = None
+
+
+class Ctx:
+    """Per-bulk-step context: slab dims, loop slots, concrete bounds."""
+
+    def __init__(self, low, node, fixed):
+        self.low = low
+        self.node = node
+        self.fixed = tuple(fixed)
+        self.slab = [d for d in node.domain if d not in fixed]
+        self.slab_ext = [low.ext[d] for d in self.slab]
+
+    def dimmap(self, payload_coords=None):
+        m = {}
+        for b, v in self.low.benv.items():
+            m[(b, "bound")] = ("const", v)
+        for d in self.node.domain:
+            if d in self.fixed:
+                m[(d, "loop")] = ("env", self.low.slot[d])
+            else:
+                m[(d, "loop")] = ("coord", self.slab.index(d))
+        if payload_coords:
+            m.update(payload_coords)
+        return m
+
+    def sink_box(self):
+        return {d: (0, self.low.ext[d] - 1) for d in self.node.domain}
+
+
+class Lowering:
+    def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None):
+        self.plan = plan
+        self.g = plan.graph
+        self.benv = plan.benv
+        self.ext = plan.ext
+        self.bufs = bufs
+        self.status = status_ptr
+        self.seed = seed
+        self.slot = {d: i for i, d in enumerate(self.g.dim_order)}
+        if len(self.slot) > N.RT_MAXENV:
+            raise LowerError("too many dims")
+        self.recs: list = []       # (kernel, params ctypes obj, grid, block, smem, label)
+        self.prog: list = []       # (op, a, b, c, d, e)
+        self.alloc = alloc         # nbytes -> device pointer (scratch)
+        self.contract = contract or {}   # sum nid -> virtual matmul nid
+        self.virtual = set(self.contract.values())
+        self.launches_per_kernel = {}
+
+    # -- buffers -------------------------------------------------------------
+
+    def storage(self, key):
+        b = self.bufs[key]
+        while b.alias is not None:
+            b = self.bufs[b.alias]
+        return b
+
+    # -- edge views ----------------------------------------------------------
+
+    def edge_val(self, ctx: Ctx, e) -> EdgeVal:
+        src = self.g.nodes[e.src]
+        sb = self.bufs[(e.src, e.oid)]
+        st = self.storage((e.src, e.oid))
+        dstr = sb.strides[:len(sb.dims)]
+        ev = EdgeVal(buf=st)
+        box = ctx.sink_box()
+        if e.psi is not None:
+            ev.psi = subst_bounds(e.psi, self.benv)
+        slice_axes = []
+        for j, c in enumerate(e.phi):
+            c = subst_bounds(c, self.benv)
+            S = dstr[j]
+            hi_dom = sb.dshape[j]
+            if c[0] == "slice":
+                lo, hi = c[1], c[2]
+                aff = ir.as_affine(lo)
+                ln = ir.as_affine(("sub", hi, lo))
+                if aff is None:
+                    raise LowerError(f"{ctx.node.name}: non-affine slice start {ir.expr_text(lo)}")
+                self._add_affine(ev, aff, S)
+                L = None
+                if ln is not None and not ln[0]:
+                    L = max(0, ln[1])
+                slice_axes.append(Axis(L, S, ("sub", hi, lo), lo))
+                continue
+            aff = ir.as_affine(c)
+            if aff is None:
+                ev.progs.append((c, S, hi_dom))
+                continue
+            self._add_affine(ev, aff, S)
+            lo_, hi_ = interval(c, box)
+            if lo_ < 0 or hi_ >= hi_dom:
+                ev.checks.append((aff[1], {n: v for (n, k), v in aff[0].items()}, hi_dom))
+        ev.axes = slice_axes + [Axis(p, s) for p, s in zip(sb.pshape, sb.payload_strides())]
+        ev.nslices = len(slice_axes)
+        return ev
+
+    def _add_affine(self, ev, aff, S):
+        co, k = aff
+        ev.off += k * S
+        for (name, kind), a in co.items():
+            if kind != "loop":
+                raise LowerError(f"unbound symbol {name}")
+            ev.coef[name] = ev.coef.get(name, 0) + a * S
+
+    def make_view(self, ctx: Ctx, ev: EdgeVal, payload_strides: list, extra_off=0,
+                  extra_checks=()) -> N.rt_view:
+        """rt_view over box = slab dims + payload dims."""
+        v = N.rt_view()
+        v.ptr = ev.buf.ptr
+        v.dtype = N.DTYPE_CODE[ev.buf.dtype]
+        v.off = ev.off + extra_off
+        nd = len(ctx.slab) + len(payload_strides)
+        if nd > N.RT_MAXD:
+            raise LowerError("box rank too large")
+        for d, s in ev.coef.items():
+            if d in ctx.fixed:
+                v.off_env[self.slot[d]] += s
+            elif d in ctx.slab:
+                v.stride[ctx.slab.index(d)] += s
+            else:
+                raise LowerError(f"{ctx.node.name}: index uses dim {d} outside its domain")
+        for i, s in enumerate(payload_strides):
+            v.stride[len(ctx.slab) + i] = s
+        checks = list(ev.checks) + list(extra_checks)
+        if len(checks) > N.RT_MAXCHK:
+            raise LowerError("too many range checks")
+        v.nchk = len(checks)
+        for ci, (k, co, hi) in enumerate(checks):
+            v.chk_c0[ci] = k
+            v.chk_hi[ci] = hi
+            for d, a in co.items():
+                if isinstance(d, int):           # payload box dim
+                    v.chk_a[ci][len(ctx.slab) + d] = a
+                elif d in ctx.fixed:
+                    v.chk_env[ci][self.slot[d]] = a
+                else:
+                    v.chk_a[ci][ctx.slab.index(d)] = a
+        return v
+
+    def out_view(self, ctx: Ctx, key) -> N.rt_view:
+        b = self.bufs[key]
+        st = self.storage(key)
+        v = N.rt_view()
+        v.ptr = st.ptr
+        v.dtype = N.DTYPE_CODE[st.dtype]
+        strides = st.strides
+        for j, d in enumerate(b.dims):
+            if d in ctx.fixed:
+                v.off_env[self.slot[d]] = strides[j]
+            else:
+                v.stride[ctx.slab.index(d)] = strides[j]
+        for i, s in enumerate(strides[len(b.dims):]):
+            v.stride[len(ctx.slab) + i] = s
+        return v
+
+    # -- payload maps -------------------------------------------------------
+
+    @staticmethod
+    def bcast(ev: EdgeVal, out_shape):
+        """numpy broadcasting of the edge value onto out_shape."""
+        V = ev.axes
+        off = len(out_shape) - len(V)
+        if off < 0:
+            raise LowerError("cannot broadcast to a lower rank")
+        out = []
+        for j in range(len(out_shape)):
+            vj = j - off
+            if vj < 0:
+                out.append(0)
+            else:
+                ax = V[vj]
+                if ax.ext is None:
+                    raise LowerError("ragged slice feeds an elementwise op")
+                out.append(0 if ax.ext == 1 else ax.stride)
+        return out
+
+    # -- records -----------------------------------------------------------------
+
+    def add_rec(self, kernel, params, grid, block, smem=0, label=""):
+        params.h.node = int(label[0]) if isinstance(label, tuple) else 0
+        params.h.status = self.status
+        self.recs.append((kernel, params, grid, block, smem, label))
+        self.prog.append((N.RT_OP_LAUNCH, len(self.recs) - 1, 0, 0, 0, 0))
+        return len(self.recs) - 1
+
+    @staticmethod
+    def grid1(total, block=256, cap=148 * 32):
+        return [max(1, min(cap, (int(total) + block - 1) // block)), 1, 1]
+
+    # -- program ----------------------------------------------------------------
+
+    def lower(self):
+        self.steps(self.plan.steps)
+        return self
+
+    def steps(self, steps):
+        for s in steps:
+            if isinstance(s, Bulk):
+                self.bulk(s)
+            else:
+                self.loop(s)
+
+    def loop(self, s: Loop):
+        n = self.ext[s.dim]
+        if s.step > 0:
+            start, stop = 0, n
+        else:
+            start, stop = n - 1, -1
+        at = len(self.prog)
+        self.prog.append([N.RT_OP_FOR, self.slot[s.dim], start, stop, s.step, 0])
+        self.steps(s.body)
+        self.prog.append((N.RT_OP_END, at, 0, 0, 0, 0))
+        self.prog[at][5] = len(self.prog)
+
+    # -- bulk steps ----------------------------------------------------------
+
+    def bulk(self, s: Bulk):
+        n = self.g.nodes[s.nid]
+        if self.bufs[(n.id, 0)].alias is not None or n.kind in ("const", "input"):
+            return  # aliases and leaves need no kernel
+        if n.id in self.virtual:
+            return  # fused into its consumer
+        ctx = Ctx(self, n, s.fixed)
+        if any(e == 0 for e in ctx.slab_ext):
+            return
+        fn = getattr(self, f"k_{n.kind}", None)
+        if fn is None:
+            if n.kind in EW_KINDS:
+                return self.ew(ctx)
+            raise LowerError(f"no kernel for op kind {n.kind!r}")
+        return fn(ctx)
+
+    # ---- elementwise family
+
+    def ew(self, ctx: Ctx):
+        n = ctx.node
+        key = (n.id, 0)
+        out_p = list(self.bufs[key].pshape)
+        ins = self.g.in_edges(n.id)
+        evs = [self.edge_val(ctx, e) for e in ins]
+        P = Prog()
+        views = []
+        f64 = n.dtype == "f64" or any(ev.buf.dtype == "f64" for ev in evs)
+        npay = len(out_p)
+        slab_n = len(ctx.slab)
+        payload_coords = None
+
+        def view_of(ev, pstrides, extra_off=0, extra_checks=()):
+            if ev.progs:
+                raise LowerError(f"{n.name}: non-affine index needs the gather path")
+            views.append(self.make_view(ctx, ev, pstrides, extra_off, extra_checks))
+            if len(views) > N.RT_MAXIN:
+                raise LowerError("too many operands")
+            return len(views) - 1
+
+        def load(ev, pstrides, **kw):
+            vi = view_of(ev, pstrides, **kw)
+            r = P.vreg()
+            P.emit("LOAD", d=r, imm=vi)
+            return r
+
+        k = n.kind
+        if k in ("add", "sub", "mul", "div"):
+            a = load(evs[0], self.bcast(evs[0], out_p))
+            b = load(evs[1], self.bcast(evs[1], out_p))
+            P.emit({"add": "VADD", "sub": "VSUB", "mul": "VMUL", "div": "VDIV"}[k], d=a, a=a, b=b)
+            P.emit("STORE", a=a)
+        elif k in ("neg", "exp", "log", "tanh", "sqrt"):
+            a = load(evs[0], self.bcast(evs[0], out_p))
+            P.emit("V" + k.upper(), d=a, a=a)
+            P.emit("STORE", a=a)
+        elif k == "pow_const":
+            a = load(evs[0], self.bcast(evs[0], out_p))
+            P.emit("VPOW", d=a, a=a, imm=P.k(n.params["exponent"]))
+            P.emit("STORE", a=a)
+        elif k == "cmp":
+            a = load(evs[0], self.bcast(evs[0], out_p))
+            b = load(evs[1], self.bcast(evs[1], out_p))
+            op = {"eq": "VEQ", "ne": "VNE", "lt": "VLT", "le": "VLE", "gt": "VGT",
+                  "ge": "VGE"}[n.params["op"]]
+            P.emit(op, d=a, a=a, b=b)
+            P.emit("STORE", a=a)
+        elif k == "where":
+            c = load(evs[0], self.bcast(evs[0], out_p))
+            a = load(evs[1], self.bcast(evs[1], out_p))
+            b = load(evs[2], self.bcast(evs[2], out_p))
+            P.emit("VWHERE", d=c, a=c, b=a, c=b)
+            P.emit("STORE", a=c)
+        elif k in ("cast", "identity", "detach", "expand", "set_symbol"):
+            a = load(evs[0], self.bcast(evs[0], out_p))
+            P.emit("STORE", a=a)
+        elif k == "reshape":
+            ev = evs[0]
+            if ev.nslices:
+                raise LowerError("reshape of a gathered slice")
+            pst = cstrides(out_p)
+            a = load(ev, pst)
+            P.emit("STORE", a=a)
+        elif k == "permute":
+            ev = evs[0]
+            order = n.params["order"]
+            pst = [ev.axes[o].stride for o in order]
+            a = load(ev, pst)
+            P.emit("STORE", a=a)
+        elif k == "squeeze":
+            ev = evs[0]
+            dd = n.params["dim"]
+            pst = [ax.stride for i, ax in enumerate(ev.axes) if i != dd]
+            a = load(ev, pst)
+            P.emit("STORE", a=a)
+        elif k == "unsqueeze":
+            ev = evs[0]
+            dd = n.params["dim"]
+            pst = [ax.stride for ax in ev.axes]
+            pst.insert(dd, 0)
+            a = load(ev, pst)
+            P.emit("STORE", a=a)
+        elif k == "eval_symbol":
+            sym = n.params["symbol"]
+            dm = ctx.dimmap()
+            r = P.int_expr(("sym", sym.name, sym.kind), dm)
+            v = P.vreg()
+            P.emit("VITOF", d=v, a=r)
+            P.emit("STORE", a=v)
+        elif k == "merge":
+            dm = ctx.dimmap()
+            conds = n.params["conds"]
+            for bi, cond in enumerate(conds):
+                ev = evs[bi]
+                if cond == ir.TRUE:
+                    a = load(ev, self.bcast(ev, out_p))
+                    P.emit("STORE", a=a)
+                    break
+                r = P.int_expr(subst_bounds(cond, self.benv), dm)
+                j = P.emit("JZ", a=r)
+                P.ifree_(r)
+                a = load(ev, self.bcast(ev, out_p))
+                P.emit("STORE", a=a)
+                P.vfree_(a)
+                P.code[j] = P.pc()
+            else:
+                # no branch holds: the reference raises (runtime.py:369-370);
+                # such points are never demanded by a valid program, store 0
+                z = P.vreg()
+                P.emit("VCONST", d=z, imm=P.k(0.0))
+                P.emit("STORE", a=z)
+        elif k == "scan":
+            # y = x + gamma*prev; prev absent (edge condition false) at the head
+            x = load(evs[0], self.bcast(evs[0], out_p))
+            psi = evs[1].psi
+            if psi is not None:
+                r = P.int_expr(psi, ctx.dimmap())
+                j = P.emit("JZ", a=r)
+            pv = load(evs[1], self.bcast(evs[1], out_p))
+            g = P.vreg()
+            P.emit("VCONST", d=g, imm=P.k(n.params["gamma"]))
+            P.emit("VMUL", d=g, a=g, b=pv)
+            P.emit("VADD", d=g, a=x, b=g)
+            P.emit("STORE", a=g)
+            if psi is not None:
+                P.code[j] = P.pc()
+            P.emit("STORE", a=x)
+        elif k == "index_select":
+            self._index_select(ctx, P, evs[0], out_p, view_of)
+        elif k == "slice_axis":
+            ev = evs[0]
+            ax = n.params["axis"]
+            bs = n.params["block"]
+            jd = n.params["dim"].name
+            pst = [a.stride for a in ev.axes]
+            if ev.axes[ax].ext is None:
+                raise LowerError("slice_axis over a ragged axis")
+            # source coordinate along ax = j*bs + k ; zero past the extent
+            co = {jd: bs, ax: 1}
+            extra = [(0, co, ev.axes[ax].ext)]
+            # j*bs*stride offset
+            ev2 = EdgeVal(buf=ev.buf, off=ev.off, coef=dict(ev.coef), checks=list(ev.checks),
+                          axes=ev.axes, nslices=ev.nslices)
+            ev2.coef[jd] = ev2.coef.get(jd, 0) + bs * ev.axes[ax].stride
+            a = load(ev2, pst, extra_checks=extra)
+            P.emit("STORE", a=a)
+        else:
+            raise LowerError(f"no elementwise lowering for {k}")
+        self._emit_ew(ctx, key, P, views, f64, out_p, (n.id, n.name))
+
+    def _index_select(self, ctx, P, ev, out_p, view_of):
+        n = ctx.node
+        dname = n.params["dim"].name
+        expr = subst_bounds(n.params["expr"], self.benv)
+        D = ev.axes[0].ext
+        S = ev.axes[0].stride
+        rest = [a.stride for a in ev.axes[1:]]
+        slab_n = len(ctx.slab)
+        if n.params.get("rows"):
+            # out[j, q] = x[expr(d := j), q]
+            dm = ctx.dimmap({(dname, "loop"): ("coord", slab_n)})
+            vi = view_of(ev, [0] + rest)
+        elif expr[0] == "slice":
+            dm = ctx.dimmap()
+            lo = P.int_expr(expr[1], dm)
+            hi = P.int_expr(expr[2], dm)
+            ok = self._range_ok(P, lo, hi, D)
+            j = P.emit("JZ", a=ok)
+            skip = P.emit("JMP")
+            P.code[j] = P.pc()
+            P.emit("ERROR", a=lo, b=hi, imm=N.RT_ERR_SLICE_RANGE)
+            P.code[skip] = P.pc()
+            P.ifree_(ok)
+            P.ifree_(hi)
+            # offset = (lo + j) * S where j = payload coord 0
+            vi = view_of(ev, [S] + rest)
+            off = P.ireg()
+            P.emit("ICONST", d=off, imm=S)
+            P.emit("IMUL", d=off, a=off, b=lo)
+            one = P.ireg()
+            P.emit("ICONST", d=one, imm=1)
+            v = P.vreg()
+            P.emit("LOADX", d=v, a=off, b=one, imm=vi)
+            P.emit("STORE", a=v)
+            return
+        else:
+            dm = ctx.dimmap()
+            vi = view_of(ev, rest)
+        row = P.int_expr(expr, dm)
+        zero = P.ireg()
+        P.emit("ICONST", d=zero, imm=0)
+        ok = P.ireg()
+        P.emit("IGE", d=ok, a=row, b=zero)
+        lim = P.ireg()
+        P.emit("ICONST", d=lim, imm=D)
+        t = P.ireg()
+        P.emit("ILT", d=t, a=row, b=lim)
+        P.emit("IAND", d=ok, a=ok, b=t)
+        j = P.emit("JZ", a=ok)
+        skip = P.emit("JMP")
+        P.code[j] = P.pc()
+        P.emit("ERROR", a=row, b=lim, imm=N.RT_ERR_ROW_RANGE)
+        P.code[skip] = P.pc()
+        off = P.ireg()
+        P.emit("ICONST", d=off, imm=S)
+        P.emit("IMUL", d=off, a=off, b=row)
+        v = P.vreg()
+        P.emit("LOADX", d=v, a=off, b=ok, imm=vi)
+        P.emit("STORE", a=v)
+
+    def _range_ok(self, P, lo, hi, D):
+        # 0 <= lo <= hi <= D
+        z = P.ireg()
+        P.emit("ICONST", d=z, imm=0)
+        ok = P.ireg()
+        P.emit("IGE", d=ok, a=lo, b=z)
+        P.emit("ILE", d=z, a=lo, b=hi)
+        P.emit("IAND", d=ok, a=ok, b=z)
+        P.emit("ICONST", d=z, imm=D)
+        P.emit("ILE", d=z, a=hi, b=z)
+        P.emit("IAND", d=ok, a=ok, b=z)
+        P.ifree_(z)
+        return ok
+
+    def _emit_ew(self, ctx, key, P, views, f64, out_p, label):
+        p = N.rt_ew_params()
+        box = list(ctx.slab_ext) + list(out_p)
+        if len(box) > N.RT_MAXD:
+            raise LowerError("box rank too large")
+        p.box.nd = len(box)
+        for i, e in enumerate(box):
+            p.box.ext[i] = e
+        p.total = prod(box)
+        p.nin = len(views)
+        p.f64 = 1 if f64 else 0
+        p.out = self.out_view(ctx, key)
+        for i, v in enumerate(views):
+            p.in_[i] = v
+        for i, w in enumerate(P.code):
+            p.code[i] = w
+        for i, c in enumerate(P.konst):
+            p.konst[i] = c
+        if p.total == 0:
+            return
+        self.add_rec(N.RT_K_EW, p, self.grid1(p.total), [256, 1, 1], 0, label)
+
+    # ---- reductions
+
+    def k_sum(self, ctx: Ctx):
+        n = ctx.node
+        if n.id in self.contract:
+            return self.k_contract(ctx, self.g.nodes[self.contract[n.id]])
+        (e,) = self.g.in_edges(n.id)
+        ev = self.edge_val(ctx, e)
+        dims = tuple(n.params["dims"])
+        return self._reduce(ctx, ev, dims, op=0)
+
+    def k_discounted_sum(self, ctx: Ctx):
+        n = ctx.node
+        (e,) = self.g.in_edges(n.id)
+        ev = self.edge_val(ctx, e)
+        ax = n.params["dim"]
+        if self._try_scan_window(ctx, ev, ax, n.params["gamma"], n.params.get("reverse", False)):
+            return
+        return self._reduce(ctx, ev, (ax,), op=1, gamma=n.params["gamma"],
+                            reverse=n.params.get("reverse", False))
+
+    def _try_scan_window(self, ctx, ev, ax, gamma, reverse):
+        """dsum/sum over r[..., t:T] (reverse scan) or r[..., 0:t+1] with
+        reversed weights (forward scan): O(T) instead of O(T^2)."""
+        n = ctx.node
+        if ax != 0 or ev.nslices != 1 or ev.progs or ev.checks:
+            return False
+        (e,) = self.g.in_edges(n.id)
+        src = self.g.nodes[e.src]
+        slice_pos = [j for j, c in enumerate(e.phi) if c[0] == "slice"]
+        (sj,) = slice_pos
+        sd = src.domain[sj]
+        if sd not in ctx.slab:
+            return False
+        # all other components must be the identity on the sink's dims
+        for j, c in enumerate(e.phi):
+            if j == sj:
+                continue
+            if c != ("sym", src.domain[j], "loop"):
+                return False
+        lo = subst_bounds(e.phi[sj][1], self.benv)
+        hi = subst_bounds(e.phi[sj][2], self.benv)
+        Tn = self.ext[sd]
+        if lo == ("sym", sd, "loop") and hi == ("int", Tn) and not reverse:
+            rev = True
+        elif lo == ("int", 0) and ir.as_affine(hi) == ({(sd, "loop"): 1}, 1) and reverse:
+            rev = False
+        else:
+            return False
+        if list(src.domain) != [d for d in n.domain] or self.bufs[(e.src, e.oid)].pshape != \
+                self.bufs[(n.id, 0)].pshape:
+            return False
+        # scan over the source buffer along sd, written to n's buffer
+        sb = self.storage((e.src, e.oid))
+        ob = self.storage((n.id, 0))
+        p = N.rt_scan_params()
+        slab = ctx.slab
+        pay = list(self.bufs[(n.id, 0)].pshape)
+        box = [self.ext[d] for d in slab] + pay
+        p.box.nd = len(box)
+        for i, x in enumerate(box):
+            p.box.ext[i] = x
+        p.sdim = slab.index(sd)
+        p.reverse = 1 if rev else 0
+        p.gamma = float(gamma) if gamma is not None else 1.0
+        p.f64 = 1 if ob.dtype == "f64" else 0
+        p.total_lines = prod(box) // box[p.sdim]
+        for which, b in (("in_", sb), ("out", ob)):
+            v = getattr(p, which)
+            v.ptr = b.ptr
+            v.dtype = N.DTYPE_CODE[b.dtype]
+            st = b.strides
+            for j, d in enumerate(n.domain):
+                if d in ctx.fixed:
+                    v.off_env[self.slot[d]] = st[j]
+                else:
+                    v.stride[slab.index(d)] = st[j]
+            for i, s in enumerate(st[len(n.domain):]):
+                v.stride[len(slab) + i] = s
+        warp = p.in_.stride[p.sdim] == 1 and p.out.stride[p.sdim] == 1
+        grid = self.grid1(p.total_lines * (32 if warp else 1))
+        self.add_rec(N.RT_K_SCAN, p, grid, [256, 1, 1], 0, (n.id, n.name))
+        return True
+
+    def _reduce(self, ctx, ev: EdgeVal, red_axes, op, gamma=1.0, reverse=False):
+        n = ctx.node
+        key = (n.id, 0)
+        if ev.progs:
+            raise LowerError(f"{n.name}: non-affine index feeding a reduction")
+        if op == 0 and len(red_axes) > 1:
+            ev, red_axes = _merge_reduced(ev, red_axes)
+        kept = [i for i in range(len(ev.axes)) if i not in red_axes]
+        out_p = list(self.bufs[key].pshape)
+        if [ev.axes[i].ext for i in kept] != out_p:
+            raise LowerError(f"{n.name}: reduction shape mismatch")
+        p = N.rt_reduce_params()
+        box = list(ctx.slab_ext) + out_p
+        p.box.nd = len(box)
+        for i, x in enumerate(box):
+            p.box.ext[i] = x
+        p.total = prod(box)
+        p.nred = len(red_axes)
+        if p.nred > 4:
+            raise LowerError("too many reduced axes")
+        p.op = op
+        p.gamma = float(gamma)
+        p.reverse = 1 if reverse else 0
+        out_dt = self.bufs[key].dtype
+        p.f64 = 1 if (ev.buf.dtype == "f64" or out_dt == "f64") else 0
+        pst = [ev.axes[i].stride for i in kept]
+        p.in_ = self.make_view(ctx, ev, pst)
+        p.out = self.out_view(ctx, key)
+        maxlen = 1
+        for j, ai in enumerate(red_axes):
+            ax = ev.axes[ai]
+            p.red_stride[j] = ax.stride
+            p.len_prog[j] = -1
+            p.lo_prog[j] = -1
+            if ax.ext is not None:
+                p.len0[j] = ax.ext
+                maxlen *= max(1, ax.ext)
+                continue
+            aff = ir.as_affine(ax.len_expr)
+            if aff is not None:
+                co, k = aff
+                p.len0[j] = k
+                for (name, kind), a in co.items():
+                    if name in ctx.fixed:
+                        p.len_env[j][self.slot[name]] = a
+                    elif name in ctx.slab:
+                        p.len_a[j][ctx.slab.index(name)] = a
+                    else:
+                        raise LowerError("slice length uses a dim outside the domain")
+                lo_, hi_ = interval(ax.len_expr, ctx.sink_box())
+                maxlen *= max(1, int(hi_) if hi_ != INF else 1 << 20)
+            else:
+                P = Prog()
+                r = P.int_expr(ax.len_expr, ctx.dimmap())
+                P.emit("ISTORE", a=r)
+                p.len_prog[j] = 0
+                for i, w in enumerate(P.code):
+                    p.code[i] = w
+                lo_, hi_ = interval(ax.len_expr, ctx.sink_box())
+                maxlen *= max(1, int(hi_) if hi_ != INF else 1 << 20)
+        if maxlen >= 256 and p.total < 148 * 64:
+            tpo = 1024 if maxlen >= 4096 else 256
+            p.threads_per_out = tpo
+            grid = [max(1, min(p.total, 148 * 16)), 1, 1]
+            block = [tpo, 1, 1]
+        else:
+            p.threads_per_out = 1
+            grid = self.grid1(p.total)
+            block = [256, 1, 1]
+        self.add_rec(N.RT_K_REDUCE, p, grid, block, 0, (n.id, n.name))
+
+    def k_window_reduce(self, ctx: Ctx):
+        n = ctx.node
+        (e,) = self.g.in_edges(n.id)
+        ev = self.edge_val(ctx, e)
+        if _ragged(ev):
+            raise LowerError("window_reduce over a ragged slice")
+        dname = n.params["dim"].name
+        nb = self.benv[n.params["bound"].name]
+        D = ev.axes[0].ext
+        lo = subst_bounds(n.params["lo"], self.benv)
+        hi = subst_bounds(n.params["hi"], self.benv)
+        op = 0 if n.params["op"] == "sum" else 1
+        gamma = n.params.get("gamma") or 1.0
+        reverse = n.params.get("reverse", False)
+        key = (n.id, 0)
+        slab_n = len(ctx.slab)
+        # payload coord 0 is the folded dim's row j
+        dm = ctx.dimmap({(dname, "loop"): ("coord", slab_n)})
+        # suffix form lo = d, hi = D: reverse scan of the value along axis 0
+        if lo == ("sym", dname, "loop") and (hi == ("int", D) or hi == ("int", nb)) and D == nb \
+                and not reverse and not ev.checks:
+            return self._scan_value(ctx, ev, key, axis=0, gamma=gamma if op else 1.0, rev=True)
+        lo_c = ("max", ("int", 0), lo)
+        hi_c = ("min", ("int", D), hi)
+        p = N.rt_reduce_params()
+        out_p = list(self.bufs[key].pshape)
+        box = list(ctx.slab_ext) + out_p
+        p.box.nd = len(box)
+        for i, x in enumerate(box):
+            p.box.ext[i] = x
+        p.total = prod(box)
+        p.nred = 1
+        p.op = op
+        p.gamma = float(gamma)
+        p.reverse = 1 if reverse else 0
+        p.f64 = 1 if ev.buf.dtype == "f64" else 0
+        pst = [0] + [a.stride for a in ev.axes[1:]]
+        p.in_ = self.make_view(ctx, ev, pst)
+        p.out = self.out_view(ctx, key)
+        P = Prog()
+        r = P.int_expr(lo_c, dm)
+        P.emit("ISTORE", a=r)
+        P.ifree_(r)
+        lo_pc = 0
+        len_pc = P.pc()
+        a = P.int_expr(hi_c, dm)
+        b = P.int_expr(lo_c, dm)
+        P.emit("ISUB", d=a, a=a, b=b)
+        P.emit("ISTORE", a=a)
+        p.lo_prog[0] = lo_pc
+        p.len_prog[0] = len_pc
+        p.red_stride[0] = ev.axes[0].stride
+        for i, w in enumerate(P.code):
+            p.code[i] = w
+        p.threads_per_out = 1
+        self.add_rec(N.RT_K_REDUCE, p, self.grid1(p.total), [256, 1, 1], 0, (n.id, n.name))
+
+    def _scan_value(self, ctx, ev, key, axis, gamma, rev):
+        n = ctx.node
+        p = N.rt_scan_params()
+        out_p = list(self.bufs[key].pshape)
+        box = list(ctx.slab_ext) + out_p
+        p.box.nd = len(box)
+        for i, x in enumerate(box):
+            p.box.ext[i] = x
+        p.sdim = len(ctx.slab) + axis
+        p.reverse = 1 if rev else 0
+        p.gamma = float(gamma)
+        ob = self.storage(key)
+        p.f64 = 1 if ob.dtype == "f64" else 0
+        p.total_lines = prod(box) // box[p.sdim]
+        p.in_ = self.make_view(ctx, ev, [a.stride for a in ev.axes])
+        p.out = self.out_view(ctx, key)
+        warp = p.in_.stride[p.sdim] == 1 and p.out.stride[p.sdim] == 1
+        grid = self.grid1(p.total_lines * (32 if warp else 1))
+        self.add_rec(N.RT_K_SCAN, p, grid, [256, 1, 1], 0, (n.id, n.name))
+
+    def k_cumsum(self, ctx: Ctx):
+        n = ctx.node
+        (e,) = self.g.in_edges(n.id)
+        ev = self.edge_val(ctx, e)
+        if _ragged(ev) or ev.checks:
+            raise LowerError("cumsum over a ragged slice")
+        return self._scan_value(ctx, ev, (n.id, 0), n.params["dim"], 1.0,
+                                bool(n.params.get("reverse")))
+
+    def k_discounted_cumsum(self, ctx: Ctx):
+        n = ctx.node
+        (e,) = self.g.in_edges(n.id)
+        ev = self.edge_val(ctx, e)
+        if _ragged(ev) or ev.checks:
+            raise LowerError("discounted_cumsum over a ragged slice")
+        return self._scan_value(ctx, ev, (n.id, 0), n.params["dim"], n.params["gamma"],
+                                bool(n.params.get("reverse")))
+
+    # ---- matmul
+
+    def k_matmul(self, ctx: Ctx):
+        n = ctx.node
+        ea, eb = self.g.in_edges(n.id)
+        A, B = self.edge_val(ctx, ea), self.edge_val(ctx, eb)
+        for ev in (A, B):
+            if _ragged(ev) or ev.checks or ev.progs:
+                raise LowerError(f"{n.name}: matmul operand needs a gather")
+        key = (n.id, 0)
+        st = self.storage(key)
+        a_ax, b_ax, batch, m, nn, kk, c_log = self._mm_shapes(A, B, st.strides[len(st.dims):])
+        cdst = {d: st.strides[j] for j, d in enumerate(self.bufs[key].dims)}
+        Z, M, Nn, K = [], [], [], []
+        nb = len(batch)
+        for d in ctx.slab:
+            a_s, b_s, c_s = A.coef.get(d, 0), B.coef.get(d, 0), cdst[d]
+            if b_s != 0:
+                Z.append((self.ext[d], a_s, b_s, c_s))
+            else:
+                M.append((self.ext[d], a_s, 0, c_s))
+        for i, x in enumerate(batch):
+            Z.append((x, self._bstride(a_ax, i, nb), self._bstride(b_ax, i, nb), c_log[i]))
+        M.append((m, a_ax[-2].stride, 0, c_log[nb]))
+        Nn.append((nn, 0, b_ax[-1].stride, c_log[nb + 1]))
+        K.append((kk, a_ax[-1].stride, b_ax[-2].stride, 0))
+        env_a = {self.slot[d]: s for d, s in A.coef.items() if d in ctx.fixed}
+        env_b = {self.slot[d]: s for d, s in B.coef.items() if d in ctx.fixed}
+        env_c = {self.slot[d]: cdst[d] for d in ctx.fixed if d in cdst}
+        self._gemm((A.buf, A.off, env_a), (B.buf, B.off, env_b), (st, 0, env_c),
+                   Z, M, Nn, K, (n.id, n.name))
+
+    @staticmethod
+    def _bstride(axes, i, nb):
+        off = nb - (len(axes) - 2)
+        j = i - off
+        if j < 0:
+            return 0
+        ax = axes[j]
+        return 0 if ax.ext == 1 else ax.stride
+
+    @staticmethod
+    def _mm_shapes(A, B, c_pstr):
+        """numpy matmul promotion (frontend.py:485-502): logical operands
+        (batch..., m, k) @ (batch..., k, n); output strides for (batch, m, n)."""
+        a_vec, b_vec = len(A.axes) == 1, len(B.axes) == 1
+        a_ax = [Axis(1, 0)] + A.axes if a_vec else list(A.axes)
+        b_ax = B.axes + [Axis(1, 0)] if b_vec else list(B.axes)
+        m, kk = a_ax[-2].ext, a_ax[-1].ext
+        k2, nn = b_ax[-2].ext, b_ax[-1].ext
+        if kk != k2:
+            raise LowerError("matmul inner dims differ")
+        batch = list(np.broadcast_shapes(tuple(x.ext for x in a_ax[:-2]),
+                                         tuple(x.ext for x in b_ax[:-2])))
+        c = list(c_pstr)
+        nb = len(batch)
+        if a_vec and b_vec:
+            c_log = c + [0, 0]
+        elif a_vec:
+            c_log = c[:nb] + [0] + c[nb:]
+        elif b_vec:
+            c_log = c + [0]
+        else:
+            c_log = c
+        if len(c_log) != nb + 2:
+            raise LowerError("matmul output layout mismatch")
+        return a_ax, b_ax, batch, m, nn, kk, c_log
+
+    def _gemm(self, A, B, Cc, Z, M, Nn, K, label, accumulate=0, epilogue=0, bias=None):
+        """Z/M/N/K: lists of (extent, a_stride, b_stride, c_stride).
+        A/B/C: (buf, element offset, {env slot: stride})."""
+        p = N.rt_gemm_params()
+        if not Z:
+            Z = [(1, 0, 0, 0)]
+        for gb, lst in ((p.Z, Z), (p.M, M), (p.N, Nn), (p.K, K)):
+            if len(lst) > 4:
+                raise LowerError("gemm decomposition too deep")
+            gb.nd = len(lst)
+            for i, t in enumerate(lst):
+                gb.ext[i] = t[0]
+        p.z, p.m, p.n, p.k = (prod(t[0] for t in Z), prod(t[0] for t in M),
+                              prod(t[0] for t in Nn), prod(t[0] for t in K))
+        for op, (buf, off, envs), role in ((p.A, A, 0), (p.B, B, 1), (p.C, Cc, 2)):
+            op.ptr = buf.ptr
+            op.dtype = N.DTYPE_CODE[buf.dtype]
+            op.off = off
+            for sl, s in envs.items():
+                op.off_env[sl] += s
+            col = 1 + role if role < 2 else 3
+            for i, t in enumerate(Z):
+                op.sz[i] = t[1 + role]
+            if role == 0:
+                for i, t in enumerate(M):
+                    op.s1[i] = t[1]
+                for i, t in enumerate(K):
+                    op.s2[i] = t[1]
+            elif role == 1:
+                for i, t in enumerate(K):
+                    op.s1[i] = t[2]
+                for i, t in enumerate(Nn):
+                    op.s2[i] = t[2]
+            else:
+                for i, t in enumerate(M):
+                    op.s1[i] = t[3]
+                for i, t in enumerate(Nn):
+                    op.s2[i] = t[3]
+            del col
+        p.f64 = 1 if Cc[0].dtype == "f64" else 0
+        p.splits = 1
+        p.accumulate = accumulate
+        p.epilogue = epilogue
+        if bias is not None:
+            p.bias = bias
+        tiles = ((p.m + 63) // 64) * ((p.n + 63) // 64) * p.z
+        splits = 1
+        if tiles < 148 and p.k >= 1024:
+            splits = int(min(128, max(1, (148 * 4) // max(1, tiles)), max(1, p.k // 512)))
+        if p.z * splits > 65535 or (p.m + 63) // 64 > 65535:
+            raise LowerError("gemm grid too large")
+        if splits > 1:
+            p.splits = splits
+            esize = 8 if p.f64 else 4
+            p.part = self.alloc(splits * p.z * p.m * p.n * esize)
+            grid = [(p.n + 63) // 64, (p.m + 63) // 64, p.z * splits]
+            self.add_rec(N.RT_K_GEMM, p, grid, [256, 1, 1], 0, label)
+            q = N.rt_splitk_params()
+            q.Z, q.M, q.N = p.Z, p.M, p.N
+            q.z, q.m, q.n = p.z, p.m, p.n
+            q.splits = splits
+            q.f64 = p.f64
+            q.accumulate = accumulate
+            q.epilogue = epilogue
+            q.part = p.part
+            q.C = p.C
+            if bias is not None:
+                q.bias = bias
+            self.add_rec(N.RT_K_SPLITK, q, self.grid1(p.z * p.m * p.n), [256, 1, 1], 0, label)
+        else:
+            grid = [(p.n + 63) // 64, (p.m + 63) // 64, p.z]
+            self.add_rec(N.RT_K_GEMM, p, grid, [256, 1, 1], 0, label)
+
+    def k_contract(self, ctx: Ctx, X):
+        """sum over full-range slices of a per-point matmul X, never
+        materialising X: one GEMM whose K runs over the gathered points
+        (the dW of the symbolic backward, frontend.py:766-776, 984-989)."""
+        S = ctx.node
+        (es,) = self.g.in_edges(S.id)
+        xctx = Ctx(self, X, ctx.fixed)
+        ea, eb = self.g.in_edges(X.id)
+        A, B = self.edge_val(xctx, ea), self.edge_val(xctx, eb)
+        for ev in (A, B):
+            if ev.nslices or ev.checks or ev.progs:
+                raise LowerError(f"{X.name}: contraction operand needs a gather")
+        key = (S.id, 0)
+        st = self.storage(key)
+        a_ax, b_ax, batch, m, nn, kk, c_log = self._mm_shapes(A, B, st.strides[len(st.dims):])
+        if batch:
+            raise LowerError("batched contraction")
+        cdst = {d: st.strides[j] for j, d in enumerate(self.bufs[key].dims)}
+        red = [X.domain[j] for j, c in enumerate(es.phi) if c[0] == "slice"]
+        Z, M, Nn, K = [], [], [], []
+        for d in ctx.slab:              # kept dims of S (identity in X)
+            a_s, b_s, c_s = A.coef.get(d, 0), B.coef.get(d, 0), cdst[d]
+            if b_s != 0:
+                Z.append((self.ext[d], a_s, b_s, c_s))
+            else:
+                M.append((self.ext[d], a_s, 0, c_s))
+        M.append((m, a_ax[-2].stride, 0, c_log[0]))
+        Nn.append((nn, 0, b_ax[-1].stride, c_log[1]))
+        for d in red:
+            K.append((self.ext[d], A.coef.get(d, 0), B.coef.get(d, 0), 0))
+        K.append((kk, a_ax[-1].stride, b_ax[-2].stride, 0))
+        env_a = {self.slot[d]: s for d, s in A.coef.items() if d in ctx.fixed}
+        env_b = {self.slot[d]: s for d, s in B.coef.items() if d in ctx.fixed}
+        env_c = {self.slot[d]: cdst[d] for d in ctx.fixed if d in cdst}
+        self._gemm((A.buf, A.off, env_a), (B.buf, B.off, env_b), (st, 0, env_c),
+                   Z, M, Nn, K, (S.id, S.name))
+
+    # ---- rng / udf
+
+    def _coord_src(self, ctx):
+        src = []
+        for d in ctx.node.domain:
+            if d in ctx.fixed:
+                src.append(-1 - self.slot[d])
+            else:
+                src.append(ctx.slab.index(d))
+        return src
+
+    @staticmethod
+    def words(v):
+        if v < 0:
+            raise LowerError("negative entropy")
+        if v == 0:
+            return [0]
+        out = []
+        while v:
+            out.append(v & 0xFFFFFFFF)
+            v >>= 32
+        return out
+
+    def k_rng(self, ctx: Ctx):
+        n = ctx.node
+        key = (n.id, 0)
+        tag = n.params.get("tag", n.params.get("uid", n.id))
+        prefix = self.words(self.seed) + self.words(tag)
+        if len(prefix) > 8:
+            raise LowerError("entropy prefix too long")
+        p = N.rt_rng_params()
+        box = list(ctx.slab_ext)
+        p.box.nd = len(box)
+        for i, x in enumerate(box):
+            p.box.ext[i] = x
+        p.total = prod(box)
+        p.nprefix = len(prefix)
+        for i, w in enumerate(prefix):
+            p.prefix[i] = w
+        cs = self._coord_src(ctx)
+        p.ncoord = len(cs)
+        for i, c in enumerate(cs):
+            p.coord_src[i] = c
+        p.dist = 0 if n.params["dist"] == "normal" else 1
+        p.count = prod(self.bufs[key].pshape)
+        p.out = self.out_view(ctx, key)
+        self.add_rec(N.RT_K_RNG, p, self.grid1(p.total, 128), [128, 1, 1], 0, (n.id, n.name))
+
+    def k_udf(self, ctx: Ctx):
+        n = ctx.node
+        spec = n.params["spec"]
+        if not getattr(spec, "synthetic", False):
+            raise LowerError(f"udf {spec.name}: only synthetic (make_udf_fn) bodies run on device")
+        tag = n.params.get("tag", n.params.get("uid", n.id))
+        prefix = self.words(self.seed) + self.words(tag)
+        p = N.rt_udf_params()
+        box = list(ctx.slab_ext)
+        p.box.nd = len(box)
+        for i, x in enumerate(box):
+            p.box.ext[i] = x
+        p.total = prod(box)
+        p.nprefix = len(prefix)
+        for i, w in enumerate(prefix):
+            p.prefix[i] = w
+        cs = self._coord_src(ctx)
+        p.ncoord = len(cs)
+        for i, c in enumerate(cs):
+            p.coord_src[i] = c
+        p.salt = zlib.crc32(spec.name.encode()) % 997 / 997.0
+        ins = self.g.in_edges(n.id)
+        if len(ins) > 4 or len(n.out_shapes) > 4:
+            raise LowerError("udf arity > 4")
+        p.nin = len(ins)
+        for i, e in enumerate(ins):
+            ev = self.edge_val(ctx, e)
+            if _ragged(ev) or ev.progs:
+                raise LowerError("udf input needs a gather")
+            cnt = prod(a.ext for a in ev.axes)
+            if [a.stride for a in ev.axes] != cstrides([a.ext for a in ev.axes]):
+                raise LowerError("udf input payload not contiguous")
+            p.in_count[i] = cnt
+            p.in_[i] = self.make_view(ctx, ev, [])
+        p.nout = len(n.out_shapes)
+        for j in range(p.nout):
+            k = (n.id, j)
+            p.out_count[j] = prod(self.bufs[k].pshape)
+            p.out_kind[j] = N.DTYPE_CODE[n.out_dtypes[j]]
+            p.out[j] = self.out_view(ctx, k)
+        self.add_rec(N.RT_K_UDF, p, self.grid1(p.total, 128), [128, 1, 1], 0, (n.id, n.name))
+
+
+def _ragged(ev):
+    return any(a.ext is None for a in ev.axes)
+
+
+def _merge_reduced(ev, red_axes):
+    """Collapse runs of reduced axes that are contiguous in memory into one
+    (e.g. the payload of a sumall), keeping at most 4 reduced axes."""
+    red = sorted(red_axes)
+    axes = list(ev.axes)
+    i = 0
+    while i + 1 < len(red):
+        a, b = red[i], red[i + 1]
+        A, B = axes[a], axes[b]
+        if b == a + 1 and A.ext is not None and B.ext is not None and \
+                A.stride == B.stride * B.ext:
+            axes[a] = Axis(A.ext * B.ext, B.stride)
+            del axes[b]
+            red = [r if r < b else r - 1 for r in red if r != b]
+            continue
+        i += 1
+    ev2 = EdgeVal(buf=ev.buf, off=ev.off, coef=ev.coef, checks=ev.checks, axes=axes,
+                  nslices=ev.nslices, progs=ev.progs, psi=ev.psi)
+    return ev2, tuple(red)
+
+
+EW_KINDS = {"add", "sub", "mul", "div", "neg", "exp", "log", "tanh", "sqrt", "pow_const",
+            "cmp", "where", "cast", "identity", "detach", "expand", "reshape", "permute",
+            "squeeze", "unsqueeze", "eval_symbol", "merge", "scan", "index_select",
+            "slice_axis", "set_symbol"}

@@ -1,0 +1,345 @@
+"""Loop-nest planning: which points of which nodes run in one launch.
+
+The reference evaluates one (node, point) at a time, on demand, recursing
+through edges (runtime.py:344-425).  A B200 executor must instead evaluate
+whole slabs of points per launch.  The planner derives the loop nest from
+the dependence structure itself, the same well-foundedness argument the
+reference uses to *validate* cycles (pdg.py:607-668, `_well_founded`):
+
+  * strongly connected components of the graph, in topological order;
+  * an acyclic component is one node: evaluated over all its remaining
+    dims at once (a "bulk" step);
+  * a cyclic component is scheduled by a loop over a dim d common to all
+    its members along which every internal dependence reads at distance
+    <= 0 (in the loop direction); edges at distance exactly 0 stay, the
+    rest are satisfied by the loop, and the body is planned recursively.
+
+Within a loop body every node is evaluated for all values of its free dims
+(e.g. all envs b at one step t) — the batching the reference's vectorizer
+cannot express across cycles.  Distances come from interval
+arithmetic over the concrete box, refined by simple edge conditions.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import ir
+from .ir import Graph
+
+INF = float("inf")
+
+
+class PlanError(Exception):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# interval arithmetic over concrete boxes
+
+
+def subst_bounds(e, benv: dict):
+    return ir.substitute(e, {(b, "bound"): ("int", v) for b, v in benv.items()})
+
+
+def interval(e, box: dict):
+    """(lo, hi) inclusive range of integer expression e over box
+    {dim: (lo, hi)}; bounds must already be substituted."""
+    k = e[0]
+    if k == "int":
+        return (e[1], e[1])
+    if k == "bool":
+        v = int(e[1])
+        return (v, v)
+    if k == "sym":
+        if e[2] == "loop" and e[1] in box:
+            return box[e[1]]
+        return (-INF, INF)
+    aff = ir.as_affine(e)
+    if aff is not None:
+        lo = hi = aff[1]
+        for (name, kind), c in aff[0].items():
+            if kind != "loop" or name not in box:
+                return (-INF, INF)
+            a, b = box[name]
+            lo += min(c * a, c * b)
+            hi += max(c * a, c * b)
+        return (lo, hi)
+    if k in ("min", "max"):
+        ivs = [interval(a, box) for a in e[1:]]
+        f = min if k == "min" else max
+        return (f(i[0] for i in ivs), f(i[1] for i in ivs))
+    if k == "neg":
+        a = interval(e[1], box)
+        return (-a[1], -a[0])
+    if k in ("add", "sub"):
+        a, b = interval(e[1], box), interval(e[2], box)
+        if k == "add":
+            return (a[0] + b[0], a[1] + b[1])
+        return (a[0] - b[1], a[1] - b[0])
+    if k == "floordiv" and e[2][0] == "int" and e[2][1] > 0:
+        a = interval(e[1], box)
+        c = e[2][1]
+        f = lambda x: x if x in (INF, -INF) else x // c  # noqa: E731
+        return (f(a[0]), f(a[1]))
+    if k == "mod" and e[2][0] == "int" and e[2][1] != 0:
+        return (0, abs(e[2][1]) - 1)
+    if k == "mul":
+        a, b = interval(e[1], box), interval(e[2], box)
+        cands = [x * y for x in a for y in b if not (x in (INF, -INF) and y == 0)
+                 and not (y in (INF, -INF) and x == 0)]
+        return (min(cands), max(cands)) if cands else (-INF, INF)
+    return (-INF, INF)
+
+
+def refine_box(psi, box: dict):
+    """Shrink box by the simple atoms of condition psi (bounds substituted).
+    Returns None when psi is unsatisfiable on the box."""
+    box = dict(box)
+    atoms = []
+
+    def collect(c):
+        if c[0] == "and":
+            collect(c[1])
+            collect(c[2])
+        else:
+            atoms.append(c)
+
+    collect(psi)
+    for a in atoms:
+        if a == ("bool", False):
+            return None
+        if a[0] not in ("eq", "lt", "le", "gt", "ge"):
+            continue
+        diff = ir.as_affine(("sub", a[1], a[2]))
+        if diff is None:
+            continue
+        co, k = diff
+        if len(co) != 1:
+            continue
+        ((name, kind), c), = co.items()
+        if kind != "loop" or name not in box or c not in (1, -1):
+            continue
+        # c*x + k  op  0
+        lo, hi = box[name]
+        op = a[0]
+        if c == -1:
+            op = {"eq": "eq", "lt": "gt", "le": "ge", "gt": "lt", "ge": "le"}[op]
+            k = -k
+        # x + k op 0  ->  x op -k
+        v = -k
+        if op == "eq":
+            lo, hi = max(lo, v), min(hi, v)
+        elif op == "lt":
+            hi = min(hi, v - 1)
+        elif op == "le":
+            hi = min(hi, v)
+        elif op == "gt":
+            lo = max(lo, v + 1)
+        elif op == "ge":
+            lo = max(lo, v)
+        if lo > hi:
+            return None
+        box[name] = (lo, hi)
+    return box
+
+
+# ---------------------------------------------------------------------------
+# plan structures
+
+
+@dataclass
+class Bulk:
+    nid: int
+    fixed: tuple          # dims bound by enclosing loops (outer first)
+
+
+@dataclass
+class Loop:
+    dim: str
+    step: int             # +1 ascending, -1 descending
+    body: list = field(default_factory=list)
+    fixed: tuple = ()
+
+
+@dataclass
+class Plan:
+    graph: Graph
+    benv: dict            # bound name -> int
+    ext: dict             # dim name -> int
+    steps: list
+
+
+def sccs(nodes, succ):
+    """Tarjan, iterative; components in discovery order."""
+    index, low, on, stack, out = {}, {}, set(), [], []
+    counter = [0]
+    for root in sorted(nodes):
+        if root in index:
+            continue
+        work = [(root, iter(sorted(succ.get(root, ()))))]
+        index[root] = low[root] = counter[0]
+        counter[0] += 1
+        stack.append(root)
+        on.add(root)
+        while work:
+            v, it = work[-1]
+            advanced = False
+            for w in it:
+                if w not in nodes:
+                    continue
+                if w not in index:
+                    index[w] = low[w] = counter[0]
+                    counter[0] += 1
+                    stack.append(w)
+                    on.add(w)
+                    work.append((w, iter(sorted(succ.get(w, ())))))
+                    advanced = True
+                    break
+                if w in on:
+                    low[v] = min(low[v], index[w])
+            if advanced:
+                continue
+            work.pop()
+            if work:
+                low[work[-1][0]] = min(low[work[-1][0]], low[v])
+            if low[v] == index[v]:
+                comp = []
+                while True:
+                    w = stack.pop()
+                    on.discard(w)
+                    comp.append(w)
+                    if w == v:
+                        break
+                out.append(sorted(comp))
+    return out
+
+
+class Planner:
+    def __init__(self, g: Graph, benv: dict):
+        self.g = g
+        self.benv = dict(benv)
+        self.ext = {d: benv[g.dim_bound[d]] for d in g.dim_order if g.dim_bound[d] in benv}
+        self._dist_cache = {}
+
+    # -- distances ----------------------------------------------------------
+
+    def sink_box(self, e):
+        n = self.g.nodes[e.sink]
+        box = {d: (0, self.ext[d] - 1) for d in n.domain}
+        if any(lo > hi for lo, hi in box.values()):
+            return None
+        if e.psi is not None:
+            box = refine_box(subst_bounds(e.psi, self.benv), box)
+        return box
+
+    def distance(self, e, d):
+        """(min, max) of src_d - snk_d over the edge, or None if vacuous.
+        Edges whose source lacks d impose nothing along d: (0, 0)."""
+        key = (id(e), d)
+        if key in self._dist_cache:
+            return self._dist_cache[key]
+        src = self.g.nodes[e.src]
+        snk = self.g.nodes[e.sink]
+        box = self.sink_box(e)
+        if box is None:
+            res = None
+        elif d not in src.domain:
+            res = (0, 0)
+        else:
+            c = subst_bounds(e.phi[src.domain.index(d)], self.benv)
+            if d not in snk.domain:
+                # sink lacks d: it reads (some) points along d of the source
+                res = (-INF, INF)
+            elif c[0] == "slice":
+                a = interval(("sub", c[1], ("sym", d, "loop")), box)
+                b = interval(("sub", ("sub", c[2], ("int", 1)), ("sym", d, "loop")), box)
+                res = (min(a[0], b[0]), max(a[1], b[1]))
+            else:
+                res = interval(("sub", c, ("sym", d, "loop")), box)
+        self._dist_cache[key] = res
+        return res
+
+    # -- recursive decomposition -----------------------------------------------
+
+    def plan(self):
+        nodes = set(self.g.nodes)
+        edges = list(self.g.edges)
+        return Plan(self.g, self.benv, self.ext, self.level(nodes, edges, ()))
+
+    def level(self, nodes: set, edges: list, fixed: tuple):
+        succ = {}
+        inner = [e for e in edges if e.src in nodes and e.sink in nodes]
+        for e in inner:
+            succ.setdefault(e.src, set()).add(e.sink)
+        comps = sccs(nodes, succ)
+        # topological order of the condensation (Kahn, ties by min id)
+        cid = {v: i for i, c in enumerate(comps) for v in c}
+        indeg = {i: 0 for i in range(len(comps))}
+        csucc = {i: set() for i in range(len(comps))}
+        for e in inner:
+            a, b = cid[e.src], cid[e.sink]
+            if a != b and b not in csucc[a]:
+                csucc[a].add(b)
+                indeg[b] += 1
+        ready = sorted((min(comps[i]), i) for i, k in indeg.items() if k == 0)
+        order = []
+        import heapq
+        heapq.heapify(ready)
+        while ready:
+            _, i = heapq.heappop(ready)
+            order.append(i)
+            for j in csucc[i]:
+                indeg[j] -= 1
+                if indeg[j] == 0:
+                    heapq.heappush(ready, (min(comps[j]), j))
+        steps = []
+        for i in order:
+            comp = comps[i]
+            cedges = [e for e in inner if e.src in comp and e.sink in comp]
+            if len(comp) == 1 and not cedges:
+                steps.append(Bulk(comp[0], fixed))
+                continue
+            steps.append(self.loop_for(set(comp), cedges, fixed))
+        return steps
+
+    def loop_for(self, comp: set, cedges: list, fixed: tuple):
+        common = [d for d in self.g.dim_order
+                  if d not in fixed and all(d in self.g.nodes[v].domain for v in comp)]
+        for d in common:
+            for step in (1, -1):
+                ok = True
+                flat = []
+                for e in cedges:
+                    dist = self.distance(e, d)
+                    if dist is None:
+                        continue  # vacuous edge
+                    lo, hi = dist
+                    if step < 0:
+                        lo, hi = -hi, -lo
+                    if hi > 0:
+                        ok = False
+                        break
+                    if hi == 0:
+                        flat.append(e)
+                # a loop must carry at least one dependence, or it only
+                # serialises independent points (e.g. envs b)
+                live = [e for e in cedges if self.distance(e, d) is not None]
+                if ok and len(flat) < len(live):
+                    body = self.level(comp, flat, fixed + (d,))
+                    return Loop(d, step, body, fixed)
+        names = ", ".join(self.g.nodes[v].name for v in sorted(comp))
+        raise PlanError(f"unschedulable cycle through [{names}]")
+
+
+def describe(steps, g: Graph, indent=0) -> str:
+    out = []
+    for s in steps:
+        if isinstance(s, Bulk):
+            n = g.nodes[s.nid]
+            free = [d for d in n.domain if d not in s.fixed]
+            out.append("  " * indent + f"bulk {n.name}:{n.kind} over ({','.join(free)})")
+        else:
+            out.append("  " * indent + f"for {s.dim} {'asc' if s.step > 0 else 'desc'}:")
+            out.append(describe(s.body, g, indent + 1))
+    return "\n".join(out)

@@ -296,12 +296,6 @@ def ctx_reinforce_mlp(B=1024, T=1000, I=1, d_o=16, H=256, d_a=4,
 
 def mlp_inputs(d_o=16, H=256, d_a=4, dtype="f32", seed=1234):
     """Weights ~ N(0, 1/fan_in) from default_rng(1234)."""
-    import numpy as np
-    rng = np.random.default_rng(seed)
-    dt = np.float32 if dtype == "f32" else np.float64
-    out = {}
-    for k, (fi, fo) in {"W1": (d_o, H), "W2": (H, H), "W3": (H, d_a)}.items():
-        out[f"{k}_0"] = (rng.standard_normal((fi, fo)) / np.sqrt(fi)).astype(dt)
-    for k, n in {"b1": H, "b2": H, "b3": d_a}.items():
-        out[f"{k}_0"] = np.zeros((1, n), dt)
-    return out
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+    from paper_2501_05408_b200.workloads import mlp_inputs as mk
+    return mk(d_o=d_o, H=H, d_a=d_a, dtype=dtype, seed=seed)
