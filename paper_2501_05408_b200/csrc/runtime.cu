@@ -256,3 +256,37 @@ extern "C" int rt_rng_fill(uint64_t dev_out, const uint32_t* prefix, int32_t npr
   cudaFree(dco);
   return rc;
 }
+
+// ------------------------------------------------------------ CUDA graphs
+// Capture a whole lowered program (every loop iteration unrolled into the
+// graph, each launch with its env already folded) and replay it with one
+// cudaGraphLaunch: the per-step launch cost of the T-long acting loop goes
+// from ~2 us of host work per kernel to the GPU's own inter-node gap.
+
+extern "C" int rt_graph_capture(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs,
+                                int32_t nrec, int64_t* env, int32_t nenv, uint64_t stream,
+                                uint64_t* graph_exec_out) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaGraph_t graph = nullptr;
+  int rc = cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+  if (rc) return rc;
+  int rrc = rt_run(prog, nprog, recs, nrec, env, nenv, stream, nullptr, 0);
+  rc = cuda_check(cudaStreamEndCapture(s, &graph), "end capture");
+  if (rrc) { if (graph) cudaGraphDestroy(graph); return rrc; }
+  if (rc) return rc;
+  cudaGraphExec_t ex = nullptr;
+  rc = cuda_check(cudaGraphInstantiate(&ex, graph, 0), "graph instantiate");
+  cudaGraphDestroy(graph);
+  if (rc) return rc;
+  *graph_exec_out = (uint64_t)ex;
+  return RT_OK;
+}
+
+extern "C" int rt_graph_launch(uint64_t graph_exec, uint64_t stream) {
+  return cuda_check(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream),
+                    "graph launch");
+}
+
+extern "C" int rt_graph_destroy(uint64_t graph_exec) {
+  return cuda_check(cudaGraphExecDestroy((cudaGraphExec_t)graph_exec), "graph destroy");
+}

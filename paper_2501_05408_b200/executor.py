@@ -342,6 +342,8 @@ class Executable:
         self.nprog = len(low.prog)
         self.env = (N.i64 * N.RT_MAXENV)()
         self.launch_count = self._count_launches(low.prog)
+        self.graph_exec = None
+        self.graph_failed = False
 
     def _scratch(self, nbytes):
         t = self.torch.empty(max(1, nbytes), dtype=self.torch.uint8, device=self.dev)
@@ -386,8 +388,8 @@ class Executable:
             b = self.bufs[(n.id, 0)]
             v = inputs[n.name]
             if isinstance(v, torch.Tensor) and v.is_cuda:
-                t = v[tuple(slice(0, e) for e in b.dshape)].to(
-                    dtype=_TORCH_DT[b.dtype]).contiguous()
+                t = v[tuple(slice(0, e) for e in b.dshape)] if b.dshape else v
+                t = t.to(dtype=_TORCH_DT[b.dtype]).contiguous()
                 if tuple(t.shape) != b.shape:
                     raise OracleError(f"{n.name} produced shape {tuple(t.shape)[len(b.dshape):]}, "
                                       f"declared {b.pshape}")
@@ -397,7 +399,7 @@ class Executable:
             arr = np.asarray(v)
             if b.dshape:
                 arr = arr[tuple(slice(0, e) for e in b.dshape)]
-            arr = np.ascontiguousarray(np.asarray(arr, DTYPES[b.dtype]))
+            arr = np.array(arr, dtype=DTYPES[b.dtype], order="C", copy=True)
             if arr.shape != b.shape:
                 raise OracleError(f"{n.name} produced shape {arr.shape[len(b.dshape):]}, "
                                   f"declared {b.pshape}")
@@ -407,12 +409,35 @@ class Executable:
                 src = src.pin_memory()
             dst.copy_(src, non_blocking=True)
 
-    def run(self, inputs, stream=None, events=None):
+    GRAPH_MIN_LAUNCHES = 64
+
+    def _ensure_graph(self, s):
+        if self.graph_exec is not None or self.graph_failed:
+            return
+        for i in range(N.RT_MAXENV):
+            self.env[i] = 0
+        cap = self.torch.cuda.Stream(self.dev)
+        cap.wait_stream(s)
+        out = N.u64()
+        rc = self.lib.rt_graph_capture(self.prog, self.nprog, self.recs, self.nrec, self.env,
+                                       N.RT_MAXENV, cap.cuda_stream, C.byref(out))
+        s.wait_stream(cap)
+        if rc != 0:
+            self.graph_failed = True
+            return
+        self.graph_exec = out.value
+
+    def run(self, inputs, stream=None, events=None, graph=True):
         torch = self.torch
         with torch.cuda.device(self.dev):
             s = stream or torch.cuda.current_stream(self.dev)
             self.upload_inputs(inputs, s)
             N.check(self.lib.rt_status_clear(self.status, s.cuda_stream), "status clear")
+            if graph and not events and self.launch_count >= self.GRAPH_MIN_LAUNCHES:
+                self._ensure_graph(s)
+                if self.graph_exec is not None:
+                    N.check(self.lib.rt_graph_launch(self.graph_exec, s.cuda_stream), "graph")
+                    return
             ev_arr, nev = None, 0
             if events:
                 ev_arr = (N.u64 * len(events))(*[e.cuda_event for e in events])
