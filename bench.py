@@ -161,34 +161,81 @@ def main():
     dev_in = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
     exe, _ = get_executable(g, bounds, dev_in, seed=rank)
 
-    def step_dev(inp, seed):
-        exe.run(inp)
+    def step_dev(inp, graph=None):
+        if graph is None:
+            exe.run(inp)
+        else:
+            exe.launch_graph(graph, inp)
         outs = exe.outputs(device_outputs=True)
         return next_inputs(outs)
 
-    # warmup (device path)
+    # warmup (device path, CUDA graph)
     inp = dev_in
     for w in range(args.warmup):
-        inp = step_dev(inp, w)
+        inp = step_dev(inp)
     torch.cuda.synchronize()
+
+    # per-kernel breakdown: one profiled step (event pair around every launch)
+    prof = exe.profile(inp)
+    from paper_2501_05408_b200 import roofline as RF
+    fam_ms, rows = {}, []
+    for r in prof:
+        fam = RF.FAMILY.get(r["kernel"], "?")
+        fam_ms[fam] = fam_ms.get(fam, 0.0) + r["ms"]
+        rows.append(r)
+    rows.sort(key=lambda r: -r["ms"])
+    dom = rows[0]
+    graph_ev, kev = exe.capture_with_events(dom["rec"])
+
     if dist:
         dist.barrier()
     clocks = Clocks()
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    dom_ms = []
     ev0.record()
     for s in range(args.steps):
-        inp = step_dev(inp, s)
+        inp = step_dev(inp, graph_ev)
+        ev1.record()
+        ev1.synchronize()
+        dom_ms.append(sum(kev[2 * i].elapsed_time(kev[2 * i + 1]) for i in range(len(kev) // 2)))
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     clk = clocks.stop()
+    exe.check_status()
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * B * T_STEPS / (ms / 1e3)
+
+    # roofline of the dominant kernel (live, inside the timed region)
+    hbm, tfl, src = peaks()
+    bytes_, flops = RF.cost(dom["kernel"], dom["params"])
+    n_inst = max(1, len(kev) // 2)
+    kms = sum(dom_ms) / len(dom_ms) / n_inst   # per launch
+    if flops and RF.FAMILY[dom["kernel"]] == "gemm":
+        ach = flops / (kms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": tfl, "unit": "TFLOP/s",
+                "frac": ach / tfl, "traffic": None}
+    else:
+        ach = bytes_ / (kms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": None}
+    roof.update({"kernel": RF.FAMILY[dom["kernel"]], "node": dom["label"][1],
+                 "ms_per_launch": kms, "launches_per_step": dom["count"],
+                 "share_of_step": dom["ms"] / max(1e-9, sum(r["ms"] for r in prof)),
+                 "peak_source": src})
+    top = []
+    for r in rows[:8]:
+        b_, f_ = RF.cost(r["kernel"], r["params"])
+        per = r["ms"] / max(1, r["count"])
+        top.append({"kernel": RF.FAMILY.get(r["kernel"]), "node": r["label"][1],
+                    "ms_step": round(r["ms"], 3), "launches": r["count"],
+                    "gbs": round(b_ / (per / 1e3) / 1e9, 1) if per > 0 else None,
+                    "tflops": round(f_ / (per / 1e3) / 1e12, 2) if f_ and per > 0 else None})
 
     # e2e through the public API with host buffers
     exe_h, _ = get_executable(g, bounds, host, seed=rank)
@@ -218,6 +265,10 @@ def main():
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": exe.launch_count * args.steps,
             "peak_hbm_bytes": exe.peak_bytes,
+            "naive_hbm_bytes": exe.naive_bytes,
+            "roofline": roof,
+            "breakdown": {"family_ms_per_step": {k: round(v, 3) for k, v in fam_ms.items()},
+                          "top": top},
             "clocks": clk}
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()

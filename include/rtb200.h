@@ -279,8 +279,15 @@ int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32
  * launch) and replay it; the graph-exec handle is returned in *out. */
 int rt_graph_capture(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,
                      int64_t* env, int32_t nenv, uint64_t stream, uint64_t* out);
+int rt_graph_capture_ev(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs,
+                        int32_t nrec, int64_t* env, int32_t nenv, uint64_t stream,
+                        const uint64_t* events, int32_t nevents, uint64_t* out);
 int rt_graph_launch(uint64_t graph_exec, uint64_t stream);
 int rt_graph_destroy(uint64_t graph_exec);
+/* Run a program with an event pair around every launch instance; per launch
+ * record: total device ms and instance count.  Synchronises the stream. */
+int rt_profile(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,
+               int64_t* env, int32_t nenv, uint64_t stream, double* rec_ms, int64_t* rec_count);
 /* Device status word: int32[4] = {code, node, aux0, aux1}; allocate/clear/read. */
 int rt_status_alloc(uint64_t* dev_ptr);
 int rt_status_read(uint64_t dev_ptr, int32_t* host4, uint64_t stream);

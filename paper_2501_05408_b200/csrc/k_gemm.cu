@@ -19,12 +19,14 @@
 #define BK 16
 
 RT_DEV int64_t gdecomp(const rt_gbox& b, int64_t flat, const int64_t* s) {
+  // all extents and flat indices are < 2^31 (checked by the planner)
+  uint32_t f = (uint32_t)flat;
   int64_t o = 0;
   for (int d = b.nd - 1; d >= 0; --d) {
-    int64_t e = b.ext[d];
-    int64_t q = flat / e;
-    o += (flat - q * e) * s[d];
-    flat = q;
+    uint32_t e = (uint32_t)b.ext[d];
+    uint32_t q = f / e;
+    o += (int64_t)(f - q * e) * s[d];
+    f = q;
   }
   return o;
 }
@@ -35,16 +37,17 @@ RT_DEV T gload(const rt_gop& o, int64_t off) {
 }
 
 template <typename T>
-RT_DEV T epi(const rt_gemm_params& p, T v) {
-  if (p.epilogue == 1) return vm_tanh<T>(v);
-  return v;
+RT_DEV T gload_f(const void* base, int dtype, int64_t off) {
+  if (dtype == RT_F32) return (T)((const float*)base)[off];
+  if (dtype == RT_F64) return (T)((const double*)base)[off];
+  return load_as<T>(base, dtype, off);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_gemm(const __grid_constant__ rt_gemm_params p) {
   __shared__ T As[BK][BM + 4];
   __shared__ T Bs[BK][BN + 4];
-  __shared__ int64_t offA_row[BM], offB_col[BN], offA_k[BK], offB_k[BK];
+  __shared__ int64_t rowA[BM], rowC[BM], colB[BN], colC[BN], colBias[BN], kA[BK], kB[BK];
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -53,15 +56,23 @@ __global__ void __launch_bounds__(256) k_gemm(const __grid_constant__ rt_gemm_pa
   const int64_t zs = blockIdx.z;
   const int64_t zi = zs / p.splits;
   const int split = (int)(zs - zi * p.splits);
+  const void* Ap = (const void*)p.A.ptr;
+  const void* Bp = (const void*)p.B.ptr;
+  const int adt = p.A.dtype, bdt = p.B.dtype;
 
-  const int64_t zA = p.A.off + gdecomp(p.Z, zi, p.A.sz);
-  const int64_t zB = p.B.off + gdecomp(p.Z, zi, p.B.sz);
   if (tid < BM) {
     int64_t m = m0 + tid;
-    offA_row[tid] = m < p.m ? zA + gdecomp(p.M, m, p.A.s1) : 0;
+    bool ok = m < p.m;
+    rowA[tid] = ok ? p.A.off + gdecomp(p.Z, zi, p.A.sz) + gdecomp(p.M, m, p.A.s1) : 0;
+    rowC[tid] = ok ? p.C.off + gdecomp(p.Z, zi, p.C.sz) + gdecomp(p.M, m, p.C.s1) : -1;
   } else if (tid < BM + BN) {
-    int64_t n = n0 + (tid - BM);
-    offB_col[tid - BM] = n < p.n ? zB + gdecomp(p.N, n, p.B.s2) : 0;
+    int c = tid - BM;
+    int64_t n = n0 + c;
+    bool ok = n < p.n;
+    colB[c] = ok ? p.B.off + gdecomp(p.Z, zi, p.B.sz) + gdecomp(p.N, n, p.B.s2) : 0;
+    colC[c] = ok ? gdecomp(p.N, n, p.C.s2) : -1;
+    colBias[c] = (ok && p.bias.ptr) ? p.bias.off + gdecomp(p.Z, zi, p.bias.sz) +
+                                          gdecomp(p.N, n, p.bias.s2) : 0;
   }
   // K range of this split
   const int64_t kper = ((p.k + p.splits - 1) / p.splits + BK - 1) / BK * BK;
@@ -74,31 +85,32 @@ __global__ void __launch_bounds__(256) k_gemm(const __grid_constant__ rt_gemm_pa
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = (T)0;
 
-  // A tile mapping: k-fast when the A operand is contiguous along K
   const bool a_kfast = (p.K.nd > 0 && p.A.s2[p.K.nd - 1] == 1);
   const bool b_nfast = (p.N.nd > 0 && p.B.s2[p.N.nd - 1] == 1);
+  const bool m_in = m0 + BM <= p.m, n_in = n0 + BN <= p.n;
 
   for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
     __syncthreads();
     if (tid < BK) {
       int64_t k = k0 + tid;
-      offA_k[tid] = k < kend ? gdecomp(p.K, k, p.A.s2) : 0;
-    } else if (tid < 2 * BK) {
-      int64_t k = k0 + tid - BK;
-      offB_k[tid - BK] = k < kend ? gdecomp(p.K, k, p.B.s1) : 0;
+      kA[tid] = k < kend ? gdecomp(p.K, k, p.A.s2) : 0;
+    } else if (tid >= 32 && tid < 32 + BK) {
+      int64_t k = k0 + tid - 32;
+      kB[tid - 32] = k < kend ? gdecomp(p.K, k, p.B.s1) : 0;
     }
     __syncthreads();
+    const bool k_in = k0 + BK <= kend;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       int e = tid + 256 * i;
       int r, kk;
-      if (a_kfast) { r = e / BK; kk = e % BK; } else { kk = e / BM; r = e % BM; }
-      int64_t m = m0 + r, k = k0 + kk;
-      As[kk][r] = (m < p.m && k < kend) ? gload<T>(p.A, offA_row[r] + offA_k[kk]) : (T)0;
+      if (a_kfast) { r = e >> 4; kk = e & 15; } else { kk = e >> 6; r = e & 63; }
+      bool ok = (m_in || m0 + r < p.m) && (k_in || k0 + kk < kend);
+      As[kk][r] = ok ? gload_f<T>(Ap, adt, rowA[r] + kA[kk]) : (T)0;
       int c, kb;
-      if (b_nfast) { kb = e / BN; c = e % BN; } else { c = e / BK; kb = e % BK; }
-      int64_t n = n0 + c, k2 = k0 + kb;
-      Bs[kb][c] = (n < p.n && k2 < kend) ? gload<T>(p.B, offB_col[c] + offB_k[kb]) : (T)0;
+      if (b_nfast) { kb = e >> 6; c = e & 63; } else { c = e >> 4; kb = e & 15; }
+      bool okb = (n_in || n0 + c < p.n) && (k_in || k0 + kb < kend);
+      Bs[kb][c] = okb ? gload_f<T>(Bp, bdt, colB[c] + kB[kb]) : (T)0;
     }
     __syncthreads();
 #pragma unroll
@@ -116,15 +128,15 @@ __global__ void __launch_bounds__(256) k_gemm(const __grid_constant__ rt_gemm_pa
   }
 
   // epilogue
-  const int64_t zC = p.C.off + gdecomp(p.Z, zi, p.C.sz);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    int64_t m = m0 + ty * 4 + i;
+    int r = ty * 4 + i;
+    int64_t m = m0 + r;
     if (m >= p.m) continue;
-    int64_t rowC = zC + gdecomp(p.M, m, p.C.s1);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      int64_t n = n0 + tx * 4 + j;
+      int c = tx * 4 + j;
+      int64_t n = n0 + c;
       if (n >= p.n) continue;
       T v = acc[i][j];
       if (p.splits > 1) {
@@ -132,14 +144,11 @@ __global__ void __launch_bounds__(256) k_gemm(const __grid_constant__ rt_gemm_pa
         part[((split * p.z + zi) * p.m + m) * p.n + n] = v;
         continue;
       }
-      int64_t oc = rowC + gdecomp(p.N, n, p.C.s2);
+      int64_t oc = rowC[r] + colC[c];
       if (p.accumulate) v += gload<T>(p.C, oc);
-      if (p.bias.ptr) {
-        int64_t ob = p.bias.off + gdecomp(p.Z, zi, p.bias.sz) + gdecomp(p.M, m, p.bias.s1) +
-                     gdecomp(p.N, n, p.bias.s2);
-        v += gload<T>(p.bias, ob);
-      }
-      store_as<T>((void*)p.C.ptr, p.C.dtype, oc, epi<T>(p, v));
+      if (p.bias.ptr) v += gload<T>(p.bias, colBias[c]);
+      if (p.epilogue == 1) v = vm_tanh<T>(v);
+      store_as<T>((void*)p.C.ptr, p.C.dtype, oc, v);
     }
   }
 }

@@ -282,6 +282,26 @@ extern "C" int rt_graph_capture(const rt_instr* prog, int32_t nprog, const rt_la
   return RT_OK;
 }
 
+extern "C" int rt_graph_capture_ev(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs,
+                                   int32_t nrec, int64_t* env, int32_t nenv, uint64_t stream,
+                                   const uint64_t* events, int32_t nevents,
+                                   uint64_t* graph_exec_out) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaGraph_t graph = nullptr;
+  int rc = cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+  if (rc) return rc;
+  int rrc = rt_run(prog, nprog, recs, nrec, env, nenv, stream, events, nevents);
+  rc = cuda_check(cudaStreamEndCapture(s, &graph), "end capture");
+  if (rrc) { if (graph) cudaGraphDestroy(graph); return rrc; }
+  if (rc) return rc;
+  cudaGraphExec_t ex = nullptr;
+  rc = cuda_check(cudaGraphInstantiate(&ex, graph, 0), "graph instantiate");
+  cudaGraphDestroy(graph);
+  if (rc) return rc;
+  *graph_exec_out = (uint64_t)ex;
+  return RT_OK;
+}
+
 extern "C" int rt_graph_launch(uint64_t graph_exec, uint64_t stream) {
   return cuda_check(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream),
                     "graph launch");
@@ -289,4 +309,57 @@ extern "C" int rt_graph_launch(uint64_t graph_exec, uint64_t stream) {
 
 extern "C" int rt_graph_destroy(uint64_t graph_exec) {
   return cuda_check(cudaGraphExecDestroy((cudaGraphExec_t)graph_exec), "graph destroy");
+}
+
+// ------------------------------------------------------------ profiling
+// Run a program with a CUDA event pair around every launch instance and
+// accumulate the device time per launch record (ms) and the instance count.
+// Used by bench.py for the per-kernel breakdown and the live roofline.
+
+extern "C" int rt_profile(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs,
+                          int32_t nrec, int64_t* env, int32_t nenv, uint64_t stream,
+                          double* rec_ms, int64_t* rec_count) {
+  cudaStream_t s = (cudaStream_t)stream;
+  static std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, int>> inst;  // (record, event pair index)
+  size_t used = 0;
+  int pc = 0;
+  while (pc < nprog) {
+    const rt_instr& in = prog[pc];
+    if (in.op == RT_OP_LAUNCH) {
+      while (pool.size() < used + 2) {
+        cudaEvent_t e;
+        int rc = cuda_check(cudaEventCreate(&e), "event create");
+        if (rc) return rc;
+        pool.push_back(e);
+      }
+      cudaEventRecord(pool[used], s);
+      int rc = launch_one(&recs[in.a], env, nenv, s);
+      if (rc) return rc;
+      cudaEventRecord(pool[used + 1], s);
+      inst.push_back({in.a, (int)used});
+      used += 2;
+      ++pc;
+    } else if (in.op == RT_OP_FOR) {
+      bool empty = in.d > 0 ? (in.b >= in.c) : (in.b <= in.c);
+      if (empty) pc = in.e; else { env[in.a] = in.b; ++pc; }
+    } else if (in.op == RT_OP_END) {
+      const rt_instr& f = prog[in.a];
+      int64_t v = env[f.a] + f.d;
+      bool more = f.d > 0 ? (v < f.c) : (v > f.c);
+      if (more) { env[f.a] = v; pc = in.a + 1; } else ++pc;
+    } else {
+      ++pc;
+    }
+  }
+  int rc = cuda_check(cudaStreamSynchronize(s), "profile sync");
+  if (rc) return rc;
+  for (int r = 0; r < nrec; ++r) { rec_ms[r] = 0.0; rec_count[r] = 0; }
+  for (auto& x : inst) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pool[x.second], pool[x.second + 1]);
+    rec_ms[x.first] += ms;
+    rec_count[x.first] += 1;
+  }
+  return RT_OK;
 }

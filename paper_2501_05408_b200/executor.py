@@ -25,6 +25,7 @@ import weakref
 import numpy as np
 
 from . import ir
+from . import memplan
 from . import native as N
 from .ir import DTYPES, Graph, as_graph
 from .lower import Buf, Lowering, prod
@@ -255,12 +256,162 @@ def find_contractions(g: Graph):
     return res
 
 
+FUSE_PRODUCERS = {"add", "sub", "mul", "div", "neg", "exp", "log", "tanh", "sqrt",
+                  "pow_const", "cmp", "where", "cast", "merge", "eval_symbol"}
+FUSE_CONSUMERS = {"add", "sub", "mul", "div", "neg", "exp", "log", "tanh", "sqrt",
+                  "pow_const", "cmp", "where", "cast", "merge"}
+
+
+def _single_identity_consumer(g, nid, out_ids):
+    outs = g.out_edges(nid)
+    if len(outs) != 1 or nid in out_ids:
+        return None
+    e = outs[0]
+    src, snk = g.nodes[e.src], g.nodes[e.sink]
+    if not _is_identity(e, src, snk):
+        return None
+    return e
+
+
+def find_gemm_epilogues(g: Graph, pshape, fixed_of, skip):
+    """matmul -> (+ bias) [-> tanh] with single pointwise consumers: one GEMM
+    whose epilogue adds the bias and applies tanh (the MLP layers)."""
+    out_ids = {nid for _, nid, _ in g.outputs}
+    res = {}
+    for x in g.sorted_nodes():
+        if x.kind != "matmul" or x.id in skip:
+            continue
+        e = _single_identity_consumer(g, x.id, out_ids)
+        if e is None:
+            continue
+        y = g.nodes[e.sink]
+        if y.kind != "add" or pshape[(y.id, 0)] != pshape[(x.id, 0)] or y.dtype != x.dtype:
+            continue
+        if len(pshape[(x.id, 0)]) != 2:
+            continue
+        ins = g.in_edges(y.id)
+        be = ins[1 - e.iid]
+        bsrc = g.nodes[be.src]
+        bshape = pshape[(bsrc.id, be.oid)]
+        nn = pshape[(x.id, 0)][-1]
+        if be.psi is not None or any(c[0] == "slice" for c in be.phi):
+            continue
+        if bshape not in ((1, nn), (nn,)) or bsrc.out_dtypes[be.oid] != x.dtype:
+            continue
+        if not set(bsrc.domain) <= set(fixed_of.get(y.id, ())):
+            continue
+        final, tanh = y, False
+        e2 = _single_identity_consumer(g, y.id, out_ids)
+        if e2 is not None:
+            z = g.nodes[e2.sink]
+            if z.kind == "tanh" and fixed_of.get(z.id) == fixed_of.get(y.id):
+                final, tanh = z, True
+        if fixed_of.get(x.id) != fixed_of.get(final.id):
+            continue
+        res[final.id] = (x.id, be, tanh)
+    return res
+
+
+def find_ew_fusions(g: Graph, pshape, skip):
+    """Single-consumer pointwise producers inlined into their consumer's
+    program (one launch, no intermediate buffer)."""
+    out_ids = {nid for _, nid, _ in g.outputs}
+    fuse = {}
+    for p in g.sorted_nodes():
+        if p.kind not in FUSE_PRODUCERS or p.id in skip or len(p.out_shapes) != 1:
+            continue
+        e = _single_identity_consumer(g, p.id, out_ids)
+        if e is None:
+            continue
+        c = g.nodes[e.sink]
+        if c.kind not in FUSE_CONSUMERS or c.id in skip:
+            continue
+        if pshape[(p.id, 0)] != pshape[(c.id, 0)]:
+            continue
+        fuse[p.id] = c.id
+    # bound each fused tree: <= RT_MAXIN operand loads, <= 6 live registers
+    children = {}
+    for p, c in fuse.items():
+        children.setdefault(c, []).append(p)
+
+    def cost(n):
+        loads, need = 0, 0
+        ins = g.in_edges(n)
+        regs = []
+        for e in ins:
+            if fuse.get(e.src) == n:
+                l2, r2 = cost(e.src)
+                loads += l2
+                regs.append(r2)
+            else:
+                loads += 1
+                regs.append(1)
+        need = max([r + i for i, r in enumerate(regs)] or [1]) + 1
+        return loads, need
+
+    changed = True
+    while changed:
+        changed = False
+        roots = {c for c in fuse.values() if c not in fuse}
+        for r in sorted(roots):
+            loads, need = cost(r)
+            if loads > N.RT_MAXIN or need > 7:
+                # drop the largest child subtree of this root
+                kids = [p for p, c in fuse.items() if c == r]
+                if not kids:
+                    continue
+                kids.sort(key=lambda k: -cost(k)[0])
+                del fuse[kids[0]]
+                changed = True
+    return fuse
+
+
+def analyze(g: Graph, benv, pshape, fuse=True):
+    """Plan the loop nest and decide aliases, contractions and fusions
+    (device-independent; the CPU tests run this directly)."""
+    ext = {d: benv[g.dim_bound[d]] for d in g.dim_order}
+    contract = find_contractions(g)
+    virtual = set(contract.values())
+    alias = find_aliases(g, pshape)
+    plan = Planner(g, benv).plan()
+    fixed_of = plan_fixed(plan.steps)
+    alias_nodes = {k[0] for k in alias}
+    gemm_epi = find_gemm_epilogues(g, pshape, fixed_of, virtual | alias_nodes) if fuse else {}
+    taken = set(virtual) | alias_nodes | set(gemm_epi)
+    for f, (x, _b, t) in gemm_epi.items():
+        taken.add(x)
+        if t:
+            taken.add(g.in_edges(f)[0].src)
+    fuse_src = find_ew_fusions(g, pshape, taken) if fuse else {}
+    virtual |= set(fuse_src)
+    for f, (x, _b, t) in gemm_epi.items():
+        virtual.add(x)
+        if t:
+            virtual.add(g.in_edges(f)[0].src)
+    bufs = {}
+    for n in g.sorted_nodes():
+        for oid in range(len(n.out_shapes)):
+            key = (n.id, oid)
+            bufs[key] = Buf(key, n.domain, tuple(ext[d] for d in n.domain), pshape[key],
+                            n.out_dtypes[oid], alias.get(key))
+    return {"contract": contract, "alias": alias, "plan": plan, "gemm_epi": gemm_epi,
+            "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs}
+
+
+def payload_shapes(g: Graph, benv):
+    pshape = {}
+    for n in g.sorted_nodes():
+        for oid, shp in enumerate(n.out_shapes):
+            pshape[(n.id, oid)] = tuple(_eval_shape(shp, benv))
+    return pshape
+
+
 # ---------------------------------------------------------------------------
 # executable cache
 
 
 class Executable:
-    def __init__(self, g: Graph, benv: dict, seed: int, device: int, input_sig):
+    def __init__(self, g: Graph, benv: dict, seed: int, device: int, input_sig, fuse=True):
         torch = _torch()
         self.torch = torch
         self.g = g
@@ -272,53 +423,60 @@ class Executable:
         lib = N.lib()
         self.lib = lib
 
-        # payload shapes
-        pshape = {}
-        for n in g.sorted_nodes():
-            for oid, shp in enumerate(n.out_shapes):
-                pshape[(n.id, oid)] = tuple(_eval_shape(shp, benv))
+        pshape = payload_shapes(g, benv)
         self.pshape = pshape
         self._check_vec()
-        self.contract = find_contractions(g)
-        virtual = set(self.contract.values())
-        alias = find_aliases(g, pshape)
-        # buffers
-        self.bufs = {}
-        for n in g.sorted_nodes():
-            for oid in range(len(n.out_shapes)):
-                key = (n.id, oid)
-                self.bufs[key] = Buf(key, n.domain, tuple(self.ext[d] for d in n.domain),
-                                     pshape[key], n.out_dtypes[oid], alias.get(key))
+        an = analyze(g, benv, pshape, fuse)
+        self.contract, self.plan, self.gemm_epi, self.fuse_src = (
+            an["contract"], an["plan"], an["gemm_epi"], an["fuse_src"])
+        self.virtual = virtual = an["virtual"]
+        self.bufs = an["bufs"]
+        roots = [k for k, b in self.bufs.items() if b.alias is None and k[0] not in virtual]
+        out_keys = {(nid, oid) for _, nid, oid in g.outputs}
+        pinned = {k for k in roots if g.nodes[k[0]].kind in ("const", "input")}
+        for k in out_keys:
+            r = k
+            while self.bufs[r].alias is not None:
+                r = self.bufs[r].alias
+            pinned.add(r)
         self.tensors = []
-        self.peak_bytes = 0
         with torch.cuda.device(self.dev):
-            for key, b in self.bufs.items():
-                if b.alias is not None or key[0] in virtual:
-                    continue
-                n = g.nodes[key[0]]
-                if n.kind == "const":
-                    host = np.asarray(n.params["value"], DTYPES[b.dtype])
-                    host = np.broadcast_to(host, b.shape).copy() if host.shape != b.shape else host
-                    t = torch.from_numpy(np.ascontiguousarray(host).view(np.uint8).reshape(-1)
-                                         ).to(self.dev)
-                else:
-                    t = torch.empty(max(1, b.nbytes), dtype=torch.uint8, device=self.dev)
-                self.tensors.append(t)
-                self.peak_bytes += t.numel()
-                b.ptr = t.data_ptr()
-            for key, b in self.bufs.items():
-                if b.alias is not None:
-                    root = b
-                    while root.alias is not None:
-                        root = self.bufs[root.alias]
-                    b.ptr = root.ptr
             st = N.u64()
             N.check(lib.rt_status_alloc(C.byref(st)), "status")
             self.status = st.value
-        # plan + lower
-        self.plan = Planner(g, benv).plan()
+        # pass 1: lower with symbolic pointers to learn which launch touches what
+        fake = {k: (i + 1) << 44 for i, k in enumerate(roots)}
+        self._set_ptrs(fake)
+        low = Lowering(self.plan, self.bufs, self.status, seed, lambda nb: 0,
+                       self.contract, self.fuse_src, self.gemm_epi).lower()
+        key_of = {v: k for k, v in fake.items()}
+        rec_ptrs = []
+        for (_, p, *_r) in low.recs:
+            rec_ptrs.append({(q >> 44) << 44 for q in memplan.touched_ptrs(p) if q >> 44})
+        life = memplan.lifetimes(low.prog, rec_ptrs, key_of, pinned)
+        for k in roots:
+            life.setdefault(k, (-1, -1))   # never touched: still allocated, tiny lifetime
+        sizes = {k: max(1, self.bufs[k].nbytes) for k in roots}
+        offs, arena = memplan.assign(sizes, life)
+        self.arena_bytes = arena
+        self.naive_bytes = sum(sizes.values())
+        with torch.cuda.device(self.dev):
+            self.arena = torch.empty(max(1, arena), dtype=torch.uint8, device=self.dev)
+            base = self.arena.data_ptr()
+            self._set_ptrs({k: base + offs[k] for k in roots})
+            for k in roots:
+                n = g.nodes[k[0]]
+                if n.kind == "const":
+                    b = self.bufs[k]
+                    host = np.asarray(n.params["value"], DTYPES[b.dtype])
+                    host = np.broadcast_to(host, b.shape).copy() if host.shape != b.shape \
+                        else np.array(host, order="C")
+                    src = torch.from_numpy(host.reshape(-1).view(np.uint8))
+                    _u8view(torch, b.ptr, b.nbytes, self.dev).copy_(src)
+        self.peak_bytes = arena
+        # pass 2: real pointers
         low = Lowering(self.plan, self.bufs, self.status, seed, self._scratch,
-                       self.contract).lower()
+                       self.contract, self.fuse_src, self.gemm_epi).lower()
         self.nrec = len(low.recs)
         self._params = [p for (_, p, _, _, _, _) in low.recs]
         recs = (N.rt_launch_rec * max(1, len(low.recs)))()
@@ -344,6 +502,16 @@ class Executable:
         self.launch_count = self._count_launches(low.prog)
         self.graph_exec = None
         self.graph_failed = False
+
+    def _set_ptrs(self, ptrs):
+        for k, p in ptrs.items():
+            self.bufs[k].ptr = p
+        for k, b in self.bufs.items():
+            if b.alias is not None:
+                r = b
+                while r.alias is not None:
+                    r = self.bufs[r.alias]
+                b.ptr = r.ptr
 
     def _scratch(self, nbytes):
         t = self.torch.empty(max(1, nbytes), dtype=self.torch.uint8, device=self.dev)
@@ -399,12 +567,13 @@ class Executable:
             arr = np.asarray(v)
             if b.dshape:
                 arr = arr[tuple(slice(0, e) for e in b.dshape)]
-            arr = np.array(arr, dtype=DTYPES[b.dtype], order="C", copy=True)
+            arr = np.array(arr, dtype=DTYPES[b.dtype], order="C", copy=True).reshape(
+                np.shape(arr))
             if arr.shape != b.shape:
                 raise OracleError(f"{n.name} produced shape {arr.shape[len(b.dshape):]}, "
                                   f"declared {b.pshape}")
             dst = _u8view(torch, b.ptr, b.nbytes, self.dev)
-            src = torch.from_numpy(arr.view(np.uint8).reshape(-1))
+            src = torch.from_numpy(arr.reshape(-1).view(np.uint8))
             if b.nbytes >= (1 << 16):
                 src = src.pin_memory()
             dst.copy_(src, non_blocking=True)
@@ -447,6 +616,93 @@ class Executable:
             rc = self.lib.rt_run(self.prog, self.nprog, self.recs, self.nrec, self.env,
                                  N.RT_MAXENV, s.cuda_stream, ev_arr, nev)
             N.check(rc, "rt_run")
+
+    def profile(self, inputs, stream=None):
+        """One run with an event pair around every launch: per-record device
+        ms and launch counts, labelled (node id, name, kernel family)."""
+        torch = self.torch
+        with torch.cuda.device(self.dev):
+            s = stream or torch.cuda.current_stream(self.dev)
+            self.upload_inputs(inputs, s)
+            N.check(self.lib.rt_status_clear(self.status, s.cuda_stream), "status clear")
+            for i in range(N.RT_MAXENV):
+                self.env[i] = 0
+            ms = (N.f64 * max(1, self.nrec))()
+            cnt = (N.i64 * max(1, self.nrec))()
+            N.check(self.lib.rt_profile(self.prog, self.nprog, self.recs, self.nrec, self.env,
+                                        N.RT_MAXENV, s.cuda_stream, ms, cnt), "rt_profile")
+        out = []
+        for i in range(self.nrec):
+            out.append({"rec": i, "kernel": self.kernels[i], "label": self.labels[i],
+                        "ms": ms[i], "count": cnt[i], "params": self._params[i]})
+        return out
+
+    def capture_with_events(self, rec_index, stream=None):
+        """A second CUDA graph of the same program with an event pair around
+        every launch of record `rec_index` (for live per-kernel timing inside
+        the timed region).  Returns (graph_exec, events)."""
+        torch = self.torch
+        ins = []
+        pairs = 0
+        for i in range(self.nprog):
+            x = self.prog[i]
+            if x.op == N.RT_OP_LAUNCH and x.a == rec_index:
+                ins.append((N.RT_OP_EVENT, 2 * pairs, 0, 0, 0, 0))
+                ins.append((x.op, x.a, x.b, x.c, x.d, x.e))
+                ins.append((N.RT_OP_EVENT, 2 * pairs + 1, 0, 0, 0, 0))
+                pairs += 1
+            else:
+                ins.append((x.op, x.a, x.b, x.c, x.d, x.e))
+        # loops: launches inside loops reuse their event pair per iteration, so
+        # the events of a looped record time its last instance
+        remap, out = {}, []
+        for old_pc in range(self.nprog):
+            pass
+        # rebuild FOR/END jump targets
+        prog = (N.rt_instr * len(ins))()
+        old_to_new = []
+        j = 0
+        for i in range(self.nprog):
+            x = self.prog[i]
+            if x.op == N.RT_OP_LAUNCH and x.a == rec_index:
+                old_to_new.append(j + 1)
+                j += 3
+            else:
+                old_to_new.append(j)
+                j += 1
+        for k, t in enumerate(ins):
+            prog[k].op, prog[k].a, prog[k].b, prog[k].c, prog[k].d, prog[k].e = t
+        for i in range(self.nprog):
+            x = self.prog[i]
+            nj = old_to_new[i]
+            if x.op == N.RT_OP_FOR:
+                prog[nj].e = old_to_new[x.e] if x.e < self.nprog else len(ins)
+            elif x.op == N.RT_OP_END:
+                prog[nj].a = old_to_new[x.a]
+        events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * pairs)]
+        with torch.cuda.device(self.dev):
+            s = stream or torch.cuda.current_stream(self.dev)
+            cap = torch.cuda.Stream(self.dev)
+            cap.wait_stream(s)
+            for e in events:
+                e.record(cap)        # materialise the event handles
+            ev_arr = (N.u64 * max(1, len(events)))(*[e.cuda_event for e in events])
+            for i in range(N.RT_MAXENV):
+                self.env[i] = 0
+            out = N.u64()
+            N.check(self.lib.rt_graph_capture_ev(prog, len(ins), self.recs, self.nrec, self.env,
+                                                 N.RT_MAXENV, cap.cuda_stream, ev_arr,
+                                                 len(events), C.byref(out)), "capture")
+            s.wait_stream(cap)
+        return out.value, events
+
+    def launch_graph(self, graph_exec, inputs, stream=None):
+        torch = self.torch
+        with torch.cuda.device(self.dev):
+            s = stream or torch.cuda.current_stream(self.dev)
+            self.upload_inputs(inputs, s)
+            N.check(self.lib.rt_status_clear(self.status, s.cuda_stream), "status clear")
+            N.check(self.lib.rt_graph_launch(graph_exec, s.cuda_stream), "graph")
 
     def check_status(self, stream=None):
         torch = self.torch
@@ -513,6 +769,17 @@ class _CudaArray:
 def _wrap_ptr(torch, ptr, nbytes, dev):
     t = torch.as_tensor(_CudaArray(ptr, nbytes, dev), device=dev)
     return t[:nbytes]
+
+
+def plan_fixed(steps, out=None):
+    out = {} if out is None else out
+    from .planner import Bulk
+    for st in steps:
+        if isinstance(st, Bulk):
+            out[st.nid] = tuple(st.fixed)
+        else:
+            plan_fixed(st.body, out)
+    return out
 
 
 def _eval_shape(shape, benv):

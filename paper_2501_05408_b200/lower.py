@@ -241,7 +241,8 @@ class Ctx:
 
 
 class Lowering:
-    def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None):
+    def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None,
+                 fuse_src=None, gemm_epi=None):
         self.plan = plan
         self.g = plan.graph
         self.benv = plan.benv
@@ -257,6 +258,13 @@ class Lowering:
         self.alloc = alloc         # nbytes -> device pointer (scratch)
         self.contract = contract or {}   # sum nid -> virtual matmul nid
         self.virtual = set(self.contract.values())
+        self.fuse_src = dict(fuse_src or {})   # producer nid -> consumer nid (inlined)
+        self.gemm_epi = dict(gemm_epi or {})   # final nid -> (matmul nid, bias edge, tanh)
+        self.virtual |= set(self.fuse_src)
+        for f, (x, _b, t) in self.gemm_epi.items():
+            self.virtual.add(x)
+            if t:
+                self.virtual.add(self.g.in_edges(f)[0].src)
         self.launches_per_kernel = {}
 
     # -- buffers -------------------------------------------------------------
@@ -436,6 +444,9 @@ class Lowering:
         ctx = Ctx(self, n, s.fixed)
         if any(e == 0 for e in ctx.slab_ext):
             return
+        if n.id in self.gemm_epi:
+            x, bias_e, tanh = self.gemm_epi[n.id]
+            return self.k_matmul(ctx, self.g.nodes[x], bias_e, 1 if tanh else 0)
         fn = getattr(self, f"k_{n.kind}", None)
         if fn is None:
             if n.kind in EW_KINDS:
@@ -449,14 +460,30 @@ class Lowering:
         n = ctx.node
         key = (n.id, 0)
         out_p = list(self.bufs[key].pshape)
-        ins = self.g.in_edges(n.id)
-        evs = [self.edge_val(ctx, e) for e in ins]
         P = Prog()
         views = []
-        f64 = n.dtype == "f64" or any(ev.buf.dtype == "f64" for ev in evs)
-        npay = len(out_p)
-        slab_n = len(ctx.slab)
-        payload_coords = None
+        self._f64 = n.dtype == "f64"
+        r = self._value(ctx, n, P, views, out_p, 0)
+        P.emit("STORE", a=r)
+        self._emit_ew(ctx, key, P, views, self._f64, out_p, (n.id, n.name))
+
+    MAX_FUSE_DEPTH = 6
+
+    def _fusable_operand(self, ctx, n, e, out_p, depth):
+        p = self.fuse_src.get(e.src)
+        if p is None or p != n.id or depth >= self.MAX_FUSE_DEPTH:
+            return False
+        src = self.g.nodes[e.src]
+        return (e.psi is None and src.domain == n.domain
+                and e.phi == tuple(("sym", d, "loop") for d in src.domain)
+                and list(self.bufs[(src.id, e.oid)].pshape) == list(out_p))
+
+    def _value(self, ctx: Ctx, n, P: Prog, views: list, out_p, depth):
+        """Compile node n's value at the current box element into a value
+        register; single-consumer pointwise producers are inlined."""
+        ins = self.g.in_edges(n.id)
+        if n.dtype == "f64":
+            self._f64 = True
 
         def view_of(ev, pstrides, extra_off=0, extra_checks=()):
             if ev.progs:
@@ -464,119 +491,138 @@ class Lowering:
             views.append(self.make_view(ctx, ev, pstrides, extra_off, extra_checks))
             if len(views) > N.RT_MAXIN:
                 raise LowerError("too many operands")
+            if ev.buf.dtype == "f64":
+                self._f64 = True
             return len(views) - 1
 
-        def load(ev, pstrides, **kw):
-            vi = view_of(ev, pstrides, **kw)
+        def operand(i, mapping="bcast"):
+            e = ins[i]
+            if mapping == "bcast" and self._fusable_operand(ctx, n, e, out_p, depth):
+                src = self.g.nodes[e.src]
+                return self._value(Ctx(self, src, ctx.fixed), src, P, views, out_p, depth + 1)
+            ev = self.edge_val(ctx, e)
+            if mapping == "bcast":
+                pst = self.bcast(ev, out_p)
+            else:
+                pst = mapping(ev)
+            vi = view_of(ev, pst)
             r = P.vreg()
             P.emit("LOAD", d=r, imm=vi)
             return r
 
         k = n.kind
         if k in ("add", "sub", "mul", "div"):
-            a = load(evs[0], self.bcast(evs[0], out_p))
-            b = load(evs[1], self.bcast(evs[1], out_p))
+            a = operand(0)
+            b = operand(1)
             P.emit({"add": "VADD", "sub": "VSUB", "mul": "VMUL", "div": "VDIV"}[k], d=a, a=a, b=b)
-            P.emit("STORE", a=a)
-        elif k in ("neg", "exp", "log", "tanh", "sqrt"):
-            a = load(evs[0], self.bcast(evs[0], out_p))
+            P.vfree_(b)
+            return a
+        if k in ("neg", "exp", "log", "tanh", "sqrt"):
+            a = operand(0)
             P.emit("V" + k.upper(), d=a, a=a)
-            P.emit("STORE", a=a)
-        elif k == "pow_const":
-            a = load(evs[0], self.bcast(evs[0], out_p))
+            return a
+        if k == "pow_const":
+            a = operand(0)
             P.emit("VPOW", d=a, a=a, imm=P.k(n.params["exponent"]))
-            P.emit("STORE", a=a)
-        elif k == "cmp":
-            a = load(evs[0], self.bcast(evs[0], out_p))
-            b = load(evs[1], self.bcast(evs[1], out_p))
+            return a
+        if k == "cmp":
+            a = operand(0)
+            b = operand(1)
             op = {"eq": "VEQ", "ne": "VNE", "lt": "VLT", "le": "VLE", "gt": "VGT",
                   "ge": "VGE"}[n.params["op"]]
             P.emit(op, d=a, a=a, b=b)
-            P.emit("STORE", a=a)
-        elif k == "where":
-            c = load(evs[0], self.bcast(evs[0], out_p))
-            a = load(evs[1], self.bcast(evs[1], out_p))
-            b = load(evs[2], self.bcast(evs[2], out_p))
+            P.vfree_(b)
+            return a
+        if k == "where":
+            c = operand(0)
+            a = operand(1)
+            b = operand(2)
             P.emit("VWHERE", d=c, a=c, b=a, c=b)
-            P.emit("STORE", a=c)
-        elif k in ("cast", "identity", "detach", "expand", "set_symbol"):
-            a = load(evs[0], self.bcast(evs[0], out_p))
-            P.emit("STORE", a=a)
-        elif k == "reshape":
-            ev = evs[0]
-            if ev.nslices:
-                raise LowerError("reshape of a gathered slice")
-            pst = cstrides(out_p)
-            a = load(ev, pst)
-            P.emit("STORE", a=a)
-        elif k == "permute":
-            ev = evs[0]
+            P.vfree_(a)
+            P.vfree_(b)
+            return c
+        if k == "cast":
+            a = operand(0)
+            P.emit("VCAST", d=a, a=a, imm=N.DTYPE_CODE[n.params["dtype"]])
+            return a
+        if k in ("identity", "detach", "expand", "set_symbol"):
+            return operand(0)
+        if k == "reshape":
+            def rs(ev):
+                if ev.nslices and [a.stride for a in ev.axes] != cstrides([a.ext for a in ev.axes]):
+                    raise LowerError("reshape of a non-contiguous gathered slice")
+                return cstrides(out_p)
+            return operand(0, rs)
+        if k == "permute":
             order = n.params["order"]
-            pst = [ev.axes[o].stride for o in order]
-            a = load(ev, pst)
-            P.emit("STORE", a=a)
-        elif k == "squeeze":
-            ev = evs[0]
+            return operand(0, lambda ev: [ev.axes[o].stride for o in order])
+        if k == "squeeze":
             dd = n.params["dim"]
-            pst = [ax.stride for i, ax in enumerate(ev.axes) if i != dd]
-            a = load(ev, pst)
-            P.emit("STORE", a=a)
-        elif k == "unsqueeze":
-            ev = evs[0]
+            return operand(0, lambda ev: [ax.stride for i, ax in enumerate(ev.axes) if i != dd])
+        if k == "unsqueeze":
             dd = n.params["dim"]
-            pst = [ax.stride for ax in ev.axes]
-            pst.insert(dd, 0)
-            a = load(ev, pst)
-            P.emit("STORE", a=a)
-        elif k == "eval_symbol":
+
+            def us(ev):
+                pst = [ax.stride for ax in ev.axes]
+                pst.insert(dd, 0)
+                return pst
+            return operand(0, us)
+        if k == "eval_symbol":
             sym = n.params["symbol"]
-            dm = ctx.dimmap()
-            r = P.int_expr(("sym", sym.name, sym.kind), dm)
+            r = P.int_expr(("sym", sym.name, sym.kind), ctx.dimmap())
             v = P.vreg()
             P.emit("VITOF", d=v, a=r)
-            P.emit("STORE", a=v)
-        elif k == "merge":
+            P.ifree_(r)
+            return v
+        if k == "merge":
             dm = ctx.dimmap()
             conds = n.params["conds"]
+            res = P.vreg()
+            joins = []
             for bi, cond in enumerate(conds):
-                ev = evs[bi]
                 if cond == ir.TRUE:
-                    a = load(ev, self.bcast(ev, out_p))
-                    P.emit("STORE", a=a)
+                    a = operand(bi)
+                    P.emit("VMOV", d=res, a=a)
+                    P.vfree_(a)
                     break
                 r = P.int_expr(subst_bounds(cond, self.benv), dm)
                 j = P.emit("JZ", a=r)
                 P.ifree_(r)
-                a = load(ev, self.bcast(ev, out_p))
-                P.emit("STORE", a=a)
+                a = operand(bi)
+                P.emit("VMOV", d=res, a=a)
                 P.vfree_(a)
+                joins.append(P.emit("JMP"))
                 P.code[j] = P.pc()
             else:
                 # no branch holds: the reference raises (runtime.py:369-370);
-                # such points are never demanded by a valid program, store 0
-                z = P.vreg()
-                P.emit("VCONST", d=z, imm=P.k(0.0))
-                P.emit("STORE", a=z)
-        elif k == "scan":
+                # such points are never demanded by a valid program
+                P.emit("VCONST", d=res, imm=P.k(0.0))
+            for j in joins:
+                P.code[j] = P.pc()
+            return res
+        if k == "scan":
             # y = x + gamma*prev; prev absent (edge condition false) at the head
-            x = load(evs[0], self.bcast(evs[0], out_p))
-            psi = evs[1].psi
+            x = operand(0)
+            psi = self.edge_val(ctx, ins[1]).psi
+            j = None
             if psi is not None:
                 r = P.int_expr(psi, ctx.dimmap())
                 j = P.emit("JZ", a=r)
-            pv = load(evs[1], self.bcast(evs[1], out_p))
+                P.ifree_(r)
+            pv = operand(1)
             g = P.vreg()
             P.emit("VCONST", d=g, imm=P.k(n.params["gamma"]))
             P.emit("VMUL", d=g, a=g, b=pv)
-            P.emit("VADD", d=g, a=x, b=g)
-            P.emit("STORE", a=g)
-            if psi is not None:
+            P.emit("VADD", d=x, a=x, b=g)
+            P.vfree_(g)
+            P.vfree_(pv)
+            if j is not None:
                 P.code[j] = P.pc()
-            P.emit("STORE", a=x)
-        elif k == "index_select":
-            self._index_select(ctx, P, evs[0], out_p, view_of)
-        elif k == "slice_axis":
-            ev = evs[0]
+            return x
+        if k == "index_select":
+            return self._index_select(ctx, P, self.edge_val(ctx, ins[0]), out_p, view_of)
+        if k == "slice_axis":
+            ev = self.edge_val(ctx, ins[0])
             ax = n.params["axis"]
             bs = n.params["block"]
             jd = n.params["dim"].name
@@ -584,17 +630,15 @@ class Lowering:
             if ev.axes[ax].ext is None:
                 raise LowerError("slice_axis over a ragged axis")
             # source coordinate along ax = j*bs + k ; zero past the extent
-            co = {jd: bs, ax: 1}
-            extra = [(0, co, ev.axes[ax].ext)]
-            # j*bs*stride offset
+            extra = [(0, {jd: bs, ax: 1}, ev.axes[ax].ext)]
             ev2 = EdgeVal(buf=ev.buf, off=ev.off, coef=dict(ev.coef), checks=list(ev.checks),
                           axes=ev.axes, nslices=ev.nslices)
             ev2.coef[jd] = ev2.coef.get(jd, 0) + bs * ev.axes[ax].stride
-            a = load(ev2, pst, extra_checks=extra)
-            P.emit("STORE", a=a)
-        else:
-            raise LowerError(f"no elementwise lowering for {k}")
-        self._emit_ew(ctx, key, P, views, f64, out_p, (n.id, n.name))
+            vi = view_of(ev2, pst, extra_checks=extra)
+            r = P.vreg()
+            P.emit("LOAD", d=r, imm=vi)
+            return r
+        raise LowerError(f"no elementwise lowering for {k}")
 
     def _index_select(self, ctx, P, ev, out_p, view_of):
         n = ctx.node
@@ -629,8 +673,7 @@ class Lowering:
             P.emit("ICONST", d=one, imm=1)
             v = P.vreg()
             P.emit("LOADX", d=v, a=off, b=one, imm=vi)
-            P.emit("STORE", a=v)
-            return
+            return v
         else:
             dm = ctx.dimmap()
             vi = view_of(ev, rest)
@@ -654,7 +697,7 @@ class Lowering:
         P.emit("IMUL", d=off, a=off, b=row)
         v = P.vreg()
         P.emit("LOADX", d=v, a=off, b=ok, imm=vi)
-        P.emit("STORE", a=v)
+        return v
 
     def _range_ok(self, P, lo, hi, D):
         # 0 <= lo <= hi <= D
@@ -675,16 +718,19 @@ class Lowering:
         box = list(ctx.slab_ext) + list(out_p)
         if len(box) > N.RT_MAXD:
             raise LowerError("box rank too large")
+        allv = [self.out_view(ctx, key)] + list(views)
+        code = list(P.code)
+        box = collapse_box(box, allv, code)
         p.box.nd = len(box)
         for i, e in enumerate(box):
             p.box.ext[i] = e
         p.total = prod(box)
         p.nin = len(views)
         p.f64 = 1 if f64 else 0
-        p.out = self.out_view(ctx, key)
-        for i, v in enumerate(views):
+        p.out = allv[0]
+        for i, v in enumerate(allv[1:]):
             p.in_[i] = v
-        for i, w in enumerate(P.code):
+        for i, w in enumerate(code):
             p.code[i] = w
         for i, c in enumerate(P.konst):
             p.konst[i] = c
@@ -944,10 +990,14 @@ class Lowering:
 
     # ---- matmul
 
-    def k_matmul(self, ctx: Ctx):
+    def k_matmul(self, ctx: Ctx, X=None, bias_edge=None, epilogue=0):
+        """GEMM for matmul node X (default: ctx.node) written into ctx.node's
+        buffer, optionally with a fused `+ bias` and `tanh` epilogue."""
         n = ctx.node
-        ea, eb = self.g.in_edges(n.id)
-        A, B = self.edge_val(ctx, ea), self.edge_val(ctx, eb)
+        X = X or n
+        xctx = ctx if X is n else Ctx(self, X, ctx.fixed)
+        ea, eb = self.g.in_edges(X.id)
+        A, B = self.edge_val(xctx, ea), self.edge_val(xctx, eb)
         for ev in (A, B):
             if _ragged(ev) or ev.checks or ev.progs:
                 raise LowerError(f"{n.name}: matmul operand needs a gather")
@@ -971,8 +1021,20 @@ class Lowering:
         env_a = {self.slot[d]: s for d, s in A.coef.items() if d in ctx.fixed}
         env_b = {self.slot[d]: s for d, s in B.coef.items() if d in ctx.fixed}
         env_c = {self.slot[d]: cdst[d] for d in ctx.fixed if d in cdst}
+        bias = None
+        if bias_edge is not None:
+            bv = self.edge_val(ctx, bias_edge)
+            if any(d in ctx.slab for d in bv.coef) or bv.checks or bv.progs or _ragged(bv):
+                raise LowerError(f"{n.name}: bias varies across the GEMM rows")
+            bias = N.rt_gop()
+            bias.ptr = bv.buf.ptr
+            bias.dtype = N.DTYPE_CODE[bv.buf.dtype]
+            bias.off = bv.off
+            for d, sv in bv.coef.items():
+                bias.off_env[self.slot[d]] += sv
+            bias.s2[0] = bv.axes[-1].stride if bv.axes and bv.axes[-1].ext != 1 else 0
         self._gemm((A.buf, A.off, env_a), (B.buf, B.off, env_b), (st, 0, env_c),
-                   Z, M, Nn, K, (n.id, n.name))
+                   Z, M, Nn, K, (n.id, n.name), epilogue=epilogue, bias=bias)
 
     @staticmethod
     def _bstride(axes, i, nb):
@@ -1209,6 +1271,58 @@ class Lowering:
             p.out_kind[j] = N.DTYPE_CODE[n.out_dtypes[j]]
             p.out[j] = self.out_view(ctx, k)
         self.add_rec(N.RT_K_UDF, p, self.grid1(p.total, 128), [128, 1, 1], 0, (n.id, n.name))
+
+
+def _coords_used(code):
+    used = set()
+    for i in range(0, len(code), 2):
+        if code[i] & 0xFF == OPC["ICOORD"]:
+            used.add(code[i + 1])
+    return used
+
+
+def collapse_box(box, views, code):
+    """Merge adjacent box dims (d, d+1) that every view walks contiguously
+    (stride[d] == stride[d+1] * ext[d+1], same for range-check coefficients)
+    and no program reads as a coordinate.  Fewer dims = fewer divides per
+    element in the kernels' index decomposition."""
+    box = list(box)
+    d = len(box) - 2
+    while d >= 0:
+        used = _coords_used(code)
+        e1 = box[d + 1]
+        ok = d not in used and (d + 1) not in used
+        if ok:
+            for v in views:
+                if v.stride[d] != v.stride[d + 1] * e1:
+                    ok = False
+                    break
+                for c in range(v.nchk):
+                    if v.chk_a[c][d] != v.chk_a[c][d + 1] * e1:
+                        ok = False
+                        break
+                if not ok:
+                    break
+        if ok:
+            for v in views:
+                v.stride[d] = v.stride[d + 1]
+                for j in range(d + 1, len(box) - 1):
+                    v.stride[j] = v.stride[j + 1]
+                v.stride[len(box) - 1] = 0
+                for c in range(v.nchk):
+                    v.chk_a[c][d] = v.chk_a[c][d + 1]
+                    for j in range(d + 1, len(box) - 1):
+                        v.chk_a[c][j] = v.chk_a[c][j + 1]
+                    v.chk_a[c][len(box) - 1] = 0
+            for i in range(0, len(code), 2):
+                if code[i] & 0xFF == OPC["ICOORD"] and code[i + 1] > d + 1:
+                    code[i + 1] -= 1
+            box[d] = box[d] * e1
+            del box[d + 1]
+        d -= 1
+        if d > len(box) - 2:
+            d = len(box) - 2
+    return box
 
 
 def _ragged(ev):

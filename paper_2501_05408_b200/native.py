@@ -142,6 +142,11 @@ def lib():
     L.rt_graph_capture.argtypes = [C.POINTER(rt_instr), i32, C.POINTER(rt_launch_rec), i32,
                                    C.POINTER(i64), i32, u64, C.POINTER(u64)]
     L.rt_graph_launch.argtypes = [u64, u64]
+    L.rt_graph_capture_ev.argtypes = [C.POINTER(rt_instr), i32, C.POINTER(rt_launch_rec), i32,
+                                      C.POINTER(i64), i32, u64, C.POINTER(u64), i32,
+                                      C.POINTER(u64)]
+    L.rt_profile.argtypes = [C.POINTER(rt_instr), i32, C.POINTER(rt_launch_rec), i32,
+                             C.POINTER(i64), i32, u64, C.POINTER(f64), C.POINTER(i64)]
     L.rt_graph_destroy.argtypes = [u64]
     L.rt_status_alloc.argtypes = [C.POINTER(u64)]
     L.rt_status_read.argtypes = [u64, C.POINTER(i32), u64]
@@ -159,7 +164,7 @@ def lib():
 EXPORTS = ("rt_version", "rt_launch", "rt_run", "rt_status_alloc", "rt_status_read",
            "rt_status_clear", "rt_status_free", "rt_memcpy_d2h_async", "rt_memcpy_h2d_async",
            "rt_rng_fill", "rt_last_error", "rt_graph_capture", "rt_graph_launch",
-           "rt_graph_destroy")
+           "rt_graph_destroy", "rt_profile", "rt_graph_capture_ev")
 
 
 def check(rc: int, what: str = ""):

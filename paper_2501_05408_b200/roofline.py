@@ -1,0 +1,74 @@
+"""Algorithmic cost of one launch record (SURVEY §8(d) cost model):
+bytes that must cross HBM at least once, and flops.  Used by bench.py to
+turn measured kernel times into roofline fractions."""
+
+from __future__ import annotations
+
+from . import native as N
+
+ITEM = {N.RT_F64: 8, N.RT_F32: 4, N.RT_I64: 8, N.RT_BOOL: 1}
+FAMILY = {N.RT_K_EW: "ew", N.RT_K_REDUCE: "reduce", N.RT_K_SCAN: "scan", N.RT_K_GEMM: "gemm",
+          N.RT_K_RNG: "rng", N.RT_K_UDF: "udf", N.RT_K_SPLITK: "splitk",
+          N.RT_K_POLICY: "policy"}
+
+
+def _prod(xs):
+    out = 1
+    for x in xs:
+        out *= x
+    return out
+
+
+def _view_bytes(v, box):
+    """Distinct elements a view touches over the box (dims with stride 0 are
+    broadcast) times the item size."""
+    n = _prod(box[d] for d in range(len(box)) if v.stride[d] != 0)
+    return n * ITEM.get(v.dtype, 4)
+
+
+def _gop_elems(o, Z, M, N_, role):
+    zs = _prod(Z.ext[i] for i in range(Z.nd) if o.sz[i] != 0)
+    a = _prod(M.ext[i] for i in range(M.nd) if o.s1[i] != 0)
+    b = _prod(N_.ext[i] for i in range(N_.nd) if o.s2[i] != 0)
+    return zs * a * b
+
+
+def cost(kernel, p):
+    """(bytes, flops) for one launch of record params p."""
+    if kernel == N.RT_K_EW:
+        box = [p.box.ext[i] for i in range(p.box.nd)]
+        b = p.total * ITEM.get(p.out.dtype, 4)
+        for i in range(p.nin):
+            b += _view_bytes(p.in_[i], box)
+        return b, 0
+    if kernel == N.RT_K_REDUCE:
+        box = [p.box.ext[i] for i in range(p.box.nd)]
+        red = 1
+        for j in range(p.nred):
+            red *= max(1, p.len0[j]) if p.len_prog[j] < 0 and not any(
+                p.len_a[j][d] for d in range(p.box.nd)) else 1
+        b = p.total * ITEM.get(p.out.dtype, 4) + p.total * red * ITEM.get(p.in_.dtype, 4)
+        return b, p.total * red
+    if kernel == N.RT_K_SCAN:
+        box = [p.box.ext[i] for i in range(p.box.nd)]
+        tot = _prod(box)
+        return tot * (ITEM.get(p.in_.dtype, 4) + ITEM.get(p.out.dtype, 4)), 2 * tot
+    if kernel == N.RT_K_GEMM:
+        fl = 2 * p.z * p.m * p.n * p.k
+        ea = _gop_elems(p.A, p.Z, p.M, p.K, 0) * ITEM.get(p.A.dtype, 4)
+        eb = _gop_elems(p.B, p.Z, p.K, p.N, 1) * ITEM.get(p.B.dtype, 4)
+        ec = p.z * p.m * p.n * ITEM.get(p.C.dtype, 4)
+        return ea + eb + ec, fl
+    if kernel == N.RT_K_RNG:
+        return p.total * p.count * ITEM.get(p.out.dtype, 4), 0
+    if kernel == N.RT_K_UDF:
+        b = 0
+        for i in range(p.nin):
+            b += p.total * p.in_count[i] * ITEM.get(p.in_[i].dtype, 4)
+        for j in range(p.nout):
+            b += p.total * p.out_count[j] * ITEM.get(p.out[j].dtype, 4)
+        return b, 0
+    if kernel == N.RT_K_SPLITK:
+        it = 8 if p.f64 else 4
+        return p.z * p.m * p.n * it * (p.splits + 1), p.z * p.m * p.n * p.splits
+    return 0, 0

@@ -23,4 +23,4 @@ PARAMS = ("W1", "b1", "W2", "b2", "W3", "b3")
 
 def next_inputs(outs):
     """Feed a training step's updated weights into the next step."""
-    return {f"{k}_0": outs[f"{k}_next"] for k in PARAMS}
+    return {f"{k}_0": outs[f"{k}_next"][-1] for k in PARAMS}

@@ -48,28 +48,19 @@ def test_struct_layouts_match_header(tmp_path):
         assert C.sizeof(getattr(N, n)) == s, n
 
 
-def dry_lower(g, benv, seed=0):
+def dry_lower(g, benv, seed=0, fuse=True):
     h = X.copy_graph(g)
     X.inline_dataflow(h, benv)
     X.eliminate_dead(h)
-    ext = {d: benv[h.dim_bound[d]] for d in h.dim_order}
-    pshape = {}
-    for n in h.sorted_nodes():
-        for oid, shp in enumerate(n.out_shapes):
-            pshape[(n.id, oid)] = tuple(X._eval_shape(shp, benv))
-    contract = X.find_contractions(h)
-    alias = X.find_aliases(h, pshape)
-    bufs, ptr = {}, 1 << 20
-    for n in h.sorted_nodes():
-        for oid in range(len(n.out_shapes)):
-            k = (n.id, oid)
-            bufs[k] = L.Buf(k, n.domain, tuple(ext[d] for d in n.domain), pshape[k],
-                            n.out_dtypes[oid], alias.get(k))
-            bufs[k].ptr = ptr
-            ptr += bufs[k].nbytes + 256
-    plan = P.Planner(h, benv).plan()
-    low = L.Lowering(plan, bufs, 0, seed, lambda nb: 1 << 40, contract).lower()
-    return plan, low, contract, alias
+    pshape = X.payload_shapes(h, benv)
+    an = X.analyze(h, benv, pshape, fuse)
+    bufs, ptr = an["bufs"], 1 << 20
+    for k, b in bufs.items():
+        b.ptr = ptr
+        ptr += b.nbytes + 256
+    low = L.Lowering(an["plan"], bufs, 0, seed, lambda nb: 1 << 40, an["contract"],
+                     an["fuse_src"], an["gemm_epi"]).lower()
+    return an["plan"], low, an["contract"], an["alias"]
 
 
 CASES = [c for c in all_cases() if not c.error]
@@ -81,8 +72,9 @@ def test_golden_graph_plans_and_lowers(case):
     benv = {g.dim_bound[d]: (case.resolved_bounds or {}).get(g.dim_bound[d],
                                                                g.bindings.get(g.dim_bound[d]))
             for d in g.dim_order}
-    plan, low, _, _ = dry_lower(g, benv)
-    assert low.recs or not g.outputs
+    for fuse in (True, False):
+        plan, low, _, _ = dry_lower(g, benv, fuse=fuse)
+        assert low.recs or not g.outputs
 
 
 def test_c2_plan_batches_envs_and_fuses_dw():
