@@ -179,7 +179,15 @@ extern "C" int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* 
       }
       case RT_OP_EVENT: {
         if (in.a < 0 || in.a >= nevents) return fail(RT_ERR_BAD_ARG, "event slot out of range");
-        int rc = cuda_check(cudaEventRecord((cudaEvent_t)events[in.a], s), "cudaEventRecord");
+        // inside stream capture, an external record node really records the
+        // event on every graph launch (a plain capture only orders nodes)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        int rc = cs == cudaStreamCaptureStatusActive
+                     ? cuda_check(cudaEventRecordWithFlags((cudaEvent_t)events[in.a], s,
+                                                           cudaEventRecordExternal),
+                                  "cudaEventRecord(external)")
+                     : cuda_check(cudaEventRecord((cudaEvent_t)events[in.a], s), "cudaEventRecord");
         if (rc) return rc;
         ++pc;
         break;

@@ -653,11 +653,6 @@ class Executable:
                 pairs += 1
             else:
                 ins.append((x.op, x.a, x.b, x.c, x.d, x.e))
-        # loops: launches inside loops reuse their event pair per iteration, so
-        # the events of a looped record time its last instance
-        remap, out = {}, []
-        for old_pc in range(self.nprog):
-            pass
         # rebuild FOR/END jump targets
         prog = (N.rt_instr * len(ins))()
         old_to_new = []
