@@ -213,10 +213,10 @@ def main():
 
     # roofline of the dominant kernel (live, inside the timed region)
     hbm, tfl, src = peaks()
-    bytes_, flops = RF.cost(dom["kernel"], dom["params"])
+    bytes_, flops = RF.cost(dom["kernel"], dom["params"], exe.loop_info.get(dom["rec"]))
     n_inst = max(1, len(kev) // 2)
     kms = sum(dom_ms) / len(dom_ms) / n_inst   # per launch
-    if flops and RF.FAMILY[dom["kernel"]] == "gemm":
+    if flops and RF.FAMILY[dom["kernel"]] in ("gemm", "loop"):
         ach = flops / (kms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": tfl, "unit": "TFLOP/s",
                 "frac": ach / tfl, "traffic": None}
@@ -230,7 +230,7 @@ def main():
                  "peak_source": src})
     top = []
     for r in rows[:8]:
-        b_, f_ = RF.cost(r["kernel"], r["params"])
+        b_, f_ = RF.cost(r["kernel"], r["params"], exe.loop_info.get(r["rec"]))
         per = r["ms"] / max(1, r["count"])
         top.append({"kernel": RF.FAMILY.get(r["kernel"]), "node": r["label"][1],
                     "ms_step": round(r["ms"], 3), "launches": r["count"],

@@ -49,7 +49,8 @@ enum rt_kernel {
   RT_K_RNG = 5,      /* SeedSequence->PCG64->{normal,uniform} per point       */
   RT_K_UDF = 6,      /* synthetic environment (dsl.py:288-307) per point      */
   RT_K_SPLITK = 7,   /* split-K partial reduction for RT_K_GEMM               */
-  RT_K_POLICY = 8    /* fused acting step: MLP policy + sample + env          */
+  RT_K_POLICY = 8,   /* reserved                                              */
+  RT_K_LOOP = 9      /* persistent kernel running a whole row-local loop      */
 };
 
 enum rt_status_code {
@@ -235,6 +236,34 @@ typedef struct {
   rt_view in[4];         /* strides over box; payload contiguous after */
   rt_view out[4];
 } rt_udf_params;
+
+/* RT_K_LOOP: one persistent launch for a whole loop whose body is row-local
+ * (every dependence inside the body keeps the slab coordinates, e.g. the
+ * acting recurrence over t with all envs b independent).  Each CTA owns a
+ * block of rows and runs every body op on them, step after step, with
+ * __syncthreads between ops; no grid-wide synchronisation is needed.
+ * Sub-op descriptors live in HBM unfolded; env terms are folded per step. */
+typedef struct {
+  int32_t kernel;       /* RT_K_EW | RT_K_GEMM | RT_K_UDF | RT_K_RNG */
+  int32_t f64;
+  uint64_t params;      /* device pointer to the op's parameter block */
+  int64_t row_elems;    /* flat box elements per row (EW/RNG/UDF: per point) */
+  uint64_t noise;       /* UDF: pre-drawn normals [rows, ..., count] (0: draw in loop) */
+  int64_t noise_off;    /* UDF: element offset of (row 0, loop index 0) in `noise` */
+  int64_t noise_row;    /* UDF: elements between consecutive rows in `noise` */
+  int64_t noise_step;   /* UDF: elements between consecutive loop indices */
+} rt_loop_op;
+
+typedef struct {
+  rt_hdr h;
+  int32_t slot;         /* env slot of the loop dim */
+  int32_t nops;
+  int64_t start, stop, step;
+  int64_t rows;         /* slab points shared by every op */
+  int32_t rows_per_cta;
+  int32_t smem_bytes;
+  uint64_t ops;         /* device pointer to rt_loop_op[nops] */
+} rt_loop_params;
 
 /* Launch record: one kernel family + its parameter block. */
 typedef struct {

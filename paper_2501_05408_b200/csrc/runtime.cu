@@ -17,6 +17,7 @@ extern "C" void* rt_kernel_rng();
 extern "C" void* rt_kernel_udf();
 extern "C" void* rt_kernel_rng_fill();
 extern "C" void* rt_kernel_policy(const void* params);
+extern "C" void* rt_kernel_loop();
 
 static thread_local std::string g_err;
 
@@ -108,6 +109,8 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
     }
     case RT_K_POLICY:
       return rt_kernel_policy(blk);
+    case RT_K_LOOP:
+      return rt_kernel_loop();
     default:
       return nullptr;
   }

@@ -451,8 +451,11 @@ class Executable:
                        self.contract, self.fuse_src, self.gemm_epi).lower()
         key_of = {v: k for k, v in fake.items()}
         rec_ptrs = []
-        for (_, p, *_r) in low.recs:
-            rec_ptrs.append({(q >> 44) << 44 for q in memplan.touched_ptrs(p) if q >> 44})
+        for ri, (_, p, *_r) in enumerate(low.recs):
+            ptrs = memplan.touched_ptrs(p)
+            for op in low.loop_subs.get(ri, {}).get("ops", ()):
+                ptrs |= memplan.touched_ptrs(op[1])
+            rec_ptrs.append({(q >> 44) << 44 for q in ptrs if q >> 44})
         life = memplan.lifetimes(low.prog, rec_ptrs, key_of, pinned)
         for k in roots:
             life.setdefault(k, (-1, -1))   # never touched: still allocated, tiny lifetime
@@ -477,6 +480,7 @@ class Executable:
         # pass 2: real pointers
         low = Lowering(self.plan, self.bufs, self.status, seed, self._scratch,
                        self.contract, self.fuse_src, self.gemm_epi).lower()
+        self._upload_loops(low)
         self.nrec = len(low.recs)
         self._params = [p for (_, p, _, _, _, _) in low.recs]
         recs = (N.rt_launch_rec * max(1, len(low.recs)))()
@@ -502,6 +506,39 @@ class Executable:
         self.launch_count = self._count_launches(low.prog)
         self.graph_exec = None
         self.graph_failed = False
+
+    def _upload_loops(self, low):
+        """Persistent-loop sub-op descriptors live in HBM: one blob per loop
+        record = [param blocks..., rt_loop_op array]."""
+        torch = self.torch
+        self.loop_info = {}
+        for ri, info in low.loop_subs.items():
+            ops = info["ops"]
+            blobs, offs, cur = [], [], 0
+            for kernel, p, re, f64, noise in ops:
+                b = C.string_at(C.addressof(p), C.sizeof(p))
+                offs.append(cur)
+                blobs.append(b + b"\0" * ((-len(b)) % 256))
+                cur += len(blobs[-1])
+            arr = (N.rt_loop_op * len(ops))()
+            total = cur + C.sizeof(arr)
+            dev = torch.empty(total, dtype=torch.uint8, device=self.dev)
+            self.tensors.append(dev)
+            base = dev.data_ptr()
+            for i, (kernel, p, re, f64, noise) in enumerate(ops):
+                a = arr[i]
+                a.kernel = kernel
+                a.f64 = int(f64)
+                a.params = base + offs[i]
+                a.row_elems = re
+                if noise:
+                    a.noise, a.noise_off, a.noise_row, a.noise_step = noise
+            host = b"".join(blobs) + C.string_at(C.addressof(arr), C.sizeof(arr))
+            dev.copy_(torch.frombuffer(bytearray(host), dtype=torch.uint8))
+            lp = low.recs[ri][1]
+            lp.ops = base + cur
+            self.loop_info[ri] = info
+        torch.cuda.synchronize(self.dev)
 
     def _set_ptrs(self, ptrs):
         for k, p in ptrs.items():

@@ -242,7 +242,7 @@ class Ctx:
 
 class Lowering:
     def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None,
-                 fuse_src=None, gemm_epi=None):
+                 fuse_src=None, gemm_epi=None, persistent=True):
         self.plan = plan
         self.g = plan.graph
         self.benv = plan.benv
@@ -258,6 +258,9 @@ class Lowering:
         self.alloc = alloc         # nbytes -> device pointer (scratch)
         self.contract = contract or {}   # sum nid -> virtual matmul nid
         self.virtual = set(self.contract.values())
+        self.persistent = persistent
+        self._capture = None
+        self.loop_subs = {}                    # loop record -> sub-op descriptors
         self.fuse_src = dict(fuse_src or {})   # producer nid -> consumer nid (inlined)
         self.gemm_epi = dict(gemm_epi or {})   # final nid -> (matmul nid, bias edge, tanh)
         self.virtual |= set(self.fuse_src)
@@ -400,6 +403,9 @@ class Lowering:
     def add_rec(self, kernel, params, grid, block, smem=0, label=""):
         params.h.node = int(label[0]) if isinstance(label, tuple) else 0
         params.h.status = self.status
+        if self._capture is not None:
+            self._capture.append((kernel, params, grid, block, smem, label))
+            return -1
         self.recs.append((kernel, params, grid, block, smem, label))
         self.prog.append((N.RT_OP_LAUNCH, len(self.recs) - 1, 0, 0, 0, 0))
         return len(self.recs) - 1
@@ -421,7 +427,133 @@ class Lowering:
             else:
                 self.loop(s)
 
+    # -- persistent loops ------------------------------------------------------
+
+    def _persistent_ok(self, s: Loop):
+        """Body = bulk steps over one common slab S whose internal dependences
+        keep the S coordinates (row-local), so CTAs can own rows."""
+        if not self.persistent or any(not isinstance(b, Bulk) for b in s.body):
+            return None
+        fixed = tuple(s.fixed) + (s.dim,)
+        body = {b.nid for b in s.body}
+        slabs = set()
+        for b in s.body:
+            n = self.g.nodes[b.nid]
+            if n.kind in ("const", "input") or self.bufs[(n.id, 0)].alias is not None:
+                continue
+            slabs.add(tuple(d for d in n.domain if d not in fixed))
+        if len(slabs) != 1:
+            return None
+        S = slabs.pop()
+        if not S:
+            return None
+        for nid in body:
+            for e in self.g.in_edges(nid):
+                if e.src not in body:
+                    continue
+                src = self.g.nodes[e.src]
+                for d in S:
+                    if d in src.domain and e.phi[src.domain.index(d)] != ("sym", d, "loop"):
+                        return None
+        return S
+
+    def _loop_persistent(self, s: Loop, S):
+        self._capture = []
+        try:
+            self.steps(s.body)
+        finally:
+            subs, self._capture = self._capture, None
+        Sext = [self.ext[d] for d in S]
+        rows = prod(Sext)
+        T = self.ext[s.dim]
+        ops = []
+        max_m = 1
+        for (kernel, p, grid, block, smem, label) in subs:
+            if kernel == N.RT_K_EW:
+                if p.total % rows:
+                    raise LowerError("ew box is not row-major over the slab")
+                ops.append([kernel, p, p.total // rows, p.f64, None])
+            elif kernel == N.RT_K_GEMM:
+                if p.z != 1 or p.splits != 1 or p.M.nd != len(S) + 1 or p.k > 4096 or \
+                        [p.M.ext[i] for i in range(len(S))] != Sext:
+                    raise LowerError("gemm is not row-blocked over the slab")
+                m = p.M.ext[len(S)]
+                max_m = max(max_m, m)
+                ops.append([kernel, p, m, p.f64, None])
+            elif kernel in (N.RT_K_UDF, N.RT_K_RNG):
+                if p.box.nd != len(S) or [p.box.ext[i] for i in range(len(S))] != Sext:
+                    raise LowerError("per-point op box differs from the slab")
+                ops.append([kernel, p, 1, 0, None])
+            else:
+                raise LowerError("op family not supported inside a persistent loop")
+        R = max(1, -(-rows // 148))
+        R = max(1, min(R, 16 // max_m))
+        smem = 0
+        for kernel, p, re, f64, _ in ops:
+            if kernel == N.RT_K_GEMM:
+                it = 8 if f64 else 4
+                need = ((R * re * p.k * it + 15) // 16) * 16 + p.k * 8
+                smem = max(smem, need)
+        if smem > 200 * 1024:
+            raise LowerError("persistent loop needs too much shared memory")
+        # hoist the env's data-independent normals out of the loop
+        for op in ops:
+            if op[0] != N.RT_K_UDF:
+                continue
+            up = op[1]
+            count = sum(up.out_count[j] for j in range(up.nout))
+            buf = self.alloc(rows * T * count * 8)
+            q = N.rt_rng_params()
+            box = Sext + [T]
+            q.box.nd = len(box)
+            for i, x in enumerate(box):
+                q.box.ext[i] = x
+            q.total = prod(box)
+            q.nprefix = up.nprefix
+            for i in range(up.nprefix):
+                q.prefix[i] = up.prefix[i]
+            udf = self.g.nodes[[lab for (k2, p2, *_r, lab) in subs if p2 is up][0][0]]
+            q.ncoord = len(udf.domain)
+            for j, d in enumerate(udf.domain):
+                if d == s.dim:
+                    q.coord_src[j] = len(S)
+                elif d in S:
+                    q.coord_src[j] = S.index(d)
+                else:
+                    q.coord_src[j] = -1 - self.slot[d]
+            q.dist = 0
+            q.count = count
+            q.out.ptr = buf
+            q.out.dtype = N.RT_F64
+            st = cstrides(Sext + [T, count])
+            for i in range(len(S) + 1):
+                q.out.stride[i] = st[i]
+            self.add_rec(N.RT_K_RNG, q, self.grid1(q.total, 128), [128, 1, 1], 0,
+                         (udf.id, udf.name + ":noise"))
+            op[4] = (buf, 0, T * count, count)
+        lp = N.rt_loop_params()
+        lp.slot = self.slot[s.dim]
+        lp.nops = len(ops)
+        n = T
+        lp.start, lp.stop, lp.step = (0, n, 1) if s.step > 0 else (n - 1, -1, -1)
+        lp.rows = rows
+        lp.rows_per_cta = R
+        lp.smem_bytes = smem
+        first = self.g.nodes[s.body[0].nid]
+        idx = self.add_rec(N.RT_K_LOOP, lp, [-(-rows // R), 1, 1], [256, 1, 1], smem,
+                           (first.id, f"loop[{s.dim}]"))
+        self.loop_subs[idx] = {"ops": ops, "trips": T}
+
     def loop(self, s: Loop):
+        S = self._persistent_ok(s)
+        if S:
+            mark = (len(self.recs), len(self.prog))
+            try:
+                return self._loop_persistent(s, S)
+            except LowerError:
+                del self.recs[mark[0]:]
+                del self.prog[mark[1]:]
+                self._capture = None
         n = self.ext[s.dim]
         if s.step > 0:
             start, stop = 0, n

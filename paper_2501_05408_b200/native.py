@@ -25,6 +25,7 @@ DTYPE_CODE = {"f64": RT_F64, "f32": RT_F32, "i64": RT_I64, "bool": RT_BOOL}
 
 RT_K_EW, RT_K_REDUCE, RT_K_SCAN, RT_K_GEMM, RT_K_RNG, RT_K_UDF, RT_K_SPLITK, RT_K_POLICY = \
     1, 2, 3, 4, 5, 6, 7, 8
+RT_K_LOOP = 9
 
 RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT = 1, 2, 3, 4
 
@@ -105,6 +106,17 @@ class rt_udf_params(C.Structure):
                 ("salt", f64), ("nin", i32), ("nout", i32), ("in_count", i32 * 4),
                 ("out_count", i32 * 4), ("out_kind", i32 * 4), ("in_", rt_view * 4),
                 ("out", rt_view * 4)]
+
+
+class rt_loop_op(C.Structure):
+    _fields_ = [("kernel", i32), ("f64", i32), ("params", u64), ("row_elems", i64),
+                ("noise", u64), ("noise_off", i64), ("noise_row", i64), ("noise_step", i64)]
+
+
+class rt_loop_params(C.Structure):
+    _fields_ = [("h", rt_hdr), ("slot", i32), ("nops", i32), ("start", i64), ("stop", i64),
+                ("step", i64), ("rows", i64), ("rows_per_cta", i32), ("smem_bytes", i32),
+                ("ops", u64)]
 
 
 class rt_launch_rec(C.Structure):

@@ -9,7 +9,7 @@ from . import native as N
 ITEM = {N.RT_F64: 8, N.RT_F32: 4, N.RT_I64: 8, N.RT_BOOL: 1}
 FAMILY = {N.RT_K_EW: "ew", N.RT_K_REDUCE: "reduce", N.RT_K_SCAN: "scan", N.RT_K_GEMM: "gemm",
           N.RT_K_RNG: "rng", N.RT_K_UDF: "udf", N.RT_K_SPLITK: "splitk",
-          N.RT_K_POLICY: "policy"}
+          N.RT_K_POLICY: "policy", N.RT_K_LOOP: "loop"}
 
 
 def _prod(xs):
@@ -33,8 +33,18 @@ def _gop_elems(o, Z, M, N_, role):
     return zs * a * b
 
 
-def cost(kernel, p):
+def cost(kernel, p, loop_info=None):
     """(bytes, flops) for one launch of record params p."""
+    if kernel == N.RT_K_LOOP:
+        if not loop_info:
+            return 0, 0
+        b = f = 0
+        rows = p.rows
+        for k, q, re, f64, noise in loop_info["ops"]:
+            b2, f2 = cost(k, q)
+            b += b2
+            f += f2
+        return b * loop_info["trips"], f * loop_info["trips"]
     if kernel == N.RT_K_EW:
         box = [p.box.ext[i] for i in range(p.box.nd)]
         b = p.total * ITEM.get(p.out.dtype, 4)
