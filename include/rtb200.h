@@ -261,7 +261,9 @@ typedef struct {
   int64_t start, stop, step;
   int64_t rows;         /* slab points shared by every op */
   int32_t rows_per_cta;
-  int32_t smem_bytes;
+  int32_t smem_bytes;   /* dynamic shared memory: [A rows | TMA ring] */
+  int32_t ring_off;     /* byte offset of the weight-panel ring */
+  int32_t _pad;
   uint64_t ops;         /* device pointer to rt_loop_op[nops] */
 } rt_loop_params;
 

@@ -37,6 +37,48 @@ RT_DEV int64_t gdec32(const rt_gbox& b, int64_t flat, const int64_t* s) {
   return o;
 }
 
+
+// ---------------------------------------------------------------- TMA bulk
+// 1-D bulk async copies global -> shared with mbarrier completion (sm_90+;
+// UBLKCP in SASS), used to stream dense weight panels through a smem ring.
+
+RT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+RT_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+RT_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+
+RT_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+RT_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+  }
+}
+
+#define RING 4
+
+struct loop_ring {
+  uint64_t* bar;       // [RING] mbarriers
+  unsigned char* buf;  // [RING][stage_bytes]
+  uint32_t stage_bytes;
+  uint32_t seq;        // chunks consumed so far (uniform across the CTA)
+};
+
 // ---------------------------------------------------------------- EW rows
 
 template <typename T>
@@ -61,6 +103,89 @@ RT_DEV void ew_rows(const rt_ew_params& p, const int64_t* env, int64_t f0, int64
 // C[r, n] = sum_k A[r, k] B[k, n] for the CTA's rows r in [m0, m1) of M
 // (M = slab rows x m), all n.  A rows are staged in shared memory; B is
 // streamed from L2 with each thread owning columns and all rows (B reuse).
+
+template <typename T>
+RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m0, int64_t m1,
+                          unsigned char* smem, loop_ring& ring) {
+  // dense row-major weights B[K][N] of type T: stream K-panels with TMA bulk copies
+  const int64_t K = p.k, Nn = p.n;
+  if (p.B.dtype != (sizeof(T) == 8 ? RT_F64 : RT_F32) || p.N.nd != 1 || p.K.nd != 1 ||
+      p.B.s2[0] != 1 || p.B.s1[0] != Nn || p.Z.nd > 1)
+    return false;
+  const int64_t kc = ring.stage_bytes / (Nn * (int64_t)sizeof(T));
+  if (kc < 1 || Nn < 64 || Nn > 4 * (int64_t)blockDim.x) return false;
+  const int mr = (int)(m1 - m0);
+  T* As = (T*)smem;
+  const int64_t aoff = fold_gop_off(p.A, env);
+  const int64_t boff = fold_gop_off(p.B, env);
+  const int64_t coff = fold_gop_off(p.C, env);
+  const int64_t biasoff = p.bias.ptr ? fold_gop_off(p.bias, env) : 0;
+  const T* Bg = (const T*)p.B.ptr + boff;
+  if ((((uintptr_t)Bg) & 15) != 0 || ((Nn * (int64_t)sizeof(T)) & 15) != 0) return false;
+  const int64_t nch = (K + kc - 1) / kc;
+  auto issue = [&](int64_t c) {
+    uint32_t st = (ring.seq + (uint32_t)c) % RING;
+    int64_t k0 = c * kc;
+    int64_t rows = min(kc, K - k0);
+    uint32_t bytes = (uint32_t)(rows * Nn * sizeof(T));
+    mbar_expect_tx(&ring.bar[st], bytes);
+    bulk_g2s(ring.buf + (size_t)st * ring.stage_bytes, Bg + k0 * Nn, bytes, &ring.bar[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t c = 0; c < (nch < RING ? nch : (int64_t)RING); ++c) issue(c);
+  // stage A rows meanwhile
+  for (int64_t i = threadIdx.x; i < (int64_t)mr * K; i += blockDim.x) {
+    int r = (int)(i / K);
+    int64_t k = i - (int64_t)r * K;
+    As[i] = load_as<T>((const void*)p.A.ptr, p.A.dtype,
+                       aoff + gdec32(p.M, m0 + r, p.A.s1) + gdec32(p.K, k, p.A.s2));
+  }
+  __syncthreads();
+  constexpr int NC = 4;   // columns per thread (Nn <= 4 * blockDim)
+  T acc[NC][LOOP_MAXR];
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+#pragma unroll
+    for (int r = 0; r < LOOP_MAXR; ++r) acc[j][r] = (T)0;
+  for (int64_t c = 0; c < nch; ++c) {
+    uint32_t g = ring.seq + (uint32_t)c;
+    uint32_t st = g % RING;
+    mbar_wait(&ring.bar[st], (g / RING) & 1);
+    const T* Bs = (const T*)(ring.buf + (size_t)st * ring.stage_bytes);
+    const int64_t k0 = c * kc;
+    const int64_t rows = min(kc, K - k0);
+    for (int64_t kk = 0; kk < rows; ++kk) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        int64_t n = threadIdx.x + j * (int64_t)blockDim.x;
+        if (n >= Nn) break;
+        T b = Bs[kk * Nn + n];
+#pragma unroll
+        for (int r = 0; r < LOOP_MAXR; ++r)
+          if (r < mr) acc[j][r] = fma(As[r * K + k0 + kk], b, acc[j][r]);
+      }
+    }
+    __syncthreads();   // everyone is done with stage st
+    if (threadIdx.x == 0 && c + RING < nch) issue(c + RING);
+  }
+  ring.seq += (uint32_t)nch;
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    int64_t n = threadIdx.x + j * (int64_t)blockDim.x;
+    if (n >= Nn) break;
+    T bias = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
+                                     biasoff + gdec32(p.N, n, p.bias.s2)) : (T)0;
+    const int64_t cn = gdec32(p.N, n, p.C.s2);
+#pragma unroll
+    for (int r = 0; r < LOOP_MAXR; ++r) {
+      if (r >= mr) break;
+      T v = acc[j][r] + bias;
+      if (p.epilogue == 1) v = vm_tanh<T>(v);
+      store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + cn, v);
+    }
+  }
+  return true;
+}
 
 template <typename T>
 RT_DEV void gemm_rows(const rt_gemm_params& p, const int64_t* env, int64_t m0, int64_t m1,
@@ -166,10 +291,43 @@ RT_DEV int push_words_l(uint32_t* w, int n, int64_t v) {
   return n;
 }
 
+// mean of n values in numpy's pairwise order (umath pairwise_sum, n <= 128:
+// 8 strided accumulators, tree-combined, remainder added in order); lane j of
+// the warp owns accumulator j, so the result is bit-identical to numpy's.
+RT_DEV double warp_pairwise_sum(const void* base, int dtype, int64_t off, int64_t n, int lane) {
+  if (n > 128) {
+    double v = lane == 0 ? pairwise_sum_l(base, dtype, off, n) : 0.0;
+    return __shfl_sync(0xffffffffu, v, 0);
+  }
+  if (n < 8) {
+    double v = 0.0;
+    if (lane == 0)
+      for (int64_t i = 0; i < n; ++i) v += load_as<double>(base, dtype, off + i);
+    return __shfl_sync(0xffffffffu, v, 0);
+  }
+  const int64_t body = n - (n % 8);
+  double r = 0.0;
+  if (lane < 8) {
+    r = load_as<double>(base, dtype, off + lane);
+    for (int64_t i = 8 + lane; i < body; i += 8) r += load_as<double>(base, dtype, off + i);
+  }
+  double r1 = __shfl_down_sync(0xffffffffu, r, 1);   // pairs (0,1) (2,3) (4,5) (6,7)
+  double p01 = r + r1;
+  double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+  double q = p01 + p23;                               // lane 0: (r0+r1)+(r2+r3); lane 4: (r4+r5)+(r6+r7)
+  double q4 = __shfl_down_sync(0xffffffffu, q, 4);
+  double res = q + q4;
+  if (lane == 0)
+    for (int64_t i = body; i < n; ++i) res += load_as<double>(base, dtype, off + i);
+  return __shfl_sync(0xffffffffu, res, 0);
+}
+
 RT_DEV void udf_rows(const rt_udf_params& p, const rt_loop_op& op, const int64_t* env,
                      int64_t r0, int64_t r1, int64_t tix) {
   int64_t idx[RT_MAXD];
-  for (int64_t row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int64_t row = r0 + warp; row < r1; row += nwarps) {
     decompose(p.box, row, idx);
     double base = p.salt;
     for (int k = 0; k < p.nin; ++k) {
@@ -177,28 +335,45 @@ RT_DEV void udf_rows(const rt_udf_params& p, const rt_loop_op& op, const int64_t
       if (c == 0) continue;
       rt_fold f = fold_of(p.in[k], env);
       int64_t o = fview_off(p.in[k], &f, p.box.nd, idx);
-      base = base + pairwise_sum_l((const void*)p.in[k].ptr, p.in[k].dtype, o, c) / (double)c;
+      base = base + warp_pairwise_sum((const void*)p.in[k].ptr, p.in[k].dtype, o, c, lane) / (double)c;
     }
     const double* noise = (const double*)op.noise;
-    int64_t nz = op.noise_off + row * op.noise_row + tix * op.noise_step;
-    rt_pcg64 g;
-    if (!noise) {
-      uint32_t words[8 + 2 * RT_MAXD];
-      int n = 0;
-      for (int i = 0; i < p.nprefix; ++i) words[n++] = p.prefix[i];
-      for (int j = 0; j < p.ncoord; ++j) {
-        int s = p.coord_src[j];
-        n = push_words_l(words, n, s >= 0 ? idx[s] : env[-1 - s]);
+    if (noise) {
+      int64_t nz = op.noise_off + row * op.noise_row + tix * op.noise_step;
+      for (int j = 0; j < p.nout; ++j) {
+        rt_fold f = fold_of(p.out[j], env);
+        int64_t o = fview_off(p.out[j], &f, p.box.nd, idx);
+        int kind = p.out_kind[j];
+        double tb = kind == RT_BOOL ? tanh(base) : 0.0;
+        for (int e = lane; e < p.out_count[j]; e += 32) {
+          double z = noise[nz + e];
+          double v;
+          if (kind == RT_BOOL) v = (tb + z > 0.8) ? 1.0 : 0.0;
+          else if (kind == RT_I64) v = floor(3.0 * tanh(base + z));
+          else v = tanh(base + 0.3 * z);
+          store_as<double>((void*)p.out[j].ptr, p.out[j].dtype, o + e, v);
+        }
+        nz += p.out_count[j];
       }
-      pcg64_seed(g, words, n);
+      continue;
     }
+    if (lane != 0) continue;
+    uint32_t words[8 + 2 * RT_MAXD];
+    int n = 0;
+    for (int i = 0; i < p.nprefix; ++i) words[n++] = p.prefix[i];
+    for (int j = 0; j < p.ncoord; ++j) {
+      int s = p.coord_src[j];
+      n = push_words_l(words, n, s >= 0 ? idx[s] : env[-1 - s]);
+    }
+    rt_pcg64 g;
+    pcg64_seed(g, words, n);
     for (int j = 0; j < p.nout; ++j) {
       rt_fold f = fold_of(p.out[j], env);
       int64_t o = fview_off(p.out[j], &f, p.box.nd, idx);
       int kind = p.out_kind[j];
       double tb = kind == RT_BOOL ? tanh(base) : 0.0;
       for (int e = 0; e < p.out_count[j]; ++e) {
-        double z = noise ? noise[nz++] : pcg64_normal(g);
+        double z = pcg64_normal(g);
         double v;
         if (kind == RT_BOOL) v = (tb + z > 0.8) ? 1.0 : 0.0;
         else if (kind == RT_I64) v = floor(3.0 * tanh(base + z));
@@ -234,16 +409,30 @@ RT_DEV void rng_rows(const rt_rng_params& p, const int64_t* env, int64_t r0, int
 // ---------------------------------------------------------------- the loop
 
 __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ rt_loop_params p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ rt_fold sfold[RT_MAXIN + 1];
+  __shared__ __align__(8) uint64_t bars[RING];
   int64_t env[RT_MAXENV];
   for (int e = 0; e < RT_MAXENV; ++e) env[e] = p.h.env[e];
   const int64_t r0 = (int64_t)blockIdx.x * p.rows_per_cta;
   const int64_t r1 = min(p.rows, r0 + p.rows_per_cta);
   if (r0 >= r1) return;
   const rt_loop_op* ops = (const rt_loop_op*)p.ops;
-  int64_t tix = 0;
-  for (int64_t t = p.start; p.step > 0 ? t < p.stop : t > p.stop; t += p.step, ++tix) {
+  // smem: [A rows | TMA ring]; the ring takes what the A tile leaves
+  const uint32_t ring_off = (uint32_t)p.ring_off;   // bytes reserved for A rows + offsets
+  loop_ring ring;
+  ring.bar = bars;
+  ring.buf = smem + ring_off;
+  ring.stage_bytes = p.smem_bytes > (int)ring_off
+                         ? (uint32_t)((p.smem_bytes - (int)ring_off) / RING) & ~127u : 0u;
+  ring.seq = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < RING; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  for (int64_t t = p.start; p.step > 0 ? t < p.stop : t > p.stop; t += p.step) {
     env[p.slot] = t;
     for (int i = 0; i < p.nops; ++i) {
       const rt_loop_op& op = ops[i];
@@ -256,8 +445,14 @@ __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ r
         }
         case RT_K_GEMM: {
           const rt_gemm_params& q = *(const rt_gemm_params*)op.params;
-          if (op.f64) gemm_rows<double>(q, env, r0 * op.row_elems, r1 * op.row_elems, smem);
-          else gemm_rows<float>(q, env, r0 * op.row_elems, r1 * op.row_elems, smem);
+          const int64_t m0 = r0 * op.row_elems, m1 = r1 * op.row_elems;
+          if (op.f64) {
+            if (ring.stage_bytes == 0 || !gemm_rows_tma<double>(q, env, m0, m1, smem, ring))
+              gemm_rows<double>(q, env, m0, m1, smem);
+          } else {
+            if (ring.stage_bytes == 0 || !gemm_rows_tma<float>(q, env, m0, m1, smem, ring))
+              gemm_rows<float>(q, env, m0, m1, smem);
+          }
           break;
         }
         case RT_K_UDF:

@@ -488,13 +488,21 @@ class Lowering:
                 raise LowerError("op family not supported inside a persistent loop")
         R = max(1, -(-rows // 148))
         R = max(1, min(R, 16 // max_m))
-        smem = 0
+        a_need, tma = 0, False
         for kernel, p, re, f64, _ in ops:
             if kernel == N.RT_K_GEMM:
                 it = 8 if f64 else 4
                 need = ((R * re * p.k * it + 15) // 16) * 16 + p.k * 8
-                smem = max(smem, need)
-        if smem > 200 * 1024:
+                a_need = max(a_need, need)
+                tma = tma or p.n >= 64
+        ring_off = (a_need + 127) // 128 * 128
+        stage = 0
+        if tma:
+            stage = 32 * 1024
+            while ring_off + 4 * stage > 200 * 1024 and stage > 4096:
+                stage //= 2
+        smem = ring_off + 4 * stage
+        if smem > 220 * 1024:
             raise LowerError("persistent loop needs too much shared memory")
         # hoist the env's data-independent normals out of the loop
         for op in ops:
@@ -539,6 +547,7 @@ class Lowering:
         lp.rows = rows
         lp.rows_per_cta = R
         lp.smem_bytes = smem
+        lp.ring_off = ring_off
         first = self.g.nodes[s.body[0].nid]
         idx = self.add_rec(N.RT_K_LOOP, lp, [-(-rows // R), 1, 1], [256, 1, 1], smem,
                            (first.id, f"loop[{s.dim}]"))

@@ -116,7 +116,7 @@ class rt_loop_op(C.Structure):
 class rt_loop_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("slot", i32), ("nops", i32), ("start", i64), ("stop", i64),
                 ("step", i64), ("rows", i64), ("rows_per_cta", i32), ("smem_bytes", i32),
-                ("ops", u64)]
+                ("ring_off", i32), ("_pad", i32), ("ops", u64)]
 
 
 class rt_launch_rec(C.Structure):
