@@ -216,7 +216,7 @@ def main():
     bytes_, flops = RF.cost(dom["kernel"], dom["params"], exe.loop_info.get(dom["rec"]))
     n_inst = max(1, len(kev) // 2)
     kms = sum(dom_ms) / len(dom_ms) / n_inst   # per launch
-    if flops and RF.FAMILY[dom["kernel"]] in ("gemm", "loop"):
+    if flops and RF.FAMILY[dom["kernel"]] in ("gemm", "gemm_tc", "loop"):
         ach = flops / (kms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": tfl, "unit": "TFLOP/s",
                 "frac": ach / tfl, "traffic": None}

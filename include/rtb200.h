@@ -50,7 +50,8 @@ enum rt_kernel {
   RT_K_UDF = 6,      /* synthetic environment (dsl.py:288-307) per point      */
   RT_K_SPLITK = 7,   /* split-K partial reduction for RT_K_GEMM               */
   RT_K_POLICY = 8,   /* reserved                                              */
-  RT_K_LOOP = 9      /* persistent kernel running a whole row-local loop      */
+  RT_K_LOOP = 9,     /* persistent kernel running a whole row-local loop      */
+  RT_K_GEMM_TC = 10  /* RT_K_GEMM on tcgen05 (3xTF32, TMEM accumulators)      */
 };
 
 enum rt_status_code {
@@ -265,6 +266,7 @@ typedef struct {
   int32_t ring_off;     /* byte offset of the weight-panel ring */
   int32_t _pad;
   uint64_t ops;         /* device pointer to rt_loop_op[nops] */
+  uint64_t prof;        /* optional int64[nops]: CTA 0's clock64 cycles per op */
 } rt_loop_params;
 
 /* Launch record: one kernel family + its parameter block. */

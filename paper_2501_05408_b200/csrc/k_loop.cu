@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ r
     env[p.slot] = t;
     for (int i = 0; i < p.nops; ++i) {
       const rt_loop_op& op = ops[i];
+      long long c0 = (p.prof && blockIdx.x == 0) ? clock64() : 0;
       switch (op.kernel) {
         case RT_K_EW: {
           const rt_ew_params& q = *(const rt_ew_params*)op.params;
@@ -465,6 +466,8 @@ __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ r
           break;
       }
       __syncthreads();
+      if (p.prof && blockIdx.x == 0 && threadIdx.x == 0)
+        ((long long*)p.prof)[i] += clock64() - c0;
     }
   }
 }

@@ -18,6 +18,7 @@ extern "C" void* rt_kernel_udf();
 extern "C" void* rt_kernel_rng_fill();
 extern "C" void* rt_kernel_policy(const void* params);
 extern "C" void* rt_kernel_loop();
+extern "C" void* rt_kernel_gemm_tc();
 
 static thread_local std::string g_err;
 
@@ -89,6 +90,14 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_gop(p->C, env, nenv);
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
       return rt_kernel_gemm(p->f64);
+    }
+    case RT_K_GEMM_TC: {
+      rt_gemm_params* p = (rt_gemm_params*)blk;
+      fold_gop(p->A, env, nenv);
+      fold_gop(p->B, env, nenv);
+      fold_gop(p->C, env, nenv);
+      if (p->bias.ptr) fold_gop(p->bias, env, nenv);
+      return rt_kernel_gemm_tc();
     }
     case RT_K_SPLITK: {
       rt_splitk_params* p = (rt_splitk_params*)blk;

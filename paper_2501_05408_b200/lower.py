@@ -242,7 +242,7 @@ class Ctx:
 
 class Lowering:
     def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None,
-                 fuse_src=None, gemm_epi=None, persistent=True):
+                 fuse_src=None, gemm_epi=None, persistent=True, use_tc=True):
         self.plan = plan
         self.g = plan.graph
         self.benv = plan.benv
@@ -259,6 +259,7 @@ class Lowering:
         self.contract = contract or {}   # sum nid -> virtual matmul nid
         self.virtual = set(self.contract.values())
         self.persistent = persistent
+        self.use_tc = use_tc
         self._capture = None
         self.loop_subs = {}                    # loop record -> sub-op descriptors
         self.fuse_src = dict(fuse_src or {})   # producer nid -> consumer nid (inlined)
@@ -1258,6 +1259,8 @@ class Lowering:
         p.epilogue = epilogue
         if bias is not None:
             p.bias = bias
+        if self.use_tc and self._tc_ok(p, A, B, Cc):
+            return self._gemm_tc(p, label, accumulate, epilogue, bias)
         tiles = ((p.m + 63) // 64) * ((p.n + 63) // 64) * p.z
         splits = 1
         if tiles < 148 and p.k >= 1024:
@@ -1285,6 +1288,43 @@ class Lowering:
         else:
             grid = [(p.n + 63) // 64, (p.m + 63) // 64, p.z]
             self.add_rec(N.RT_K_GEMM, p, grid, [256, 1, 1], 0, label)
+
+    TC_MIN_MACS = 1 << 26
+
+    def _tc_ok(self, p, A, B, Cc):
+        f32 = all(x[0].dtype == "f32" for x in (A, B, Cc))
+        return (f32 and p.m * p.n * p.k >= self.TC_MIN_MACS and p.m >= 64
+                and p.m < (1 << 31) and p.k < (1 << 31) and not self._capture_active())
+
+    def _capture_active(self):
+        return self._capture is not None
+
+    def _gemm_tc(self, p, label, accumulate, epilogue, bias):
+        """tcgen05 3xTF32 path (csrc/k_gemm_tc.cu): 128 x 256 CTA tiles."""
+        tiles = ((p.m + 127) // 128) * ((p.n + 255) // 256) * p.z
+        splits = 1
+        if tiles < 148 and p.k >= 4096:
+            splits = int(max(1, min(148 * 2 // max(1, tiles), p.k // 2048)))
+        if p.z * splits > 65535 or (p.m + 127) // 128 > 65535:
+            raise LowerError("gemm grid too large")
+        p.splits = splits
+        if splits > 1:
+            p.part = self.alloc(splits * p.z * p.m * p.n * 4)
+        grid = [(p.n + 255) // 256, (p.m + 127) // 128, p.z * splits]
+        self.add_rec(N.RT_K_GEMM_TC, p, grid, [128, 1, 1], N.TC_SMEM, label)
+        if splits > 1:
+            q = N.rt_splitk_params()
+            q.Z, q.M, q.N = p.Z, p.M, p.N
+            q.z, q.m, q.n = p.z, p.m, p.n
+            q.splits = splits
+            q.f64 = 0
+            q.accumulate = accumulate
+            q.epilogue = epilogue
+            q.part = p.part
+            q.C = p.C
+            if bias is not None:
+                q.bias = bias
+            self.add_rec(N.RT_K_SPLITK, q, self.grid1(p.z * p.m * p.n), [256, 1, 1], 0, label)
 
     def k_contract(self, ctx: Ctx, X):
         """sum over full-range slices of a per-point matmul X, never

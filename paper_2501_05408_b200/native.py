@@ -26,6 +26,8 @@ DTYPE_CODE = {"f64": RT_F64, "f32": RT_F32, "i64": RT_I64, "bool": RT_BOOL}
 RT_K_EW, RT_K_REDUCE, RT_K_SCAN, RT_K_GEMM, RT_K_RNG, RT_K_UDF, RT_K_SPLITK, RT_K_POLICY = \
     1, 2, 3, 4, 5, 6, 7, 8
 RT_K_LOOP = 9
+RT_K_GEMM_TC = 10
+TC_SMEM = 2 * (2 * 128 * 16 * 4 + 2 * 256 * 16 * 4)
 
 RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT = 1, 2, 3, 4
 
@@ -116,7 +118,7 @@ class rt_loop_op(C.Structure):
 class rt_loop_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("slot", i32), ("nops", i32), ("start", i64), ("stop", i64),
                 ("step", i64), ("rows", i64), ("rows_per_cta", i32), ("smem_bytes", i32),
-                ("ring_off", i32), ("_pad", i32), ("ops", u64)]
+                ("ring_off", i32), ("_pad", i32), ("ops", u64), ("prof", u64)]
 
 
 class rt_launch_rec(C.Structure):

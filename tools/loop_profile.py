@@ -1,0 +1,42 @@
+"""Per-op cycle breakdown of the persistent loop kernel on the C2 workload
+(CTA 0's clock64 deltas, accumulated over all steps)."""
+import ctypes as C
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from golden_cases import load_graph  # noqa: E402
+from paper_2501_05408_b200 import get_executable, native as N, roofline as RF  # noqa: E402
+from paper_2501_05408_b200.workloads import mlp_inputs  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
+g = load_graph("reinforce_mlp_c2")
+inp = {k: torch.from_numpy(v).cuda() for k, v in mlp_inputs().items()}
+exe, _ = get_executable(g, {"I": 1, "B": B, "T": T}, inp, seed=0)
+for ri, info in exe.loop_info.items():
+    lp = exe.recs[ri]
+    params = exe._params[ri]
+    prof = torch.zeros(len(info["ops"]), dtype=torch.int64, device="cuda")
+    params.prof = prof.data_ptr()
+    exe.run(inp, graph=False)
+    torch.cuda.synchronize()
+    prof.zero_()
+    exe.run(inp, graph=False)
+    torch.cuda.synchronize()
+    cyc = prof.cpu().tolist()
+    tot = sum(cyc)
+    print(f"loop record {ri}: rows={params.rows} rows_per_cta={params.rows_per_cta} "
+          f"smem={params.smem_bytes} trips={info['trips']}")
+    for (k, q, re, f64, noise), c in zip(info["ops"], cyc):
+        print(f"  {RF.FAMILY.get(k):6s} row_elems={re:5d} cycles/step={c / info['trips']:10.0f} "
+              f"share={100 * c / max(1, tot):5.1f}%")
+    print(f"  total cycles/step {tot / info['trips']:.0f}")
+    params.prof = 0
+prof = exe.profile(inp)
+for r in sorted(prof, key=lambda r: -r["ms"])[:6]:
+    print(RF.FAMILY.get(r["kernel"]), r["label"], round(r["ms"], 3), "ms")
