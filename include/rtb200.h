@@ -253,6 +253,8 @@ typedef struct {
   int64_t noise_off;    /* UDF: element offset of (row 0, loop index 0) in `noise` */
   int64_t noise_row;    /* UDF: elements between consecutive rows in `noise` */
   int64_t noise_step;   /* UDF: elements between consecutive loop indices */
+  int32_t param_bytes;  /* size of the parameter block */
+  int32_t smem_off;     /* byte offset of the CTA's shared-memory copy of it */
 } rt_loop_op;
 
 typedef struct {
@@ -264,7 +266,7 @@ typedef struct {
   int32_t rows_per_cta;
   int32_t smem_bytes;   /* dynamic shared memory: [A rows | TMA ring] */
   int32_t ring_off;     /* byte offset of the weight-panel ring */
-  int32_t _pad;
+  int32_t a_off;        /* byte offset of the GEMM A-row staging area */
   uint64_t ops;         /* device pointer to rt_loop_op[nops] */
   uint64_t prof;        /* optional int64[nops]: CTA 0's clock64 cycles per op */
 } rt_loop_params;

@@ -115,7 +115,8 @@ RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m
   const int64_t kc = ring.stage_bytes / (Nn * (int64_t)sizeof(T));
   if (kc < 1 || Nn < 64 || Nn > 4 * (int64_t)blockDim.x) return false;
   const int mr = (int)(m1 - m0);
-  T* As = (T*)smem;
+  const int mrp = (mr + 3) & ~3;                           // rows padded to a multiple of 4
+  T* As = (T*)smem;                                        // k-major: As[k * mrp + r]
   const int64_t aoff = fold_gop_off(p.A, env);
   const int64_t boff = fold_gop_off(p.B, env);
   const int64_t coff = fold_gop_off(p.C, env);
@@ -133,12 +134,15 @@ RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m
   };
   if (threadIdx.x == 0)
     for (int64_t c = 0; c < (nch < RING ? nch : (int64_t)RING); ++c) issue(c);
-  // stage A rows meanwhile
-  for (int64_t i = threadIdx.x; i < (int64_t)mr * K; i += blockDim.x) {
-    int r = (int)(i / K);
-    int64_t k = i - (int64_t)r * K;
-    As[i] = load_as<T>((const void*)p.A.ptr, p.A.dtype,
-                       aoff + gdec32(p.M, m0 + r, p.A.s1) + gdec32(p.K, k, p.A.s2));
+  // stage A rows meanwhile (k-major, zero-padded rows)
+  {
+    const int64_t sk = p.A.s2[0];
+    for (int64_t i = threadIdx.x; i < (int64_t)mrp * K; i += blockDim.x) {
+      int r = (int)(i / K);
+      int64_t k = i - (int64_t)r * K;
+      As[k * mrp + r] = r < mr ? load_as<T>((const void*)p.A.ptr, p.A.dtype,
+                                            aoff + gdec32(p.M, m0 + r, p.A.s1) + k * sk) : (T)0;
+    }
   }
   __syncthreads();
   constexpr int NC = 4;   // columns per thread (Nn <= 4 * blockDim)
@@ -155,6 +159,17 @@ RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m
     const int64_t k0 = c * kc;
     const int64_t rows = min(kc, K - k0);
     for (int64_t kk = 0; kk < rows; ++kk) {
+      const T* ak = As + (k0 + kk) * mrp;
+      T a[LOOP_MAXR];
+#pragma unroll
+      for (int q = 0; q < LOOP_MAXR / 4; ++q) {
+        if (4 * q < mrp) {
+          a[4 * q + 0] = ak[4 * q + 0];
+          a[4 * q + 1] = ak[4 * q + 1];
+          a[4 * q + 2] = ak[4 * q + 2];
+          a[4 * q + 3] = ak[4 * q + 3];
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
         int64_t n = threadIdx.x + j * (int64_t)blockDim.x;
@@ -162,7 +177,7 @@ RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m
         T b = Bs[kk * Nn + n];
 #pragma unroll
         for (int r = 0; r < LOOP_MAXR; ++r)
-          if (r < mr) acc[j][r] = fma(As[r * K + k0 + kk], b, acc[j][r]);
+          if (r < mrp) acc[j][r] = fma(a[r], b, acc[j][r]);
       }
     }
     __syncthreads();   // everyone is done with stage st
@@ -418,7 +433,14 @@ __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ r
   const int64_t r1 = min(p.rows, r0 + p.rows_per_cta);
   if (r0 >= r1) return;
   const rt_loop_op* ops = (const rt_loop_op*)p.ops;
-  // smem: [A rows | TMA ring]; the ring takes what the A tile leaves
+  // every op's descriptor is read each step: keep a copy in shared memory
+  for (int i = 0; i < p.nops; ++i) {
+    const int4* src = (const int4*)ops[i].params;
+    int4* dst = (int4*)(smem + ops[i].smem_off);
+    for (int w = threadIdx.x; w < (ops[i].param_bytes + 15) / 16; w += blockDim.x) dst[w] = src[w];
+  }
+  unsigned char* sA = smem + p.a_off;
+  // smem: [op descriptors | A rows | TMA ring]
   const uint32_t ring_off = (uint32_t)p.ring_off;   // bytes reserved for A rows + offsets
   loop_ring ring;
   ring.bar = bars;
@@ -439,28 +461,28 @@ __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ r
       long long c0 = (p.prof && blockIdx.x == 0) ? clock64() : 0;
       switch (op.kernel) {
         case RT_K_EW: {
-          const rt_ew_params& q = *(const rt_ew_params*)op.params;
+          const rt_ew_params& q = *(const rt_ew_params*)(smem + op.smem_off);
           if (op.f64) ew_rows<double>(q, env, r0 * op.row_elems, r1 * op.row_elems, sfold);
           else ew_rows<float>(q, env, r0 * op.row_elems, r1 * op.row_elems, sfold);
           break;
         }
         case RT_K_GEMM: {
-          const rt_gemm_params& q = *(const rt_gemm_params*)op.params;
+          const rt_gemm_params& q = *(const rt_gemm_params*)(smem + op.smem_off);
           const int64_t m0 = r0 * op.row_elems, m1 = r1 * op.row_elems;
           if (op.f64) {
-            if (ring.stage_bytes == 0 || !gemm_rows_tma<double>(q, env, m0, m1, smem, ring))
-              gemm_rows<double>(q, env, m0, m1, smem);
+            if (ring.stage_bytes == 0 || !gemm_rows_tma<double>(q, env, m0, m1, sA, ring))
+              gemm_rows<double>(q, env, m0, m1, sA);
           } else {
-            if (ring.stage_bytes == 0 || !gemm_rows_tma<float>(q, env, m0, m1, smem, ring))
-              gemm_rows<float>(q, env, m0, m1, smem);
+            if (ring.stage_bytes == 0 || !gemm_rows_tma<float>(q, env, m0, m1, sA, ring))
+              gemm_rows<float>(q, env, m0, m1, sA);
           }
           break;
         }
         case RT_K_UDF:
-          udf_rows(*(const rt_udf_params*)op.params, op, env, r0, r1, t);
+          udf_rows(*(const rt_udf_params*)(smem + op.smem_off), op, env, r0, r1, t);
           break;
         case RT_K_RNG:
-          rng_rows(*(const rt_rng_params*)op.params, env, r0, r1);
+          rng_rows(*(const rt_rng_params*)(smem + op.smem_off), env, r0, r1);
           break;
         default:
           break;

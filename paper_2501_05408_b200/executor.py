@@ -515,7 +515,7 @@ class Executable:
         for ri, info in low.loop_subs.items():
             ops = info["ops"]
             blobs, offs, cur = [], [], 0
-            for kernel, p, re, f64, noise in ops:
+            for kernel, p, re, f64, noise, soff in ops:
                 b = C.string_at(C.addressof(p), C.sizeof(p))
                 offs.append(cur)
                 blobs.append(b + b"\0" * ((-len(b)) % 256))
@@ -525,9 +525,11 @@ class Executable:
             dev = torch.empty(total, dtype=torch.uint8, device=self.dev)
             self.tensors.append(dev)
             base = dev.data_ptr()
-            for i, (kernel, p, re, f64, noise) in enumerate(ops):
+            for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
                 a = arr[i]
                 a.kernel = kernel
+                a.param_bytes = C.sizeof(p)
+                a.smem_off = soff
                 a.f64 = int(f64)
                 a.params = base + offs[i]
                 a.row_elems = re

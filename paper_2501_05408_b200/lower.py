@@ -493,14 +493,19 @@ class Lowering:
         for kernel, p, re, f64, _ in ops:
             if kernel == N.RT_K_GEMM:
                 it = 8 if f64 else 4
-                need = ((R * re * p.k * it + 15) // 16) * 16 + p.k * 8
+                need = ((((R * re + 3) // 4 * 4) * p.k * it + 15) // 16) * 16 + p.k * 8
                 a_need = max(a_need, need)
                 tma = tma or p.n >= 64
-        ring_off = (a_need + 127) // 128 * 128
+        p_off, cur = [], 0
+        for kernel, p, re, f64, _ in ops:
+            p_off.append(cur)
+            cur += (C.sizeof(p) + 127) // 128 * 128
+        a_off = cur
+        ring_off = (a_off + a_need + 127) // 128 * 128
         stage = 0
         if tma:
             stage = 32 * 1024
-            while ring_off + 4 * stage > 200 * 1024 and stage > 4096:
+            while ring_off + 4 * stage > 210 * 1024 and stage > 4096:
                 stage //= 2
         smem = ring_off + 4 * stage
         if smem > 220 * 1024:
@@ -549,6 +554,9 @@ class Lowering:
         lp.rows_per_cta = R
         lp.smem_bytes = smem
         lp.ring_off = ring_off
+        lp.a_off = a_off
+        for op, off in zip(ops, p_off):
+            op.append(off)
         first = self.g.nodes[s.body[0].nid]
         idx = self.add_rec(N.RT_K_LOOP, lp, [-(-rows // R), 1, 1], [256, 1, 1], smem,
                            (first.id, f"loop[{s.dim}]"))

@@ -112,13 +112,14 @@ class rt_udf_params(C.Structure):
 
 class rt_loop_op(C.Structure):
     _fields_ = [("kernel", i32), ("f64", i32), ("params", u64), ("row_elems", i64),
-                ("noise", u64), ("noise_off", i64), ("noise_row", i64), ("noise_step", i64)]
+                ("noise", u64), ("noise_off", i64), ("noise_row", i64), ("noise_step", i64),
+                ("param_bytes", i32), ("smem_off", i32)]
 
 
 class rt_loop_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("slot", i32), ("nops", i32), ("start", i64), ("stop", i64),
                 ("step", i64), ("rows", i64), ("rows_per_cta", i32), ("smem_bytes", i32),
-                ("ring_off", i32), ("_pad", i32), ("ops", u64), ("prof", u64)]
+                ("ring_off", i32), ("a_off", i32), ("ops", u64), ("prof", u64)]
 
 
 class rt_launch_rec(C.Structure):

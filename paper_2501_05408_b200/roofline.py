@@ -40,7 +40,7 @@ def cost(kernel, p, loop_info=None):
             return 0, 0
         b = f = 0
         rows = p.rows
-        for k, q, re, f64, noise in loop_info["ops"]:
+        for k, q, re, f64, noise, *_ in loop_info["ops"]:
             b2, f2 = cost(k, q)
             b += b2
             f += f2

@@ -32,7 +32,7 @@ for ri, info in exe.loop_info.items():
     tot = sum(cyc)
     print(f"loop record {ri}: rows={params.rows} rows_per_cta={params.rows_per_cta} "
           f"smem={params.smem_bytes} trips={info['trips']}")
-    for (k, q, re, f64, noise), c in zip(info["ops"], cyc):
+    for (k, q, re, f64, noise, *_), c in zip(info["ops"], cyc):
         print(f"  {RF.FAMILY.get(k):6s} row_elems={re:5d} cycles/step={c / info['trips']:10.0f} "
               f"share={100 * c / max(1, tot):5.1f}%")
     print(f"  total cycles/step {tot / info['trips']:.0f}")
