@@ -104,6 +104,87 @@ RT_DEV void ew_rows(const rt_ew_params& p, const int64_t* env, int64_t f0, int64
 // (M = slab rows x m), all n.  A rows are staged in shared memory; B is
 // streamed from L2 with each thread owning columns and all rows (B reuse).
 
+
+// A loads for MRP rows at one k: float4 / double2 vector broadcasts from smem
+template <typename T, int MRP>
+RT_DEV void load_a(const T* ak, T (&a)[MRP]) {
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int q = 0; q < MRP / 4; ++q) {
+      float4 v = reinterpret_cast<const float4*>(ak)[q];
+      a[4 * q] = v.x; a[4 * q + 1] = v.y; a[4 * q + 2] = v.z; a[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < MRP / 2; ++q) {
+      double2 v = reinterpret_cast<const double2*>(ak)[q];
+      a[2 * q] = v.x; a[2 * q + 1] = v.y;
+    }
+  }
+}
+
+// chunk loop + epilogue with the padded row count MRP known at compile time
+template <typename T, int MRP>
+RT_DEV bool tma_body(const rt_gemm_params& p, const T* As, const T* Bg, int64_t K, int64_t Nn,
+                     int64_t kc, int64_t nch, int mr, int64_t m0, int64_t coff, int64_t biasoff,
+                     loop_ring& ring) {
+  constexpr int NC = 4;   // columns per thread (Nn <= 4 * blockDim)
+  const int nn = (int)Nn;
+  T acc[NC][MRP];
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+#pragma unroll
+    for (int r = 0; r < MRP; ++r) acc[j][r] = (T)0;
+  auto issue = [&](int c) {
+    uint32_t st = (ring.seq + (uint32_t)c) % RING;
+    int64_t k0 = (int64_t)c * kc;
+    int64_t rows = min(kc, K - k0);
+    uint32_t bytes = (uint32_t)(rows * Nn * sizeof(T));
+    mbar_expect_tx(&ring.bar[st], bytes);
+    bulk_g2s(ring.buf + (size_t)st * ring.stage_bytes, Bg + k0 * Nn, bytes, &ring.bar[st]);
+  };
+  for (int c = 0; c < (int)nch; ++c) {
+    uint32_t g = ring.seq + (uint32_t)c;
+    uint32_t st = g % RING;
+    mbar_wait(&ring.bar[st], (g / RING) & 1);
+    const T* Bs = (const T*)(ring.buf + (size_t)st * ring.stage_bytes);
+    const int k0 = c * (int)kc;
+    const int rows = (int)min(kc, K - (int64_t)k0);
+    const T* ak = As + (size_t)k0 * MRP;
+    for (int kk = 0; kk < rows; ++kk, ak += MRP) {
+      T a[MRP];
+      load_a<T, MRP>(ak, a);
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const int n = (int)threadIdx.x + j * (int)blockDim.x;
+        if (n < nn) {
+          const T b = Bs[kk * nn + n];
+#pragma unroll
+          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[r], b, acc[j][r]);
+        }
+      }
+    }
+    __syncthreads();   // everyone is done with stage st
+    if (threadIdx.x == 0 && c + RING < (int)nch) issue(c + RING);
+  }
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int64_t n = threadIdx.x + j * (int64_t)blockDim.x;
+    if (n >= Nn) break;
+    T bias = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
+                                     biasoff + gdec32(p.N, n, p.bias.s2)) : (T)0;
+    const int64_t cn = gdec32(p.N, n, p.C.s2);
+#pragma unroll
+    for (int r = 0; r < MRP; ++r) {
+      if (r >= mr) break;
+      T v = acc[j][r] + bias;
+      if (p.epilogue == 1) v = vm_tanh<T>(v);
+      store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + cn, v);
+    }
+  }
+  return true;
+}
+
 template <typename T>
 RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m0, int64_t m1,
                           unsigned char* smem, loop_ring& ring) {
@@ -145,60 +226,14 @@ RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m
     }
   }
   __syncthreads();
-  constexpr int NC = 4;   // columns per thread (Nn <= 4 * blockDim)
-  T acc[NC][LOOP_MAXR];
-#pragma unroll
-  for (int j = 0; j < NC; ++j)
-#pragma unroll
-    for (int r = 0; r < LOOP_MAXR; ++r) acc[j][r] = (T)0;
-  for (int64_t c = 0; c < nch; ++c) {
-    uint32_t g = ring.seq + (uint32_t)c;
-    uint32_t st = g % RING;
-    mbar_wait(&ring.bar[st], (g / RING) & 1);
-    const T* Bs = (const T*)(ring.buf + (size_t)st * ring.stage_bytes);
-    const int64_t k0 = c * kc;
-    const int64_t rows = min(kc, K - k0);
-    for (int64_t kk = 0; kk < rows; ++kk) {
-      const T* ak = As + (k0 + kk) * mrp;
-      T a[LOOP_MAXR];
-#pragma unroll
-      for (int q = 0; q < LOOP_MAXR / 4; ++q) {
-        if (4 * q < mrp) {
-          a[4 * q + 0] = ak[4 * q + 0];
-          a[4 * q + 1] = ak[4 * q + 1];
-          a[4 * q + 2] = ak[4 * q + 2];
-          a[4 * q + 3] = ak[4 * q + 3];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        int64_t n = threadIdx.x + j * (int64_t)blockDim.x;
-        if (n >= Nn) break;
-        T b = Bs[kk * Nn + n];
-#pragma unroll
-        for (int r = 0; r < LOOP_MAXR; ++r)
-          if (r < mrp) acc[j][r] = fma(a[r], b, acc[j][r]);
-      }
-    }
-    __syncthreads();   // everyone is done with stage st
-    if (threadIdx.x == 0 && c + RING < nch) issue(c + RING);
+  bool ok = false;
+  switch (mrp) {
+    case 4: ok = tma_body<T, 4>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
+    case 8: ok = tma_body<T, 8>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
+    case 12: ok = tma_body<T, 12>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
+    default: ok = tma_body<T, 16>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
   }
   ring.seq += (uint32_t)nch;
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    int64_t n = threadIdx.x + j * (int64_t)blockDim.x;
-    if (n >= Nn) break;
-    T bias = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
-                                     biasoff + gdec32(p.N, n, p.bias.s2)) : (T)0;
-    const int64_t cn = gdec32(p.N, n, p.C.s2);
-#pragma unroll
-    for (int r = 0; r < LOOP_MAXR; ++r) {
-      if (r >= mr) break;
-      T v = acc[j][r] + bias;
-      if (p.epilogue == 1) v = vm_tanh<T>(v);
-      store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + cn, v);
-    }
-  }
   return true;
 }
 

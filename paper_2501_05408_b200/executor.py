@@ -366,6 +366,36 @@ def find_ew_fusions(g: Graph, pshape, skip):
     return fuse
 
 
+LAYOUT_KINDS = ("permute", "reshape", "squeeze", "unsqueeze", "expand")
+ABSORB_CONSUMERS = {"matmul", "sum", "add", "sub", "mul", "div", "neg", "exp", "log", "tanh",
+                    "sqrt", "pow_const", "cmp", "where", "cast", "merge", "permute", "squeeze",
+                    "unsqueeze", "expand", "identity", "detach"}
+
+
+def find_absorbed_layouts(g: Graph, skip):
+    """Layout nodes read through an identity edge from a materialised source
+    are never copied: consumers read the source with transformed strides."""
+    out_ids = {nid for _, nid, _ in g.outputs}
+    res = set()
+    for n in g.sorted_nodes():
+        if n.kind not in LAYOUT_KINDS or n.id in out_ids or n.id in skip:
+            continue
+        ins = g.in_edges(n.id)
+        if len(ins) != 1:
+            continue
+        e = ins[0]
+        src = g.nodes[e.src]
+        if not _is_identity(e, src, n):
+            continue
+        if n.kind == "reshape" and (src.id in res or src.kind in LAYOUT_KINDS):
+            continue
+        outs = g.out_edges(n.id)
+        if not outs or any(g.nodes[o.sink].kind not in ABSORB_CONSUMERS for o in outs):
+            continue
+        res.add(n.id)
+    return res
+
+
 def analyze(g: Graph, benv, pshape, fuse=True):
     """Plan the loop nest and decide aliases, contractions and fusions
     (device-independent; the CPU tests run this directly)."""
@@ -376,6 +406,8 @@ def analyze(g: Graph, benv, pshape, fuse=True):
     plan = Planner(g, benv).plan()
     fixed_of = plan_fixed(plan.steps)
     alias_nodes = {k[0] for k in alias}
+    absorbed = find_absorbed_layouts(g, virtual | alias_nodes) if fuse else set()
+    virtual |= absorbed
     gemm_epi = find_gemm_epilogues(g, pshape, fixed_of, virtual | alias_nodes) if fuse else {}
     taken = set(virtual) | alias_nodes | set(gemm_epi)
     for f, (x, _b, t) in gemm_epi.items():
@@ -395,7 +427,7 @@ def analyze(g: Graph, benv, pshape, fuse=True):
             bufs[key] = Buf(key, n.domain, tuple(ext[d] for d in n.domain), pshape[key],
                             n.out_dtypes[oid], alias.get(key))
     return {"contract": contract, "alias": alias, "plan": plan, "gemm_epi": gemm_epi,
-            "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs}
+            "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs, "absorbed": absorbed}
 
 
 def payload_shapes(g: Graph, benv):
@@ -429,6 +461,7 @@ class Executable:
         an = analyze(g, benv, pshape, fuse)
         self.contract, self.plan, self.gemm_epi, self.fuse_src = (
             an["contract"], an["plan"], an["gemm_epi"], an["fuse_src"])
+        self.absorbed = an["absorbed"]
         self.virtual = virtual = an["virtual"]
         self.bufs = an["bufs"]
         roots = [k for k, b in self.bufs.items() if b.alias is None and k[0] not in virtual]
@@ -448,7 +481,8 @@ class Executable:
         fake = {k: (i + 1) << 44 for i, k in enumerate(roots)}
         self._set_ptrs(fake)
         low = Lowering(self.plan, self.bufs, self.status, seed, lambda nb: 0,
-                       self.contract, self.fuse_src, self.gemm_epi).lower()
+                       self.contract, self.fuse_src, self.gemm_epi,
+                       absorbed=self.absorbed).lower()
         key_of = {v: k for k, v in fake.items()}
         rec_ptrs = []
         for ri, (_, p, *_r) in enumerate(low.recs):
@@ -479,7 +513,8 @@ class Executable:
         self.peak_bytes = arena
         # pass 2: real pointers
         low = Lowering(self.plan, self.bufs, self.status, seed, self._scratch,
-                       self.contract, self.fuse_src, self.gemm_epi).lower()
+                       self.contract, self.fuse_src, self.gemm_epi,
+                       absorbed=self.absorbed).lower()
         self._upload_loops(low)
         self.nrec = len(low.recs)
         self._params = [p for (_, p, _, _, _, _) in low.recs]

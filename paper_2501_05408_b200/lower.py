@@ -242,7 +242,7 @@ class Ctx:
 
 class Lowering:
     def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None,
-                 fuse_src=None, gemm_epi=None, persistent=True, use_tc=True):
+                 fuse_src=None, gemm_epi=None, persistent=True, use_tc=True, absorbed=None):
         self.plan = plan
         self.g = plan.graph
         self.benv = plan.benv
@@ -258,6 +258,8 @@ class Lowering:
         self.alloc = alloc         # nbytes -> device pointer (scratch)
         self.contract = contract or {}   # sum nid -> virtual matmul nid
         self.virtual = set(self.contract.values())
+        self.absorbed = set(absorbed or ())
+        self.virtual |= self.absorbed
         self.persistent = persistent
         self.use_tc = use_tc
         self._capture = None
@@ -282,6 +284,8 @@ class Lowering:
     # -- edge views ----------------------------------------------------------
 
     def edge_val(self, ctx: Ctx, e) -> EdgeVal:
+        if e.src in self.absorbed:
+            return self._absorbed_val(ctx, e)
         src = self.g.nodes[e.src]
         sb = self.bufs[(e.src, e.oid)]
         st = self.storage((e.src, e.oid))
@@ -317,6 +321,45 @@ class Lowering:
                 ev.checks.append((aff[1], {n: v for (n, k), v in aff[0].items()}, hi_dom))
         ev.axes = slice_axes + [Axis(p, s) for p, s in zip(sb.pshape, sb.payload_strides())]
         ev.nslices = len(slice_axes)
+        return ev
+
+    def _absorbed_val(self, ctx, e):
+        """Edge into a layout node that was never materialised: read its
+        source through the same point map, then apply the node's payload
+        transform (permute/reshape/squeeze/unsqueeze/expand) to the axes."""
+        L = self.g.nodes[e.src]
+        (ein,) = self.g.in_edges(L.id)
+        ev = self.edge_val(ctx, ir.Edge(e.sink, e.iid, e.phi, e.psi, ein.oid, ein.src))
+        sl = ev.axes[:ev.nslices]
+        pay = ev.axes[ev.nslices:]
+        k = L.kind
+        if k == "permute":
+            pay = [pay[o] for o in L.params["order"]]
+        elif k == "squeeze":
+            dd = L.params["dim"]
+            pay = pay[:dd] + pay[dd + 1:]
+        elif k == "unsqueeze":
+            dd = L.params["dim"]
+            pay = pay[:dd] + [Axis(1, 0)] + pay[dd:]
+        elif k == "reshape":
+            if [a.stride for a in pay] != cstrides([a.ext for a in pay]):
+                raise LowerError(f"{L.name}: reshape of a non-contiguous view")
+            shape = list(self.bufs[(L.id, 0)].pshape)
+            pay = [Axis(x, st) for x, st in zip(shape, cstrides(shape))]
+        elif k == "expand":
+            shape = list(self.bufs[(L.id, 0)].pshape)
+            off = len(shape) - len(pay)
+            new = []
+            for j, x in enumerate(shape):
+                vj = j - off
+                if vj < 0 or pay[vj].ext == 1:
+                    new.append(Axis(x, 0))
+                else:
+                    new.append(pay[vj])
+            pay = new
+        else:
+            raise LowerError(f"cannot absorb {k}")
+        ev.axes = list(sl) + list(pay)
         return ev
 
     def _add_affine(self, ev, aff, S):
@@ -916,6 +959,8 @@ class Lowering:
         if ax != 0 or ev.nslices != 1 or ev.progs or ev.checks:
             return False
         (e,) = self.g.in_edges(n.id)
+        if e.src in self.absorbed:
+            return False
         src = self.g.nodes[e.src]
         slice_pos = [j for j, c in enumerate(e.phi) if c[0] == "slice"]
         (sj,) = slice_pos
