@@ -159,7 +159,11 @@ def main():
     bounds = {"I": 1, "B": B, "T": T_STEPS}
     host = mlp_inputs()
     dev_in = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
-    exe, _ = get_executable(g, bounds, dev_in, seed=rank)
+    shard = None
+    if world > 1:
+        from paper_2501_05408_b200.shard import ShardSpec
+        shard = ShardSpec("b", rank, world)     # envs [rank*B, (rank+1)*B) of B*world
+    exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard)
 
     def step_dev(inp, graph=None):
         if graph is None:
@@ -185,7 +189,10 @@ def main():
         rows.append(r)
     rows.sort(key=lambda r: -r["ms"])
     dom = rows[0]
-    graph_ev, kev = exe.capture_with_events(dom["rec"])
+    if exe.hooks:      # sharded: all-reduce hooks between program segments, no single graph
+        graph_ev, kev = None, []
+    else:
+        graph_ev, kev = exe.capture_with_events(dom["rec"])
 
     if dist:
         dist.barrier()
@@ -197,9 +204,11 @@ def main():
     ev0.record()
     for s in range(args.steps):
         inp = step_dev(inp, graph_ev)
-        ev1.record()
-        ev1.synchronize()
-        dom_ms.append(sum(kev[2 * i].elapsed_time(kev[2 * i + 1]) for i in range(len(kev) // 2)))
+        if kev:
+            ev1.record()
+            ev1.synchronize()
+            dom_ms.append(sum(kev[2 * i].elapsed_time(kev[2 * i + 1])
+                              for i in range(len(kev) // 2)))
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -215,7 +224,10 @@ def main():
     hbm, tfl, src = peaks()
     bytes_, flops = RF.cost(dom["kernel"], dom["params"], exe.loop_info.get(dom["rec"]))
     n_inst = max(1, len(kev) // 2)
-    kms = sum(dom_ms) / len(dom_ms) / n_inst   # per launch
+    if dom_ms:
+        kms = sum(dom_ms) / len(dom_ms) / n_inst   # per launch, live in the timed graph
+    else:
+        kms = dom["ms"] / max(1, dom["count"])     # per launch, from the profiled step
     if flops and RF.FAMILY[dom["kernel"]] in ("gemm", "gemm_tc", "loop"):
         ach = flops / (kms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": tfl, "unit": "TFLOP/s",
@@ -238,19 +250,24 @@ def main():
                     "tflops": round(f_ / (per / 1e3) / 1e12, 2) if f_ and per > 0 else None})
 
     # e2e through the public API with host buffers
-    exe_h, _ = get_executable(g, bounds, host, seed=rank)
     hin = host
     for w in range(max(1, args.warmup)):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=rank)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard)
         hin = next_inputs(outs)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     for s in range(args.steps):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=rank)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard)
         hin = next_inputs(outs)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     h2d = sum(v.nbytes for v in host.values())
     d2h = sum(np.asarray(v).nbytes for v in outs.values())
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
     e2e = world * B * T_STEPS / (e2e_ms / 1e3)
 
     line = {"metric": "env-steps/s per train iter", "value": value, "unit": "env-steps/s",

@@ -213,6 +213,7 @@ typedef struct {
   int32_t ncoord;        /* number of point coordinates (full node domain) */
   uint32_t prefix[8];
   int32_t coord_src[RT_MAXD];
+  int64_t coord_add[RT_MAXD];   /* added to coordinate j (global index of a sharded dim) */
   int32_t dist;          /* 0 normal, 1 uniform */
   int32_t count;         /* values per point */
   rt_view out;           /* strides over box; `count` contiguous values per point */
@@ -228,6 +229,7 @@ typedef struct {
   int32_t ncoord;
   uint32_t prefix[8];
   int32_t coord_src[RT_MAXD];
+  int64_t coord_add[RT_MAXD];
   double salt;
   int32_t nin;
   int32_t nout;
@@ -290,8 +292,12 @@ enum rt_op {
                        /*     d = step, e = pc after matching END          */
   RT_OP_END = 3,       /* a = pc of matching FOR                           */
   RT_OP_EVENT = 4,     /* a = event slot: record on the stream             */
-  RT_OP_COPY = 5       /* device copy: a = rec idx of an rt_copy record    */
+  RT_OP_COPY = 5,      /* device copy: a = rec idx of an rt_copy record    */
+  RT_OP_HOOK = 6       /* host hook a (e.g. an NCCL all-reduce of a slab):  */
+                       /* rt_run_segment returns RT_HOOK with the next pc   */
 };
+
+#define RT_HOOK 100
 
 typedef struct {
   int32_t op;
@@ -310,6 +316,10 @@ int rt_launch(const rt_launch_rec* rec, const int64_t* env, int32_t nenv, uint64
  * cudaEvent_t handles for RT_OP_EVENT. */
 int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,
            int64_t* env, int32_t nenv, uint64_t stream, const uint64_t* events, int32_t nevents);
+/* Run from *pc_io until the end (returns 0) or until a RT_OP_HOOK (returns
+ * RT_HOOK with *pc_io = pc after the hook and *hook_out = its id). */
+int rt_run_segment(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,
+                   int64_t* env, int32_t nenv, uint64_t stream, int32_t* pc_io, int32_t* hook_out);
 /* Capture a program into a CUDA graph (loops unrolled, env folded per
  * launch) and replay it; the graph-exec handle is returned in *out. */
 int rt_graph_capture(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,

@@ -413,7 +413,7 @@ RT_DEV void udf_rows(const rt_udf_params& p, const rt_loop_op& op, const int64_t
     for (int i = 0; i < p.nprefix; ++i) words[n++] = p.prefix[i];
     for (int j = 0; j < p.ncoord; ++j) {
       int s = p.coord_src[j];
-      n = push_words_l(words, n, s >= 0 ? idx[s] : env[-1 - s]);
+      n = push_words_l(words, n, (s >= 0 ? idx[s] : env[-1 - s]) + p.coord_add[j]);
     }
     rt_pcg64 g;
     pcg64_seed(g, words, n);
@@ -443,7 +443,7 @@ RT_DEV void rng_rows(const rt_rng_params& p, const int64_t* env, int64_t r0, int
     for (int i = 0; i < p.nprefix; ++i) words[n++] = p.prefix[i];
     for (int j = 0; j < p.ncoord; ++j) {
       int s = p.coord_src[j];
-      n = push_words_l(words, n, s >= 0 ? idx[s] : env[-1 - s]);
+      n = push_words_l(words, n, (s >= 0 ? idx[s] : env[-1 - s]) + p.coord_add[j]);
     }
     rt_pcg64 g;
     pcg64_seed(g, words, n);

@@ -20,13 +20,13 @@ RT_DEV int push_words(uint32_t* w, int n, int64_t v) {
 }
 
 RT_DEV int assemble_words(uint32_t* w, const uint32_t* prefix, int nprefix, const int32_t* src,
-                          int ncoord, const int64_t* idx, const int64_t* env) {
+                          int ncoord, const int64_t* idx, const int64_t* env, const int64_t* add) {
   int n = 0;
   for (int i = 0; i < nprefix; ++i) w[n++] = prefix[i];
   for (int j = 0; j < ncoord; ++j) {
     int s = src[j];
     int64_t c = s >= 0 ? idx[s] : env[-1 - s];
-    n = push_words(w, n, c);
+    n = push_words(w, n, c + add[j]);
   }
   return n;
 }
@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(128) k_rng(const __grid_constant__ rt_rng_para
   for (int64_t flat = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; flat < p.total;
        flat += (int64_t)gridDim.x * blockDim.x) {
     decompose(p.box, flat, idx);
-    int n = assemble_words(words, p.prefix, p.nprefix, p.coord_src, p.ncoord, idx, p.h.env);
+    int n = assemble_words(words, p.prefix, p.nprefix, p.coord_src, p.ncoord, idx, p.h.env,
+                           p.coord_add);
     rt_pcg64 g;
     pcg64_seed(g, words, n);
     int64_t o = view_off(p.out, p.box.nd, idx);
@@ -83,7 +84,8 @@ __global__ void __launch_bounds__(128) k_udf(const __grid_constant__ rt_udf_para
       int64_t o = view_off(p.in[k], p.box.nd, idx);
       base = base + pairwise_sum((const void*)p.in[k].ptr, p.in[k].dtype, o, c) / (double)c;
     }
-    int n = assemble_words(words, p.prefix, p.nprefix, p.coord_src, p.ncoord, idx, p.h.env);
+    int n = assemble_words(words, p.prefix, p.nprefix, p.coord_src, p.ncoord, idx, p.h.env,
+                           p.coord_add);
     rt_pcg64 g;
     pcg64_seed(g, words, n);
     for (int j = 0; j < p.nout; ++j) {

@@ -204,10 +204,51 @@ extern "C" int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* 
         ++pc;
         break;
       }
+      case RT_OP_HOOK:
+        return fail(RT_ERR_BAD_ARG, "program has host hooks: use rt_run_segment");
       default:
         return fail(RT_ERR_BAD_ARG, "bad program instruction");
     }
   }
+  return RT_OK;
+}
+
+extern "C" int rt_run_segment(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs,
+                              int32_t nrec, int64_t* env, int32_t nenv, uint64_t stream,
+                              int32_t* pc_io, int32_t* hook_out) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int pc = *pc_io;
+  while (pc < nprog) {
+    const rt_instr& in = prog[pc];
+    switch (in.op) {
+      case RT_OP_LAUNCH: {
+        int rc = launch_one(&recs[in.a], env, nenv, s);
+        if (rc) return rc;
+        ++pc;
+        break;
+      }
+      case RT_OP_FOR: {
+        bool empty = in.d > 0 ? (in.b >= in.c) : (in.b <= in.c);
+        if (empty) pc = in.e; else { env[in.a] = in.b; ++pc; }
+        break;
+      }
+      case RT_OP_END: {
+        const rt_instr& f = prog[in.a];
+        int64_t v = env[f.a] + f.d;
+        bool more = f.d > 0 ? (v < f.c) : (v > f.c);
+        if (more) { env[f.a] = v; pc = in.a + 1; } else ++pc;
+        break;
+      }
+      case RT_OP_HOOK:
+        *pc_io = pc + 1;
+        *hook_out = in.a;
+        return RT_HOOK;
+      default:
+        ++pc;
+        break;
+    }
+  }
+  *pc_io = nprog;
   return RT_OK;
 }
 

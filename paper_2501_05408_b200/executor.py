@@ -392,6 +392,8 @@ def find_absorbed_layouts(g: Graph, skip):
         outs = g.out_edges(n.id)
         if not outs or any(g.nodes[o.sink].kind not in ABSORB_CONSUMERS for o in outs):
             continue
+        if any(o.sink in skip for o in outs):
+            continue   # an alias of it would resolve to storage that never exists
         res.add(n.id)
     return res
 
@@ -443,7 +445,8 @@ def payload_shapes(g: Graph, benv):
 
 
 class Executable:
-    def __init__(self, g: Graph, benv: dict, seed: int, device: int, input_sig, fuse=True):
+    def __init__(self, g: Graph, benv: dict, seed: int, device: int, input_sig, fuse=True,
+                 shard=None, comm=None):
         torch = _torch()
         self.torch = torch
         self.g = g
@@ -458,6 +461,12 @@ class Executable:
         pshape = payload_shapes(g, benv)
         self.pshape = pshape
         self._check_vec()
+        self.shard = shard
+        self.comm = comm
+        self.shard_reduce = set()
+        if shard is not None:
+            from .shard import check_shardable
+            self.shard_reduce = check_shardable(g, shard.dim)
         an = analyze(g, benv, pshape, fuse)
         self.contract, self.plan, self.gemm_epi, self.fuse_src = (
             an["contract"], an["plan"], an["gemm_epi"], an["fuse_src"])
@@ -482,7 +491,8 @@ class Executable:
         self._set_ptrs(fake)
         low = Lowering(self.plan, self.bufs, self.status, seed, lambda nb: 0,
                        self.contract, self.fuse_src, self.gemm_epi,
-                       absorbed=self.absorbed).lower()
+                       absorbed=self.absorbed, shard=shard,
+                       shard_reduce=self.shard_reduce).lower()
         key_of = {v: k for k, v in fake.items()}
         rec_ptrs = []
         for ri, (_, p, *_r) in enumerate(low.recs):
@@ -514,7 +524,9 @@ class Executable:
         # pass 2: real pointers
         low = Lowering(self.plan, self.bufs, self.status, seed, self._scratch,
                        self.contract, self.fuse_src, self.gemm_epi,
-                       absorbed=self.absorbed).lower()
+                       absorbed=self.absorbed, shard=shard,
+                       shard_reduce=self.shard_reduce).lower()
+        self.hooks = low.hooks
         self._upload_loops(low)
         self.nrec = len(low.recs)
         self._params = [p for (_, p, _, _, _, _) in low.recs]
@@ -676,6 +688,8 @@ class Executable:
             s = stream or torch.cuda.current_stream(self.dev)
             self.upload_inputs(inputs, s)
             N.check(self.lib.rt_status_clear(self.status, s.cuda_stream), "status clear")
+            if self.hooks:
+                return self._run_with_hooks(s)
             if graph and not events and self.launch_count >= self.GRAPH_MIN_LAUNCHES:
                 self._ensure_graph(s)
                 if self.graph_exec is not None:
@@ -690,6 +704,26 @@ class Executable:
             rc = self.lib.rt_run(self.prog, self.nprog, self.recs, self.nrec, self.env,
                                  N.RT_MAXENV, s.cuda_stream, ev_arr, nev)
             N.check(rc, "rt_run")
+
+    def _run_with_hooks(self, s):
+        """Sharded run: program segments between all-reduce hooks."""
+        torch = self.torch
+        for i in range(N.RT_MAXENV):
+            self.env[i] = 0
+        pc, hook = N.i32(0), N.i32(-1)
+        while True:
+            rc = self.lib.rt_run_segment(self.prog, self.nprog, self.recs, self.nrec, self.env,
+                                         N.RT_MAXENV, s.cuda_stream, C.byref(pc), C.byref(hook))
+            if rc == 0:
+                return
+            if rc != N.RT_HOOK:
+                N.check(rc, "rt_run_segment")
+            h = self.hooks[hook.value]
+            off = h["off0"] + sum(self.env[k] * v for k, v in h["off_env"].items())
+            item = ITEMSIZE_OF[h["dtype"]]
+            t = _wrap_ptr(torch, h["ptr"] + off * item, h["count"] * item, self.dev)
+            t = t.view(_TORCH_DT[h["dtype"]])
+            self.comm.allreduce_(t)
 
     def profile(self, inputs, stream=None):
         """One run with an event pair around every launch: per-record device
@@ -813,6 +847,7 @@ class Executable:
 
 
 _TORCH_DT = None
+ITEMSIZE_OF = {"f64": 8, "f32": 4, "i64": 8, "bool": 1}
 
 
 def _u8view(torch, ptr, nbytes, dev):
@@ -936,7 +971,7 @@ def _input_sig(inputs):
     return tuple(sig)
 
 
-def get_executable(g, bounds=None, inputs=None, seed=0, device=None):
+def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None, comm=None):
     global _TORCH_DT
     torch = _torch()
     if _TORCH_DT is None:
@@ -947,14 +982,17 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None):
     if dyn:
         benv = _resolve_dynamic(graph, benv, dyn, inputs, seed, device)
     dev = torch.cuda.current_device() if device is None else int(device)
-    key = (id(g), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs))
+    key = (id(g), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs), shard)
     ex = _CACHE.get(key)
     if ex is not None and ex[0]() is g:
         return ex[1], benv
     h = copy_graph(graph)
     inline_dataflow(h, benv)
     eliminate_dead(h)
-    exe = Executable(h, benv, int(seed), dev, _input_sig(inputs))
+    if shard is not None and comm is None:
+        from .shard import TorchComm
+        comm = TorchComm()
+    exe = Executable(h, benv, int(seed), dev, _input_sig(inputs), shard=shard, comm=comm)
     try:
         _CACHE[key] = (weakref.ref(g), exe)
     except TypeError:
@@ -1007,9 +1045,14 @@ def _resolve_dynamic(g: Graph, benv, dyn, inputs, seed, device):
 
 
 def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=None,
-            device_outputs=False, stream=None):
-    """Drop-in for reference `reference_execute` (runtime.py:460-475)."""
-    exe, benv = get_executable(g, bounds, inputs, seed, device)
+            device_outputs=False, stream=None, shard=None, comm=None):
+    """Drop-in for reference `reference_execute` (runtime.py:460-475).
+
+    shard=ShardSpec(dim, rank, world): this process runs envs
+    [rank*B, (rank+1)*B) of a G-way env-sharded run (bounds give the local
+    extent B); reductions over the dim are all-reduced through `comm`
+    (default: torch.distributed)."""
+    exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm)
     exe.run(inputs or {}, stream)
     exe.check_status(stream)
     outs = exe.outputs(device_outputs)

@@ -242,7 +242,8 @@ class Ctx:
 
 class Lowering:
     def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None,
-                 fuse_src=None, gemm_epi=None, persistent=True, use_tc=True, absorbed=None):
+                 fuse_src=None, gemm_epi=None, persistent=True, use_tc=True, absorbed=None,
+                 shard=None, shard_reduce=None):
         self.plan = plan
         self.g = plan.graph
         self.benv = plan.benv
@@ -262,6 +263,9 @@ class Lowering:
         self.virtual |= self.absorbed
         self.persistent = persistent
         self.use_tc = use_tc
+        self.shard = shard
+        self.shard_reduce = set(shard_reduce or ())
+        self.hooks = []                        # all-reduce hooks (sharded reductions)
         self._capture = None
         self.loop_subs = {}                    # loop record -> sub-op descriptors
         self.fuse_src = dict(fuse_src or {})   # producer nid -> consumer nid (inlined)
@@ -480,6 +484,8 @@ class Lowering:
             return None
         fixed = tuple(s.fixed) + (s.dim,)
         body = {b.nid for b in s.body}
+        if body & self.shard_reduce:
+            return None
         slabs = set()
         for b in s.body:
             n = self.g.nodes[b.nid]
@@ -578,6 +584,7 @@ class Lowering:
                     q.coord_src[j] = S.index(d)
                 else:
                     q.coord_src[j] = -1 - self.slot[d]
+            self._coord_add(q, udf)
             q.dist = 0
             q.count = count
             q.out.ptr = buf
@@ -639,13 +646,33 @@ class Lowering:
             return
         if n.id in self.gemm_epi:
             x, bias_e, tanh = self.gemm_epi[n.id]
-            return self.k_matmul(ctx, self.g.nodes[x], bias_e, 1 if tanh else 0)
-        fn = getattr(self, f"k_{n.kind}", None)
-        if fn is None:
-            if n.kind in EW_KINDS:
-                return self.ew(ctx)
-            raise LowerError(f"no kernel for op kind {n.kind!r}")
-        return fn(ctx)
+            self.k_matmul(ctx, self.g.nodes[x], bias_e, 1 if tanh else 0)
+        else:
+            fn = getattr(self, f"k_{n.kind}", None)
+            if fn is None:
+                if n.kind not in EW_KINDS:
+                    raise LowerError(f"no kernel for op kind {n.kind!r}")
+                fn = self.ew
+            fn(ctx)
+        if n.id in self.shard_reduce:
+            self._hook_allreduce(ctx, (n.id, 0))
+
+    def _hook_allreduce(self, ctx, key):
+        """Partial sums over the sharded env dim -> sum all-reduce of the
+        slab this launch wrote (contiguous by construction of the layout)."""
+        if self._capture is not None:
+            raise LowerError("sharded reduction inside a persistent loop")
+        v = self.out_view(ctx, key)
+        box = list(ctx.slab_ext) + list(self.bufs[key].pshape)
+        want = cstrides(box)
+        if any(v.stride[i] != want[i] for i in range(len(box)) if box[i] > 1):
+            raise LowerError("all-reduced slab is not contiguous")
+        st = self.storage(key)
+        self.hooks.append({"ptr": st.ptr, "dtype": st.dtype, "off0": v.off,
+                           "off_env": {i: v.off_env[i] for i in range(N.RT_MAXENV)
+                                       if v.off_env[i]},
+                           "count": prod(box), "node": ctx.node.name})
+        self.prog.append((N.RT_OP_HOOK, len(self.hooks) - 1, 0, 0, 0, 0))
 
     # ---- elementwise family
 
@@ -1427,6 +1454,14 @@ class Lowering:
                 src.append(ctx.slab.index(d))
         return src
 
+    def _coord_add(self, p, n):
+        """Entropy uses GLOBAL env indices when envs are sharded."""
+        if self.shard is None:
+            return
+        for j, d in enumerate(n.domain):
+            if d == self.shard.dim:
+                p.coord_add[j] = self.shard.offset(self.ext[d])
+
     @staticmethod
     def words(v):
         if v < 0:
@@ -1459,6 +1494,7 @@ class Lowering:
         p.ncoord = len(cs)
         for i, c in enumerate(cs):
             p.coord_src[i] = c
+        self._coord_add(p, n)
         p.dist = 0 if n.params["dist"] == "normal" else 1
         p.count = prod(self.bufs[key].pshape)
         p.out = self.out_view(ctx, key)
@@ -1484,6 +1520,7 @@ class Lowering:
         p.ncoord = len(cs)
         for i, c in enumerate(cs):
             p.coord_src[i] = c
+        self._coord_add(p, n)
         p.salt = zlib.crc32(spec.name.encode()) % 997 / 997.0
         ins = self.g.in_edges(n.id)
         if len(ins) > 4 or len(n.out_shapes) > 4:

@@ -29,7 +29,8 @@ RT_K_LOOP = 9
 RT_K_GEMM_TC = 10
 TC_SMEM = 2 * (2 * 128 * 16 * 4 + 2 * 256 * 16 * 4)
 
-RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT = 1, 2, 3, 4
+RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK = 1, 2, 3, 4, 6
+RT_HOOK = 100
 
 RT_ERR_ROW_RANGE, RT_ERR_SLICE_RANGE = 1, 2
 
@@ -99,13 +100,13 @@ class rt_splitk_params(C.Structure):
 class rt_rng_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("box", rt_box), ("total", i64), ("nprefix", i32),
                 ("ncoord", i32), ("prefix", u32 * 8), ("coord_src", i32 * RT_MAXD),
-                ("dist", i32), ("count", i32), ("out", rt_view)]
+                ("coord_add", i64 * RT_MAXD), ("dist", i32), ("count", i32), ("out", rt_view)]
 
 
 class rt_udf_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("box", rt_box), ("total", i64), ("nprefix", i32),
                 ("ncoord", i32), ("prefix", u32 * 8), ("coord_src", i32 * RT_MAXD),
-                ("salt", f64), ("nin", i32), ("nout", i32), ("in_count", i32 * 4),
+                ("coord_add", i64 * RT_MAXD), ("salt", f64), ("nin", i32), ("nout", i32), ("in_count", i32 * 4),
                 ("out_count", i32 * 4), ("out_kind", i32 * 4), ("in_", rt_view * 4),
                 ("out", rt_view * 4)]
 
@@ -154,6 +155,8 @@ def lib():
     L.rt_launch.argtypes = [C.POINTER(rt_launch_rec), C.POINTER(i64), i32, u64]
     L.rt_run.argtypes = [C.POINTER(rt_instr), i32, C.POINTER(rt_launch_rec), i32,
                          C.POINTER(i64), i32, u64, C.POINTER(u64), i32]
+    L.rt_run_segment.argtypes = [C.POINTER(rt_instr), i32, C.POINTER(rt_launch_rec), i32,
+                                 C.POINTER(i64), i32, u64, C.POINTER(i32), C.POINTER(i32)]
     L.rt_graph_capture.argtypes = [C.POINTER(rt_instr), i32, C.POINTER(rt_launch_rec), i32,
                                    C.POINTER(i64), i32, u64, C.POINTER(u64)]
     L.rt_graph_launch.argtypes = [u64, u64]
@@ -179,7 +182,7 @@ def lib():
 EXPORTS = ("rt_version", "rt_launch", "rt_run", "rt_status_alloc", "rt_status_read",
            "rt_status_clear", "rt_status_free", "rt_memcpy_d2h_async", "rt_memcpy_h2d_async",
            "rt_rng_fill", "rt_last_error", "rt_graph_capture", "rt_graph_launch",
-           "rt_graph_destroy", "rt_profile", "rt_graph_capture_ev")
+           "rt_graph_destroy", "rt_profile", "rt_graph_capture_ev", "rt_run_segment")
 
 
 def check(rc: int, what: str = ""):

@@ -1,0 +1,93 @@
+"""Env sharding across GPUs.
+
+Within one training iteration every (b, t) node reads only its own env b;
+the only cross-env dependences are full-range reductions over b (the
+REINFORCE/PPO objective and gradient sums, e.g. reference
+pkg/programs/reinforce.rtl:29-31 `it[i] = sum(ep[i,0:B])`).  So the env dim
+shards into contiguous blocks of B/G per rank with:
+
+  * per-point RNG keyed by the GLOBAL env index (rank * B_local + b), so the
+    draws — and hence the results — do not depend on G;
+  * a sum all-reduce (NCCL over NVLink on GPUs) of each reduction over b,
+    right after the kernel that produced the local partial sum; everything
+    downstream of those reductions (parameter updates) is replicated.
+
+`check_shardable` proves the graph fits that shape or explains why not.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import ir
+
+
+class ShardError(Exception):
+    pass
+
+
+@dataclass(frozen=True)
+class ShardSpec:
+    dim: str             # the sharded loop dim (envs)
+    rank: int
+    world: int
+
+    def offset(self, local_extent: int) -> int:
+        return self.rank * local_extent
+
+
+def _mentions(e, d) -> bool:
+    return (d, "loop") in ir.free_syms(e)
+
+
+def check_shardable(g: ir.Graph, d: str) -> set:
+    """Node ids whose outputs are partial sums over d (need an all-reduce).
+    Raises ShardError when some dependence crosses envs otherwise."""
+    bound = g.dim_bound[d]
+    reduce_nodes = set()
+    for n in g.sorted_nodes():
+        vec = [s.name for s in n.params.get("vec", ())]
+        if d in vec:
+            raise ShardError(f"{n.name}: dim {d} is folded into a payload axis")
+        if n.kind == "merge" and any(_mentions(c, d) for c in n.params["conds"]):
+            raise ShardError(f"{n.name}: branch condition depends on {d}")
+        if n.kind == "eval_symbol" and n.params["symbol"].name == d:
+            raise ShardError(f"{n.name}: reads the value of {d}")
+        if n.kind in ("index_select", "window_reduce", "slice_axis", "scan") and \
+                getattr(n.params.get("dim"), "name", None) == d:
+            raise ShardError(f"{n.name}: {n.kind} along {d}")
+    for e in g.edges:
+        src, snk = g.nodes[e.src], g.nodes[e.sink]
+        if e.psi is not None and _mentions(e.psi, d):
+            raise ShardError(f"{snk.name}: edge condition depends on {d}")
+        if d not in src.domain:
+            continue
+        c = e.phi[src.domain.index(d)]
+        if d in snk.domain:
+            if c != ("sym", d, "loop"):
+                raise ShardError(f"{snk.name} reads {src.name} at {ir.expr_text(c)} along {d}")
+            continue
+        full = c == ("slice", ("int", 0), ("sym", bound, "bound"))
+        if not full:
+            raise ShardError(f"{snk.name} reads {src.name}[{ir.expr_text(c)}] across envs")
+        if snk.kind != "sum":
+            raise ShardError(f"{snk.name}: {snk.kind} over all envs is not a sum")
+        slice_axes = [j for j, cc in enumerate(e.phi) if cc[0] == "slice"]
+        ax = slice_axes.index(src.domain.index(d))
+        if ax not in tuple(snk.params["dims"]):
+            raise ShardError(f"{snk.name}: gathers {src.name} over envs without reducing")
+        reduce_nodes.add(snk.id)
+    return reduce_nodes
+
+
+class TorchComm:
+    """Sum all-reduce through torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def allreduce_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t

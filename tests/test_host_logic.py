@@ -95,3 +95,39 @@ def test_interval_and_refine():
     assert P.interval(("sub", ("sym", "t", "loop"), ("int", 1)), box) == (-1, 8)
     assert P.refine_box(("ge", ("sym", "t", "loop"), ("int", 1)), box) == {"t": (1, 9)}
     assert P.refine_box(("lt", ("sym", "t", "loop"), ("int", 0)), box) is None
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_every_touched_buffer_is_materialised(case):
+    """No launch may address a buffer that the analysis decided never to
+    allocate (fused, absorbed or contracted nodes), directly or via aliases."""
+    from paper_2501_05408_b200 import memplan
+    g = case.graph()
+    benv = {g.dim_bound[d]: (case.resolved_bounds or {}).get(g.dim_bound[d],
+                                                               g.bindings.get(g.dim_bound[d]))
+            for d in g.dim_order}
+    h = X.copy_graph(g)
+    X.inline_dataflow(h, benv)
+    X.eliminate_dead(h)
+    pshape = X.payload_shapes(h, benv)
+    an = X.analyze(h, benv, pshape, True)
+    bufs = an["bufs"]
+    roots = [k for k, b in bufs.items() if b.alias is None and k[0] not in an["virtual"]]
+    fake = {k: (i + 1) << 44 for i, k in enumerate(roots)}
+    for i, k in enumerate(bufs):
+        bufs[k].ptr = (0x7000 + i) << 32          # never-allocated sentinel
+    for k, p in fake.items():
+        bufs[k].ptr = p
+    for k, b in bufs.items():
+        r = b
+        while r.alias is not None:
+            r = bufs[r.alias]
+        b.ptr = r.ptr
+    low = L.Lowering(an["plan"], bufs, 0, 0, lambda nb: 1 << 60, an["contract"], an["fuse_src"],
+                     an["gemm_epi"], absorbed=an["absorbed"]).lower()
+    valid = set(fake.values()) | {1 << 60}
+    for ri, (kind, p, *_r) in enumerate(low.recs):
+        ptrs = memplan.touched_ptrs(p)
+        for op in low.loop_subs.get(ri, {}).get("ops", ()):
+            ptrs |= memplan.touched_ptrs(op[1])
+        assert ptrs <= valid, (ri, [hex(x) for x in ptrs - valid])
