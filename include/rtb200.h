@@ -26,7 +26,19 @@
 #ifndef RTB200_H
 #define RTB200_H
 
+#ifdef __CUDACC_RTC__   /* NVRTC: no libc headers */
+typedef signed char int8_t;
+typedef short int16_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long long uintptr_t;
+#else
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -282,6 +294,7 @@ typedef struct {
   int32_t block[3];
   int32_t smem;
   int32_t _pad;
+  uint64_t jit_fn;     /* CUfunction specialised for this record (0: library kernel) */
 } rt_launch_rec;
 
 /* Program instructions for rt_run. */
@@ -308,6 +321,7 @@ typedef struct {
 } rt_instr;
 
 /* ---- entry points ------------------------------------------------------ */
+#ifndef __CUDACC_RTC__
 
 int rt_version(void);
 /* Launch one kernel family with `rec`, patching env[0..nenv) into its header. */
@@ -333,6 +347,16 @@ int rt_graph_destroy(uint64_t graph_exec);
  * record: total device ms and instance count.  Synchronises the stream. */
 int rt_profile(const rt_instr* prog, int32_t nprog, const rt_launch_rec* recs, int32_t nrec,
                int64_t* env, int32_t nenv, uint64_t stream, double* rec_ms, int64_t* rec_count);
+/* Compile CUDA source with NVRTC for sm_100a and load kernel `name`; the
+ * CUfunction handle is returned in *fn_out (module kept for the process).
+ * opts: NUL-separated option strings (count nopt).  On failure the NVRTC log
+ * is available from rt_last_error(). */
+int rt_jit_compile(const char* src, const char* name, const char* opts, int32_t nopt,
+                   uint64_t* fn_out);
+/* Load a previously compiled cubin image and fetch kernel `name`. */
+int rt_jit_load(const void* image, const char* name, uint64_t* fn_out);
+/* Compile to a cubin image (for an on-disk cache); *size in/out. */
+int rt_jit_cubin(const char* src, const char* opts, int32_t nopt, void* out, uint64_t* size);
 /* Device status word: int32[4] = {code, node, aux0, aux1}; allocate/clear/read. */
 int rt_status_alloc(uint64_t* dev_ptr);
 int rt_status_read(uint64_t dev_ptr, int32_t* host4, uint64_t stream);
@@ -347,6 +371,7 @@ int rt_rng_fill(uint64_t dev_out, const uint32_t* prefix, int32_t nprefix,
                 const int64_t* coords, int32_t ncoord, int64_t rows, int32_t count,
                 int32_t dist, uint64_t stream);
 const char* rt_last_error(void);
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,9 @@
 // numpy binary (tools/gen_ziggurat_tables.py).  Validated against numpy in
 // tests/test_rng.py (C oracle) and tests/test_gpu_parity.py (device).
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#endif
 #include "ziggurat_tables.h"
 
 #define SS_INIT_A 0x43b0d7e5u

@@ -1,7 +1,9 @@
 // C-ABI runtime: kernel table, launch with env patching, the loop-nest
 // program interpreter (the executor loop that replaces the reference's
 // demand-driven recursion, runtime.py:285-475), status word, tier moves.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvrtc.h>
 #include <stdio.h>
 #include <string.h>
 #include <string>
@@ -21,6 +23,39 @@ extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 
 static thread_local std::string g_err;
+
+// Driver API entry points resolved through the runtime, so the library loads
+// (and its CPU-side tests run) on machines without libcuda.so.
+struct DriverApi {
+  decltype(&cuModuleLoadData) moduleLoadData = nullptr;
+  decltype(&cuModuleGetFunction) moduleGetFunction = nullptr;
+  decltype(&cuLaunchKernel) launchKernel = nullptr;
+  decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
+  decltype(&cuGetErrorString) getErrorString = nullptr;
+  bool ok = false;
+};
+
+static DriverApi& drv() {
+  static DriverApi d;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    bool all = true;
+#define RT_GET(field, name)                                                              \
+    if (cudaGetDriverEntryPoint(name, (void**)&d.field, cudaEnableDefault, &q) != cudaSuccess || \
+        q != cudaDriverEntryPointSuccess)                                                  \
+      all = false;
+    RT_GET(moduleLoadData, "cuModuleLoadData")
+    RT_GET(moduleGetFunction, "cuModuleGetFunction")
+    RT_GET(launchKernel, "cuLaunchKernel")
+    RT_GET(funcSetAttribute, "cuFuncSetAttribute")
+    RT_GET(getErrorString, "cuGetErrorString")
+#undef RT_GET
+    d.ok = all;
+  }
+  return d;
+}
 
 static int fail(int code, const char* what) {
   g_err = what;
@@ -136,6 +171,21 @@ static int launch_one(const rt_launch_rec* rec, const int64_t* env, int nenv, cu
   void* args[1] = {blk};
   dim3 g(rec->grid[0], rec->grid[1] > 0 ? rec->grid[1] : 1, rec->grid[2] > 0 ? rec->grid[2] : 1);
   dim3 b(rec->block[0], rec->block[1] > 0 ? rec->block[1] : 1, rec->block[2] > 0 ? rec->block[2] : 1);
+  if (rec->jit_fn) {
+    DriverApi& D = drv();
+    if (!D.ok) return fail(RT_ERR_CUDA, "driver API unavailable");
+    CUfunction f = (CUfunction)rec->jit_fn;
+    if (rec->smem > 48 * 1024)
+      D.funcSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, rec->smem);
+    CUresult r = D.launchKernel(f, g.x, g.y, g.z, b.x, b.y, b.z, rec->smem, (CUstream)s, args,
+                                nullptr);
+    if (r != CUDA_SUCCESS) {
+      const char* m = nullptr;
+      D.getErrorString(r, &m);
+      return fail(RT_ERR_CUDA, m ? m : "cuLaunchKernel failed");
+    }
+    return RT_OK;
+  }
   if (rec->smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, rec->smem);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
@@ -423,4 +473,80 @@ extern "C" int rt_profile(const rt_instr* prog, int32_t nprog, const rt_launch_r
     rec_count[x.first] += 1;
   }
   return RT_OK;
+}
+
+// ------------------------------------------------------------ JIT
+// Fused elementwise programs and persistent loop bodies are compiled to
+// straight-line CUDA at executable-build time (the interpreter VM stays as
+// the reference semantics and the fallback for the library kernels).
+
+static std::vector<std::string> split_opts(const char* opts, int nopt) {
+  std::vector<std::string> v;
+  const char* p = opts;
+  for (int i = 0; i < nopt; ++i) {
+    v.emplace_back(p);
+    p += v.back().size() + 1;
+  }
+  return v;
+}
+
+static int nvrtc_build(const char* src, const char* opts, int nopt, std::string& image) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src, "rtb200_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    return fail(RT_ERR_CUDA, "nvrtcCreateProgram failed");
+  std::vector<std::string> o = split_opts(opts, nopt);
+  std::vector<const char*> po;
+  for (auto& x : o) po.push_back(x.c_str());
+  nvrtcResult r = nvrtcCompileProgram(prog, (int)po.size(), po.data());
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    g_err = "nvrtc: " + log;
+    return RT_ERR_CUDA;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  image.resize(n);
+  nvrtcGetCUBIN(prog, &image[0]);
+  nvrtcDestroyProgram(&prog);
+  return RT_OK;
+}
+
+extern "C" int rt_jit_load(const void* image, const char* name, uint64_t* fn_out) {
+  cudaFree(0);  // make sure the primary context is current
+  DriverApi& D = drv();
+  if (!D.ok) return fail(RT_ERR_CUDA, "driver API unavailable");
+  CUmodule mod;
+  CUresult r = D.moduleLoadData(&mod, image);
+  if (r != CUDA_SUCCESS) {
+    const char* m = nullptr;
+    D.getErrorString(r, &m);
+    return fail(RT_ERR_CUDA, m ? m : "cuModuleLoadData failed");
+  }
+  CUfunction f;
+  r = D.moduleGetFunction(&f, mod, name);
+  if (r != CUDA_SUCCESS) return fail(RT_ERR_CUDA, "cuModuleGetFunction failed");
+  *fn_out = (uint64_t)f;
+  return RT_OK;
+}
+
+extern "C" int rt_jit_cubin(const char* src, const char* opts, int32_t nopt, void* out,
+                            uint64_t* size) {
+  std::string image;
+  int rc = nvrtc_build(src, opts, nopt, image);
+  if (rc) return rc;
+  if (out && *size >= image.size()) memcpy(out, image.data(), image.size());
+  *size = image.size();
+  return RT_OK;
+}
+
+extern "C" int rt_jit_compile(const char* src, const char* name, const char* opts, int32_t nopt,
+                              uint64_t* fn_out) {
+  std::string image;
+  int rc = nvrtc_build(src, opts, nopt, image);
+  if (rc) return rc;
+  return rt_jit_load(image.data(), name, fn_out);
 }

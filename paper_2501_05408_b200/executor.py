@@ -543,6 +543,8 @@ class Executable:
         self.recs = recs
         self.labels = [lab for (*_, lab) in low.recs]
         self.kernels = [k for (k, *_rest) in low.recs]
+        from . import jit
+        self.jit_count = jit.specialise(recs, self.kernels, self._params, self.labels)
         prog = (N.rt_instr * max(1, len(low.prog)))()
         for i, ins in enumerate(low.prog):
             prog[i].op, prog[i].a, prog[i].b, prog[i].c, prog[i].d, prog[i].e = (

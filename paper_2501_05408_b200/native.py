@@ -125,7 +125,7 @@ class rt_loop_params(C.Structure):
 
 class rt_launch_rec(C.Structure):
     _fields_ = [("kernel", i32), ("param_bytes", i32), ("params", u64), ("grid", i32 * 3),
-                ("block", i32 * 3), ("smem", i32), ("_pad", i32)]
+                ("block", i32 * 3), ("smem", i32), ("_pad", i32), ("jit_fn", u64)]
 
 
 class rt_instr(C.Structure):
@@ -166,6 +166,9 @@ def lib():
     L.rt_profile.argtypes = [C.POINTER(rt_instr), i32, C.POINTER(rt_launch_rec), i32,
                              C.POINTER(i64), i32, u64, C.POINTER(f64), C.POINTER(i64)]
     L.rt_graph_destroy.argtypes = [u64]
+    L.rt_jit_compile.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, i32, C.POINTER(u64)]
+    L.rt_jit_load.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(u64)]
+    L.rt_jit_cubin.argtypes = [C.c_char_p, C.c_char_p, i32, C.c_void_p, C.POINTER(u64)]
     L.rt_status_alloc.argtypes = [C.POINTER(u64)]
     L.rt_status_read.argtypes = [u64, C.POINTER(i32), u64]
     L.rt_status_clear.argtypes = [u64, u64]
@@ -182,7 +185,8 @@ def lib():
 EXPORTS = ("rt_version", "rt_launch", "rt_run", "rt_status_alloc", "rt_status_read",
            "rt_status_clear", "rt_status_free", "rt_memcpy_d2h_async", "rt_memcpy_h2d_async",
            "rt_rng_fill", "rt_last_error", "rt_graph_capture", "rt_graph_launch",
-           "rt_graph_destroy", "rt_profile", "rt_graph_capture_ev", "rt_run_segment")
+           "rt_graph_destroy", "rt_profile", "rt_graph_capture_ev", "rt_run_segment",
+           "rt_jit_compile", "rt_jit_load", "rt_jit_cubin")
 
 
 def check(rc: int, what: str = ""):

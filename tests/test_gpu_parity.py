@@ -72,3 +72,20 @@ def test_index_select_error_maps_to_runtime_error():
     g.outputs = [("y", 1, 0)]
     with pytest.raises(RuntimeError_, match="row 4 outside"):
         execute(g, inputs={"x": np.arange(4.0)})
+
+
+JIT_CASES = ["mlp_f32_I2B3T5", "mlp_f64_I2B3T5", "corpus_reinforce_plain_s3", "kat_if_order_plain",
+             "corpus_checkpoint_vecfuse_s3", "corpus_epoch_minibatch_vec_s3", "tr_widesum_inc7",
+             "corpus_stream_window_plain_s3", "kat_flag_plain", "corpus_gated_value_vec_s3"]
+
+
+@pytest.mark.parametrize("name", JIT_CASES)
+def test_jit_specialised_kernels_match_reference(name, monkeypatch):
+    """Every elementwise launch JIT-compiled (NVRTC, straight-line CUDA)
+    gives the same results as the reference."""
+    from paper_2501_05408_b200 import execute, jit
+    monkeypatch.setattr(jit, "JIT_MIN_ELEMS", 0)
+    c = load_case(name)
+    outs = execute(c.graph(), bounds=c.bounds, inputs=c.inputs, seed=c.seed)
+    for k, want in c.outputs.items():
+        assert_close(outs[k], want, k)
