@@ -123,18 +123,25 @@ RT_DEV void load_a(const T* ak, T (&a)[MRP]) {
   }
 }
 
-// chunk loop + epilogue with the padded row count MRP known at compile time
-template <typename T, int MRP>
-RT_DEV bool tma_body(const rt_gemm_params& p, const T* As, const T* Bg, int64_t K, int64_t Nn,
+// chunk loop + epilogue with the padded row count MRP and the columns per
+// thread NC known at compile time; k unrolled by 4 with loads batched ahead
+// of the FMAs (the loop is issue/latency bound, not bandwidth bound).
+template <typename T, int MRP, int NC>
+RT_DEV void tma_body(const rt_gemm_params& p, const T* As, const T* Bg, int64_t K, int64_t Nn,
                      int64_t kc, int64_t nch, int mr, int64_t m0, int64_t coff, int64_t biasoff,
                      loop_ring& ring) {
-  constexpr int NC = 4;   // columns per thread (Nn <= 4 * blockDim)
   const int nn = (int)Nn;
   T acc[NC][MRP];
 #pragma unroll
   for (int j = 0; j < NC; ++j)
 #pragma unroll
     for (int r = 0; r < MRP; ++r) acc[j][r] = (T)0;
+  int col[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    col[j] = (int)threadIdx.x + j * (int)blockDim.x;
+    if (col[j] >= nn) col[j] = nn - 1;   // duplicate work, never stored
+  }
   auto issue = [&](int c) {
     uint32_t st = (ring.seq + (uint32_t)c) % RING;
     int64_t k0 = (int64_t)c * kc;
@@ -151,17 +158,31 @@ RT_DEV bool tma_body(const rt_gemm_params& p, const T* As, const T* Bg, int64_t 
     const int k0 = c * (int)kc;
     const int rows = (int)min(kc, K - (int64_t)k0);
     const T* ak = As + (size_t)k0 * MRP;
-    for (int kk = 0; kk < rows; ++kk, ak += MRP) {
+    int kk = 0;
+    for (; kk + 4 <= rows; kk += 4, ak += 4 * MRP) {
+      T b[4][NC];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) b[u][j] = Bs[(kk + u) * nn + col[j]];
+      T a[4][MRP];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_a<T, MRP>(ak + u * MRP, a[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+#pragma unroll
+          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+    }
+    for (; kk < rows; ++kk, ak += MRP) {
       T a[MRP];
       load_a<T, MRP>(ak, a);
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
-        const int n = (int)threadIdx.x + j * (int)blockDim.x;
-        if (n < nn) {
-          const T b = Bs[kk * nn + n];
+        const T bb = Bs[kk * nn + col[j]];
 #pragma unroll
-          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[r], b, acc[j][r]);
-        }
+        for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[r], bb, acc[j][r]);
       }
     }
     __syncthreads();   // everyone is done with stage st
@@ -182,7 +203,15 @@ RT_DEV bool tma_body(const rt_gemm_params& p, const T* As, const T* Bg, int64_t 
       store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + cn, v);
     }
   }
-  return true;
+}
+
+template <typename T, int MRP>
+RT_DEV void tma_body_nc(const rt_gemm_params& p, const T* As, const T* Bg, int64_t K, int64_t Nn,
+                        int64_t kc, int64_t nch, int mr, int64_t m0, int64_t coff,
+                        int64_t biasoff, loop_ring& ring) {
+  const int nc = (int)((Nn + blockDim.x - 1) / blockDim.x);
+  if (nc <= 1 || sizeof(T) == 8) tma_body<T, MRP, 1>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
+  else tma_body<T, MRP, 2>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
 }
 
 template <typename T>
@@ -194,8 +223,9 @@ RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m
       p.B.s2[0] != 1 || p.B.s1[0] != Nn || p.Z.nd > 1)
     return false;
   const int64_t kc = ring.stage_bytes / (Nn * (int64_t)sizeof(T));
-  if (kc < 1 || Nn < 64 || Nn > 4 * (int64_t)blockDim.x) return false;
   const int mr = (int)(m1 - m0);
+  if (kc < 1 || Nn < 64 || mr > 8 || Nn > (sizeof(T) == 8 ? 1 : 2) * (int64_t)blockDim.x)
+    return false;
   const int mrp = (mr + 3) & ~3;                           // rows padded to a multiple of 4
   T* As = (T*)smem;                                        // k-major: As[k * mrp + r]
   const int64_t aoff = fold_gop_off(p.A, env);
@@ -226,13 +256,8 @@ RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m
     }
   }
   __syncthreads();
-  bool ok = false;
-  switch (mrp) {
-    case 4: ok = tma_body<T, 4>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
-    case 8: ok = tma_body<T, 8>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
-    case 12: ok = tma_body<T, 12>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
-    default: ok = tma_body<T, 16>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring); break;
-  }
+  if (mrp <= 4) tma_body_nc<T, 4>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
+  else tma_body_nc<T, 8>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
   ring.seq += (uint32_t)nch;
   return true;
 }

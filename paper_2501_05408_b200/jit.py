@@ -217,7 +217,9 @@ _FN_CACHE: dict = {}
 
 
 def _opts():
-    return [b"-arch=sm_100a", b"-std=c++17", b"-lineinfo",
+    # -fmad=false: each elementwise op rounds like the reference's numpy ops
+    # (no contraction of a*b+c across program statements)
+    return [b"-arch=sm_100a", b"-std=c++17", b"-lineinfo", b"-fmad=false",
             b"-I" + os.path.join(HERE, "csrc").encode()]
 
 
