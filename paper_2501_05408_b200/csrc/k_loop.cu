@@ -1,485 +1,7 @@
-// RT_K_LOOP — a whole row-local loop in one persistent launch.
-//
-// The reference runs a recurrence such as the acting loop
-//     o[b,t] -> policy MLP -> a[b,t] -> env -> o[b,t+1]
-// one (node, point) at a time (runtime.py:344-389).  The planner turns it
-// into a loop over t whose body evaluates every node for all envs b; here
-// that whole loop is ONE kernel: each CTA owns a block of rows (envs) and
-// steps through t itself, running every body op on its rows with a
-// __syncthreads between ops.  Rows never read other rows (checked by the
-// planner), so no grid-wide synchronisation is needed and the per-step cost
-// is the ops' latency, not ~6 kernel launches.
-//
-// Ops: the EW program VM, a row-block GEMM (+bias, tanh) streaming the
-// weights from L2, the synthetic env (with its normals pre-drawn by an RNG
-// launch hoisted out of the loop), and per-row RNG draws.
-#include "common.cuh"
-#include "rng.cuh"
-
-#define LOOP_THREADS 256
-#define LOOP_MAXR 16   // max GEMM rows held per thread (rows_per_cta * m)
-
-RT_DEV int64_t fold_gop_off(const rt_gop& g, const int64_t* env) {
-  int64_t o = g.off;
-  for (int e = 0; e < RT_MAXENV; ++e) o += env[e] * g.off_env[e];
-  return o;
-}
-
-RT_DEV int64_t gdec32(const rt_gbox& b, int64_t flat, const int64_t* s) {
-  uint32_t f = (uint32_t)flat;
-  int64_t o = 0;
-  for (int d = b.nd - 1; d >= 0; --d) {
-    uint32_t e = (uint32_t)b.ext[d];
-    uint32_t q = f / e;
-    o += (int64_t)(f - q * e) * s[d];
-    f = q;
-  }
-  return o;
-}
-
-
-// ---------------------------------------------------------------- TMA bulk
-// 1-D bulk async copies global -> shared with mbarrier completion (sm_90+;
-// UBLKCP in SASS), used to stream dense weight panels through a smem ring.
-
-RT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-RT_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-RT_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes) : "memory");
-}
-
-RT_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-
-RT_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
-  }
-}
-
-#define RING 4
-
-struct loop_ring {
-  uint64_t* bar;       // [RING] mbarriers
-  unsigned char* buf;  // [RING][stage_bytes]
-  uint32_t stage_bytes;
-  uint32_t seq;        // chunks consumed so far (uniform across the CTA)
-};
-
-// ---------------------------------------------------------------- EW rows
-
-template <typename T>
-RT_DEV void ew_rows(const rt_ew_params& p, const int64_t* env, int64_t f0, int64_t f1,
-                    rt_fold* sfold) {
-  // fold every view once per step (thread i -> view i; slot 0 = output)
-  const int nv = p.nin + 1;
-  if (threadIdx.x < nv) sfold[threadIdx.x] = fold_of(threadIdx.x == 0 ? p.out : p.in[threadIdx.x - 1], env);
-  __syncthreads();
-  int64_t idx[RT_MAXD];
-  const int nd = p.box.nd;
-  for (int64_t f = f0 + threadIdx.x; f < f1; f += blockDim.x) {
-    decompose(p.box, f, idx);
-    T v = (T)0;
-    int64_t dummy;
-    vm_run_env<T>(p.code, 0, p.konst, p.h, env, idx, nd, p.in, sfold + 1, &v, &dummy);
-    store_as<T>((void*)p.out.ptr, p.out.dtype, fview_off(p.out, sfold, nd, idx), v);
-  }
-}
-
-// ---------------------------------------------------------------- GEMM rows
-// C[r, n] = sum_k A[r, k] B[k, n] for the CTA's rows r in [m0, m1) of M
-// (M = slab rows x m), all n.  A rows are staged in shared memory; B is
-// streamed from L2 with each thread owning columns and all rows (B reuse).
-
-
-// A loads for MRP rows at one k: float4 / double2 vector broadcasts from smem
-template <typename T, int MRP>
-RT_DEV void load_a(const T* ak, T (&a)[MRP]) {
-  if constexpr (sizeof(T) == 4) {
-#pragma unroll
-    for (int q = 0; q < MRP / 4; ++q) {
-      float4 v = reinterpret_cast<const float4*>(ak)[q];
-      a[4 * q] = v.x; a[4 * q + 1] = v.y; a[4 * q + 2] = v.z; a[4 * q + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < MRP / 2; ++q) {
-      double2 v = reinterpret_cast<const double2*>(ak)[q];
-      a[2 * q] = v.x; a[2 * q + 1] = v.y;
-    }
-  }
-}
-
-// chunk loop + epilogue with the padded row count MRP and the columns per
-// thread NC known at compile time; k unrolled by 4 with loads batched ahead
-// of the FMAs (the loop is issue/latency bound, not bandwidth bound).
-template <typename T, int MRP, int NC>
-RT_DEV void tma_body(const rt_gemm_params& p, const T* As, const T* Bg, int64_t K, int64_t Nn,
-                     int64_t kc, int64_t nch, int mr, int64_t m0, int64_t coff, int64_t biasoff,
-                     loop_ring& ring) {
-  const int nn = (int)Nn;
-  T acc[NC][MRP];
-#pragma unroll
-  for (int j = 0; j < NC; ++j)
-#pragma unroll
-    for (int r = 0; r < MRP; ++r) acc[j][r] = (T)0;
-  int col[NC];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    col[j] = (int)threadIdx.x + j * (int)blockDim.x;
-    if (col[j] >= nn) col[j] = nn - 1;   // duplicate work, never stored
-  }
-  auto issue = [&](int c) {
-    uint32_t st = (ring.seq + (uint32_t)c) % RING;
-    int64_t k0 = (int64_t)c * kc;
-    int64_t rows = min(kc, K - k0);
-    uint32_t bytes = (uint32_t)(rows * Nn * sizeof(T));
-    mbar_expect_tx(&ring.bar[st], bytes);
-    bulk_g2s(ring.buf + (size_t)st * ring.stage_bytes, Bg + k0 * Nn, bytes, &ring.bar[st]);
-  };
-  for (int c = 0; c < (int)nch; ++c) {
-    uint32_t g = ring.seq + (uint32_t)c;
-    uint32_t st = g % RING;
-    mbar_wait(&ring.bar[st], (g / RING) & 1);
-    const T* Bs = (const T*)(ring.buf + (size_t)st * ring.stage_bytes);
-    const int k0 = c * (int)kc;
-    const int rows = (int)min(kc, K - (int64_t)k0);
-    const T* ak = As + (size_t)k0 * MRP;
-    int kk = 0;
-    for (; kk + 4 <= rows; kk += 4, ak += 4 * MRP) {
-      T b[4][NC];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int j = 0; j < NC; ++j) b[u][j] = Bs[(kk + u) * nn + col[j]];
-      T a[4][MRP];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) load_a<T, MRP>(ak + u * MRP, a[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int j = 0; j < NC; ++j)
-#pragma unroll
-          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
-    }
-    for (; kk < rows; ++kk, ak += MRP) {
-      T a[MRP];
-      load_a<T, MRP>(ak, a);
-#pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        const T bb = Bs[kk * nn + col[j]];
-#pragma unroll
-        for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[r], bb, acc[j][r]);
-      }
-    }
-    __syncthreads();   // everyone is done with stage st
-    if (threadIdx.x == 0 && c + RING < (int)nch) issue(c + RING);
-  }
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    const int64_t n = threadIdx.x + j * (int64_t)blockDim.x;
-    if (n >= Nn) break;
-    T bias = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
-                                     biasoff + gdec32(p.N, n, p.bias.s2)) : (T)0;
-    const int64_t cn = gdec32(p.N, n, p.C.s2);
-#pragma unroll
-    for (int r = 0; r < MRP; ++r) {
-      if (r >= mr) break;
-      T v = acc[j][r] + bias;
-      if (p.epilogue == 1) v = vm_tanh<T>(v);
-      store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + cn, v);
-    }
-  }
-}
-
-template <typename T, int MRP>
-RT_DEV void tma_body_nc(const rt_gemm_params& p, const T* As, const T* Bg, int64_t K, int64_t Nn,
-                        int64_t kc, int64_t nch, int mr, int64_t m0, int64_t coff,
-                        int64_t biasoff, loop_ring& ring) {
-  const int nc = (int)((Nn + blockDim.x - 1) / blockDim.x);
-  if (nc <= 1 || sizeof(T) == 8) tma_body<T, MRP, 1>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
-  else tma_body<T, MRP, 2>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
-}
-
-template <typename T>
-RT_DEV bool gemm_rows_tma(const rt_gemm_params& p, const int64_t* env, int64_t m0, int64_t m1,
-                          unsigned char* smem, loop_ring& ring) {
-  // dense row-major weights B[K][N] of type T: stream K-panels with TMA bulk copies
-  const int64_t K = p.k, Nn = p.n;
-  if (p.B.dtype != (sizeof(T) == 8 ? RT_F64 : RT_F32) || p.N.nd != 1 || p.K.nd != 1 ||
-      p.B.s2[0] != 1 || p.B.s1[0] != Nn || p.Z.nd > 1)
-    return false;
-  const int64_t kc = ring.stage_bytes / (Nn * (int64_t)sizeof(T));
-  const int mr = (int)(m1 - m0);
-  if (kc < 1 || Nn < 64 || mr > 8 || Nn > (sizeof(T) == 8 ? 1 : 2) * (int64_t)blockDim.x)
-    return false;
-  const int mrp = (mr + 3) & ~3;                           // rows padded to a multiple of 4
-  T* As = (T*)smem;                                        // k-major: As[k * mrp + r]
-  const int64_t aoff = fold_gop_off(p.A, env);
-  const int64_t boff = fold_gop_off(p.B, env);
-  const int64_t coff = fold_gop_off(p.C, env);
-  const int64_t biasoff = p.bias.ptr ? fold_gop_off(p.bias, env) : 0;
-  const T* Bg = (const T*)p.B.ptr + boff;
-  if ((((uintptr_t)Bg) & 15) != 0 || ((Nn * (int64_t)sizeof(T)) & 15) != 0) return false;
-  const int64_t nch = (K + kc - 1) / kc;
-  auto issue = [&](int64_t c) {
-    uint32_t st = (ring.seq + (uint32_t)c) % RING;
-    int64_t k0 = c * kc;
-    int64_t rows = min(kc, K - k0);
-    uint32_t bytes = (uint32_t)(rows * Nn * sizeof(T));
-    mbar_expect_tx(&ring.bar[st], bytes);
-    bulk_g2s(ring.buf + (size_t)st * ring.stage_bytes, Bg + k0 * Nn, bytes, &ring.bar[st]);
-  };
-  if (threadIdx.x == 0)
-    for (int64_t c = 0; c < (nch < RING ? nch : (int64_t)RING); ++c) issue(c);
-  // stage A rows meanwhile (k-major, zero-padded rows)
-  {
-    const int64_t sk = p.A.s2[0];
-    for (int64_t i = threadIdx.x; i < (int64_t)mrp * K; i += blockDim.x) {
-      int r = (int)(i / K);
-      int64_t k = i - (int64_t)r * K;
-      As[k * mrp + r] = r < mr ? load_as<T>((const void*)p.A.ptr, p.A.dtype,
-                                            aoff + gdec32(p.M, m0 + r, p.A.s1) + k * sk) : (T)0;
-    }
-  }
-  __syncthreads();
-  if (mrp <= 4) tma_body_nc<T, 4>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
-  else tma_body_nc<T, 8>(p, As, Bg, K, Nn, kc, nch, mr, m0, coff, biasoff, ring);
-  ring.seq += (uint32_t)nch;
-  return true;
-}
-
-template <typename T>
-RT_DEV void gemm_rows(const rt_gemm_params& p, const int64_t* env, int64_t m0, int64_t m1,
-                      unsigned char* smem) {
-  const int64_t K = p.k, Nn = p.n;
-  const int mr = (int)(m1 - m0);
-  T* As = (T*)smem;                                        // [mr][K]
-  int64_t* kB = (int64_t*)(smem + ((mr * K * sizeof(T) + 15) / 16) * 16);   // [K]
-  const int64_t aoff = fold_gop_off(p.A, env);
-  const int64_t boff = fold_gop_off(p.B, env);
-  const int64_t coff = fold_gop_off(p.C, env);
-  const int64_t biasoff = p.bias.ptr ? fold_gop_off(p.bias, env) : 0;
-  // stage A rows
-  for (int64_t i = threadIdx.x; i < (int64_t)mr * K; i += blockDim.x) {
-    int r = (int)(i / K);
-    int64_t k = i - (int64_t)r * K;
-    int64_t o = aoff + gdec32(p.M, m0 + r, p.A.s1) + gdec32(p.K, k, p.A.s2);
-    As[i] = load_as<T>((const void*)p.A.ptr, p.A.dtype, o);
-  }
-  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) kB[k] = gdec32(p.K, k, p.B.s1);
-  __syncthreads();
-  const void* Bp = (const void*)p.B.ptr;
-  if (Nn >= 64 || mr * Nn >= (int64_t)blockDim.x) {
-    // thread owns column n, all rows
-    for (int64_t n = threadIdx.x; n < Nn; n += blockDim.x) {
-      T acc[LOOP_MAXR];
-#pragma unroll
-      for (int r = 0; r < LOOP_MAXR; ++r) acc[r] = (T)0;
-      const int64_t cb = boff + gdec32(p.N, n, p.B.s2);
-      for (int64_t k = 0; k < K; ++k) {
-        T b = load_as<T>(Bp, p.B.dtype, cb + kB[k]);
-#pragma unroll
-        for (int r = 0; r < LOOP_MAXR; ++r)
-          if (r < mr) acc[r] = fma(As[r * K + k], b, acc[r]);
-      }
-      T bias = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
-                                       biasoff + gdec32(p.N, n, p.bias.s2)) : (T)0;
-      const int64_t cn = gdec32(p.N, n, p.C.s2);
-#pragma unroll
-      for (int r = 0; r < LOOP_MAXR; ++r) {
-        if (r >= mr) break;
-        T v = acc[r] + bias;
-        if (p.epilogue == 1) v = vm_tanh<T>(v);
-        store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + cn, v);
-      }
-    }
-  } else {
-    // few outputs: a group of lanes splits K for each output, shuffle-reduce
-    const int outs = (int)(mr * Nn);
-    int g = 1;
-    while (g * 2 * outs <= (int)blockDim.x && g < 32) g *= 2;
-    const int lane_in = threadIdx.x % g;
-    const int per = (int)blockDim.x / g;
-    for (int base = 0; base < outs; base += per) {
-      const int o = base + (int)threadIdx.x / g;
-      const bool act = o < outs;
-      const int r = act ? o / (int)Nn : 0;
-      const int64_t n = act ? o - (int64_t)r * Nn : 0;
-      const int64_t cb = boff + gdec32(p.N, n, p.B.s2);
-      T acc = (T)0;
-      if (act)
-        for (int64_t k = lane_in; k < K; k += g)
-          acc = fma(As[r * K + k], load_as<T>(Bp, p.B.dtype, cb + kB[k]), acc);
-      for (int sft = g / 2; sft > 0; sft >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, sft, g);
-      if (act && lane_in == 0) {
-        T v = acc;
-        if (p.bias.ptr)
-          v += load_as<T>((const void*)p.bias.ptr, p.bias.dtype, biasoff + gdec32(p.N, n, p.bias.s2));
-        if (p.epilogue == 1) v = vm_tanh<T>(v);
-        store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + gdec32(p.N, n, p.C.s2), v);
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------- UDF rows
-
-RT_DEV double pairwise_sum_l(const void* base, int dtype, int64_t off, int64_t n) {
-  if (n < 8) {
-    double r = 0.0;
-    for (int64_t i = 0; i < n; ++i) r += load_as<double>(base, dtype, off + i);
-    return r;
-  }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = load_as<double>(base, dtype, off + j);
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] += load_as<double>(base, dtype, off + i + j);
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res += load_as<double>(base, dtype, off + i);
-    return res;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return pairwise_sum_l(base, dtype, off, n2) + pairwise_sum_l(base, dtype, off + n2, n - n2);
-}
-
-RT_DEV int push_words_l(uint32_t* w, int n, int64_t v) {
-  uint64_t u = (uint64_t)v;
-  if (u == 0) { w[n++] = 0; return n; }
-  while (u) { w[n++] = (uint32_t)(u & 0xffffffffu); u >>= 32; }
-  return n;
-}
-
-// mean of n values in numpy's pairwise order (umath pairwise_sum, n <= 128:
-// 8 strided accumulators, tree-combined, remainder added in order); lane j of
-// the warp owns accumulator j, so the result is bit-identical to numpy's.
-RT_DEV double warp_pairwise_sum(const void* base, int dtype, int64_t off, int64_t n, int lane) {
-  if (n > 128) {
-    double v = lane == 0 ? pairwise_sum_l(base, dtype, off, n) : 0.0;
-    return __shfl_sync(0xffffffffu, v, 0);
-  }
-  if (n < 8) {
-    double v = 0.0;
-    if (lane == 0)
-      for (int64_t i = 0; i < n; ++i) v += load_as<double>(base, dtype, off + i);
-    return __shfl_sync(0xffffffffu, v, 0);
-  }
-  const int64_t body = n - (n % 8);
-  double r = 0.0;
-  if (lane < 8) {
-    r = load_as<double>(base, dtype, off + lane);
-    for (int64_t i = 8 + lane; i < body; i += 8) r += load_as<double>(base, dtype, off + i);
-  }
-  double r1 = __shfl_down_sync(0xffffffffu, r, 1);   // pairs (0,1) (2,3) (4,5) (6,7)
-  double p01 = r + r1;
-  double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
-  double q = p01 + p23;                               // lane 0: (r0+r1)+(r2+r3); lane 4: (r4+r5)+(r6+r7)
-  double q4 = __shfl_down_sync(0xffffffffu, q, 4);
-  double res = q + q4;
-  if (lane == 0)
-    for (int64_t i = body; i < n; ++i) res += load_as<double>(base, dtype, off + i);
-  return __shfl_sync(0xffffffffu, res, 0);
-}
-
-RT_DEV void udf_rows(const rt_udf_params& p, const rt_loop_op& op, const int64_t* env,
-                     int64_t r0, int64_t r1, int64_t tix) {
-  int64_t idx[RT_MAXD];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int64_t row = r0 + warp; row < r1; row += nwarps) {
-    decompose(p.box, row, idx);
-    double base = p.salt;
-    for (int k = 0; k < p.nin; ++k) {
-      int64_t c = p.in_count[k];
-      if (c == 0) continue;
-      rt_fold f = fold_of(p.in[k], env);
-      int64_t o = fview_off(p.in[k], &f, p.box.nd, idx);
-      base = base + warp_pairwise_sum((const void*)p.in[k].ptr, p.in[k].dtype, o, c, lane) / (double)c;
-    }
-    const double* noise = (const double*)op.noise;
-    if (noise) {
-      int64_t nz = op.noise_off + row * op.noise_row + tix * op.noise_step;
-      for (int j = 0; j < p.nout; ++j) {
-        rt_fold f = fold_of(p.out[j], env);
-        int64_t o = fview_off(p.out[j], &f, p.box.nd, idx);
-        int kind = p.out_kind[j];
-        double tb = kind == RT_BOOL ? tanh(base) : 0.0;
-        for (int e = lane; e < p.out_count[j]; e += 32) {
-          double z = noise[nz + e];
-          double v;
-          if (kind == RT_BOOL) v = (tb + z > 0.8) ? 1.0 : 0.0;
-          else if (kind == RT_I64) v = floor(3.0 * tanh(base + z));
-          else v = tanh(base + 0.3 * z);
-          store_as<double>((void*)p.out[j].ptr, p.out[j].dtype, o + e, v);
-        }
-        nz += p.out_count[j];
-      }
-      continue;
-    }
-    if (lane != 0) continue;
-    uint32_t words[8 + 2 * RT_MAXD];
-    int n = 0;
-    for (int i = 0; i < p.nprefix; ++i) words[n++] = p.prefix[i];
-    for (int j = 0; j < p.ncoord; ++j) {
-      int s = p.coord_src[j];
-      n = push_words_l(words, n, (s >= 0 ? idx[s] : env[-1 - s]) + p.coord_add[j]);
-    }
-    rt_pcg64 g;
-    pcg64_seed(g, words, n);
-    for (int j = 0; j < p.nout; ++j) {
-      rt_fold f = fold_of(p.out[j], env);
-      int64_t o = fview_off(p.out[j], &f, p.box.nd, idx);
-      int kind = p.out_kind[j];
-      double tb = kind == RT_BOOL ? tanh(base) : 0.0;
-      for (int e = 0; e < p.out_count[j]; ++e) {
-        double z = pcg64_normal(g);
-        double v;
-        if (kind == RT_BOOL) v = (tb + z > 0.8) ? 1.0 : 0.0;
-        else if (kind == RT_I64) v = floor(3.0 * tanh(base + z));
-        else v = tanh(base + 0.3 * z);
-        store_as<double>((void*)p.out[j].ptr, p.out[j].dtype, o + e, v);
-      }
-    }
-  }
-}
-
-RT_DEV void rng_rows(const rt_rng_params& p, const int64_t* env, int64_t r0, int64_t r1) {
-  int64_t idx[RT_MAXD];
-  uint32_t words[8 + 2 * RT_MAXD];
-  for (int64_t row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
-    decompose(p.box, row, idx);
-    int n = 0;
-    for (int i = 0; i < p.nprefix; ++i) words[n++] = p.prefix[i];
-    for (int j = 0; j < p.ncoord; ++j) {
-      int s = p.coord_src[j];
-      n = push_words_l(words, n, (s >= 0 ? idx[s] : env[-1 - s]) + p.coord_add[j]);
-    }
-    rt_pcg64 g;
-    pcg64_seed(g, words, n);
-    rt_fold f = fold_of(p.out, env);
-    int64_t o = fview_off(p.out, &f, p.box.nd, idx);
-    for (int j = 0; j < p.count; ++j) {
-      double v = p.dist == 0 ? pcg64_normal(g) : pcg64_double(g);
-      store_as<double>((void*)p.out.ptr, p.out.dtype, o + j, v);
-    }
-  }
-}
+// RT_K_LOOP — a whole row-local loop in one persistent launch (interpreting
+// form: the op list is dispatched at run time; `jit.loop_source` emits the
+// same kernel with the body specialised).  See loop_lib.cuh for the ops.
+#include "loop_lib.cuh"
 
 // ---------------------------------------------------------------- the loop
 
@@ -493,27 +15,10 @@ __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ r
   const int64_t r1 = min(p.rows, r0 + p.rows_per_cta);
   if (r0 >= r1) return;
   const rt_loop_op* ops = (const rt_loop_op*)p.ops;
-  // every op's descriptor is read each step: keep a copy in shared memory
-  for (int i = 0; i < p.nops; ++i) {
-    const int4* src = (const int4*)ops[i].params;
-    int4* dst = (int4*)(smem + ops[i].smem_off);
-    for (int w = threadIdx.x; w < (ops[i].param_bytes + 15) / 16; w += blockDim.x) dst[w] = src[w];
-  }
-  unsigned char* sA = smem + p.a_off;
   // smem: [op descriptors | A rows | TMA ring]
-  const uint32_t ring_off = (uint32_t)p.ring_off;   // bytes reserved for A rows + offsets
+  unsigned char* sA = smem + p.a_off;
   loop_ring ring;
-  ring.bar = bars;
-  ring.buf = smem + ring_off;
-  ring.stage_bytes = p.smem_bytes > (int)ring_off
-                         ? (uint32_t)((p.smem_bytes - (int)ring_off) / RING) & ~127u : 0u;
-  ring.seq = 0;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < RING; ++i) mbar_init(&bars[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
+  loop_prologue(p, smem, bars, ring);
   for (int64_t t = p.start; p.step > 0 ? t < p.stop : t > p.stop; t += p.step) {
     env[p.slot] = t;
     for (int i = 0; i < p.nops; ++i) {
@@ -529,13 +34,8 @@ __global__ void __launch_bounds__(LOOP_THREADS) k_loop(const __grid_constant__ r
         case RT_K_GEMM: {
           const rt_gemm_params& q = *(const rt_gemm_params*)(smem + op.smem_off);
           const int64_t m0 = r0 * op.row_elems, m1 = r1 * op.row_elems;
-          if (op.f64) {
-            if (ring.stage_bytes == 0 || !gemm_rows_tma<double>(q, env, m0, m1, sA, ring))
-              gemm_rows<double>(q, env, m0, m1, sA);
-          } else {
-            if (ring.stage_bytes == 0 || !gemm_rows_tma<float>(q, env, m0, m1, sA, ring))
-              gemm_rows<float>(q, env, m0, m1, sA);
-          }
+          if (op.f64) gemm_op<double>(q, env, m0, m1, sA, ring);
+          else gemm_op<float>(q, env, m0, m1, sA, ring);
           break;
         }
         case RT_K_UDF:

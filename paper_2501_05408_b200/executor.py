@@ -529,6 +529,7 @@ class Executable:
         self.hooks = low.hooks
         self._upload_loops(low)
         self.nrec = len(low.recs)
+        self._low_recs = low.recs
         self._params = [p for (_, p, _, _, _, _) in low.recs]
         recs = (N.rt_launch_rec * max(1, len(low.recs)))()
         for i, (kernel, p, grid, block, smem, label) in enumerate(low.recs):
@@ -544,7 +545,8 @@ class Executable:
         self.labels = [lab for (*_, lab) in low.recs]
         self.kernels = [k for (k, *_rest) in low.recs]
         from . import jit
-        self.jit_count = jit.specialise(recs, self.kernels, self._params, self.labels)
+        self.jit_count = jit.specialise(recs, self.kernels, self._params, self.labels,
+                                        self.loop_info)
         prog = (N.rt_instr * max(1, len(low.prog)))()
         for i, ins in enumerate(low.prog):
             prog[i].op, prog[i].a, prog[i].b, prog[i].c, prog[i].d, prog[i].e = (

@@ -22,6 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CACHE = os.environ.get("RTB200_JIT_CACHE", os.path.join(os.path.expanduser("~"), ".cache",
                                                         "rtb200_jit"))
 JIT_MIN_ELEMS = int(os.environ.get("RTB200_JIT_MIN", str(1 << 18)))
+JIT_LOOP_MIN = int(os.environ.get("RTB200_JIT_LOOP_MIN", str(1 << 16)))   # rows x trips
 ENABLED = os.environ.get("RTB200_JIT", "1") != "0"
 
 CT = {N.RT_F64: "double", N.RT_F32: "float", N.RT_I64: "long long", N.RT_BOOL: "unsigned char"}
@@ -48,19 +49,19 @@ def _flit(x, T):
     return f"(({T}){r})"
 
 
-def _offset_expr(base, v, nd):
+def _offset_expr(base, v, nd, var="i"):
     terms = [base]
     for d in range(nd):
         s = v.stride[d]
         if s:
-            terms.append(f"i{d}*{_lit(s)}")
+            terms.append(f"{var}{d}*{_lit(s)}")
     return " + ".join(terms)
 
 
-def _valid_expr(pfx, v, nd):
+def _valid_expr(pfx, v, nd, c0=None):
     conds = []
     for c in range(v.nchk):
-        terms = [f"{pfx}.chk_c0[{c}]"]
+        terms = [c0(c) if c0 else f"{pfx}.chk_c0[{c}]"]
         for d in range(nd):
             a = v.chk_a[c][d]
             if a:
@@ -70,13 +71,9 @@ def _valid_expr(pfx, v, nd):
     return " && ".join(conds) if conds else "true"
 
 
-def ew_source(p, name):
-    """CUDA source of a kernel equivalent to k_ew<T> on parameter block p."""
-    nd = p.box.nd
-    ext = [p.box.ext[i] for i in range(nd)]
-    T = "double" if p.f64 else "float"
+def _program_lines(p, T, nd, base=None, chk=None, env="p.h.env"):
+    """Straight-line C statements for the VM program of EW params p."""
     code = [p.code[i] for i in range(N.RT_CODE)]
-    # find the program end and jump targets
     targets = set()
     pc, end = 0, 0
     while pc < N.RT_CODE:
@@ -102,7 +99,7 @@ def ew_source(p, name):
         elif o == "ICOORD":
             w(f"n{d} = i{imm};")
         elif o == "IENV":
-            w(f"n{d} = p.h.env[{imm}];")
+            w(f"n{d} = {env}[{imm}];")
         elif o == "ICONST":
             w(f"n{d} = {_lit(imm)};")
         elif o in ("IADD", "ISUB", "IMUL"):
@@ -131,8 +128,8 @@ def ew_source(p, name):
         elif o in ("LOAD", "LOADX"):
             v = p.in_[imm]
             pfx = f"p.in[{imm}]"
-            off = _offset_expr(f"{pfx}.off", v, nd)
-            valid = _valid_expr(pfx, v, nd)
+            off = _offset_expr(base(imm) if base else f"{pfx}.off", v, nd)
+            valid = _valid_expr(pfx, v, nd, (lambda cc, k=imm: chk(k, cc)) if chk else None)
             if o == "LOADX":
                 off = f"{off} + n{a}"
                 valid = f"(n{b} != 0) && {valid}"
@@ -173,27 +170,43 @@ def ew_source(p, name):
         else:
             raise ValueError(f"cannot translate VM op {op}")
         pc += 2
-    body = "\n      ".join(lines)
-    total = 1
-    for e in ext:
-        total *= e
-    small = total < (1 << 31)
+    return lines
+
+
+def _decompose(nd, ext, flat="flat", small=True):
     dec = []
     idx_t = "unsigned int" if small else "long long"
-    dec.append(f"{idx_t} r = ({idx_t})flat;")
+    dec.append(f"{idx_t} r = ({idx_t}){flat};")
     for dd in reversed(range(nd)):
         if dd == 0:
-            dec.append(f"const long long i0 = (long long)r;")
+            dec.append("const long long i0 = (long long)r;")
         else:
             dec.append(f"const long long i{dd} = (long long)(r % {ext[dd]}u); r /= {ext[dd]}u;"
                        if small else
                        f"const long long i{dd} = r % {ext[dd]}LL; r /= {ext[dd]}LL;")
-    dec_s = "\n      ".join(dec)
+    return dec
+
+
+def _store(p, T, nd, base):
     ov = p.out
-    out_off = _offset_expr("p.out.off", ov, nd)
+    out_off = _offset_expr(base, ov, nd)
     oct_ = CT[ov.dtype]
-    store = (f"((unsigned char*)p.out.ptr)[{out_off}] = res != ({T})0;" if ov.dtype == N.RT_BOOL
-             else f"(({oct_}*)p.out.ptr)[{out_off}] = ({oct_})res;")
+    return (f"((unsigned char*)p.out.ptr)[{out_off}] = res != ({T})0;" if ov.dtype == N.RT_BOOL
+            else f"(({oct_}*)p.out.ptr)[{out_off}] = ({oct_})res;")
+
+
+def ew_source(p, name):
+    """CUDA source of a kernel equivalent to k_ew<T> on parameter block p."""
+    nd = p.box.nd
+    ext = [p.box.ext[i] for i in range(nd)]
+    T = "double" if p.f64 else "float"
+    lines = _program_lines(p, T, nd)
+    body = "\n      ".join(lines)
+    total = 1
+    for e in ext:
+        total *= e
+    dec_s = "\n      ".join(_decompose(nd, ext, small=total < (1 << 31)))
+    store = _store(p, T, nd, "p.out.off")
     regs = ", ".join(f"v{i}" for i in range(8))
     iregs = ", ".join(f"n{i}" for i in range(8))
     return f"""#include "common.cuh"
@@ -213,13 +226,101 @@ extern "C" __global__ void __launch_bounds__(256) {name}(const __grid_constant__
 """
 
 
+def _env_fold(base, coefs):
+    terms = [base] + [f"env[{e}]*{_lit(c)}" for e, c in enumerate(coefs) if c]
+    return " + ".join(terms)
+
+
+def loop_source(lp, ops, name):
+    """A persistent loop kernel with the op sequence specialised: EW bodies
+    straight-line, GEMM/UDF/RNG as single template instantiations."""
+    parts = []
+    for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
+        if kernel == N.RT_K_EW:
+            nd = p.box.nd
+            ext = [p.box.ext[j] for j in range(nd)]
+            T = "double" if p.f64 else "float"
+            bases = []
+            for k in range(p.nin):
+                v = p.in_[k]
+                bases.append(f"const long long b{k} = " + _env_fold(
+                    f"p.in[{k}].off", [v.off_env[e] for e in range(N.RT_MAXENV)]) + ";")
+                for c in range(v.nchk):
+                    bases.append(f"const long long c{k}_{c} = " + _env_fold(
+                        f"p.in[{k}].chk_c0[{c}]", [v.chk_env[c][e] for e in range(N.RT_MAXENV)]) + ";")
+            bases.append("const long long bo = " + _env_fold(
+                "p.out.off", [p.out.off_env[e] for e in range(N.RT_MAXENV)]) + ";")
+            lines = _program_lines(p, T, nd, base=lambda k: f"b{k}",
+                                   chk=lambda k, c: f"c{k}_{c}", env="env")
+            regs = ", ".join(f"v{j}" for j in range(8))
+            iregs = ", ".join(f"n{j}" for j in range(8))
+            body = "\n        ".join(lines)
+            dec = "\n        ".join(_decompose(nd, ext))
+            bl = "\n      ".join(bases)
+            parts.append(f"""    {{  // op {i}: elementwise
+      const rt_ew_params& p = *(const rt_ew_params*)(smem + {soff});
+      {bl}
+      for (long long flat = r0 * {re}LL + threadIdx.x; flat < r1 * {re}LL; flat += blockDim.x) {{
+        {dec}
+        {T} {regs};
+        long long {iregs};
+        {T} res = ({T})0;
+        (void)n0;
+        {body}
+      Lend{i}:
+        {_store(p, T, nd, "bo")}
+      }}
+    }}""".replace("goto Lend;", f"goto Lend{i};").replace("L", "L") .replace(
+                "goto L", f"goto X{i}L").replace(f"goto X{i}Lend{i}", f"goto Lend{i}"))
+            # labels of this op are renamed to keep them unique per op
+            parts[-1] = _rename_labels(parts[-1], i)
+        elif kernel == N.RT_K_GEMM:
+            T = "double" if f64 else "float"
+            parts.append(f"""    gemm_op<{T}>(*(const rt_gemm_params*)(smem + {soff}), env, r0 * {re}LL, r1 * {re}LL,
+                 sA, ring);""")
+        elif kernel == N.RT_K_UDF:
+            parts.append(f"""    udf_op(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env, r0, r1, t);""")
+        elif kernel == N.RT_K_RNG:
+            parts.append(f"""    rng_op(*(const rt_rng_params*)(smem + {soff}), env, r0, r1);""")
+        else:
+            raise ValueError("unsupported op in loop JIT")
+        parts.append("    __syncthreads();")
+    body = "\n".join(parts)
+    cmp = "<" if lp.step > 0 else ">"
+    return f"""#include "loop_lib.cuh"
+extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constant__ rt_loop_params p) {{
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[RING];
+  long long env[RT_MAXENV];
+  for (int e = 0; e < RT_MAXENV; ++e) env[e] = p.h.env[e];
+  const long long r0 = (long long)blockIdx.x * {lp.rows_per_cta}LL;
+  const long long r1 = r0 + {lp.rows_per_cta}LL < {lp.rows}LL ? r0 + {lp.rows_per_cta}LL : {lp.rows}LL;
+  if (r0 >= r1) return;
+  const rt_loop_op* ops = (const rt_loop_op*)p.ops;
+  unsigned char* sA = smem + p.a_off;
+  loop_ring ring;
+  loop_prologue(p, smem, bars, ring);
+  for (long long t = {lp.start}LL; t {cmp} {lp.stop}LL; t += {lp.step}LL) {{
+    env[{lp.slot}] = t;
+{body}
+  }}
+}}
+"""
+
+
+def _rename_labels(src, i):
+    import re
+    src = re.sub(r"\bL(\d+):;", lambda m: f"X{i}L{m.group(1)}:;", src)
+    return src
+
+
 _FN_CACHE: dict = {}
 
 
 def _opts():
     # -fmad=false: each elementwise op rounds like the reference's numpy ops
     # (no contraction of a*b+c across program statements)
-    return [b"-arch=sm_100a", b"-std=c++17", b"-lineinfo", b"-fmad=false",
+    return [b"-arch=sm_100a", b"-std=c++17", b"-lineinfo", b"-fmad=false", b"--device-int128",
             b"-I" + os.path.join(HERE, "csrc").encode()]
 
 
@@ -256,11 +357,17 @@ def compile_kernel(src: str, name: str) -> int:
     return fn.value
 
 
-def specialise(recs, kernels, params, labels):
-    """Attach JIT kernels to large EW records (in place)."""
+def specialise(recs, kernels, params, labels, loop_info=None):
+    """Attach JIT kernels to large EW records and persistent loops (in place)."""
     if not ENABLED:
         return 0
     n = 0
+    for ri, info in (loop_info or {}).items():
+        if params[ri].rows * info["trips"] < JIT_LOOP_MIN:
+            continue
+        src = loop_source(params[ri], info["ops"], "loop_jit")
+        recs[ri].jit_fn = compile_kernel(src, "loop_jit")
+        n += 1
     for i, (k, p) in enumerate(zip(kernels, params)):
         if k != N.RT_K_EW or p.total < JIT_MIN_ELEMS:
             continue

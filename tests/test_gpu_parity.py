@@ -89,3 +89,18 @@ def test_jit_specialised_kernels_match_reference(name, monkeypatch):
     outs = execute(c.graph(), bounds=c.bounds, inputs=c.inputs, seed=c.seed)
     for k, want in c.outputs.items():
         assert_close(outs[k], want, k)
+
+
+def test_jit_loop_kernel_matches_interpreter(monkeypatch):
+    """The JIT-specialised persistent loop (straight-line body) reproduces
+    the interpreting loop kernel on the benchmark program at small scale."""
+    from golden_cases import load_graph
+    from paper_2501_05408_b200 import execute, jit
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    bounds = {"I": 1, "B": 64, "T": 48}
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 1 << 40)
+    ref = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=1)
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 0)
+    got = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=1)
+    for k in ref:
+        np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
