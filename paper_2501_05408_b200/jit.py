@@ -285,6 +285,8 @@ def loop_source(lp, ops, name):
         else:
             raise ValueError("unsupported op in loop JIT")
         parts.append("    __syncthreads();")
+        parts.append(f"    if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {{ long long c1 = clock64(); "
+                     f"((long long*)p.prof)[{i}] += c1 - c0; c0 = c1; }}")
     body = "\n".join(parts)
     cmp = "<" if lp.step > 0 else ">"
     return f"""#include "loop_lib.cuh"
@@ -300,6 +302,7 @@ extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constan
   unsigned char* sA = smem + p.a_off;
   loop_ring ring;
   loop_prologue(p, smem, bars, ring);
+  long long c0 = clock64();
   for (long long t = {lp.start}LL; t {cmp} {lp.stop}LL; t += {lp.step}LL) {{
     env[{lp.slot}] = t;
 {body}
