@@ -17,8 +17,8 @@
 #include "common.cuh"
 
 #define TC_BM 128
-#define TC_BK 16
-#define TC_THREADS 128
+#define TC_BK 32
+#define TC_THREADS 256
 #define TC_STAGES 2
 
 RT_DEV uint32_t tc_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -72,6 +72,22 @@ RT_DEV int64_t tc_decomp(const rt_gbox& b, int64_t flat, const int64_t* s) {
     f = q;
   }
   return o;
+}
+
+// 3xTF32 split of x into (hi, lo) stored at the same offset of the hi and lo
+// tiles (lo tile `lo_off` bytes after the hi tile).
+RT_DEV void split_store1(unsigned char* base, uint32_t lo_off, uint32_t o, float x) {
+  float h = tf32_hi(x);
+  *(float*)(base + o) = h;
+  *(float*)(base + lo_off + o) = tf32_hi(x - h);
+}
+
+RT_DEV void split_store4(unsigned char* base, uint32_t lo_off, uint32_t o, float4 x) {
+  float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+  float4 l = make_float4(tf32_hi(x.x - h.x), tf32_hi(x.y - h.y), tf32_hi(x.z - h.z),
+                         tf32_hi(x.w - h.w));
+  *(float4*)(base + o) = h;
+  *(float4*)(base + lo_off + o) = l;
 }
 
 // byte offset of element (row r, k) in a K-major no-swizzle tile with BK
@@ -138,6 +154,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   const int64_t ntiles = kend > kbeg ? (kend - kbeg + TC_BK - 1) / TC_BK : 0;
   const bool a_kfast = (p.K.nd > 0 && p.A.s2[p.K.nd - 1] == 1);
   const bool b_kfast = (p.K.nd > 0 && p.B.s1[p.K.nd - 1] == 1);
+  // 128-bit loads: 4 consecutive elements along the contiguous dim, all groups
+  // 16-byte aligned (every offset a multiple of 4 elements)
+  const bool a_mfast = (p.M.nd > 0 && p.A.s1[p.M.nd - 1] == 1);
+  const bool b_nfast = (p.N.nd > 0 && p.B.s2[p.N.nd - 1] == 1);
+  bool a_vec = false, b_vec = false;
+  {
+    bool a_al = ((p.A.ptr + 4 * (uint64_t)p.A.off) & 15) == 0;
+    bool b_al = ((p.B.ptr + 4 * (uint64_t)p.B.off) & 15) == 0;
+    bool ka = a_kfast && (p.K.ext[p.K.nd - 1] % 4 == 0);
+    for (int d = 0; d < p.K.nd - 1 && ka; ++d) ka = (p.A.s2[d] % 4 == 0);
+    for (int d = 0; d < p.M.nd && ka; ++d) ka = (p.A.s1[d] % 4 == 0);
+    bool ma = !a_kfast && a_mfast && (p.M.ext[p.M.nd - 1] % 4 == 0);
+    for (int d = 0; d < p.M.nd - 1 && ma; ++d) ma = (p.A.s1[d] % 4 == 0);
+    for (int d = 0; d < p.K.nd && ma; ++d) ma = (p.A.s2[d] % 4 == 0);
+    for (int d = 0; d < p.Z.nd; ++d) a_al = a_al && (p.A.sz[d] % 4 == 0);
+    a_vec = a_al && (ka || ma) && p.A.dtype == RT_F32;
+    bool kb = b_kfast && (p.K.ext[p.K.nd - 1] % 4 == 0);
+    for (int d = 0; d < p.K.nd - 1 && kb; ++d) kb = (p.B.s1[d] % 4 == 0);
+    for (int d = 0; d < p.N.nd && kb; ++d) kb = (p.B.s2[d] % 4 == 0);
+    bool nb = !b_kfast && b_nfast && (p.N.ext[p.N.nd - 1] % 4 == 0);
+    for (int d = 0; d < p.N.nd - 1 && nb; ++d) nb = (p.B.s2[d] % 4 == 0);
+    for (int d = 0; d < p.K.nd && nb; ++d) nb = (p.B.s1[d] % 4 == 0);
+    for (int d = 0; d < p.Z.nd; ++d) b_al = b_al && (p.B.sz[d] % 4 == 0);
+    b_vec = b_al && (kb || nb) && p.B.dtype == RT_F32;
+    if (a_vec && !a_kfast) { /* M-contiguous */ }
+  }
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)(TC_BM >> 4) << 24);
   const float* Ap = (const float*)p.A.ptr;
@@ -151,36 +193,90 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
     if (tid < TC_BK) {
       int64_t k = k0 + tid;
       kA[tid] = k < kend ? tc_decomp(p.K, k, p.A.s2) : 0;
-    } else if (tid >= 32 && tid < 32 + TC_BK) {
-      int64_t k = k0 + tid - 32;
-      kB[tid - 32] = k < kend ? tc_decomp(p.K, k, p.B.s1) : 0;
+    } else if (tid >= 64 && tid < 64 + TC_BK) {
+      int64_t k = k0 + tid - 64;
+      kB[tid - 64] = k < kend ? tc_decomp(p.K, k, p.B.s1) : 0;
     }
     __syncthreads();
-    // A tile: 128 x 16
-#pragma unroll 4
-    for (int i = 0; i < (TC_BM * TC_BK) / TC_THREADS; ++i) {
-      int e = tid + TC_THREADS * i;
-      int r, k;
-      if (a_kfast) { r = e >> 4; k = e & 15; } else { k = e >> 7; r = e & 127; }
-      bool ok = (m0 + r < p.m) && (k0 + k < kend);
-      float x = ok ? Ap[rowA[r] + kA[k]] : 0.f;
-      float h = tf32_hi(x);
-      uint32_t o = tc_off(r, k);
-      *(float*)(sb + o) = h;
-      *(float*)(sb + a_bytes + o) = tf32_hi(x - h);
+    // A tile: 128 x BK, 128-bit loads along the operand's contiguous dim
+    if (a_vec) {
+      if (a_kfast) {
+#pragma unroll
+        for (int i = 0; i < (TC_BM * TC_BK / 4) / TC_THREADS; ++i) {
+          int e = tid + TC_THREADS * i;
+          int r = e / (TC_BK / 4), k4 = (e % (TC_BK / 4)) * 4;
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (m0 + r < p.m && k0 + k4 + 3 < kend)
+            x = *(const float4*)(Ap + rowA[r] + kA[k4]);
+          else if (m0 + r < p.m)
+            for (int j = 0; j < 4; ++j)
+              if (k0 + k4 + j < kend) (&x.x)[j] = Ap[rowA[r] + kA[k4 + j]];
+          split_store4(sb, a_bytes, tc_off(r, k4), x);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < (TC_BM * TC_BK / 4) / TC_THREADS; ++i) {
+          int e = tid + TC_THREADS * i;
+          int k = e / (TC_BM / 4), r4 = (e % (TC_BM / 4)) * 4;
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (k0 + k < kend) {
+            if (m0 + r4 + 3 < p.m) x = *(const float4*)(Ap + rowA[r4] + kA[k]);
+            else
+              for (int j = 0; j < 4; ++j)
+                if (m0 + r4 + j < p.m) (&x.x)[j] = Ap[rowA[r4 + j] + kA[k]];
+          }
+          for (int j = 0; j < 4; ++j) split_store1(sb, a_bytes, tc_off(r4 + j, k), (&x.x)[j]);
+        }
+      }
+    } else {
+      for (int i = 0; i < (TC_BM * TC_BK) / TC_THREADS; ++i) {
+        int e = tid + TC_THREADS * i;
+        int r, k;
+        if (a_kfast) { r = e / TC_BK; k = e % TC_BK; } else { k = e / TC_BM; r = e % TC_BM; }
+        bool ok = (m0 + r < p.m) && (k0 + k < kend);
+        split_store1(sb, a_bytes, tc_off(r, k), ok ? Ap[rowA[r] + kA[k]] : 0.f);
+      }
     }
-    // B tile: BN x 16 (rows = n)
-    for (int i = 0; i < (256 * TC_BK) / TC_THREADS; ++i) {
-      int e = tid + TC_THREADS * i;
-      int c, k;
-      if (b_kfast) { c = e >> 4; k = e & 15; } else { k = e >> 8; c = e & 255; }
-      if (c >= BN) continue;
-      bool ok = (n0 + c < p.n) && (k0 + k < kend);
-      float x = ok ? Bp[colB[c] + kB[k]] : 0.f;
-      float h = tf32_hi(x);
-      uint32_t o = tc_off(c, k);
-      *(float*)(sb + 2 * a_bytes + o) = h;
-      *(float*)(sb + 2 * a_bytes + b_bytes + o) = tf32_hi(x - h);
+    // B tile: BN x BK (rows = n)
+    unsigned char* sbB = sb + 2 * a_bytes;
+    if (b_vec) {
+      if (b_kfast) {
+        for (int i = 0; i < (256 * TC_BK / 4) / TC_THREADS; ++i) {
+          int e = tid + TC_THREADS * i;
+          int c = e / (TC_BK / 4), k4 = (e % (TC_BK / 4)) * 4;
+          if (c >= BN) continue;
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (n0 + c < p.n && k0 + k4 + 3 < kend)
+            x = *(const float4*)(Bp + colB[c] + kB[k4]);
+          else if (n0 + c < p.n)
+            for (int j = 0; j < 4; ++j)
+              if (k0 + k4 + j < kend) (&x.x)[j] = Bp[colB[c] + kB[k4 + j]];
+          split_store4(sbB, b_bytes, tc_off(c, k4), x);
+        }
+      } else {
+        for (int i = 0; i < (256 * TC_BK / 4) / TC_THREADS; ++i) {
+          int e = tid + TC_THREADS * i;
+          int k = e / 64, c4 = (e % 64) * 4;
+          if (c4 >= BN) continue;
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (k0 + k < kend) {
+            if (n0 + c4 + 3 < p.n) x = *(const float4*)(Bp + colB[c4] + kB[k]);
+            else
+              for (int j = 0; j < 4; ++j)
+                if (n0 + c4 + j < p.n) (&x.x)[j] = Bp[colB[c4 + j] + kB[k]];
+          }
+          for (int j = 0; j < 4; ++j) split_store1(sbB, b_bytes, tc_off(c4 + j, k), (&x.x)[j]);
+        }
+      }
+    } else {
+      for (int i = 0; i < (256 * TC_BK) / TC_THREADS; ++i) {
+        int e = tid + TC_THREADS * i;
+        int c, k;
+        if (b_kfast) { c = e / TC_BK; k = e % TC_BK; } else { k = e / 256; c = e % 256; }
+        if (c >= BN) continue;
+        bool ok = (n0 + c < p.n) && (k0 + k < kend);
+        split_store1(sbB, b_bytes, tc_off(c, k), ok ? Bp[colB[c] + kB[k]] : 0.f);
+      }
     }
     // make the generic-proxy smem writes visible to the tensor core (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -188,7 +284,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t base = tc_smem(sb);
-      const uint32_t sbo = TC_BK * 32;   // 8-row group stride
+      const uint32_t sbo = TC_BK * 32;   // 8-row group stride (BK/4 core matrices of 128 B)
 #pragma unroll
       for (int s = 0; s < TC_BK / 8; ++s) {
         const uint32_t ko = s * 256;      // two 16B core matrices along K per MMA
@@ -211,12 +307,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
   }
   asm volatile("tcgen05.fence::after_thread_sync;");
 
-  // epilogue: warp w reads TMEM lanes [32w, 32w+32) = tile rows
-  const int r = warp * 32 + lane;
+  // epilogue: warp w reads TMEM lanes [32(w%4), +32) = tile rows, column half w/4
+  const int wq = warp & 3, wh = warp >> 2;
+  const int r = wq * 32 + lane;
   const int64_t m = m0 + r;
-  for (int c0 = 0; c0 < BN; c0 += 16) {
+  const int half = ((BN / 2) + 15) / 16 * 16;
+  const int cbeg = wh * half, cend = wh ? BN : (half < BN ? half : BN);
+  for (int c0 = cbeg; c0 < cend; c0 += 16) {
     uint32_t v[16];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+    const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),

@@ -526,3 +526,202 @@ __device__ __noinline__ void rng_op(const rt_rng_params& p, const int64_t* env, 
                                     int64_t r1) {
   rng_rows(p, env, r0, r1);
 }
+
+// ================================================================ JIT ops
+// Shape-specialised op bodies for JIT-compiled loop kernels: K, N, rows and
+// panel sizes are template constants, shared memory is addressed with
+// explicit ld.shared (the generic-pointer path costs an LD.E + 64-bit address
+// math per operand), and every op is a single inlined instantiation.
+
+RT_DEV float lds1(uint32_t a, float) { float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v; }
+RT_DEV double lds1(uint32_t a, double) { double v; asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a)); return v; }
+RT_DEV void sts1(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
+RT_DEV void sts1(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+
+template <int MRP>
+RT_DEV void lds_rows(uint32_t a, float (&x)[MRP]) {
+#pragma unroll
+  for (int q = 0; q < MRP / 4; ++q)
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(x[4 * q]), "=f"(x[4 * q + 1]), "=f"(x[4 * q + 2]), "=f"(x[4 * q + 3])
+                 : "r"(a + 16 * q));
+}
+template <int MRP>
+RT_DEV void lds_rows(uint32_t a, double (&x)[MRP]) {
+#pragma unroll
+  for (int q = 0; q < MRP / 2; ++q)
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(x[2 * q]), "=d"(x[2 * q + 1]) : "r"(a + 16 * q));
+}
+
+// stage A rows [m0, m0+mr) x K into shared memory k-major (As[k*MRP + r]),
+// zero-padded to MRP rows; the K stride of A is the compile-time KS.
+template <typename T, int MRP, int K>
+RT_DEV void stage_a(const rt_gemm_params& p, const int64_t* env, int64_t m0, int mr, uint32_t sA) {
+  const int64_t aoff = fold_gop_off(p.A, env);
+  const int64_t ks = p.A.s2[0];
+  for (int i = threadIdx.x; i < MRP * K; i += blockDim.x) {
+    const int r = i / K, k = i - r * K;
+    T v = (T)0;
+    if (r < mr) v = load_as<T>((const void*)p.A.ptr, p.A.dtype, aoff + gdec32(p.M, m0 + r, p.A.s1) + k * ks);
+    sts1(sA + (uint32_t)((k * MRP + r) * sizeof(T)), v);
+  }
+}
+
+// C[r, n] = act(sum_k A[r,k] B[k,n] + bias[n]) with dense row-major B[K][N]
+// streamed by TMA bulk copies in KC-row panels through the ring.
+template <typename T, int MRP, int NC, int K, int N, int KC>
+RT_DEV void gemm_tma_fixed(const rt_gemm_params& p, const int64_t* env, int64_t m0, int64_t m1,
+                           uint32_t sA, loop_ring& ring) {
+  constexpr int NCH = (K + KC - 1) / KC;
+  const int mr = (int)(m1 - m0);
+  const T* Bg = (const T*)p.B.ptr + fold_gop_off(p.B, env);
+  auto issue = [&](int c) {
+    const uint32_t st = (ring.seq + (uint32_t)c) % RING;
+    const int rows = (c + 1) * KC <= K ? KC : K - c * KC;
+    const uint32_t bytes = (uint32_t)(rows * N * sizeof(T));
+    mbar_expect_tx(&ring.bar[st], bytes);
+    bulk_g2s(ring.buf + (size_t)st * ring.stage_bytes, Bg + (size_t)c * KC * N, bytes, &ring.bar[st]);
+  };
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int c = 0; c < (NCH < RING ? NCH : RING); ++c) issue(c);
+  stage_a<T, MRP, K>(p, env, m0, mr, sA);
+  __syncthreads();
+  T acc[NC][MRP];
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+#pragma unroll
+    for (int r = 0; r < MRP; ++r) acc[j][r] = (T)0;
+  int col[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    col[j] = (int)threadIdx.x + j * (int)blockDim.x;
+    if (col[j] >= N) col[j] = N - 1;
+  }
+  const uint32_t ring_base = smem_u32(ring.buf);
+  for (int c = 0; c < NCH; ++c) {
+    const uint32_t g = ring.seq + (uint32_t)c;
+    const uint32_t st = g % RING;
+    mbar_wait(&ring.bar[st], (g / RING) & 1);
+    const uint32_t bs = ring_base + st * ring.stage_bytes;
+    const int rows = (c + 1) * KC <= K ? KC : K - c * KC;
+    uint32_t ak = sA + (uint32_t)(c * KC * MRP * sizeof(T));
+#pragma unroll 2
+    for (int kk = 0; kk < rows; kk += 4) {
+      T b[4][NC];
+      T a[4][MRP];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          b[u][j] = kk + u < rows ? lds1(bs + (uint32_t)(((kk + u) * N + col[j]) * sizeof(T)), (T)0) : (T)0;
+        lds_rows<MRP>(ak + (uint32_t)((kk + u) * MRP * sizeof(T)), a[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+#pragma unroll
+          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && c + RING < NCH) issue(c + RING);
+  }
+  ring.seq += NCH;
+  const int64_t coff = fold_gop_off(p.C, env);
+  const int64_t boff = p.bias.ptr ? fold_gop_off(p.bias, env) : 0;
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int n = (int)threadIdx.x + j * (int)blockDim.x;
+    if (n >= N) break;
+    const T bias = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
+                                           boff + (int64_t)n * p.bias.s2[0]) : (T)0;
+    const int64_t cn = (int64_t)n * p.C.s2[0];
+#pragma unroll
+    for (int r = 0; r < MRP; ++r) {
+      if (r >= mr) break;
+      T v = acc[j][r] + bias;
+      if (p.epilogue == 1) v = vm_tanh<T>(v);
+      store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + cn, v);
+    }
+  }
+}
+
+// small N (< 64): B[K][N] staged whole in shared memory, each output's K
+// range split over G lanes and shuffle-reduced.
+template <typename T, int MRP, int K, int N>
+RT_DEV void gemm_small_fixed(const rt_gemm_params& p, const int64_t* env, int64_t m0, int64_t m1,
+                             uint32_t sA, uint32_t sB) {
+  const int mr = (int)(m1 - m0);
+  const int64_t boff = fold_gop_off(p.B, env);
+  for (int i = threadIdx.x; i < K * N; i += blockDim.x) {
+    const int k = i / N, n = i - k * N;
+    sts1(sB + (uint32_t)(i * sizeof(T)),
+         load_as<T>((const void*)p.B.ptr, p.B.dtype, boff + gdec32(p.K, k, p.B.s1) + gdec32(p.N, n, p.B.s2)));
+  }
+  stage_a<T, MRP, K>(p, env, m0, mr, sA);
+  __syncthreads();
+  constexpr int OUTS = MRP * N;
+  constexpr int G0 = 256 / OUTS;
+  constexpr int G = G0 >= 32 ? 32 : G0 >= 16 ? 16 : G0 >= 8 ? 8 : G0 >= 4 ? 4 : G0 >= 2 ? 2 : 1;
+  const int lane_in = threadIdx.x % G;
+  const int64_t coff = fold_gop_off(p.C, env);
+  const int64_t bo = p.bias.ptr ? fold_gop_off(p.bias, env) : 0;
+  for (int base = 0; base < OUTS; base += 256 / G) {
+    const int o = base + (int)threadIdx.x / G;
+    const bool act = o < OUTS && (o / N) < mr;
+    const int r = act ? o / N : 0, n = act ? o % N : 0;
+    T acc = (T)0;
+    if (act)
+#pragma unroll 4
+      for (int k = lane_in; k < K; k += G)
+        acc = fma(lds1(sA + (uint32_t)((k * MRP + r) * sizeof(T)), (T)0),
+                  lds1(sB + (uint32_t)((k * N + n) * sizeof(T)), (T)0), acc);
+#pragma unroll
+    for (int s = G / 2; s > 0; s >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, s, G);
+    if (act && lane_in == 0) {
+      T v = acc;
+      if (p.bias.ptr) v += load_as<T>((const void*)p.bias.ptr, p.bias.dtype, bo + (int64_t)n * p.bias.s2[0]);
+      if (p.epilogue == 1) v = vm_tanh<T>(v);
+      store_as<T>((void*)p.C.ptr, p.C.dtype, coff + gdec32(p.M, m0 + r, p.C.s1) + (int64_t)n * p.C.s2[0], v);
+    }
+  }
+}
+
+// synthetic env with hoisted normals: one warp per row, numpy pairwise means
+// of the inputs, one lane per output element.
+template <int NIN, int NOUT>
+RT_DEV void udf_fixed(const rt_udf_params& p, const rt_loop_op& op, const int64_t* env,
+                      int64_t r0, int64_t r1, int64_t t) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int64_t idx[RT_MAXD];
+  for (int64_t row = r0 + warp; row < r1; row += nwarps) {
+    decompose(p.box, row, idx);
+    double base = p.salt;
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      const int64_t c = p.in_count[k];
+      rt_fold f = fold_of(p.in[k], env);
+      const int64_t o = fview_off(p.in[k], &f, p.box.nd, idx);
+      base = base + warp_pairwise_sum((const void*)p.in[k].ptr, p.in[k].dtype, o, c, lane) / (double)c;
+    }
+    const double* noise = (const double*)op.noise;
+    int64_t nz = op.noise_off + row * op.noise_row + t * op.noise_step;
+#pragma unroll
+    for (int j = 0; j < NOUT; ++j) {
+      rt_fold f = fold_of(p.out[j], env);
+      const int64_t o = fview_off(p.out[j], &f, p.box.nd, idx);
+      const int kind = p.out_kind[j];
+      const double tb = kind == RT_BOOL ? tanh(base) : 0.0;
+      for (int e = lane; e < p.out_count[j]; e += 32) {
+        const double z = noise[nz + e];
+        double v;
+        if (kind == RT_BOOL) v = (tb + z > 0.8) ? 1.0 : 0.0;
+        else if (kind == RT_I64) v = floor(3.0 * tanh(base + z));
+        else v = tanh(base + 0.3 * z);
+        store_as<double>((void*)p.out[j].ptr, p.out[j].dtype, o + e, v);
+      }
+      nz += p.out_count[j];
+    }
+  }
+}

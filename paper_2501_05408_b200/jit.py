@@ -275,11 +275,13 @@ def loop_source(lp, ops, name):
             # labels of this op are renamed to keep them unique per op
             parts[-1] = _rename_labels(parts[-1], i)
         elif kernel == N.RT_K_GEMM:
-            T = "double" if f64 else "float"
-            parts.append(f"""    gemm_op<{T}>(*(const rt_gemm_params*)(smem + {soff}), env, r0 * {re}LL, r1 * {re}LL,
-                 sA, ring);""")
+            parts.append(_gemm_call(lp, p, re, f64, soff))
         elif kernel == N.RT_K_UDF:
-            parts.append(f"""    udf_op(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env, r0, r1, t);""")
+            if noise:
+                parts.append(f"""    udf_fixed<{p.nin}, {p.nout}>(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env,
+                                 r0, r1, t);""")
+            else:
+                parts.append(f"""    udf_op(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env, r0, r1, t);""")
         elif kernel == N.RT_K_RNG:
             parts.append(f"""    rng_op(*(const rt_rng_params*)(smem + {soff}), env, r0, r1);""")
         else:
@@ -300,8 +302,10 @@ extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constan
   if (r0 >= r1) return;
   const rt_loop_op* ops = (const rt_loop_op*)p.ops;
   unsigned char* sA = smem + p.a_off;
+  const uint32_t sA32 = smem_u32(sA);
   loop_ring ring;
   loop_prologue(p, smem, bars, ring);
+  (void)sA32;
   long long c0 = clock64();
   for (long long t = {lp.start}LL; t {cmp} {lp.stop}LL; t += {lp.step}LL) {{
     env[{lp.slot}] = t;
@@ -309,6 +313,29 @@ extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constan
   }}
 }}
 """
+
+
+def _gemm_call(lp, q, re, f64, soff):
+    """Pick a shape-specialised GEMM body for a persistent-loop op."""
+    T = "double" if f64 else "float"
+    it = 8 if f64 else 4
+    mrp = (lp.rows_per_cta * re + 3) // 4 * 4
+    K, Nn = q.k, q.n
+    stage = ((lp.smem_bytes - lp.ring_off) // 4) & ~127
+    dense_1d = q.N.nd == 1 and q.K.nd == 1 and q.Z.nd <= 1 and q.z == 1
+    b_dt = q.B.dtype == (N.RT_F64 if f64 else N.RT_F32)
+    aligned = q.B.off % 4 == 0 and all(q.B.off_env[e] % 4 == 0 for e in range(N.RT_MAXENV))
+    q_ref = f"*(const rt_gemm_params*)(smem + {soff})"
+    if dense_1d and b_dt and mrp <= 8 and 64 <= Nn <= (256 if f64 else 512) and stage and \
+            q.B.s2[0] == 1 and q.B.s1[0] == Nn and aligned and (Nn * it) % 16 == 0:
+        kc = max(1, min(K, stage // (Nn * it)))
+        nc = 1 if Nn <= 256 else 2
+        return (f"    gemm_tma_fixed<{T}, {mrp}, {nc}, {K}, {Nn}, {kc}>({q_ref}, env, r0 * {re}LL, "
+                f"r1 * {re}LL, sA32, ring);")
+    if dense_1d and mrp <= 8 and Nn < 64 and K * Nn * it <= 4 * stage and K * mrp * it <= 64 * 1024:
+        return (f"    gemm_small_fixed<{T}, {mrp}, {K}, {Nn}>({q_ref}, env, r0 * {re}LL, r1 * {re}LL, "
+                f"sA32, smem_u32(ring.buf));")
+    return f"    gemm_op<{T}>({q_ref}, env, r0 * {re}LL, r1 * {re}LL, sA, ring);"
 
 
 def _rename_labels(src, i):

@@ -1391,7 +1391,7 @@ class Lowering:
         if splits > 1:
             p.part = self.alloc(splits * p.z * p.m * p.n * 4)
         grid = [(p.n + 255) // 256, (p.m + 127) // 128, p.z * splits]
-        self.add_rec(N.RT_K_GEMM_TC, p, grid, [128, 1, 1], N.TC_SMEM, label)
+        self.add_rec(N.RT_K_GEMM_TC, p, grid, [256, 1, 1], N.TC_SMEM, label)
         if splits > 1:
             q = N.rt_splitk_params()
             q.Z, q.M, q.N = p.Z, p.M, p.N
