@@ -141,7 +141,8 @@ typedef struct {
   int64_t red_stride[4];   /* input element stride per reduced dim */
   int32_t lo_prog[4];      /* -1 none; else program computing the start offset shift */
   int32_t threads_per_out; /* 1 or a power of two <= 1024 */
-  int32_t _pad;
+  int32_t splits;      /* column mode: reduce range split in `splits` partials */
+  uint64_t part;       /* column mode: fp64 scratch [splits][total] (0: row mode) */
   rt_view in;          /* strides over the output box; lo folded in */
   rt_view out;
   int32_t code[RT_CODE];

@@ -46,6 +46,8 @@ RT_DEV void red_setup(const rt_reduce_params& p, const int64_t* idx, int64_t* le
 
 template <typename T>
 RT_DEV double red_term(const rt_reduce_params& p, int64_t base, const int64_t* len, int64_t k) {
+  if (p.nred == 1 && p.op == 0)
+    return (double)load_as<T>((const void*)p.in.ptr, p.in.dtype, base + k * p.red_stride[0]);
   int64_t off = base;
   int64_t r = k, k0 = 0;
   for (int j = p.nred - 1; j >= 0; --j) {
@@ -101,6 +103,46 @@ __global__ void __launch_bounds__(1024) k_reduce_block(const __grid_constant__ r
     }
     __syncthreads();
   }
+}
+
+// Column mode: outputs contiguous in the input (e.g. a bias gradient summed
+// over all T*E points of a [points, 256] tensor).  Pass 1: each thread owns
+// one output and a slice of the reduced range (coalesced across threads);
+// pass 2 sums the fp64 partials in a fixed order (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_cols(const __grid_constant__ rt_reduce_params p) {
+  int64_t idx[RT_MAXD];
+  int64_t len[4];
+  const int nd = p.box.nd;
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  double* part = (double*)p.part;
+  if (o >= p.total) return;
+  decompose(p.box, o, idx);
+  int64_t base, tot;
+  red_setup<T>(p, idx, len, &base, &tot);
+  const int64_t per = (tot + p.splits - 1) / p.splits;
+  const int64_t k0 = s * per, k1 = min(tot, k0 + per);
+  double acc = 0.0;
+  for (int64_t k = k0; k < k1; ++k) acc += red_term<T>(p, base, len, k);
+  part[(int64_t)s * p.total + o] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_reduce_cols_fin(const __grid_constant__ rt_reduce_params p) {
+  int64_t idx[RT_MAXD];
+  const double* part = (const double*)p.part;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < p.total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < p.splits; ++s) acc += part[(int64_t)s * p.total + o];
+    decompose(p.box, o, idx);
+    store_as<double>((void*)p.out.ptr, p.out.dtype, view_off(p.out, p.box.nd, idx), acc);
+  }
+}
+
+extern "C" void* rt_kernel_reduce_cols(int f64, int fin) {
+  if (fin) return (void*)k_reduce_cols_fin;
+  return f64 ? (void*)k_reduce_cols<double> : (void*)k_reduce_cols<float>;
 }
 
 extern "C" void* rt_kernel_reduce(int f64, int block) {

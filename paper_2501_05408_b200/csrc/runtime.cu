@@ -12,6 +12,7 @@
 
 extern "C" void* rt_kernel_ew(int f64);
 extern "C" void* rt_kernel_reduce(int f64, int block);
+extern "C" void* rt_kernel_reduce_cols(int f64, int fin);
 extern "C" void* rt_kernel_scan(int f64, int warp);
 extern "C" void* rt_kernel_gemm(int f64);
 extern "C" void* rt_kernel_splitk(int f64);
@@ -109,6 +110,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_view(p->out, env, nenv);
       for (int j = 0; j < p->nred; ++j)
         for (int e = 0; e < nenv && e < RT_MAXENV; ++e) p->len0[j] += env[e] * p->len_env[j][e];
+      if (p->part) return rt_kernel_reduce_cols(p->f64, p->threads_per_out == -1);
       return rt_kernel_reduce(p->f64, p->threads_per_out > 1);
     }
     case RT_K_SCAN: {

@@ -1104,6 +1104,22 @@ class Lowering:
                     p.code[i] = w
                 lo_, hi_ = interval(ax.len_expr, ctx.sink_box())
                 maxlen *= max(1, int(hi_) if hi_ != INF else 1 << 20)
+        # column mode: outputs contiguous along the input's innermost box dim and
+        # a long constant reduce range (bias gradients over all T*E points)
+        const_lens = all(p.len_prog[j] < 0 and not any(p.len_a[j][d] for d in range(p.box.nd))
+                         and not any(p.len_env[j][e] for e in range(N.RT_MAXENV))
+                         for j in range(p.nred))
+        if const_lens and p.box.nd >= 1 and p.in_.stride[p.box.nd - 1] == 1 and \
+                maxlen >= 4096 and p.total >= 32 and p.total * maxlen >= (1 << 22):
+            ob = (p.total + 255) // 256
+            splits = int(max(1, min(maxlen // 256, (148 * 8) // ob, 1024)))
+            p.splits = splits
+            p.part = self.alloc(splits * p.total * 8)
+            self.add_rec(N.RT_K_REDUCE, p, [ob, splits, 1], [256, 1, 1], 0, (n.id, n.name))
+            q = N.rt_reduce_params.from_buffer_copy(p)
+            q.threads_per_out = -1
+            self.add_rec(N.RT_K_REDUCE, q, self.grid1(p.total), [256, 1, 1], 0, (n.id, n.name))
+            return
         if maxlen >= 256 and p.total < 148 * 64:
             tpo = 1024 if maxlen >= 4096 else 256
             p.threads_per_out = tpo

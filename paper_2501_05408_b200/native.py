@@ -64,7 +64,8 @@ class rt_reduce_params(C.Structure):
                 ("gamma", f64), ("reverse", i32), ("f64", i32), ("len_prog", i32 * 4),
                 ("len0", i64 * 4), ("len_env", (i64 * RT_MAXENV) * 4),
                 ("len_a", (i64 * RT_MAXD) * 4), ("red_stride", i64 * 4), ("lo_prog", i32 * 4),
-                ("threads_per_out", i32), ("_pad", i32), ("in_", rt_view), ("out", rt_view),
+                ("threads_per_out", i32), ("splits", i32), ("part", u64), ("in_", rt_view),
+                ("out", rt_view),
                 ("code", i32 * RT_CODE), ("konst", f64 * RT_KONST)]
 
 
