@@ -725,3 +725,73 @@ RT_DEV void udf_fixed(const rt_udf_params& p, const rt_loop_op& op, const int64_
     }
   }
 }
+
+// ---------------------------------------------------------------- JIT cores
+// Raw-pointer cores: all descriptor values are supplied by the generated code
+// as literals or registers, so nothing is re-read from shared memory after a
+// global store.
+
+// acc[j][r] += sum_k A_s[k][r] * B[k][col_j]; A staged k-major in smem at sA,
+// B[K][N] dense in global memory at Bg, streamed by TMA in KC-row panels.
+template <typename T, int MRP, int NC, int K, int N, int KC>
+RT_DEV void tma_core(const T* Bg, uint32_t sA, loop_ring& ring, T (&acc)[NC][MRP]) {
+  constexpr int NCH = (K + KC - 1) / KC;
+  int col[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    col[j] = (int)threadIdx.x + j * (int)blockDim.x;
+    if (col[j] >= N) col[j] = N - 1;
+  }
+  const uint32_t ring_base = smem_u32(ring.buf);
+  for (int c = 0; c < NCH; ++c) {
+    const uint32_t g = ring.seq + (uint32_t)c;
+    const uint32_t st = g % RING;
+    mbar_wait(&ring.bar[st], (g / RING) & 1);
+    const uint32_t bs = ring_base + st * ring.stage_bytes;
+    const int rows = (c + 1) * KC <= K ? KC : K - c * KC;
+    const uint32_t ak = sA + (uint32_t)(c * KC * MRP * sizeof(T));
+#pragma unroll 2
+    for (int kk = 0; kk < rows; kk += 4) {
+      T b[4][NC];
+      T a[4][MRP];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          b[u][j] = kk + u < rows ? lds1(bs + (uint32_t)(((kk + u) * N + col[j]) * sizeof(T)), (T)0) : (T)0;
+        lds_rows<MRP>(ak + (uint32_t)((kk + u) * MRP * sizeof(T)), a[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+#pragma unroll
+          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && c + RING < NCH) {
+      const int cc = c + RING;
+      const uint32_t st2 = (ring.seq + (uint32_t)cc) % RING;
+      const int rows2 = (cc + 1) * KC <= K ? KC : K - cc * KC;
+      const uint32_t bytes = (uint32_t)(rows2 * N * sizeof(T));
+      mbar_expect_tx(&ring.bar[st2], bytes);
+      bulk_g2s(ring.buf + (size_t)st2 * ring.stage_bytes, Bg + (size_t)cc * KC * N, bytes, &ring.bar[st2]);
+    }
+  }
+  ring.seq += NCH;
+}
+
+template <typename T, int K, int N, int KC>
+RT_DEV void tma_prefetch(const T* Bg, loop_ring& ring) {
+  constexpr int NCH = (K + KC - 1) / KC;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < (NCH < RING ? NCH : RING); ++c) {
+      const uint32_t st = (ring.seq + (uint32_t)c) % RING;
+      const int rows = (c + 1) * KC <= K ? KC : K - c * KC;
+      const uint32_t bytes = (uint32_t)(rows * N * sizeof(T));
+      mbar_expect_tx(&ring.bar[st], bytes);
+      bulk_g2s(ring.buf + (size_t)st * ring.stage_bytes, Bg + (size_t)c * KC * N, bytes, &ring.bar[st]);
+    }
+  }
+}

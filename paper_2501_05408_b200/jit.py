@@ -278,8 +278,7 @@ def loop_source(lp, ops, name):
             parts.append(_gemm_call(lp, p, re, f64, soff))
         elif kernel == N.RT_K_UDF:
             if noise:
-                parts.append(f"""    udf_fixed<{p.nin}, {p.nout}>(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env,
-                                 r0, r1, t);""")
+                parts.append(_udf_literal(p, i, soff, noise))
             else:
                 parts.append(f"""    udf_op(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env, r0, r1, t);""")
         elif kernel == N.RT_K_RNG:
@@ -315,6 +314,150 @@ extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constan
 """
 
 
+def _env_terms(coefs):
+    return "".join(f" + env[{e}]*{_lit(c)}" for e, c in enumerate(coefs) if c)
+
+
+def _gbox_off(gb, strides, var):
+    """Offset expression of flat index `var` decomposed over gbox gb."""
+    nd = gb.nd
+    if nd == 0:
+        return "0LL"
+    terms, rem = [], var
+    for d in reversed(range(nd)):
+        e, st = gb.ext[d], strides[d]
+        if d == 0:
+            if st:
+                terms.append(f"({rem})*{_lit(st)}")
+        else:
+            if st:
+                terms.append(f"(({rem}) % {e}LL)*{_lit(st)}")
+            rem = f"(({rem}) / {e}LL)"
+    return " + ".join(terms) if terms else "0LL"
+
+
+def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
+    """Fully specialised loop GEMM: shapes, strides and decompositions baked,
+    descriptor pointers read once into registers."""
+    T = "double" if f64 else "float"
+    mrp = (lp.rows_per_cta * re + 3) // 4 * 4
+    K, Nn = q.k, q.n
+    nc = (Nn + 255) // 256
+    env_a = _env_terms([q.A.off_env[e] for e in range(N.RT_MAXENV)])
+    env_b = _env_terms([q.B.off_env[e] for e in range(N.RT_MAXENV)])
+    env_c = _env_terms([q.C.off_env[e] for e in range(N.RT_MAXENV)])
+    env_bias = _env_terms([q.bias.off_env[e] for e in range(N.RT_MAXENV)])
+    a_m = _gbox_off(q.M, [q.A.s1[d] for d in range(4)], "m")
+    c_m = _gbox_off(q.M, [q.C.s1[d] for d in range(4)], "m")
+    a_k = _gbox_off(q.K, [q.A.s2[d] for d in range(4)], "k")
+    c_n = _gbox_off(q.N, [q.C.s2[d] for d in range(4)], "n")
+    bias_n = _gbox_off(q.N, [q.bias.s2[d] for d in range(4)], "n")
+    has_bias = bool(q.bias.ptr)
+    tanh = q.epilogue == 1
+    lines = [f"const rt_gemm_params& q = *(const rt_gemm_params*)(smem + {soff});",
+             f"const {T}* Ap = (const {T}*)q.A.ptr; const long long aoff = q.A.off{env_a};",
+             f"{T}* Cp = ({T}*)q.C.ptr; const long long coff = q.C.off{env_c};",
+             f"const long long m0 = r0 * {re}LL; const int mr = (int)((r1 - r0) * {re}LL);"]
+    if has_bias:
+        lines.append(f"const {T}* Bp_ = (const {T}*)q.bias.ptr; const long long boff = q.bias.off{env_bias};")
+    if tma:
+        lines.append(f"const {T}* Bg = (const {T}*)q.B.ptr + (q.B.off{env_b});")
+        lines.append(f"tma_prefetch<{T}, {K}, {Nn}, {kc}>(Bg, ring);")
+    else:
+        b_k = _gbox_off(q.K, [q.B.s1[d] for d in range(4)], "k")
+        b_n = _gbox_off(q.N, [q.B.s2[d] for d in range(4)], "n")
+        lines.append(f"const {T}* Bq = (const {T}*)q.B.ptr; const long long bqo = q.B.off{env_b};")
+        lines.append(f"const uint32_t sB = smem_u32(ring.buf);")
+        lines.append(f"for (int i = threadIdx.x; i < {K * Nn}; i += blockDim.x) {{ const long long k = i / {Nn}, n = i % {Nn}; "
+                     f"sts1(sB + (uint32_t)(i * sizeof({T})), Bq[bqo + {b_k} + {b_n}]); }}")
+    lines.append(f"for (int i = threadIdx.x; i < {mrp * K}; i += blockDim.x) {{ const int r = i / {K}; "
+                 f"const long long k = i - r * {K}; const long long m = m0 + r; "
+                 f"sts1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), r < mr ? Ap[aoff + {a_m} + {a_k}] : ({T})0); }}")
+    lines.append("__syncthreads();")
+    if tma:
+        lines.append(f"{T} acc[{nc}][{mrp}];")
+        lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = ({T})0; }}")
+        lines.append(f"tma_core<{T}, {mrp}, {nc}, {K}, {Nn}, {kc}>(Bg, sA32, ring, acc);")
+        epi = [f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{",
+               f"  const long long n = threadIdx.x + j * 256LL; if (n >= {Nn}) break;",
+               f"  const {T} bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else f"({T})0;"),
+               f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
+               f"    {T} v = acc[j][r] + bias;" + (f" v = vm_tanh<{T}>(v);" if tanh else ""),
+               f"    Cp[coff + {c_m} + {c_n}] = v; }}",
+               "}"]
+        lines += epi
+    else:
+        outs = mrp * Nn
+        g0 = 256 // outs
+        G = max(x for x in (1, 2, 4, 8, 16, 32) if x <= max(1, g0))
+        lines += [f"const int lane_in = threadIdx.x % {G};",
+                  f"for (int base = 0; base < {outs}; base += {256 // G}) {{",
+                  f"  const int o = base + (int)threadIdx.x / {G};",
+                  f"  const bool act = o < {outs} && (o / {Nn}) < mr;",
+                  f"  const int r = act ? o / {Nn} : 0; const long long n = act ? o % {Nn} : 0;",
+                  f"  {T} a = ({T})0;",
+                  f"  if (act) {{\n#pragma unroll 4\n    for (int k = lane_in; k < {K}; k += {G}) a = fma(lds1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), ({T})0), lds1(sB + (uint32_t)((k * {Nn} + n) * sizeof({T})), ({T})0), a); }}",
+                  f"  #pragma unroll\n  for (int s = {G // 2}; s > 0; s >>= 1) a += __shfl_down_sync(0xffffffffu, a, s, {G});",
+                  f"  if (act && lane_in == 0) {{ const long long m = m0 + r; {T} v = a" + (f" + Bp_[boff + {bias_n}]" if has_bias else "") + ";"
+                  + (f" v = vm_tanh<{T}>(v);" if tanh else "") + f" Cp[coff + {c_m} + {c_n}] = v; }}",
+                  "}"]
+    return "    {  // gemm (specialised)\n      " + "\n      ".join(lines) + "\n    }"
+
+
+def _udf_literal(p, op_index, soff, noise):
+    """Synthetic env body with counts, strides and the row decomposition baked."""
+    nd = p.box.nd
+    ext = [p.box.ext[j] for j in range(nd)]
+    lines = [f"const rt_udf_params& q = *(const rt_udf_params*)(smem + {soff});",
+             f"const double* noise = (const double*)ops[{op_index}].noise;",
+             f"const long long nz0 = ops[{op_index}].noise_off; const long long nzr = ops[{op_index}].noise_row; const long long nzs = ops[{op_index}].noise_step;"]
+    for k in range(p.nin):
+        v = p.in_[k]
+        ct = CT[v.dtype]
+        lines.append(f"const {ct}* in{k} = (const {ct}*)q.in[{k}].ptr; const long long io{k} = q.in[{k}].off"
+                     + _env_terms([v.off_env[e] for e in range(N.RT_MAXENV)]) + ";")
+    for j in range(p.nout):
+        v = p.out[j]
+        ct = CT[v.dtype]
+        lines.append(f"{ct}* out{j} = ({ct}*)q.out[{j}].ptr; const long long oo{j} = q.out[{j}].off"
+                     + _env_terms([v.off_env[e] for e in range(N.RT_MAXENV)]) + ";")
+    lines.append("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;")
+    lines.append("for (long long row = r0 + warp; row < r1; row += nwarps) {")
+    dec = ["  unsigned int rr = (unsigned int)row;"]
+    for dd in reversed(range(nd)):
+        if dd == 0:
+            dec.append("  const long long i0 = (long long)rr;")
+        else:
+            dec.append(f"  const long long i{dd} = (long long)(rr % {ext[dd]}u); rr /= {ext[dd]}u;")
+    lines += dec
+    lines.append(f"  double base = {repr(float(p.salt))};")
+    for k in range(p.nin):
+        v = p.in_[k]
+        off = _offset_expr(f"io{k}", v, nd)
+        lines.append(f"  base = base + warp_pairwise_sum((const void*)in{k}, {v.dtype}, {off}, {p.in_count[k]}LL, lane) / {float(p.in_count[k])!r};")
+    lines.append("  long long nz = nz0 + row * nzr + t * nzs;")
+    for j in range(p.nout):
+        v = p.out[j]
+        off = _offset_expr(f"oo{j}", v, nd)
+        kind = p.out_kind[j]
+        if kind == N.RT_BOOL:
+            expr = "((tb + z > 0.8) ? 1.0 : 0.0)"
+            pre = "  const double tb = tanh(base);"
+        elif kind == N.RT_I64:
+            expr, pre = "floor(3.0 * tanh(base + z))", ""
+        else:
+            expr, pre = "tanh(base + 0.3 * z)", ""
+        ct = CT[v.dtype]
+        if pre:
+            lines.append(pre)
+        store = (f"out{j}[{off} + e] = ({expr}) != 0.0;" if v.dtype == N.RT_BOOL
+                 else f"out{j}[{off} + e] = ({ct})({expr});")
+        lines.append(f"  for (int e = lane; e < {p.out_count[j]}; e += 32) {{ const double z = __ldg(noise + nz + e); {store} }}")
+        lines.append(f"  nz += {p.out_count[j]};")
+    lines.append("}")
+    return "    {  // env (specialised)\n      " + "\n      ".join(lines) + "\n    }"
+
+
 def _gemm_call(lp, q, re, f64, soff):
     """Pick a shape-specialised GEMM body for a persistent-loop op."""
     T = "double" if f64 else "float"
@@ -326,13 +469,19 @@ def _gemm_call(lp, q, re, f64, soff):
     b_dt = q.B.dtype == (N.RT_F64 if f64 else N.RT_F32)
     aligned = q.B.off % 4 == 0 and all(q.B.off_env[e] % 4 == 0 for e in range(N.RT_MAXENV))
     q_ref = f"*(const rt_gemm_params*)(smem + {soff})"
+    tdt = N.RT_F64 if f64 else N.RT_F32
+    same_dt = q.A.dtype == tdt and q.C.dtype == tdt and (not q.bias.ptr or q.bias.dtype == tdt)
     if dense_1d and b_dt and mrp <= 8 and 64 <= Nn <= (256 if f64 else 512) and stage and \
             q.B.s2[0] == 1 and q.B.s1[0] == Nn and aligned and (Nn * it) % 16 == 0:
         kc = max(1, min(K, stage // (Nn * it)))
+        if same_dt:
+            return _gemm_literal(lp, q, re, f64, soff, True, kc)
         nc = 1 if Nn <= 256 else 2
         return (f"    gemm_tma_fixed<{T}, {mrp}, {nc}, {K}, {Nn}, {kc}>({q_ref}, env, r0 * {re}LL, "
                 f"r1 * {re}LL, sA32, ring);")
     if dense_1d and mrp <= 8 and Nn < 64 and K * Nn * it <= 4 * stage and K * mrp * it <= 64 * 1024:
+        if same_dt and q.B.dtype == q.A.dtype:
+            return _gemm_literal(lp, q, re, f64, soff, False)
         return (f"    gemm_small_fixed<{T}, {mrp}, {K}, {Nn}>({q_ref}, env, r0 * {re}LL, r1 * {re}LL, "
                 f"sA32, smem_u32(ring.buf));")
     return f"    gemm_op<{T}>({q_ref}, env, r0 * {re}LL, r1 * {re}LL, sA, ring);"
