@@ -63,7 +63,8 @@ enum rt_kernel {
   RT_K_SPLITK = 7,   /* split-K partial reduction for RT_K_GEMM               */
   RT_K_POLICY = 8,   /* reserved                                              */
   RT_K_LOOP = 9,     /* persistent kernel running a whole row-local loop      */
-  RT_K_GEMM_TC = 10  /* RT_K_GEMM on tcgen05 (3xTF32, TMEM accumulators)      */
+  RT_K_GEMM_TC = 10, /* RT_K_GEMM on tcgen05 (3xTF32, TMEM accumulators)      */
+  RT_K_THIN = 11     /* HBM-bound skinny GEMMs (narrow contraction / small K)  */
 };
 
 enum rt_status_code {
@@ -212,6 +213,28 @@ typedef struct {
   rt_gop C;
   rt_gop bias;
 } rt_splitk_params;
+
+/* RT_K_THIN: GEMMs with one narrow side, which are HBM-bound (the dW of a
+ * narrow layer over all T*E points, or a K<=32 product).  Names: W is the
+ * wide index (streamed, contiguous), R the narrow one, K the contraction.
+ *   variant 1: C[w,r] = sum_k X[k,w] * Y[k,r]   (K split over blockIdx.y,
+ *              fp32/fp64 partials part[s, w*part_w + r*part_r] -> RT_K_SPLITK)
+ *   variant 2: C[w,r] = epi(sum_k X[w,k] * Y[k,r] + bias[r])   (K <= 32)
+ * Strides: X.s1[0] along k, X.s2[0] along w; Y.s1[0] along k, Y.s2[0]
+ * along r; C.s1[0] along w, C.s2[0] along r; bias.s2[0] along r. */
+typedef struct {
+  rt_hdr h;
+  int32_t variant;
+  int32_t f64;
+  int64_t w, r, k;
+  int32_t splits;
+  int32_t accumulate;
+  int32_t epilogue;
+  int32_t _pad;
+  int64_t part_w, part_r;
+  uint64_t part;
+  rt_gop X, Y, C, bias;
+} rt_thin_params;
 
 /* Point coordinates for per-point entropy: coordinate j of the node's
  * domain point is box index coord_src[j] when >= 0, else env[-1-coord_src[j]]. */

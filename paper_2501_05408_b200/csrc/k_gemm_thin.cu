@@ -1,0 +1,134 @@
+// RT_K_THIN — the HBM-bound GEMMs of the MLP backward over T*E points.
+//
+// The symbolic backward (reference frontend.py:766-776, 984-989) turns every
+// per-point matmul into weight gradients summed over all T*E points.  When one
+// side is narrow (the 16-wide observation layer, the 4-wide action head) the
+// product is a stream over a [points, wide] activation with a handful of FMAs
+// per element: tensor-core tiles would mostly multiply padding, so these run
+// as coalesced streams at HBM speed instead.
+//
+//   variant 1  C[w,r] = sum_k X[k,w] * Y[k,r]   narrow contraction, K split
+//              over blockIdx.y; per-split partials -> RT_K_SPLITK
+//   variant 2  C[w,r] = epi(sum_k X[w,k] * Y[k,r] + bias[r]) for K <= 32
+//              (d(hidden) = d(logits) @ W^T: write-bound)
+#include "common.cuh"
+
+namespace {
+
+constexpr int THREADS = 256;
+constexpr int KT = 64;
+
+template <typename T, int R>
+__global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant__ rt_thin_params p) {
+  __shared__ __align__(16) T ys[KT][R];
+  const int64_t w = (int64_t)blockIdx.x * THREADS + threadIdx.x;
+  const bool wok = w < p.w;
+  const int s = blockIdx.y;
+  const int64_t per = ((p.k + p.splits - 1) / p.splits + KT - 1) / KT * KT;
+  const int64_t k0 = (int64_t)s * per;
+  const int64_t k1 = k0 + per < p.k ? k0 + per : p.k;
+  const T* X = (const T*)p.X.ptr + p.X.off;
+  const T* Y = (const T*)p.Y.ptr + p.Y.off;
+  const int64_t xk = p.X.s1[0], yk = p.Y.s1[0], yr = p.Y.s2[0];
+  const int nr = (int)p.r;
+  const T* xp = X + (wok ? w : 0) * p.X.s2[0];
+  T acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = (T)0;
+  for (int64_t kb = k0; kb < k1; kb += KT) {
+    const int nk = (int)(k1 - kb < KT ? k1 - kb : KT);
+    __syncthreads();
+    for (int i = threadIdx.x; i < KT * R; i += THREADS) {
+      const int kk = i / R, r = i - kk * R;
+      ys[kk][r] = (kk < nk && r < nr) ? __ldg(Y + (kb + kk) * yk + r * yr) : (T)0;
+    }
+    __syncthreads();
+    if (!wok) continue;
+    const T* xb = xp + kb * xk;
+    if (nk == KT) {
+#pragma unroll 16
+      for (int kk = 0; kk < KT; ++kk) {
+        const T x = __ldcs(xb + kk * xk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fma(x, ys[kk][r], acc[r]);
+      }
+    } else {
+      for (int kk = 0; kk < nk; ++kk) {
+        const T x = __ldcs(xb + kk * xk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fma(x, ys[kk][r], acc[r]);
+      }
+    }
+  }
+  if (!wok) return;
+  T* part = (T*)p.part + (int64_t)s * p.w * p.r;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r < nr) part[w * p.part_w + r * p.part_r] = acc[r];
+}
+
+// variant 2: rows of X (K <= 32 values each) times a resident [K, R] Y.
+template <typename T>
+__global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__ rt_thin_params p) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  constexpr int RT = 32;  // rows per tile
+  const int K = (int)p.k, R = (int)p.r;
+  T* ys = (T*)sm_raw;             // [K][R]
+  T* xs = ys + K * R;             // [RT][K]
+  T* bs = xs + RT * K;            // [R]
+  const T* X = (const T*)p.X.ptr + p.X.off;
+  const T* Y = (const T*)p.Y.ptr + p.Y.off;
+  T* Cp = (T*)p.C.ptr + p.C.off;
+  for (int i = threadIdx.x; i < K * R; i += THREADS) {
+    const int k = i / R, r = i - k * R;
+    ys[i] = Y[k * p.Y.s1[0] + r * p.Y.s2[0]];
+  }
+  for (int r = threadIdx.x; r < R; r += THREADS)
+    bs[r] = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + r * p.bias.s2[0])
+                       : (T)0;
+  const int64_t xw = p.X.s2[0], xk = p.X.s1[0], cw = p.C.s1[0], cr = p.C.s2[0];
+  const int64_t ntiles = (p.w + RT - 1) / RT;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t w0 = tile * RT;
+    const int nrow = (int)(p.w - w0 < RT ? p.w - w0 : RT);
+    __syncthreads();
+    for (int i = threadIdx.x; i < RT * K; i += THREADS) {
+      const int rr = i / K, k = i - rr * K;
+      xs[i] = rr < nrow ? __ldcs(X + (w0 + rr) * xw + k * xk) : (T)0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < R; r += THREADS) {
+      T yreg[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) yreg[k] = k < K ? ys[k * R + r] : (T)0;
+      const T b = bs[r];
+      for (int rr = 0; rr < nrow; ++rr) {
+        T a = (T)0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < K) a = fma(xs[rr * K + k], yreg[k], a);
+        T* cptr = Cp + (w0 + rr) * cw + r * cr;
+        if (p.accumulate) a += *cptr;
+        a += b;
+        if (p.epilogue == 1) a = vm_tanh<T>(a);
+        __stcs(cptr, a);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" void* rt_kernel_thin(int variant, int f64, int r) {
+  if (variant == 2) return f64 ? (void*)k_thin_smallk<double> : (void*)k_thin_smallk<float>;
+  if (f64) {
+    if (r <= 4) return (void*)k_thin_contract<double, 4>;
+    if (r <= 8) return (void*)k_thin_contract<double, 8>;
+    if (r <= 16) return (void*)k_thin_contract<double, 16>;
+    return (void*)k_thin_contract<double, 32>;
+  }
+  if (r <= 4) return (void*)k_thin_contract<float, 4>;
+  if (r <= 8) return (void*)k_thin_contract<float, 8>;
+  if (r <= 16) return (void*)k_thin_contract<float, 16>;
+  return (void*)k_thin_contract<float, 32>;
+}

@@ -106,26 +106,53 @@ __global__ void __launch_bounds__(1024) k_reduce_block(const __grid_constant__ r
 }
 
 // Column mode: outputs contiguous in the input (e.g. a bias gradient summed
-// over all T*E points of a [points, 256] tensor).  Pass 1: each thread owns
-// one output and a slice of the reduced range (coalesced across threads);
-// pass 2 sums the fp64 partials in a fixed order (deterministic).
+// over all T*E points of a [points, 256] tensor).  Pass 1: a block covers up
+// to 256 outputs; with fewer outputs, 256/total lanes per output walk the
+// rows interleaved and are combined in a fixed order in shared memory.  Each
+// blockIdx.y takes one slice of the reduced range.  Pass 2 sums the fp64
+// partials in a fixed order (deterministic).
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce_cols(const __grid_constant__ rt_reduce_params p) {
+  __shared__ double red[256];
   int64_t idx[RT_MAXD];
   int64_t len[4];
-  const int nd = p.box.nd;
-  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per_blk = p.total < 256 ? (int)p.total : 256;
+  const int lanes = 256 / per_blk;
+  const int oi = threadIdx.x % per_blk, lane = threadIdx.x / per_blk;
+  const int64_t o = (int64_t)blockIdx.x * per_blk + oi;
   const int s = blockIdx.y;
-  double* part = (double*)p.part;
-  if (o >= p.total) return;
-  decompose(p.box, o, idx);
-  int64_t base, tot;
-  red_setup<T>(p, idx, len, &base, &tot);
-  const int64_t per = (tot + p.splits - 1) / p.splits;
-  const int64_t k0 = s * per, k1 = min(tot, k0 + per);
   double acc = 0.0;
-  for (int64_t k = k0; k < k1; ++k) acc += red_term<T>(p, base, len, k);
-  part[(int64_t)s * p.total + o] = acc;
+  if (lane < lanes && o < p.total) {
+    decompose(p.box, o, idx);
+    int64_t base, tot;
+    red_setup<T>(p, idx, len, &base, &tot);
+    const int64_t per = (tot + p.splits - 1) / p.splits;
+    const int64_t k0 = s * per, k1 = min(tot, k0 + per);
+    const bool fast = p.nred == 1 && p.op == 0 &&
+                      p.in.dtype == (sizeof(T) == 8 ? RT_F64 : RT_F32);
+    if (fast) {
+      const T* src = (const T*)p.in.ptr + base;
+      const int64_t st = p.red_stride[0];
+      int64_t k = k0 + lane;
+      for (; k + 7 * lanes < k1; k += 8 * lanes) {
+        T x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = __ldcs(src + (k + u * lanes) * st);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += (double)x[u];
+      }
+      for (; k < k1; k += lanes) acc += (double)src[k * st];
+    } else {
+      for (int64_t k = k0 + lane; k < k1; k += lanes) acc += red_term<T>(p, base, len, k);
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (lane == 0 && o < p.total) {
+    double v = 0.0;
+    for (int l = 0; l < lanes; ++l) v += red[l * per_blk + oi];
+    ((double*)p.part)[(int64_t)s * p.total + o] = v;
+  }
 }
 
 __global__ void __launch_bounds__(256) k_reduce_cols_fin(const __grid_constant__ rt_reduce_params p) {

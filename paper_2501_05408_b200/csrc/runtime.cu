@@ -22,6 +22,7 @@ extern "C" void* rt_kernel_rng_fill();
 extern "C" void* rt_kernel_policy(const void* params);
 extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
+extern "C" void* rt_kernel_thin(int variant, int f64, int r);
 
 static thread_local std::string g_err;
 
@@ -135,6 +136,14 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_gop(p->C, env, nenv);
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
       return rt_kernel_gemm_tc();
+    }
+    case RT_K_THIN: {
+      rt_thin_params* p = (rt_thin_params*)blk;
+      fold_gop(p->X, env, nenv);
+      fold_gop(p->Y, env, nenv);
+      fold_gop(p->C, env, nenv);
+      if (p->bias.ptr) fold_gop(p->bias, env, nenv);
+      return rt_kernel_thin(p->variant, p->f64, (int)p->r);
     }
     case RT_K_SPLITK: {
       rt_splitk_params* p = (rt_splitk_params*)blk;

@@ -1110,7 +1110,7 @@ class Lowering:
                          and not any(p.len_env[j][e] for e in range(N.RT_MAXENV))
                          for j in range(p.nred))
         if const_lens and p.box.nd >= 1 and p.in_.stride[p.box.nd - 1] == 1 and \
-                maxlen >= 4096 and p.total >= 32 and p.total * maxlen >= (1 << 22):
+                maxlen >= 4096 and p.total * maxlen >= (1 << 20):
             ob = (p.total + 255) // 256
             splits = int(max(1, min(maxlen // 256, (148 * 8) // ob, 1024)))
             p.splits = splits
@@ -1355,6 +1355,9 @@ class Lowering:
         p.epilogue = epilogue
         if bias is not None:
             p.bias = bias
+        if not self._capture_active() and self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
+                                                          epilogue, bias):
+            return
         if self.use_tc and self._tc_ok(p, A, B, Cc):
             return self._gemm_tc(p, label, accumulate, epilogue, bias)
         tiles = ((p.m + 63) // 64) * ((p.n + 63) // 64) * p.z
@@ -1384,6 +1387,92 @@ class Lowering:
         else:
             grid = [(p.n + 63) // 64, (p.m + 63) // 64, p.z]
             self.add_rec(N.RT_K_GEMM, p, grid, [256, 1, 1], 0, label)
+
+    @staticmethod
+    def _collapse(lst, cols):
+        """Merge the (extent, strides...) dims of a GEMM box into one dim when
+        every operand in `cols` walks them contiguously; None otherwise."""
+        dims = [t for t in lst if t[0] != 1]
+        if not dims:
+            return 1, [0] * len(cols)
+        ext, st = dims[-1][0], [dims[-1][c] for c in cols]
+        for t in reversed(dims[:-1]):
+            if any(t[c] != st[i] * ext for i, c in enumerate(cols)):
+                return None
+            ext *= t[0]
+        return ext, st
+
+    THIN_MAX_R = 32
+    THIN_MIN_K = 4096
+
+    def _gemm_thin(self, p, Z, M, Nn, K, label, accumulate, epilogue, bias):
+        """Narrow GEMMs -> RT_K_THIN (csrc/k_gemm_thin.cu); False if not one."""
+        if p.z != 1 or any(t[0] != 1 for t in Z):
+            return False
+        mc, nc, kc = self._collapse(M, (1, 3)), self._collapse(Nn, (2, 3)), self._collapse(K, (1, 2))
+        if mc is None or nc is None or kc is None:
+            return False
+        (m, (a_m, c_m)), (n, (b_n, c_n)), (k, (a_k, b_k)) = mc, nc, kc
+        dt = [self._gop_dtype(x) for x in (p.A, p.B, p.C)]
+        f64 = dt == ["f64"] * 3
+        if not (f64 or dt == ["f32"] * 3):
+            return False
+        q = N.rt_thin_params()
+        q.f64 = int(f64)
+        esize = 8 if f64 else 4
+
+        def gop(src, s1, s2):
+            g = N.rt_gop()
+            C.memmove(C.addressof(g), C.addressof(src), C.sizeof(g))
+            for arr in (g.sz, g.s1, g.s2):
+                for i in range(4):
+                    arr[i] = 0
+            g.s1[0], g.s2[0] = s1, s2
+            return g
+
+        if k >= self.THIN_MIN_K and (n <= self.THIN_MAX_R < m and a_m == 1
+                                      or m <= self.THIN_MAX_R < n and b_n == 1):
+            q.variant = 1
+            if n <= self.THIN_MAX_R and a_m == 1:
+                q.w, q.r = m, n
+                q.X, q.Y = gop(p.A, a_k, a_m), gop(p.B, b_k, b_n)
+                q.part_w, q.part_r = n, 1
+            else:
+                q.w, q.r = n, m
+                q.X, q.Y = gop(p.B, b_k, b_n), gop(p.A, a_k, a_m)
+                q.part_w, q.part_r = 1, n
+            q.k = k
+            gx = (q.w + 255) // 256
+            q.splits = int(max(1, min(k // 256, (148 * 8) // gx, 65535)))
+            q.part = self.alloc(q.splits * m * n * esize)
+            self.add_rec(N.RT_K_THIN, q, [gx, q.splits, 1], [256, 1, 1], 0, label)
+            r = N.rt_splitk_params()
+            r.Z, r.M, r.N = p.Z, p.M, p.N
+            r.z, r.m, r.n = p.z, p.m, p.n
+            r.splits, r.f64, r.accumulate, r.epilogue = q.splits, q.f64, accumulate, epilogue
+            r.part, r.C = q.part, p.C
+            if bias is not None:
+                r.bias = bias
+            self.add_rec(N.RT_K_SPLITK, r, self.grid1(p.m * p.n), [256, 1, 1], 0, label)
+            return True
+        smem = (k * n + 32 * k + n) * esize
+        if k <= 32 and m >= 4096 and c_n == 1 and smem <= 48 * 1024 and \
+                (bias is None or len(Nn) == 1):
+            q.variant = 2
+            q.w, q.r, q.k = m, n, k
+            q.X, q.Y = gop(p.A, a_k, a_m), gop(p.B, b_k, b_n)
+            q.C = gop(p.C, c_m, c_n)
+            if bias is not None:
+                q.bias = gop(bias, 0, bias.s2[0])
+            q.accumulate, q.epilogue = accumulate, epilogue
+            grid = [int(min((m + 31) // 32, 148 * 8)), 1, 1]
+            self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
+            return True
+        return False
+
+    @staticmethod
+    def _gop_dtype(g):
+        return {v: k for k, v in N.DTYPE_CODE.items()}[g.dtype]
 
     TC_MIN_MACS = 1 << 26
 

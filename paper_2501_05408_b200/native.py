@@ -27,6 +27,7 @@ RT_K_EW, RT_K_REDUCE, RT_K_SCAN, RT_K_GEMM, RT_K_RNG, RT_K_UDF, RT_K_SPLITK, RT_
     1, 2, 3, 4, 5, 6, 7, 8
 RT_K_LOOP = 9
 RT_K_GEMM_TC = 10
+RT_K_THIN = 11
 TC_SMEM = 2 * (2 * 128 * 32 * 4 + 2 * 256 * 32 * 4)
 
 RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK = 1, 2, 3, 4, 6
@@ -96,6 +97,13 @@ class rt_splitk_params(C.Structure):
                 ("z", i64), ("m", i64), ("n", i64), ("splits", i32), ("f64", i32),
                 ("accumulate", i32), ("epilogue", i32), ("part", u64), ("C", rt_gop),
                 ("bias", rt_gop)]
+
+
+class rt_thin_params(C.Structure):
+    _fields_ = [("h", rt_hdr), ("variant", i32), ("f64", i32), ("w", i64), ("r", i64), ("k", i64),
+                ("splits", i32), ("accumulate", i32), ("epilogue", i32), ("_pad", i32),
+                ("part_w", i64), ("part_r", i64), ("part", u64), ("X", rt_gop), ("Y", rt_gop),
+                ("C", rt_gop), ("bias", rt_gop)]
 
 
 class rt_rng_params(C.Structure):

@@ -9,7 +9,8 @@ from . import native as N
 ITEM = {N.RT_F64: 8, N.RT_F32: 4, N.RT_I64: 8, N.RT_BOOL: 1}
 FAMILY = {N.RT_K_EW: "ew", N.RT_K_REDUCE: "reduce", N.RT_K_SCAN: "scan", N.RT_K_GEMM: "gemm",
           N.RT_K_RNG: "rng", N.RT_K_UDF: "udf", N.RT_K_SPLITK: "splitk",
-          N.RT_K_POLICY: "policy", N.RT_K_LOOP: "loop", N.RT_K_GEMM_TC: "gemm_tc"}
+          N.RT_K_POLICY: "policy", N.RT_K_LOOP: "loop", N.RT_K_GEMM_TC: "gemm_tc",
+          N.RT_K_THIN: "thin"}
 
 
 def _prod(xs):
@@ -69,6 +70,12 @@ def cost(kernel, p, loop_info=None):
         eb = _gop_elems(p.B, p.Z, p.K, p.N, 1) * ITEM.get(p.B.dtype, 4)
         ec = p.z * p.m * p.n * ITEM.get(p.C.dtype, 4)
         return ea + eb + ec, fl
+    if kernel == N.RT_K_THIN:
+        it = 8 if p.f64 else 4
+        if p.variant == 1:   # stream X[k, w], Y[k, r]; partials out
+            return (p.k * (p.w + p.r) + p.splits * p.w * p.r) * it, 2 * p.w * p.r * p.k
+        return (p.w * p.k + p.k * p.r + p.w * p.r * (2 if p.accumulate else 1)) * it, \
+            2 * p.w * p.r * p.k
     if kernel == N.RT_K_RNG:
         return p.total * p.count * ITEM.get(p.out.dtype, 4), 0
     if kernel == N.RT_K_UDF:

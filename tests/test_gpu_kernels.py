@@ -20,21 +20,21 @@ def graph(dims):
                                                                      zip(dims, [None] * len(dims))})
 
 
-def mm_graph(B, K, N, contract=False):
+def mm_graph(B, K, N, contract=False, dt="f32"):
     """y[b] = x[b] @ W  (rows GEMM, M = B)      or
        s = sum(permute(x[b]) @ g[b], b)        (contraction GEMM, K = B)."""
     g = ir.Graph(["b"], {"b": "B"}, {"B": B})
-    g.nodes[0] = ir.Node(0, "x", "input", ("b",), ((1, K),), ("f32",))
+    g.nodes[0] = ir.Node(0, "x", "input", ("b",), ((1, K),), (dt,))
     if not contract:
-        g.nodes[1] = ir.Node(1, "W", "input", (), ((K, N),), ("f32",))
-        g.nodes[2] = ir.Node(2, "y", "matmul", ("b",), ((1, N),), ("f32",), {}, 2)
+        g.nodes[1] = ir.Node(1, "W", "input", (), ((K, N),), (dt,))
+        g.nodes[2] = ir.Node(2, "y", "matmul", ("b",), ((1, N),), (dt,), {}, 2)
         g.edges += [ir.Edge(2, 0, (S("b"),), None, 0, 0), ir.Edge(2, 1, (), None, 0, 1)]
         g.outputs = [("y", 2, 0)]
     else:
-        g.nodes[1] = ir.Node(1, "gr", "input", ("b",), ((1, N),), ("f32",))
-        g.nodes[2] = ir.Node(2, "xt", "permute", ("b",), ((K, 1),), ("f32",), {"order": (1, 0)}, 1)
-        g.nodes[3] = ir.Node(3, "op", "matmul", ("b",), ((K, N),), ("f32",), {}, 2)
-        g.nodes[4] = ir.Node(4, "s", "sum", (), ((K, N),), ("f32",), {"dims": (0,)}, 1)
+        g.nodes[1] = ir.Node(1, "gr", "input", ("b",), ((1, N),), (dt,))
+        g.nodes[2] = ir.Node(2, "xt", "permute", ("b",), ((K, 1),), (dt,), {"order": (1, 0)}, 1)
+        g.nodes[3] = ir.Node(3, "op", "matmul", ("b",), ((K, N),), (dt,), {}, 2)
+        g.nodes[4] = ir.Node(4, "s", "sum", (), ((K, N),), (dt,), {"dims": (0,)}, 1)
         g.edges += [ir.Edge(2, 0, (S("b"),), None, 0, 0),
                     ir.Edge(3, 0, (S("b"),), None, 0, 2), ir.Edge(3, 1, (S("b"),), None, 0, 1),
                     ir.Edge(4, 0, (("slice", ("int", 0), S("B", "bound")),), None, 0, 3)]
@@ -80,3 +80,58 @@ def test_suffix_dsum_scan_at_c2_scale():
         acc = r[:, t].astype(np.float64) + 0.99 * acc
         want[:, t] = acc
     np.testing.assert_allclose(out, want.astype(np.float32), rtol=1e-5, atol=1e-5)
+
+
+def _kinds(g, inputs):
+    from paper_2501_05408_b200 import get_executable
+    exe, _ = get_executable(g, None, inputs, seed=0)
+    return {r[0] for r in exe.recs}
+
+
+@pytest.mark.parametrize("K,N,dt", [(256, 4, "f32"), (16, 256, "f32"), (256, 4, "f64"),
+                                    (16, 200, "f32"), (3, 256, "f32")])
+def test_thin_contraction(K, N, dt):
+    """dW of a narrow layer over all points (frontend.py:766-776 backward):
+    RT_K_THIN variant 1 + split-K partial sum."""
+    from paper_2501_05408_b200 import native as NN
+    B = 20000
+    npdt = np.float64 if dt == "f64" else np.float32
+    rng = np.random.default_rng(K * 1000 + N)
+    x = rng.standard_normal((B, 1, K)).astype(npdt)
+    gr = rng.standard_normal((B, 1, N)).astype(npdt)
+    g = mm_graph(B, K, N, contract=True, dt=dt)
+    assert NN.RT_K_THIN in _kinds(g, {"x": x, "gr": gr})
+    out = execute(g, inputs={"x": x, "gr": gr})["s"]
+    want = np.einsum("bk,bn->kn", x[:, 0].astype(np.float64), gr[:, 0].astype(np.float64))
+    tol = 1e-12 if dt == "f64" else 1e-5
+    np.testing.assert_allclose(out, want.astype(npdt), rtol=tol, atol=tol * np.sqrt(B) * 10)
+
+
+@pytest.mark.parametrize("K,N", [(4, 256), (16, 300), (1, 64)])
+def test_thin_small_k_rows(K, N):
+    """y[b] = x[b] @ W with K <= 32 (write-bound): RT_K_THIN variant 2."""
+    from paper_2501_05408_b200 import native as NN
+    B = 9000
+    rng = np.random.default_rng(K + N)
+    x = rng.standard_normal((B, 1, K)).astype(np.float32)
+    W = rng.standard_normal((K, N)).astype(np.float32)
+    g = mm_graph(B, K, N)
+    assert NN.RT_K_THIN in _kinds(g, {"x": x, "W": W})
+    out = execute(g, inputs={"x": x, "W": W})["y"]
+    want = (x.astype(np.float64) @ W.astype(np.float64)).astype(np.float32)
+    np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("N", [256, 4, 37])
+def test_column_reduce(N):
+    """bias gradient: s = sum(g[0:B]) over many points (runtime.py:95-96)."""
+    B = 50000
+    g = ir.Graph(["b"], {"b": "B"}, {"B": B})
+    g.nodes[0] = ir.Node(0, "gr", "input", ("b",), ((N,),), ("f32",))
+    g.nodes[1] = ir.Node(1, "s", "sum", (), ((N,),), ("f32",), {"dims": (0,)}, 1)
+    g.edges.append(ir.Edge(1, 0, (("slice", ("int", 0), S("B", "bound")),), None, 0, 0))
+    g.outputs = [("s", 1, 0)]
+    gr = np.random.default_rng(N).standard_normal((B, N)).astype(np.float32)
+    out = execute(g, inputs={"gr": gr})["s"]
+    want = gr.astype(np.float64).sum(0).astype(np.float32)
+    np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-4)

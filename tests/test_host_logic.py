@@ -38,7 +38,7 @@ def test_struct_layouts_match_header(tmp_path):
     src = tmp_path / "sz.c"
     names = ["rt_box", "rt_view", "rt_hdr", "rt_ew_params", "rt_reduce_params",
              "rt_scan_params", "rt_gemm_params", "rt_splitk_params", "rt_rng_params",
-             "rt_udf_params", "rt_launch_rec", "rt_instr", "rt_gop"]
+             "rt_udf_params", "rt_launch_rec", "rt_instr", "rt_gop", "rt_thin_params"]
     src.write_text('#include <stdio.h>\n#include "rtb200.h"\nint main(){' +
                    "".join(f'printf("%zu\\n", sizeof({n}));' for n in names) + "}")
     exe = tmp_path / "sz"
@@ -131,3 +131,21 @@ def test_every_touched_buffer_is_materialised(case):
         for op in low.loop_subs.get(ri, {}).get("ops", ()):
             ptrs |= memplan.touched_ptrs(op[1])
         assert ptrs <= valid, (ri, [hex(x) for x in ptrs - valid])
+
+
+def test_thin_gemm_selection():
+    """Narrow GEMMs over many points lower to RT_K_THIN, square ones don't."""
+    from test_gpu_kernels import mm_graph
+    cases = [((20000, 256, 4, True), 1), ((20000, 16, 256, True), 1),
+             ((9000, 4, 256, False), 2), ((20000, 256, 256, True), None),
+             ((9000, 256, 256, False), None)]
+    for (B, K, Nn, contract), variant in cases:
+        g = mm_graph(B, K, Nn, contract=contract)
+        _, low, _, _ = dry_lower(g, {"B": B})
+        thin = [r[1] for r in low.recs if r[0] == N.RT_K_THIN]
+        if variant is None:
+            assert not thin
+        else:
+            assert thin and thin[0].variant == variant
+            if variant == 1:
+                assert any(r[0] == N.RT_K_SPLITK for r in low.recs)
