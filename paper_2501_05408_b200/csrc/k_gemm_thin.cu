@@ -67,50 +67,54 @@ __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant
     if (r < nr) part[w * p.part_w + r * p.part_r] = acc[r];
 }
 
-// variant 2: rows of X (K <= 32 values each) times a resident [K, R] Y.
-template <typename T>
+// variant 2: rows of X (K <= KP values each, zero-padded to KP) times a
+// resident [KP, R] Y; each thread owns output columns, rows stream through
+// a shared-memory tile, stores are coalesced along r.
+template <typename T, int KP>
 __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__ rt_thin_params p) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  constexpr int RT = 32;  // rows per tile
+  constexpr int RT = 64;  // rows per tile
   const int K = (int)p.k, R = (int)p.r;
-  T* ys = (T*)sm_raw;             // [K][R]
-  T* xs = ys + K * R;             // [RT][K]
-  T* bs = xs + RT * K;            // [R]
+  T* ys = (T*)sm_raw;             // [KP][R]
+  T* xs = ys + KP * R;            // [RT][KP]
+  T* bs = xs + RT * KP;           // [R]
   const T* X = (const T*)p.X.ptr + p.X.off;
   const T* Y = (const T*)p.Y.ptr + p.Y.off;
   T* Cp = (T*)p.C.ptr + p.C.off;
-  for (int i = threadIdx.x; i < K * R; i += THREADS) {
+  for (int i = threadIdx.x; i < KP * R; i += THREADS) {
     const int k = i / R, r = i - k * R;
-    ys[i] = Y[k * p.Y.s1[0] + r * p.Y.s2[0]];
+    ys[i] = k < K ? Y[k * p.Y.s1[0] + r * p.Y.s2[0]] : (T)0;
   }
   for (int r = threadIdx.x; r < R; r += THREADS)
     bs[r] = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + r * p.bias.s2[0])
                        : (T)0;
   const int64_t xw = p.X.s2[0], xk = p.X.s1[0], cw = p.C.s1[0], cr = p.C.s2[0];
   const int64_t ntiles = (p.w + RT - 1) / RT;
+  const bool acc_in = p.accumulate != 0, tanh_epi = p.epilogue == 1;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t w0 = tile * RT;
     const int nrow = (int)(p.w - w0 < RT ? p.w - w0 : RT);
     __syncthreads();
-    for (int i = threadIdx.x; i < RT * K; i += THREADS) {
-      const int rr = i / K, k = i - rr * K;
-      xs[i] = rr < nrow ? __ldcs(X + (w0 + rr) * xw + k * xk) : (T)0;
+    for (int i = threadIdx.x; i < RT * KP; i += THREADS) {
+      const int rr = i / KP, k = i - rr * KP;
+      xs[i] = (rr < nrow && k < K) ? __ldcs(X + (w0 + rr) * xw + k * xk) : (T)0;
     }
     __syncthreads();
     for (int r = threadIdx.x; r < R; r += THREADS) {
-      T yreg[32];
+      T yreg[KP];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) yreg[k] = k < K ? ys[k * R + r] : (T)0;
+      for (int k = 0; k < KP; ++k) yreg[k] = ys[k * R + r];
       const T b = bs[r];
+      T* cbase = Cp + w0 * cw + r * cr;
+#pragma unroll 4
       for (int rr = 0; rr < nrow; ++rr) {
         T a = (T)0;
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < K) a = fma(xs[rr * K + k], yreg[k], a);
-        T* cptr = Cp + (w0 + rr) * cw + r * cr;
-        if (p.accumulate) a += *cptr;
+        for (int k = 0; k < KP; ++k) a = fma(xs[rr * KP + k], yreg[k], a);
+        T* cptr = cbase + rr * cw;
+        if (acc_in) a += *cptr;
         a += b;
-        if (p.epilogue == 1) a = vm_tanh<T>(a);
+        if (tanh_epi) a = vm_tanh<T>(a);
         __stcs(cptr, a);
       }
     }
@@ -120,7 +124,19 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
 }  // namespace
 
 extern "C" void* rt_kernel_thin(int variant, int f64, int r) {
-  if (variant == 2) return f64 ? (void*)k_thin_smallk<double> : (void*)k_thin_smallk<float>;
+  if (variant == 2) {
+    // r carries K for this variant (see lower.py _gemm_thin)
+    if (f64) {
+      if (r <= 4) return (void*)k_thin_smallk<double, 4>;
+      if (r <= 8) return (void*)k_thin_smallk<double, 8>;
+      if (r <= 16) return (void*)k_thin_smallk<double, 16>;
+      return (void*)k_thin_smallk<double, 32>;
+    }
+    if (r <= 4) return (void*)k_thin_smallk<float, 4>;
+    if (r <= 8) return (void*)k_thin_smallk<float, 8>;
+    if (r <= 16) return (void*)k_thin_smallk<float, 16>;
+    return (void*)k_thin_smallk<float, 32>;
+  }
   if (f64) {
     if (r <= 4) return (void*)k_thin_contract<double, 4>;
     if (r <= 8) return (void*)k_thin_contract<double, 8>;

@@ -105,6 +105,44 @@ __global__ void __launch_bounds__(1024) k_reduce_block(const __grid_constant__ r
   }
 }
 
+// Warp mode: one warp per output for medium contiguous ranges (e.g. the
+// per-point sum over a 256-wide payload axis): lanes read consecutive
+// elements, fixed shuffle tree (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_warp(const __grid_constant__ rt_reduce_params p) {
+  int64_t idx[RT_MAXD];
+  int64_t len[4];
+  const int nd = p.box.nd;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const bool fast = p.nred == 1 && p.op == 0 && p.in.dtype == (sizeof(T) == 8 ? RT_F64 : RT_F32);
+  for (int64_t flat = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); flat < p.total;
+       flat += nw) {
+    decompose(p.box, flat, idx);
+    int64_t base, tot;
+    red_setup<T>(p, idx, len, &base, &tot);
+    double acc = 0.0;
+    if (fast) {
+      const T* src = (const T*)p.in.ptr + base;
+      const int64_t st = p.red_stride[0];
+      int64_t k = lane;
+      for (; k + 96 < tot; k += 128) {
+        T x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = src[(k + 32 * u) * st];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc += (double)x[u];
+      }
+      for (; k < tot; k += 32) acc += (double)src[k * st];
+    } else {
+      for (int64_t k = lane; k < tot; k += 32) acc += red_term<T>(p, base, len, k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) store_as<double>((void*)p.out.ptr, p.out.dtype, view_off(p.out, nd, idx), acc);
+  }
+}
+
 // Column mode: outputs contiguous in the input (e.g. a bias gradient summed
 // over all T*E points of a [points, 256] tensor).  Pass 1: a block covers up
 // to 256 outputs; with fewer outputs, 256/total lanes per output walk the
@@ -172,7 +210,8 @@ extern "C" void* rt_kernel_reduce_cols(int f64, int fin) {
   return f64 ? (void*)k_reduce_cols<double> : (void*)k_reduce_cols<float>;
 }
 
-extern "C" void* rt_kernel_reduce(int f64, int block) {
-  if (block) return f64 ? (void*)k_reduce_block<double> : (void*)k_reduce_block<float>;
+extern "C" void* rt_kernel_reduce(int f64, int tpo) {
+  if (tpo == 32) return f64 ? (void*)k_reduce_warp<double> : (void*)k_reduce_warp<float>;
+  if (tpo > 1) return f64 ? (void*)k_reduce_block<double> : (void*)k_reduce_block<float>;
   return f64 ? (void*)k_reduce_thread<double> : (void*)k_reduce_thread<float>;
 }

@@ -11,7 +11,7 @@
 #include "../../include/rtb200.h"
 
 extern "C" void* rt_kernel_ew(int f64);
-extern "C" void* rt_kernel_reduce(int f64, int block);
+extern "C" void* rt_kernel_reduce(int f64, int tpo);
 extern "C" void* rt_kernel_reduce_cols(int f64, int fin);
 extern "C" void* rt_kernel_scan(int f64, int warp);
 extern "C" void* rt_kernel_gemm(int f64);
@@ -112,7 +112,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       for (int j = 0; j < p->nred; ++j)
         for (int e = 0; e < nenv && e < RT_MAXENV; ++e) p->len0[j] += env[e] * p->len_env[j][e];
       if (p->part) return rt_kernel_reduce_cols(p->f64, p->threads_per_out == -1);
-      return rt_kernel_reduce(p->f64, p->threads_per_out > 1);
+      return rt_kernel_reduce(p->f64, p->threads_per_out);
     }
     case RT_K_SCAN: {
       rt_scan_params* p = (rt_scan_params*)blk;
@@ -143,7 +143,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_gop(p->Y, env, nenv);
       fold_gop(p->C, env, nenv);
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
-      return rt_kernel_thin(p->variant, p->f64, (int)p->r);
+      return rt_kernel_thin(p->variant, p->f64, (int)(p->variant == 2 ? p->k : p->r));
     }
     case RT_K_SPLITK: {
       rt_splitk_params* p = (rt_splitk_params*)blk;

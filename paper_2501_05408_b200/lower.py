@@ -1125,6 +1125,10 @@ class Lowering:
             p.threads_per_out = tpo
             grid = [max(1, min(p.total, 148 * 16)), 1, 1]
             block = [tpo, 1, 1]
+        elif maxlen >= 32 and p.nred == 1 and abs(p.red_stride[0]) == 1:
+            p.threads_per_out = 32
+            grid = [max(1, min((p.total + 7) // 8, 148 * 16)), 1, 1]
+            block = [256, 1, 1]
         else:
             p.threads_per_out = 1
             grid = self.grid1(p.total)
@@ -1455,7 +1459,8 @@ class Lowering:
                 r.bias = bias
             self.add_rec(N.RT_K_SPLITK, r, self.grid1(p.m * p.n), [256, 1, 1], 0, label)
             return True
-        smem = (k * n + 32 * k + n) * esize
+        kp = 4 if k <= 4 else 8 if k <= 8 else 16 if k <= 16 else 32
+        smem = (kp * n + 64 * kp + n) * esize
         if k <= 32 and m >= 4096 and c_n == 1 and smem <= 48 * 1024 and \
                 (bias is None or len(Nn) == 1):
             q.variant = 2
@@ -1465,7 +1470,7 @@ class Lowering:
             if bias is not None:
                 q.bias = gop(bias, 0, bias.s2[0])
             q.accumulate, q.epilogue = accumulate, epilogue
-            grid = [int(min((m + 31) // 32, 148 * 8)), 1, 1]
+            grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
             self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
             return True
         return False

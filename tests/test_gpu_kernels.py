@@ -85,7 +85,7 @@ def test_suffix_dsum_scan_at_c2_scale():
 def _kinds(g, inputs):
     from paper_2501_05408_b200 import get_executable
     exe, _ = get_executable(g, None, inputs, seed=0)
-    return {r[0] for r in exe.recs}
+    return {r.kernel for r in exe.recs}
 
 
 @pytest.mark.parametrize("K,N,dt", [(256, 4, "f32"), (16, 256, "f32"), (256, 4, "f64"),
@@ -135,3 +135,19 @@ def test_column_reduce(N):
     out = execute(g, inputs={"gr": gr})["s"]
     want = gr.astype(np.float64).sum(0).astype(np.float32)
     np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("W", [256, 40])
+def test_warp_reduce_per_point(W):
+    """s[b] = sum(g[b]) over a W-wide payload axis for many points
+    (runtime.py:95-96; warp-per-output mode)."""
+    B = 70000
+    g = ir.Graph(["b"], {"b": "B"}, {"B": B})
+    g.nodes[0] = ir.Node(0, "gr", "input", ("b",), ((W,),), ("f32",))
+    g.nodes[1] = ir.Node(1, "s", "sum", ("b",), ((),), ("f32",), {"dims": (0,)}, 1)
+    g.edges.append(ir.Edge(1, 0, (S("b"),), None, 0, 0))
+    g.outputs = [("s", 1, 0)]
+    gr = np.random.default_rng(W).standard_normal((B, W)).astype(np.float32)
+    out = execute(g, inputs={"gr": gr})["s"]
+    want = gr.astype(np.float64).sum(1).astype(np.float32)
+    np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-5)
