@@ -64,7 +64,8 @@ enum rt_kernel {
   RT_K_POLICY = 8,   /* reserved                                              */
   RT_K_LOOP = 9,     /* persistent kernel running a whole row-local loop      */
   RT_K_GEMM_TC = 10, /* RT_K_GEMM on tcgen05 (3xTF32, TMEM accumulators)      */
-  RT_K_THIN = 11     /* HBM-bound skinny GEMMs (narrow contraction / small K)  */
+  RT_K_THIN = 11,    /* HBM-bound skinny GEMMs (narrow contraction / small K)  */
+  RT_K_GEMM_TMA = 12 /* RT_K_GEMM on tcgen05 fed by TMA (plain 2-D operands)   */
 };
 
 enum rt_status_code {

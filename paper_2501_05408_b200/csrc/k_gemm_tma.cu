@@ -1,0 +1,335 @@
+// RT_K_GEMM_TMA — the learner GEMMs of the PDG backward on tcgen05 with a
+// TMA-fed, warp-specialised pipeline (3xTF32 for fp32 accuracy; reference
+// products are fp32 np.matmul, runtime.py:249; north_star tolerance 1e-5).
+//
+//   dX = G @ W^T over all T*E points   (M = 1M rows, K-major operands)
+//   dW = sum_points x^T g              (K = 1M points, MN-major operands, split-K)
+//
+// Roles (320 threads):
+//   warp 8 lane 0  TMA producer: raw fp32 tiles -> smem ring (SWIZZLE_64B
+//                  K-major or SWIZZLE_128B MN-major canonical UMMA layouts)
+//   warps 0-7      converters: in place hi = tf32(x), lo = tf32(x - hi) into a
+//                  twin buffer (elementwise, so layout-agnostic and
+//                  conflict-free), then the epilogue (TMEM -> global)
+//   warp 9 lane 0  MMA issuer: hi*hi + hi*lo + lo*hi per K=8 step, commit
+//                  releases the stage back to the producer
+// Stage = A(128 x 16) + B(256 x 16) fp32, hi and lo: 48 KB; 4 stages.
+// Operands must be plain 2-D (collapsed boxes), one unit-stride dim, 16-byte
+// aligned — lower.py checks that, else RT_K_GEMM_TC (generic staging) runs.
+#include <cuda.h>
+#include "common.cuh"
+
+#define TM_BM 128
+#define TM_BN 256
+#define TM_BK 16
+#define TM_ST 4
+#define TM_CONV 256
+#define TM_THREADS (TM_CONV + 64)
+#define TM_A_BYTES (TM_BM * TM_BK * 4)
+#define TM_B_BYTES (TM_BN * TM_BK * 4)
+#define TM_STAGE (2 * TM_A_BYTES + 2 * TM_B_BYTES)
+#define TM_SMEM (TM_ST * TM_STAGE + 1024)
+
+struct tm_args {
+  CUtensorMap ta;
+  CUtensorMap tb;
+  rt_gemm_params p;
+  int32_t a_mn, b_mn;      // operand is MN-major (unit stride along M / N)
+  int64_t c_m, c_n;        // collapsed C strides
+  int64_t bias_n;          // collapsed bias stride along N
+};
+
+namespace {
+
+RT_DEV uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+RT_DEV void mb_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+RT_DEV void mb_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+  }
+}
+RT_DEV void mb_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+RT_DEV void mb_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+RT_DEV void tma2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+// smem matrix descriptor (sm_100 version 1), layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
+RT_DEV uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+RT_DEV void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+      ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+RT_DEV void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(bar) : "memory");
+}
+RT_DEV uint32_t rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// descriptor of operand tile at `base` for MMA K-step ks (8 fp32 of K)
+RT_DEV uint64_t op_desc(uint32_t base, int ks, int mn) {
+  if (mn)  // MN-major SW128: 32-wide MN atoms 2 KB apart (LBO), 8-k groups 1 KB apart (SBO)
+    return sdesc(base + ks * 1024, 2048, 1024, 2);
+  // K-major SW64: 64 B rows, 8-row groups 512 B apart; K-step = +32 B
+  return sdesc(base + ks * 32, 16, 512, 4);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma(const __grid_constant__ tm_args a) {
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[TM_ST], conv[TM_ST], empty[TM_ST], done;
+  __shared__ uint32_t tmem_s;
+  const rt_gemm_params& p = a.p;
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = su32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * TM_BM;
+  const int64_t n0 = (int64_t)blockIdx.x * TM_BN;
+  const int64_t nrem = p.n - n0;
+  const int split = blockIdx.z;
+  // MMA N: multiple of 16 (K-major B) / of 32 (MN-major B, whole 32-wide atoms)
+  const int BN = nrem >= TM_BN ? TM_BN
+               : a.b_mn ? (int)((nrem + 31) / 32 * 32) : (int)((nrem + 15) / 16 * 16);
+  const int nbB = a.b_mn ? BN / 32 : 1;
+  const uint32_t bytesB = a.b_mn ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
+
+  if (tid == 0) {
+    for (int i = 0; i < TM_ST; ++i) {
+      mb_init(su32(&full[i]), 1);
+      mb_init(su32(&conv[i]), TM_CONV);
+      mb_init(su32(&empty[i]), 1);
+    }
+    mb_init(su32(&done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;"
+                 ::"r"(su32(&tmem_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_s;
+
+  const int64_t kper = ((p.k + p.splits - 1) / p.splits + TM_BK - 1) / TM_BK * TM_BK;
+  const int64_t kbeg = split * kper;
+  const int64_t kend = p.k < kbeg + kper ? p.k : kbeg + kper;
+  const int ntiles = kend > kbeg ? (int)((kend - kbeg + TM_BK - 1) / TM_BK) : 0;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int kt = 0; kt < ntiles; ++kt) {
+        const int s = kt % TM_ST;
+        if (kt >= TM_ST) mb_wait(su32(&empty[s]), (uint32_t)(((kt / TM_ST) - 1) & 1));
+        const uint32_t st = sbase + s * TM_STAGE;
+        const uint32_t fb = su32(&full[s]);
+        mb_expect(fb, TM_A_BYTES + bytesB);
+        const int32_t k0 = (int32_t)(kbeg + (int64_t)kt * TM_BK);
+        if (a.a_mn)
+          for (int j = 0; j < TM_BM / 32; ++j)
+            tma2d(st + j * 2048, &a.ta, (int32_t)(m0 + 32 * j), k0, fb);
+        else
+          tma2d(st, &a.ta, k0, (int32_t)m0, fb);
+        const uint32_t sb = st + 2 * TM_A_BYTES;
+        if (a.b_mn)
+          for (int j = 0; j < nbB; ++j) tma2d(sb + j * 2048, &a.tb, (int32_t)(n0 + 32 * j), k0, fb);
+        else
+          tma2d(sb, &a.tb, k0, (int32_t)n0, fb);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a.a_mn << 15) |
+                             ((uint32_t)a.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(TM_BM >> 4) << 24);
+      for (int kt = 0; kt < ntiles; ++kt) {
+        const int s = kt % TM_ST;
+        mb_wait(su32(&conv[s]), (uint32_t)((kt / TM_ST) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t st = sbase + s * TM_STAGE;
+        const uint32_t ahi = st, alo = st + TM_A_BYTES;
+        const uint32_t bhi = st + 2 * TM_A_BYTES, blo = bhi + TM_B_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < TM_BK / 8; ++ks) {
+          const uint64_t dah = op_desc(ahi, ks, a.a_mn), dal = op_desc(alo, ks, a.a_mn);
+          const uint64_t dbh = op_desc(bhi, ks, a.b_mn), dbl = op_desc(blo, ks, a.b_mn);
+          mma_tf32(tmem, dah, dbh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32(tmem, dah, dbl, idesc, 1u);
+          mma_tf32(tmem, dal, dbh, idesc, 1u);
+        }
+        mma_commit(su32(&empty[s]));
+      }
+      mma_commit(su32(&done));
+    }
+  } else {
+    // converters: hi in place, lo into the twin buffer
+    for (int kt = 0; kt < ntiles; ++kt) {
+      const int s = kt % TM_ST;
+      mb_wait(su32(&full[s]), (uint32_t)((kt / TM_ST) & 1));
+      unsigned char* st = smem + s * TM_STAGE;
+      constexpr int NA = TM_A_BYTES / 16, NB = TM_B_BYTES / 16;
+#pragma unroll
+      for (int i = tid; i < NA + NB; i += TM_CONV) {
+        const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
+        const uint32_t lo_off = i < NA ? TM_A_BYTES : TM_B_BYTES;
+        float4 x = *(const float4*)(st + off);
+        uint4 h, l;
+        h.x = rna(x.x); h.y = rna(x.y); h.z = rna(x.z); h.w = rna(x.w);
+        l.x = rna(x.x - __uint_as_float(h.x)); l.y = rna(x.y - __uint_as_float(h.y));
+        l.z = rna(x.z - __uint_as_float(h.z)); l.w = rna(x.w - __uint_as_float(h.w));
+        *(uint4*)(st + off) = h;
+        *(uint4*)(st + off + lo_off) = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mb_arrive(su32(&conv[s]));
+    }
+    // epilogue: warp w reads TMEM lanes 32(w%4).. (= tile rows), column half w/4
+    if (ntiles > 0) mb_wait(su32(&done), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int wq = warp & 3, wh = warp >> 2;
+    const int r = wq * 32 + lane;
+    const int64_t m = m0 + r;
+    const int half = ((BN / 2) + 15) / 16 * 16;
+    const int cbeg = wh * half, cend = wh ? BN : (half < BN ? half : BN);
+    float* Cp = (float*)p.C.ptr;
+    const bool vec = p.splits == 1 && a.c_n == 1 && ((p.C.ptr + 4 * (p.C.off + m * a.c_m)) & 15) == 0;
+    for (int c0 = cbeg; c0 < cend; c0 += 16) {
+      uint32_t v[16];
+      const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      if (ntiles == 0)
+        for (int j = 0; j < 16; ++j) v[j] = 0u;
+      if (m >= p.m) continue;
+      float x[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = __uint_as_float(v[j]);
+      if (p.splits > 1) {
+        float* part = (float*)p.part + ((int64_t)split * p.m + m) * p.n + n0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (n0 + c0 + j < p.n) part[c0 + j] = x[j];
+        continue;
+      }
+      const int64_t rowoff = p.C.off + m * a.c_m;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int64_t n = n0 + c0 + j;
+        if (n >= p.n) break;
+        if (p.accumulate) x[j] += Cp[rowoff + n * a.c_n];
+        if (p.bias.ptr)
+          x[j] += load_as<float>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + n * a.bias_n);
+        if (p.epilogue == 1) x[j] = tanhf(x[j]);
+      }
+      if (vec && n0 + c0 + 16 <= p.n) {
+        float4* dst = (float4*)(Cp + rowoff + n0 + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          __stcs(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+      } else {
+        for (int j = 0; j < 16; ++j) {
+          const int64_t n = n0 + c0 + j;
+          if (n >= p.n) break;
+          Cp[rowoff + n * a.c_n] = x[j];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+
+// 2-D fp32 map over (inner, outer) with unit inner stride.
+static int tm_encode(encode_fn_t enc, CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer,
+                     uint64_t outer_stride_elems, uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapSwizzle sw) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {outer_stride_elems * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  if (outer == 1) strides[0] = ((inner * 4 + 15) / 16) * 16;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)addr, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+// Pack a folded rt_gemm_params (1-D M/N/K boxes) into the kernel's argument
+// block (tensor maps first, 64-byte aligned) in place.  Returns the kernel.
+extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
+  rt_gemm_params p;
+  memcpy(&p, blk, sizeof p);
+  tm_args a;
+  memset(&a, 0, sizeof a);
+  a.p = p;
+  encode_fn_t enc = (encode_fn_t)encode;
+  const int64_t a_m = p.A.s1[0], a_k = p.A.s2[0], b_k = p.B.s1[0], b_n = p.B.s2[0];
+  a.c_m = p.C.s1[0];
+  a.c_n = p.C.s2[0];
+  a.bias_n = p.bias.s2[0];
+  const uint64_t abase = p.A.ptr + 4 * (uint64_t)p.A.off, bbase = p.B.ptr + 4 * (uint64_t)p.B.off;
+  int rc;
+  if (a_k == 1 || p.k == 1) {
+    a.a_mn = 0;
+    rc = tm_encode(enc, &a.ta, abase, p.k, p.m, a_m, TM_BK, TM_BM, CU_TENSOR_MAP_SWIZZLE_64B);
+  } else {
+    a.a_mn = 1;
+    rc = tm_encode(enc, &a.ta, abase, p.m, p.k, a_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (rc) return nullptr;
+  if (b_k == 1 || p.k == 1) {
+    a.b_mn = 0;
+    rc = tm_encode(enc, &a.tb, bbase, p.k, p.n, b_n, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
+  } else {
+    a.b_mn = 1;
+    rc = tm_encode(enc, &a.tb, bbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  if (rc) return nullptr;
+  memcpy(blk, &a, sizeof a);
+  return (void*)k_gemm_tma;
+}
+
+extern "C" int rt_gemm_tma_smem() { return TM_SMEM; }
+extern "C" int rt_gemm_tma_args_bytes() { return (int)sizeof(tm_args); }

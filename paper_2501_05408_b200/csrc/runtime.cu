@@ -23,6 +23,7 @@ extern "C" void* rt_kernel_policy(const void* params);
 extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
+extern "C" void* rt_gemm_tma_pack(void* blk, void* encode);
 
 static thread_local std::string g_err;
 
@@ -34,6 +35,7 @@ struct DriverApi {
   decltype(&cuLaunchKernel) launchKernel = nullptr;
   decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
   decltype(&cuGetErrorString) getErrorString = nullptr;
+  void* tensorMapEncodeTiled = nullptr;
   bool ok = false;
 };
 
@@ -53,6 +55,7 @@ static DriverApi& drv() {
     RT_GET(launchKernel, "cuLaunchKernel")
     RT_GET(funcSetAttribute, "cuFuncSetAttribute")
     RT_GET(getErrorString, "cuGetErrorString")
+    RT_GET(tensorMapEncodeTiled, "cuTensorMapEncodeTiled")
 #undef RT_GET
     d.ok = all;
   }
@@ -137,6 +140,16 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
       return rt_kernel_gemm_tc();
     }
+    case RT_K_GEMM_TMA: {
+      rt_gemm_params* p = (rt_gemm_params*)blk;
+      fold_gop(p->A, env, nenv);
+      fold_gop(p->B, env, nenv);
+      fold_gop(p->C, env, nenv);
+      if (p->bias.ptr) fold_gop(p->bias, env, nenv);
+      DriverApi& D = drv();
+      if (!D.ok) return nullptr;
+      return rt_gemm_tma_pack(blk, D.tensorMapEncodeTiled);
+    }
     case RT_K_THIN: {
       rt_thin_params* p = (rt_thin_params*)blk;
       fold_gop(p->X, env, nenv);
@@ -172,7 +185,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
 }
 
 static int launch_one(const rt_launch_rec* rec, const int64_t* env, int nenv, cudaStream_t s) {
-  alignas(16) static thread_local unsigned char blk[32768];
+  alignas(128) static thread_local unsigned char blk[32768];
   if (rec->param_bytes <= 0 || rec->param_bytes > (int)sizeof blk)
     return fail(RT_ERR_BAD_ARG, "parameter block size out of range");
   memcpy(blk, (const void*)rec->params, rec->param_bytes);

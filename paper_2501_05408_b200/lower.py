@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import zlib
 from dataclasses import dataclass, field
 
@@ -263,6 +264,7 @@ class Lowering:
         self.virtual |= self.absorbed
         self.persistent = persistent
         self.use_tc = use_tc
+        self.use_tma = os.environ.get("RTB200_GEMM", "") != "tc"
         self.shard = shard
         self.shard_reduce = set(shard_reduce or ())
         self.hooks = []                        # all-reduce hooks (sharded reductions)
@@ -1318,6 +1320,9 @@ class Lowering:
         """Z/M/N/K: lists of (extent, a_stride, b_stride, c_stride).
         A/B/C: (buf, element offset, {env slot: stride})."""
         p = N.rt_gemm_params()
+        M, K = self._collapse_box(M), self._collapse_box(K)
+        if bias is None:
+            Nn = self._collapse_box(Nn)
         if not Z:
             Z = [(1, 0, 0, 0)]
         for gb, lst in ((p.Z, Z), (p.M, M), (p.N, Nn), (p.K, K)):
@@ -1406,6 +1411,22 @@ class Lowering:
             ext *= t[0]
         return ext, st
 
+    @staticmethod
+    def _collapse_box(lst):
+        """Merge adjacent (extent, a, b, c strides) GEMM box dims that every
+        operand walks contiguously; extent-1 dims are dropped."""
+        dims = [t for t in lst if t[0] != 1]
+        if not dims:
+            return [(1, 0, 0, 0)]
+        out = [dims[-1]]
+        for t in reversed(dims[:-1]):
+            nxt = out[0]
+            if all(t[c] == nxt[c] * nxt[0] for c in (1, 2, 3)):
+                out[0] = (t[0] * nxt[0],) + tuple(nxt[1:])
+            else:
+                out.insert(0, t)
+        return out
+
     THIN_MAX_R = 32
     THIN_MIN_K = 4096
 
@@ -1489,6 +1510,21 @@ class Lowering:
     def _capture_active(self):
         return self._capture is not None
 
+    @staticmethod
+    def _tma_ok(p):
+        """Plain 2-D f32 operands with a unit-stride dim and 16-byte aligned
+        rows: eligible for the TMA-fed pipeline (csrc/k_gemm_tma.cu)."""
+        if p.z != 1 or p.Z.nd > 1 or any(b.nd != 1 for b in (p.M, p.N, p.K)) or p.n < 16:
+            return False
+        if any(g.dtype != N.RT_F32 for g in (p.A, p.B, p.C)):
+            return False
+        for g, s_mn, s_k in ((p.A, p.A.s1[0], p.A.s2[0]), (p.B, p.B.s2[0], p.B.s1[0])):
+            if (g.ptr + 4 * g.off) % 16 or any(g.off_env[e] % 4 for e in range(N.RT_MAXENV)):
+                return False
+            if not ((s_k == 1 and s_mn % 4 == 0 and s_mn > 0) or (s_mn == 1 and s_k % 4 == 0 and s_k > 0)):
+                return False
+        return max(p.m, p.n, p.k) < (1 << 31)
+
     def _gemm_tc(self, p, label, accumulate, epilogue, bias):
         """tcgen05 3xTF32 path (csrc/k_gemm_tc.cu): 128 x 256 CTA tiles."""
         tiles = ((p.m + 127) // 128) * ((p.n + 255) // 256) * p.z
@@ -1501,7 +1537,10 @@ class Lowering:
         if splits > 1:
             p.part = self.alloc(splits * p.z * p.m * p.n * 4)
         grid = [(p.n + 255) // 256, (p.m + 127) // 128, p.z * splits]
-        self.add_rec(N.RT_K_GEMM_TC, p, grid, [256, 1, 1], N.TC_SMEM, label)
+        if self.use_tma and self._tma_ok(p):
+            self.add_rec(N.RT_K_GEMM_TMA, p, grid, [320, 1, 1], N.TMA_SMEM, label)
+        else:
+            self.add_rec(N.RT_K_GEMM_TC, p, grid, [256, 1, 1], N.TC_SMEM, label)
         if splits > 1:
             q = N.rt_splitk_params()
             q.Z, q.M, q.N = p.Z, p.M, p.N

@@ -10,7 +10,7 @@ ITEM = {N.RT_F64: 8, N.RT_F32: 4, N.RT_I64: 8, N.RT_BOOL: 1}
 FAMILY = {N.RT_K_EW: "ew", N.RT_K_REDUCE: "reduce", N.RT_K_SCAN: "scan", N.RT_K_GEMM: "gemm",
           N.RT_K_RNG: "rng", N.RT_K_UDF: "udf", N.RT_K_SPLITK: "splitk",
           N.RT_K_POLICY: "policy", N.RT_K_LOOP: "loop", N.RT_K_GEMM_TC: "gemm_tc",
-          N.RT_K_THIN: "thin"}
+          N.RT_K_THIN: "thin", N.RT_K_GEMM_TMA: "gemm_tma"}
 
 
 def _prod(xs):
@@ -64,7 +64,7 @@ def cost(kernel, p, loop_info=None):
         box = [p.box.ext[i] for i in range(p.box.nd)]
         tot = _prod(box)
         return tot * (ITEM.get(p.in_.dtype, 4) + ITEM.get(p.out.dtype, 4)), 2 * tot
-    if kernel in (N.RT_K_GEMM, N.RT_K_GEMM_TC):
+    if kernel in (N.RT_K_GEMM, N.RT_K_GEMM_TC, N.RT_K_GEMM_TMA):
         fl = 2 * p.z * p.m * p.n * p.k
         ea = _gop_elems(p.A, p.Z, p.M, p.K, 0) * ITEM.get(p.A.dtype, 4)
         eb = _gop_elems(p.B, p.Z, p.K, p.N, 1) * ITEM.get(p.B.dtype, 4)

@@ -151,3 +151,28 @@ def test_warp_reduce_per_point(W):
     out = execute(g, inputs={"gr": gr})["s"]
     want = gr.astype(np.float64).sum(1).astype(np.float32)
     np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("B,K,N,contract", [(5000, 100, 200, False), (9000, 40, 256, False),
+                                            (8192, 256, 256, False), (20000, 64, 96, True),
+                                            (70000, 256, 256, True), (3001, 256, 520, False)])
+def test_tma_gemm_pipeline(B, K, N, contract):
+    """TMA-fed tcgen05 pipeline (RT_K_GEMM_TMA): K-major and MN-major
+    operands, M/N/K tails, split-K."""
+    from paper_2501_05408_b200 import native as NN
+    rng = np.random.default_rng(B + K + N)
+    x = rng.standard_normal((B, 1, K)).astype(np.float32)
+    if contract:
+        gr = rng.standard_normal((B, 1, N)).astype(np.float32)
+        inp = {"x": x, "gr": gr}
+        want = np.einsum("bk,bn->kn", x[:, 0].astype(np.float64), gr[:, 0].astype(np.float64))
+        atol = 1e-4 * np.sqrt(B)
+    else:
+        W = (rng.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32)
+        inp = {"x": x, "W": W}
+        want = x.astype(np.float64) @ W.astype(np.float64)
+        atol = 1e-5
+    g = mm_graph(B, K, N, contract=contract)
+    assert NN.RT_K_GEMM_TMA in _kinds(g, inp)
+    out = execute(g, inputs=inp)["s" if contract else "y"]
+    np.testing.assert_allclose(out, want.astype(np.float32), rtol=1e-5, atol=atol)

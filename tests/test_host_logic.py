@@ -57,7 +57,7 @@ def dry_lower(g, benv, seed=0, fuse=True):
     bufs, ptr = an["bufs"], 1 << 20
     for k, b in bufs.items():
         b.ptr = ptr
-        ptr += b.nbytes + 256
+        ptr += (b.nbytes + 511) // 256 * 256
     low = L.Lowering(an["plan"], bufs, 0, seed, lambda nb: 1 << 40, an["contract"],
                      an["fuse_src"], an["gemm_epi"], absorbed=an["absorbed"]).lower()
     return an["plan"], low, an["contract"], an["alias"]
