@@ -7,7 +7,7 @@
 //
 // Roles (320 threads):
 //   warp 8 lane 0  TMA producer: raw fp32 tiles -> smem ring (SWIZZLE_64B
-//                  K-major or SWIZZLE_128B MN-major canonical UMMA layouts)
+//                  K-major or SWIZZLE_128B_BASE32B MN-major UMMA layouts)
 //   warps 0-7      converters: in place hi = tf32(x), lo = tf32(x - hi) into a
 //                  twin buffer (elementwise, so layout-agnostic and
 //                  conflict-free), then the epilogue (TMEM -> global)
@@ -97,8 +97,12 @@ RT_DEV uint32_t rna(float x) {
 
 // descriptor of operand tile at `base` for MMA K-step ks (8 fp32 of K)
 RT_DEV uint64_t op_desc(uint32_t base, int ks, int mn) {
-  if (mn)  // MN-major SW128: 32-wide MN atoms 2 KB apart (LBO), 8-k groups 1 KB apart (SBO)
-    return sdesc(base + ks * 1024, 2048, 1024, 2);
+  // MN-major 32-bit operands need SWIZZLE_128B_BASE32B (layout 1; plain
+  // SWIZZLE_128B reads as zeros for tf32 — measured, tools/probe/tc_probe2.cu):
+  // 128 B MN rows, 4-k atoms 512 B apart (SBO), 32-wide MN groups 2 KB apart
+  // (LBO); one K=8 MMA step spans two atoms.
+  if (mn)
+    return sdesc(base + ks * 1024, 2048, 512, 1);
   // K-major SW64: 64 B rows, 8-row groups 512 B apart; K-step = +32 B
   return sdesc(base + ks * 32, 16, 512, 4);
 }
@@ -316,7 +320,7 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
     rc = tm_encode(enc, &a.ta, abase, p.k, p.m, a_m, TM_BK, TM_BM, CU_TENSOR_MAP_SWIZZLE_64B);
   } else {
     a.a_mn = 1;
-    rc = tm_encode(enc, &a.ta, abase, p.m, p.k, a_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = tm_encode(enc, &a.ta, abase, p.m, p.k, a_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
   if (rc) return nullptr;
   if (b_k == 1 || p.k == 1) {
@@ -324,7 +328,7 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
     rc = tm_encode(enc, &a.tb, bbase, p.k, p.n, b_n, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
   } else {
     a.b_mn = 1;
-    rc = tm_encode(enc, &a.tb, bbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = tm_encode(enc, &a.tb, bbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
   if (rc) return nullptr;
   memcpy(blk, &a, sizeof a);
