@@ -526,10 +526,15 @@ class Lowering:
                     raise LowerError("ew box is not row-major over the slab")
                 ops.append([kernel, p, p.total // rows, p.f64, None])
             elif kernel == N.RT_K_GEMM:
-                if p.z != 1 or p.splits != 1 or p.M.nd != len(S) + 1 or p.k > 4096 or \
-                        [p.M.ext[i] for i in range(len(S))] != Sext:
+                # M = slab rows x m, row-major; the index path may have
+                # collapsed adjacent dims (m == 1 -> M is the slab itself)
+                mext = [p.M.ext[i] for i in range(p.M.nd)]
+                if p.z != 1 or p.splits != 1 or p.k > 4096 or prod(mext) % rows:
                     raise LowerError("gemm is not row-blocked over the slab")
-                m = p.M.ext[len(S)]
+                m = prod(mext) // rows
+                if not (mext == Sext + [m] or (m == 1 and mext == Sext)
+                        or (p.M.nd == 1 and mext[0] == rows * m)):
+                    raise LowerError("gemm is not row-blocked over the slab")
                 max_m = max(max_m, m)
                 ops.append([kernel, p, m, p.f64, None])
             elif kernel in (N.RT_K_UDF, N.RT_K_RNG):
