@@ -50,6 +50,38 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+# 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz (boost clock seen under load)
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+# kernel family -> the kernel name in the committed ncu --set full capture
+_NCU_NAME = {"loop": "loop_jit", "gemm_tma": "k_gemm_tma", "ew": "ew_jit", "scan": "k_scan"}
+
+
+def ncu_traffic(family):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the family's
+    kernel, from the committed `ncu --set full` capture under profiles/ (the
+    newest round's), or None."""
+    import csv
+    import glob
+    name = _NCU_NAME.get(family)
+    if not name:
+        return None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{name}_raw.csv")))
+    if not files:
+        return None
+    try:
+        rows = list(csv.reader(open(files[-1])))
+        h, units, row = rows[0], rows[1], rows[2]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(m)
+            tot += float(row[i].replace(",", "")) * scale[units[i]]
+        return tot
+    except Exception:
+        return None
+
+
 class Clocks:
     def __init__(self):
         self.samples = []
@@ -236,6 +268,11 @@ def main():
         ach = bytes_ / (kms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": None}
+    roof["traffic"] = ncu_traffic(RF.FAMILY[dom["kernel"]])
+    if roof["unit"] == "TFLOP/s":
+        # the acting loop runs FP32 FMAs on the SIMT pipe: its own ceiling
+        roof["fp32_simt_peak"] = FP32_SIMT_TFLOPS
+        roof["fp32_simt_frac"] = ach / FP32_SIMT_TFLOPS
     roof.update({"kernel": RF.FAMILY[dom["kernel"]], "node": dom["label"][1],
                  "ms_per_launch": kms, "launches_per_step": dom["count"],
                  "share_of_step": dom["ms"] / max(1e-9, sum(r["ms"] for r in prof)),
