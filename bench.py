@@ -1,15 +1,21 @@
-"""Benchmark: REINFORCE training iterations of a 2-layer 256-wide MLP policy
-on E=1024 synthetic envs x T=1000 steps (BASELINE.json configs[1], SURVEY
-§8(d) C2), through the B200 executor.
+"""Benchmark: training iterations of recurrent-tensor RL programs through
+the B200 executor (BASELINE.json metric: env-steps/s per train iter, peak
+HBM).  Workloads:
 
-One step = one call of the program at I=1: roll out E envs for T steps,
-discounted returns-to-go (suffix scan), surrogate backward through the MLP,
-and the SGD update of all six parameters (outputs `*_next`, fed back as the
-next step's inputs).  env-steps per step = E*T.
+  c2 (default): REINFORCE, E=1024 envs x T=1000 steps per GPU, 2-hidden-
+      layer 256-wide tanh MLP policy (BASELINE.json configs[1]).
+  c3: PPO with GAE(lambda), 4 epochs x 4 minibatches, E=4096 x T=512,
+      shared policy/value MLP (configs[2]).
+  c5: c3's program with E=32768 envs in total, split E/N per GPU, NCCL
+      all-reduce of every minibatch gradient (configs[4]; strong scaling).
+
+One step = one call of the program at I=1: roll out, returns/advantages
+(suffix scans), backward through the MLP, parameter updates (outputs
+`*_next`, fed back as the next step's inputs).  env-steps per step = E*T.
 
   value : device-resident (weights already in HBM, outputs left in HBM)
   e2e   : public API `execute()` with host numpy weights in and updated
-          weights + objective out (H2D/D2H inside the timed region)
+          weights + outputs out (H2D/D2H inside the timed region)
 
 `--impl reference` times the reference CPU implementation of the same
 program (the oracle port of reference_execute, oracle/pdg_oracle.py) on a
@@ -30,14 +36,59 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-E_PER_GPU = 1024
-T_STEPS = 1000
-GRAPH = "reinforce_mlp_c2"
+
+class Workload:
+    def __init__(self, name, graph, T, env_total=None, env_per_gpu=None, minibatches=None,
+                 ppo=False, desc=""):
+        self.name, self.graph, self.T = name, graph, T
+        self.env_total, self.env_per_gpu = env_total, env_per_gpu
+        self.minibatches, self.ppo, self.desc = minibatches, ppo, desc
+
+    def local_envs(self, world):
+        if self.env_per_gpu:
+            return self.env_per_gpu
+        assert self.env_total % world == 0
+        return self.env_total // world
+
+    def bounds(self, B):
+        if self.ppo:
+            return {"I": 1, "E": 4, "M": self.minibatches, "U": B // self.minibatches,
+                    "B": B, "T": self.T}
+        return {"I": 1, "B": B, "T": self.T}
+
+    def inputs(self):
+        from paper_2501_05408_b200.workloads import mlp_inputs, ppo_inputs
+        return ppo_inputs() if self.ppo else mlp_inputs()
+
+    def params(self):
+        from paper_2501_05408_b200.workloads import PARAMS, PPO_PARAMS
+        return PPO_PARAMS if self.ppo else PARAMS
+
+    def shard(self, rank, world):
+        from paper_2501_05408_b200.shard import ShardSpec
+        return ShardSpec("b", rank, world, ("u",) if self.ppo else ())
+
+    @property
+    def scaling(self):
+        return "strong" if self.env_total else "weak"
+
+
+WORKLOADS = {
+    "c2": Workload("reinforce_mlp_c2", "reinforce_mlp_c2", 1000, env_per_gpu=1024,
+                   desc="REINFORCE, E=1024/GPU x T=1000, MLP 16-256-256-4"),
+    "c3": Workload("ppo_gae_c3", "ppo_c3", 512, env_per_gpu=4096, minibatches=4, ppo=True,
+                   desc="PPO+GAE(0.95), E=4096 x T=512, 4 epochs x 4 minibatches, "
+                        "shared MLP 16-256-256-(4|1)"),
+    "c5": Workload("ppo_gae_c5", "ppo_c3", 512, env_total=32768, minibatches=4, ppo=True,
+                   desc="PPO+GAE(0.95), E=32768 total split over GPUs x T=512, "
+                        "4 epochs x 4 minibatches"),
+}
+WL = WORKLOADS["c2"]
 
 
 def load_graph():
     from paper_2501_05408_b200 import ir
-    with open(os.path.join(ROOT, "tests", "golden", "graphs", f"{GRAPH}.json")) as fh:
+    with open(os.path.join(ROOT, "tests", "golden", "graphs", f"{WL.graph}.json")) as fh:
         return ir.Graph.from_json(fh.read())
 
 
@@ -125,22 +176,27 @@ class Clocks:
 
 def cpu_baseline(seconds=12.0):
     """Oracle port (reference_execute restated) on a bounded sample of the
-    same program: E=4 envs, T=32 steps at full width (H=256)."""
+    same program at full width (H=256): C2 at E=4 envs x T=32 steps; PPO at
+    E=4 x T=16 with 2 epochs x 2 minibatches."""
     from oracle.pdg_oracle import oracle_execute
-    from paper_2501_05408_b200.workloads import mlp_inputs
     g = load_graph()
-    inputs = mlp_inputs()
-    B, T = 4, 32
+    inputs = WL.inputs()
+    if WL.ppo:
+        B, T = 4, 16
+        bounds = {"I": 1, "E": 2, "M": 2, "U": 2, "B": B, "T": T}
+    else:
+        B, T = 4, 32
+        bounds = {"I": 1, "B": B, "T": T}
     t0 = time.perf_counter()
     n = 0
     while True:
-        oracle_execute(g, bounds={"I": 1, "B": B, "T": T}, inputs=inputs, seed=n)
+        oracle_execute(g, bounds=bounds, inputs=inputs, seed=n)
         n += 1
         if time.perf_counter() - t0 > seconds:
             break
     dt = time.perf_counter() - t0
     return {"value": n * B * T / dt, "unit": "env-steps/s", "cores": 1, "kind": "port",
-            "sample": f"{n} x oracle_execute(E={B}, T={T}, H=256) of the C2 program, "
+            "sample": f"{n} x oracle_execute({bounds}, H=256) of the {WL.name} program, "
                       f"{dt:.1f}s, single-threaded Python+numpy (reference_execute restated)"}
 
 
@@ -153,9 +209,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": "env-steps/s per train iter",
             "value": base["value"], "unit": "env-steps/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "reinforce_mlp_c2 (bounded CPU sample)", "E": 4, "T": 32,
-                       "hidden": [256, 256], "obs": 16, "act": 4},
+            "scaling": WL.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{WL.name} (bounded CPU sample)",
+                       "sample": base["sample"], "hidden": [256, 256], "obs": 16, "act": 4},
             "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -169,14 +225,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
+    global WL
+    WL = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args)
 
     import numpy as np
     import torch
     from paper_2501_05408_b200 import execute, get_executable
-    from paper_2501_05408_b200.workloads import mlp_inputs, next_inputs, PARAMS
+    from paper_2501_05408_b200.workloads import next_inputs
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -187,14 +246,15 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl")
     g = load_graph()
-    B = E_PER_GPU
-    bounds = {"I": 1, "B": B, "T": T_STEPS}
-    host = mlp_inputs()
+    B = WL.local_envs(world)
+    T_STEPS = WL.T
+    bounds = WL.bounds(B)
+    host = WL.inputs()
+    params = WL.params()
     dev_in = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
     shard = None
     if world > 1:
-        from paper_2501_05408_b200.shard import ShardSpec
-        shard = ShardSpec("b", rank, world)     # envs [rank*B, (rank+1)*B) of B*world
+        shard = WL.shard(rank, world)     # envs [rank*B, (rank+1)*B) of B*world
     exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard)
 
     def step_dev(inp, graph=None):
@@ -203,7 +263,7 @@ def main():
         else:
             exe.launch_graph(graph, inp)
         outs = exe.outputs(device_outputs=True)
-        return next_inputs(outs)
+        return next_inputs(outs, params)
 
     # warmup (device path, CUDA graph)
     inp = dev_in
@@ -290,14 +350,14 @@ def main():
     hin = host
     for w in range(max(1, args.warmup)):
         outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard)
-        hin = next_inputs(outs)
+        hin = next_inputs(outs, params)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for s in range(args.steps):
         outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard)
-        hin = next_inputs(outs)
+        hin = next_inputs(outs, params)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     h2d = sum(v.nbytes for v in host.values())
     d2h = sum(np.asarray(v).nbytes for v in outs.values())
@@ -309,9 +369,10 @@ def main():
 
     line = {"metric": "env-steps/s per train iter", "value": value, "unit": "env-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "reinforce_mlp_c2", "E_per_gpu": B, "T": T_STEPS,
+            "higher_is_better": True, "scaling": WL.scaling, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WL.name, "desc": WL.desc, "E_per_gpu": B,
+                       "E_total": B * world, "T": T_STEPS, "bounds": bounds,
                        "hidden": [256, 256], "obs": 16, "act": 4, "iters_per_step": 1,
                        "l2": "activations (GBs) exceed L2 every step",
                        "parallelism": f"env-shard x{world}"},
@@ -319,6 +380,7 @@ def main():
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": exe.launch_count * args.steps,
             "peak_hbm_bytes": exe.peak_bytes,
+            "peak_hbm_allocated_bytes": int(torch.cuda.max_memory_allocated()),
             "naive_hbm_bytes": exe.naive_bytes,
             "roofline": roof,
             "breakdown": {"family_ms_per_step": {k: round(v, 3) for k, v in fam_ms.items()},

@@ -22,6 +22,8 @@ import ctypes as C
 import itertools
 import weakref
 
+import os
+
 import numpy as np
 
 from . import ir
@@ -185,6 +187,63 @@ def eliminate_dead(g: Graph):
     return g
 
 
+def _provably_true(c, box):
+    """Condition c (bounds substituted) holds at every point of box."""
+    from .planner import interval
+    k = c[0]
+    if k == "bool":
+        return bool(c[1])
+    if k == "and":
+        return _provably_true(c[1], box) and _provably_true(c[2], box)
+    if k == "or":
+        return _provably_true(c[1], box) or _provably_true(c[2], box)
+    if k in ("lt", "le", "gt", "ge", "eq", "ne"):
+        lo, hi = interval(("sub", c[1], c[2]), box)
+        return {"lt": hi < 0, "le": hi <= 0, "gt": lo > 0, "ge": lo >= 0,
+                "eq": lo == hi == 0, "ne": hi < 0 or lo > 0}[k]
+    return False
+
+
+def simplify_guards(g: Graph, benv):
+    """Drop edge conditions and merge branches that are provably true over
+    the concrete domain box (e.g. the in-domain guards the symbolic
+    backward wraps around shifted reads, frontend.py:716-745, when the
+    read index provably stays inside the source's domain): a merge whose
+    first branch always holds is that branch; nothing downstream changes
+    (the reference would take the same first-true branch at every point,
+    runtime.py:362-371)."""
+    from .planner import subst_bounds
+    ext = {d: benv[g.dim_bound[d]] for d in g.dim_order if g.dim_bound[d] in benv}
+    changed = False
+    for n in g.sorted_nodes():
+        box = {d: (0, ext[d] - 1) for d in n.domain if d in ext}
+        if len(box) != len(n.domain) or any(lo > hi for lo, hi in box.values()):
+            continue
+        for e in g.in_edges(n.id):
+            if e.psi is not None and _provably_true(subst_bounds(e.psi, benv), box):
+                e.psi = None
+                changed = True
+        if n.kind == "merge":
+            c0 = n.params["conds"][0]
+            if c0 != ir.TRUE and _provably_true(subst_bounds(c0, benv), box):
+                n.params["conds"] = (ir.TRUE,)
+                g.edges = [e for e in g.edges if not (e.sink == n.id and e.iid > 0)]
+                n.nin = 1
+                changed = True
+    if changed:
+        g.invalidate()
+    return g
+
+
+def prepare(g: Graph, benv):
+    """Per-bounds graph preparation before planning: inline `dataflow`
+    groups, drop provably-true guards, remove dead nodes."""
+    inline_dataflow(g, benv)
+    simplify_guards(g, benv)
+    eliminate_dead(g)
+    return g
+
+
 def copy_graph(g: Graph) -> Graph:
     h = Graph(g.dim_order, g.dim_bound, g.bindings)
     h.nodes = {k: ir.Node(n.id, n.name, n.kind, n.domain, n.out_shapes, n.out_dtypes,
@@ -232,6 +291,12 @@ def find_contractions(g: Graph):
             continue
         e = ins[0]
         x = g.nodes[e.src]
+        # look through pass-through merges (an always-true guard around the
+        # VJP product, frontend.py:716-745)
+        while (x.kind == "merge" and x.params["conds"] == (ir.TRUE,) and x.id not in out_ids
+               and len(g.out_edges(x.id)) == 1 and len(g.in_edges(x.id)) == 1
+               and _is_identity(g.in_edges(x.id)[0], g.nodes[g.in_edges(x.id)[0].src], x)):
+            x = g.nodes[g.in_edges(x.id)[0].src]
         if x.kind != "matmul" or x.id in out_ids or len(g.out_edges(x.id)) != 1:
             continue
         kept, nsl, ok = [], 0, True
@@ -398,7 +463,14 @@ def find_absorbed_layouts(g: Graph, skip):
     return res
 
 
-def analyze(g: Graph, benv, pshape, fuse=True):
+# debugging knobs (RTB200_NOFUSE=1 / RTB200_NOFOLD=1): every combination
+# must give the same results
+OPTS = {"fuse": os.environ.get("RTB200_NOFUSE") != "1",
+        "fold": os.environ.get("RTB200_NOFOLD") != "1",
+        "persistent": os.environ.get("RTB200_NOPERSIST") != "1"}
+
+
+def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
     """Plan the loop nest and decide aliases, contractions and fusions
     (device-independent; the CPU tests run this directly)."""
     ext = {d: benv[g.dim_bound[d]] for d in g.dim_order}
@@ -428,8 +500,77 @@ def analyze(g: Graph, benv, pshape, fuse=True):
             key = (n.id, oid)
             bufs[key] = Buf(key, n.domain, tuple(ext[d] for d in n.domain), pshape[key],
                             n.out_dtypes[oid], alias.get(key))
+    if fold:
+        for key, dims in find_folds(g, bufs, fixed_of, virtual, ext).items():
+            bufs[key].folded = dims
     return {"contract": contract, "alias": alias, "plan": plan, "gemm_epi": gemm_epi,
             "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs, "absorbed": absorbed}
+
+
+def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, depth=0):
+    """Edge e reads the producer's value made in the same iteration of the
+    loop over d: the consumer's loops down to d are the producer's (same
+    order), and it reads at its own index along every one of them (a read
+    along an outer loop at another index, or of a producer that lacks an
+    outer loop dim, sees a slot later iterations overwrote)."""
+    snk = g.nodes[e.sink]
+    fixed_c = fixed_of.get(snk.id, ())
+    if d not in fixed_c:
+        return False
+    k = fixed_c.index(d) + 1
+    if tuple(fixed_p[:k]) != tuple(fixed_c[:k]):
+        return False
+    src = g.nodes[e.src]
+    for x in fixed_c[:k]:
+        if x not in src_dom:
+            # a loop dim the producer lacks: both sit in the one peeled
+            # iteration (planner.peel_for), or the consumer re-reads later
+            if x in snk.domain:
+                return False
+        elif x not in snk.domain:
+            return False
+        elif x in src.domain and e.phi[src.domain.index(x)] != ("sym", x, "loop"):
+            return False
+    if snk.id in virtual:
+        if depth > 32:
+            return False
+        return all(_read_in_iteration(g, f, d, fixed_p, snk.domain, fixed_of, virtual,
+                                      depth + 1)
+                   for f in g.out_edges(snk.id))
+    return True
+
+
+def find_folds(g: Graph, bufs, fixed_of, virtual, ext):
+    """Storage contraction: a buffer whose every value is produced and
+    consumed within one iteration of an enclosing loop over d keeps a
+    single slot along d (the deallocate-after-last-use of
+    polysched.py:936-1105 at its tightest: the value dies in the iteration
+    that made it).  E.g. the PPO minibatch activations over (e, j, u, t)
+    need one (u, t) slab, not epochs x minibatches of them."""
+    out_keys = {(nid, oid) for _, nid, oid in g.outputs}
+    members = {}
+    for k, b in bufs.items():
+        r = k
+        while bufs[r].alias is not None:
+            r = bufs[r].alias
+        members.setdefault(r, []).append(k)
+    folds = {}
+    for r, mem in members.items():
+        n = g.nodes[r[0]]
+        if n.kind in ("const", "input") or r[0] in virtual or any(m in out_keys for m in mem):
+            continue
+        ok = {d for d in n.domain if d in fixed_of.get(r[0], ()) and ext[d] > 1}
+        for m in mem:
+            if not ok:
+                break
+            for e in g.out_edges(m[0]):
+                if e.oid == m[1]:
+                    ok = {d for d in ok if _read_in_iteration(
+                        g, e, d, fixed_of.get(r[0], ()), n.domain, fixed_of, virtual)}
+        if ok:
+            for m in mem:
+                folds[m] = frozenset(ok)
+    return folds
 
 
 def payload_shapes(g: Graph, benv):
@@ -466,8 +607,8 @@ class Executable:
         self.shard_reduce = set()
         if shard is not None:
             from .shard import check_shardable
-            self.shard_reduce = check_shardable(g, shard.dim)
-        an = analyze(g, benv, pshape, fuse)
+            self.shard_reduce = check_shardable(g, shard.dim, shard.also, benv)
+        an = analyze(g, benv, pshape, fuse and OPTS["fuse"], OPTS["fold"])
         self.contract, self.plan, self.gemm_epi, self.fuse_src = (
             an["contract"], an["plan"], an["gemm_epi"], an["fuse_src"])
         self.absorbed = an["absorbed"]
@@ -492,7 +633,8 @@ class Executable:
         low = Lowering(self.plan, self.bufs, self.status, seed, lambda nb: 0,
                        self.contract, self.fuse_src, self.gemm_epi,
                        absorbed=self.absorbed, shard=shard,
-                       shard_reduce=self.shard_reduce).lower()
+                       shard_reduce=self.shard_reduce,
+                       persistent=OPTS["persistent"]).lower()
         key_of = {v: k for k, v in fake.items()}
         rec_ptrs = []
         for ri, (_, p, *_r) in enumerate(low.recs):
@@ -525,7 +667,8 @@ class Executable:
         low = Lowering(self.plan, self.bufs, self.status, seed, self._scratch,
                        self.contract, self.fuse_src, self.gemm_epi,
                        absorbed=self.absorbed, shard=shard,
-                       shard_reduce=self.shard_reduce).lower()
+                       shard_reduce=self.shard_reduce,
+                       persistent=OPTS["persistent"]).lower()
         self.hooks = low.hooks
         self._upload_loops(low)
         self.nrec = len(low.recs)
@@ -991,8 +1134,7 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
     if ex is not None and ex[0]() is g:
         return ex[1], benv
     h = copy_graph(graph)
-    inline_dataflow(h, benv)
-    eliminate_dead(h)
+    prepare(h, benv)
     if shard is not None and comm is None:
         from .shard import TorchComm
         comm = TorchComm()
@@ -1022,8 +1164,7 @@ def _resolve_dynamic(g: Graph, benv, dyn, inputs, seed, device):
             cap = min(tentative, DYN_CAP)
             h = copy_graph(g)
             h.outputs = [("__driver__", node.id, 0)]
-            inline_dataflow(h, {**benv, b: cap})
-            eliminate_dead(h)
+            prepare(h, {**benv, b: cap})
             trial = dict(benv)
             trial[b] = cap
             for d2 in h.dim_order:

@@ -61,6 +61,7 @@ class Buf:
     alias: tuple | None = None   # (nid, oid) whose storage this is
     host: np.ndarray | None = None  # constant/input contents
     ptr: int = 0
+    folded: frozenset = frozenset()  # loop dims stored as one slot (stride 0)
 
     @property
     def shape(self):
@@ -68,7 +69,14 @@ class Buf:
 
     @property
     def strides(self):
-        return cstrides(self.shape)
+        if not self.folded:
+            return cstrides(self.shape)
+        ext = [1 if d in self.folded else x for d, x in zip(self.dims, self.dshape)]
+        st = list(cstrides(ext + list(self.pshape)))
+        for j, d in enumerate(self.dims):
+            if d in self.folded:
+                st[j] = 0
+        return tuple(st)
 
     def dim_stride(self, d):
         return self.strides[self.dims.index(d)]
@@ -78,7 +86,8 @@ class Buf:
 
     @property
     def nbytes(self):
-        return prod(self.shape) * ir.ITEMSIZE[self.dtype]
+        ext = [1 if d in self.folded else x for d, x in zip(self.dims, self.dshape)]
+        return prod(ext) * prod(self.pshape) * ir.ITEMSIZE[self.dtype]
 
 
 # ---------------------------------------------------------------------------
@@ -517,6 +526,8 @@ class Lowering:
             subs, self._capture = self._capture, None
         Sext = [self.ext[d] for d in S]
         rows = prod(Sext)
+        if s.lo not in (None, 0) or s.hi not in (None, self.ext[s.dim]):
+            raise LowerError("persistent loops run a dim's full extent")
         T = self.ext[s.dim]
         ops = []
         max_m = 1
@@ -629,11 +640,12 @@ class Lowering:
                 del self.recs[mark[0]:]
                 del self.prog[mark[1]:]
                 self._capture = None
-        n = self.ext[s.dim]
+        lo = 0 if s.lo is None else s.lo
+        hi = self.ext[s.dim] if s.hi is None else s.hi
         if s.step > 0:
-            start, stop = 0, n
+            start, stop = lo, hi
         else:
-            start, stop = n - 1, -1
+            start, stop = hi - 1, lo - 1
         at = len(self.prog)
         self.prog.append([N.RT_OP_FOR, self.slot[s.dim], start, stop, s.step, 0])
         self.steps(s.body)
@@ -1613,7 +1625,7 @@ class Lowering:
         if self.shard is None:
             return
         for j, d in enumerate(n.domain):
-            if d == self.shard.dim:
+            if d in self.shard.dims:
                 p.coord_add[j] = self.shard.offset(self.ext[d])
 
     @staticmethod

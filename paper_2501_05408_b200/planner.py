@@ -160,6 +160,8 @@ class Loop:
     step: int             # +1 ascending, -1 descending
     body: list = field(default_factory=list)
     fixed: tuple = ()
+    lo: int | None = None  # iteration range [lo, hi) (None: the dim's full extent)
+    hi: int | None = None
 
 
 @dataclass
@@ -300,7 +302,8 @@ class Planner:
             if len(comp) == 1 and not cedges:
                 steps.append(Bulk(comp[0], fixed))
                 continue
-            steps.append(self.loop_for(set(comp), cedges, fixed))
+            lp = self.loop_for(set(comp), cedges, fixed)
+            steps.extend(lp if isinstance(lp, list) else [lp])
         return steps
 
     def loop_for(self, comp: set, cedges: list, fixed: tuple):
@@ -328,8 +331,62 @@ class Planner:
                 if ok and len(flat) < len(live):
                     body = self.level(comp, flat, fixed + (d,))
                     return Loop(d, step, body, fixed)
+        peeled = self.peel_for(comp, cedges, fixed)
+        if peeled is not None:
+            return peeled
         names = ", ".join(self.g.nodes[v].name for v in sorted(comp))
         raise PlanError(f"unschedulable cycle through [{names}]")
+
+    def peel_for(self, comp: set, cedges: list, fixed: tuple):
+        """A cycle whose members do not all share a dim: some members lack d
+        and read the d-members only at d == 0 (e.g. a PPO rollout over (b,t)
+        reading the parameters theta[i, k=0] that the update loop over k
+        then advances).  Peel the first iteration: loop d over [0, 1) with
+        every member (the d-less ones evaluated there, once), then over
+        [1, n) with the d-members alone.  Point-level, this is the schedule
+        theta(v) = 0 along d for the d-less members (polysched's `const`
+        placement of a statement without the dim, polysched.py:594-608)."""
+        g = self.g
+        cands = [d for d in g.dim_order if d not in fixed and self.ext.get(d, 0) > 1
+                 and any(d in g.nodes[v].domain for v in comp)]
+        for d in cands:
+            has = {v for v in comp if d in g.nodes[v].domain}
+            lacks = comp - has
+            if not lacks:
+                continue
+            ok = True
+            flat0, rest = [], []
+            for e in cedges:
+                dist = self.distance(e, d)
+                if dist is None:
+                    continue
+                s_has, k_has = e.src in has, e.sink in has
+                if s_has and k_has:
+                    if dist[1] > 0:
+                        ok = False
+                        break
+                    if dist[1] == 0:
+                        rest.append(e)
+                        flat0.append(e)
+                elif s_has and not k_has:
+                    # a d-less member reads d-members: only at d == 0
+                    c = subst_bounds(e.phi[g.nodes[e.src].domain.index(d)], self.benv)
+                    if interval(c, self.sink_box(e) or {}) != (0, 0):
+                        ok = False
+                        break
+                    flat0.append(e)
+                else:
+                    # produced once at d == 0, read at any d >= 0
+                    flat0.append(e)
+            if not ok:
+                continue
+            first = self.level(comp, flat0, fixed + (d,))
+            out = [Loop(d, 1, first, fixed, 0, 1)]
+            if self.ext[d] > 1:
+                out.append(Loop(d, 1, self.level(has, rest, fixed + (d,)), fixed, 1,
+                                self.ext[d]))
+            return out
+        return None
 
 
 def describe(steps, g: Graph, indent=0) -> str:
@@ -340,6 +397,7 @@ def describe(steps, g: Graph, indent=0) -> str:
             free = [d for d in n.domain if d not in s.fixed]
             out.append("  " * indent + f"bulk {n.name}:{n.kind} over ({','.join(free)})")
         else:
-            out.append("  " * indent + f"for {s.dim} {'asc' if s.step > 0 else 'desc'}:")
+            rng = f" [{s.lo}, {s.hi})" if s.lo is not None else ""
+            out.append("  " * indent + f"for {s.dim} {'asc' if s.step > 0 else 'desc'}{rng}:")
             out.append(describe(s.body, g, indent + 1))
     return "\n".join(out)

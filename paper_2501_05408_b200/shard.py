@@ -31,6 +31,12 @@ class ShardSpec:
     dim: str             # the sharded loop dim (envs)
     rank: int
     world: int
+    also: tuple = ()     # co-sharded dims indexing the same envs (e.g. the
+    #                      minibatch-local env u of a PPO update, b = u*M + j)
+
+    @property
+    def dims(self):
+        return (self.dim,) + tuple(self.also)
 
     def offset(self, local_extent: int) -> int:
         return self.rank * local_extent
@@ -40,9 +46,20 @@ def _mentions(e, d) -> bool:
     return (d, "loop") in ir.free_syms(e)
 
 
-def check_shardable(g: ir.Graph, d: str) -> set:
-    """Node ids whose outputs are partial sums over d (need an all-reduce).
-    Raises ShardError when some dependence crosses envs otherwise."""
+def check_shardable(g: ir.Graph, d: str, also=(), benv=None) -> set:
+    """Node ids whose outputs are partial sums over d or a co-sharded dim
+    (need an all-reduce).  Raises ShardError when some dependence crosses
+    envs otherwise.  A co-sharded dim u may index d only as u*m + f with
+    m = ext(d)/ext(u) and 0 <= f < m (each env shard holds the same slice
+    of every u-block; needs the concrete bounds `benv`)."""
+    reduce_nodes = set()
+    for dd in (d,) + tuple(also):
+        reduce_nodes |= _check_dim(g, dd, d, tuple(also), benv)
+    return reduce_nodes
+
+
+def _check_dim(g: ir.Graph, d: str, env_dim: str, also: tuple, benv) -> set:
+    from .planner import interval, subst_bounds
     bound = g.dim_bound[d]
     reduce_nodes = set()
     for n in g.sorted_nodes():
@@ -66,6 +83,26 @@ def check_shardable(g: ir.Graph, d: str) -> set:
         if d in snk.domain:
             if c != ("sym", d, "loop"):
                 raise ShardError(f"{snk.name} reads {src.name} at {ir.expr_text(c)} along {d}")
+            continue
+        co = [u for u in also if u in snk.domain and (u, "loop") in ir.free_syms(c)]
+        if d == env_dim and co:
+            u = co[0]
+            ok = False
+            if benv is not None:
+                aff = ir.as_affine(subst_bounds(c, benv))
+                ext = {x: benv[g.dim_bound[x]] for x in g.dim_order if g.dim_bound[x] in benv}
+                if aff is not None and ext.get(u) and ext[d] % ext[u] == 0:
+                    coef, k0 = aff
+                    m = ext[d] // ext[u]
+                    rest = ("int", k0)
+                    for (name, kind), cc in coef.items():
+                        if (name, kind) != (u, "loop"):
+                            rest = ("add", rest, ("mul", ("int", cc), ("sym", name, kind)))
+                    box = {x: (0, ext[x] - 1) for x in snk.domain if x in ext}
+                    lo, hi = interval(rest, box)
+                    ok = coef.get((u, "loop")) == m and lo >= 0 and hi < m
+            if not ok:
+                raise ShardError(f"{snk.name} reads {src.name}[{ir.expr_text(c)}] across envs")
             continue
         full = c == ("slice", ("int", 0), ("sym", bound, "bound"))
         if not full:

@@ -91,10 +91,43 @@ def write_case(name, g, bounds, inputs, seed, meta):
           f"{doc['ref_seconds']}s")
 
 
+def ppo_inputs(d_o, H, d_a, dtype, seed=1234):
+    """PPO trunk + heads ~ N(0, 1/fan_in) from default_rng(seed), biases zero."""
+    sys.path.insert(0, ROOT)
+    from paper_2501_05408_b200.workloads import ppo_inputs as mk
+    return mk(d_o=d_o, H=H, d_a=d_a, dtype=dtype, seed=seed)
+
+
+def ppo_cases():
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+    # (I, B, T, epochs, minibatches)
+    for dt, (I, B, T, ep, mb) in (("f64", (2, 4, 5, 2, 2)), ("f32", (2, 4, 5, 2, 2)),
+                                  ("f32", (1, 8, 6, 2, 4)), ("f64", (1, 6, 7, 3, 2))):
+        ctx = P.ctx_ppo_mlp(B=B, T=T, I=I, epochs=ep, minibatches=mb, d_o=4, H=8, d_a=2,
+                            dtype=dt, lr=0.002)
+        g = pdg.build(ctx)
+        pdg.eliminate_dead(g)
+        inputs = ppo_inputs(4, 8, 2, dt)
+        write_case(f"ppo_{dt}_I{I}B{B}T{T}E{ep}M{mb}", g, None, inputs, 0,
+                   {"program": "ppo_mlp", "dtype": dt})
+    # benchmark graphs: C3 (E=4096 x T=512) and the per-GPU shard of C5
+    for name, B in (("ppo_c3", 4096),):
+        ctx = P.ctx_ppo_mlp(B=B)
+        g = pdg.build(ctx)
+        pdg.eliminate_dead(g)
+        with open(os.path.join(GRAPHS, f"{name}.json"), "w") as fh:
+            fh.write(ir.from_pdg(g).to_json())
+        print(f"wrote graphs/{name}.json")
+
+
 def main():
     dsl, fe, pdg, tr, rt, ps = P.recten()
     os.makedirs(CASES, exist_ok=True)
     os.makedirs(GRAPHS, exist_ok=True)
+    if "--only" in sys.argv:
+        what = sys.argv[sys.argv.index("--only") + 1]
+        return {"ppo": ppo_cases}[what]()
+    ppo_cases()
     V = variants()
 
     # corpus x variants x seeds (reference pkg/tests/test_dsl.py:240-248)

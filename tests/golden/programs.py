@@ -299,3 +299,128 @@ def mlp_inputs(d_o=16, H=256, d_a=4, dtype="f32", seed=1234):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
     from paper_2501_05408_b200.workloads import mlp_inputs as mk
     return mk(d_o=d_o, H=H, d_a=d_a, dtype=dtype, seed=seed)
+
+
+# ---------------------------------------------------------------------------
+# C3/C5: PPO with GAE(lambda) and epochs x minibatches over a shared
+# policy/value MLP (BASELINE.json configs[2], configs[4]).
+
+
+def ctx_ppo_mlp(B=4096, T=512, I=1, epochs=4, minibatches=4, d_o=16, H=256, d_a=4,
+                gamma=0.99, lam=0.95, lr=None, beta=0.5, cv=0.5, dtype="f32"):
+    """One PPO iteration per point of `i`.
+
+    Rollout over (i,b,t) at the iteration's entry weights theta[i,0,0]:
+    shared tanh trunk h1,h2, policy head mu (d_a) and value head V (1);
+    Gaussian actions a = mu + eps; the reference's synthetic env
+    (dsl.py:288-307).  Advantages by GAE(lambda) written as the suffix
+    discounted sum A = dsum(delta[t:T], gamma*lam) (the lifted form of
+    SURVEY Appendix C), delta = r + gamma*V[t+1] - V (bootstrap 0 at T-1);
+    returns R = A + V.
+
+    Updates over epochs e and minibatches j (the two-level carry of the
+    reference's epoch_minibatch.rtl: w[e,k+1] from w[e,k], w[e+1,0] from
+    w[e,K-1]): minibatch j is the fixed env set {u*M + j : u < B/M} (an
+    interleaved partition, so that an env shard [r*B/G, (r+1)*B/G) holds an
+    equal slice of every minibatch and the sharded run is the same
+    program); the policy/value are re-evaluated at theta[i,e,j] on the
+    stored rollout and theta advances by -lr * grad.
+
+    Loss per (e,j,u,t): -ratio*A + cv*(V_new - R)^2 + beta*(lp_new - lp_old)^2
+    with ratio = exp(lp_new - lp_old).  The front end has no differentiable
+    clip/min (`where`/`cmp` are gradient barriers, frontend.py:238-243), so
+    the clipped surrogate is replaced by this quadratic trust-region penalty
+    (SURVEY H9)."""
+    dsl, fe, pdg, tr, rt, ps = recten()
+    import recten.symexpr as se
+    M, E = minibatches, epochs
+    assert B % M == 0
+    Bm = B // M
+    if lr is None:
+        lr = 0.01 / (Bm * T)
+    ctx = fe.Context()
+    i, Ib = ctx.declare_dim("i", "I")
+    e, Eb = ctx.declare_dim("e", "E")
+    j, Mb = ctx.declare_dim("j", "M")
+    u, Ub = ctx.declare_dim("u", "U")
+    b, Bb = ctx.declare_dim("b", "B")
+    t, Tb = ctx.declare_dim("t", "T")
+    for s, v in ((Ib, I), (Eb, E), (Mb, M), (Ub, Bm), (Bb, B), (Tb, T)):
+        ctx.bind(s, v)
+    shapes = {"W1": (d_o, H), "b1": (1, H), "W2": (H, H), "b2": (1, H),
+              "W3": (H, d_a), "b3": (1, d_a), "Wv": (H, 1), "bv": (1, 1)}
+    init = {n: ctx.input(f"{n}_0", s, dtype) for n, s in shapes.items()}
+    par = {n: ctx.recurrent(n, s, dtype, (i, e, j)) for n, s in shapes.items()}
+    grad = {n: ctx.recurrent(f"g{n}", s, dtype, (i, e, j)) for n, s in shapes.items()}
+    cond = {c: se.parse(c, ctx.resolve_symbol) for c in
+            ("i == 0 and e == 0 and j == 0", "i >= 1 and e == 0 and j == 0",
+             "e >= 1 and j == 0")}
+    last = "E - 1,M - 1"
+
+    def sgd(p, g_, at):
+        return ctx.detach(p[at]) - ctx.detach(g_[at]) * lr
+
+    for n in shapes:
+        par[n].define([(cond["i == 0 and e == 0 and j == 0"], init[n]),
+                       (cond["i >= 1 and e == 0 and j == 0"], sgd(par[n], grad[n], f"i-1,{last}")),
+                       (cond["e >= 1 and j == 0"], sgd(par[n], grad[n], "i,e-1,M - 1")),
+                       (None, sgd(par[n], grad[n], "i,e,j-1"))])
+    ctx.register_udf("envstep", dsl.make_udf_fn("envstep", [(1, d_o)], [dtype]),
+                     [(1, d_o)], [dtype])
+
+    def trunk(o, p, tag):
+        h1 = ctx.op("tanh", [o @ p["W1"] + p["b1"]], name=f"h1{tag}")
+        h2 = ctx.op("tanh", [h1 @ p["W2"] + p["b2"]], name=f"h2{tag}")
+        mu = ctx.op("add", [h2 @ p["W3"], p["b3"]], name=f"mu{tag}")
+        v = ctx.op("add", [h2 @ p["Wv"], p["bv"]], name=f"V{tag}")
+        return mu, ctx.sum(ctx.sum(v, 1), 0)
+
+    # rollout at theta[i,0,0]
+    p0 = {n: par[n]["i,0,0"] for n in shapes}
+    eps = ctx.rng("eps", (1, d_a), dtype, (i, b, t), "normal")
+    o = ctx.recurrent("o", (1, d_o), dtype, (i, b, t))
+    z0 = ctx.constant(0.1, dtype, (1, d_o), name="z0")
+    mu, V = trunk(o, p0, "")
+    a = ctx.op("add", [ctx.detach(mu), eps], name="a")
+    (onext,) = ctx.udf("envstep", [o, a])
+    o.define([(se.eq(se.sym(t), se.cint(0)), z0), (None, onext["i,b,t-1"])])
+    r = ctx.sum(ctx.sum(o, 1), 0)
+    Vd = ctx.detach(V)
+    zero = ctx.constant(0.0, dtype, (), name="vboot")
+    Vn = ctx.recurrent("Vn", (), dtype, (i, b, t))
+    Vn.define([(se.parse("t == T - 1", ctx.resolve_symbol), zero), (None, Vd["i,b,t+1"])])
+    delta = ctx.op("sub", [r + Vn * gamma, Vd], name="delta")
+    A = ctx.discounted_sum(delta["i,b,t:T"], gamma * lam, dim=0)
+    Rt = ctx.op("add", [A, Vd], name="R")
+    d0 = a - ctx.detach(mu)
+    lp_old = ctx.sum(ctx.sum(-(d0 * d0) * 0.5, 1), 0)
+
+    # updates at (e, j) on minibatch j: env b = u * M + j
+    idx = "i,u * M + j,t"
+    mu_n, V_n = trunk(o[idx], par, "_n")
+    dn = a[idx] - mu_n
+    lp_new = ctx.sum(ctx.sum(-(dn * dn) * 0.5, 1), 0)
+    diff = lp_new - ctx.detach(lp_old)[idx]
+    ratio = ctx.op("exp", [diff], name="ratio")
+    verr = V_n - ctx.detach(Rt)[idx]
+    L = ctx.op("add", [-(ratio * ctx.detach(A)[idx]) + verr * verr * cv, diff * diff * beta],
+               name="L")
+    Lu = ctx.sum(L["i,e,j,u,0:T"], 0)
+    Lj = ctx.sum(Lu["i,e,j,0:U"], 0)
+    Le = ctx.sum(Lj["i,e,0:M"], 0)
+    Li = ctx.sum(Le["i,0:E"], 0)
+    loss = ctx.sum(Li["0:I"], 0)
+    gr = ctx.backward(loss, [par[n] for n in shapes])
+    for n in shapes:
+        grad[n].define([(None, gr[par[n]])])
+    nxt = {n: ctx.op("sub", [ctx.detach(par[n][f"i,{last}"]),
+                             ctx.detach(grad[n][f"i,{last}"]) * lr], name=f"{n}_next")
+           for n in shapes}
+    for n in shapes:
+        ctx.mark_output(nxt[n], f"{n}_next")
+    ctx.mark_output(Lj, "loss")
+    ctx.mark_output(A, "A")
+    return ctx
+
+
+PPO_PARAMS = ("W1", "b1", "W2", "b2", "W3", "b3", "Wv", "bv")

@@ -50,8 +50,7 @@ def test_struct_layouts_match_header(tmp_path):
 
 def dry_lower(g, benv, seed=0, fuse=True):
     h = X.copy_graph(g)
-    X.inline_dataflow(h, benv)
-    X.eliminate_dead(h)
+    X.prepare(h, benv)
     pshape = X.payload_shapes(h, benv)
     an = X.analyze(h, benv, pshape, fuse)
     bufs, ptr = an["bufs"], 1 << 20
@@ -84,7 +83,7 @@ def test_c2_plan_batches_envs_and_fuses_dw():
     plan, low, contract, alias = dry_lower(g, {"I": 1, "B": 1024, "T": 1000})
     txt = P.describe(plan.steps, plan.graph)
     assert "for t asc" in txt and "for b" not in txt
-    assert "bulk o:merge over (b)" in txt
+    assert "bulk o:merge over (b)" in txt or "bulk o:merge over (i,b)" in txt
     assert len(contract) == 3
     kinds = [k for (k, *_r) in low.recs]
     assert kinds.count(N.RT_K_SCAN) == 1           # G = dsum(r[t:T]) as one reverse scan
@@ -107,8 +106,7 @@ def test_every_touched_buffer_is_materialised(case):
                                                                g.bindings.get(g.dim_bound[d]))
             for d in g.dim_order}
     h = X.copy_graph(g)
-    X.inline_dataflow(h, benv)
-    X.eliminate_dead(h)
+    X.prepare(h, benv)
     pshape = X.payload_shapes(h, benv)
     an = X.analyze(h, benv, pshape, True)
     bufs = an["bufs"]
@@ -149,3 +147,53 @@ def test_thin_gemm_selection():
             assert thin and thin[0].variant == variant
             if variant == 1:
                 assert any(r[0] == N.RT_K_SPLITK for r in low.recs)
+
+
+PPO_BOUNDS = {"I": 1, "E": 4, "M": 4, "U": 1024, "B": 4096, "T": 512}
+
+
+def _ppo_analysis():
+    g = load_graph("ppo_c3")
+    h = X.copy_graph(g)
+    X.prepare(h, PPO_BOUNDS)
+    an = X.analyze(h, PPO_BOUNDS, X.payload_shapes(h, PPO_BOUNDS))
+    byname = {h.nodes[k[0]].name: b for k, b in an["bufs"].items() if k[1] == 0}
+    return h, an, byname
+
+
+def test_ppo_plan_peels_rollout_into_first_update():
+    """The rollout (over b,t) reads theta[i,0,0] that the update loops
+    advance: planned as e in [0,1) / j in [0,1) peels holding the rollout,
+    then the remaining minibatches and epochs (planner.peel_for)."""
+    h, an, _ = _ppo_analysis()
+    txt = P.describe(an["plan"].steps, h)
+    assert "for e asc [0, 1):" in txt and "for e asc [1, 4):" in txt
+    assert "for j asc [0, 1):" in txt and "for j asc [1, 4):" in txt
+    assert "bulk o:merge over (b)" in txt        # all envs per acting step
+
+
+def test_ppo_storage_folding():
+    """Minibatch activations keep one (u,t) slab (folded along e and j);
+    a permute of the rollout over (i,j,u,t) that later epochs re-read is
+    NOT folded along j (it is produced once, in the e = 0 peel)."""
+    h, an, bufs = _ppo_analysis()
+    assert bufs["h1_n"].folded == frozenset({"e", "j"})
+    assert bufs["h2_n"].folded == frozenset({"e", "j"})
+    lacking_e = [b for name, b in bufs.items()
+                 if "j" in b.dims and "e" not in b.dims and "u" in b.dims]
+    assert lacking_e and all(not b.folded for b in lacking_e)
+    assert all(not b.folded for name, b in bufs.items() if name in ("A", "R", "o", "a"))
+
+
+def test_ppo_env_shard_co_shards_minibatch_envs():
+    """b = u*M + j: sharding envs b shards every minibatch's u with them;
+    the reductions over u (losses, 8 parameter gradients) get all-reduces."""
+    from paper_2501_05408_b200.shard import check_shardable
+    g = load_graph("ppo_c3")
+    b = dict(PPO_BOUNDS, U=512, B=2048)
+    h = X.copy_graph(g)
+    X.prepare(h, b)
+    red = check_shardable(h, "b", ("u",), b)
+    assert len(red) == 9
+    with pytest.raises(Exception):
+        check_shardable(h, "b", (), b)        # without u: b read across envs

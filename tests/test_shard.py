@@ -42,8 +42,7 @@ def test_cross_env_reads_are_refused():
 
 def _dry(g, benv, shard):
     h = X.copy_graph(g)
-    X.inline_dataflow(h, benv)
-    X.eliminate_dead(h)
+    X.prepare(h, benv)
     red = check_shardable(h, shard.dim)
     an = X.analyze(h, benv, X.payload_shapes(h, benv), True)
     ptr = 1 << 20
