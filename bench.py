@@ -240,11 +240,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one process per GPU; BENCH_DIST_BACKEND=gloo lets several ranks share
+    # one GPU (a functional check of the sharded path, not a measurement)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
     g = load_graph()
     B = WL.local_envs(world)
     T_STEPS = WL.T

@@ -165,7 +165,7 @@ typedef struct {
   rt_view out;
   /* window form: y[j] = S[lo(j)] - gamma^(hi-lo) * S[hi(j)], unused if win=0 */
   int32_t win;
-  int32_t _pad2;
+  int32_t tile;        /* 1: tiled kernel (64 contiguous lines per CTA, 16-B I/O) */
 } rt_scan_params;
 
 /* RT_K_GEMM: for z in Z, C[z,m,n] (+)= sum_k A[z,m,k] * B[z,k,n].
@@ -221,6 +221,11 @@ typedef struct {
  *   variant 1: C[w,r] = sum_k X[k,w] * Y[k,r]   (K split over blockIdx.y,
  *              fp32/fp64 partials part[s, w*part_w + r*part_r] -> RT_K_SPLITK)
  *   variant 2: C[w,r] = epi(sum_k X[w,k] * Y[k,r] + bias[r])   (K <= 32)
+ *   variant 3: C[w,r] (+)= epi(sum_k X[w,k] * Y[k,r] + bias[r]) for R <= 8
+ *              and 32 <= K <= 1024 (policy/value heads over all points):
+ *              a warp per row group, Y held in registers, rows streamed
+ *              with 16-byte loads; w decomposed over the box W (strides
+ *              X.s2[0..], C.s1[0..]); vec != 0 when rows are 16-B aligned.
  * Strides: X.s1[0] along k, X.s2[0] along w; Y.s1[0] along k, Y.s2[0]
  * along r; C.s1[0] along w, C.s2[0] along r; bias.s2[0] along r. */
 typedef struct {
@@ -231,10 +236,11 @@ typedef struct {
   int32_t splits;
   int32_t accumulate;
   int32_t epilogue;
-  int32_t _pad;
+  int32_t vec;
   int64_t part_w, part_r;
   uint64_t part;
   rt_gop X, Y, C, bias;
+  rt_gbox W;           /* variant 3: decomposition of w (nd == 0: flat) */
 } rt_thin_params;
 
 /* Point coordinates for per-point entropy: coordinate j of the node's

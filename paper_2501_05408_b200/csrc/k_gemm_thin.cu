@@ -121,7 +121,154 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
   }
 }
 
+// variant 3: narrow-N row products C[w, 0:R] = X[w, 0:K] @ Y[0:K, 0:R].
+// One warp per RW (4 or 8) rows per iteration; lane l owns k in {l*VW + 32*VW*i}
+// for i < KI, with the matching Y rows held in registers for the whole
+// kernel.  Rows stream through 16-byte loads (RW rows x KI vectors in
+// flight per lane), partial dots reduce with xor shuffles, and lane
+// rr*R + r stores element (rr, r).
+template <typename T> struct vec16;
+template <> struct vec16<float> { using V = float4; static constexpr int W = 4; };
+template <> struct vec16<double> { using V = double2; static constexpr int W = 2; };
+
+template <typename T>
+RT_DEV void unpack(const typename vec16<T>::V& v, T* out);
+template <> RT_DEV void unpack<float>(const float4& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+template <> RT_DEV void unpack<double>(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
+RT_DEV void unpack_zero(float4& v) { v = make_float4(0.f, 0.f, 0.f, 0.f); }
+RT_DEV void unpack_zero(double2& v) { v = make_double2(0.0, 0.0); }
+
+RT_DEV int64_t wdec(const rt_gbox& b, int64_t flat, const int64_t* s) {
+  if (b.nd <= 1) return flat * s[0];
+  int64_t o = 0;
+  for (int d = b.nd - 1; d >= 0; --d) {
+    const int64_t e = b.ext[d];
+    const int64_t q = flat / e;
+    o += (flat - q * e) * s[d];
+    flat = q;
+  }
+  return o;
+}
+
+template <typename T, int R, int KI>
+__global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ rt_thin_params p) {
+  using V = typename vec16<T>::V;
+  constexpr int VW = vec16<T>::W;
+  constexpr int RW = (R * KI * VW >= 16) ? 4 : 8;   // rows per warp iteration
+  const int lane = threadIdx.x & 31;
+  const int K = (int)p.k;
+  const T* X = (const T*)p.X.ptr + p.X.off;
+  const T* Y = (const T*)p.Y.ptr + p.Y.off;
+  T* Cp = (T*)p.C.ptr + p.C.off;
+  const int64_t xk = p.X.s1[0];
+  T y[KI][VW][R];
+#pragma unroll
+  for (int i = 0; i < KI; ++i)
+#pragma unroll
+    for (int j = 0; j < VW; ++j) {
+      const int k = (i * 32 + lane) * VW + j;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        y[i][j][r] = (k < K && r < p.r) ? Y[k * p.Y.s1[0] + r * p.Y.s2[0]] : (T)0;
+    }
+  T bias[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    bias[r] = (p.bias.ptr && r < p.r)
+                  ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + r * p.bias.s2[0])
+                  : (T)0;
+  const int64_t gw = (int64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (THREADS / 32);
+  for (int64_t w0 = gw * RW; w0 < p.w; w0 += nw * RW) {
+    T acc[RW][R];
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[rr][r] = (T)0;
+    int64_t xo[RW];
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+      const int64_t w = w0 + rr < p.w ? w0 + rr : p.w - 1;
+      xo[rr] = wdec(p.W, w, p.X.s2);
+    }
+    if (p.vec) {
+      V xv[RW][KI];
+#pragma unroll
+      for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+        for (int i = 0; i < KI; ++i) {
+          const int k = (i * 32 + lane) * VW;
+          if (k < K) xv[rr][i] = __ldcs(reinterpret_cast<const V*>(X + xo[rr] + k));
+          else unpack_zero(xv[rr][i]);
+        }
+#pragma unroll
+      for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+        for (int i = 0; i < KI; ++i) {
+          T xs[VW];
+          unpack<T>(xv[rr][i], xs);
+#pragma unroll
+          for (int j = 0; j < VW; ++j)
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[rr][r] = fma(xs[j], y[i][j][r], acc[rr][r]);
+        }
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+        for (int i = 0; i < KI; ++i)
+#pragma unroll
+          for (int j = 0; j < VW; ++j) {
+            const int k = (i * 32 + lane) * VW + j;
+            const T x = k < K ? __ldcs(X + xo[rr] + k * xk) : (T)0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[rr][r] = fma(x, y[i][j][r], acc[rr][r]);
+          }
+    }
+    T mine = (T)0;
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        T v = acc[rr][r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == rr * R + r) mine = v;
+      }
+    if (lane < RW * R) {
+      const int rr = lane / R, r = lane - rr * R;
+      const int64_t w = w0 + rr;
+      if (w < p.w && r < p.r) {
+        T* cptr = Cp + wdec(p.W, w, p.C.s1) + r * p.C.s2[0];
+        T a = mine;
+        if (p.accumulate) a += *cptr;
+        a += bias[r];
+        if (p.epilogue == 1) a = vm_tanh<T>(a);
+        *cptr = a;
+      }
+    }
+  }
+}
+
 }  // namespace
+
+extern "C" void* rt_kernel_thin_rows(int f64, int r, int k) {
+#define RT_ROWS(T, R)                                            \
+  if (r <= R) {                                                  \
+    constexpr int C = 32 * vec16<T>::W;                          \
+    if (k <= C) return (void*)k_thin_rows<T, R, 1>;              \
+    if (k <= 2 * C) return (void*)k_thin_rows<T, R, 2>;          \
+    if (k <= 4 * C) return (void*)k_thin_rows<T, R, 4>;          \
+    return (void*)k_thin_rows<T, R, 8>;                          \
+  }
+  if (f64) {
+    RT_ROWS(double, 1) RT_ROWS(double, 2) RT_ROWS(double, 4)
+  } else {
+    RT_ROWS(float, 1) RT_ROWS(float, 2) RT_ROWS(float, 4)
+  }
+#undef RT_ROWS
+  return nullptr;
+}
 
 extern "C" void* rt_kernel_thin(int variant, int f64, int r) {
   if (variant == 2) {

@@ -23,6 +23,8 @@ extern "C" void* rt_kernel_policy(const void* params);
 extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
+extern "C" void* rt_kernel_thin_rows(int f64, int r, int k);
+extern "C" void* rt_kernel_scan_tile(int f64);
 extern "C" void* rt_gemm_tma_pack(void* blk, void* encode);
 
 static thread_local std::string g_err;
@@ -121,6 +123,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       rt_scan_params* p = (rt_scan_params*)blk;
       fold_view(p->in, env, nenv);
       fold_view(p->out, env, nenv);
+      if (p->tile) return rt_kernel_scan_tile(p->f64);
       int warp = p->in.stride[p->sdim] == 1 && p->out.stride[p->sdim] == 1;
       return rt_kernel_scan(p->f64, warp);
     }
@@ -156,6 +159,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_gop(p->Y, env, nenv);
       fold_gop(p->C, env, nenv);
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
+      if (p->variant == 3) return rt_kernel_thin_rows(p->f64, (int)p->r, (int)p->k);
       return rt_kernel_thin(p->variant, p->f64, (int)(p->variant == 2 ? p->k : p->r));
     }
     case RT_K_SPLITK: {

@@ -1058,9 +1058,7 @@ class Lowering:
                     v.stride[slab.index(d)] = st[j]
             for i, s in enumerate(st[len(n.domain):]):
                 v.stride[len(slab) + i] = s
-        warp = p.in_.stride[p.sdim] == 1 and p.out.stride[p.sdim] == 1
-        grid = self.grid1(p.total_lines * (32 if warp else 1))
-        self.add_rec(N.RT_K_SCAN, p, grid, [256, 1, 1], 0, (n.id, n.name))
+        self._scan_launch(p, (n.id, n.name))
         return True
 
     def _reduce(self, ctx, ev: EdgeVal, red_axes, op, gamma=1.0, reverse=False):
@@ -1227,9 +1225,37 @@ class Lowering:
         p.total_lines = prod(box) // box[p.sdim]
         p.in_ = self.make_view(ctx, ev, [a.stride for a in ev.axes])
         p.out = self.out_view(ctx, key)
-        warp = p.in_.stride[p.sdim] == 1 and p.out.stride[p.sdim] == 1
-        grid = self.grid1(p.total_lines * (32 if warp else 1))
-        self.add_rec(N.RT_K_SCAN, p, grid, [256, 1, 1], 0, (n.id, n.name))
+        self._scan_launch(p, (n.id, n.name))
+
+    def _scan_launch(self, p, label):
+        """Pick the scan kernel (csrc/k_scan.cu): tiled 64-line CTAs with
+        16-byte I/O for contiguous lines whose starts and length are
+        vector-aligned; warp-per-line for other contiguous lines; one
+        thread per line (64-thread CTAs, many in flight) for strided lines."""
+        sd = p.sdim
+        contig = p.in_.stride[sd] == 1 and p.out.stride[sd] == 1
+        same_t = p.in_.dtype == p.out.dtype == (N.RT_F64 if p.f64 else N.RT_F32)
+        vw = 2 if p.f64 else 4
+        esize = 8 if p.f64 else 4
+
+        def aligned(v):
+            if (v.ptr + esize * v.off) % 16:
+                return False
+            if any(v.off_env[e] % vw for e in range(N.RT_MAXENV)):
+                return False
+            return all(v.stride[d] % vw == 0 for d in range(p.box.nd)
+                       if d != sd and p.box.ext[d] > 1)
+
+        L = p.box.ext[sd]
+        if contig and same_t and L % vw == 0 and aligned(p.in_) and aligned(p.out):
+            p.tile = 1
+            grid = [int(max(1, min(-(-p.total_lines // 64), 148 * 16))), 1, 1]
+            self.add_rec(N.RT_K_SCAN, p, grid, [64, 1, 1], 0, label)
+        elif contig:
+            self.add_rec(N.RT_K_SCAN, p, self.grid1(p.total_lines * 32), [256, 1, 1], 0, label)
+        else:
+            self.add_rec(N.RT_K_SCAN, p, self.grid1(p.total_lines, 64, 148 * 64), [64, 1, 1], 0,
+                         label)
 
     def k_cumsum(self, ctx: Ctx):
         n = ctx.node
@@ -1452,13 +1478,16 @@ class Lowering:
         if p.z != 1 or any(t[0] != 1 for t in Z):
             return False
         mc, nc, kc = self._collapse(M, (1, 3)), self._collapse(Nn, (2, 3)), self._collapse(K, (1, 2))
-        if mc is None or nc is None or kc is None:
-            return False
-        (m, (a_m, c_m)), (n, (b_n, c_n)), (k, (a_k, b_k)) = mc, nc, kc
         dt = [self._gop_dtype(x) for x in (p.A, p.B, p.C)]
         f64 = dt == ["f64"] * 3
         if not (f64 or dt == ["f32"] * 3):
             return False
+        if nc is not None and kc is not None and self._gemm_rows(p, M, nc, kc, f64, label,
+                                                                 accumulate, epilogue, bias):
+            return True
+        if mc is None or nc is None or kc is None:
+            return False
+        (m, (a_m, c_m)), (n, (b_n, c_n)), (k, (a_k, b_k)) = mc, nc, kc
         q = N.rt_thin_params()
         q.f64 = int(f64)
         esize = 8 if f64 else 4
@@ -1512,6 +1541,57 @@ class Lowering:
             self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
             return True
         return False
+
+    ROWS_MAX_R = 4
+
+    def _gemm_rows(self, p, M, nc, kc, f64, label, accumulate, epilogue, bias):
+        """Narrow-N products over many rows (policy/value heads, N <= 4,
+        32 <= K <= 1024, contiguous K) -> RT_K_THIN variant 3: HBM-bound
+        row streams instead of tensor-core tiles that would be 98% padding."""
+        (n, (b_n, c_n)), (k, (a_k, b_k)) = nc, kc
+        m = prod(t[0] for t in M)
+        vw = 2 if f64 else 4
+        ki = -(-k // (32 * vw))
+        if not (n <= self.ROWS_MAX_R and 32 <= k and ki <= 8 and ki * vw * n <= 32
+                and m >= 2048 and a_k == 1):
+            return False
+        mdims = [t for t in M if t[0] != 1] or [(1, 0, 0, 0)]
+        if len(mdims) > 4:
+            return False
+        esize = 8 if f64 else 4
+        q = N.rt_thin_params()
+        q.variant, q.f64 = 3, int(f64)
+        q.w, q.r, q.k = m, n, k
+        q.W.nd = len(mdims)
+        for i, t in enumerate(mdims):
+            q.W.ext[i] = t[0]
+
+        def gop(src, s1, s2):
+            g = N.rt_gop()
+            C.memmove(C.addressof(g), C.addressof(src), C.sizeof(g))
+            for arr in (g.sz, g.s1, g.s2):
+                for i in range(4):
+                    arr[i] = 0
+            for i, v in enumerate(s1):
+                g.s1[i] = v
+            for i, v in enumerate(s2):
+                g.s2[i] = v
+            return g
+
+        q.X = gop(p.A, [1], [t[1] for t in mdims])
+        q.Y = gop(p.B, [b_k], [b_n])
+        q.C = gop(p.C, [t[3] for t in mdims], [c_n])
+        if bias is not None:
+            q.bias = gop(bias, [0], [bias.s2[0]])
+        q.accumulate, q.epilogue = accumulate, epilogue
+        A = p.A
+        q.vec = int(k % vw == 0 and (A.ptr + esize * A.off) % 16 == 0
+                    and all(t[1] % vw == 0 for t in mdims)
+                    and all(A.off_env[e] % vw == 0 for e in range(N.RT_MAXENV)))
+        rows_per_cta = 8 * 8
+        grid = [int(max(1, min(-(-m // rows_per_cta), 148 * 16))), 1, 1]
+        self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], 0, label)
+        return True
 
     @staticmethod
     def _gop_dtype(g):

@@ -75,7 +75,7 @@ class rt_reduce_params(C.Structure):
 class rt_scan_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("box", rt_box), ("total_lines", i64), ("sdim", i32),
                 ("reverse", i32), ("gamma", f64), ("f64", i32), ("chunk", i32),
-                ("in_", rt_view), ("out", rt_view), ("win", i32), ("_pad2", i32)]
+                ("in_", rt_view), ("out", rt_view), ("win", i32), ("tile", i32)]
 
 
 class rt_gbox(C.Structure):
@@ -103,9 +103,9 @@ class rt_splitk_params(C.Structure):
 
 class rt_thin_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("variant", i32), ("f64", i32), ("w", i64), ("r", i64), ("k", i64),
-                ("splits", i32), ("accumulate", i32), ("epilogue", i32), ("_pad", i32),
+                ("splits", i32), ("accumulate", i32), ("epilogue", i32), ("vec", i32),
                 ("part_w", i64), ("part_r", i64), ("part", u64), ("X", rt_gop), ("Y", rt_gop),
-                ("C", rt_gop), ("bias", rt_gop)]
+                ("C", rt_gop), ("bias", rt_gop), ("W", rt_gbox)]
 
 
 class rt_rng_params(C.Structure):

@@ -120,13 +120,32 @@ def ppo_cases():
         print(f"wrote graphs/{name}.json")
 
 
+def kernel_graphs():
+    """Single-kernel programs for bench_kernels.py (HBM-roofline checks of
+    the scan and gather kernels at full HBM scale) + small oracle cases."""
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+    import numpy as np
+    for name in P.KERNEL_NAMES:
+        g = pdg.build(P.ctx_kernel(name))
+        with open(os.path.join(GRAPHS, f"{name}.json"), "w") as fh:
+            fh.write(ir.from_pdg(g).to_json())
+        rng = np.random.default_rng(7)
+        inputs = {}
+        for n in g.sorted_nodes():
+            if n.kind == "input":
+                dom = tuple(g.bindings[g.dim_bound[d]] for d in n.domain)
+                inputs[n.name] = rng.standard_normal(dom + tuple(n.out_shapes[0])).astype(
+                    np.float32)
+        write_case(name, g, None, inputs, 0, {"program": name})
+
+
 def main():
     dsl, fe, pdg, tr, rt, ps = P.recten()
     os.makedirs(CASES, exist_ok=True)
     os.makedirs(GRAPHS, exist_ok=True)
     if "--only" in sys.argv:
         what = sys.argv[sys.argv.index("--only") + 1]
-        return {"ppo": ppo_cases}[what]()
+        return {"ppo": ppo_cases, "kernels": kernel_graphs}[what]()
     ppo_cases()
     V = variants()
 

@@ -424,3 +424,54 @@ def ctx_ppo_mlp(B=4096, T=512, I=1, epochs=4, minibatches=4, d_o=16, H=256, d_a=
 
 
 PPO_PARAMS = ("W1", "b1", "W2", "b2", "W3", "b3", "Wv", "bv")
+
+
+# ---------------------------------------------------------------------------
+# Single-kernel f32 programs for bench_kernels.py (scan / gather rooflines)
+
+
+def ctx_kernel(name, B=4, T=5, M=2):
+    dsl, fe, pdg, tr, rt, ps = recten()
+    import recten.symexpr as se
+    ctx = fe.Context()
+    if name == "k_returns_tb":
+        t, Tb = ctx.declare_dim("t", "T")
+        b, Bb = ctx.declare_dim("b", "B")
+    else:
+        if name == "k_gather_mb":
+            j, Mb = ctx.declare_dim("j", "M")
+            u, Ub = ctx.declare_dim("u", "U")
+            ctx.bind(Mb, M)
+            ctx.bind(Ub, B // M)
+        b, Bb = ctx.declare_dim("b", "B")
+        t, Tb = ctx.declare_dim("t", "T")
+    ctx.bind(Bb, B)
+    ctx.bind(Tb, T)
+    if name == "k_returns_bt":
+        r = ctx.input("r", (), "f32", (b, t))
+        G = ctx.discounted_sum(r["b,t:T"], 0.99, dim=0)
+        ctx.mark_output(G, "G")
+    elif name == "k_returns_tb":
+        r = ctx.input("r", (), "f32", (t, b))
+        G = ctx.discounted_sum(r["t:T,b"], 0.99, dim=0)
+        ctx.mark_output(G, "G")
+    elif name == "k_gae_bt":
+        r = ctx.input("r", (), "f32", (b, t))
+        V = ctx.input("V", (), "f32", (b, t))
+        Vn = ctx.recurrent("Vn", (), "f32", (b, t))
+        zero = ctx.constant(0.0, "f32", (), name="vboot")
+        Vn.define([(se.parse("t == T - 1", ctx.resolve_symbol), zero), (None, V["b,t+1"])])
+        d = ctx.op("sub", [r + Vn * 0.99, V], name="delta")
+        A = ctx.discounted_sum(d["b,t:T"], 0.99 * 0.95, dim=0)
+        ctx.mark_output(A, "A")
+    elif name == "k_gather_mb":
+        x = ctx.input("x", (16,), "f32", (b, t))
+        y = ctx.op("mul", [x["u * M + j,t"], ctx.constant(1.0, "f32", (), name="one")],
+                   name="y")
+        ctx.mark_output(y, "y")
+    else:
+        raise KeyError(name)
+    return ctx
+
+
+KERNEL_NAMES = ("k_returns_bt", "k_returns_tb", "k_gae_bt", "k_gather_mb")

@@ -176,3 +176,18 @@ def test_tma_gemm_pipeline(B, K, N, contract):
     assert NN.RT_K_GEMM_TMA in _kinds(g, inp)
     out = execute(g, inputs=inp)["s" if contract else "y"]
     np.testing.assert_allclose(out, want.astype(np.float32), rtol=1e-5, atol=atol)
+
+
+@pytest.mark.parametrize("N,K,dt", [(1, 256, "f32"), (4, 256, "f32"), (2, 100, "f32"),
+                                    (4, 256, "f64"), (3, 64, "f64")])
+def test_narrow_head_rows_gemm(N, K, dt):
+    """Policy/value heads over all points (N <= 4): RT_K_THIN variant 3."""
+    B = 20000
+    npd = np.float32 if dt == "f32" else np.float64
+    rng = np.random.default_rng(N * 100 + K)
+    x = rng.standard_normal((B, 1, K)).astype(npd)
+    W = (rng.standard_normal((K, N)) / 16).astype(npd)
+    out = execute(mm_graph(B, K, N, dt=dt), inputs={"x": x, "W": W})["y"]
+    want = (x.astype(np.float64) @ W.astype(np.float64))
+    tol = 1e-5 if dt == "f32" else 1e-12
+    np.testing.assert_allclose(out, want, rtol=tol, atol=tol)

@@ -197,3 +197,15 @@ def test_ppo_env_shard_co_shards_minibatch_envs():
     assert len(red) == 9
     with pytest.raises(Exception):
         check_shardable(h, "b", (), b)        # without u: b read across envs
+
+
+def test_ppo_heads_use_row_stream_gemm():
+    """mu_n (N=4) and V_n (N=1) over a minibatch's (u,t) rows are narrow-N
+    row streams (thin variant 3), not 128x256 tensor-core tiles."""
+    g = load_graph("ppo_c3")
+    plan, low, _, _ = dry_lower(g, PPO_BOUNDS)
+    fam = {}
+    for (k, p, *_r, lab) in low.recs:
+        if lab[1] in ("mu_n", "V_n", "V"):
+            fam.setdefault(lab[1], set()).add((k, getattr(p, "variant", None)))
+    assert fam["mu_n"] == {(N.RT_K_THIN, 3)} and fam["V_n"] == {(N.RT_K_THIN, 3)}
