@@ -227,8 +227,163 @@ __global__ void __launch_bounds__(SCAN_LB) k_scan_tile(const __grid_constant__ r
   }
 }
 
+// Pipelined tiled scan: the same 64-line CTA tiles, but chunks land in a
+// 3-stage shared-memory ring through cp.async 16-byte copies (two chunks in
+// flight while the third is scanned), so HBM sees a steady stream instead
+// of one register-prefetched chunk per CTA.
+//   STEP_MAJOR = false: lines contiguous (x[b, t], scan along t); a tile
+//     row is one line's chunk, vector slots XOR-swizzled by (line & 7) so the
+//     scan phase's 16-byte reads are bank-conflict free.
+//   STEP_MAJOR = true: the 64 lines of a CTA are adjacent in memory (x[t, b],
+//     scan along t with stride S); a tile row is one step of 64 lines.
+RT_DEV void cp16(void* smem, const void* gmem, bool valid) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;   // src-size 0: zero-fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+RT_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+RT_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+#define SCAN_NS 3
+
+template <typename T, bool STEP_MAJOR>
+__global__ void __launch_bounds__(SCAN_LB) k_scan_pipe(const __grid_constant__ rt_scan_params p) {
+  using V = typename svec<T>::V;
+  constexpr int VW = svec<T>::W;
+  constexpr int TC = 16 * VW;                  // steps per chunk
+  constexpr int NVEC = SCAN_LB * TC / VW;      // vectors per stage (1024)
+  constexpr int NV = NVEC / SCAN_LB;           // per thread (16)
+  constexpr int VPR = SCAN_LB / VW;            // step-major: vectors per row of 64 lines
+  extern __shared__ __align__(16) unsigned char sraw[];
+  V* ring = reinterpret_cast<V*>(sraw);        // [NS][NVEC], then the line bases
+  int64_t* ib = reinterpret_cast<int64_t*>(ring + SCAN_NS * NVEC);
+  int64_t* ob = ib + SCAN_LB;
+  const int tid = threadIdx.x;
+  const double g = p.gamma;
+  const T* X = (const T*)p.in.ptr;
+  T* Y = (T*)p.out.ptr;
+  const int64_t L = p.box.ext[p.sdim];
+  const int64_t si = p.in.stride[p.sdim], so = p.out.stride[p.sdim];
+  const int64_t nch = (L + TC - 1) / TC;
+  const int64_t l0 = (int64_t)blockIdx.x * SCAN_LB;
+  const int nl = (int)(p.total_lines - l0 < SCAN_LB ? p.total_lines - l0 : SCAN_LB);
+  {
+    int64_t i0, o0, a, b, LL;
+    line_base(p, l0 + (tid < nl ? tid : 0), &i0, &o0, &a, &b, &LL);
+    ib[tid] = i0;
+    ob[tid] = o0;
+  }
+  __syncthreads();
+  auto chunk = [&](int64_t c, int64_t& j0, int& cnt) {
+    const int64_t a = c * TC, b = (c + 1) * TC < L ? (c + 1) * TC : L;
+    cnt = (int)(b - a);
+    j0 = p.reverse ? L - b : a;
+  };
+  // tile vector v of a stage -> (row, vector-in-row) and its smem slot
+  auto issue = [&](int64_t c) {
+    int64_t j0;
+    int cnt;
+    chunk(c, j0, cnt);
+    V* st = ring + (c % SCAN_NS) * NVEC;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const int v = tid + SCAN_LB * q;
+      if (!STEP_MAJOR) {
+        const int ln = v >> 4, pc = v & 15;
+        const bool ok = ln < nl && pc * VW < cnt;
+        cp16(st + ln * 16 + (pc ^ (ln & 7)), X + ib[ok ? ln : 0] + (ok ? j0 + pc * VW : 0), ok);
+      } else {
+        const int k = v / VPR, pc = v % VPR;
+        const bool ok = k < cnt;
+        cp16(st + v, X + ib[0] + pc * VW + (ok ? (j0 + k) * si : 0), ok);
+      }
+    }
+  };
+  issue(0);
+  cp_commit();
+  if (nch > 1) issue(1);
+  cp_commit();
+  double acc = 0.0;
+  for (int64_t c = 0; c < nch; ++c) {
+    int64_t j0;
+    int cnt;
+    chunk(c, j0, cnt);
+    cp_wait<1>();
+    __syncthreads();
+    V* st = ring + (c % SCAN_NS) * NVEC;
+    if (!STEP_MAJOR) {
+      V* row = st + tid * 16;
+      const int nv = cnt / VW;
+      if (p.reverse) {
+        for (int pc = nv - 1; pc >= 0; --pc) {
+          V* slot = row + (pc ^ (tid & 7));
+          T e[VW];
+          sunpack(*slot, e);
+#pragma unroll
+          for (int q = VW - 1; q >= 0; --q) {
+            const double x = (double)e[q];
+            acc = (c == 0 && pc == nv - 1 && q == VW - 1) ? x : x + g * acc;
+            e[q] = (T)acc;
+          }
+          *slot = spack(e);
+        }
+      } else {
+        for (int pc = 0; pc < nv; ++pc) {
+          V* slot = row + (pc ^ (tid & 7));
+          T e[VW];
+          sunpack(*slot, e);
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            const double x = (double)e[q];
+            acc = (c == 0 && pc == 0 && q == 0) ? x : x + g * acc;
+            e[q] = (T)acc;
+          }
+          *slot = spack(e);
+        }
+      }
+    } else {
+      T* t = reinterpret_cast<T*>(st);
+      if (p.reverse) {
+        for (int k = cnt - 1; k >= 0; --k) {
+          const double x = (double)t[k * SCAN_LB + tid];
+          acc = (c == 0 && k == cnt - 1) ? x : x + g * acc;
+          t[k * SCAN_LB + tid] = (T)acc;
+        }
+      } else {
+        for (int k = 0; k < cnt; ++k) {
+          const double x = (double)t[k * SCAN_LB + tid];
+          acc = (c == 0 && k == 0) ? x : x + g * acc;
+          t[k * SCAN_LB + tid] = (T)acc;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const int v = tid + SCAN_LB * q;
+      if (!STEP_MAJOR) {
+        const int ln = v >> 4, pc = v & 15;
+        if (ln < nl && pc * VW < cnt)
+          __stcs(reinterpret_cast<V*>(Y + ob[ln] + j0 + pc * VW), st[ln * 16 + (pc ^ (ln & 7))]);
+      } else {
+        const int k = v / VPR, pc = v % VPR;
+        if (k < cnt) __stcs(reinterpret_cast<V*>(Y + ob[0] + pc * VW + (j0 + k) * so), st[v]);
+      }
+    }
+    if (c + 2 < nch) issue(c + 2);
+    cp_commit();
+  }
+}
+
 extern "C" void* rt_kernel_scan_tile(int f64) {
   return f64 ? (void*)k_scan_tile<double> : (void*)k_scan_tile<float>;
+}
+
+// tile == 2: pipelined line-major, tile == 3: pipelined step-major
+extern "C" void* rt_kernel_scan_pipe(int f64, int step_major) {
+  if (step_major) return f64 ? (void*)k_scan_pipe<double, true> : (void*)k_scan_pipe<float, true>;
+  return f64 ? (void*)k_scan_pipe<double, false> : (void*)k_scan_pipe<float, false>;
 }
 
 extern "C" void* rt_kernel_scan(int f64, int warp) {

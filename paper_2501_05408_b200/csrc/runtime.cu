@@ -25,6 +25,7 @@ extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
 extern "C" void* rt_kernel_thin_rows(int f64, int r, int k);
 extern "C" void* rt_kernel_scan_tile(int f64);
+extern "C" void* rt_kernel_scan_pipe(int f64, int step_major);
 extern "C" void* rt_gemm_tma_pack(void* blk, void* encode);
 
 static thread_local std::string g_err;
@@ -123,7 +124,8 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       rt_scan_params* p = (rt_scan_params*)blk;
       fold_view(p->in, env, nenv);
       fold_view(p->out, env, nenv);
-      if (p->tile) return rt_kernel_scan_tile(p->f64);
+      if (p->tile == 1) return rt_kernel_scan_tile(p->f64);
+      if (p->tile >= 2) return rt_kernel_scan_pipe(p->f64, p->tile == 3);
       int warp = p->in.stride[p->sdim] == 1 && p->out.stride[p->sdim] == 1;
       return rt_kernel_scan(p->f64, warp);
     }

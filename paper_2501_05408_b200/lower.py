@@ -1227,6 +1227,8 @@ class Lowering:
         p.out = self.out_view(ctx, key)
         self._scan_launch(p, (n.id, n.name))
 
+    SCAN_STAGES = 3
+
     def _scan_launch(self, p, label):
         """Pick the scan kernel (csrc/k_scan.cu): tiled 64-line CTAs with
         16-byte I/O for contiguous lines whose starts and length are
@@ -1238,19 +1240,29 @@ class Lowering:
         vw = 2 if p.f64 else 4
         esize = 8 if p.f64 else 4
 
-        def aligned(v):
+        def aligned(v, skip=(sd,)):
             if (v.ptr + esize * v.off) % 16:
                 return False
             if any(v.off_env[e] % vw for e in range(N.RT_MAXENV)):
                 return False
             return all(v.stride[d] % vw == 0 for d in range(p.box.nd)
-                       if d != sd and p.box.ext[d] > 1)
+                       if d not in skip and p.box.ext[d] > 1)
 
         L = p.box.ext[sd]
-        if contig and same_t and L % vw == 0 and aligned(p.in_) and aligned(p.out):
-            p.tile = 1
-            grid = [int(max(1, min(-(-p.total_lines // 64), 148 * 16))), 1, 1]
-            self.add_rec(N.RT_K_SCAN, p, grid, [64, 1, 1], 0, label)
+        smem = self.SCAN_STAGES * 64 * 16 * 16 + 2 * 64 * 8
+        lines = [d for d in range(p.box.nd) if d != sd and p.box.ext[d] > 1]
+        inner = lines[-1] if lines else None
+        nblk = -(-p.total_lines // 64)
+        if contig and same_t and L % vw == 0 and aligned(p.in_) and aligned(p.out) \
+                and nblk < (1 << 31):
+            p.tile = 2
+            self.add_rec(N.RT_K_SCAN, p, [nblk, 1, 1], [64, 1, 1], smem, label)
+        elif (same_t and inner is not None and p.in_.stride[inner] == 1
+              and p.out.stride[inner] == 1 and p.box.ext[inner] % 64 == 0
+              and aligned(p.in_, (inner,)) and aligned(p.out, (inner,))
+              and nblk < (1 << 31)):
+            p.tile = 3
+            self.add_rec(N.RT_K_SCAN, p, [nblk, 1, 1], [64, 1, 1], smem, label)
         elif contig:
             self.add_rec(N.RT_K_SCAN, p, self.grid1(p.total_lines * 32), [256, 1, 1], 0, label)
         else:

@@ -191,3 +191,45 @@ def test_narrow_head_rows_gemm(N, K, dt):
     want = (x.astype(np.float64) @ W.astype(np.float64))
     tol = 1e-5 if dt == "f32" else 1e-12
     np.testing.assert_allclose(out, want, rtol=tol, atol=tol)
+
+
+def _scan_graph(layout, n_env, T, dt, forward):
+    """G = dsum over a suffix r[t:T] (reverse scan) or, forward, the
+    reversed-weight prefix dsum r[0:t+1] (reference runtime.py:108-122),
+    env-major (b,t) or time-major (t,b)."""
+    dims = [("b", "B"), ("t", "T")] if layout == "bt" else [("t", "T"), ("b", "B")]
+    g = ir.Graph([d for d, _ in dims], dict(dims), {"B": n_env, "T": T})
+    dom = tuple(d for d, _ in dims)
+    g.nodes[0] = ir.Node(0, "r", "input", dom, ((),), (dt,))
+    g.nodes[1] = ir.Node(1, "G", "discounted_sum", dom, ((),), (dt,),
+                         {"dim": 0, "gamma": 0.97, "reverse": forward}, 1)
+    tsl = ("slice", ("int", 0), ("add", S("t"), ("int", 1))) if forward else \
+        ("slice", S("t"), S("T", "bound"))
+    phi = tuple(tsl if d == "t" else S(d) for d in dom)
+    g.edges.append(ir.Edge(1, 0, phi, None, 0, 0))
+    g.outputs = [("G", 1, 0)]
+    return g
+
+
+@pytest.mark.parametrize("layout", ["bt", "tb"])
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+@pytest.mark.parametrize("forward", [False, True])
+@pytest.mark.parametrize("n_env,T", [(4096, 1000), (192, 37), (100, 64)])
+def test_scan_kernels_layouts(layout, dt, forward, n_env, T):
+    """Pipelined tiled scans (line-major / step-major) and their fallbacks
+    (ragged lengths, line counts not a multiple of 64) vs a float64 scan."""
+    npd = np.float32 if dt == "f32" else np.float64
+    shape = (n_env, T) if layout == "bt" else (T, n_env)
+    r = np.random.default_rng(T + n_env).standard_normal(shape).astype(npd)
+    out = execute(_scan_graph(layout, n_env, T, dt, forward), inputs={"r": r})["G"]
+    x = (r if layout == "bt" else r.T).astype(np.float64)
+    want = np.zeros_like(x)
+    acc = np.zeros(x.shape[0])
+    order = range(T) if forward else reversed(range(T))
+    for i, t in enumerate(order):
+        acc = x[:, t] + (0.97 * acc if i else 0.0)
+        want[:, t] = acc
+    if layout == "tb":
+        want = want.T
+    tol = 1e-5 if dt == "f32" else 1e-12
+    np.testing.assert_allclose(out, want, rtol=tol, atol=tol * 10)
