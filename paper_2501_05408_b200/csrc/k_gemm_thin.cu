@@ -18,6 +18,20 @@ namespace {
 constexpr int THREADS = 256;
 constexpr int KT = 64;
 
+// offset of flat row index `flat` over box b (nd <= 1: flat * s[0])
+RT_DEV int64_t wdec(const rt_gbox& b, int64_t flat, const int64_t* s) {
+  if (b.nd <= 1) return flat * s[0];
+  int64_t o = 0;
+  for (int d = b.nd - 1; d >= 0; --d) {
+    const int64_t e = b.ext[d];
+    const int64_t q = flat / e;
+    o += (flat - q * e) * s[d];
+    flat = q;
+  }
+  return o;
+}
+
+
 template <typename T, int R>
 __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant__ rt_thin_params p) {
   __shared__ __align__(16) T ys[KT][R];
@@ -88,7 +102,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
   for (int r = threadIdx.x; r < R; r += THREADS)
     bs[r] = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + r * p.bias.s2[0])
                        : (T)0;
-  const int64_t xw = p.X.s2[0], xk = p.X.s1[0], cw = p.C.s1[0], cr = p.C.s2[0];
+  const int64_t xk = p.X.s1[0], cr = p.C.s2[0];
   const int64_t ntiles = (p.w + RT - 1) / RT;
   const bool acc_in = p.accumulate != 0, tanh_epi = p.epilogue == 1;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -97,7 +111,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
     __syncthreads();
     for (int i = threadIdx.x; i < RT * KP; i += THREADS) {
       const int rr = i / KP, k = i - rr * KP;
-      xs[i] = (rr < nrow && k < K) ? __ldcs(X + (w0 + rr) * xw + k * xk) : (T)0;
+      xs[i] = (rr < nrow && k < K) ? __ldcs(X + wdec(p.W, w0 + rr, p.X.s2) + k * xk) : (T)0;
     }
     __syncthreads();
     for (int r = threadIdx.x; r < R; r += THREADS) {
@@ -105,13 +119,13 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
 #pragma unroll
       for (int k = 0; k < KP; ++k) yreg[k] = ys[k * R + r];
       const T b = bs[r];
-      T* cbase = Cp + w0 * cw + r * cr;
+      T* cbase = Cp + r * cr;
 #pragma unroll 4
       for (int rr = 0; rr < nrow; ++rr) {
         T a = (T)0;
 #pragma unroll
         for (int k = 0; k < KP; ++k) a = fma(xs[rr * KP + k], yreg[k], a);
-        T* cptr = cbase + rr * cw;
+        T* cptr = cbase + wdec(p.W, w0 + rr, p.C.s1);
         if (acc_in) a += *cptr;
         a += b;
         if (tanh_epi) a = vm_tanh<T>(a);
@@ -137,18 +151,6 @@ template <> RT_DEV void unpack<float>(const float4& v, float* o) { o[0] = v.x; o
 template <> RT_DEV void unpack<double>(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
 RT_DEV void unpack_zero(float4& v) { v = make_float4(0.f, 0.f, 0.f, 0.f); }
 RT_DEV void unpack_zero(double2& v) { v = make_double2(0.0, 0.0); }
-
-RT_DEV int64_t wdec(const rt_gbox& b, int64_t flat, const int64_t* s) {
-  if (b.nd <= 1) return flat * s[0];
-  int64_t o = 0;
-  for (int d = b.nd - 1; d >= 0; --d) {
-    const int64_t e = b.ext[d];
-    const int64_t q = flat / e;
-    o += (flat - q * e) * s[d];
-    flat = q;
-  }
-  return o;
-}
 
 template <typename T, int R, int KI>
 __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ rt_thin_params p) {

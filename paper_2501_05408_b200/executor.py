@@ -338,10 +338,11 @@ def _single_identity_consumer(g, nid, out_ids):
     return e
 
 
-def find_gemm_epilogues(g: Graph, pshape, fixed_of, skip):
+def find_gemm_epilogues(g: Graph, pshape, fixed_of, skip, ext=None):
     """matmul -> (+ bias) [-> tanh] with single pointwise consumers: one GEMM
     whose epilogue adds the bias and applies tanh (the MLP layers)."""
     out_ids = {nid for _, nid, _ in g.outputs}
+    ext = ext or {}
     res = {}
     for x in g.sorted_nodes():
         if x.kind != "matmul" or x.id in skip:
@@ -363,8 +364,8 @@ def find_gemm_epilogues(g: Graph, pshape, fixed_of, skip):
             continue
         if bshape not in ((1, nn), (nn,)) or bsrc.out_dtypes[be.oid] != x.dtype:
             continue
-        if not set(bsrc.domain) <= set(fixed_of.get(y.id, ())):
-            continue
+        if any(d not in fixed_of.get(y.id, ()) and ext.get(d, 0) != 1 for d in bsrc.domain):
+            continue      # the bias varies across the GEMM rows
         final, tanh = y, False
         e2 = _single_identity_consumer(g, y.id, out_ids)
         if e2 is not None:
@@ -482,7 +483,7 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
     alias_nodes = {k[0] for k in alias}
     absorbed = find_absorbed_layouts(g, virtual | alias_nodes) if fuse else set()
     virtual |= absorbed
-    gemm_epi = find_gemm_epilogues(g, pshape, fixed_of, virtual | alias_nodes) if fuse else {}
+    gemm_epi = find_gemm_epilogues(g, pshape, fixed_of, virtual | alias_nodes, ext) if fuse else {}
     taken = set(virtual) | alias_nodes | set(gemm_epi)
     for f, (x, _b, t) in gemm_epi.items():
         taken.add(x)

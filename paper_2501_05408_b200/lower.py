@@ -554,8 +554,11 @@ class Lowering:
                 ops.append([kernel, p, 1, 0, None])
             else:
                 raise LowerError("op family not supported inside a persistent loop")
-        R = max(1, -(-rows // 148))
-        R = max(1, min(R, 16 // max_m))
+        # rows per CTA: the specialised in-loop GEMMs hold <= 8 rows (jit.py
+        # _gemm_call); spread rows evenly over the waves that needs
+        rmax = max(1, 8 // max_m)
+        waves = -(-rows // (148 * rmax))
+        R = max(1, min(rmax, -(-rows // (148 * waves))))
         a_need, tma = 0, False
         for kernel, p, re, f64, _ in ops:
             if kernel == N.RT_K_GEMM:
@@ -1323,7 +1326,8 @@ class Lowering:
         bias = None
         if bias_edge is not None:
             bv = self.edge_val(ctx, bias_edge)
-            if any(d in ctx.slab for d in bv.coef) or bv.checks or bv.progs or _ragged(bv):
+            if any(d in ctx.slab and self.ext[d] != 1 for d in bv.coef) or bv.checks \
+                    or bv.progs or _ragged(bv):
                 raise LowerError(f"{n.name}: bias varies across the GEMM rows")
             bias = N.rt_gop()
             bias.ptr = bv.buf.ptr
@@ -1497,8 +1501,12 @@ class Lowering:
         if nc is not None and kc is not None and self._gemm_rows(p, M, nc, kc, f64, label,
                                                                  accumulate, epilogue, bias):
             return True
-        if mc is None or nc is None or kc is None:
+        if nc is None or kc is None:
             return False
+        if mc is None:
+            # rows that do not collapse (e.g. gathered minibatch rows): only
+            # the small-K variant walks a multi-dim row box
+            return self._gemm_smallk(p, M, nc, kc, f64, label, accumulate, epilogue, bias)
         (m, (a_m, c_m)), (n, (b_n, c_n)), (k, (a_k, b_k)) = mc, nc, kc
         q = N.rt_thin_params()
         q.f64 = int(f64)
@@ -1538,21 +1546,51 @@ class Lowering:
                 r.bias = bias
             self.add_rec(N.RT_K_SPLITK, r, self.grid1(p.m * p.n), [256, 1, 1], 0, label)
             return True
+        return self._gemm_smallk(p, M, nc, kc, f64, label, accumulate, epilogue, bias)
+
+    def _gemm_smallk(self, p, M, nc, kc, f64, label, accumulate, epilogue, bias):
+        """K <= 32 products over many rows (the observation layer, dX of a
+        narrow head) -> RT_K_THIN variant 2; rows may be a multi-dim box
+        (gathered minibatch rows)."""
+        (n, (b_n, c_n)), (k, (a_k, b_k)) = nc, kc
+        m = prod(t[0] for t in M)
+        esize = 8 if f64 else 4
         kp = 4 if k <= 4 else 8 if k <= 8 else 16 if k <= 16 else 32
         smem = (kp * n + 64 * kp + n) * esize
-        if k <= 32 and m >= 4096 and c_n == 1 and smem <= 48 * 1024 and \
-                (bias is None or len(Nn) == 1):
-            q.variant = 2
-            q.w, q.r, q.k = m, n, k
-            q.X, q.Y = gop(p.A, a_k, a_m), gop(p.B, b_k, b_n)
-            q.C = gop(p.C, c_m, c_n)
-            if bias is not None:
-                q.bias = gop(bias, 0, bias.s2[0])
-            q.accumulate, q.epilogue = accumulate, epilogue
-            grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
-            self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
-            return True
-        return False
+        mdims = [t for t in M if t[0] != 1] or [(1, 0, 0, 0)]
+        if not (k <= 32 and m >= 4096 and c_n == 1 and smem <= 48 * 1024 and len(mdims) <= 4):
+            return False
+        if bias is not None and p.N.nd > 1:
+            return False
+        q = N.rt_thin_params()
+        q.f64 = int(f64)
+        q.variant = 2
+        q.w, q.r, q.k = m, n, k
+        q.W.nd = len(mdims)
+        for i, t in enumerate(mdims):
+            q.W.ext[i] = t[0]
+
+        def gop(src, s1, s2):
+            g = N.rt_gop()
+            C.memmove(C.addressof(g), C.addressof(src), C.sizeof(g))
+            for arr in (g.sz, g.s1, g.s2):
+                for i in range(4):
+                    arr[i] = 0
+            for i, v in enumerate(s1):
+                g.s1[i] = v
+            for i, v in enumerate(s2):
+                g.s2[i] = v
+            return g
+
+        q.X = gop(p.A, [a_k], [t[1] for t in mdims])
+        q.Y = gop(p.B, [b_k], [b_n])
+        q.C = gop(p.C, [t[3] for t in mdims], [c_n])
+        if bias is not None:
+            q.bias = gop(bias, [0], [bias.s2[0]])
+        q.accumulate, q.epilogue = accumulate, epilogue
+        grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
+        self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
+        return True
 
     ROWS_MAX_R = 4
 

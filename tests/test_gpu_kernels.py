@@ -233,3 +233,28 @@ def test_scan_kernels_layouts(layout, dt, forward, n_env, T):
         want = want.T
     tol = 1e-5 if dt == "f32" else 1e-12
     np.testing.assert_allclose(out, want, rtol=tol, atol=tol * 10)
+
+
+@pytest.mark.parametrize("K,N,dt", [(16, 256, "f32"), (16, 64, "f64"), (7, 33, "f32")])
+def test_gathered_rows_small_k_gemm(K, N, dt):
+    """y[j,u,t] = x[u*M + j, t] @ W: minibatch rows gathered by a symbolic
+    index (a multi-dim row box, thin variant 2 with K <= 32)."""
+    Mb, U, T = 4, 256, 24
+    B = Mb * U
+    npd = np.float32 if dt == "f32" else np.float64
+    g = ir.Graph(["j", "u", "b", "t"], {"j": "M", "u": "U", "b": "B", "t": "T"},
+                 {"M": Mb, "U": U, "B": B, "T": T})
+    g.nodes[0] = ir.Node(0, "x", "input", ("b", "t"), ((1, K),), (dt,))
+    g.nodes[1] = ir.Node(1, "W", "input", (), ((K, N),), (dt,))
+    g.nodes[2] = ir.Node(2, "y", "matmul", ("j", "u", "t"), ((1, N),), (dt,), {}, 2)
+    bidx = ("add", ("mul", S("u"), S("M", "bound")), S("j"))
+    g.edges += [ir.Edge(2, 0, (bidx, S("t")), None, 0, 0), ir.Edge(2, 1, (), None, 0, 1)]
+    g.outputs = [("y", 2, 0)]
+    rng = np.random.default_rng(K * N)
+    x = rng.standard_normal((B, T, 1, K)).astype(npd)
+    W = rng.standard_normal((K, N)).astype(npd)
+    out = execute(g, inputs={"x": x, "W": W})["y"]
+    xs = x.reshape(U, Mb, T, 1, K).transpose(1, 0, 2, 3, 4).astype(np.float64)
+    want = xs @ W.astype(np.float64)
+    tol = 1e-5 if dt == "f32" else 1e-12
+    np.testing.assert_allclose(out, want, rtol=tol, atol=tol)

@@ -11,13 +11,15 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 from golden_cases import load_graph  # noqa: E402
 from paper_2501_05408_b200 import get_executable, native as N, roofline as RF  # noqa: E402
-from paper_2501_05408_b200.workloads import mlp_inputs  # noqa: E402
 
-B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
-T = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
-g = load_graph("reinforce_mlp_c2")
-inp = {k: torch.from_numpy(v).cuda() for k, v in mlp_inputs().items()}
-exe, _ = get_executable(g, {"I": 1, "B": B, "T": T}, inp, seed=0)
+import bench  # noqa: E402
+
+WL = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+bench.WL = WL
+B = int(sys.argv[2]) if len(sys.argv) > 2 else WL.local_envs(1)
+g = load_graph(WL.graph)
+inp = {k: torch.from_numpy(v).cuda() for k, v in WL.inputs().items()}
+exe, _ = get_executable(g, WL.bounds(B), inp, seed=0)
 for ri, info in exe.loop_info.items():
     lp = exe.recs[ri]
     params = exe._params[ri]
