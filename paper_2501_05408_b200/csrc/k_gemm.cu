@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(256) k_gemm(const __grid_constant__ rt_gemm_pa
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
   const int64_t zs = blockIdx.z;
   const int64_t zi = zs / p.splits;
   const int split = (int)(zs - zi * p.splits);

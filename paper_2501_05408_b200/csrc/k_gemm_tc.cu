@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.y * TC_BM;
-  const int64_t n0 = (int64_t)blockIdx.x * 256;
+  const int64_t m0 = (int64_t)blockIdx.x * TC_BM;
+  const int64_t n0 = (int64_t)blockIdx.y * 256;
   const int64_t nrem = p.n - n0;
   const int BN = nrem >= 256 ? 256 : (int)((nrem + 15) / 16 * 16);   // MMA N: multiple of 16
   const int64_t zs = blockIdx.z;

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
   T* ys = (T*)sm_raw;             // [KP][R]
   T* xs = ys + KP * R;            // [RT][KP]
   T* bs = xs + RT * KP;           // [R]
+  __shared__ int64_t coff[RT];    // output row offsets of the tile
   const T* X = (const T*)p.X.ptr + p.X.off;
   const T* Y = (const T*)p.Y.ptr + p.Y.off;
   T* Cp = (T*)p.C.ptr + p.C.off;
@@ -109,9 +110,13 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
     const int64_t w0 = tile * RT;
     const int nrow = (int)(p.w - w0 < RT ? p.w - w0 : RT);
     __syncthreads();
-    for (int i = threadIdx.x; i < RT * KP; i += THREADS) {
-      const int rr = i / KP, k = i - rr * KP;
-      xs[i] = (rr < nrow && k < K) ? __ldcs(X + wdec(p.W, w0 + rr, p.X.s2) + k * xk) : (T)0;
+    if (threadIdx.x < RT) {
+      const int rr = threadIdx.x;
+      const int64_t w = w0 + (rr < nrow ? rr : 0);
+      coff[rr] = wdec(p.W, w, p.C.s1);
+      const T* xr = X + wdec(p.W, w, p.X.s2);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) xs[rr * KP + k] = (rr < nrow && k < K) ? __ldcs(xr + k * xk) : (T)0;
     }
     __syncthreads();
     for (int r = threadIdx.x; r < R; r += THREADS) {
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
         T a = (T)0;
 #pragma unroll
         for (int k = 0; k < KP; ++k) a = fma(xs[rr * KP + k], yreg[k], a);
-        T* cptr = cbase + wdec(p.W, w0 + rr, p.C.s1);
+        T* cptr = cbase + coff[rr];
         if (acc_in) a += *cptr;
         a += b;
         if (tanh_epi) a = vm_tanh<T>(a);

@@ -117,8 +117,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma(const __grid_constan
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = su32(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.y * TM_BM;
-  const int64_t n0 = (int64_t)blockIdx.x * TM_BN;
+  const int64_t m0 = (int64_t)blockIdx.x * TM_BM;
+  const int64_t n0 = (int64_t)blockIdx.y * TM_BN;
   const int64_t nrem = p.n - n0;
   const int split = blockIdx.z;
   // MMA N: multiple of 16 (K-major B) / of 32 (MN-major B, whole 32-wide atoms)

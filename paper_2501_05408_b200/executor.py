@@ -574,6 +574,15 @@ def find_folds(g: Graph, bufs, fixed_of, virtual, ext):
     return folds
 
 
+def fold_slots(bufs, slot_of):
+    """root buffer key -> env slots of the loop dims it is folded along."""
+    out = {}
+    for k, b in bufs.items():
+        if b.alias is None and b.folded:
+            out[k] = {slot_of[d] for d in b.folded}
+    return out
+
+
 def payload_shapes(g: Graph, benv):
     pshape = {}
     for n in g.sorted_nodes():
@@ -643,7 +652,8 @@ class Executable:
             for op in low.loop_subs.get(ri, {}).get("ops", ()):
                 ptrs |= memplan.touched_ptrs(op[1])
             rec_ptrs.append({(q >> 44) << 44 for q in ptrs if q >> 44})
-        life = memplan.lifetimes(low.prog, rec_ptrs, key_of, pinned)
+        life = memplan.lifetimes(low.prog, rec_ptrs, key_of, pinned,
+                                 fold_slots(self.bufs, low.slot))
         for k in roots:
             life.setdefault(k, (-1, -1))   # never touched: still allocated, tiny lifetime
         sizes = {k: max(1, self.bufs[k].nbytes) for k in roots}

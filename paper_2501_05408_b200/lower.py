@@ -1432,13 +1432,13 @@ class Lowering:
         splits = 1
         if tiles < 148 and p.k >= 1024:
             splits = int(min(128, max(1, (148 * 4) // max(1, tiles)), max(1, p.k // 512)))
-        if p.z * splits > 65535 or (p.m + 63) // 64 > 65535:
+        if p.z * splits > 65535 or (p.n + 63) // 64 > 65535:
             raise LowerError("gemm grid too large")
         if splits > 1:
             p.splits = splits
             esize = 8 if p.f64 else 4
             p.part = self.alloc(splits * p.z * p.m * p.n * esize)
-            grid = [(p.n + 63) // 64, (p.m + 63) // 64, p.z * splits]
+            grid = [(p.m + 63) // 64, (p.n + 63) // 64, p.z * splits]
             self.add_rec(N.RT_K_GEMM, p, grid, [256, 1, 1], 0, label)
             q = N.rt_splitk_params()
             q.Z, q.M, q.N = p.Z, p.M, p.N
@@ -1453,7 +1453,7 @@ class Lowering:
                 q.bias = bias
             self.add_rec(N.RT_K_SPLITK, q, self.grid1(p.z * p.m * p.n), [256, 1, 1], 0, label)
         else:
-            grid = [(p.n + 63) // 64, (p.m + 63) // 64, p.z]
+            grid = [(p.m + 63) // 64, (p.n + 63) // 64, p.z]
             self.add_rec(N.RT_K_GEMM, p, grid, [256, 1, 1], 0, label)
 
     @staticmethod
@@ -1678,12 +1678,13 @@ class Lowering:
         splits = 1
         if tiles < 148 and p.k >= 4096:
             splits = int(max(1, min(148 * 2 // max(1, tiles), p.k // 2048)))
-        if p.z * splits > 65535 or (p.m + 127) // 128 > 65535:
+        if p.z * splits > 65535 or (p.n + 255) // 256 > 65535:
             raise LowerError("gemm grid too large")
         p.splits = splits
         if splits > 1:
             p.part = self.alloc(splits * p.z * p.m * p.n * 4)
-        grid = [(p.n + 255) // 256, (p.m + 127) // 128, p.z * splits]
+        # M tiles on grid.x (up to 2^31 - 1: E*T rows), N tiles on grid.y
+        grid = [(p.m + 127) // 128, (p.n + 255) // 256, p.z * splits]
         if self.use_tma and self._tma_ok(p):
             self.add_rec(N.RT_K_GEMM_TMA, p, grid, [320, 1, 1], N.TMA_SMEM, label)
         else:

@@ -45,19 +45,22 @@ def touched_ptrs(params) -> set:
 
 
 def loop_spans(prog):
-    """[(for_pc, end_pc, trips)] for every loop of a lowered program."""
+    """[(for_pc, end_pc, trips, env slot)] for every loop of a lowered program."""
     spans, stack = [], []
     for pc, ins in enumerate(prog):
         if ins[0] == N.RT_OP_FOR:
-            stack.append((pc, abs(ins[3] - ins[2])))
+            stack.append((pc, abs(ins[3] - ins[2]), ins[1]))
         elif ins[0] == N.RT_OP_END:
-            a, trips = stack.pop()
-            spans.append((a, pc, trips))
+            a, trips, slot = stack.pop()
+            spans.append((a, pc, trips, slot))
     return spans
 
 
-def lifetimes(prog, rec_ptrs, key_of_ptr, pinned):
-    """key -> (first pc, last pc)."""
+def lifetimes(prog, rec_ptrs, key_of_ptr, pinned, folds=None):
+    """key -> (first pc, last pc).  A buffer folded along a loop's dim
+    (executor.find_folds: produced and consumed within one iteration) is
+    not kept live across that loop's iterations."""
+    folds = folds or {}
     spans = [s for s in loop_spans(prog) if s[2] > 1]
     touch = {}
     for pc, ins in enumerate(prog):
@@ -73,7 +76,10 @@ def lifetimes(prog, rec_ptrs, key_of_ptr, pinned):
     out = {}
     for k, (lo, hi) in touch.items():
         # outermost multi-trip loop containing any touch
-        for a, b, _ in spans:
+        fs = folds.get(k, ())
+        for a, b, _, slot in spans:
+            if slot in fs:
+                continue
             if a <= lo <= b or a <= hi <= b:
                 lo, hi = min(lo, a), max(hi, b)
         out[k] = (lo, hi)
