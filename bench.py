@@ -39,8 +39,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 class Workload:
     def __init__(self, name, graph, T, env_total=None, env_per_gpu=None, minibatches=None,
-                 ppo=False, desc=""):
-        self.name, self.graph, self.T = name, graph, T
+                 ppo=False, desc="", block=None):
+        self.name, self.graph, self.T, self.block = name, graph, T, block
         self.env_total, self.env_per_gpu = env_total, env_per_gpu
         self.minibatches, self.ppo, self.desc = minibatches, ppo, desc
 
@@ -79,6 +79,10 @@ WORKLOADS = {
     "c3": Workload("ppo_gae_c3", "ppo_c3", 512, env_per_gpu=4096, minibatches=4, ppo=True,
                    desc="PPO+GAE(0.95), E=4096 x T=512, 4 epochs x 4 minibatches, "
                         "shared MLP 16-256-256-(4|1)"),
+    "c4": Workload("reinforce_mlp_c4", "reinforce_mlp_c2", 100000, env_per_gpu=256,
+                   block=("t", 10000),
+                   desc="long-horizon REINFORCE, E=256/GPU x T=100k, MLP 16-256-256-4, "
+                        "backward time-blocked by 10k steps (blocking.block_dim)"),
     "c5": Workload("ppo_gae_c5", "ppo_c3", 512, env_total=32768, minibatches=4, ppo=True,
                    desc="PPO+GAE(0.95), E=32768 total split over GPUs x T=512, "
                         "4 epochs x 4 minibatches"),
@@ -257,7 +261,7 @@ def main():
     shard = None
     if world > 1:
         shard = WL.shard(rank, world)     # envs [rank*B, (rank+1)*B) of B*world
-    exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard)
+    exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard, block=WL.block)
 
     def step_dev(inp, graph=None):
         if graph is None:
@@ -351,14 +355,14 @@ def main():
     # e2e through the public API with host buffers
     hin = host
     for w in range(max(1, args.warmup)):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block)
         hin = next_inputs(outs, params)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for s in range(args.steps):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block)
         hin = next_inputs(outs, params)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     h2d = sum(v.nbytes for v in host.values())
@@ -375,6 +379,7 @@ def main():
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": WL.name, "desc": WL.desc, "E_per_gpu": B,
                        "E_total": B * world, "T": T_STEPS, "bounds": bounds,
+                       "time_block": WL.block,
                        "hidden": [256, 256], "obs": 16, "act": 4, "iters_per_step": 1,
                        "l2": "activations (GBs) exceed L2 every step",
                        "parallelism": f"env-shard x{world}"},

@@ -478,7 +478,7 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
     contract = find_contractions(g)
     virtual = set(contract.values())
     alias = find_aliases(g, pshape)
-    plan = Planner(g, benv).plan()
+    plan = Planner(g, benv).plan(getattr(g, "block_dims", ()))
     fixed_of = plan_fixed(plan.steps)
     alias_nodes = {k[0] for k in alias}
     absorbed = find_absorbed_layouts(g, virtual | alias_nodes) if fuse else set()
@@ -1125,11 +1125,13 @@ def _input_sig(inputs):
     for k in sorted(inputs or {}):
         v = inputs[k]
         shp = tuple(getattr(v, "shape", np.shape(v)))
-        sig.append((k, shp, str(getattr(v, "dtype", type(v).__name__))))
+        # torch.float32 and numpy float32 inputs share one executable
+        sig.append((k, shp, str(getattr(v, "dtype", type(v).__name__)).replace("torch.", "")))
     return tuple(sig)
 
 
-def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None, comm=None):
+def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None, comm=None,
+                   block=None):
     global _TORCH_DT
     torch = _torch()
     if _TORCH_DT is None:
@@ -1140,12 +1142,17 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
     if dyn:
         benv = _resolve_dynamic(graph, benv, dyn, inputs, seed, device)
     dev = torch.cuda.current_device() if device is None else int(device)
-    key = (id(g), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs), shard)
+    block = tuple(block) if block else None
+    key = (id(g), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs), shard, block)
     ex = _CACHE.get(key)
     if ex is not None and ex[0]() is g:
         return ex[1], benv
     h = copy_graph(graph)
     prepare(h, benv)
+    outer_benv = benv
+    if block:
+        from .blocking import block_dim
+        benv = block_dim(h, benv, block[0], int(block[1]))
     if shard is not None and comm is None:
         from .shard import TorchComm
         comm = TorchComm()
@@ -1154,7 +1161,7 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         _CACHE[key] = (weakref.ref(g), exe)
     except TypeError:
         pass
-    return exe, benv
+    return exe, outer_benv
 
 
 def _resolve_dynamic(g: Graph, benv, dyn, inputs, seed, device):
@@ -1201,14 +1208,14 @@ def _resolve_dynamic(g: Graph, benv, dyn, inputs, seed, device):
 
 
 def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=None,
-            device_outputs=False, stream=None, shard=None, comm=None):
+            device_outputs=False, stream=None, shard=None, comm=None, block=None):
     """Drop-in for reference `reference_execute` (runtime.py:460-475).
 
     shard=ShardSpec(dim, rank, world): this process runs envs
     [rank*B, (rank+1)*B) of a G-way env-sharded run (bounds give the local
     extent B); reductions over the dim are all-reduced through `comm`
     (default: torch.distributed)."""
-    exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm)
+    exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm, block)
     exe.run(inputs or {}, stream)
     exe.check_status(stream)
     outs = exe.outputs(device_outputs)

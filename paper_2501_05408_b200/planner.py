@@ -264,10 +264,13 @@ class Planner:
 
     # -- recursive decomposition -----------------------------------------------
 
-    def plan(self):
+    def plan(self, block_dims=()):
         nodes = set(self.g.nodes)
         edges = list(self.g.edges)
-        return Plan(self.g, self.benv, self.ext, self.level(nodes, edges, ()))
+        steps = self.level(nodes, edges, ())
+        for kb in block_dims:
+            steps = group_block_loop(steps, self.g, kb)
+        return Plan(self.g, self.benv, self.ext, steps)
 
     def level(self, nodes: set, edges: list, fixed: tuple):
         succ = {}
@@ -387,6 +390,55 @@ class Planner:
                                 self.ext[d]))
             return out
         return None
+
+
+def _step_nodes(st):
+    if isinstance(st, Bulk):
+        return {st.nid}
+    out = set()
+    for b in st.body:
+        out |= _step_nodes(b)
+    return out
+
+
+def group_block_loop(steps, g: Graph, kb: str):
+    """Put the top-level bulk steps over block dim kb (blocking.block_dim)
+    into one loop over kb, so each block's chain runs start to finish and
+    its intermediates fold to one block of storage.  Steps the block nodes
+    depend on go before the loop, steps depending on them after; unchanged
+    if some step sits on a path between two block steps."""
+    blk = [st for st in steps if isinstance(st, Bulk) and kb in g.nodes[st.nid].domain]
+    if not blk:
+        return steps
+    bset = {st.nid for st in blk}
+    succ = {}
+    for e in g.edges:
+        succ.setdefault(e.src, set()).add(e.sink)
+
+    def reach(starts):
+        seen, work = set(), list(starts)
+        while work:
+            v = work.pop()
+            for w in succ.get(v, ()):
+                if w not in seen:
+                    seen.add(w)
+                    work.append(w)
+        return seen
+
+    desc = reach(bset)
+    before, after = [], []
+    for st in steps:
+        if isinstance(st, Bulk) and st.nid in bset:
+            continue
+        nodes = _step_nodes(st)
+        if nodes & desc:
+            if reach(nodes) & bset:
+                return steps      # a step between two block steps: keep flat
+            after.append(st)
+        else:
+            before.append(st)
+    body = [Bulk(st.nid, tuple(st.fixed) + (kb,)) for st in blk]
+    return before + [Loop(kb, 1, body, ())] + after
 
 
 def describe(steps, g: Graph, indent=0) -> str:

@@ -104,3 +104,16 @@ def test_jit_loop_kernel_matches_interpreter(monkeypatch):
     got = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=1)
     for k in ref:
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
+
+
+@pytest.mark.parametrize("name", ["mlp_f32_I1B4T6", "mlp_f64_I1B4T6"])
+@pytest.mark.parametrize("bs", [2, 3])
+def test_time_blocked_backward_matches_reference(name, bs):
+    """Long-horizon mode (blocking.block_dim): the backward chain runs per
+    block of bs steps with block-sized intermediates; sums over t become
+    per-block partials + totals (incrementalize over the time dim)."""
+    from paper_2501_05408_b200 import execute
+    c = load_case(name)
+    got = execute(c.graph(), bounds=c.bounds, inputs=c.inputs, seed=c.seed, block=("t", bs))
+    for k, want in c.outputs.items():
+        assert_close(got[k], want, k)

@@ -209,3 +209,22 @@ def test_ppo_heads_use_row_stream_gemm():
         if lab[1] in ("mu_n", "V_n", "V"):
             fam.setdefault(lab[1], set()).add((k, getattr(p, "variant", None)))
     assert fam["mu_n"] == {(N.RT_K_THIN, 3)} and fam["V_n"] == {(N.RT_K_THIN, 3)}
+
+
+def test_time_blocking_shrinks_long_horizon_plan():
+    """C4 (E=256, T=100k): blocking t by 10k puts the backward chain in a
+    loop over blocks with block-sized storage: the static peak drops from
+    ~159 GB (over one B200's HBM with the env noise) to ~68 GB."""
+    from paper_2501_05408_b200 import blocking
+    g = load_graph("reinforce_mlp_c2")
+    benv = {"I": 1, "B": 256, "T": 100000}
+    h = X.copy_graph(g)
+    X.prepare(h, benv)
+    b2 = blocking.block_dim(h, benv, "t", 10000)
+    an = X.analyze(h, b2, X.payload_shapes(h, b2))
+    txt = P.describe(an["plan"].steps, h)
+    assert "for t_blk asc:" in txt
+    folded = [k for k, b in an["bufs"].items() if "t_blk" in b.folded]
+    assert len(folded) >= 20
+    assert an["bufs"][[k for k in an["bufs"] if h.nodes[k[0]].name == "v126"][0]].nbytes \
+        == 256 * 10000 * 256 * 4
