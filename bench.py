@@ -39,8 +39,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 class Workload:
     def __init__(self, name, graph, T, env_total=None, env_per_gpu=None, minibatches=None,
-                 ppo=False, desc="", block=None):
-        self.name, self.graph, self.T, self.block = name, graph, T, block
+                 ppo=False, desc="", block=None, swap=False):
+        self.name, self.graph, self.T, self.block, self.swap = name, graph, T, block, swap
         self.env_total, self.env_per_gpu = env_total, env_per_gpu
         self.minibatches, self.ppo, self.desc = minibatches, ppo, desc
 
@@ -80,9 +80,13 @@ WORKLOADS = {
                    desc="PPO+GAE(0.95), E=4096 x T=512, 4 epochs x 4 minibatches, "
                         "shared MLP 16-256-256-(4|1)"),
     "c4": Workload("reinforce_mlp_c4", "reinforce_mlp_c2", 100000, env_per_gpu=256,
-                   block=("t", 10000),
+                   block=("t", 10000), swap=True,
                    desc="long-horizon REINFORCE, E=256/GPU x T=100k, MLP 16-256-256-4, "
-                        "backward time-blocked by 10k steps (blocking.block_dim)"),
+                        "backward time-blocked by 10k steps (blocking.block_dim), acting "
+                        "activations swapped to pinned host per block (swap.py)"),
+    "c4_noswap": Workload("reinforce_mlp_c4_noswap", "reinforce_mlp_c2", 100000,
+                          env_per_gpu=256, block=("t", 10000),
+                          desc="C4 time-blocked, activations resident in HBM (no swap)"),
     "c5": Workload("ppo_gae_c5", "ppo_c3", 512, env_total=32768, minibatches=4, ppo=True,
                    desc="PPO+GAE(0.95), E=32768 total split over GPUs x T=512, "
                         "4 epochs x 4 minibatches"),
@@ -261,7 +265,8 @@ def main():
     shard = None
     if world > 1:
         shard = WL.shard(rank, world)     # envs [rank*B, (rank+1)*B) of B*world
-    exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard, block=WL.block)
+    exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard, block=WL.block,
+                            swap=WL.swap)
 
     def step_dev(inp, graph=None):
         if graph is None:
@@ -355,14 +360,16 @@ def main():
     # e2e through the public API with host buffers
     hin = host
     for w in range(max(1, args.warmup)):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block,
+                       swap=WL.swap)
         hin = next_inputs(outs, params)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for s in range(args.steps):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block,
+                       swap=WL.swap)
         hin = next_inputs(outs, params)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     h2d = sum(v.nbytes for v in host.values())
@@ -388,6 +395,12 @@ def main():
             "gpu_launches": exe.launch_count * args.steps,
             "peak_hbm_bytes": exe.peak_bytes,
             "peak_hbm_allocated_bytes": int(torch.cuda.max_memory_allocated()),
+            "swap": None if exe.swap_rt is None else {
+                "managed": [exe.g.nodes[k[0]].name for k in exe.swap_plan.keys],
+                "pinned_host_bytes": exe.swap_rt.host_bytes,
+                "offload_bytes_per_step": exe.swap_rt.host_bytes,
+                "fetch_bytes_per_step": exe.swap_rt.host_bytes,
+                "time_block": exe.swap_plan.bs},
             "naive_hbm_bytes": exe.naive_bytes,
             "roofline": roof,
             "breakdown": {"family_ms_per_step": {k: round(v, 3) for k, v in fam_ms.items()},

@@ -314,6 +314,9 @@ typedef struct {
   int32_t a_off;        /* byte offset of the GEMM A-row staging area */
   uint64_t ops;         /* device pointer to rt_loop_op[nops] */
   uint64_t prof;        /* optional int64[nops]: CTA 0's clock64 cycles per op */
+  int32_t blk_slot;     /* blk_len > 0: run [env[blk_slot]*blk_len, +blk_len) */
+  int32_t _pad;         /*   (one time block of a long horizon per launch)    */
+  int64_t blk_len;
 } rt_loop_params;
 
 /* Launch record: one kernel family + its parameter block. */
@@ -337,8 +340,10 @@ enum rt_op {
   RT_OP_END = 3,       /* a = pc of matching FOR                           */
   RT_OP_EVENT = 4,     /* a = event slot: record on the stream             */
   RT_OP_COPY = 5,      /* device copy: a = rec idx of an rt_copy record    */
-  RT_OP_HOOK = 6       /* host hook a (e.g. an NCCL all-reduce of a slab):  */
-                       /* rt_run_segment returns RT_HOOK with the next pc   */
+  RT_OP_HOOK = 6,      /* host hook a (e.g. an NCCL all-reduce of a slab,   */
+                       /* a swap copy): rt_run_segment returns RT_HOOK      */
+                       /* with the next pc                                  */
+  RT_OP_ENVMOD = 7     /* env[a] = env[b] mod c (ring slot of a time block) */
 };
 
 #define RT_HOOK 100
@@ -395,6 +400,13 @@ int rt_status_clear(uint64_t dev_ptr, uint64_t stream);
 int rt_status_free(uint64_t dev_ptr);
 /* Pinned-host tier moves (offload / fetch) on a side stream with an event. */
 int rt_memcpy_d2h_async(void* host_pinned, uint64_t dev, uint64_t bytes, uint64_t stream);
+/* Strided tier moves (offload / fetch of one time block of a swap-managed
+ * buffer: `height` rows of `width` bytes; polysched.py:936-1105 offload/fetch
+ * realised as cudaMemcpy2DAsync on the copy stream). */
+int rt_memcpy2d_d2h_async(void* host_pinned, uint64_t hpitch, uint64_t dev, uint64_t dpitch,
+                          uint64_t width, uint64_t height, uint64_t stream);
+int rt_memcpy2d_h2d_async(uint64_t dev, uint64_t dpitch, const void* host_pinned,
+                          uint64_t hpitch, uint64_t width, uint64_t height, uint64_t stream);
 int rt_memcpy_h2d_async(uint64_t dev, const void* host_pinned, uint64_t bytes, uint64_t stream);
 /* Standalone bit-exact RNG fill (numpy default_rng((words..., *coords)) per
  * row): rows x count values of dist into dev (f64).  For tests/tools. */

@@ -183,8 +183,15 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
     }
     case RT_K_POLICY:
       return rt_kernel_policy(blk);
-    case RT_K_LOOP:
+    case RT_K_LOOP: {
+      rt_loop_params* p = (rt_loop_params*)blk;
+      if (p->blk_len > 0) {
+        if (p->blk_slot < 0 || p->blk_slot >= nenv) return nullptr;
+        p->start = env[p->blk_slot] * p->blk_len;
+        p->stop = p->start + p->blk_len;
+      }
       return rt_kernel_loop();
+    }
     default:
       return nullptr;
   }
@@ -284,6 +291,13 @@ extern "C" int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* 
         ++pc;
         break;
       }
+      case RT_OP_ENVMOD: {
+        if (in.a < 0 || in.a >= nenv || in.b < 0 || in.b >= nenv || in.c <= 0)
+          return fail(RT_ERR_BAD_ARG, "bad envmod");
+        env[in.a] = env[in.b] % in.c;
+        ++pc;
+        break;
+      }
       case RT_OP_HOOK:
         return fail(RT_ERR_BAD_ARG, "program has host hooks: use rt_run_segment");
       default:
@@ -319,6 +333,12 @@ extern "C" int rt_run_segment(const rt_instr* prog, int32_t nprog, const rt_laun
         if (more) { env[f.a] = v; pc = in.a + 1; } else ++pc;
         break;
       }
+      case RT_OP_ENVMOD:
+        if (in.a < 0 || in.a >= nenv || in.b < 0 || in.b >= nenv || in.c <= 0)
+          return fail(RT_ERR_BAD_ARG, "bad envmod");
+        env[in.a] = env[in.b] % in.c;
+        ++pc;
+        break;
       case RT_OP_HOOK:
         *pc_io = pc + 1;
         *hook_out = in.a;
@@ -369,6 +389,20 @@ extern "C" int rt_memcpy_d2h_async(void* host_pinned, uint64_t dev, uint64_t byt
 extern "C" int rt_memcpy_h2d_async(uint64_t dev, const void* host_pinned, uint64_t bytes, uint64_t stream) {
   return cuda_check(cudaMemcpyAsync((void*)dev, host_pinned, bytes, cudaMemcpyHostToDevice,
                                     (cudaStream_t)stream), "h2d");
+}
+
+extern "C" int rt_memcpy2d_d2h_async(void* host_pinned, uint64_t hpitch, uint64_t dev,
+                                     uint64_t dpitch, uint64_t width, uint64_t height,
+                                     uint64_t stream) {
+  return cuda_check(cudaMemcpy2DAsync(host_pinned, hpitch, (const void*)dev, dpitch, width, height,
+                                      cudaMemcpyDeviceToHost, (cudaStream_t)stream), "d2h 2d");
+}
+
+extern "C" int rt_memcpy2d_h2d_async(uint64_t dev, uint64_t dpitch, const void* host_pinned,
+                                     uint64_t hpitch, uint64_t width, uint64_t height,
+                                     uint64_t stream) {
+  return cuda_check(cudaMemcpy2DAsync((void*)dev, dpitch, host_pinned, hpitch, width, height,
+                                      cudaMemcpyHostToDevice, (cudaStream_t)stream), "h2d 2d");
 }
 
 // ------------------------------------------------------------ rng fill
@@ -489,6 +523,10 @@ extern "C" int rt_profile(const rt_instr* prog, int32_t nprog, const rt_launch_r
       int64_t v = env[f.a] + f.d;
       bool more = f.d > 0 ? (v < f.c) : (v > f.c);
       if (more) { env[f.a] = v; pc = in.a + 1; } else ++pc;
+    } else if (in.op == RT_OP_ENVMOD) {
+      if (in.c > 0 && in.a >= 0 && in.a < nenv && in.b >= 0 && in.b < nenv)
+        env[in.a] = env[in.b] % in.c;
+      ++pc;
     } else {
       ++pc;
     }

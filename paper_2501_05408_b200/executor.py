@@ -597,7 +597,7 @@ def payload_shapes(g: Graph, benv):
 
 class Executable:
     def __init__(self, g: Graph, benv: dict, seed: int, device: int, input_sig, fuse=True,
-                 shard=None, comm=None):
+                 shard=None, comm=None, swap=False):
         torch = _torch()
         self.torch = torch
         self.g = g
@@ -624,6 +624,19 @@ class Executable:
         self.absorbed = an["absorbed"]
         self.virtual = virtual = an["virtual"]
         self.bufs = an["bufs"]
+        self.swap_plan = None
+        if swap:
+            from .swap import plan_swap
+            kw = {} if swap is True else {"threshold": int(swap)}
+            sp = plan_swap(g, self.plan, self.bufs, virtual, benv, **kw)
+            if sp is not None and sp.ring_slot < N.RT_MAXENV:
+                self.swap_plan = sp
+                for k, b in self.bufs.items():
+                    r = k
+                    while self.bufs[r].alias is not None:
+                        r = self.bufs[r].alias
+                    if r in sp.keys:
+                        b.ring = (sp.dim, sp.bs)
         roots = [k for k, b in self.bufs.items() if b.alias is None and k[0] not in virtual]
         out_keys = {(nid, oid) for _, nid, oid in g.outputs}
         pinned = {k for k in roots if g.nodes[k[0]].kind in ("const", "input")}
@@ -644,7 +657,7 @@ class Executable:
                        self.contract, self.fuse_src, self.gemm_epi,
                        absorbed=self.absorbed, shard=shard,
                        shard_reduce=self.shard_reduce,
-                       persistent=OPTS["persistent"]).lower()
+                       persistent=OPTS["persistent"], swap=self.swap_plan).lower()
         key_of = {v: k for k, v in fake.items()}
         rec_ptrs = []
         for ri, (_, p, *_r) in enumerate(low.recs):
@@ -679,8 +692,12 @@ class Executable:
                        self.contract, self.fuse_src, self.gemm_epi,
                        absorbed=self.absorbed, shard=shard,
                        shard_reduce=self.shard_reduce,
-                       persistent=OPTS["persistent"]).lower()
+                       persistent=OPTS["persistent"], swap=self.swap_plan).lower()
         self.hooks = low.hooks
+        self.swap_rt = None
+        if self.swap_plan is not None:
+            from .swap import SwapRuntime
+            self.swap_rt = SwapRuntime(self, self.swap_plan)
         self._upload_loops(low)
         self.nrec = len(low.recs)
         self._low_recs = low.recs
@@ -877,6 +894,9 @@ class Executable:
             if rc != N.RT_HOOK:
                 N.check(rc, "rt_run_segment")
             h = self.hooks[hook.value]
+            if h.get("kind", "allreduce") != "allreduce":
+                self.swap_rt.hook(h["kind"], int(self.env[h["slot"]]), s)
+                continue
             off = h["off0"] + sum(self.env[k] * v for k, v in h["off_env"].items())
             item = ITEMSIZE_OF[h["dtype"]]
             t = _wrap_ptr(torch, h["ptr"] + off * item, h["count"] * item, self.dev)
@@ -1131,7 +1151,7 @@ def _input_sig(inputs):
 
 
 def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None, comm=None,
-                   block=None):
+                   block=None, swap=False):
     global _TORCH_DT
     torch = _torch()
     if _TORCH_DT is None:
@@ -1143,7 +1163,8 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         benv = _resolve_dynamic(graph, benv, dyn, inputs, seed, device)
     dev = torch.cuda.current_device() if device is None else int(device)
     block = tuple(block) if block else None
-    key = (id(g), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs), shard, block)
+    key = (id(g), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs), shard, block,
+           swap)
     ex = _CACHE.get(key)
     if ex is not None and ex[0]() is g:
         return ex[1], benv
@@ -1156,7 +1177,8 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
     if shard is not None and comm is None:
         from .shard import TorchComm
         comm = TorchComm()
-    exe = Executable(h, benv, int(seed), dev, _input_sig(inputs), shard=shard, comm=comm)
+    exe = Executable(h, benv, int(seed), dev, _input_sig(inputs), shard=shard, comm=comm,
+                     swap=swap if block else False)
     try:
         _CACHE[key] = (weakref.ref(g), exe)
     except TypeError:
@@ -1208,14 +1230,20 @@ def _resolve_dynamic(g: Graph, benv, dyn, inputs, seed, device):
 
 
 def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=None,
-            device_outputs=False, stream=None, shard=None, comm=None, block=None):
+            device_outputs=False, stream=None, shard=None, comm=None, block=None, swap=False):
     """Drop-in for reference `reference_execute` (runtime.py:460-475).
 
     shard=ShardSpec(dim, rank, world): this process runs envs
     [rank*B, (rank+1)*B) of a G-way env-sharded run (bounds give the local
     extent B); reductions over the dim are all-reduced through `comm`
-    (default: torch.distributed)."""
-    exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm, block)
+    (default: torch.distributed).
+
+    block=(dim, bs): time-block the backward along dim (blocking.block_dim);
+    swap=True (with block): activations of the acting recurrence keep two
+    time blocks in HBM and are offloaded to / fetched from pinned host
+    memory per block (swap.py); an int is the swap threshold in bytes
+    (default 64 MiB, the reference's polysched.py:28)."""
+    exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm, block, swap)
     exe.run(inputs or {}, stream)
     exe.check_status(stream)
     outs = exe.outputs(device_outputs)

@@ -290,6 +290,9 @@ def loop_source(lp, ops, name):
                      f"((long long*)p.prof)[{i}] += c1 - c0; c0 = c1; }}")
     body = "\n".join(parts)
     cmp = "<" if lp.step > 0 else ">"
+    # a time-blocked loop takes its range from the launch (prepare() folds
+    # the block index from env); otherwise the range is a literal
+    t0, t1 = ("p.start", "p.stop") if lp.blk_len else (f"{lp.start}LL", f"{lp.stop}LL")
     return f"""#include "loop_lib.cuh"
 extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constant__ rt_loop_params p) {{
   extern __shared__ __align__(128) unsigned char smem[];
@@ -306,7 +309,7 @@ extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constan
   loop_prologue(p, smem, bars, ring);
   (void)sA32;
   long long c0 = clock64();
-  for (long long t = {lp.start}LL; t {cmp} {lp.stop}LL; t += {lp.step}LL) {{
+  for (long long t = {t0}; t {cmp} {t1}; t += {lp.step}LL) {{
     env[{lp.slot}] = t;
 {body}
   }}

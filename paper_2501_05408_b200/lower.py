@@ -62,17 +62,23 @@ class Buf:
     host: np.ndarray | None = None  # constant/input contents
     ptr: int = 0
     folded: frozenset = frozenset()  # loop dims stored as one slot (stride 0)
+    ring: tuple | None = None        # (dim, bs): swap-managed, 2 time blocks resident
 
     @property
     def shape(self):
         return tuple(self.dshape) + tuple(self.pshape)
 
+    def storage_ext(self):
+        ext = [1 if d in self.folded else x for d, x in zip(self.dims, self.dshape)]
+        if self.ring:
+            ext[self.dims.index(self.ring[0])] = 2 * self.ring[1]
+        return ext
+
     @property
     def strides(self):
-        if not self.folded:
+        if not self.folded and not self.ring:
             return cstrides(self.shape)
-        ext = [1 if d in self.folded else x for d, x in zip(self.dims, self.dshape)]
-        st = list(cstrides(ext + list(self.pshape)))
+        st = list(cstrides(self.storage_ext() + list(self.pshape)))
         for j, d in enumerate(self.dims):
             if d in self.folded:
                 st[j] = 0
@@ -86,8 +92,12 @@ class Buf:
 
     @property
     def nbytes(self):
-        ext = [1 if d in self.folded else x for d, x in zip(self.dims, self.dshape)]
-        return prod(ext) * prod(self.pshape) * ir.ITEMSIZE[self.dtype]
+        return prod(self.storage_ext()) * prod(self.pshape) * ir.ITEMSIZE[self.dtype]
+
+    @property
+    def full_nbytes(self):
+        """bytes of every value (the pinned host copy of a swap-managed buffer)"""
+        return prod(self.dshape) * prod(self.pshape) * ir.ITEMSIZE[self.dtype]
 
 
 # ---------------------------------------------------------------------------
@@ -253,7 +263,7 @@ class Ctx:
 class Lowering:
     def __init__(self, plan, bufs: dict, status_ptr: int, seed: int, alloc, contract=None,
                  fuse_src=None, gemm_epi=None, persistent=True, use_tc=True, absorbed=None,
-                 shard=None, shard_reduce=None):
+                 shard=None, shard_reduce=None, swap=None):
         self.plan = plan
         self.g = plan.graph
         self.benv = plan.benv
@@ -277,6 +287,7 @@ class Lowering:
         self.shard = shard
         self.shard_reduce = set(shard_reduce or ())
         self.hooks = []                        # all-reduce hooks (sharded reductions)
+        self.swap = swap                       # swap.SwapPlan (time-blocked swapping)
         self._capture = None
         self.loop_subs = {}                    # loop record -> sub-op descriptors
         self.fuse_src = dict(fuse_src or {})   # producer nid -> consumer nid (inlined)
@@ -477,6 +488,12 @@ class Lowering:
 
     def lower(self):
         self.steps(self.plan.steps)
+        if self.swap is not None:
+            from .swap import adjust_views
+            params = [p for (_, p, *_r) in self.recs]
+            for info in self.loop_subs.values():
+                params += [op[1] for op in info["ops"]]
+            adjust_views(params, self.swap, self.bufs, self.slot)
         return self
 
     def steps(self, steps):
@@ -518,7 +535,7 @@ class Lowering:
                         return None
         return S
 
-    def _loop_persistent(self, s: Loop, S):
+    def _loop_persistent(self, s: Loop, S, blk=None):
         self._capture = []
         try:
             self.steps(s.body)
@@ -619,6 +636,8 @@ class Lowering:
         lp = N.rt_loop_params()
         lp.slot = self.slot[s.dim]
         lp.nops = len(ops)
+        if blk is not None:
+            lp.blk_slot, lp.blk_len = blk
         n = T
         lp.start, lp.stop, lp.step = (0, n, 1) if s.step > 0 else (n - 1, -1, -1)
         lp.rows = rows
@@ -633,7 +652,44 @@ class Lowering:
                            (first.id, f"loop[{s.dim}]"))
         self.loop_subs[idx] = {"ops": ops, "trips": T}
 
+    def _swap_hook(self, kind):
+        self.hooks.append({"kind": kind, "slot": self.slot[self.swap.kb]})
+        self.prog.append((N.RT_OP_HOOK, len(self.hooks) - 1, 0, 0, 0, 0))
+
+    def _swap_loop(self, s: Loop):
+        """Time-blocked acting loop with swap-managed outputs: one persistent
+        launch per time block inside a loop over blocks; the ring slot is set
+        from the block index, the previous use of the slot is awaited, and
+        the finished block is offloaded (swap.SwapRuntime)."""
+        sw = self.swap
+        S = self._persistent_ok(s)
+        if not S:
+            raise LowerError("swapping needs a persistent acting loop")
+        mark = len(self.prog)
+        self._loop_persistent(s, S, blk=(self.slot[sw.kb], sw.bs))
+        launch = self.prog.pop()          # the loop record; hoisted draws stay before
+        assert launch[0] == N.RT_OP_LAUNCH and len(self.prog) >= mark
+        at = len(self.prog)
+        self.prog.append([N.RT_OP_FOR, self.slot[sw.kb], 0, sw.DI, 1, 0])
+        self.prog.append((N.RT_OP_ENVMOD, sw.ring_slot, self.slot[sw.kb], 2, 0, 0))
+        self._swap_hook("swap_wait")
+        self.prog.append(launch)
+        self._swap_hook("swap_out")
+        self.prog.append((N.RT_OP_END, at, 0, 0, 0, 0))
+        self.prog[at][5] = len(self.prog)
+
     def loop(self, s: Loop):
+        if self.swap is not None and s.dim == self.swap.dim and s.lo is None and not s.fixed:
+            return self._swap_loop(s)
+        if self.swap is not None and s.dim == self.swap.kb:
+            at = len(self.prog)
+            self.prog.append([N.RT_OP_FOR, self.slot[s.dim], 0, self.ext[s.dim], 1, 0])
+            self.prog.append((N.RT_OP_ENVMOD, self.swap.ring_slot, self.slot[s.dim], 2, 0, 0))
+            self._swap_hook("swap_in")
+            self.steps(s.body)
+            self.prog.append((N.RT_OP_END, at, 0, 0, 0, 0))
+            self.prog[at][5] = len(self.prog)
+            return
         S = self._persistent_ok(s)
         if S:
             mark = (len(self.recs), len(self.prog))

@@ -32,7 +32,7 @@ RT_K_GEMM_TMA = 12
 TMA_SMEM = 4 * 48 * 1024 + 1024
 TC_SMEM = 2 * (2 * 128 * 32 * 4 + 2 * 256 * 32 * 4)
 
-RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK = 1, 2, 3, 4, 6
+RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK, RT_OP_ENVMOD = 1, 2, 3, 4, 6, 7
 RT_HOOK = 100
 
 RT_ERR_ROW_RANGE, RT_ERR_SLICE_RANGE = 1, 2
@@ -131,7 +131,8 @@ class rt_loop_op(C.Structure):
 class rt_loop_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("slot", i32), ("nops", i32), ("start", i64), ("stop", i64),
                 ("step", i64), ("rows", i64), ("rows_per_cta", i32), ("smem_bytes", i32),
-                ("ring_off", i32), ("a_off", i32), ("ops", u64), ("prof", u64)]
+                ("ring_off", i32), ("a_off", i32), ("ops", u64), ("prof", u64),
+                ("blk_slot", i32), ("_pad", i32), ("blk_len", i64)]
 
 
 class rt_launch_rec(C.Structure):
@@ -187,6 +188,8 @@ def lib():
     L.rt_rng_fill.argtypes = [u64, C.POINTER(u32), i32, C.POINTER(i64), i32, i64, i32, i32, u64]
     L.rt_memcpy_d2h_async.argtypes = [C.c_void_p, u64, u64, u64]
     L.rt_memcpy_h2d_async.argtypes = [u64, C.c_void_p, u64, u64]
+    L.rt_memcpy2d_d2h_async.argtypes = [C.c_void_p, u64, u64, u64, u64, u64, u64]
+    L.rt_memcpy2d_h2d_async.argtypes = [u64, u64, C.c_void_p, u64, u64, u64, u64]
     if L.rt_version() != 1:
         raise NativeError("librtb200 ABI version mismatch")
     _lib = L
@@ -197,7 +200,8 @@ EXPORTS = ("rt_version", "rt_launch", "rt_run", "rt_status_alloc", "rt_status_re
            "rt_status_clear", "rt_status_free", "rt_memcpy_d2h_async", "rt_memcpy_h2d_async",
            "rt_rng_fill", "rt_last_error", "rt_graph_capture", "rt_graph_launch",
            "rt_graph_destroy", "rt_profile", "rt_graph_capture_ev", "rt_run_segment",
-           "rt_jit_compile", "rt_jit_load", "rt_jit_cubin")
+           "rt_jit_compile", "rt_jit_load", "rt_jit_cubin", "rt_memcpy2d_d2h_async",
+           "rt_memcpy2d_h2d_async")
 
 
 def check(rc: int, what: str = ""):

@@ -117,3 +117,19 @@ def test_time_blocked_backward_matches_reference(name, bs):
     got = execute(c.graph(), bounds=c.bounds, inputs=c.inputs, seed=c.seed, block=("t", bs))
     for k, want in c.outputs.items():
         assert_close(got[k], want, k)
+
+
+@pytest.mark.parametrize("name", ["mlp_f32_I1B4T6", "mlp_f64_I1B4T6"])
+@pytest.mark.parametrize("bs", [2, 3])
+def test_swapped_time_blocks_match_reference(name, bs):
+    """GPU<->host swapping (swap.py): the acting loop's activations keep two
+    time blocks in HBM, each block is offloaded to pinned host memory after
+    the recurrence writes it and fetched back for the backward block."""
+    from paper_2501_05408_b200 import execute, get_executable
+    c = load_case(name)
+    got = execute(c.graph(), bounds=c.bounds, inputs=c.inputs, seed=c.seed, block=("t", bs),
+                  swap=1)
+    exe, _ = get_executable(c.graph(), c.bounds, c.inputs, c.seed, block=("t", bs), swap=1)
+    assert exe.swap_plan is not None and len(exe.swap_plan.keys) >= 2
+    for k, want in c.outputs.items():
+        assert_close(got[k], want, k)

@@ -228,3 +228,20 @@ def test_time_blocking_shrinks_long_horizon_plan():
     assert len(folded) >= 20
     assert an["bufs"][[k for k in an["bufs"] if h.nodes[k[0]].name == "v126"][0]].nbytes \
         == 256 * 10000 * 256 * 4
+
+
+def test_swap_plan_manages_acting_activations():
+    """C4 blocked: h1, h2 (26 GB each at E=256, T=100k) are swap-managed
+    (written by the acting loop, read per time block); o is not (the
+    recurrence reads o[t-1] across block boundaries)."""
+    from paper_2501_05408_b200 import blocking, swap as SW
+    g = load_graph("reinforce_mlp_c2")
+    benv = {"I": 1, "B": 256, "T": 100000}
+    h = X.copy_graph(g)
+    X.prepare(h, benv)
+    b2 = blocking.block_dim(h, benv, "t", 10000)
+    an = X.analyze(h, b2, X.payload_shapes(h, b2))
+    sp = SW.plan_swap(h, an["plan"], an["bufs"], an["virtual"], b2)
+    names = {h.nodes[k[0]].name for k in sp.keys}
+    assert {"h1", "h2"} <= names and "o" not in names
+    assert sp.DI == 10 and sp.bs == 10000
