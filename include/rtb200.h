@@ -315,8 +315,8 @@ typedef struct {
   uint64_t ops;         /* device pointer to rt_loop_op[nops] */
   uint64_t prof;        /* optional int64[nops]: CTA 0's clock64 cycles per op */
   int32_t blk_slot;     /* blk_len > 0: run [env[blk_slot]*blk_len, +blk_len) */
-  int32_t _pad;         /*   (one time block of a long horizon per launch)    */
-  int64_t blk_len;
+  int32_t red_off;      /*   (one time block per launch); red_off: byte      */
+  int64_t blk_len;      /*   offset of the K-split GEMM reduction area         */
 } rt_loop_params;
 
 /* Launch record: one kernel family + its parameter block. */

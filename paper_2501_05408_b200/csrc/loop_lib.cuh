@@ -781,6 +781,83 @@ RT_DEV void tma_core(const T* Bg, uint32_t sA, loop_ring& ring, T (&acc)[NC][MRP
   ring.seq += NCH;
 }
 
+// K-split variant for wide N (N = 32*CPL, CPL <= 8) and few rows: warp w
+// takes rows w, w+W, ... of every streamed panel for ALL N columns (lane l
+// owns columns [l*CPL, (l+1)*CPL)), so each k costs CPL/4 + MRP/4 16-byte
+// shared loads for CPL*MRP FMAs (the column-per-thread core spends 3 loads
+// per MRP*... FMAs and is LSU-bound).  The W per-warp partial tiles are
+// summed through `red` ([W][MRP][N] in shared memory) once per step; on
+// return acc[q] holds output (row, col) = (o / N, o % N) for
+// o = tid * OPT + q, OPT = MRP * N / blockDim.
+template <typename T, int MRP, int K, int N, int KC>
+RT_DEV void tma_core_ks(const T* Bg, uint32_t sA, loop_ring& ring, uint32_t red,
+                        T (&out)[MRP * N / 256]) {
+  constexpr int NCH = (K + KC - 1) / KC;
+  constexpr int CPL = N / 32;
+  constexpr int W = 8;                       // warps (blockDim 256)
+  constexpr int OPT = MRP * N / 256;
+  static_assert(N % 32 == 0 && CPL <= 8 && CPL % 4 == 0, "K-split core: N = 32*{4,8}");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T acc[MRP][CPL];
+#pragma unroll
+  for (int r = 0; r < MRP; ++r)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[r][c] = (T)0;
+  const uint32_t ring_base = smem_u32(ring.buf);
+  for (int ch = 0; ch < NCH; ++ch) {
+    const uint32_t g = ring.seq + (uint32_t)ch;
+    const uint32_t st = g % RING;
+    mbar_wait(&ring.bar[st], (g / RING) & 1);
+    const uint32_t bs = ring_base + st * ring.stage_bytes;
+    const int rows = (ch + 1) * KC <= K ? KC : K - ch * KC;
+    const uint32_t ak = sA + (uint32_t)(ch * KC * MRP * sizeof(T));
+#pragma unroll 2
+    for (int kk = warp; kk < rows; kk += W) {
+      T a[MRP], b[CPL];
+      lds_rows<MRP>(ak + (uint32_t)(kk * MRP * sizeof(T)), a);
+      lds_rows<CPL>(bs + (uint32_t)((kk * N + lane * CPL) * sizeof(T)), b);
+#pragma unroll
+      for (int r = 0; r < MRP; ++r)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && ch + RING < NCH) {
+      const int cc = ch + RING;
+      const uint32_t st2 = (ring.seq + (uint32_t)cc) % RING;
+      const int rows2 = (cc + 1) * KC <= K ? KC : K - cc * KC;
+      const uint32_t bytes = (uint32_t)(rows2 * N * sizeof(T));
+      mbar_expect_tx(&ring.bar[st2], bytes);
+      bulk_g2s(ring.buf + (size_t)st2 * ring.stage_bytes, Bg + (size_t)cc * KC * N, bytes, &ring.bar[st2]);
+    }
+  }
+  ring.seq += NCH;
+  // cross-warp sum: red[w][r][n]
+#pragma unroll
+  for (int r = 0; r < MRP; ++r)
+#pragma unroll
+    for (int c = 0; c < CPL; c += 4) {
+      const uint32_t a = red + (uint32_t)(((warp * MRP + r) * N + lane * CPL + c) * sizeof(T));
+      if constexpr (sizeof(T) == 4)
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(acc[r][c]), "f"(acc[r][c + 1]),
+                     "f"(acc[r][c + 2]), "f"(acc[r][c + 3]));
+      else {
+        sts1(a, acc[r][c]); sts1(a + 8, acc[r][c + 1]); sts1(a + 16, acc[r][c + 2]); sts1(a + 24, acc[r][c + 3]);
+      }
+    }
+  __syncthreads();
+  const int o0 = threadIdx.x * OPT;
+#pragma unroll
+  for (int q = 0; q < OPT; ++q) out[q] = (T)0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    T v[OPT];
+    lds_rows<OPT>(red + (uint32_t)((w * MRP * N + o0) * sizeof(T)), v);
+#pragma unroll
+    for (int q = 0; q < OPT; ++q) out[q] += v[q];
+  }
+}
+
 template <typename T, int K, int N, int KC>
 RT_DEV void tma_prefetch(const T* Bg, loop_ring& ring) {
   constexpr int NCH = (K + KC - 1) / KC;

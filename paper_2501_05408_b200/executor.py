@@ -438,7 +438,7 @@ ABSORB_CONSUMERS = {"matmul", "sum", "add", "sub", "mul", "div", "neg", "exp", "
                     "unsqueeze", "expand", "identity", "detach"}
 
 
-def find_absorbed_layouts(g: Graph, skip):
+def find_absorbed_layouts(g: Graph, skip, allow=frozenset()):
     """Layout nodes read through an identity edge from a materialised source
     are never copied: consumers read the source with transformed strides."""
     out_ids = {nid for _, nid, _ in g.outputs}
@@ -458,8 +458,11 @@ def find_absorbed_layouts(g: Graph, skip):
         outs = g.out_edges(n.id)
         if not outs or any(g.nodes[o.sink].kind not in ABSORB_CONSUMERS for o in outs):
             continue
-        if any(o.sink in skip for o in outs):
+        if any(o.sink in skip and o.sink not in allow for o in outs):
             continue   # an alias of it would resolve to storage that never exists
+        # (contraction matmuls are virtual but read their operands' views
+        # directly in the contraction GEMM: a transposed activation is a
+        # stride swap there, never a copy)
         res.add(n.id)
     return res
 
@@ -481,7 +484,8 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
     plan = Planner(g, benv).plan(getattr(g, "block_dims", ()))
     fixed_of = plan_fixed(plan.steps)
     alias_nodes = {k[0] for k in alias}
-    absorbed = find_absorbed_layouts(g, virtual | alias_nodes) if fuse else set()
+    absorbed = find_absorbed_layouts(g, virtual | alias_nodes, set(contract.values())) \
+        if fuse else set()
     virtual |= absorbed
     gemm_epi = find_gemm_epilogues(g, pshape, fixed_of, virtual | alias_nodes, ext) if fuse else {}
     taken = set(virtual) | alias_nodes | set(gemm_epi)

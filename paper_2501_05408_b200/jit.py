@@ -377,7 +377,18 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
                  f"const long long k = i - r * {K}; const long long m = m0 + r; "
                  f"sts1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), r < mr ? Ap[aoff + {a_m} + {a_k}] : ({T})0); }}")
     lines.append("__syncthreads();")
-    if tma:
+    if tma and lp.red_off and KS_ENABLED and ks_eligible(lp.rows_per_cta, re, q, f64):
+        opt = mrp * Nn // 256
+        lines.append(f"{T} o[{opt}];")
+        lines.append(f"tma_core_ks<{T}, {mrp}, {K}, {Nn}, {kc}>(Bg, sA32, ring, smem_u32(smem + {lp.red_off}), o);")
+        lines += [f"const int o0 = threadIdx.x * {opt}; const int r = o0 / {Nn};",
+                  f"if (r < mr) {{ const long long m = m0 + r;",
+                  f"  #pragma unroll\n  for (int q = 0; q < {opt}; ++q) {{ const long long n = (o0 % {Nn}) + q;",
+                  f"    const {T} bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else f"({T})0;"),
+                  f"    {T} v = o[q] + bias;" + (f" v = vm_tanh<{T}>(v);" if tanh else ""),
+                  f"    Cp[coff + {c_m} + {c_n}] = v; }}",
+                  "}"]
+    elif tma:
         lines.append(f"{T} acc[{nc}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = ({T})0; }}")
         lines.append(f"tma_core<{T}, {mrp}, {nc}, {K}, {Nn}, {kc}>(Bg, sA32, ring, acc);")
@@ -459,6 +470,19 @@ def _udf_literal(p, op_index, soff, noise):
         lines.append(f"  nz += {p.out_count[j]};")
     lines.append("}")
     return "    {  // env (specialised)\n      " + "\n      ".join(lines) + "\n    }"
+
+
+def ks_eligible(rows_per_cta, re, q, f64):
+    """In-loop GEMMs that take the K-split core (loop_lib.cuh tma_core_ks):
+    fp32, N = 256 (or 128 with 8 rows), dense row-major B."""
+    mrp = (rows_per_cta * re + 3) // 4 * 4
+    dense_1d = q.N.nd == 1 and q.K.nd == 1 and q.Z.nd <= 1 and q.z == 1
+    return (not f64 and dense_1d and mrp <= 8 and q.n in (128, 256) and q.k >= 128
+            and (mrp * q.n // 256) % 4 == 0
+            and q.B.s2[0] == 1 and q.B.s1[0] == q.n and q.B.dtype == N.RT_F32)
+
+
+KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
 
 
 def _gemm_call(lp, q, re, f64, soff):

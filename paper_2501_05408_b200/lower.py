@@ -588,7 +588,17 @@ class Lowering:
             p_off.append(cur)
             cur += (C.sizeof(p) + 127) // 128 * 128
         a_off = cur
-        ring_off = (a_off + a_need + 127) // 128 * 128
+        # K-split in-loop GEMMs (jit.ks_eligible) sum per-warp partial tiles
+        # through a [8 warps][rows][N] area before the weight ring
+        from .jit import KS_ENABLED, ks_eligible
+        red_bytes = 0
+        for kernel, p, re, f64, _ in ops:
+            if KS_ENABLED and kernel == N.RT_K_GEMM and p.n >= 64 and p.k >= 128 and \
+                    ks_eligible(R, re, p, f64):
+                mrp = (R * re + 3) // 4 * 4
+                red_bytes = max(red_bytes, 8 * mrp * p.n * 4)
+        red_off = (a_off + a_need + 127) // 128 * 128
+        ring_off = (red_off + red_bytes + 127) // 128 * 128
         stage = 0
         if tma:
             stage = 32 * 1024
@@ -645,6 +655,7 @@ class Lowering:
         lp.smem_bytes = smem
         lp.ring_off = ring_off
         lp.a_off = a_off
+        lp.red_off = red_off if red_bytes else 0
         for op, off in zip(ops, p_off):
             op.append(off)
         first = self.g.nodes[s.body[0].nid]
@@ -1192,6 +1203,17 @@ class Lowering:
             p.splits = splits
             p.part = self.alloc(splits * p.total * 8)
             self.add_rec(N.RT_K_REDUCE, p, [ob, splits, 1], [256, 1, 1], 0, (n.id, n.name))
+            q = N.rt_reduce_params.from_buffer_copy(p)
+            q.threads_per_out = -1
+            self.add_rec(N.RT_K_REDUCE, q, self.grid1(p.total), [256, 1, 1], 0, (n.id, n.name))
+            return
+        if const_lens and p.total <= 64 and maxlen >= 4096 and p.total * maxlen >= (1 << 18):
+            # few outputs, long constant ranges (a head's bias gradient over all
+            # points): split the range over CTAs (column kernel, lanes per output)
+            splits = int(max(1, min(maxlen // 1024, 148 * 4, 1024)))
+            p.splits = splits
+            p.part = self.alloc(splits * p.total * 8)
+            self.add_rec(N.RT_K_REDUCE, p, [1, splits, 1], [256, 1, 1], 0, (n.id, n.name))
             q = N.rt_reduce_params.from_buffer_copy(p)
             q.threads_per_out = -1
             self.add_rec(N.RT_K_REDUCE, q, self.grid1(p.total), [256, 1, 1], 0, (n.id, n.name))

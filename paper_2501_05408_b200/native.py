@@ -132,7 +132,7 @@ class rt_loop_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("slot", i32), ("nops", i32), ("start", i64), ("stop", i64),
                 ("step", i64), ("rows", i64), ("rows_per_cta", i32), ("smem_bytes", i32),
                 ("ring_off", i32), ("a_off", i32), ("ops", u64), ("prof", u64),
-                ("blk_slot", i32), ("_pad", i32), ("blk_len", i64)]
+                ("blk_slot", i32), ("red_off", i32), ("blk_len", i64)]
 
 
 class rt_launch_rec(C.Structure):
