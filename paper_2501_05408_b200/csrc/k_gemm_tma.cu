@@ -22,7 +22,7 @@
 #define TM_BM 128
 #define TM_BN 256
 #define TM_BK 16
-#define TM_ST 4
+#define TM_ST 2   // 2 stages: two CTAs per SM, one's epilogue overlaps the other's mainloop
 #define TM_CONV 256
 #define TM_THREADS (TM_CONV + 64)
 #define TM_A_BYTES (TM_BM * TM_BK * 4)
@@ -109,7 +109,7 @@ RT_DEV uint64_t op_desc(uint32_t base, int ks, int mn) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma(const __grid_constant__ tm_args a) {
+__global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constant__ tm_args a) {
   extern __shared__ unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[TM_ST], conv[TM_ST], empty[TM_ST], done;
   __shared__ uint32_t tmem_s;
