@@ -327,7 +327,7 @@ typedef struct {
   int32_t grid[3];
   int32_t block[3];
   int32_t smem;
-  int32_t _pad;
+  int32_t cluster;     /* > 1: thread-block cluster size along x (JIT kernels) */
   uint64_t jit_fn;     /* CUfunction specialised for this record (0: library kernel) */
 } rt_launch_rec;
 

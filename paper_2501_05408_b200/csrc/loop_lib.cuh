@@ -73,6 +73,40 @@ RT_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 #define RING 4
 
+// ---------------------------------------------------------------- clusters
+// A CTA pair of the persistent acting loop keeps one K-half of a large
+// weight matrix resident in each SM's shared memory and exchanges operand
+// rows / partial sums through distributed shared memory (DSMEM).
+RT_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+RT_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+RT_DEV uint32_t dsmem_map(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+RT_DEV float dsmem_ld(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+RT_DEV float4 dsmem_ld4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+RT_DEV void sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+}
+
+
 struct loop_ring {
   uint64_t* bar;       // [RING] mbarriers
   unsigned char* buf;  // [RING][stage_bytes]
@@ -722,6 +756,25 @@ RT_DEV void udf_fixed(const rt_udf_params& p, const rt_loop_op& op, const int64_
         store_as<double>((void*)p.out[j].ptr, p.out[j].dtype, o + e, v);
       }
       nz += p.out_count[j];
+    }
+  }
+}
+
+// pair GEMM core: acc_own[r] += sum_{k in my half} A_own[k][r] B[k][col],
+// acc_par[r] likewise for the partner's rows (A_par = its k-half, copied).
+template <int MRP, int KH, int N>
+RT_DEV void pair_core(uint32_t sA_own, uint32_t sA_par, uint32_t sB, int col, float (&ao)[MRP],
+                      float (&ap)[MRP]) {
+#pragma unroll 4
+  for (int kk = 0; kk < KH; ++kk) {
+    const float b = lds1(sB + (uint32_t)((kk * N + col) * 4), 0.f);
+    float a1[MRP], a2[MRP];
+    lds_rows<MRP>(sA_own + (uint32_t)(kk * MRP * 4), a1);
+    lds_rows<MRP>(sA_par + (uint32_t)(kk * MRP * 4), a2);
+#pragma unroll
+    for (int r = 0; r < MRP; ++r) {
+      ao[r] = fma(a1[r], b, ao[r]);
+      ap[r] = fma(a2[r], b, ap[r]);
     }
   }
 }

@@ -36,6 +36,7 @@ struct DriverApi {
   decltype(&cuModuleLoadData) moduleLoadData = nullptr;
   decltype(&cuModuleGetFunction) moduleGetFunction = nullptr;
   decltype(&cuLaunchKernel) launchKernel = nullptr;
+  decltype(&cuLaunchKernelEx) launchKernelEx = nullptr;
   decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
   decltype(&cuGetErrorString) getErrorString = nullptr;
   void* tensorMapEncodeTiled = nullptr;
@@ -56,6 +57,7 @@ static DriverApi& drv() {
     RT_GET(moduleLoadData, "cuModuleLoadData")
     RT_GET(moduleGetFunction, "cuModuleGetFunction")
     RT_GET(launchKernel, "cuLaunchKernel")
+    RT_GET(launchKernelEx, "cuLaunchKernelEx")
     RT_GET(funcSetAttribute, "cuFuncSetAttribute")
     RT_GET(getErrorString, "cuGetErrorString")
     RT_GET(tensorMapEncodeTiled, "cuTensorMapEncodeTiled")
@@ -214,8 +216,26 @@ static int launch_one(const rt_launch_rec* rec, const int64_t* env, int nenv, cu
     CUfunction f = (CUfunction)rec->jit_fn;
     if (rec->smem > 48 * 1024)
       D.funcSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, rec->smem);
-    CUresult r = D.launchKernel(f, g.x, g.y, g.z, b.x, b.y, b.z, rec->smem, (CUstream)s, args,
-                                nullptr);
+    CUresult r;
+    if (rec->cluster > 1) {
+      // thread-block clusters (e.g. a CTA pair splitting a resident weight
+      // matrix of the persistent acting loop across its two SMs)
+      CUlaunchConfig cfg = {};
+      CUlaunchAttribute attr[1];
+      attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+      attr[0].value.clusterDim.x = (unsigned)rec->cluster;
+      attr[0].value.clusterDim.y = 1;
+      attr[0].value.clusterDim.z = 1;
+      cfg.gridDimX = g.x; cfg.gridDimY = g.y; cfg.gridDimZ = g.z;
+      cfg.blockDimX = b.x; cfg.blockDimY = b.y; cfg.blockDimZ = b.z;
+      cfg.sharedMemBytes = rec->smem;
+      cfg.hStream = (CUstream)s;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      r = D.launchKernelEx(&cfg, f, args, nullptr);
+    } else {
+      r = D.launchKernel(f, g.x, g.y, g.z, b.x, b.y, b.z, rec->smem, (CUstream)s, args, nullptr);
+    }
     if (r != CUDA_SUCCESS) {
       const char* m = nullptr;
       D.getErrorString(r, &m);

@@ -716,6 +716,7 @@ class Executable:
                 r.grid[j] = grid[j]
                 r.block[j] = block[j]
             r.smem = smem
+            r.cluster = low.rec_cluster.get(i, 0)
         self.recs = recs
         self.labels = [lab for (*_, lab) in low.recs]
         self.kernels = [k for (k, *_rest) in low.recs]

@@ -231,11 +231,20 @@ def _env_fold(base, coefs):
     return " + ".join(terms)
 
 
-def loop_source(lp, ops, name):
+def loop_source(lp, ops, name, info=None):
     """A persistent loop kernel with the op sequence specialised: EW bodies
-    straight-line, GEMM/UDF/RNG as single template instantiations."""
+    straight-line, GEMM/UDF/RNG as single template instantiations.  With
+    info["pair"] the kernel runs as 2-CTA clusters and that GEMM keeps its
+    weights resident (one K-half per CTA, _gemm_pair_literal)."""
+    pair = (info or {}).get("pair")
     parts = []
     for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
+        if pair is not None and i == pair["op"]:
+            parts.append(_gemm_pair_literal(lp, p, soff, pair))
+            parts.append("    __syncthreads();")
+            parts.append(f"    if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {{ long long c1 = clock64(); "
+                         f"((long long*)p.prof)[{i}] += c1 - c0; c0 = c1; }}")
+            continue
         if kernel == N.RT_K_EW:
             nd = p.box.nd
             ext = [p.box.ext[j] for j in range(nd)]
@@ -293,6 +302,12 @@ def loop_source(lp, ops, name):
     # a time-blocked loop takes its range from the launch (prepare() folds
     # the block index from env); otherwise the range is a literal
     t0, t1 = ("p.start", "p.stop") if lp.blk_len else (f"{lp.start}LL", f"{lp.stop}LL")
+    early, pair_pro = "  if (r0 >= r1) return;", ""
+    if pair is not None:
+        # both CTAs of a pair take part in every cluster barrier, even one
+        # without rows (the grid is padded to an even CTA count)
+        early = "  const long long r1c = r1 > r0 ? r1 : r0; (void)r1c;"
+        pair_pro = _pair_prologue(lp, ops[pair["op"]][1], ops[pair["op"]][5], pair)
     return f"""#include "loop_lib.cuh"
 extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constant__ rt_loop_params p) {{
   extern __shared__ __align__(128) unsigned char smem[];
@@ -301,13 +316,14 @@ extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constan
   for (int e = 0; e < RT_MAXENV; ++e) env[e] = p.h.env[e];
   const long long r0 = (long long)blockIdx.x * {lp.rows_per_cta}LL;
   const long long r1 = r0 + {lp.rows_per_cta}LL < {lp.rows}LL ? r0 + {lp.rows_per_cta}LL : {lp.rows}LL;
-  if (r0 >= r1) return;
+{early}
   const rt_loop_op* ops = (const rt_loop_op*)p.ops;
   unsigned char* sA = smem + p.a_off;
   const uint32_t sA32 = smem_u32(sA);
   loop_ring ring;
   loop_prologue(p, smem, bars, ring);
   (void)sA32;
+{pair_pro}
   long long c0 = clock64();
   for (long long t = {t0}; t {cmp} {t1}; t += {lp.step}LL) {{
     env[{lp.slot}] = t;
@@ -315,6 +331,90 @@ extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constan
   }}
 }}
 """
+
+
+def _pair_prologue(lp, q, soff, pair):
+    """Load this CTA's K-half of the pair GEMM's weights into shared memory
+    (once: the weights do not move with the loop dim)."""
+    kh, n = pair["kh"], q.n
+    env_b = _env_terms([q.B.off_env[e] for e in range(N.RT_MAXENV)])
+    return f"""  {{  // pair GEMM: resident K-half of B
+    const rt_gemm_params& q = *(const rt_gemm_params*)(smem + {soff});
+    const float* Bg = (const float*)q.B.ptr + (q.B.off{env_b}) + (long long)cluster_rank() * {kh * n}LL;
+    const uint32_t pB = smem_u32(smem + {pair["b_off"]});
+    for (int i = threadIdx.x; i < {kh * n // 4}; i += blockDim.x)
+      sts4(pB + 16u * (uint32_t)i, __ldg(reinterpret_cast<const float4*>(Bg) + i));
+  }}
+  __syncthreads();"""
+
+
+def _gemm_pair_literal(lp, q, soff, pair):
+    """One in-loop GEMM C = act(A B + bias) on a 2-CTA cluster: each CTA holds
+    B[k-half] in shared memory, computes partial sums over its half for its
+    own rows AND its partner's rows (the partner's A k-half is read through
+    DSMEM), hands the partner's partials over, and finishes its own rows."""
+    K, Nn, kh = q.k, q.n, pair["kh"]
+    mrp = (lp.rows_per_cta + 3) // 4 * 4
+    env_a = _env_terms([q.A.off_env[e] for e in range(N.RT_MAXENV)])
+    env_c = _env_terms([q.C.off_env[e] for e in range(N.RT_MAXENV)])
+    env_bias = _env_terms([q.bias.off_env[e] for e in range(N.RT_MAXENV)])
+    a_m = _gbox_off(q.M, [q.A.s1[d] for d in range(4)], "m")
+    c_m = _gbox_off(q.M, [q.C.s1[d] for d in range(4)], "m")
+    a_k = _gbox_off(q.K, [q.A.s2[d] for d in range(4)], "k")
+    c_n = _gbox_off(q.N, [q.C.s2[d] for d in range(4)], "n")
+    bias_n = _gbox_off(q.N, [q.bias.s2[d] for d in range(4)], "n")
+    has_bias = bool(q.bias.ptr)
+    tanh = q.epilogue == 1
+    bias = f"Bp_[boff + {bias_n}]" if has_bias else "0.f"
+    act = "v = vm_tanh<float>(v);" if tanh else ""
+    lines = [
+        f"const rt_gemm_params& q = *(const rt_gemm_params*)(smem + {soff});",
+        f"const float* Ap = (const float*)q.A.ptr; const long long aoff = q.A.off{env_a};",
+        f"float* Cp = (float*)q.C.ptr; const long long coff = q.C.off{env_c};",
+        "const long long m0 = r0; const int mr = (int)(r1 > r0 ? r1 - r0 : 0);",
+        (f"const float* Bp_ = (const float*)q.bias.ptr; const long long boff = q.bias.off{env_bias};"
+         if has_bias else ""),
+        f"for (int i = threadIdx.x; i < {mrp * K}; i += blockDim.x) {{ const int r = i / {K}; "
+        f"const long long k = i - r * {K}; const long long m = m0 + r; "
+        f"sts1(sA32 + (uint32_t)((k * {mrp} + r) * 4), r < mr ? Ap[aoff + {a_m} + {a_k}] : 0.f); }}",
+        "__syncthreads();",
+        "PHASE(0);",
+        "cluster_sync_all();                     // partner's rows are staged",
+        "PHASE(1);",
+        "const uint32_t me = cluster_rank(), pr = me ^ 1u;",
+        f"const uint32_t kb = me * {kh}u;",
+        f"const uint32_t pA = smem_u32(smem + {pair['pa_off']}), pB = smem_u32(smem + {pair['b_off']}), "
+        f"pP = smem_u32(smem + {pair['p_off']});",
+        "const uint32_t rA = dsmem_map(sA32, pr);",
+        f"for (int i = threadIdx.x; i < {kh * mrp // 4}; i += blockDim.x) "
+        f"sts4(pA + 16u * (uint32_t)i, dsmem_ld4(rA + kb * {mrp * 4}u + 16u * (uint32_t)i));",
+        "__syncthreads();",
+        f"float ao[{mrp}], ap[{mrp}];",
+        f"#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) {{ ao[r] = 0.f; ap[r] = 0.f; }}",
+        f"const int col = threadIdx.x < {Nn} ? (int)threadIdx.x : {Nn - 1};",
+        "PHASE(2);",
+        f"pair_core<{mrp}, {kh}, {Nn}>(sA32 + kb * {mrp * 4}u, pA, pB, col, ao, ap);",
+        "__syncthreads(); PHASE(3);",
+        f"if (threadIdx.x < {Nn}) {{\n#pragma unroll\n  for (int r = 0; r < {mrp}; ++r) "
+        f"sts1(pP + (uint32_t)((r * {Nn} + col) * 4), ap[r]); }}",
+        "__syncthreads();",
+        "PHASE(4);",
+        "cluster_sync_all();                     // partner's partials for my rows",
+        "PHASE(5);",
+        "const uint32_t rP = dsmem_map(pP, pr);",
+        f"if (threadIdx.x < {Nn}) {{ const long long n = threadIdx.x; const float bias = {bias};",
+        f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
+        f"    float v = (ao[r] + dsmem_ld(rP + (uint32_t)((r * {Nn} + col) * 4))) + bias; {act}",
+        f"    Cp[coff + {c_m} + {c_n}] = v; }}",
+        "}",
+    ]
+    ph = ("#define PHASE(k) if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) "
+          f"{{ long long c1 = clock64(); ((long long*)p.prof)[{pair['nops']} + (k)] += c1 - c0; c0 = c1; }}"
+          if PHASES else "#define PHASE(k)")
+    lines.insert(0, ph)
+    lines.append("#undef PHASE")
+    return "    {  // gemm (CTA pair, resident weights)\n      " + "\n      ".join(
+        x for x in lines if x) + "\n    }"
 
 
 def _env_terms(coefs):
@@ -482,6 +582,8 @@ def ks_eligible(rows_per_cta, re, q, f64):
             and q.B.s2[0] == 1 and q.B.s1[0] == q.n and q.B.dtype == N.RT_F32)
 
 
+PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
+PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
 
 
@@ -571,7 +673,7 @@ def specialise(recs, kernels, params, labels, loop_info=None):
     for ri, info in (loop_info or {}).items():
         if params[ri].rows * info["trips"] < JIT_LOOP_MIN:
             continue
-        src = loop_source(params[ri], info["ops"], "loop_jit")
+        src = loop_source(params[ri], info["ops"], "loop_jit", info)
         recs[ri].jit_fn = compile_kernel(src, "loop_jit")
         n += 1
     for i, (k, p) in enumerate(zip(kernels, params)):

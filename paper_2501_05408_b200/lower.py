@@ -287,6 +287,7 @@ class Lowering:
         self.shard = shard
         self.shard_reduce = set(shard_reduce or ())
         self.hooks = []                        # all-reduce hooks (sharded reductions)
+        self.rec_cluster = {}                  # launch record -> cluster size (pair loops)
         self.swap = swap                       # swap.SwapPlan (time-blocked swapping)
         self._capture = None
         self.loop_subs = {}                    # loop record -> sub-op descriptors
@@ -535,6 +536,32 @@ class Lowering:
                         return None
         return S
 
+    PAIR_MIN_BYTES = 64 * 1024
+
+    def _pair_op(self, ops, R, rows, T, dim):
+        """Index of the in-loop GEMM to run in CTA-pair mode, or None: fp32,
+        one row per point, dense row-major B of >= 64 KB that does not move
+        with the loop dim, N <= 256, K even; the loop must be JIT-specialised
+        (the pair code exists only there)."""
+        from . import jit
+        if not (jit.ENABLED and jit.PAIR_ENABLED) or rows * T < jit.JIT_LOOP_MIN or R > 8:
+            return None
+        best, size = None, 0
+        for i, (kernel, p, re, f64, _) in enumerate(ops):
+            if kernel != N.RT_K_GEMM or f64 or re != 1:
+                continue
+            if any(g.dtype != N.RT_F32 for g in (p.A, p.B, p.C)):
+                continue
+            if not (p.N.nd == 1 and p.K.nd == 1 and p.z == 1 and p.B.s2[0] == 1
+                    and p.B.s1[0] == p.n and p.n <= 256 and p.k % 8 == 0):
+                continue
+            if p.B.off_env[self.slot[dim]] != 0 or (p.B.ptr + 4 * p.B.off) % 16:
+                continue
+            nb = p.k * p.n * 4
+            if nb >= self.PAIR_MIN_BYTES and nb > size:
+                best, size = i, nb
+        return best
+
     def _loop_persistent(self, s: Loop, S, blk=None):
         self._capture = []
         try:
@@ -598,7 +625,22 @@ class Lowering:
                 mrp = (R * re + 3) // 4 * 4
                 red_bytes = max(red_bytes, 8 * mrp * p.n * 4)
         red_off = (a_off + a_need + 127) // 128 * 128
-        ring_off = (red_off + red_bytes + 127) // 128 * 128
+        # CTA-pair mode (jit._gemm_pair_literal): the largest in-loop weight
+        # matrix stays resident, one K-half per SM of a 2-CTA cluster, instead
+        # of streaming through the ring from L2 every step
+        pair = self._pair_op(ops, R, rows, T, s.dim)
+        pair_info = None
+        pair_bytes = 0
+        if pair is not None:
+            q = ops[pair][1]
+            mrp = (R + 3) // 4 * 4
+            kh = q.k // 2
+            b_bytes, p_bytes, pa_bytes = kh * q.n * 4, mrp * q.n * 4, kh * mrp * 4
+            base = (red_off + red_bytes + 127) // 128 * 128
+            pair_info = {"op": pair, "kh": kh, "b_off": base, "p_off": base + b_bytes,
+                         "pa_off": base + b_bytes + p_bytes, "nops": len(ops)}
+            pair_bytes = b_bytes + p_bytes + pa_bytes
+        ring_off = (red_off + red_bytes + pair_bytes + 127) // 128 * 128
         stage = 0
         if tma:
             stage = 32 * 1024
@@ -659,9 +701,16 @@ class Lowering:
         for op, off in zip(ops, p_off):
             op.append(off)
         first = self.g.nodes[s.body[0].nid]
-        idx = self.add_rec(N.RT_K_LOOP, lp, [-(-rows // R), 1, 1], [256, 1, 1], smem,
+        nct = -(-rows // R)
+        if pair_info is not None:
+            nct += nct % 2
+            if smem > 225 * 1024:
+                raise LowerError("pair loop needs too much shared memory")
+        idx = self.add_rec(N.RT_K_LOOP, lp, [nct, 1, 1], [256, 1, 1], smem,
                            (first.id, f"loop[{s.dim}]"))
-        self.loop_subs[idx] = {"ops": ops, "trips": T}
+        self.loop_subs[idx] = {"ops": ops, "trips": T, "pair": pair_info}
+        if pair_info is not None:
+            self.rec_cluster[idx] = 2
 
     def _swap_hook(self, kind):
         self.hooks.append({"kind": kind, "slot": self.slot[self.swap.kb]})

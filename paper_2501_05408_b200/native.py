@@ -137,7 +137,7 @@ class rt_loop_params(C.Structure):
 
 class rt_launch_rec(C.Structure):
     _fields_ = [("kernel", i32), ("param_bytes", i32), ("params", u64), ("grid", i32 * 3),
-                ("block", i32 * 3), ("smem", i32), ("_pad", i32), ("jit_fn", u64)]
+                ("block", i32 * 3), ("smem", i32), ("cluster", i32), ("jit_fn", u64)]
 
 
 class rt_instr(C.Structure):

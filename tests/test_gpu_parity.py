@@ -133,3 +133,24 @@ def test_swapped_time_blocks_match_reference(name, bs):
     assert exe.swap_plan is not None and len(exe.swap_plan.keys) >= 2
     for k, want in c.outputs.items():
         assert_close(got[k], want, k)
+
+
+def test_pair_cluster_loop_matches_interpreter(monkeypatch):
+    """CTA-pair persistent loop (2-CTA clusters, resident K-halves of W2,
+    DSMEM exchange of operand rows and partial sums) reproduces the
+    interpreting loop kernel."""
+    from golden_cases import load_graph
+    from paper_2501_05408_b200 import execute, jit
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    bounds = {"I": 1, "B": 96, "T": 40}
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 1 << 40)
+    ref = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=2)
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 0)
+    monkeypatch.setattr(jit, "PAIR_ENABLED", True)
+    from paper_2501_05408_b200 import get_executable
+    g = load_graph("reinforce_mlp_c2")
+    exe, _ = get_executable(g, bounds, mlp_inputs(), 2)
+    assert any(info.get("pair") for info in exe.loop_info.values())
+    got = execute(g, bounds=bounds, inputs=mlp_inputs(), seed=2)
+    for k in ref:
+        np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)

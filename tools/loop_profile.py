@@ -23,7 +23,7 @@ exe, _ = get_executable(g, WL.bounds(B), inp, seed=0)
 for ri, info in exe.loop_info.items():
     lp = exe.recs[ri]
     params = exe._params[ri]
-    prof = torch.zeros(len(info["ops"]), dtype=torch.int64, device="cuda")
+    prof = torch.zeros(len(info["ops"]) + 16, dtype=torch.int64, device="cuda")
     params.prof = prof.data_ptr()
     exe.run(inp, graph=False)
     torch.cuda.synchronize()
@@ -31,13 +31,17 @@ for ri, info in exe.loop_info.items():
     exe.run(inp, graph=False)
     torch.cuda.synchronize()
     cyc = prof.cpu().tolist()
-    tot = sum(cyc)
+    tot = sum(cyc[:len(info["ops"])])
     print(f"loop record {ri}: rows={params.rows} rows_per_cta={params.rows_per_cta} "
           f"smem={params.smem_bytes} trips={info['trips']}")
     for (k, q, re, f64, noise, *_), c in zip(info["ops"], cyc):
         print(f"  {RF.FAMILY.get(k):6s} row_elems={re:5d} cycles/step={c / info['trips']:10.0f} "
               f"share={100 * c / max(1, tot):5.1f}%")
     print(f"  total cycles/step {tot / info['trips']:.0f}")
+    extra = cyc[len(info["ops"]):]
+    if any(extra):
+        print("  pair GEMM phases (cycles/step):",
+              [round(c / info["trips"]) for c in extra[:6]])
     params.prof = 0
 prof = exe.profile(inp)
 for r in sorted(prof, key=lambda r: -r["ms"])[:6]:
