@@ -308,8 +308,9 @@ def loop_source(lp, ops, name, info=None):
         # without rows (the grid is padded to an even CTA count)
         early = "  const long long r1c = r1 > r0 ? r1 : r0; (void)r1c;"
         pair_pro = _pair_prologue(lp, ops[pair["op"]][1], ops[pair["op"]][5], pair)
+    per_sm = (info or {}).get("ctas_per_sm", 1)
     return f"""#include "loop_lib.cuh"
-extern "C" __global__ void __launch_bounds__(256, 1) {name}(const __grid_constant__ rt_loop_params p) {{
+extern "C" __global__ void __launch_bounds__(256, {per_sm}) {name}(const __grid_constant__ rt_loop_params p) {{
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bars[RING];
   long long env[RT_MAXENV];
@@ -582,6 +583,7 @@ def ks_eligible(rows_per_cta, re, q, f64):
             and q.B.s2[0] == 1 and q.B.s1[0] == q.n and q.B.dtype == N.RT_F32)
 
 
+DUAL_ENABLED = os.environ.get("RTB200_LOOP_DUAL", "1") != "0"   # two loop CTAs per SM
 PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
 PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)

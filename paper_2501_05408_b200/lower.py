@@ -600,9 +600,18 @@ class Lowering:
                 raise LowerError("op family not supported inside a persistent loop")
         # rows per CTA: the specialised in-loop GEMMs hold <= 8 rows (jit.py
         # _gemm_call); spread rows evenly over the waves that needs
+        # JIT-specialised loops fit two CTAs per SM (<= 128 registers,
+        # <= 112 KB shared memory): twice the resident row groups, and two
+        # independent step chains interleaved on every SM
+        from . import jit as _jit
         rmax = max(1, 8 // max_m)
-        waves = -(-rows // (148 * rmax))
-        R = max(1, min(rmax, -(-rows // (148 * waves))))
+        # (only when one CTA per SM would need several waves: a single wave of
+        # 7-row CTAs is faster than two interleaved 4-row chains, C2 measured)
+        dual = (_jit.ENABLED and _jit.DUAL_ENABLED and rows * T >= _jit.JIT_LOOP_MIN
+                and rows > 148 * rmax)
+        slots = 148 * (2 if dual else 1)
+        waves = -(-rows // (slots * rmax))
+        R = max(1, min(rmax, -(-rows // (slots * waves))))
         a_need, tma = 0, False
         for kernel, p, re, f64, _ in ops:
             if kernel == N.RT_K_GEMM:
@@ -628,7 +637,7 @@ class Lowering:
         # CTA-pair mode (jit._gemm_pair_literal): the largest in-loop weight
         # matrix stays resident, one K-half per SM of a 2-CTA cluster, instead
         # of streaming through the ring from L2 every step
-        pair = self._pair_op(ops, R, rows, T, s.dim)
+        pair = None if dual else self._pair_op(ops, R, rows, T, s.dim)
         pair_info = None
         pair_bytes = 0
         if pair is not None:
@@ -642,11 +651,14 @@ class Lowering:
             pair_bytes = b_bytes + p_bytes + pa_bytes
         ring_off = (red_off + red_bytes + pair_bytes + 127) // 128 * 128
         stage = 0
+        budget = (112 if dual else 210) * 1024
         if tma:
             stage = 32 * 1024
-            while ring_off + 4 * stage > 210 * 1024 and stage > 4096:
+            while ring_off + 4 * stage > budget and stage > 4096:
                 stage //= 2
         smem = ring_off + 4 * stage
+        if dual and smem > budget:
+            dual = False
         if smem > 220 * 1024:
             raise LowerError("persistent loop needs too much shared memory")
         # hoist the env's data-independent normals out of the loop
@@ -708,7 +720,8 @@ class Lowering:
                 raise LowerError("pair loop needs too much shared memory")
         idx = self.add_rec(N.RT_K_LOOP, lp, [nct, 1, 1], [256, 1, 1], smem,
                            (first.id, f"loop[{s.dim}]"))
-        self.loop_subs[idx] = {"ops": ops, "trips": T, "pair": pair_info}
+        self.loop_subs[idx] = {"ops": ops, "trips": T, "pair": pair_info,
+                               "ctas_per_sm": 2 if dual else 1}
         if pair_info is not None:
             self.rec_cluster[idx] = 2
 

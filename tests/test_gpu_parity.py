@@ -147,6 +147,7 @@ def test_pair_cluster_loop_matches_interpreter(monkeypatch):
     ref = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=2)
     monkeypatch.setattr(jit, "JIT_LOOP_MIN", 0)
     monkeypatch.setattr(jit, "PAIR_ENABLED", True)
+    monkeypatch.setattr(jit, "DUAL_ENABLED", False)
     from paper_2501_05408_b200 import get_executable
     g = load_graph("reinforce_mlp_c2")
     exe, _ = get_executable(g, bounds, mlp_inputs(), 2)
