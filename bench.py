@@ -182,11 +182,7 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(seconds=12.0):
-    """Oracle port (reference_execute restated) on a bounded sample of the
-    same program at full width (H=256): C2 at E=4 envs x T=32 steps; PPO at
-    E=4 x T=16 with 2 epochs x 2 minibatches."""
-    from oracle.pdg_oracle import oracle_execute
+def _oracle_sample():
     g = load_graph()
     inputs = WL.inputs()
     if WL.ppo:
@@ -195,17 +191,49 @@ def cpu_baseline(seconds=12.0):
     else:
         B, T = 4, 32
         bounds = {"I": 1, "B": B, "T": T}
+    return g, inputs, bounds, B * T
+
+
+def _oracle_worker(args):
+    """One host process: run the oracle port on distinct seeds for `seconds`."""
+    wl, seconds, seed0 = args
+    global WL
+    WL = WORKLOADS[wl]
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle.pdg_oracle import oracle_execute
+    g, inputs, bounds, per = _oracle_sample()
     t0 = time.perf_counter()
     n = 0
     while True:
-        oracle_execute(g, bounds=bounds, inputs=inputs, seed=n)
+        oracle_execute(g, bounds=bounds, inputs=inputs, seed=seed0 + n)
         n += 1
         if time.perf_counter() - t0 > seconds:
             break
-    dt = time.perf_counter() - t0
-    return {"value": n * B * T / dt, "unit": "env-steps/s", "cores": 1, "kind": "port",
-            "sample": f"{n} x oracle_execute({bounds}, H=256) of the {WL.name} program, "
-                      f"{dt:.1f}s, single-threaded Python+numpy (reference_execute restated)"}
+    return n * per, time.perf_counter() - t0
+
+
+def cpu_baseline(seconds=12.0, processes=1):
+    """Oracle port (reference_execute restated, single-threaded Python +
+    numpy) on a bounded sample of the same program at full width (H=256):
+    C2 at E=4 envs x T=32 steps; PPO at E=4 x T=16 with 2 epochs x 2
+    minibatches.  processes > 1 runs that many independent samples in
+    parallel host processes (the reference arm: all host cores)."""
+    name = [k for k, v in WORKLOADS.items() if v is WL][0]
+    g, inputs, bounds, per = _oracle_sample()
+    if processes <= 1:
+        steps, dt = _oracle_worker((name, seconds, 0))
+        value = steps / dt
+    else:
+        import multiprocessing as mp
+        with mp.get_context("spawn").Pool(processes) as pool:
+            res = pool.map(_oracle_worker, [(name, seconds, 100000 * i) for i in range(processes)])
+        steps = sum(r[0] for r in res)
+        dt = max(r[1] for r in res)
+        value = sum(r[0] / r[1] for r in res)
+    return {"value": value, "unit": "env-steps/s", "cores": processes, "kind": "port",
+            "sample": f"{steps // per} x oracle_execute({bounds}, H=256) of the {WL.name} "
+                      f"program over {processes} process(es), {dt:.1f}s each, single-threaded "
+                      f"Python+numpy per process (reference_execute restated)"}
 
 
 def run_reference(args):
@@ -213,7 +241,8 @@ def run_reference(args):
     if rank != 0:
         return
     steps_total = args.warmup + args.steps
-    base = cpu_baseline(seconds=max(5.0, 2.0 * steps_total))
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    base = cpu_baseline(seconds=max(5.0, 2.0 * steps_total), processes=procs)
     line = {"impl": "reference", "metric": "env-steps/s per train iter",
             "value": base["value"], "unit": "env-steps/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,

@@ -32,6 +32,39 @@ CASES = {
 }
 
 
+def cpu_numpy_ms(name, bounds):
+    """The reference's numpy kernel for the same op on the host (one core):
+    `_k_discounted_cumsum` (reference runtime.py:133-146: acc = x[j] + g*acc
+    along the axis) for the scans, a fancy-index row gather for the
+    minibatch gather (runtime.py:161-179 rows mode)."""
+    import time
+    rng = np.random.default_rng(0)
+    if name.startswith("returns") or name.startswith("gae"):
+        E, T = bounds["B"], bounds["T"]
+        x = rng.standard_normal((E, T)).astype(np.float32)
+        if name == "gae_bt":
+            V = rng.standard_normal((E, T)).astype(np.float32)
+        t0 = time.perf_counter()
+        if name == "gae_bt":
+            Vn = np.concatenate([V[:, 1:], np.zeros((E, 1), np.float32)], axis=1)
+            x = x + np.float32(0.99) * Vn - V
+        g = np.float32(0.9405 if name == "gae_bt" else 0.99)
+        xt = np.moveaxis(x, 1, 0) if name != "returns_tb" else x.T
+        out = np.empty_like(xt)
+        acc = None
+        for j in reversed(range(xt.shape[0])):
+            acc = xt[j].copy() if acc is None else xt[j] + g * acc
+            out[j] = acc
+        return (time.perf_counter() - t0) * 1e3
+    M, U, B, T = bounds["M"], bounds["U"], bounds["B"], bounds["T"]
+    x = rng.standard_normal((B, T, 16)).astype(np.float32)
+    t0 = time.perf_counter()
+    idx = (np.arange(U)[None, :] * M + np.arange(M)[:, None])
+    y = x[idx] * np.float32(1.0)
+    del y
+    return (time.perf_counter() - t0) * 1e3
+
+
 def peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -74,10 +107,13 @@ def main():
                          "ms": round(ms, 4), "launches": r["count"]})
         tot = sum(r["ms"] for r in recs)
         gbs = algo / (tot / 1e3) / 1e9
+        cpu_ms = cpu_numpy_ms(name, bounds)
         print(json.dumps({"program": name, "bounds": bounds, "algorithmic_bytes": algo,
                           "ms": round(tot, 4), "achieved_gbs": round(gbs, 1),
                           "peak_gbs": hbm, "peak_source": src, "frac": round(gbs / hbm, 3),
-                          "kernels": recs}))
+                          "kernels": recs,
+                          "cpu_numpy": {"ms": round(cpu_ms, 2), "cores": 1,
+                                        "gbs": round(algo / (cpu_ms / 1e3) / 1e9, 2)}}))
         del exe
         torch.cuda.empty_cache()
 
