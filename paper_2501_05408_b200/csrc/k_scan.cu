@@ -251,7 +251,8 @@ template <typename T, bool STEP_MAJOR>
 __global__ void __launch_bounds__(SCAN_LB) k_scan_pipe(const __grid_constant__ rt_scan_params p) {
   using V = typename svec<T>::V;
   constexpr int VW = svec<T>::W;
-  constexpr int TC = 16 * VW;                  // steps per chunk
+  constexpr int VPL = 16;                      // vectors per line per chunk
+  constexpr int TC = VPL * VW;                 // steps per chunk
   constexpr int NVEC = SCAN_LB * TC / VW;      // vectors per stage (1024)
   constexpr int NV = NVEC / SCAN_LB;           // per thread (16)
   constexpr int VPR = SCAN_LB / VW;            // step-major: vectors per row of 64 lines
@@ -290,9 +291,9 @@ __global__ void __launch_bounds__(SCAN_LB) k_scan_pipe(const __grid_constant__ r
     for (int q = 0; q < NV; ++q) {
       const int v = tid + SCAN_LB * q;
       if (!STEP_MAJOR) {
-        const int ln = v >> 4, pc = v & 15;
+        const int ln = v / VPL, pc = v % VPL;
         const bool ok = ln < nl && pc * VW < cnt;
-        cp16(st + ln * 16 + (pc ^ (ln & 7)), X + ib[ok ? ln : 0] + (ok ? j0 + pc * VW : 0), ok);
+        cp16(st + ln * VPL + (pc ^ (ln & 7)), X + ib[ok ? ln : 0] + (ok ? j0 + pc * VW : 0), ok);
       } else {
         const int k = v / VPR, pc = v % VPR;
         const bool ok = k < cnt;
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(SCAN_LB) k_scan_pipe(const __grid_constant__ r
     __syncthreads();
     V* st = ring + (c % SCAN_NS) * NVEC;
     if (!STEP_MAJOR) {
-      V* row = st + tid * 16;
+      V* row = st + tid * VPL;
       const int nv = cnt / VW;
       if (p.reverse) {
         for (int pc = nv - 1; pc >= 0; --pc) {
@@ -363,9 +364,9 @@ __global__ void __launch_bounds__(SCAN_LB) k_scan_pipe(const __grid_constant__ r
     for (int q = 0; q < NV; ++q) {
       const int v = tid + SCAN_LB * q;
       if (!STEP_MAJOR) {
-        const int ln = v >> 4, pc = v & 15;
+        const int ln = v / VPL, pc = v % VPL;
         if (ln < nl && pc * VW < cnt)
-          __stcs(reinterpret_cast<V*>(Y + ob[ln] + j0 + pc * VW), st[ln * 16 + (pc ^ (ln & 7))]);
+          __stcs(reinterpret_cast<V*>(Y + ob[ln] + j0 + pc * VW), st[ln * VPL + (pc ^ (ln & 7))]);
       } else {
         const int k = v / VPR, pc = v % VPR;
         if (k < cnt) __stcs(reinterpret_cast<V*>(Y + ob[0] + pc * VW + (j0 + k) * so), st[v]);
@@ -374,6 +375,130 @@ __global__ void __launch_bounds__(SCAN_LB) k_scan_pipe(const __grid_constant__ r
     if (c + 2 < nch) issue(c + 2);
     cp_commit();
   }
+}
+
+RT_DEV float rn_add(float a, float b) { return __fadd_rn(a, b); }
+RT_DEV double rn_add(double a, double b) { return __dadd_rn(a, b); }
+RT_DEV float rn_sub(float a, float b) { return __fsub_rn(a, b); }
+RT_DEV double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+RT_DEV float rn_mul(float a, float b) { return __fmul_rn(a, b); }
+RT_DEV double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+
+// GAE-fused pipelined scan (line-major, reverse): two input rings (r and V),
+// the TD residual delta = (r + c * V[t+1]) - V is formed in the scan phase in
+// the program's precision with the reference's operation order (no FMA
+// contraction: numpy evaluates add(r, mul(Vn, c)) then sub(.., V)), V[t+1]
+// across a chunk boundary comes from the previously processed chunk (carried
+// per line), and the bootstrap value vb stands in for V[T].
+template <typename T>
+__global__ void __launch_bounds__(SCAN_LB) k_scan_gae(const __grid_constant__ rt_scan_params p) {
+  using V = typename svec<T>::V;
+  constexpr int VW = svec<T>::W;
+  constexpr int VPL = 8;                       // vectors per line per chunk
+  constexpr int TC = VPL * VW;
+  constexpr int NVEC = SCAN_LB * TC / VW;
+  constexpr int NV = NVEC / SCAN_LB;
+  extern __shared__ __align__(16) unsigned char sraw[];
+  V* ring = reinterpret_cast<V*>(sraw);                 // r: [NS][NVEC]
+  V* ring2 = ring + SCAN_NS * NVEC;                     // V: [NS][NVEC]
+  int64_t* ib = reinterpret_cast<int64_t*>(ring2 + SCAN_NS * NVEC);
+  int64_t* ib2 = ib + SCAN_LB;
+  int64_t* ob = ib2 + SCAN_LB;
+  const int tid = threadIdx.x;
+  const double g = p.gamma;
+  const T c = (T)p.gae_c;
+  const T* X = (const T*)p.in.ptr;
+  const T* X2 = (const T*)p.in2.ptr;
+  T* Y = (T*)p.out.ptr;
+  const int64_t L = p.box.ext[p.sdim];
+  const int64_t nch = (L + TC - 1) / TC;
+  const int64_t l0 = (int64_t)blockIdx.x * SCAN_LB;
+  const int nl = (int)(p.total_lines - l0 < SCAN_LB ? p.total_lines - l0 : SCAN_LB);
+  {
+    int64_t i0, o0, a, b, LL;
+    line_base(p, l0 + (tid < nl ? tid : 0), &i0, &o0, &a, &b, &LL);
+    ib[tid] = i0;
+    ob[tid] = o0;
+    // second input: same decomposition over its own strides
+    int64_t r = l0 + (tid < nl ? tid : 0), o2 = p.in2.off;
+    for (int d = p.box.nd - 1; d >= 0; --d) {
+      if (d == p.sdim) continue;
+      const int64_t e = p.box.ext[d], q = r / e;
+      o2 += (r - q * e) * p.in2.stride[d];
+      r = q;
+    }
+    ib2[tid] = o2;
+  }
+  __syncthreads();
+  auto chunk = [&](int64_t cc, int64_t& j0, int& cnt) {   // reverse order
+    const int64_t a = cc * TC, b = (cc + 1) * TC < L ? (cc + 1) * TC : L;
+    cnt = (int)(b - a);
+    j0 = L - b;
+  };
+  auto issue = [&](int64_t cc) {
+    int64_t j0;
+    int cnt;
+    chunk(cc, j0, cnt);
+    V* st = ring + (cc % SCAN_NS) * NVEC;
+    V* st2 = ring2 + (cc % SCAN_NS) * NVEC;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const int v = tid + SCAN_LB * q;
+      const int ln = v / VPL, pc = v % VPL;
+      const bool ok = ln < nl && pc * VW < cnt;
+      const int slot = ln * VPL + (pc ^ (ln & 7));
+      cp16(st + slot, X + ib[ok ? ln : 0] + (ok ? j0 + pc * VW : 0), ok);
+      cp16(st2 + slot, X2 + ib2[ok ? ln : 0] + (ok ? j0 + pc * VW : 0), ok);
+    }
+  };
+  issue(0);
+  cp_commit();
+  if (nch > 1) issue(1);
+  cp_commit();
+  double acc = 0.0;
+  T vnext = (T)p.gae_vb;
+  for (int64_t cc = 0; cc < nch; ++cc) {
+    int64_t j0;
+    int cnt;
+    chunk(cc, j0, cnt);
+    cp_wait<1>();
+    __syncthreads();
+    V* st = ring + (cc % SCAN_NS) * NVEC;
+    V* st2 = ring2 + (cc % SCAN_NS) * NVEC;
+    V* row = st + tid * VPL;
+    V* row2 = st2 + tid * VPL;
+    const int nv = cnt / VW;
+    for (int pc = nv - 1; pc >= 0; --pc) {
+      V* slot = row + (pc ^ (tid & 7));
+      T e[VW], w[VW];
+      sunpack(*slot, e);
+      sunpack(row2[pc ^ (tid & 7)], w);
+#pragma unroll
+      for (int q = VW - 1; q >= 0; --q) {
+        T d = rn_add(e[q], rn_mul(vnext, c));   // add(r, mul(Vn, c)), no contraction
+        d = rn_sub(d, w[q]);                    // sub(.., V)
+        vnext = w[q];
+        const double x = (double)d;
+        acc = (cc == 0 && pc == nv - 1 && q == VW - 1) ? x : x + g * acc;
+        e[q] = (T)acc;
+      }
+      *slot = spack(e);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const int v = tid + SCAN_LB * q;
+      const int ln = v / VPL, pc = v % VPL;
+      if (ln < nl && pc * VW < cnt)
+        __stcs(reinterpret_cast<V*>(Y + ob[ln] + j0 + pc * VW), st[ln * VPL + (pc ^ (ln & 7))]);
+    }
+    if (cc + 2 < nch) issue(cc + 2);
+    cp_commit();
+  }
+}
+
+extern "C" void* rt_kernel_scan_gae(int f64) {
+  return f64 ? (void*)k_scan_gae<double> : (void*)k_scan_gae<float>;
 }
 
 extern "C" void* rt_kernel_scan_tile(int f64) {

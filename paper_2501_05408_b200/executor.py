@@ -378,6 +378,100 @@ def find_gemm_epilogues(g: Graph, pshape, fixed_of, skip, ext=None):
     return res
 
 
+def _const_scalar(g, nid):
+    n = g.nodes[nid]
+    if n.kind != "const" or n.domain or tuple(n.out_shapes[0]) not in ((), (1,)):
+        return None
+    v = np.asarray(n.params["value"]).reshape(-1)
+    return float(v[0]) if v.size == 1 else None
+
+
+def find_gae_fusions(g: Graph, benv, alias, out_ids):
+    """dsum(delta[.., t:T]) with delta = r + c * Vn - V and Vn = (t == T-1 ?
+    vb : V[t+1]) (GAE(lambda) over the TD residual): one
+    scan kernel forms delta on the fly (csrc/k_scan.cu k_scan_gae).  Returns
+    {dsum id: info}; the delta chain (sub, add, mul, Vn) gets no storage."""
+    def root(k):
+        while k in alias:
+            k = alias[k]
+        return k
+
+    def single(nid):
+        return nid not in out_ids and len(g.out_edges(nid)) == 1
+
+    def ident(e):
+        src, snk = g.nodes[e.src], g.nodes[e.sink]
+        return e.psi is None and src.domain == snk.domain and \
+            e.phi == tuple(("sym", d, "loop") for d in src.domain)
+
+    res = {}
+    for s in g.sorted_nodes():
+        if s.kind != "discounted_sum" or s.params.get("reverse") or s.dtype not in ("f32", "f64"):
+            continue
+        ins = g.in_edges(s.id)
+        if len(ins) != 1 or ins[0].psi is not None:
+            continue
+        e = ins[0]
+        delta = g.nodes[e.src]
+        if delta.kind != "sub" or delta.domain != s.domain or not single(delta.id) or \
+                not s.domain or s.params.get("dim") != 0:
+            continue
+        d = s.domain[-1]
+        bound = g.dim_bound[d]
+        want = tuple(("sym", x, "loop") for x in s.domain[:-1]) + (
+            ("slice", ("sym", d, "loop"), ("sym", bound, "bound")),)
+        if e.phi != want or delta.dtype != s.dtype:
+            continue
+        a_e, z_e = g.in_edges(delta.id)
+        A = g.nodes[a_e.src]
+        if A.kind != "add" or not ident(a_e) or not ident(z_e) or not single(A.id):
+            continue
+        found = None
+        for x_e, m_e in (tuple(g.in_edges(A.id)), tuple(reversed(g.in_edges(A.id)))):
+            M = g.nodes[m_e.src]
+            if M.kind != "mul" or not ident(x_e) or not ident(m_e) or not single(M.id):
+                continue
+            for v_e, c_e in (tuple(g.in_edges(M.id)), tuple(reversed(g.in_edges(M.id)))):
+                c = _const_scalar(g, c_e.src)
+                Vn = g.nodes[v_e.src]
+                if c is None or Vn.kind != "merge" or not ident(v_e) or not single(Vn.id):
+                    continue
+                conds = Vn.params["conds"]
+                if len(conds) != 2 or conds[1] != ir.TRUE:
+                    continue
+                c0 = subst_bounds(conds[0], benv)
+                aff = ir.as_affine(("sub", c0[1], c0[2])) if c0[0] == "eq" else None
+                if aff is None or not (
+                        (aff[0] == {(d, "loop"): 1} and aff[1] == -(benv[bound] - 1))
+                        or (aff[0] == {(d, "loop"): -1} and aff[1] == benv[bound] - 1)):
+                    continue
+                b0, b1 = g.in_edges(Vn.id)
+                vb = _const_scalar(g, b0.src)
+                shifted = tuple(("sym", x, "loop") for x in s.domain[:-1]) + (
+                    ("add", ("sym", d, "loop"), ("int", 1)),)
+                sh = ir.as_affine(subst_bounds(b1.phi[-1], benv))
+                # (branch edges may carry their merge condition as a guard:
+                # implied by the merge, reference runtime.py:362-371)
+                if vb is None or sh != ({(d, "loop"): 1}, 1) or b1.phi[:-1] != shifted[:-1]:
+                    continue
+                if root((b1.src, b1.oid)) != root((z_e.src, z_e.oid)):
+                    continue
+                found = (x_e, c, vb, M.id, Vn.id)
+                break
+            if found:
+                break
+        if not found:
+            continue
+        x_e, c, vb, mid, vnid = found
+        T = benv[bound]
+        vw = 2 if s.dtype == "f64" else 4
+        if T % vw:
+            continue
+        res[s.id] = {"x": x_e, "z": z_e, "c": c, "vb": vb,
+                     "nodes": {delta.id, A.id, mid, vnid}}
+    return res
+
+
 def find_ew_fusions(g: Graph, pshape, skip):
     """Single-consumer pointwise producers inlined into their consumer's
     program (one launch, no intermediate buffer)."""
@@ -493,6 +587,11 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
         taken.add(x)
         if t:
             taken.add(g.in_edges(f)[0].src)
+    gae = find_gae_fusions(g, benv, alias, {nid for _, nid, _ in g.outputs}) if fuse else {}
+    for info in gae.values():
+        taken |= info["nodes"]
+        virtual |= info["nodes"]
+    plan.gae = gae
     fuse_src = find_ew_fusions(g, pshape, taken) if fuse else {}
     virtual |= set(fuse_src)
     for f, (x, _b, t) in gemm_epi.items():
@@ -509,7 +608,8 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
         for key, dims in find_folds(g, bufs, fixed_of, virtual, ext).items():
             bufs[key].folded = dims
     return {"contract": contract, "alias": alias, "plan": plan, "gemm_epi": gemm_epi,
-            "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs, "absorbed": absorbed}
+            "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs, "absorbed": absorbed,
+            "gae": gae}
 
 
 def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, depth=0):

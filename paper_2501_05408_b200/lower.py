@@ -294,6 +294,8 @@ class Lowering:
         self.fuse_src = dict(fuse_src or {})   # producer nid -> consumer nid (inlined)
         self.gemm_epi = dict(gemm_epi or {})   # final nid -> (matmul nid, bias edge, tanh)
         self.virtual |= set(self.fuse_src)
+        for info in getattr(plan, "gae", {}).values():
+            self.virtual |= info["nodes"]          # delta chain formed inside the scan
         for f, (x, _b, t) in self.gemm_epi.items():
             self.virtual.add(x)
             if t:
@@ -1122,6 +1124,9 @@ class Lowering:
 
     def k_discounted_sum(self, ctx: Ctx):
         n = ctx.node
+        gae = getattr(self.plan, "gae", {}).get(n.id)
+        if gae is not None:
+            return self._gae_scan(ctx, gae)
         (e,) = self.g.in_edges(n.id)
         ev = self.edge_val(ctx, e)
         ax = n.params["dim"]
@@ -1372,6 +1377,45 @@ class Lowering:
 
     SCAN_STAGES = 3
 
+    def _gae_scan(self, ctx, info):
+        """A = dsum(delta[t:T]) with delta = r + c*V[t+1] - V formed inside
+        the scan (executor.find_gae_fusions, csrc/k_scan.cu k_scan_gae)."""
+        n = ctx.node
+        key = (n.id, 0)
+        delta = self.g.nodes[info["x"].sink]
+        dctx = Ctx(self, delta, ctx.fixed)
+        p = N.rt_scan_params()
+        box = list(ctx.slab_ext)
+        p.box.nd = len(box)
+        for i, x in enumerate(box):
+            p.box.ext[i] = x
+        p.sdim = len(ctx.slab) - 1
+        if ctx.slab[-1] != n.domain[-1]:
+            raise LowerError("GAE scan over a fixed dim")
+        p.reverse = 1
+        p.gamma = float(n.params["gamma"])
+        ob = self.storage(key)
+        p.f64 = 1 if ob.dtype == "f64" else 0
+        p.total_lines = prod(box) // box[p.sdim]
+        rx = self.edge_val(dctx, info["x"])
+        vz = self.edge_val(dctx, info["z"])
+        for ev in (rx, vz):
+            if ev.progs or ev.checks or _ragged(ev) or ev.buf.dtype != ob.dtype:
+                raise LowerError("GAE scan operand needs a gather")
+        p.in_ = self.make_view(dctx, rx, [])
+        p.in2 = self.make_view(dctx, vz, [])
+        p.out = self.out_view(ctx, key)
+        p.gae, p.gae_c, p.gae_vb = 1, info["c"], info["vb"]
+        vw, esize = (2, 8) if p.f64 else (4, 4)
+        for v in (p.in_, p.in2, p.out):
+            if v.stride[p.sdim] != 1 or (v.ptr + esize * v.off) % 16 or \
+                    any(v.off_env[e] % vw for e in range(N.RT_MAXENV)) or \
+                    any(v.stride[d] % vw for d in range(p.box.nd) if d != p.sdim and box[d] > 1):
+                raise LowerError("GAE scan operands are not line-major and 16-B aligned")
+        smem = 2 * self.SCAN_STAGES * 64 * 8 * 16 + 3 * 64 * 8      # k_scan_gae: 8 vectors/line
+        self.add_rec(N.RT_K_SCAN, p, [-(-p.total_lines // 64), 1, 1], [64, 1, 1], smem,
+                     (n.id, n.name))
+
     def _scan_launch(self, p, label):
         """Pick the scan kernel (csrc/k_scan.cu): tiled 64-line CTAs with
         16-byte I/O for contiguous lines whose starts and length are
@@ -1392,7 +1436,7 @@ class Lowering:
                        if d not in skip and p.box.ext[d] > 1)
 
         L = p.box.ext[sd]
-        smem = self.SCAN_STAGES * 64 * 16 * 16 + 2 * 64 * 8
+        smem = self.SCAN_STAGES * 64 * 16 * 16 + 2 * 64 * 8         # 16 vectors per line
         lines = [d for d in range(p.box.nd) if d != sd and p.box.ext[d] > 1]
         inner = lines[-1] if lines else None
         nblk = -(-p.total_lines // 64)

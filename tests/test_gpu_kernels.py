@@ -258,3 +258,24 @@ def test_gathered_rows_small_k_gemm(K, N, dt):
     want = xs @ W.astype(np.float64)
     tol = 1e-5 if dt == "f32" else 1e-12
     np.testing.assert_allclose(out, want, rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("B,T", [(4096, 512), (100, 36), (64, 4)])
+def test_gae_fused_scan(B, T):
+    """A = dsum(delta[t:T], gamma*lam) with delta = r + 0.99*V[t+1] - V
+    (bootstrap 0) formed inside the scan kernel (k_scan_gae) == numpy: the
+    residual in float32 with numpy's operation order, the discounted sum
+    in float64."""
+    from golden_cases import load_graph
+    rng = np.random.default_rng(B + T)
+    r = rng.standard_normal((B, T)).astype(np.float32)
+    V = rng.standard_normal((B, T)).astype(np.float32)
+    out = execute(load_graph("k_gae_bt"), bounds={"B": B, "T": T}, inputs={"r": r, "V": V})["A"]
+    Vn = np.concatenate([V[:, 1:], np.zeros((B, 1), np.float32)], axis=1)
+    delta = (r + Vn * np.float32(0.99)) - V
+    want = np.zeros((B, T))
+    acc = np.zeros(B)
+    for t in reversed(range(T)):
+        acc = delta[:, t].astype(np.float64) + (0.99 * 0.95 * acc if t < T - 1 else 0.0)
+        want[:, t] = acc
+    np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-5)

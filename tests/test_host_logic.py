@@ -245,3 +245,14 @@ def test_swap_plan_manages_acting_activations():
     names = {h.nodes[k[0]].name for k in sp.keys}
     assert {"h1", "h2"} <= names and "o" not in names
     assert sp.DI == 10 and sp.bs == 10000
+
+
+def test_gae_delta_fused_into_the_scan():
+    """GAE: delta = r + gamma*V[t+1] - V is formed inside the scan kernel (no
+    delta buffer) for the kernel program and for the PPO program."""
+    for name, benv in (("k_gae_bt", {"B": 4096, "T": 512}), ("ppo_c3", PPO_BOUNDS)):
+        g = load_graph(name)
+        plan, low, _, _ = dry_lower(g, benv)
+        scans = [p for (k, p, *_r) in low.recs if k == N.RT_K_SCAN]
+        assert any(p.gae for p in scans), name
+        assert not any(lab[1] == "delta" for (*_r, lab) in low.recs), name
