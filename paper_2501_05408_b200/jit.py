@@ -22,6 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CACHE = os.environ.get("RTB200_JIT_CACHE", os.path.join(os.path.expanduser("~"), ".cache",
                                                         "rtb200_jit"))
 JIT_MIN_ELEMS = int(os.environ.get("RTB200_JIT_MIN", str(1 << 18)))
+EW_UNROLL = int(os.environ.get("RTB200_EW_UNROLL", "4"))
 JIT_LOOP_MIN = int(os.environ.get("RTB200_JIT_LOOP_MIN", str(1 << 16)))   # rows x trips
 ENABLED = os.environ.get("RTB200_JIT", "1") != "0"
 
@@ -209,10 +210,26 @@ def ew_source(p, name):
     store = _store(p, T, nd, "p.out.off")
     regs = ", ".join(f"v{i}" for i in range(8))
     iregs = ", ".join(f"n{i}" for i in range(8))
+    # EW_UNROLL elements per thread, blockDim apart (coalescing unchanged):
+    # every element's loads and arithmetic are issued before any store, so
+    # EW_UNROLL independent load streams per thread are in flight
+    U = EW_UNROLL
+    out_off = _offset_expr("p.out.off", p.out, nd)
+    oct_ = CT[p.out.dtype]
+    st = (f"((unsigned char*)p.out.ptr)[oo[q]] = rr[q] != ({T})0;" if p.out.dtype == N.RT_BOOL
+          else f"(({oct_}*)p.out.ptr)[oo[q]] = ({oct_})rr[q];")
+    del store
     return f"""#include "common.cuh"
 extern "C" __global__ void __launch_bounds__(256) {name}(const __grid_constant__ rt_ew_params p) {{
-  for (long long flat = (long long)blockIdx.x * 256 + threadIdx.x; flat < {total}LL;
-       flat += (long long)gridDim.x * 256) {{
+  for (long long b0 = (long long)blockIdx.x * {256 * U} + threadIdx.x; b0 < {total}LL;
+       b0 += (long long)gridDim.x * {256 * U}) {{
+    {T} rr[{U}];
+    long long oo[{U}];
+#pragma unroll
+    for (int q = 0; q < {U}; ++q) {{
+      const long long flat = b0 + q * 256LL;
+      oo[q] = -1;
+      if (flat >= {total}LL) continue;
       {dec_s}
       {T} {regs};
       long long {iregs};
@@ -220,7 +237,12 @@ extern "C" __global__ void __launch_bounds__(256) {name}(const __grid_constant__
       (void)n0;
       {body}
     Lend:
-      {store}
+      rr[q] = res;
+      oo[q] = {out_off};
+    }}
+#pragma unroll
+    for (int q = 0; q < {U}; ++q)
+      if (oo[q] >= 0) {st}
   }}
 }}
 """
