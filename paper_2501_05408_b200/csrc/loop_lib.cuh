@@ -779,6 +779,82 @@ RT_DEV void pair_core(uint32_t sA_own, uint32_t sA_par, uint32_t sB, int col, fl
   }
 }
 
+// ---------------------------------------------------------------- warp MMA
+// 3xTF32 warp-level tensor-core core for the in-loop GEMM: few rows (<= 8,
+// padded to the m16 tile), wide N.  C = A_hi B_hi + A_hi B_lo + A_lo B_hi
+// with mma.sync.m16n8k8 tf32 (fp32 accumulate): the dropped A_lo B_lo term
+// is ~2^-22 relative, i.e. fp32-grade products for the 1e-5 parity bar.
+// Warp w owns columns [w*N/8, (w+1)*N/8) as N/64 n8 tiles; rows 8..15 of
+// the A tile are zero (R <= 8), so only c0/c1 (row g = lane/4) are kept.
+RT_DEV uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+RT_DEV void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = tf32_rna(x);
+  lo = tf32_rna(x - __uint_as_float(hi));
+}
+RT_DEV void mma_tf32(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  // A rows 8..15 (a1, a3) are the zero padding of an 8-row block
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// acc[j][0..1] = C[row g][n0_j + 2t + {0,1}] for the warp's NT = N/64 tiles
+template <int MRP, int K, int N, int KC>
+RT_DEV void mma_core(const float* Bg, uint32_t sA, loop_ring& ring, float (&acc)[N / 64][4]) {
+  static_assert(MRP == 8 && N % 64 == 0 && K % 8 == 0 && KC % 8 == 0, "mma core shape");
+  constexpr int NCH = (K + KC - 1) / KC;
+  constexpr int NT = N / 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nw0 = warp * (N / 8);
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
+  const uint32_t ring_base = smem_u32(ring.buf);
+  for (int c = 0; c < NCH; ++c) {
+    const uint32_t gq = ring.seq + (uint32_t)c;
+    const uint32_t st = gq % RING;
+    mbar_wait(&ring.bar[st], (gq / RING) & 1);
+    const uint32_t bs = ring_base + st * ring.stage_bytes;
+    const int rows = (c + 1) * KC <= K ? KC : K - c * KC;
+    const uint32_t ak = sA + (uint32_t)(c * KC * MRP * 4);
+#pragma unroll 2
+    for (int k8 = 0; k8 < rows; k8 += 8) {
+      // A[row g][k8 + t], A[row g][k8 + t + 4]   (sA is k-major [k][MRP])
+      uint32_t ah0, al0, ah2, al2;
+      split_tf32(lds1(ak + (uint32_t)(((k8 + t) * MRP + g) * 4), 0.f), ah0, al0);
+      split_tf32(lds1(ak + (uint32_t)(((k8 + t + 4) * MRP + g) * 4), 0.f), ah2, al2);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int n = nw0 + j * 8 + g;
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(lds1(bs + (uint32_t)(((k8 + t) * N + n) * 4), 0.f), bh0, bl0);
+        split_tf32(lds1(bs + (uint32_t)(((k8 + t + 4) * N + n) * 4), 0.f), bh1, bl1);
+        mma_tf32(acc[j], ah0, ah2, bl0, bl1);
+        mma_tf32(acc[j], al0, al2, bh0, bh1);
+        mma_tf32(acc[j], ah0, ah2, bh0, bh1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && c + RING < NCH) {
+      const int cc = c + RING;
+      const uint32_t st2 = (ring.seq + (uint32_t)cc) % RING;
+      const int rows2 = (cc + 1) * KC <= K ? KC : K - cc * KC;
+      const uint32_t bytes = (uint32_t)(rows2 * N * 4);
+      mbar_expect_tx(&ring.bar[st2], bytes);
+      bulk_g2s(ring.buf + (size_t)st2 * ring.stage_bytes, Bg + (size_t)cc * KC * N, bytes, &ring.bar[st2]);
+    }
+  }
+  ring.seq += NCH;
+}
+
 // ---------------------------------------------------------------- JIT cores
 // Raw-pointer cores: all descriptor values are supplied by the generated code
 // as literals or registers, so nothing is re-read from shared memory after a

@@ -213,7 +213,7 @@ def ew_source(p, name):
     # EW_UNROLL elements per thread, blockDim apart (coalescing unchanged):
     # every element's loads and arithmetic are issued before any store, so
     # EW_UNROLL independent load streams per thread are in flight
-    U = EW_UNROLL
+    U = EW_UNROLL if p.nin <= 2 else 1     # (measured: wider bodies lose to register pressure)
     out_off = _offset_expr("p.out.off", p.out, nd)
     oct_ = CT[p.out.dtype]
     st = (f"((unsigned char*)p.out.ptr)[oo[q]] = rr[q] != ({T})0;" if p.out.dtype == N.RT_BOOL
@@ -511,6 +511,21 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
                   f"    {T} v = o[q] + bias;" + (f" v = vm_tanh<{T}>(v);" if tanh else ""),
                   f"    Cp[coff + {c_m} + {c_n}] = v; }}",
                   "}"]
+    elif tma and MMA_ENABLED and not f64 and mrp == 8 and Nn % 64 == 0 and K % 8 == 0 \
+            and kc % 8 == 0:
+        nt = Nn // 64
+        lines.append(f"float acc[{nt}][4];")
+        lines.append(f"mma_core<{mrp}, {K}, {Nn}, {kc}>(Bg, sA32, ring, acc);")
+        lines += ["const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;",
+                  f"const int nw0 = (int)(threadIdx.x >> 5) * {Nn // 8};",
+                  "if (g < mr) { const long long m = m0 + g;",
+                  f"  #pragma unroll\n  for (int j = 0; j < {nt}; ++j) {{",
+                  "    #pragma unroll\n    for (int h = 0; h < 2; ++h) {",
+                  "      const long long n = nw0 + j * 8 + 2 * t4 + h;",
+                  f"      const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
+                  "      float v = acc[j][h] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
+                  f"      Cp[coff + {c_m} + {c_n}] = v; }} }}",
+                  "}"]
     elif tma:
         lines.append(f"{T} acc[{nc}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = ({T})0; }}")
@@ -606,6 +621,7 @@ def ks_eligible(rows_per_cta, re, q, f64):
 
 
 DUAL_ENABLED = os.environ.get("RTB200_LOOP_DUAL", "1") != "0"   # two loop CTAs per SM
+MMA_ENABLED = os.environ.get("RTB200_LOOP_MMA", "0") == "1"     # 3xTF32 mma.sync in-loop GEMMs (measured slower: 18.5k vs 15.6k cycles for h2)
 PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
 PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)

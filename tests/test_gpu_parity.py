@@ -155,3 +155,23 @@ def test_pair_cluster_loop_matches_interpreter(monkeypatch):
     got = execute(g, bounds=bounds, inputs=mlp_inputs(), seed=2)
     for k in ref:
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
+
+
+def test_mma_loop_kernel_matches_interpreter(monkeypatch):
+    """8-row CTAs (E=1024): the in-loop layers run on the 3xTF32 warp MMA
+    core (loop_lib.cuh mma_core) and match the interpreting loop kernel."""
+    from golden_cases import load_graph
+    from paper_2501_05408_b200 import execute, get_executable, jit
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    bounds = {"I": 1, "B": 1024, "T": 12}
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 1 << 40)
+    ref = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=4)
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 0)
+    monkeypatch.setattr(jit, "MMA_ENABLED", True)
+    g = load_graph("reinforce_mlp_c2")
+    exe, _ = get_executable(g, bounds, mlp_inputs(), 4)
+    lp = [exe._params[ri] for ri in exe.loop_info][0]
+    assert lp.rows_per_cta == 7
+    got = execute(g, bounds=bounds, inputs=mlp_inputs(), seed=4)
+    for k in ref:
+        np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
