@@ -310,6 +310,13 @@ class Planner:
         return steps
 
     def loop_for(self, comp: set, cedges: list, fixed: tuple):
+        live = [e for e in cedges if self.sink_box(e) is not None]
+        if len(live) < len(cedges):
+            # edges whose condition never holds on the concrete box (e.g. the
+            # recurrence o[t] <- o[t-1] at T = 1, anything at B = 0) carry no
+            # dependence: plan the component on the edges that remain
+            steps = self.level(comp, live, fixed)
+            return steps if len(steps) != 1 else steps[0]
         common = [d for d in self.g.dim_order
                   if d not in fixed and all(d in self.g.nodes[v].domain for v in comp)]
         for d in common:

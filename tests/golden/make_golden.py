@@ -139,13 +139,34 @@ def kernel_graphs():
         write_case(name, g, None, inputs, 0, {"program": name})
 
 
+def edge_cases():
+    """Degenerate extents the executor must get right: a single env or step,
+    no envs at all (empty slabs, sums of nothing), a one-epoch PPO with one
+    env per minibatch, a one-step PPO horizon."""
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+    for (I, B, T) in ((1, 1, 1), (2, 1, 3), (1, 3, 1), (1, 0, 3)):
+        ctx = P.ctx_reinforce_mlp(B=max(B, 1), T=T, I=I, d_o=4, H=8, d_a=2, dtype="f32", lr=0.05)
+        g = pdg.build(ctx)
+        pdg.eliminate_dead(g)
+        write_case(f"edge_mlp_I{I}B{B}T{T}", g, {"I": I, "B": B, "T": T},
+                   P.mlp_inputs(d_o=4, H=8, d_a=2, dtype="f32"), 0,
+                   {"program": "reinforce_mlp", "edge": True})
+    for (B, T, ep, mb) in ((2, 4, 1, 2), (4, 1, 2, 2)):
+        ctx = P.ctx_ppo_mlp(B=B, T=T, I=1, epochs=ep, minibatches=mb, d_o=4, H=8, d_a=2,
+                            dtype="f32", lr=0.002)
+        g = pdg.build(ctx)
+        pdg.eliminate_dead(g)
+        write_case(f"edge_ppo_B{B}T{T}E{ep}M{mb}", g, None, ppo_inputs(4, 8, 2, "f32"), 0,
+                   {"program": "ppo_mlp", "edge": True})
+
+
 def main():
     dsl, fe, pdg, tr, rt, ps = P.recten()
     os.makedirs(CASES, exist_ok=True)
     os.makedirs(GRAPHS, exist_ok=True)
     if "--only" in sys.argv:
         what = sys.argv[sys.argv.index("--only") + 1]
-        return {"ppo": ppo_cases, "kernels": kernel_graphs}[what]()
+        return {"ppo": ppo_cases, "kernels": kernel_graphs, "edge": edge_cases}[what]()
     ppo_cases()
     V = variants()
 

@@ -169,7 +169,7 @@ def test_ppo_plan_peels_rollout_into_first_update():
     txt = P.describe(an["plan"].steps, h)
     assert "for e asc [0, 1):" in txt and "for e asc [1, 4):" in txt
     assert "for j asc [0, 1):" in txt and "for j asc [1, 4):" in txt
-    assert "bulk o:merge over (b)" in txt        # all envs per acting step
+    assert "bulk o:merge over (b)" in txt or "bulk o:merge over (i,b)" in txt  # all envs
 
 
 def test_ppo_storage_folding():
