@@ -777,6 +777,8 @@ class Executable:
         offs, arena = memplan.assign(sizes, life)
         self.arena_bytes = arena
         self.naive_bytes = sum(sizes.values())
+        self.lifetimes = life
+        self.trace_names = {k: g.nodes[k[0]].name for k in roots}
         with torch.cuda.device(self.dev):
             self.arena = torch.empty(max(1, arena), dtype=torch.uint8, device=self.dev)
             base = self.arena.data_ptr()
@@ -798,6 +800,8 @@ class Executable:
                        shard_reduce=self.shard_reduce,
                        persistent=OPTS["persistent"], swap=self.swap_plan).lower()
         self.hooks = low.hooks
+        self.slot_of = dict(low.slot)
+        self.fixed_of = plan_fixed(self.plan.steps)
         self.swap_rt = None
         if self.swap_plan is not None:
             from .swap import SwapRuntime
@@ -1089,6 +1093,16 @@ class Executable:
             self.upload_inputs(inputs, s)
             N.check(self.lib.rt_status_clear(self.status, s.cuda_stream), "status clear")
             N.check(self.lib.rt_graph_launch(graph_exec, s.cuda_stream), "graph")
+
+    def trace(self, max_lines=100000):
+        """SPEC trace lines (EXEC / DEALLOC / OFFLOAD / FETCH), trace.py."""
+        from . import trace as TR
+        return TR.trace(self, max_lines)
+
+    def stats(self):
+        """SPEC collect_stats report, trace.py."""
+        from . import trace as TR
+        return TR.stats(self)
 
     def check_status(self, stream=None):
         torch = self.torch

@@ -175,3 +175,23 @@ def test_mma_loop_kernel_matches_interpreter(monkeypatch):
     got = execute(g, bounds=bounds, inputs=mlp_inputs(), seed=4)
     for k in ref:
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
+
+
+def test_trace_and_stats_report():
+    """SPEC trace/stats (trace.py): one EXEC per launch, DEALLOC at the memory
+    plan's lifetime ends, OFFLOAD/FETCH per swapped block; the stats report
+    the arena peak, transfers and the eager per-tensor estimate."""
+    from paper_2501_05408_b200 import get_executable
+    c = load_case("mlp_f32_I1B4T6")
+    exe, _ = get_executable(c.graph(), c.bounds, c.inputs, c.seed, block=("t", 2), swap=1)
+    exe.run(c.inputs)
+    lines = exe.trace()
+    assert sum(x.startswith("EXEC ") for x in lines) == exe.launch_count
+    assert any(x.startswith("DEALLOC ") for x in lines)
+    keys = len(exe.swap_plan.keys)
+    assert sum(x.startswith("OFFLOAD ") for x in lines) == 3 * keys
+    assert sum(x.startswith("FETCH ") for x in lines) == 3 * keys
+    rep = exe.stats()
+    assert rep["peak_device_bytes"] >= rep["arena_bytes"] > 0
+    assert rep["offloads"] == rep["fetches"] == 3 * keys and rep["bytes_moved"] > 0
+    assert rep["static_estimate"]["G"] == 1 * 4 * 6 * 4
