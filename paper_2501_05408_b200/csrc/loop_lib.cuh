@@ -987,6 +987,64 @@ RT_DEV void tma_core_ks(const T* Bg, uint32_t sA, loop_ring& ring, uint32_t red,
   }
 }
 
+// NCOL adjacent columns per thread (threads < N/NCOL compute, the rest
+// only join the barriers): per k one NCOL*4-byte B load and MRP/4 16-byte A
+// loads feed NCOL*MRP FMAs (the column-per-thread core is shared-memory-issue
+// bound at 1 B + MRP/4 A loads per MRP FMAs).
+template <int MRP, int K, int N, int KC, int NCOL>
+RT_DEV void tma_core2(const float* Bg, uint32_t sA, loop_ring& ring, float (&acc)[NCOL][MRP]) {
+  constexpr int NCH = (K + KC - 1) / KC;
+  const bool act = (int)threadIdx.x < N / NCOL;
+  const int c0 = act ? NCOL * (int)threadIdx.x : 0;
+  const uint32_t ring_base = smem_u32(ring.buf);
+  for (int c = 0; c < NCH; ++c) {
+    const uint32_t g = ring.seq + (uint32_t)c;
+    const uint32_t st = g % RING;
+    mbar_wait(&ring.bar[st], (g / RING) & 1);
+    const uint32_t bs = ring_base + st * ring.stage_bytes;
+    const int rows = (c + 1) * KC <= K ? KC : K - c * KC;
+    const uint32_t ak = sA + (uint32_t)(c * KC * MRP * 4);
+    if (act) {
+#pragma unroll 2
+      for (int kk = 0; kk < rows; kk += 4) {
+        float b[4][NCOL];
+        float a[4][MRP];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t ba = bs + (uint32_t)(((kk + u) * N + c0) * 4);
+          if (kk + u < rows) {
+            if constexpr (NCOL == 4)
+              asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                           : "=f"(b[u][0]), "=f"(b[u][1]), "=f"(b[u][2]), "=f"(b[u][3]) : "r"(ba));
+            else
+              asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(b[u][0]), "=f"(b[u][1]) : "r"(ba));
+          } else {
+#pragma unroll
+            for (int j = 0; j < NCOL; ++j) b[u][j] = 0.f;
+          }
+          lds_rows<MRP>(ak + (uint32_t)((kk + u) * MRP * 4), a[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int r = 0; r < MRP; ++r)
+#pragma unroll
+            for (int j = 0; j < NCOL; ++j) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && c + RING < NCH) {
+      const int cc = c + RING;
+      const uint32_t st2 = (ring.seq + (uint32_t)cc) % RING;
+      const int rows2 = (cc + 1) * KC <= K ? KC : K - cc * KC;
+      const uint32_t bytes = (uint32_t)(rows2 * N * 4);
+      mbar_expect_tx(&ring.bar[st2], bytes);
+      bulk_g2s(ring.buf + (size_t)st2 * ring.stage_bytes, Bg + (size_t)cc * KC * N, bytes, &ring.bar[st2]);
+    }
+  }
+  ring.seq += NCH;
+}
+
 template <typename T, int K, int N, int KC>
 RT_DEV void tma_prefetch(const T* Bg, loop_ring& ring) {
   constexpr int NCH = (K + KC - 1) / KC;

@@ -526,6 +526,20 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
                   "      float v = acc[j][h] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
                   f"      Cp[coff + {c_m} + {c_n}] = v; }} }}",
                   "}"]
+    elif tma and CORE2_NCOL > 1 and not f64 and Nn % CORE2_NCOL == 0 and \
+            Nn <= 256 * CORE2_NCOL and kc % 4 == 0 and K >= 64:
+        nc2 = CORE2_NCOL
+        lines.append(f"float acc[{nc2}][{mrp}];")
+        lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
+        lines.append(f"tma_core2<{mrp}, {K}, {Nn}, {kc}, {nc2}>(Bg, sA32, ring, acc);")
+        lines += [f"if ((int)threadIdx.x < {Nn // nc2}) {{",
+                  f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{",
+                  f"  const long long n = {nc2} * (long long)threadIdx.x + j;",
+                  f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
+                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
+                  "    float v = acc[j][r] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
+                  f"    Cp[coff + {c_m} + {c_n}] = v; }}",
+                  "} }"]
     elif tma:
         lines.append(f"{T} acc[{nc}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = ({T})0; }}")
@@ -621,6 +635,7 @@ def ks_eligible(rows_per_cta, re, q, f64):
 
 
 DUAL_ENABLED = os.environ.get("RTB200_LOOP_DUAL", "1") != "0"   # two loop CTAs per SM
+CORE2_NCOL = int(os.environ.get("RTB200_LOOP_NCOL", "2"))   # columns per thread in-loop (1: one)
 MMA_ENABLED = os.environ.get("RTB200_LOOP_MMA", "0") == "1"     # 3xTF32 mma.sync in-loop GEMMs (measured slower: 18.5k vs 15.6k cycles for h2)
 PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
 PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
