@@ -259,6 +259,7 @@ def loop_source(lp, ops, name, info=None):
     info["pair"] the kernel runs as 2-CTA clusters and that GEMM keeps its
     weights resident (one K-half per CTA, _gemm_pair_literal)."""
     pair = (info or {}).get("pair")
+    fwd = _forward_pairs(lp, ops) if FORWARD_ENABLED and pair is None else set()
     parts = []
     for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
         if pair is not None and i == pair["op"]:
@@ -306,7 +307,8 @@ def loop_source(lp, ops, name, info=None):
             # labels of this op are renamed to keep them unique per op
             parts[-1] = _rename_labels(parts[-1], i)
         elif kernel == N.RT_K_GEMM:
-            parts.append(_gemm_call(lp, p, re, f64, soff))
+            parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
+                                    fwd_out=(i, i + 1) in fwd))
         elif kernel == N.RT_K_UDF:
             if noise:
                 parts.append(_udf_literal(p, i, soff, noise))
@@ -462,7 +464,7 @@ def _gbox_off(gb, strides, var):
     return " + ".join(terms) if terms else "0LL"
 
 
-def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
+def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False):
     """Fully specialised loop GEMM: shapes, strides and decompositions baked,
     descriptor pointers read once into registers."""
     T = "double" if f64 else "float"
@@ -496,10 +498,16 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
         lines.append(f"const uint32_t sB = smem_u32(ring.buf);")
         lines.append(f"for (int i = threadIdx.x; i < {K * Nn}; i += blockDim.x) {{ const long long k = i / {Nn}, n = i % {Nn}; "
                      f"sts1(sB + (uint32_t)(i * sizeof({T})), Bq[bqo + {b_k} + {b_n}]); }}")
-    lines.append(f"for (int i = threadIdx.x; i < {mrp * K}; i += blockDim.x) {{ const int r = i / {K}; "
-                 f"const long long k = i - r * {K}; const long long m = m0 + r; "
-                 f"sts1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), r < mr ? Ap[aoff + {a_m} + {a_k}] : ({T})0); }}")
-    lines.append("__syncthreads();")
+    if not fwd_in:
+        lines.append(f"for (int i = threadIdx.x; i < {mrp * K}; i += blockDim.x) {{ const int r = i / {K}; "
+                     f"const long long k = i - r * {K}; const long long m = m0 + r; "
+                     f"sts1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), r < mr ? Ap[aoff + {a_m} + {a_k}] : ({T})0); }}")
+        lines.append("__syncthreads();")
+    else:
+        # A rows forwarded in shared memory by the previous op's epilogue (the
+        # barrier still orders this op's own shared-memory weight loads)
+        lines.append("__syncthreads();")
+    fwd_store = (f" sts1(sA32 + (uint32_t)((n * {mrp} + r) * sizeof({T})), v);" if fwd_out else "")
     if tma and lp.red_off and KS_ENABLED and ks_eligible(lp.rows_per_cta, re, q, f64):
         opt = mrp * Nn // 256
         lines.append(f"{T} o[{opt}];")
@@ -524,7 +532,9 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
                   "      const long long n = nw0 + j * 8 + 2 * t4 + h;",
                   f"      const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
                   "      float v = acc[j][h] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
-                  f"      Cp[coff + {c_m} + {c_n}] = v; }} }}",
+                  f"      Cp[coff + {c_m} + {c_n}] = v;"
+                  + (f" sts1(sA32 + (uint32_t)((n * {mrp} + g) * 4), v);" if fwd_out else "")
+                  + " } }",
                   "}"]
     elif tma and CORE2_NCOL > 1 and not f64 and Nn % CORE2_NCOL == 0 and \
             Nn <= 256 * CORE2_NCOL and kc % 4 == 0 and K >= 64:
@@ -538,7 +548,7 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
                   f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
                   f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
                   "    float v = acc[j][r] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
-                  f"    Cp[coff + {c_m} + {c_n}] = v; }}",
+                  f"    Cp[coff + {c_m} + {c_n}] = v;{fwd_store} }}",
                   "} }"]
     elif tma:
         lines.append(f"{T} acc[{nc}][{mrp}];")
@@ -549,7 +559,7 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0):
                f"  const {T} bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else f"({T})0;"),
                f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
                f"    {T} v = acc[j][r] + bias;" + (f" v = vm_tanh<{T}>(v);" if tanh else ""),
-               f"    Cp[coff + {c_m} + {c_n}] = v; }}",
+               f"    Cp[coff + {c_m} + {c_n}] = v;{fwd_store} }}",
                "}"]
         lines += epi
     else:
@@ -642,7 +652,54 @@ PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes insid
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
 
 
-def _gemm_call(lp, q, re, f64, soff):
+def _same_gop(a, b):
+    return (a.ptr == b.ptr and a.off == b.off and a.dtype == b.dtype
+            and all(a.off_env[e] == b.off_env[e] for e in range(N.RT_MAXENV)))
+
+
+def _forward_pairs(lp, ops):
+    """(i, i+1): GEMM op i+1 reads as its A exactly the rows GEMM op i just
+    wrote as its C (h1 -> h2 -> mu of an MLP).  Op i's epilogue then also
+    leaves its output in the A staging area, k-major, and op i+1 skips the
+    global round trip.  Only for TMA-streamed producers (their core ends
+    with a CTA barrier, so nobody still reads the producer's own A)."""
+    out = set()
+    for i in range(len(ops) - 1):
+        (k1, p1, re1, f1, _n1, _s1), (k2, p2, re2, f2, _n2, _s2) = ops[i][:6], ops[i + 1][:6]
+        if k1 != N.RT_K_GEMM or k2 != N.RT_K_GEMM or re1 != 1 or re2 != 1 or f1 or f2:
+            continue
+        if _gemm_kind(lp, p1, re1, f1) != "tma" or (KS_ENABLED and lp.red_off):
+            continue
+        if not _same_gop(p1.C, p2.A):
+            continue
+        if [p1.M.ext[d] for d in range(p1.M.nd)] != [p2.M.ext[d] for d in range(p2.M.nd)] or \
+                p1.M.nd != p2.M.nd or p1.n != p2.k or p1.N.nd != 1 or p2.K.nd != 1:
+            continue
+        if any(p1.C.s1[d] != p2.A.s1[d] for d in range(p1.M.nd)) or p1.C.s2[0] != p2.A.s2[0]:
+            continue
+        out.add((i, i + 1))
+    return out
+
+
+def _gemm_kind(lp, q, re, f64):
+    it = 8 if f64 else 4
+    mrp = (lp.rows_per_cta * re + 3) // 4 * 4
+    stage = ((lp.smem_bytes - lp.ring_off) // 4) & ~127
+    dense_1d = q.N.nd == 1 and q.K.nd == 1 and q.Z.nd <= 1 and q.z == 1
+    b_dt = q.B.dtype == (N.RT_F64 if f64 else N.RT_F32)
+    aligned = q.B.off % 4 == 0 and all(q.B.off_env[e] % 4 == 0 for e in range(N.RT_MAXENV))
+    tdt = N.RT_F64 if f64 else N.RT_F32
+    same_dt = q.A.dtype == tdt and q.C.dtype == tdt and (not q.bias.ptr or q.bias.dtype == tdt)
+    if dense_1d and b_dt and mrp <= 8 and 64 <= q.n <= (256 if f64 else 512) and stage and \
+            q.B.s2[0] == 1 and q.B.s1[0] == q.n and aligned and (q.n * it) % 16 == 0 and same_dt:
+        return "tma"
+    return "other"
+
+
+FORWARD_ENABLED = os.environ.get("RTB200_LOOP_FORWARD", "1") != "0"
+
+
+def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False):
     """Pick a shape-specialised GEMM body for a persistent-loop op."""
     T = "double" if f64 else "float"
     it = 8 if f64 else 4
@@ -659,13 +716,13 @@ def _gemm_call(lp, q, re, f64, soff):
             q.B.s2[0] == 1 and q.B.s1[0] == Nn and aligned and (Nn * it) % 16 == 0:
         kc = max(1, min(K, stage // (Nn * it)))
         if same_dt:
-            return _gemm_literal(lp, q, re, f64, soff, True, kc)
+            return _gemm_literal(lp, q, re, f64, soff, True, kc, fwd_in, fwd_out)
         nc = 1 if Nn <= 256 else 2
         return (f"    gemm_tma_fixed<{T}, {mrp}, {nc}, {K}, {Nn}, {kc}>({q_ref}, env, r0 * {re}LL, "
                 f"r1 * {re}LL, sA32, ring);")
     if dense_1d and mrp <= 8 and Nn < 64 and K * Nn * it <= 4 * stage and K * mrp * it <= 64 * 1024:
         if same_dt and q.B.dtype == q.A.dtype:
-            return _gemm_literal(lp, q, re, f64, soff, False)
+            return _gemm_literal(lp, q, re, f64, soff, False, 0, fwd_in, False)
         return (f"    gemm_small_fixed<{T}, {mrp}, {K}, {Nn}>({q_ref}, env, r0 * {re}LL, r1 * {re}LL, "
                 f"sA32, smem_u32(ring.buf));")
     return f"    gemm_op<{T}>({q_ref}, env, r0 * {re}LL, r1 * {re}LL, sA, ring);"
