@@ -1045,6 +1045,33 @@ RT_DEV void tma_core2(const float* Bg, uint32_t sA, loop_ring& ring, float (&acc
   ring.seq += NCH;
 }
 
+// Same core over a weight matrix that stays resident in shared memory for
+// the whole loop (small, loop-invariant B: the observation layer W1, the
+// policy head W3): no per-step stream, no ring waits.  Ends with a CTA
+// barrier (callers may overwrite the A staging area afterwards).
+template <int MRP, int K, int N, int NCOL>
+RT_DEV void res_core(uint32_t sB, uint32_t sA, float (&acc)[NCOL][MRP]) {
+  const bool act = (int)threadIdx.x < N / NCOL;
+  const int c0 = act ? NCOL * (int)threadIdx.x : 0;
+  if (act) {
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+      float b[NCOL], a[MRP];
+      const uint32_t ba = sB + (uint32_t)((k * N + c0) * 4);
+      if constexpr (NCOL == 2)
+        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(b[0]), "=f"(b[1]) : "r"(ba));
+      else
+        b[0] = lds1(ba, 0.f);
+      lds_rows<MRP>(sA + (uint32_t)(k * MRP * 4), a);
+#pragma unroll
+      for (int r = 0; r < MRP; ++r)
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j) acc[j][r] = fma(a[r], b[j], acc[j][r]);
+    }
+  }
+  __syncthreads();
+}
+
 template <typename T, int K, int N, int KC>
 RT_DEV void tma_prefetch(const T* Bg, loop_ring& ring) {
   constexpr int NCH = (K + KC - 1) / KC;

@@ -308,7 +308,8 @@ def loop_source(lp, ops, name, info=None):
             parts[-1] = _rename_labels(parts[-1], i)
         elif kernel == N.RT_K_GEMM:
             parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
-                                    fwd_out=(i, i + 1) in fwd))
+                                    fwd_out=(i, i + 1) in fwd,
+                                    resident=((info or {}).get("resident") or {}).get(i)))
         elif kernel == N.RT_K_UDF:
             if noise:
                 parts.append(_udf_literal(p, i, soff, noise))
@@ -327,6 +328,17 @@ def loop_source(lp, ops, name, info=None):
     # the block index from env); otherwise the range is a literal
     t0, t1 = ("p.start", "p.stop") if lp.blk_len else (f"{lp.start}LL", f"{lp.stop}LL")
     early, pair_pro = "  if (r0 >= r1) return;", ""
+    for ri_op, roff in ((info or {}).get("resident") or {}).items():
+        q = ops[ri_op][1]
+        env_b = _env_terms([q.B.off_env[e] for e in range(N.RT_MAXENV)])
+        pair_pro += f"""
+  {{  // resident weights of op {ri_op}
+    const rt_gemm_params& q = *(const rt_gemm_params*)(smem + {ops[ri_op][5]});
+    const float4* Bg = reinterpret_cast<const float4*>((const float*)q.B.ptr + (q.B.off{env_b}));
+    const uint32_t sB = smem_u32(smem + {roff});
+    for (int i = threadIdx.x; i < {q.k * q.n // 4}; i += blockDim.x) sts4(sB + 16u * (uint32_t)i, __ldg(Bg + i));
+  }}
+  __syncthreads();"""
     if pair is not None:
         # both CTAs of a pair take part in every cluster barrier, even one
         # without rows (the grid is padded to an even CTA count)
@@ -464,7 +476,7 @@ def _gbox_off(gb, strides, var):
     return " + ".join(terms) if terms else "0LL"
 
 
-def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False):
+def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, resident=None):
     """Fully specialised loop GEMM: shapes, strides and decompositions baked,
     descriptor pointers read once into registers."""
     T = "double" if f64 else "float"
@@ -488,7 +500,9 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False):
              f"const long long m0 = r0 * {re}LL; const int mr = (int)((r1 - r0) * {re}LL);"]
     if has_bias:
         lines.append(f"const {T}* Bp_ = (const {T}*)q.bias.ptr; const long long boff = q.bias.off{env_bias};")
-    if tma:
+    if resident is not None:
+        lines.append(f"const uint32_t sB = smem_u32(smem + {resident});   // resident weights")
+    elif tma:
         lines.append(f"const {T}* Bg = (const {T}*)q.B.ptr + (q.B.off{env_b});")
         lines.append(f"tma_prefetch<{T}, {K}, {Nn}, {kc}>(Bg, ring);")
     else:
@@ -508,7 +522,20 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False):
         # barrier still orders this op's own shared-memory weight loads)
         lines.append("__syncthreads();")
     fwd_store = (f" sts1(sA32 + (uint32_t)((n * {mrp} + r) * sizeof({T})), v);" if fwd_out else "")
-    if tma and lp.red_off and KS_ENABLED and ks_eligible(lp.rows_per_cta, re, q, f64):
+    if resident is not None and Nn >= 16:
+        nc2 = 2 if Nn % 2 == 0 and Nn <= 512 else 1
+        lines.append(f"float acc[{nc2}][{mrp}];")
+        lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
+        lines.append(f"res_core<{mrp}, {K}, {Nn}, {nc2}>(sB, sA32, acc);")
+        lines += [f"if ((int)threadIdx.x < {-(-Nn // nc2)}) {{",
+                  f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{",
+                  f"  const long long n = {nc2} * (long long)threadIdx.x + j; if (n >= {Nn}) break;",
+                  f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
+                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
+                  "    float v = acc[j][r] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
+                  f"    Cp[coff + {c_m} + {c_n}] = v;{fwd_store} }}",
+                  "} }"]
+    elif tma and lp.red_off and KS_ENABLED and ks_eligible(lp.rows_per_cta, re, q, f64):
         opt = mrp * Nn // 256
         lines.append(f"{T} o[{opt}];")
         lines.append(f"tma_core_ks<{T}, {mrp}, {K}, {Nn}, {kc}>(Bg, sA32, ring, smem_u32(smem + {lp.red_off}), o);")
@@ -697,9 +724,10 @@ def _gemm_kind(lp, q, re, f64):
 
 
 FORWARD_ENABLED = os.environ.get("RTB200_LOOP_FORWARD", "1") != "0"
+RESIDENT_ENABLED = os.environ.get("RTB200_LOOP_RESIDENT", "1") != "0"
 
 
-def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False):
+def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False, resident=None):
     """Pick a shape-specialised GEMM body for a persistent-loop op."""
     T = "double" if f64 else "float"
     it = 8 if f64 else 4
@@ -712,6 +740,8 @@ def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False):
     q_ref = f"*(const rt_gemm_params*)(smem + {soff})"
     tdt = N.RT_F64 if f64 else N.RT_F32
     same_dt = q.A.dtype == tdt and q.C.dtype == tdt and (not q.bias.ptr or q.bias.dtype == tdt)
+    if resident is not None and same_dt and mrp <= 8:
+        return _gemm_literal(lp, q, re, f64, soff, False, 0, fwd_in, fwd_out, resident)
     if dense_1d and b_dt and mrp <= 8 and 64 <= Nn <= (256 if f64 else 512) and stage and \
             q.B.s2[0] == 1 and q.B.s1[0] == Nn and aligned and (Nn * it) % 16 == 0:
         kc = max(1, min(K, stage // (Nn * it)))

@@ -539,6 +539,30 @@ class Lowering:
         return S
 
     PAIR_MIN_BYTES = 64 * 1024
+    RESIDENT_MAX_BYTES = 32 * 1024
+
+    def _resident_ops(self, ops, rows, T, dim, base):
+        """{op index: shared-memory offset} for in-loop GEMMs whose weights are
+        fp32, dense row-major, <= 32 KB and do not move with the loop dim."""
+        from . import jit
+        if not (jit.ENABLED and jit.RESIDENT_ENABLED) or rows * T < jit.JIT_LOOP_MIN:
+            return {}, 0
+        out, cur = {}, 0
+        for i, (kernel, p, re, f64, _) in enumerate(ops):
+            if kernel != N.RT_K_GEMM or f64 or p.B.dtype != N.RT_F32:
+                continue
+            if not (p.N.nd == 1 and p.K.nd == 1 and p.z == 1 and p.B.s2[0] == 1
+                    and p.B.s1[0] == p.n and p.n % 4 == 0):
+                continue
+            if p.B.off_env[self.slot[dim]] != 0 or (p.B.ptr + 4 * p.B.off) % 16 or \
+                    any(p.B.off_env[e] % 4 for e in range(N.RT_MAXENV)):
+                continue
+            nb = p.k * p.n * 4
+            if nb > self.RESIDENT_MAX_BYTES or p.n >= 64:
+                continue   # (wide layers: the TMA-streamed core measured faster)
+            out[i] = base + cur
+            cur += (nb + 127) // 128 * 128
+        return out, cur
 
     def _pair_op(self, ops, R, rows, T, dim):
         """Index of the in-loop GEMM to run in CTA-pair mode, or None: fp32,
@@ -651,7 +675,13 @@ class Lowering:
             pair_info = {"op": pair, "kh": kh, "b_off": base, "p_off": base + b_bytes,
                          "pa_off": base + b_bytes + p_bytes, "nops": len(ops)}
             pair_bytes = b_bytes + p_bytes + pa_bytes
-        ring_off = (red_off + red_bytes + pair_bytes + 127) // 128 * 128
+        # small loop-invariant weights stay resident in shared memory
+        # (jit._gemm_literal resident=...): no per-step reload or stream
+        resident, res_bytes = {}, 0
+        res_base = (red_off + red_bytes + pair_bytes + 127) // 128 * 128
+        if pair is None:
+            resident, res_bytes = self._resident_ops(ops, rows, T, s.dim, res_base)
+        ring_off = (res_base + res_bytes + 127) // 128 * 128
         stage = 0
         budget = (112 if dual else 210) * 1024
         if tma:
@@ -723,7 +753,7 @@ class Lowering:
         idx = self.add_rec(N.RT_K_LOOP, lp, [nct, 1, 1], [256, 1, 1], smem,
                            (first.id, f"loop[{s.dim}]"))
         self.loop_subs[idx] = {"ops": ops, "trips": T, "pair": pair_info,
-                               "ctas_per_sm": 2 if dual else 1}
+                               "ctas_per_sm": 2 if dual else 1, "resident": resident}
         if pair_info is not None:
             self.rec_cluster[idx] = 2
 
