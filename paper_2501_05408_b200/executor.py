@@ -837,6 +837,7 @@ class Executable:
         self.launch_count = self._count_launches(low.prog)
         self.graph_exec = None
         self.graph_failed = False
+        self._stage_in, self._stage_ev, self._stage_out = {}, {}, None
 
     def _upload_loops(self, low):
         """Persistent-loop sub-op descriptors live in HBM: one blob per loop
@@ -937,16 +938,26 @@ class Executable:
             arr = np.asarray(v)
             if b.dshape:
                 arr = arr[tuple(slice(0, e) for e in b.dshape)]
-            arr = np.array(arr, dtype=DTYPES[b.dtype], order="C", copy=True).reshape(
-                np.shape(arr))
             if arr.shape != b.shape:
                 raise OracleError(f"{n.name} produced shape {arr.shape[len(b.dshape):]}, "
                                   f"declared {b.pshape}")
             dst = _u8view(torch, b.ptr, b.nbytes, self.dev)
-            src = torch.from_numpy(arr.reshape(-1).view(np.uint8))
-            if b.nbytes >= (1 << 16):
-                src = src.pin_memory()
-            dst.copy_(src, non_blocking=True)
+            # a pinned staging buffer per input, reused across calls: the
+            # host->device copy is asynchronous and needs no per-call pinning
+            stage = self._stage_in.get(n.name)
+            if stage is None or stage.numel() != b.nbytes:
+                stage = torch.empty(max(1, b.nbytes), dtype=torch.uint8, pin_memory=True)
+                self._stage_in[n.name] = stage
+                self._stage_ev[n.name] = None
+            ev = self._stage_ev.get(n.name)
+            if ev is not None:
+                ev.synchronize()          # the previous call's copy out of it is done
+            host = stage.numpy()[:b.nbytes].view(DTYPES[b.dtype]).reshape(b.shape)
+            np.copyto(host, arr, casting="unsafe")
+            dst.copy_(stage[:b.nbytes], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self._stage_ev[n.name] = ev
 
     GRAPH_MIN_LAUNCHES = 64
 
@@ -1116,7 +1127,52 @@ class Executable:
                                                                       b1=st[3] - 1)
             raise RuntimeError_(f"{name}: {txt}")
 
-    def outputs(self, device_outputs=False):
+    def fetch(self, stream=None):
+        """Status word + every output in ONE device->host synchronisation:
+        outputs are copied (asynchronously) into one reused pinned staging
+        buffer, then into fresh numpy arrays.  Raises like check_status."""
+        torch = self.torch
+        s = stream or torch.cuda.current_stream(self.dev)
+        if self._stage_out is None:
+            total = 16 + sum((self.bufs[(nid, oid)].nbytes + 255) // 256 * 256
+                             for _, nid, oid in self.g.outputs)
+            self._stage_out = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+        st = self._stage_out
+        views = self.outputs(device_outputs=True, clone=False)
+        with torch.cuda.device(self.dev):
+            with torch.cuda.stream(s):
+                st[:16].copy_(_u8view(torch, self.status, 16, self.dev), non_blocking=True)
+                off, spans = 16, {}
+                for name, nid, oid in self.g.outputs:
+                    t = views[name]
+                    nb = t.numel() * t.element_size()
+                    if nb:
+                        src = t.contiguous().reshape(-1).view(torch.uint8)
+                        st[off:off + nb].copy_(src, non_blocking=True)
+                    spans[name] = (off, nb, t.shape, t.dtype)
+                    off += (nb + 255) // 256 * 256
+            s.synchronize()
+        hostst = st[:16].numpy().view(np.int32)
+        self._raise_status(hostst)
+        res = {}
+        buf = st.numpy()
+        for name, nid, oid in self.g.outputs:
+            off, nb, shape, tdt = spans[name]
+            b = self.bufs[(nid, oid)]
+            npdt = DTYPES[b.dtype]
+            a = np.array(buf[off:off + nb].view(npdt).reshape(tuple(shape)), copy=True)
+            res[name] = a
+        return res
+
+    def _raise_status(self, st):
+        if st[0] != 0:
+            node = self.g.nodes.get(int(st[1]))
+            name = node.name if node else f"n{int(st[1])}"
+            txt = _ERR_TEXT.get(int(st[0]), "device error {a} {b}").format(
+                a=int(st[2]), b=int(st[3]), b1=int(st[3]) - 1)
+            raise RuntimeError_(f"{name}: {txt}")
+
+    def outputs(self, device_outputs=False, clone=True):
         torch = self.torch
         res = {}
         for name, nid, oid in self.g.outputs:
@@ -1136,7 +1192,7 @@ class Executable:
                     range(nd + len(vec), len(b.shape)))
                 t = t.permute(perm)
             if device_outputs:
-                res[name] = t.clone()
+                res[name] = t.clone() if clone else t
             else:
                 a = t.contiguous().cpu().numpy()
                 res[name] = a.astype(DTYPES[b.dtype], copy=False)
@@ -1364,8 +1420,11 @@ def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=
     (default 64 MiB, the reference's polysched.py:28)."""
     exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm, block, swap)
     exe.run(inputs or {}, stream)
-    exe.check_status(stream)
-    outs = exe.outputs(device_outputs)
+    if device_outputs:
+        exe.check_status(stream)
+        outs = exe.outputs(True)
+    else:
+        outs = exe.fetch(stream)
     if return_bounds:
         return outs, dict(benv)
     return outs
