@@ -838,6 +838,7 @@ class Executable:
         self.graph_exec = None
         self.graph_failed = False
         self._stage_in, self._stage_ev, self._stage_out = {}, {}, None
+        self._pgraph, self._pgraph_failed = None, False
 
     def _upload_loops(self, low):
         """Persistent-loop sub-op descriptors live in HBM: one blob per loop
@@ -1000,12 +1001,58 @@ class Executable:
                                  N.RT_MAXENV, s.cuda_stream, ev_arr, nev)
             N.check(rc, "rt_run")
 
+    def _hook_free_prefix(self):
+        """Length of the longest program prefix that ends before the first
+        host hook at loop depth 0 (every loop opened in it closes in it)."""
+        depth, end = 0, 0
+        for i in range(self.nprog):
+            op = self.prog[i].op
+            if op == N.RT_OP_HOOK:
+                break
+            if op == N.RT_OP_FOR:
+                depth += 1
+            elif op == N.RT_OP_END:
+                depth -= 1
+            if depth == 0:
+                end = i + 1
+        return end
+
+    def _prefix_graph(self, s):
+        """CUDA graph of the hook-free prefix (the acting loop and most of the
+        backward of a sharded run: the all-reduce hooks come at the end)."""
+        if self._pgraph is not None or self._pgraph_failed:
+            return self._pgraph
+        n = self._hook_free_prefix()
+        if n < self.GRAPH_MIN_PREFIX:
+            self._pgraph_failed = True
+            return None
+        for i in range(N.RT_MAXENV):
+            self.env[i] = 0
+        cap = self.torch.cuda.Stream(self.dev)
+        cap.wait_stream(s)
+        out = N.u64()
+        rc = self.lib.rt_graph_capture(self.prog, n, self.recs, self.nrec, self.env,
+                                       N.RT_MAXENV, cap.cuda_stream, C.byref(out))
+        s.wait_stream(cap)
+        if rc != 0:
+            self._pgraph_failed = True
+            return None
+        self._pgraph = (out.value, n)
+        return self._pgraph
+
+    GRAPH_MIN_PREFIX = 16
+
     def _run_with_hooks(self, s):
-        """Sharded run: program segments between all-reduce hooks."""
+        """Sharded / swapping run: program segments between host hooks; the
+        hook-free prefix replays as one CUDA graph."""
         torch = self.torch
+        pre = self._prefix_graph(s) if self.swap_rt is None else None
         for i in range(N.RT_MAXENV):
             self.env[i] = 0
         pc, hook = N.i32(0), N.i32(-1)
+        if pre is not None:
+            N.check(self.lib.rt_graph_launch(pre[0], s.cuda_stream), "prefix graph")
+            pc = N.i32(pre[1])
         while True:
             rc = self.lib.rt_run_segment(self.prog, self.nprog, self.recs, self.nrec, self.env,
                                          N.RT_MAXENV, s.cuda_stream, C.byref(pc), C.byref(hook))
