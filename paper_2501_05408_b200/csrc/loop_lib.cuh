@@ -73,6 +73,15 @@ RT_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 #define RING 4
 
+// ---------------------------------------------------------------- cp.async
+// 8-byte global -> shared async copies (LDGSTS): completion is tracked per
+// thread by commit groups, not by register scoreboards.
+RT_DEV void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+RT_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+RT_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ---------------------------------------------------------------- clusters
 // A CTA pair of the persistent acting loop keeps one K-half of a large
 // weight matrix resident in each SM's shared memory and exchanges operand
@@ -104,6 +113,27 @@ RT_DEV float4 dsmem_ld4(uint32_t addr) {
 }
 RT_DEV void sts4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+}
+
+// acc[r] += a[r] * b over a row block.  fp32: packed FFMA2 (fma.rn.f32x2,
+// sm_100+) on row pairs with b broadcast — two IEEE fused multiply-adds per
+// issued instruction, bit-identical to scalar fma; the in-loop GEMM cores
+// are issue bound, so this halves their FMA instruction count.
+RT_DEV void fma2(float& d0, float& d1, float a0, float a1, float b) {
+  asm("{.reg .b64 d, a, bb;\n\tmov.b64 d, {%0,%1};\n\tmov.b64 a, {%2,%3};\n\tmov.b64 bb, {%4,%4};\n\t"
+      "fma.rn.f32x2 d, a, bb, d;\n\tmov.b64 {%0,%1}, d;}"
+      : "+f"(d0), "+f"(d1) : "f"(a0), "f"(a1), "f"(b));
+}
+template <int MRP>
+RT_DEV void fma_rows(float (&acc)[MRP], const float (&a)[MRP], float b) {
+  static_assert(MRP % 2 == 0, "row blocks are padded to even counts");
+#pragma unroll
+  for (int r = 0; r < MRP; r += 2) fma2(acc[r], acc[r + 1], a[r], a[r + 1], b);
+}
+template <int MRP>
+RT_DEV void fma_rows(double (&acc)[MRP], const double (&a)[MRP], double b) {
+#pragma unroll
+  for (int r = 0; r < MRP; ++r) acc[r] = fma(a[r], b, acc[r]);
 }
 
 
@@ -206,9 +236,7 @@ RT_DEV void tma_body(const rt_gemm_params& p, const T* As, const T* Bg, int64_t 
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int j = 0; j < NC; ++j)
-#pragma unroll
-          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+        for (int j = 0; j < NC; ++j) fma_rows<MRP>(acc[j], a[u], b[u][j]);
     }
     for (; kk < rows; ++kk, ak += MRP) {
       T a[MRP];
@@ -654,9 +682,7 @@ RT_DEV void gemm_tma_fixed(const rt_gemm_params& p, const int64_t* env, int64_t 
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int j = 0; j < NC; ++j)
-#pragma unroll
-          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+        for (int j = 0; j < NC; ++j) fma_rows<MRP>(acc[j], a[u], b[u][j]);
     }
     __syncthreads();
     if (threadIdx.x == 0 && c + RING < NCH) issue(c + RING);
@@ -893,9 +919,7 @@ RT_DEV void tma_core(const T* Bg, uint32_t sA, loop_ring& ring, T (&acc)[NC][MRP
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int j = 0; j < NC; ++j)
-#pragma unroll
-          for (int r = 0; r < MRP; ++r) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+        for (int j = 0; j < NC; ++j) fma_rows<MRP>(acc[j], a[u], b[u][j]);
     }
     __syncthreads();
     if (threadIdx.x == 0 && c + RING < NCH) {
@@ -1027,9 +1051,7 @@ RT_DEV void tma_core2(const float* Bg, uint32_t sA, loop_ring& ring, float (&acc
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int r = 0; r < MRP; ++r)
-#pragma unroll
-            for (int j = 0; j < NCOL; ++j) acc[j][r] = fma(a[u][r], b[u][j], acc[j][r]);
+          for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a[u], b[u][j]);
       }
     }
     __syncthreads();
@@ -1043,6 +1065,154 @@ RT_DEV void tma_core2(const float* Bg, uint32_t sA, loop_ring& ring, float (&acc
     }
   }
   ring.seq += NCH;
+}
+
+// tma_core2 over both thread halves: threads [0, HT) and [HT, 2 HT) (HT =
+// N / NCOL) take the lower and upper half of every ring chunk's k rows, so
+// all eight warps issue FMAs (with one computing warp per scheduler the
+// LDS -> FFMA2 latencies stayed exposed: ncu, profiles/README.md), then the
+// upper half's partial sums join the lower half's through shared memory
+// (red: MRP x N floats).  The final sums are in threads < HT, as tma_core2's.
+template <int MRP, int K, int N, int KC, int NCOL>
+RT_DEV void tma_core2k(const float* Bg, uint32_t sA, loop_ring& ring, uint32_t red,
+                       float (&acc)[NCOL][MRP]) {
+  static_assert(NCOL == 2, "partial sums are exchanged as float2");
+  constexpr int NCH = (K + KC - 1) / KC;
+  constexpr int HT = N / NCOL;
+  const int tid = (int)threadIdx.x;
+  const int h = tid >= HT ? 1 : 0;
+  const bool act = tid < 2 * HT;
+  const int c0 = act ? NCOL * (tid - h * HT) : 0;
+  const uint32_t ring_base = smem_u32(ring.buf);
+  for (int c = 0; c < NCH; ++c) {
+    const uint32_t g = ring.seq + (uint32_t)c;
+    const uint32_t st = g % RING;
+    mbar_wait(&ring.bar[st], (g / RING) & 1);
+    const uint32_t bs = ring_base + st * ring.stage_bytes;
+    const int rows = (c + 1) * KC <= K ? KC : K - c * KC;
+    const int hr = ((rows + 1) / 2 + 3) / 4 * 4;
+    const int lo = h * hr, hi = (h + 1) * hr < rows ? (h + 1) * hr : rows;
+    const uint32_t ak = sA + (uint32_t)(c * KC * MRP * 4);
+    if (act) {
+#pragma unroll 2
+      for (int kk = lo; kk < hi; kk += 4) {
+        float b[4][NCOL];
+        float a[4][MRP];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t ba = bs + (uint32_t)(((kk + u) * N + c0) * 4);
+          if (kk + u < hi)
+            asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(b[u][0]), "=f"(b[u][1]) : "r"(ba));
+          else
+            b[u][0] = b[u][1] = 0.f;
+          lds_rows<MRP>(ak + (uint32_t)((kk + u) * MRP * 4), a[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a[u], b[u][j]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && c + RING < NCH) {
+      const int cc = c + RING;
+      const uint32_t st2 = (ring.seq + (uint32_t)cc) % RING;
+      const int rows2 = (cc + 1) * KC <= K ? KC : K - cc * KC;
+      const uint32_t bytes = (uint32_t)(rows2 * N * 4);
+      mbar_expect_tx(&ring.bar[st2], bytes);
+      bulk_g2s(ring.buf + (size_t)st2 * ring.stage_bytes, Bg + (size_t)cc * KC * N, bytes, &ring.bar[st2]);
+    }
+  }
+  ring.seq += NCH;
+  if (act && h == 1) {
+#pragma unroll
+    for (int r = 0; r < MRP; ++r)
+      asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(red + (uint32_t)((r * N + c0) * 4)),
+                   "f"(acc[0][r]), "f"(acc[1][r]));
+  }
+  __syncthreads();
+  if (act && h == 0) {
+#pragma unroll
+    for (int r = 0; r < MRP; ++r) {
+      float x0, x1;
+      asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(x0), "=f"(x1) : "r"(red + (uint32_t)((r * N + c0) * 4)));
+      acc[0][r] += x0;
+      acc[1][r] += x1;
+    }
+  }
+}
+
+// NC adjacent floats from / to shared memory in one access (NC = 1, 2, 4)
+template <int NC>
+RT_DEV void lds_cols(uint32_t a, float (&x)[NC]) {
+  if constexpr (NC == 1) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(a));
+  else if constexpr (NC == 2) asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(x[0]), "=f"(x[1]) : "r"(a));
+  else asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]) : "r"(a));
+}
+template <int NC>
+RT_DEV void sts_cols(uint32_t a, const float (&x)[NC]) {
+  if constexpr (NC == 1) asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x[0]));
+  else if constexpr (NC == 2) asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(a), "f"(x[0]), "f"(x[1]));
+  else asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]));
+}
+
+// On-chip weights for the widest in-loop layer (N = 256 = blockDim): the
+// CTA's threads form P = NCOL parts of N / NCOL threads; part p owns k rows
+// [p K/P, (p+1) K/P) and each thread NCOL adjacent columns.  The first KRP
+// of a part's rows live in registers (w[j][kk]) for the whole loop, the
+// rest in shared memory (sB: part-major, row-major within a part), so a
+// step streams nothing from L2 and waits on no ring.  More columns per
+// thread divide the A broadcast loads (the same MRP values for every
+// thread of a part) by NCOL.  Parts p > 0 hand their partial sums to part
+// 0 through red ([P-1][MRP][N] floats); the final sums are in threads
+// < N / NCOL.  A is k-major in sA (MRP rows per k).
+template <int MRP, int K, int N, int NCOL, int KRP>
+RT_DEV void hyb_core(const float (&w)[NCOL][KRP], uint32_t sB, uint32_t sA, uint32_t red,
+                     float (&acc)[NCOL][MRP]) {
+  constexpr int P = NCOL, HT = N / NCOL, KP = K / P, KS = KP - KRP;
+  static_assert(K % P == 0 && KS >= 0, "K splits evenly over the parts");
+  const int tid = (int)threadIdx.x;
+  const int part = tid / HT, c0 = NCOL * (tid - part * HT);
+  const uint32_t a0 = sA + (uint32_t)(part * KP * MRP * 4);
+#pragma unroll
+  for (int kk = 0; kk < KRP; ++kk) {
+    float a[MRP];
+    lds_rows<MRP>(a0 + (uint32_t)(kk * MRP * 4), a);
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a, w[j][kk]);
+  }
+  const uint32_t bn = sB + (uint32_t)((part * KS * N + c0) * 4);
+#pragma unroll 4
+  for (int kk = 0; kk < KS; ++kk) {
+    float a[MRP], b[NCOL];
+    lds_rows<MRP>(a0 + (uint32_t)((KRP + kk) * MRP * 4), a);
+    lds_cols<NCOL>(bn + (uint32_t)(kk * N * 4), b);
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a, b[j]);
+  }
+  if constexpr (P > 1) {
+    if (part > 0) {
+#pragma unroll
+      for (int r = 0; r < MRP; ++r) {
+        float x[NCOL];
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j) x[j] = acc[j][r];
+        sts_cols<NCOL>(red + (uint32_t)((((part - 1) * MRP + r) * N + c0) * 4), x);
+      }
+    }
+    __syncthreads();
+    if (part == 0) {
+#pragma unroll
+      for (int q = 1; q < P; ++q)
+#pragma unroll
+        for (int r = 0; r < MRP; ++r) {
+          float x[NCOL];
+          lds_cols<NCOL>(red + (uint32_t)((((q - 1) * MRP + r) * N + c0) * 4), x);
+#pragma unroll
+          for (int j = 0; j < NCOL; ++j) acc[j][r] += x[j];
+        }
+    }
+  }
 }
 
 // Same core over a weight matrix that stays resident in shared memory for
@@ -1064,9 +1234,7 @@ RT_DEV void res_core(uint32_t sB, uint32_t sA, float (&acc)[NCOL][MRP]) {
         b[0] = lds1(ba, 0.f);
       lds_rows<MRP>(sA + (uint32_t)(k * MRP * 4), a);
 #pragma unroll
-      for (int r = 0; r < MRP; ++r)
-#pragma unroll
-        for (int j = 0; j < NCOL; ++j) acc[j][r] = fma(a[r], b[j], acc[j][r]);
+      for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a, b[j]);
     }
   }
   __syncthreads();

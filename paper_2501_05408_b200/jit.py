@@ -259,8 +259,8 @@ def loop_source(lp, ops, name, info=None):
     info["pair"] the kernel runs as 2-CTA clusters and that GEMM keeps its
     weights resident (one K-half per CTA, _gemm_pair_literal)."""
     pair = (info or {}).get("pair")
-    fwd = _forward_pairs(lp, ops) if FORWARD_ENABLED and pair is None else set()
-    parts = []
+    fwd = _forward_pairs(lp, ops, info) if FORWARD_ENABLED and pair is None else set()
+    parts, step_pre = [], []
     for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
         if pair is not None and i == pair["op"]:
             parts.append(_gemm_pair_literal(lp, p, soff, pair))
@@ -307,12 +307,24 @@ def loop_source(lp, ops, name, info=None):
             # labels of this op are renamed to keep them unique per op
             parts[-1] = _rename_labels(parts[-1], i)
         elif kernel == N.RT_K_GEMM:
-            parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
-                                    fwd_out=(i, i + 1) in fwd,
-                                    resident=((info or {}).get("resident") or {}).get(i)))
+            hy = (info or {}).get("hybrid")
+            if hy is not None and hy["op"] == i:
+                parts.append(_gemm_literal(lp, p, re, f64, soff, False, 0, (i - 1, i) in fwd,
+                                           (i, i + 1) in fwd, hybrid=hy))
+            else:
+                parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
+                                        fwd_out=(i, i + 1) in fwd,
+                                        resident=((info or {}).get("resident") or {}).get(i)))
         elif kernel == N.RT_K_UDF:
             if noise:
-                parts.append(_udf_literal(p, i, soff, noise))
+                nz_off = (info or {}).get("nz_off")
+                pf = _udf_prefetch(lp, p, i, nz_off) if UDF_PREFETCH and nz_off and \
+                    _nz_row(p) * 8 * 8 <= (info or {}).get("nz_bytes", 0) else None
+                if pf is not None:
+                    step_pre.append("    " + pf[0])
+                t1s = "p.stop" if lp.blk_len else f"{lp.stop}LL"
+                parts.append(_udf_literal(p, i, soff, noise, prefetched=None if pf is None else
+                                          (nz_off, pf[1], lp.step, t1s)))
             else:
                 parts.append(f"""    udf_op(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env, r0, r1, t);""")
         elif kernel == N.RT_K_RNG:
@@ -337,6 +349,34 @@ def loop_source(lp, ops, name, info=None):
     const float4* Bg = reinterpret_cast<const float4*>((const float*)q.B.ptr + (q.B.off{env_b}));
     const uint32_t sB = smem_u32(smem + {roff});
     for (int i = threadIdx.x; i < {q.k * q.n // 4}; i += blockDim.x) sts4(sB + 16u * (uint32_t)i, __ldg(Bg + i));
+  }}
+  __syncthreads();"""
+    hy = (info or {}).get("hybrid")
+    if hy is not None:
+        q = ops[hy["op"]][1]
+        kr = hy["kr"]
+        env_b = _env_terms([q.B.off_env[e] for e in range(N.RT_MAXENV)])
+        nc, n_ = hy["ncol"], q.n
+        kp = q.k // nc
+        krp, ks = kr // nc, q.k // nc - kr // nc
+        pair_pro += f"""
+  // on-chip weights of op {hy["op"]}: part p = tid / {n_ // nc} owns k rows [p*{kp}, (p+1)*{kp}),
+  // the first {krp} of them in registers (NCOL = {nc} columns per thread), the rest in smem
+  float wreg[{nc}][{krp}];
+  {{
+    const rt_gemm_params& q = *(const rt_gemm_params*)(smem + {ops[hy["op"]][5]});
+    const float* Bg = (const float*)q.B.ptr + (q.B.off{env_b});
+    const int part = threadIdx.x / {n_ // nc}, c0 = {nc} * (threadIdx.x % {n_ // nc});
+    #pragma unroll
+    for (int k = 0; k < {krp}; ++k)
+      #pragma unroll
+      for (int j = 0; j < {nc}; ++j)   // (an opaque load: the compiler may not re-load it per step)
+        asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(wreg[j][k]) : "l"(Bg + (part * {kp} + k) * {n_} + c0 + j));
+    const uint32_t sB = smem_u32(smem + {hy["off"]});
+    for (int i = threadIdx.x; i < {nc * ks * n_ // 4}; i += blockDim.x) {{
+      const int row = i / {n_ // 4}, p2 = row / {max(ks, 1)}, kk = row % {max(ks, 1)};
+      sts4(sB + 16u * (uint32_t)i, __ldg(reinterpret_cast<const float4*>(Bg + (p2 * {kp} + {krp} + kk) * {n_}) + i % {n_ // 4}));
+    }}
   }}
   __syncthreads();"""
     if pair is not None:
@@ -364,6 +404,7 @@ extern "C" __global__ void __launch_bounds__(256, {per_sm}) {name}(const __grid_
   long long c0 = clock64();
   for (long long t = {t0}; t {cmp} {t1}; t += {lp.step}LL) {{
     env[{lp.slot}] = t;
+{chr(10).join(step_pre)}
 {body}
   }}
 }}
@@ -476,7 +517,8 @@ def _gbox_off(gb, strides, var):
     return " + ".join(terms) if terms else "0LL"
 
 
-def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, resident=None):
+def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, resident=None,
+                  hybrid=None):
     """Fully specialised loop GEMM: shapes, strides and decompositions baked,
     descriptor pointers read once into registers."""
     T = "double" if f64 else "float"
@@ -500,7 +542,9 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
              f"const long long m0 = r0 * {re}LL; const int mr = (int)((r1 - r0) * {re}LL);"]
     if has_bias:
         lines.append(f"const {T}* Bp_ = (const {T}*)q.bias.ptr; const long long boff = q.bias.off{env_bias};")
-    if resident is not None:
+    if hybrid is not None:
+        lines.append(f"const uint32_t sB = smem_u32(smem + {hybrid['off']});   // on-chip weights (rows >= KR)")
+    elif resident is not None:
         lines.append(f"const uint32_t sB = smem_u32(smem + {resident});   // resident weights")
     elif tma:
         lines.append(f"const {T}* Bg = (const {T}*)q.B.ptr + (q.B.off{env_b});")
@@ -522,7 +566,28 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
         # barrier still orders this op's own shared-memory weight loads)
         lines.append("__syncthreads();")
     fwd_store = (f" sts1(sA32 + (uint32_t)((n * {mrp} + r) * sizeof({T})), v);" if fwd_out else "")
-    if resident is not None and Nn >= 16:
+    if hybrid is not None:
+        kr, nc = hybrid["kr"], hybrid["ncol"]
+        red = f"smem_u32(smem + {hybrid['red']})" if nc > 1 else "0u"
+        lines.append(f"float acc[{nc}][{mrp}];")
+        lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
+        lines.append(f"hyb_core<{mrp}, {K}, {Nn}, {nc}, {kr // nc}>(wreg, sB, sA32, {red}, acc);")
+        if fwd_out:
+            lines.append("__syncthreads();   // every thread is done reading A before it is overwritten")
+        lines += [f"if ((int)threadIdx.x < {Nn // nc}) {{",
+                  f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{",
+                  f"  const long long n = {nc} * (long long)threadIdx.x + j;",
+                  f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
+                  f"  float v[{mrp}];",
+                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ v[r] = 0.f; if (r < mr) {{ v[r] = acc[j][r] + bias;"
+                  + (" v[r] = vm_tanh<float>(v[r]);" if tanh else "") + " } }",
+                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
+                  f"    Cp[coff + {c_m} + {c_n}] = v[r]; }}"]
+        if fwd_out:
+            lines.append(f"  #pragma unroll\n  for (int r = 0; r < {mrp}; r += 4) sts4(sA32 + (uint32_t)((n * {mrp} + r) * 4), "
+                         f"make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]));")
+        lines.append("} }")
+    elif resident is not None and Nn >= 16:
         nc2 = 2 if Nn % 2 == 0 and Nn <= 512 else 1
         lines.append(f"float acc[{nc2}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
@@ -568,14 +633,26 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
         nc2 = CORE2_NCOL
         lines.append(f"float acc[{nc2}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
-        lines.append(f"tma_core2<{mrp}, {K}, {Nn}, {kc}, {nc2}>(Bg, sA32, ring, acc);")
+        if lp.red_off and k2_eligible(lp.rows_per_cta, re, q, f64) and kc % 8 == 0:
+            lines.append(f"tma_core2k<{mrp}, {K}, {Nn}, {kc}, {nc2}>(Bg, sA32, ring, "
+                         f"smem_u32(smem + {lp.red_off}), acc);")
+        else:
+            lines.append(f"tma_core2<{mrp}, {K}, {Nn}, {kc}, {nc2}>(Bg, sA32, ring, acc);")
+        # forwarded A rows: this thread's column n is A row k = n, MRP
+        # contiguous floats (k-major staging), so store them as float4s
+        # (scalar stores at a 2 x MRP x 4 B lane stride were 16-way conflicts)
+        fwd_vec = (f"  #pragma unroll\n  for (int r = 0; r < {mrp}; r += 4) sts4(sA32 + (uint32_t)((n * {mrp} + r) * 4), "
+                   f"make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]));" if fwd_out else "")
         lines += [f"if ((int)threadIdx.x < {Nn // nc2}) {{",
                   f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{",
                   f"  const long long n = {nc2} * (long long)threadIdx.x + j;",
                   f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
+                  f"  float v[{mrp}];",
+                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ v[r] = 0.f; if (r < mr) {{ v[r] = acc[j][r] + bias;"
+                  + (" v[r] = vm_tanh<float>(v[r]);" if tanh else "") + " } }",
                   f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
-                  "    float v = acc[j][r] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
-                  f"    Cp[coff + {c_m} + {c_n}] = v;{fwd_store} }}",
+                  f"    Cp[coff + {c_m} + {c_n}] = v[r]; }}",
+                  fwd_vec,
                   "} }"]
     elif tma:
         lines.append(f"{T} acc[{nc}][{mrp}];")
@@ -607,7 +684,38 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
     return "    {  // gemm (specialised)\n      " + "\n      ".join(lines) + "\n    }"
 
 
-def _udf_literal(p, op_index, soff, noise):
+def _udf_prefetch(lp, p, op_index, soff_nz):
+    """Pre-drawn normals of a loop env op copied to shared memory one step
+    ahead (cp.async, one row per warp, one output element per lane): the
+    HBM latency of step t+1's normals overlaps step t's remaining work and
+    t+1's MLP, and no register scoreboard is shared with the step's other
+    loads (register prefetches made unrelated loads wait on them).  Returns
+    (code run at the first step, code issuing step tn's copies) or None
+    when a warp has several rows or a row has more than 32 values."""
+    if lp.rows_per_cta > 8 or any(p.out_count[j] > 32 for j in range(p.nout)):
+        return None
+    def issue(tv):
+        lines = ["{ const int lane_ = threadIdx.x & 31, w_ = threadIdx.x >> 5; const long long row_ = r0 + w_;",
+                 f"  const double* nzb = (const double*)ops[{op_index}].noise + ops[{op_index}].noise_off"
+                 f" + row_ * ops[{op_index}].noise_row + ({tv}) * ops[{op_index}].noise_step;"]
+        e0 = 0
+        for j in range(p.nout):
+            c = p.out_count[j]
+            lines.append(f"  if (row_ < r1 && lane_ < {c}) cp_async8(smem_u32(smem + {soff_nz}) + "
+                         f"(uint32_t)((w_ * {_nz_row(p)} + {e0} + lane_) * 8), nzb + {e0} + lane_);")
+            e0 += c
+        lines.append("  cp_async_commit(); }")
+        return "\n    ".join(lines)
+    t_first = "p.start" if lp.blk_len else f"{lp.start}LL"
+    first = f"if (t == {t_first}) {{\n    {issue('t')}\n    }}"
+    return first, issue
+
+
+def _nz_row(p):
+    return sum(p.out_count[j] for j in range(p.nout))
+
+
+def _udf_literal(p, op_index, soff, noise, prefetched=False):
     """Synthetic env body with counts, strides and the row decomposition baked."""
     nd = p.box.nd
     ext = [p.box.ext[j] for j in range(nd)]
@@ -638,7 +746,9 @@ def _udf_literal(p, op_index, soff, noise):
         v = p.in_[k]
         off = _offset_expr(f"io{k}", v, nd)
         lines.append(f"  base = base + warp_pairwise_sum((const void*)in{k}, {v.dtype}, {off}, {p.in_count[k]}LL, lane) / {float(p.in_count[k])!r};")
-    lines.append("  long long nz = nz0 + row * nzr + t * nzs;")
+    lines.append("  long long nz = nz0 + row * nzr + t * nzs; (void)nz;")
+    if prefetched:
+        lines.append("  cp_async_wait_all();")
     for j in range(p.nout):
         v = p.out[j]
         off = _offset_expr(f"oo{j}", v, nd)
@@ -655,9 +765,18 @@ def _udf_literal(p, op_index, soff, noise):
             lines.append(pre)
         store = (f"out{j}[{off} + e] = ({expr}) != 0.0;" if v.dtype == N.RT_BOOL
                  else f"out{j}[{off} + e] = ({ct})({expr});")
-        lines.append(f"  for (int e = lane; e < {p.out_count[j]}; e += 32) {{ const double z = __ldg(noise + nz + e); {store} }}")
+        if prefetched:
+            e0 = sum(p.out_count[jj] for jj in range(j))
+            lines.append(f"  if (lane < {p.out_count[j]}) {{ const int e = lane; const double z = lds1(smem_u32(smem + "
+                         f"{prefetched[0]}) + (uint32_t)((warp * {_nz_row(p)} + {e0} + lane) * 8), 0.0); {store} }}")
+        else:
+            lines.append(f"  for (int e = lane; e < {p.out_count[j]}; e += 32) {{ const double z = __ldg(noise + nz + e); {store} }}")
         lines.append(f"  nz += {p.out_count[j]};")
     lines.append("}")
+    if prefetched:
+        # each lane re-fills only the slots it read itself, so no barrier is needed
+        tn, stop = ("t + " + str(prefetched[2]) + "LL"), prefetched[3]
+        lines.append(f"if ({tn} {'<' if prefetched[2] > 0 else '>'} {stop}) {prefetched[1](tn)}")
     return "    {  // env (specialised)\n      " + "\n      ".join(lines) + "\n    }"
 
 
@@ -677,6 +796,22 @@ MMA_ENABLED = os.environ.get("RTB200_LOOP_MMA", "0") == "1"     # 3xTF32 mma.syn
 PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
 PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
+K2_ENABLED = os.environ.get("RTB200_LOOP_K2", "0") == "1"   # both thread halves on N=256 layers (measured: no gain)
+WIDE_RESIDENT = os.environ.get("RTB200_LOOP_WIDE_RESIDENT", "1") != "0"   # small wide layers resident when hybrid
+UDF_PREFETCH = os.environ.get("RTB200_LOOP_UDF_PREFETCH", "1") != "0"   # env normals loaded at step start
+HYBRID_ENABLED = os.environ.get("RTB200_LOOP_HYBRID", "1") != "0"   # widest layer's weights on chip
+HYBRID_KR = int(os.environ.get("RTB200_LOOP_HYBRID_KR", "128"))   # of its K rows, in registers
+HYBRID_NCOL = int(os.environ.get("RTB200_LOOP_HYBRID_NCOL", "2"))   # columns per thread = K parts
+
+
+def k2_eligible(rows_per_cta, re, q, f64):
+    """In-loop GEMMs that take tma_core2k (2 columns per thread, the two
+    thread halves splitting every chunk's k rows): fp32, N = 256 (= 2 x 128
+    threads), dense row-major B, <= 8 rows."""
+    mrp = (rows_per_cta * re + 3) // 4 * 4
+    dense_1d = q.N.nd == 1 and q.K.nd == 1 and q.Z.nd <= 1 and q.z == 1
+    return (K2_ENABLED and CORE2_NCOL == 2 and not f64 and dense_1d and mrp <= 8 and q.n == 256
+            and q.k >= 64 and q.B.s2[0] == 1 and q.B.s1[0] == q.n and q.B.dtype == N.RT_F32)
 
 
 def _same_gop(a, b):
@@ -684,7 +819,7 @@ def _same_gop(a, b):
             and all(a.off_env[e] == b.off_env[e] for e in range(N.RT_MAXENV)))
 
 
-def _forward_pairs(lp, ops):
+def _forward_pairs(lp, ops, info=None):
     """(i, i+1): GEMM op i+1 reads as its A exactly the rows GEMM op i just
     wrote as its C (h1 -> h2 -> mu of an MLP).  Op i's epilogue then also
     leaves its output in the A staging area, k-major, and op i+1 skips the
@@ -695,7 +830,11 @@ def _forward_pairs(lp, ops):
         (k1, p1, re1, f1, _n1, _s1), (k2, p2, re2, f2, _n2, _s2) = ops[i][:6], ops[i + 1][:6]
         if k1 != N.RT_K_GEMM or k2 != N.RT_K_GEMM or re1 != 1 or re2 != 1 or f1 or f2:
             continue
-        if _gemm_kind(lp, p1, re1, f1) != "tma" or (KS_ENABLED and lp.red_off):
+        # producers whose core ends with a CTA barrier: TMA-streamed, resident
+        # (res_core) and on-chip (hybrid: barrier added before a forward)
+        hy = (info or {}).get("hybrid")
+        on_chip = i in ((info or {}).get("resident") or {}) or (hy is not None and hy["op"] == i)
+        if (_gemm_kind(lp, p1, re1, f1) != "tma" and not on_chip) or (KS_ENABLED and lp.red_off):
             continue
         if not _same_gop(p1.C, p2.A):
             continue
@@ -774,9 +913,24 @@ def _opts():
             b"-I" + os.path.join(HERE, "csrc").encode()]
 
 
+def _headers_key():
+    """Digest of the csrc headers JIT sources include (a header edit must not
+    reuse a cubin cached for the same source text)."""
+    h = hashlib.sha256()
+    d = os.path.join(HERE, "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cuh", ".h")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(f.encode() + fh.read())
+    return h.hexdigest()
+
+
+_HDR_KEY = _headers_key()
+
+
 def compile_kernel(src: str, name: str) -> int:
     """CUfunction handle for `name` in `src` (process + on-disk cubin cache)."""
-    key = hashlib.sha256((src + name).encode()).hexdigest()
+    key = hashlib.sha256((src + name + _HDR_KEY).encode()).hexdigest()
     if key in _FN_CACHE:
         return _FN_CACHE[key]
     lib = N.lib()

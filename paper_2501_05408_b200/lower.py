@@ -541,15 +541,17 @@ class Lowering:
     PAIR_MIN_BYTES = 64 * 1024
     RESIDENT_MAX_BYTES = 32 * 1024
 
-    def _resident_ops(self, ops, rows, T, dim, base):
+    def _resident_ops(self, ops, rows, T, dim, base, wide=False, skip=None):
         """{op index: shared-memory offset} for in-loop GEMMs whose weights are
-        fp32, dense row-major, <= 32 KB and do not move with the loop dim."""
+        fp32, dense row-major, <= 32 KB and do not move with the loop dim
+        (wide layers only with `wide`: when the widest layer is on chip
+        (hybrid), nothing else keeps the TMA ring busy)."""
         from . import jit
         if not (jit.ENABLED and jit.RESIDENT_ENABLED) or rows * T < jit.JIT_LOOP_MIN:
             return {}, 0
         out, cur = {}, 0
         for i, (kernel, p, re, f64, _) in enumerate(ops):
-            if kernel != N.RT_K_GEMM or f64 or p.B.dtype != N.RT_F32:
+            if kernel != N.RT_K_GEMM or f64 or p.B.dtype != N.RT_F32 or i == skip:
                 continue
             if not (p.N.nd == 1 and p.K.nd == 1 and p.z == 1 and p.B.s2[0] == 1
                     and p.B.s1[0] == p.n and p.n % 4 == 0):
@@ -558,11 +560,38 @@ class Lowering:
                     any(p.B.off_env[e] % 4 for e in range(N.RT_MAXENV)):
                 continue
             nb = p.k * p.n * 4
-            if nb > self.RESIDENT_MAX_BYTES or p.n >= 64:
+            if nb > self.RESIDENT_MAX_BYTES or (p.n >= 64 and not wide):
                 continue   # (wide layers: the TMA-streamed core measured faster)
             out[i] = base + cur
             cur += (nb + 127) // 128 * 128
         return out, cur
+
+    def _hybrid_op(self, ops, R, rows, T, dim, dual):  # noqa: C901
+        """(op index, KR) for the in-loop GEMM whose weights stay on chip for
+        the whole loop split between registers and shared memory
+        (jit.py HYBRID_*: rows [0, KR) of B in KR registers per thread, one
+        column per thread; rows [KR, K) resident in shared memory), or None.
+        fp32, N = 256 = blockDim, dense row-major B that does not move with
+        the loop dim, one CTA per SM (the register budget)."""
+        from . import jit
+        if not (jit.ENABLED and jit.HYBRID_ENABLED) or dual or rows * T < jit.JIT_LOOP_MIN:
+            return None
+        best = None
+        for i, (kernel, p, re, f64, _) in enumerate(ops):
+            if kernel != N.RT_K_GEMM or f64 or p.B.dtype != N.RT_F32 or p.A.dtype != N.RT_F32 \
+                    or p.C.dtype != N.RT_F32 or (p.bias.ptr and p.bias.dtype != N.RT_F32):
+                continue
+            if not (p.N.nd == 1 and p.K.nd == 1 and p.z == 1 and p.B.s2[0] == 1
+                    and p.B.s1[0] == p.n and p.n == 256 and p.k >= jit.HYBRID_KR + 16 and p.k % jit.HYBRID_NCOL == 0
+                    and jit.HYBRID_NCOL in (1, 2, 4) and jit.HYBRID_KR % jit.HYBRID_NCOL == 0
+                    and (R * re + 3) // 4 * 4 <= 8):
+                continue
+            if p.B.off_env[self.slot[dim]] != 0 or (p.B.ptr + 4 * p.B.off) % 16 or \
+                    any(p.B.off_env[e] % 4 for e in range(N.RT_MAXENV)):
+                continue
+            if best is None or p.k > ops[best][1].k:
+                best = i
+        return None if best is None else (best, jit.HYBRID_KR, jit.HYBRID_NCOL)
 
     def _pair_op(self, ops, R, rows, T, dim):
         """Index of the in-loop GEMM to run in CTA-pair mode, or None: fp32,
@@ -652,13 +681,19 @@ class Lowering:
         a_off = cur
         # K-split in-loop GEMMs (jit.ks_eligible) sum per-warp partial tiles
         # through a [8 warps][rows][N] area before the weight ring
-        from .jit import KS_ENABLED, ks_eligible
+        from .jit import KS_ENABLED, ks_eligible, k2_eligible as jit_k2
+
+        def jit_wide():
+            return _jit.WIDE_RESIDENT
         red_bytes = 0
         for kernel, p, re, f64, _ in ops:
             if KS_ENABLED and kernel == N.RT_K_GEMM and p.n >= 64 and p.k >= 128 and \
                     ks_eligible(R, re, p, f64):
                 mrp = (R * re + 3) // 4 * 4
                 red_bytes = max(red_bytes, 8 * mrp * p.n * 4)
+            if kernel == N.RT_K_GEMM and jit_k2(R, re, p, f64):
+                mrp = (R * re + 3) // 4 * 4
+                red_bytes = max(red_bytes, mrp * p.n * 4)
         red_off = (a_off + a_need + 127) // 128 * 128
         # CTA-pair mode (jit._gemm_pair_literal): the largest in-loop weight
         # matrix stays resident, one K-half per SM of a 2-CTA cluster, instead
@@ -679,9 +714,38 @@ class Lowering:
         # (jit._gemm_literal resident=...): no per-step reload or stream
         resident, res_bytes = {}, 0
         res_base = (red_off + red_bytes + pair_bytes + 127) // 128 * 128
+        hy = None if pair is not None else self._hybrid_op(ops, R, rows, T, s.dim, dual)
         if pair is None:
-            resident, res_bytes = self._resident_ops(ops, rows, T, s.dim, res_base)
+            resident, res_bytes = self._resident_ops(ops, rows, T, s.dim, res_base,
+                                                     wide=hy is not None and jit_wide(),
+                                                     skip=None if hy is None else hy[0])
+        # the largest N=256 layer keeps its weights on chip: KR rows in
+        # registers, the rest in shared memory (when that leaves room for a
+        # small ring for the other streamed layers)
+        hybrid = None
+        if hy is not None:
+            hi, kr, nc = hy
+            q = ops[hi][1]
+            h_off = (res_base + res_bytes + 127) // 128 * 128
+            h_bytes = (q.k - kr) * q.n * 4
+            mrp = (R * ops[hi][2] + 3) // 4 * 4
+            r_bytes = (nc - 1) * mrp * q.n * 4
+            if h_off + h_bytes + r_bytes + 4 * 4096 <= 210 * 1024:
+                hybrid = {"op": hi, "kr": kr, "ncol": nc, "off": h_off, "red": h_off + h_bytes}
+                res_bytes = h_off + h_bytes + r_bytes - res_base
         ring_off = (res_base + res_bytes + 127) // 128 * 128
+        # env normals staged one step ahead (jit._udf_prefetch): 8 rows, in
+        # front of the ring (jit derives the ring stage from smem - ring_off)
+        nz_bytes = max([8 * 8 * sum(p.out_count[j] for j in range(p.nout))
+                        for k, p, *_r in ops if k == N.RT_K_UDF] + [0])
+        nz_off = 0
+        if nz_bytes:
+            nz_off = ring_off
+            ring_off = (nz_off + nz_bytes + 127) // 128 * 128
+        if hybrid is not None:
+            # the ring only feeds wide layers that are neither resident nor on chip
+            tma = any(k == N.RT_K_GEMM and p.n >= 64 and i not in resident and i != hybrid["op"]
+                      for i, (k, p, *_r) in enumerate(ops))
         stage = 0
         budget = (112 if dual else 210) * 1024
         if tma:
@@ -753,7 +817,8 @@ class Lowering:
         idx = self.add_rec(N.RT_K_LOOP, lp, [nct, 1, 1], [256, 1, 1], smem,
                            (first.id, f"loop[{s.dim}]"))
         self.loop_subs[idx] = {"ops": ops, "trips": T, "pair": pair_info,
-                               "ctas_per_sm": 2 if dual else 1, "resident": resident}
+                               "ctas_per_sm": 2 if dual else 1, "resident": resident,
+                               "hybrid": hybrid, "nz_off": nz_off, "nz_bytes": nz_bytes}
         if pair_info is not None:
             self.rec_cluster[idx] = 2
 

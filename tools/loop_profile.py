@@ -33,7 +33,18 @@ for ri, info in exe.loop_info.items():
     cyc = prof.cpu().tolist()
     tot = sum(cyc[:len(info["ops"])])
     print(f"loop record {ri}: rows={params.rows} rows_per_cta={params.rows_per_cta} "
-          f"smem={params.smem_bytes} trips={info['trips']}")
+          f"smem={params.smem_bytes} trips={info['trips']} hybrid={info.get('hybrid')}")
+    fn = getattr(exe.recs[ri], "jit_fn", 0)
+    if fn:
+        cu = C.CDLL("libcuda.so.1")
+        for name, attr in (("regs", 4), ("local_bytes", 3)):
+            v = C.c_int(0)
+            cu.cuFuncGetAttribute(C.byref(v), attr, C.c_void_p(fn))
+            print(f"  jit {name}: {v.value}")
+        from paper_2501_05408_b200 import jit as J
+        os.makedirs("gpurun_out", exist_ok=True)
+        with open(f"gpurun_out/loop_src_{ri}.cu", "w") as fh:
+            fh.write(J.loop_source(params, info["ops"], "loop_jit", info))
     for (k, q, re, f64, noise, *_), c in zip(info["ops"], cyc):
         print(f"  {RF.FAMILY.get(k):6s} row_elems={re:5d} cycles/step={c / info['trips']:10.0f} "
               f"share={100 * c / max(1, tot):5.1f}%")
