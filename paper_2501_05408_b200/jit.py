@@ -260,7 +260,9 @@ def loop_source(lp, ops, name, info=None):
     weights resident (one K-half per CTA, _gemm_pair_literal)."""
     pair = (info or {}).get("pair")
     fwd = _forward_pairs(lp, ops, info) if FORWARD_ENABLED and pair is None else set()
-    parts, step_pre = [], []
+    ew_fwd = _ew_forward_pairs(lp, ops) if FORWARD_ENABLED and pair is None else set()
+    fwd |= ew_fwd
+    parts, step_pre, pair_pre_bias = [], [], []
     for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
         if pair is not None and i == pair["op"]:
             parts.append(_gemm_pair_literal(lp, p, soff, pair))
@@ -287,6 +289,11 @@ def loop_source(lp, ops, name, info=None):
             regs = ", ".join(f"v{j}" for j in range(8))
             iregs = ", ".join(f"n{j}" for j in range(8))
             body = "\n        ".join(lines)
+            fwd_st = ""
+            if (i, i + 1) in ew_fwd:
+                mrp_n = (lp.rows_per_cta * ops[i + 1][2] + 3) // 4 * 4
+                fwd_st = (f"\n        {{ const int lf = (int)(flat - r0 * {re}LL); "
+                          f"sts1(sA32 + (uint32_t)(((lf % {re}) * {mrp_n} + lf / {re}) * 4), (float)res); }}")
             dec = "\n        ".join(_decompose(nd, ext))
             bl = "\n      ".join(bases)
             parts.append(f"""    {{  // op {i}: elementwise
@@ -300,13 +307,14 @@ def loop_source(lp, ops, name, info=None):
         (void)n0;
         {body}
       Lend{i}:
-        {_store(p, T, nd, "bo")}
+        {_store(p, T, nd, "bo")}{fwd_st}
       }}
     }}""".replace("goto Lend;", f"goto Lend{i};").replace("L", "L") .replace(
                 "goto L", f"goto X{i}L").replace(f"goto X{i}Lend{i}", f"goto Lend{i}"))
             # labels of this op are renamed to keep them unique per op
             parts[-1] = _rename_labels(parts[-1], i)
         elif kernel == N.RT_K_GEMM:
+            nparts = len(parts)
             hy = (info or {}).get("hybrid")
             if hy is not None and hy["op"] == i:
                 parts.append(_gemm_literal(lp, p, re, f64, soff, False, 0, (i - 1, i) in fwd,
@@ -315,6 +323,20 @@ def loop_source(lp, ops, name, info=None):
                 parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
                                         fwd_out=(i, i + 1) in fwd,
                                         resident=((info or {}).get("resident") or {}).get(i)))
+            boff_s = ((info or {}).get("bias_smem") or {}).get(i)
+            if boff_s is not None and len(parts) == nparts + 1:
+                bn = _gbox_off(p.N, [p.bias.s2[d] for d in range(4)], "n")
+                T_ = "double" if f64 else "float"
+                parts[-1] = parts[-1].replace(
+                    f"Bp_[boff + {bn}]",
+                    f"lds1(smem_u32(smem + {boff_s}) + (uint32_t)(n) * {8 if f64 else 4}u, ({T_})0)")
+                env_bias = _env_terms([p.bias.off_env[e] for e in range(N.RT_MAXENV)])
+                pair_pre_bias.append(f"""
+  {{  // loop-invariant bias of op {i}
+    const rt_gemm_params& q = *(const rt_gemm_params*)(smem + {soff});
+    const {T_}* Bp_ = (const {T_}*)q.bias.ptr; const long long boff = q.bias.off{env_bias};
+    for (long long n = threadIdx.x; n < {p.n}; n += blockDim.x) sts1(smem_u32(smem + {boff_s}) + (uint32_t)(n) * {8 if f64 else 4}u, Bp_[boff + {bn}]);
+  }}""")
         elif kernel == N.RT_K_UDF:
             if noise:
                 nz_off = (info or {}).get("nz_off")
@@ -351,6 +373,7 @@ def loop_source(lp, ops, name, info=None):
     for (int i = threadIdx.x; i < {q.k * q.n // 4}; i += blockDim.x) sts4(sB + 16u * (uint32_t)i, __ldg(Bg + i));
   }}
   __syncthreads();"""
+    bias_pro = "".join(pair_pre_bias) + "\n  __syncthreads();" if pair_pre_bias else ""
     hy = (info or {}).get("hybrid")
     if hy is not None:
         q = ops[hy["op"]][1]
@@ -400,6 +423,7 @@ extern "C" __global__ void __launch_bounds__(256, {per_sm}) {name}(const __grid_
   loop_ring ring;
   loop_prologue(p, smem, bars, ring);
   (void)sA32;
+{bias_pro}
 {pair_pro}
   long long c0 = clock64();
   for (long long t = {t0}; t {cmp} {t1}; t += {lp.step}LL) {{
@@ -596,10 +620,15 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
                   f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{",
                   f"  const long long n = {nc2} * (long long)threadIdx.x + j; if (n >= {Nn}) break;",
                   f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
+                  f"  float v[{mrp}];",
+                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ v[r] = 0.f; if (r < mr) {{ v[r] = acc[j][r] + bias;"
+                  + (" v[r] = vm_tanh<float>(v[r]);" if tanh else "") + " } }",
                   f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
-                  "    float v = acc[j][r] + bias;" + (" v = vm_tanh<float>(v);" if tanh else ""),
-                  f"    Cp[coff + {c_m} + {c_n}] = v;{fwd_store} }}",
-                  "} }"]
+                  f"    Cp[coff + {c_m} + {c_n}] = v[r]; }}"]
+        if fwd_out:
+            lines.append(f"  #pragma unroll\n  for (int r = 0; r < {mrp}; r += 4) sts4(sA32 + (uint32_t)((n * {mrp} + r) * 4), "
+                         f"make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]));")
+        lines.append("} }")
     elif tma and lp.red_off and KS_ENABLED and ks_eligible(lp.rows_per_cta, re, q, f64):
         opt = mrp * Nn // 256
         lines.append(f"{T} o[{opt}];")
@@ -798,6 +827,7 @@ PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes insid
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
 K2_ENABLED = os.environ.get("RTB200_LOOP_K2", "0") == "1"   # both thread halves on N=256 layers (measured: no gain)
 WIDE_RESIDENT = os.environ.get("RTB200_LOOP_WIDE_RESIDENT", "1") != "0"   # small wide layers resident when hybrid
+BIAS_SMEM = os.environ.get("RTB200_LOOP_BIAS_SMEM", "1") != "0"   # loop-invariant biases in shared memory
 UDF_PREFETCH = os.environ.get("RTB200_LOOP_UDF_PREFETCH", "1") != "0"   # env normals loaded at step start
 HYBRID_ENABLED = os.environ.get("RTB200_LOOP_HYBRID", "1") != "0"   # widest layer's weights on chip
 HYBRID_KR = int(os.environ.get("RTB200_LOOP_HYBRID_KR", "128"))   # of its K rows, in registers
@@ -844,6 +874,54 @@ def _forward_pairs(lp, ops, info=None):
         if any(p1.C.s1[d] != p2.A.s1[d] for d in range(p1.M.nd)) or p1.C.s2[0] != p2.A.s2[0]:
             continue
         out.add((i, i + 1))
+    return out
+
+
+def _gbox_eval(gb, strides, x):
+    """Python twin of _gbox_off: offset of flat index x over gbox gb."""
+    off = 0
+    for d in reversed(range(gb.nd)):
+        e = gb.ext[d]
+        if d == 0:
+            off += x * strides[d]
+        else:
+            off += (x % e) * strides[d]
+            x //= e
+    return off
+
+
+def _ew_forward_pairs(lp, ops):
+    """(i, i+1): elementwise op i writes exactly the A rows of GEMM op i+1
+    (same buffer view; element e of slab row r is A[r][e]).  Op i then also
+    leaves its output in the A staging area (k-major) and the GEMM skips
+    the global round trip (the observation copy feeding the first layer)."""
+    out = set()
+    for i in range(len(ops) - 1):
+        (k1, p1, re1, f1, _n1, _s1), (k2, p2, re2, f2, _n2, _s2) = ops[i][:6], ops[i + 1][:6]
+        if k1 != N.RT_K_EW or k2 != N.RT_K_GEMM or p1.f64 or f2 or re2 != 1:
+            continue
+        if p1.out.dtype != N.RT_F32 or p2.A.dtype != N.RT_F32 or re1 != p2.k or p2.K.nd != 1:
+            continue
+        if p1.out.ptr != p2.A.ptr or p1.out.off != p2.A.off or \
+                any(p1.out.off_env[e] != p2.A.off_env[e] for e in range(N.RT_MAXENV)):
+            continue
+        nd = p1.box.nd
+        ext = [p1.box.ext[d] for d in range(nd)]
+        rows = lp.rows
+
+        def ew_off(f):
+            o = 0
+            for d in reversed(range(nd)):
+                o += (f % ext[d]) * p1.out.stride[d]
+                f //= ext[d]
+            return o
+        s1 = [p2.A.s1[d] for d in range(4)]
+        s2 = [p2.A.s2[d] for d in range(4)]
+        ok = all(ew_off(r * re1 + e) == _gbox_eval(p2.M, s1, r) + _gbox_eval(p2.K, s2, e)
+                 for r in sorted({0, 1, rows // 2, rows - 1}) if 0 <= r < rows
+                 for e in sorted({0, 1, re1 - 1}) if 0 <= e < re1)
+        if ok:
+            out.add((i, i + 1))
     return out
 
 

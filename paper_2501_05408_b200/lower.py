@@ -742,6 +742,18 @@ class Lowering:
         if nz_bytes:
             nz_off = ring_off
             ring_off = (nz_off + nz_bytes + 127) // 128 * 128
+        # loop-invariant GEMM biases copied to shared memory once (their
+        # per-step global loads sat on each layer's epilogue critical path)
+        bias_smem = {}
+        from . import jit as _jit2
+        if _jit2.ENABLED and _jit2.BIAS_SMEM and rows * T >= _jit2.JIT_LOOP_MIN:
+            for i, (k, p, re, f64, _) in enumerate(ops):
+                if k != N.RT_K_GEMM or not p.bias.ptr or \
+                        p.bias.dtype != (N.RT_F64 if f64 else N.RT_F32) or \
+                        p.bias.off_env[self.slot[s.dim]] != 0:
+                    continue
+                bias_smem[i] = ring_off
+                ring_off = (ring_off + p.n * (8 if f64 else 4) + 127) // 128 * 128
         if hybrid is not None:
             # the ring only feeds wide layers that are neither resident nor on chip
             tma = any(k == N.RT_K_GEMM and p.n >= 64 and i not in resident and i != hybrid["op"]
@@ -818,7 +830,8 @@ class Lowering:
                            (first.id, f"loop[{s.dim}]"))
         self.loop_subs[idx] = {"ops": ops, "trips": T, "pair": pair_info,
                                "ctas_per_sm": 2 if dual else 1, "resident": resident,
-                               "hybrid": hybrid, "nz_off": nz_off, "nz_bytes": nz_bytes}
+                               "hybrid": hybrid, "nz_off": nz_off, "nz_bytes": nz_bytes,
+                               "bias_smem": bias_smem}
         if pair_info is not None:
             self.rec_cluster[idx] = 2
 
