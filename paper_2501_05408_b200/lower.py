@@ -829,6 +829,8 @@ class Lowering:
         idx = self.add_rec(N.RT_K_LOOP, lp, [nct, 1, 1], [256, 1, 1], smem,
                            (first.id, f"loop[{s.dim}]"))
         self.loop_subs[idx] = {"ops": ops, "trips": T, "pair": pair_info,
+                               # a time-blocked loop runs one block per launch
+                               "trips_per_launch": min(T, lp.blk_len) if lp.blk_len else T,
                                "ctas_per_sm": 2 if dual else 1, "resident": resident,
                                "hybrid": hybrid, "nz_off": nz_off, "nz_bytes": nz_bytes,
                                "bias_smem": bias_smem}

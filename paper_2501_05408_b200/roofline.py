@@ -45,7 +45,8 @@ def cost(kernel, p, loop_info=None):
             b2, f2 = cost(k, q)
             b += b2
             f += f2
-        return b * loop_info["trips"], f * loop_info["trips"]
+        n = loop_info.get("trips_per_launch", loop_info["trips"])
+        return b * n, f * n
     if kernel == N.RT_K_EW:
         box = [p.box.ext[i] for i in range(p.box.nd)]
         b = p.total * ITEM.get(p.out.dtype, 4)
