@@ -263,6 +263,7 @@ def loop_source(lp, ops, name, info=None):
     ew_fwd = _ew_forward_pairs(lp, ops) if FORWARD_ENABLED and pair is None else set()
     fwd |= ew_fwd
     parts, step_pre, pair_pre_bias = [], [], []
+    n_gemm = 0
     for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
         if pair is not None and i == pair["op"]:
             parts.append(_gemm_pair_literal(lp, p, soff, pair))
@@ -323,6 +324,12 @@ def loop_source(lp, ops, name, info=None):
                 parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
                                         fwd_out=(i, i + 1) in fwd,
                                         resident=((info or {}).get("resident") or {}).get(i)))
+            if GEMM_PHASES and n_gemm < 5:
+                for mk, j in (("/*PHASE_A*/", 0), ("/*PHASE_C*/", 1)):
+                    parts[-1] = parts[-1].replace(
+                        mk, f"if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {{ long long c1 = clock64(); "
+                            f"((long long*)p.prof)[{len(ops)} + {3 * n_gemm + j}] += c1 - c0; c0 = c1; }}")
+            n_gemm += 1
             boff_s = ((info or {}).get("bias_smem") or {}).get(i)
             if boff_s is not None and len(parts) == nparts + 1:
                 bn = _gbox_off(p.N, [p.bias.s2[d] for d in range(4)], "n")
@@ -541,6 +548,18 @@ def _gbox_off(gb, strides, var):
     return " + ".join(terms) if terms else "0LL"
 
 
+def _epi_rows(mrp, tanh):
+    """v[r] = act(acc[j][r] + bias) for the padded rows of a loop GEMM
+    epilogue; rows >= mr are zeroed by a select (no branch around the
+    activation, so the rows' tanh chains interleave)."""
+    if tanh and FAST_TANH:
+        return (f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ const float x_ = tanh_fast(acc[j][r] + bias); "
+                "v[r] = r < mr ? x_ : 0.f; }")
+    act = " v[r] = vm_tanh<float>(v[r]);" if tanh else ""
+    return (f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ v[r] = 0.f; if (r < mr) {{ v[r] = acc[j][r] + bias;"
+            + act + " } }")
+
+
 def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, resident=None,
                   hybrid=None):
     """Fully specialised loop GEMM: shapes, strides and decompositions baked,
@@ -595,7 +614,9 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
         red = f"smem_u32(smem + {hybrid['red']})" if nc > 1 else "0u"
         lines.append(f"float acc[{nc}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
+        lines.append("/*PHASE_A*/")
         lines.append(f"hyb_core<{mrp}, {K}, {Nn}, {nc}, {kr // nc}>(wreg, sB, sA32, {red}, acc);")
+        lines.append("/*PHASE_C*/")
         if fwd_out:
             lines.append("__syncthreads();   // every thread is done reading A before it is overwritten")
         lines += [f"if ((int)threadIdx.x < {Nn // nc}) {{",
@@ -603,8 +624,7 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
                   f"  const long long n = {nc} * (long long)threadIdx.x + j;",
                   f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
                   f"  float v[{mrp}];",
-                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ v[r] = 0.f; if (r < mr) {{ v[r] = acc[j][r] + bias;"
-                  + (" v[r] = vm_tanh<float>(v[r]);" if tanh else "") + " } }",
+                  _epi_rows(mrp, tanh),
                   f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
                   f"    Cp[coff + {c_m} + {c_n}] = v[r]; }}"]
         if fwd_out:
@@ -615,14 +635,15 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
         nc2 = 2 if Nn % 2 == 0 and Nn <= 512 else 1
         lines.append(f"float acc[{nc2}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
+        lines.append("/*PHASE_A*/")
         lines.append(f"res_core<{mrp}, {K}, {Nn}, {nc2}>(sB, sA32, acc);")
+        lines.append("/*PHASE_C*/")
         lines += [f"if ((int)threadIdx.x < {-(-Nn // nc2)}) {{",
                   f"#pragma unroll\nfor (int j = 0; j < {nc2}; ++j) {{",
                   f"  const long long n = {nc2} * (long long)threadIdx.x + j; if (n >= {Nn}) break;",
                   f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
                   f"  float v[{mrp}];",
-                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ v[r] = 0.f; if (r < mr) {{ v[r] = acc[j][r] + bias;"
-                  + (" v[r] = vm_tanh<float>(v[r]);" if tanh else "") + " } }",
+                  _epi_rows(mrp, tanh),
                   f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
                   f"    Cp[coff + {c_m} + {c_n}] = v[r]; }}"]
         if fwd_out:
@@ -677,8 +698,7 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
                   f"  const long long n = {nc2} * (long long)threadIdx.x + j;",
                   f"  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
                   f"  float v[{mrp}];",
-                  f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ v[r] = 0.f; if (r < mr) {{ v[r] = acc[j][r] + bias;"
-                  + (" v[r] = vm_tanh<float>(v[r]);" if tanh else "") + " } }",
+                  _epi_rows(mrp, tanh),
                   f"  #pragma unroll\n  for (int r = 0; r < {mrp}; ++r) {{ if (r >= mr) break; const long long m = m0 + r;",
                   f"    Cp[coff + {c_m} + {c_n}] = v[r]; }}",
                   fwd_vec,
@@ -824,6 +844,8 @@ CORE2_NCOL = int(os.environ.get("RTB200_LOOP_NCOL", "2"))   # columns per thread
 MMA_ENABLED = os.environ.get("RTB200_LOOP_MMA", "0") == "1"     # 3xTF32 mma.sync in-loop GEMMs (measured slower: 18.5k vs 15.6k cycles for h2)
 PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
 PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
+FAST_TANH = os.environ.get("RTB200_LOOP_FAST_TANH", "1") != "0"   # branch-free tanh in loop epilogues
+GEMM_PHASES = os.environ.get("RTB200_LOOP_GEMM_PHASES", "0") == "1"   # staging / core / epilogue probes
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
 K2_ENABLED = os.environ.get("RTB200_LOOP_K2", "0") == "1"   # both thread halves on N=256 layers (measured: no gain)
 WIDE_RESIDENT = os.environ.get("RTB200_LOOP_WIDE_RESIDENT", "1") != "0"   # small wide layers resident when hybrid

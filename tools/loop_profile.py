@@ -50,6 +50,9 @@ for ri, info in exe.loop_info.items():
               f"share={100 * c / max(1, tot):5.1f}%")
     print(f"  total cycles/step {tot / info['trips']:.0f}")
     extra = cyc[len(info["ops"]):]
+    if os.environ.get("RTB200_LOOP_GEMM_PHASES") == "1":
+        print("  gemm phases (cycles/step: op start..core start, core, [epilogue = the op line])",
+              [round(c / info["trips"]) for c in extra[:15]])
     if any(extra):
         print("  pair GEMM phases (cycles/step):",
               [round(c / info["trips"]) for c in extra[:6]])
