@@ -1068,7 +1068,10 @@ class Executable:
             item = ITEMSIZE_OF[h["dtype"]]
             t = _wrap_ptr(torch, h["ptr"] + off * item, h["count"] * item, self.dev)
             t = t.view(_TORCH_DT[h["dtype"]])
-            self.comm.allreduce_(t)
+            # NCCL orders the collective after torch's *current* stream:
+            # make that the stream the program runs on
+            with torch.cuda.stream(s):
+                self.comm.allreduce_(t)
 
     def profile(self, inputs, stream=None):
         """One run with an event pair around every launch: per-record device

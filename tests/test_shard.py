@@ -198,3 +198,40 @@ def _dry_shard(g, benv, shard):
     return L.Lowering(an["plan"], an["bufs"], 0, 0, lambda nb: 1 << 40, an["contract"],
                       an["fuse_src"], an["gemm_epi"], absorbed=an["absorbed"], shard=shard,
                       shard_reduce=red).lower()
+
+
+def _nccl_worker(port, q, B, T):
+    import torch.distributed as dist
+    from paper_2501_05408_b200 import execute
+    from paper_2501_05408_b200.shard import ShardSpec
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    g = load_graph("reinforce_mlp_c2")
+    side = torch.cuda.Stream()
+    outs = execute(g, bounds={"I": 1, "B": B, "T": T}, inputs=mlp_inputs(), seed=0,
+                   shard=ShardSpec("b", 0, 1), stream=side)
+    side.synchronize()
+    q.put({k: v for k, v in outs.items()})
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_run_over_nccl_on_a_side_stream():
+    """The sharded program's gradient all-reduce hooks over a real NCCL
+    communicator (one rank: the multi-GPU plumbing — hook segments, prefix
+    CUDA graph, the collective ordered on the program's own non-default
+    stream) reproduce the unsharded run."""
+    from paper_2501_05408_b200 import execute
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    B, T = 64, 32
+    full = execute(load_graph("reinforce_mlp_c2"), bounds={"I": 1, "B": B, "T": T},
+                   inputs=mlp_inputs(), seed=0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(free_port(), q, B, T))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    for k, want in full.items():
+        np.testing.assert_allclose(res[k], want, rtol=1e-5, atol=1e-6, err_msg=k)
