@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_gemm_tc(const __grid_constant
       int64_t oc = rowC[r] + colC[c];
       if (p.accumulate) x += ((const float*)p.C.ptr)[oc];
       if (p.bias.ptr) x += load_as<float>((const void*)p.bias.ptr, p.bias.dtype, colBias[c]);
-      if (p.epilogue == 1) x = tanhf(x);
+      if (p.epilogue == 1) x = tanh_fast(x);
       ((float*)p.C.ptr)[oc] = x;
     }
   }

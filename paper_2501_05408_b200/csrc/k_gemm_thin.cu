@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
         T* cptr = cbase + coff[rr];
         if (acc_in) a += *cptr;
         a += b;
-        if (tanh_epi) a = vm_tanh<T>(a);
+        if (tanh_epi) a = epi_tanh<T>(a);
         __stcs(cptr, a);
       }
     }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
         T a = mine;
         if (p.accumulate) a += *cptr;
         a += bias[r];
-        if (p.epilogue == 1) a = vm_tanh<T>(a);
+        if (p.epilogue == 1) a = epi_tanh<T>(a);
         *cptr = a;
       }
     }

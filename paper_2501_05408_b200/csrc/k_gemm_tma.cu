@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
         if (p.accumulate) x[j] += Cp[rowoff + n * a.c_n];
         if (p.bias.ptr)
           x[j] += load_as<float>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + n * a.bias_n);
-        if (p.epilogue == 1) x[j] = tanhf(x[j]);
+        if (p.epilogue == 1) x[j] = tanh_fast(x[j]);
       }
       if (vec && n0 + c0 + 16 <= p.n) {
         float4* dst = (float4*)(Cp + rowoff + n0 + c0);

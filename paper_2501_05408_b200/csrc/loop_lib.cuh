@@ -73,25 +73,6 @@ RT_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 #define RING 4
 
-// ---------------------------------------------------------------- tanh
-// Branch-free fp32 tanh for the in-loop layer epilogues: |x| < 0.55 an odd
-// polynomial (least-squares fit of (tanh(x)/x - 1)/x^2 in x^2, degree 4),
-// else 1 - 2/(e^{2|x|} + 1).  Max relative error 3e-7 (2-3 ulp; libdevice
-// tanhf: 1-2 ulp) against the 1e-5 parity bar; with no branch the 14 tanh
-// of a thread's epilogue interleave (libdevice's branchy tanhf serialised
-// them: ~1.9 k cycles per layer per step, loop_profile GEMM phases).
-RT_DEV float tanh_fast(float x) {
-  const float ax = fabsf(x), u = x * x;
-  float p = fmaf(-0.013635578565299511f, u, 0.026972131803631783f);
-  p = fmaf(p, u, -0.055414460599422455f);
-  p = fmaf(p, u, 0.13347633183002472f);
-  p = fmaf(p, u, -0.3333369195461273f);
-  const float small = fmaf(ax * u, p, ax);
-  const float e = __expf(2.f * fminf(ax, 20.f));
-  const float big = 1.f - __fdividef(2.f, e + 1.f);
-  return copysignf(ax < 0.55f ? small : big, x);
-}
-
 // ---------------------------------------------------------------- cp.async
 // 8-byte global -> shared async copies (LDGSTS): completion is tracked per
 // thread by commit groups, not by register scoreboards.
@@ -1185,8 +1166,13 @@ RT_DEV void sts_cols(uint32_t a, const float (&x)[NC]) {
 // thread of a part) by NCOL.  Parts p > 0 hand their partial sums to part
 // 0 through red ([P-1][MRP][N] floats); the final sums are in threads
 // < N / NCOL.  A is k-major in sA (MRP rows per k).
-template <int MRP, int K, int N, int NCOL, int KRP>
-RT_DEV void hyb_core(const float (&w)[NCOL][KRP], uint32_t sB, uint32_t sA, uint32_t red,
+//
+// SPLIT (P = 2, MRP = 8): the two parts instead finalise half of the rows
+// each (part p keeps rows [4p, 4p+4) in acc[j][0..3]) so the epilogue
+// (bias, tanh, stores) runs on all eight warps.  KRP = 0: no register rows
+// (a shared-memory resident layer such as W1 through the same core).
+template <int MRP, int K, int N, int NCOL, int KRP, bool SPLIT = false>
+RT_DEV void hyb_core(const float (&w)[NCOL][KRP > 0 ? KRP : 1], uint32_t sB, uint32_t sA, uint32_t red,
                      float (&acc)[NCOL][MRP]) {
   constexpr int P = NCOL, HT = N / NCOL, KP = K / P, KS = KP - KRP;
   static_assert(K % P == 0 && KS >= 0, "K splits evenly over the parts");
@@ -1209,7 +1195,26 @@ RT_DEV void hyb_core(const float (&w)[NCOL][KRP], uint32_t sB, uint32_t sA, uint
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a, b[j]);
   }
-  if constexpr (P > 1) {
+  if constexpr (SPLIT) {
+    static_assert(P == 2 && MRP == 8, "row-split finalisation: two parts, 8 rows");
+    constexpr int H = MRP / 2;
+    // part p hands the other part's rows to red[p][rr][n], keeps its own
+#pragma unroll
+    for (int rr = 0; rr < H; ++rr) {
+      float x[NCOL];
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) x[j] = part == 0 ? acc[j][H + rr] : acc[j][rr];
+      sts_cols<NCOL>(red + (uint32_t)(((part * H + rr) * N + c0) * 4), x);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < H; ++rr) {
+      float x[NCOL];
+      lds_cols<NCOL>(red + (uint32_t)((((1 - part) * H + rr) * N + c0) * 4), x);
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) acc[j][rr] = (part == 0 ? acc[j][rr] : acc[j][H + rr]) + x[j];
+    }
+  } else if constexpr (P > 1) {
     if (part > 0) {
 #pragma unroll
       for (int r = 0; r < MRP; ++r) {

@@ -323,7 +323,8 @@ def loop_source(lp, ops, name, info=None):
             else:
                 parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
                                         fwd_out=(i, i + 1) in fwd,
-                                        resident=((info or {}).get("resident") or {}).get(i)))
+                                        resident=((info or {}).get("resident") or {}).get(i),
+                                        split_red=None if hy is None or hy["ncol"] != 2 else hy["red"]))
             if GEMM_PHASES and n_gemm < 5:
                 for mk, j in (("/*PHASE_A*/", 0), ("/*PHASE_C*/", 1)):
                     parts[-1] = parts[-1].replace(
@@ -560,8 +561,27 @@ def _epi_rows(mrp, tanh):
             + act + " } }")
 
 
+def _split_epilogue(mrp, tanh, has_bias, bias_n, c_m, c_n, fwd_out):
+    """Epilogue after hyb_core<..., SPLIT>: thread t of part p = t / 128
+    holds columns 2 (t % 128) + {0, 1} of rows [4p, 4p + 4) in acc[j][0..3]."""
+    act = "tanh_fast(acc[j][rr] + bias)" if tanh and FAST_TANH else \
+        ("vm_tanh<float>(acc[j][rr] + bias)" if tanh else "acc[j][rr] + bias")
+    lines = ["{ const int part_ = (int)threadIdx.x / 128; const int rlo = part_ * 4;",
+             "#pragma unroll\nfor (int j = 0; j < 2; ++j) {",
+             "  const long long n = 2 * (long long)(threadIdx.x % 128) + j;",
+             "  const float bias = " + (f"Bp_[boff + {bias_n}];" if has_bias else "0.f;"),
+             "  float v[4];",
+             f"  #pragma unroll\n  for (int rr = 0; rr < 4; ++rr) {{ const float x_ = {act}; v[rr] = rlo + rr < mr ? x_ : 0.f; }}",
+             "  #pragma unroll\n  for (int rr = 0; rr < 4; ++rr) { if (rlo + rr >= mr) break; const long long m = m0 + rlo + rr;",
+             f"    Cp[coff + {c_m} + {c_n}] = v[rr]; }}"]
+    if fwd_out:
+        lines.append(f"  sts4(sA32 + (uint32_t)((n * {mrp} + rlo) * 4), make_float4(v[0], v[1], v[2], v[3]));")
+    lines.append("} }")
+    return lines
+
+
 def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, resident=None,
-                  hybrid=None):
+                  hybrid=None, split_red=None):
     """Fully specialised loop GEMM: shapes, strides and decompositions baked,
     descriptor pointers read once into registers."""
     T = "double" if f64 else "float"
@@ -614,6 +634,12 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
         red = f"smem_u32(smem + {hybrid['red']})" if nc > 1 else "0u"
         lines.append(f"float acc[{nc}][{mrp}];")
         lines.append(f"#pragma unroll\nfor (int j = 0; j < {nc}; ++j) {{\n#pragma unroll\nfor (int r = 0; r < {mrp}; ++r) acc[j][r] = 0.f; }}")
+        if SPLIT_EPI and nc == 2 and mrp == 8 and Nn == 256:
+            lines.append("/*PHASE_A*/")
+            lines.append(f"hyb_core<{mrp}, {K}, {Nn}, {nc}, {kr // nc}, true>(wreg, sB, sA32, {red}, acc);")
+            lines.append("/*PHASE_C*/")
+            lines += _split_epilogue(mrp, tanh, has_bias, bias_n, c_m, c_n, fwd_out)
+            return "    {  // gemm (specialised)\n      " + "\n      ".join(lines) + "\n    }"
         lines.append("/*PHASE_A*/")
         lines.append(f"hyb_core<{mrp}, {K}, {Nn}, {nc}, {kr // nc}>(wreg, sB, sA32, {red}, acc);")
         lines.append("/*PHASE_C*/")
@@ -631,6 +657,15 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
             lines.append(f"  #pragma unroll\n  for (int r = 0; r < {mrp}; r += 4) sts4(sA32 + (uint32_t)((n * {mrp} + r) * 4), "
                          f"make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]));")
         lines.append("} }")
+    elif resident is not None and split_red is not None and SPLIT_EPI and not f64 and Nn == 256 \
+            and mrp == 8 and K % 2 == 0:
+        lines.append("float acc[2][8];")
+        lines.append("#pragma unroll\nfor (int j = 0; j < 2; ++j) {\n#pragma unroll\nfor (int r = 0; r < 8; ++r) acc[j][r] = 0.f; }")
+        lines.append("float wdum_[2][1];")
+        lines.append("/*PHASE_A*/")
+        lines.append(f"hyb_core<8, {K}, 256, 2, 0, true>(wdum_, sB, sA32, smem_u32(smem + {split_red}), acc);")
+        lines.append("/*PHASE_C*/")
+        lines += _split_epilogue(mrp, tanh, has_bias, bias_n, c_m, c_n, fwd_out)
     elif resident is not None and Nn >= 16:
         nc2 = 2 if Nn % 2 == 0 and Nn <= 512 else 1
         lines.append(f"float acc[{nc2}][{mrp}];")
@@ -844,6 +879,7 @@ CORE2_NCOL = int(os.environ.get("RTB200_LOOP_NCOL", "2"))   # columns per thread
 MMA_ENABLED = os.environ.get("RTB200_LOOP_MMA", "0") == "1"     # 3xTF32 mma.sync in-loop GEMMs (measured slower: 18.5k vs 15.6k cycles for h2)
 PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
 PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
+SPLIT_EPI = os.environ.get("RTB200_LOOP_SPLIT_EPI", "1") != "0"   # 2-part cores finalise half the rows each
 FAST_TANH = os.environ.get("RTB200_LOOP_FAST_TANH", "1") != "0"   # branch-free tanh in loop epilogues
 GEMM_PHASES = os.environ.get("RTB200_LOOP_GEMM_PHASES", "0") == "1"   # staging / core / epilogue probes
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
@@ -966,7 +1002,7 @@ FORWARD_ENABLED = os.environ.get("RTB200_LOOP_FORWARD", "1") != "0"
 RESIDENT_ENABLED = os.environ.get("RTB200_LOOP_RESIDENT", "1") != "0"
 
 
-def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False, resident=None):
+def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False, resident=None, split_red=None):
     """Pick a shape-specialised GEMM body for a persistent-loop op."""
     T = "double" if f64 else "float"
     it = 8 if f64 else 4
@@ -980,7 +1016,8 @@ def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False, resident=None)
     tdt = N.RT_F64 if f64 else N.RT_F32
     same_dt = q.A.dtype == tdt and q.C.dtype == tdt and (not q.bias.ptr or q.bias.dtype == tdt)
     if resident is not None and same_dt and mrp <= 8:
-        return _gemm_literal(lp, q, re, f64, soff, False, 0, fwd_in, fwd_out, resident)
+        return _gemm_literal(lp, q, re, f64, soff, False, 0, fwd_in, fwd_out, resident,
+                             split_red=split_red)
     if dense_1d and b_dt and mrp <= 8 and 64 <= Nn <= (256 if f64 else 512) and stage and \
             q.B.s2[0] == 1 and q.B.s1[0] == Nn and aligned and (Nn * it) % 16 == 0:
         kc = max(1, min(K, stage // (Nn * it)))
