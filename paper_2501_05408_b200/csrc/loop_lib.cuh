@@ -79,6 +79,9 @@ RT_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
 RT_DEV void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
+RT_DEV void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
 RT_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 RT_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 

@@ -72,8 +72,9 @@ def _valid_expr(pfx, v, nd, c0=None):
     return " && ".join(conds) if conds else "true"
 
 
-def _program_lines(p, T, nd, base=None, chk=None, env="p.h.env"):
-    """Straight-line C statements for the VM program of EW params p."""
+def _program_lines(p, T, nd, base=None, chk=None, env="p.h.env", load_override=None):
+    """Straight-line C statements for the VM program of EW params p
+    (load_override: {input k: expression} for unchecked LOADs of input k)."""
     code = [p.code[i] for i in range(N.RT_CODE)]
     targets = set()
     pc, end = 0, 0
@@ -135,6 +136,10 @@ def _program_lines(p, T, nd, base=None, chk=None, env="p.h.env"):
                 off = f"{off} + n{a}"
                 valid = f"(n{b} != 0) && {valid}"
             ct = CT[v.dtype]
+            if o == "LOAD" and load_override and imm in load_override and valid == "true":
+                w(f"v{d} = {load_override[imm]};")
+                pc += 2
+                continue
             load = f"(({T})((const {ct}*){pfx}.ptr)[{off}])"
             if v.dtype == N.RT_BOOL:
                 load = f"(((const unsigned char*){pfx}.ptr)[{off}] ? ({T})1 : ({T})0)"
@@ -262,8 +267,10 @@ def loop_source(lp, ops, name, info=None):
     fwd = _forward_pairs(lp, ops, info) if FORWARD_ENABLED and pair is None else set()
     ew_fwd = _ew_forward_pairs(lp, ops) if FORWARD_ENABLED and pair is None else set()
     fwd |= ew_fwd
+    xfwd = _gemm_ew_forwards(lp, ops, info) if pair is None else {}
+    xfwd_src = {g: e for e, (_k, g) in xfwd.items()}
     parts, step_pre, pair_pre_bias = [], [], []
-    n_gemm = 0
+    n_gemm = n_xpf = 0
     for i, (kernel, p, re, f64, noise, soff) in enumerate(ops):
         if pair is not None and i == pair["op"]:
             parts.append(_gemm_pair_literal(lp, p, soff, pair))
@@ -285,8 +292,38 @@ def loop_source(lp, ops, name, info=None):
                         f"p.in[{k}].chk_c0[{c}]", [v.chk_env[c][e] for e in range(N.RT_MAXENV)]) + ";")
             bases.append("const long long bo = " + _env_fold(
                 "p.out.off", [p.out.off_env[e] for e in range(N.RT_MAXENV)]) + ";")
+            ov = None
+            if i in xfwd and not p.f64:
+                kx = xfwd[i][0]
+                ov = {kx: f"lds1(smem_u32(smem + {info['xfwd_off']}) + (uint32_t)((int)(flat - r0 * {re}LL) * 4), 0.f)"}
+            # operands no loop op writes (pre-drawn normals): staged one step
+            # ahead by cp.async; the first step reads them from global
+            pf_pre, pf_post = "", ""
+            # (time-varying ones only; each (op, operand) its own slot row)
+            xpf = [k for k in ((info or {}).get("ext_in") or {}).get(i, [])
+                   if EW_PREFETCH and not p.f64 and p.in_[k].dtype == N.RT_F32 and not p.in_[k].nchk
+                   and p.in_[k].off_env[lp.slot] != 0 and (ov is None or k not in ov)]
+            xpf = xpf[:max(0, XPF_SLOTS - n_xpf)]
+            if xpf and (info or {}).get("xpf_off") and lp.rows_per_cta * re <= 256 and pair is None:
+                ov = dict(ov or {})
+                t_first = "p.start" if lp.blk_len else f"{lp.start}LL"
+                t_stop = "p.stop" if lp.blk_len else f"{lp.stop}LL"
+                cmp_ = "<" if lp.step > 0 else ">"
+                for si0, k in enumerate(xpf):
+                    si = n_xpf + si0
+                    v = p.in_[k]
+                    off = _offset_expr(f"b{k}", v, nd)
+                    slot = (f"smem_u32(smem + {info['xpf_off']}) + (uint32_t)(({si * 256} + "
+                            f"(int)(flat - r0 * {re}LL)) * 4)")
+                    ov[k] = f"(t == {t_first} ? ((const float*)p.in[{k}].ptr)[{off}] : lds1({slot}, 0.f))"
+                    step_off = v.off_env[lp.slot] * lp.step
+                    pf_post += (f"\n        if (t + {lp.step}LL {cmp_} {t_stop}) cp_async4({slot}, "
+                                f"(const float*)p.in[{k}].ptr + ({off} + {step_off}LL));")
+                n_xpf += len(xpf)
+                pf_pre = f"if (t != {t_first}) cp_async_wait_all();"
+                pf_post += "\n        cp_async_commit();"
             lines = _program_lines(p, T, nd, base=lambda k: f"b{k}",
-                                   chk=lambda k, c: f"c{k}_{c}", env="env")
+                                   chk=lambda k, c: f"c{k}_{c}", env="env", load_override=ov)
             regs = ", ".join(f"v{j}" for j in range(8))
             iregs = ", ".join(f"n{j}" for j in range(8))
             body = "\n        ".join(lines)
@@ -301,6 +338,7 @@ def loop_source(lp, ops, name, info=None):
       const rt_ew_params& p = *(const rt_ew_params*)(smem + {soff});
       {bl}
       for (long long flat = r0 * {re}LL + threadIdx.x; flat < r1 * {re}LL; flat += blockDim.x) {{
+        {pf_pre}
         {dec}
         {T} {regs};
         long long {iregs};
@@ -308,7 +346,7 @@ def loop_source(lp, ops, name, info=None):
         (void)n0;
         {body}
       Lend{i}:
-        {_store(p, T, nd, "bo")}{fwd_st}
+        {_store(p, T, nd, "bo")}{fwd_st}{pf_post}
       }}
     }}""".replace("goto Lend;", f"goto Lend{i};").replace("L", "L") .replace(
                 "goto L", f"goto X{i}L").replace(f"goto X{i}Lend{i}", f"goto Lend{i}"))
@@ -324,7 +362,8 @@ def loop_source(lp, ops, name, info=None):
                 parts.append(_gemm_call(lp, p, re, f64, soff, fwd_in=(i - 1, i) in fwd,
                                         fwd_out=(i, i + 1) in fwd,
                                         resident=((info or {}).get("resident") or {}).get(i),
-                                        split_red=None if hy is None or hy["ncol"] != 2 else hy["red"]))
+                                        split_red=None if hy is None or hy["ncol"] != 2 else hy["red"],
+                                        ew_fwd=(info or {}).get("xfwd_off") if i in xfwd_src else None))
             if GEMM_PHASES and n_gemm < 5:
                 for mk, j in (("/*PHASE_A*/", 0), ("/*PHASE_C*/", 1)):
                     parts[-1] = parts[-1].replace(
@@ -581,7 +620,7 @@ def _split_epilogue(mrp, tanh, has_bias, bias_n, c_m, c_n, fwd_out):
 
 
 def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, resident=None,
-                  hybrid=None, split_red=None):
+                  hybrid=None, split_red=None, ew_fwd=None):
     """Fully specialised loop GEMM: shapes, strides and decompositions baked,
     descriptor pointers read once into registers."""
     T = "double" if f64 else "float"
@@ -760,10 +799,20 @@ def _gemm_literal(lp, q, re, f64, soff, tma, kc=0, fwd_in=False, fwd_out=False, 
                   f"  const bool act = o < {outs} && (o / {Nn}) < mr;",
                   f"  const int r = act ? o / {Nn} : 0; const long long n = act ? o % {Nn} : 0;",
                   f"  {T} a = ({T})0;",
-                  f"  if (act) {{\n#pragma unroll 4\n    for (int k = lane_in; k < {K}; k += {G}) a = fma(lds1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), ({T})0), lds1(sB + (uint32_t)((k * {Nn} + n) * sizeof({T})), ({T})0), a); }}",
+                  (f"  if (act) {{\n#pragma unroll 4\n    for (int k = lane_in; k < {K}; k += {G}) a = fma(lds1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), ({T})0), lds1(sB + (uint32_t)((k * {Nn} + n) * sizeof({T})), ({T})0), a); }}"
+                   if K % (4 * G) or not HEAD_ILP else
+                   # four partial sums: a 4x shorter dependent FMA chain
+                   f"  if (act) {{ {T} a1 = ({T})0, a2 = ({T})0, a3 = ({T})0;\n#pragma unroll 2\n    for (int k = lane_in; k < {K}; k += {4 * G}) {{"
+                   f" a = fma(lds1(sA32 + (uint32_t)((k * {mrp} + r) * sizeof({T})), ({T})0), lds1(sB + (uint32_t)((k * {Nn} + n) * sizeof({T})), ({T})0), a);"
+                   f" a1 = fma(lds1(sA32 + (uint32_t)(((k + {G}) * {mrp} + r) * sizeof({T})), ({T})0), lds1(sB + (uint32_t)(((k + {G}) * {Nn} + n) * sizeof({T})), ({T})0), a1);"
+                   f" a2 = fma(lds1(sA32 + (uint32_t)(((k + {2 * G}) * {mrp} + r) * sizeof({T})), ({T})0), lds1(sB + (uint32_t)(((k + {2 * G}) * {Nn} + n) * sizeof({T})), ({T})0), a2);"
+                   f" a3 = fma(lds1(sA32 + (uint32_t)(((k + {3 * G}) * {mrp} + r) * sizeof({T})), ({T})0), lds1(sB + (uint32_t)(((k + {3 * G}) * {Nn} + n) * sizeof({T})), ({T})0), a3); }}"
+                   " a = (a + a1) + (a2 + a3); }"),
                   f"  #pragma unroll\n  for (int s = {G // 2}; s > 0; s >>= 1) a += __shfl_down_sync(0xffffffffu, a, s, {G});",
                   f"  if (act && lane_in == 0) {{ const long long m = m0 + r; {T} v = a" + (f" + Bp_[boff + {bias_n}]" if has_bias else "") + ";"
-                  + (f" v = vm_tanh<{T}>(v);" if tanh else "") + f" Cp[coff + {c_m} + {c_n}] = v; }}",
+                  + (f" v = vm_tanh<{T}>(v);" if tanh else "") + f" Cp[coff + {c_m} + {c_n}] = v;"
+                  + (f" sts1(smem_u32(smem + {ew_fwd}) + (uint32_t)((r * {Nn} + n) * sizeof({T})), v);" if ew_fwd is not None else "")
+                  + " }",
                   "}"]
     return "    {  // gemm (specialised)\n      " + "\n      ".join(lines) + "\n    }"
 
@@ -880,6 +929,9 @@ MMA_ENABLED = os.environ.get("RTB200_LOOP_MMA", "0") == "1"     # 3xTF32 mma.syn
 PAIR_ENABLED = os.environ.get("RTB200_LOOP_PAIR", "0") == "1"   # measured: no gain at E=1024 (profiles/README.md)
 PHASES = os.environ.get("RTB200_LOOP_PHASES", "0") == "1"   # clock probes inside the pair GEMM
 SPLIT_EPI = os.environ.get("RTB200_LOOP_SPLIT_EPI", "1") != "0"   # 2-part cores finalise half the rows each
+HEAD_ILP = os.environ.get("RTB200_LOOP_HEAD_ILP", "0") == "1"   # 4 partial sums in narrow-N loop GEMMs (measured slower)
+XPF_SLOTS = 2   # staged operand rows (lower.py reserves 2 x 256 floats)
+EW_PREFETCH = os.environ.get("RTB200_LOOP_EW_PREFETCH", "1") != "0"   # loop-external EW operands one step ahead
 FAST_TANH = os.environ.get("RTB200_LOOP_FAST_TANH", "1") != "0"   # branch-free tanh in loop epilogues
 GEMM_PHASES = os.environ.get("RTB200_LOOP_GEMM_PHASES", "0") == "1"   # staging / core / epilogue probes
 KS_ENABLED = os.environ.get("RTB200_LOOP_KSPLIT", "0") == "1"   # measured slower (profiles/README.md)
@@ -983,6 +1035,49 @@ def _ew_forward_pairs(lp, ops):
     return out
 
 
+def _gemm_ew_forwards(lp, ops, info):
+    """{i + 1: (k, i)}: narrow in-loop GEMM op i (resident weights, N < 16:
+    the policy head) whose output is input k of elementwise op i + 1 at the
+    same (row, column) points; op i also leaves its rows in shared memory
+    (info["xfwd_off"], [rows][N]) and op i + 1 reads them there instead of
+    waiting on an L2 round trip."""
+    out = {}
+    res = (info or {}).get("resident") or {}
+    if not (info or {}).get("xfwd_off") or not FORWARD_ENABLED:
+        return out
+    for i in range(len(ops) - 1):
+        (k1, q, re1, f1, _n1, _s1), (k2, p2, re2, _f2, _n2, _s2) = ops[i][:6], ops[i + 1][:6]
+        if k1 != N.RT_K_GEMM or k2 != N.RT_K_EW or f1 or p2.f64 or i not in res or q.n >= 16:
+            continue
+        mrp = (lp.rows_per_cta * re1 + 3) // 4 * 4
+        if re1 != 1 or mrp > 8 or re2 != q.n or q.n * mrp > 8 * 32 or q.C.dtype != N.RT_F32 or \
+                q.A.dtype != N.RT_F32 or (q.bias.ptr and q.bias.dtype != N.RT_F32) or q.N.nd != 1:
+            continue
+        nd = p2.box.nd
+        ext = [p2.box.ext[d] for d in range(nd)]
+        for kk in range(p2.nin):
+            v = p2.in_[kk]
+            if v.dtype != N.RT_F32 or v.nchk or v.ptr != q.C.ptr or v.off != q.C.off or \
+                    any(v.off_env[e] != q.C.off_env[e] for e in range(N.RT_MAXENV)):
+                continue
+
+            def ew_off(f):
+                o = 0
+                for d in reversed(range(nd)):
+                    o += (f % ext[d]) * v.stride[d]
+                    f //= ext[d]
+                return o
+            s1 = [q.C.s1[d] for d in range(4)]
+            s2 = [q.C.s2[d] for d in range(4)]
+            rows = lp.rows
+            if all(ew_off(r * re2 + e) == _gbox_eval(q.M, s1, r) + _gbox_eval(q.N, s2, e)
+                   for r in sorted({0, 1, rows // 2, rows - 1}) if 0 <= r < rows
+                   for e in range(re2)):
+                out[i + 1] = (kk, i)
+                break
+    return out
+
+
 def _gemm_kind(lp, q, re, f64):
     it = 8 if f64 else 4
     mrp = (lp.rows_per_cta * re + 3) // 4 * 4
@@ -1002,7 +1097,8 @@ FORWARD_ENABLED = os.environ.get("RTB200_LOOP_FORWARD", "1") != "0"
 RESIDENT_ENABLED = os.environ.get("RTB200_LOOP_RESIDENT", "1") != "0"
 
 
-def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False, resident=None, split_red=None):
+def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False, resident=None, split_red=None,
+               ew_fwd=None):
     """Pick a shape-specialised GEMM body for a persistent-loop op."""
     T = "double" if f64 else "float"
     it = 8 if f64 else 4
@@ -1017,7 +1113,7 @@ def _gemm_call(lp, q, re, f64, soff, fwd_in=False, fwd_out=False, resident=None,
     same_dt = q.A.dtype == tdt and q.C.dtype == tdt and (not q.bias.ptr or q.bias.dtype == tdt)
     if resident is not None and same_dt and mrp <= 8:
         return _gemm_literal(lp, q, re, f64, soff, False, 0, fwd_in, fwd_out, resident,
-                             split_red=split_red)
+                             split_red=split_red, ew_fwd=ew_fwd)
     if dense_1d and b_dt and mrp <= 8 and 64 <= Nn <= (256 if f64 else 512) and stage and \
             q.B.s2[0] == 1 and q.B.s1[0] == Nn and aligned and (Nn * it) % 16 == 0:
         kc = max(1, min(K, stage // (Nn * it)))

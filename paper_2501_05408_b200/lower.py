@@ -742,6 +742,30 @@ class Lowering:
         if nz_bytes:
             nz_off = ring_off
             ring_off = (nz_off + nz_bytes + 127) // 128 * 128
+        # EW operands read from buffers no op of this loop writes
+        written = set()
+        for (kernel, p, grid, block, smem_, label) in subs:
+            nd_ = self.g.nodes.get(label[0]) if isinstance(label, tuple) else None
+            for oid in range(len(nd_.out_shapes) if nd_ is not None else 0):
+                try:
+                    written.add(id(self.storage((label[0], oid))))
+                except Exception:
+                    pass
+        ext_in = {}
+        for i, (kernel, p, re, f64, _) in enumerate(ops):
+            keys = p.__dict__.get("in_keys") if kernel == N.RT_K_EW else None
+            if keys:
+                try:
+                    ext_in[i] = [k for k, key in enumerate(keys)
+                                 if id(self.storage(key)) not in written]
+                except Exception:
+                    pass
+        # narrow GEMM outputs forwarded to the next elementwise op (8 rows x
+        # <= 32 columns) and loop-external elementwise inputs staged one step
+        # ahead (256 threads x 4 inputs x 8 B): jit._ew_stage_plan
+        xfwd_off = ring_off
+        xpf_off = xfwd_off + 8 * 32 * 4
+        ring_off = (xpf_off + 256 * 4 * 2 + 127) // 128 * 128
         # loop-invariant GEMM biases copied to shared memory once (their
         # per-step global loads sat on each layer's epilogue critical path)
         bias_smem = {}
@@ -833,7 +857,8 @@ class Lowering:
                                "trips_per_launch": min(T, lp.blk_len) if lp.blk_len else T,
                                "ctas_per_sm": 2 if dual else 1, "resident": resident,
                                "hybrid": hybrid, "nz_off": nz_off, "nz_bytes": nz_bytes,
-                               "bias_smem": bias_smem}
+                               "bias_smem": bias_smem, "xfwd_off": xfwd_off, "xpf_off": xpf_off,
+                               "ext_in": ext_in}
         if pair_info is not None:
             self.rec_cluster[idx] = 2
 
@@ -945,6 +970,7 @@ class Lowering:
         out_p = list(self.bufs[key].pshape)
         P = Prog()
         views = []
+        self._view_keys = []
         self._f64 = n.dtype == "f64"
         r = self._value(ctx, n, P, views, out_p, 0)
         P.emit("STORE", a=r)
@@ -972,6 +998,7 @@ class Lowering:
             if ev.progs:
                 raise LowerError(f"{n.name}: non-affine index needs the gather path")
             views.append(self.make_view(ctx, ev, pstrides, extra_off, extra_checks))
+            self._view_keys.append(ev.buf.key)
             if len(views) > N.RT_MAXIN:
                 raise LowerError("too many operands")
             if ev.buf.dtype == "f64":
@@ -1219,6 +1246,10 @@ class Lowering:
             p.konst[i] = c
         if p.total == 0:
             return
+        # source buffers of the operands (persistent loops stage the ones no
+        # loop op writes one step ahead: jit._ew_prefetch_inputs)
+        keys = list(getattr(self, "_view_keys", []))
+        p.__dict__["in_keys"] = keys if len(keys) == len(views) else None
         self.add_rec(N.RT_K_EW, p, self.grid1(p.total), [256, 1, 1], 0, label)
 
     # ---- reductions
