@@ -600,6 +600,34 @@ __device__ __noinline__ void rng_op(const rt_rng_params& p, const int64_t* env, 
 
 RT_DEV float lds1(uint32_t a, float) { float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v; }
 RT_DEV double lds1(uint32_t a, double) { double v; asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a)); return v; }
+
+// warp_pairwise_sum over n <= 128 fp32 values staged in shared memory at
+// byte address a (same summation order: numpy's pairwise sum)
+RT_DEV double warp_pairwise_sum_s(uint32_t a, int n, int lane) {
+  auto ld = [&](int i) { return (double)lds1(a + 4u * (uint32_t)i, 0.f); };
+  if (n < 8) {
+    double v = 0.0;
+    if (lane == 0)
+      for (int i = 0; i < n; ++i) v += ld(i);
+    return __shfl_sync(0xffffffffu, v, 0);
+  }
+  const int body = n - (n % 8);
+  double r = 0.0;
+  if (lane < 8) {
+    r = ld(lane);
+    for (int i = 8 + lane; i < body; i += 8) r += ld(i);
+  }
+  double r1 = __shfl_down_sync(0xffffffffu, r, 1);
+  double p01 = r + r1;
+  double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+  double q = p01 + p23;
+  double q4 = __shfl_down_sync(0xffffffffu, q, 4);
+  double res = q + q4;
+  if (lane == 0)
+    for (int i = body; i < n; ++i) res += ld(i);
+  return __shfl_sync(0xffffffffu, res, 0);
+}
+
 RT_DEV void sts1(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
 RT_DEV void sts1(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
 

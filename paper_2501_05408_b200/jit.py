@@ -268,6 +268,11 @@ def loop_source(lp, ops, name, info=None):
     ew_fwd = _ew_forward_pairs(lp, ops) if FORWARD_ENABLED and pair is None else set()
     fwd |= ew_fwd
     xfwd = _gemm_ew_forwards(lp, ops, info) if pair is None else {}
+    xu = _ew_udf_forwards(lp, ops, info) if pair is None else {}
+    xu_src = {}
+    for u_, m_ in xu.items():
+        for k_, (e_, off_) in m_.items():
+            xu_src.setdefault(e_, []).append(off_)
     xfwd_src = {g: e for e, (_k, g) in xfwd.items()}
     parts, step_pre, pair_pre_bias = [], [], []
     n_gemm = n_xpf = 0
@@ -328,9 +333,12 @@ def loop_source(lp, ops, name, info=None):
             iregs = ", ".join(f"n{j}" for j in range(8))
             body = "\n        ".join(lines)
             fwd_st = ""
+            for off_ in xu_src.get(i, []):
+                fwd_st += (f"\n        sts1(smem_u32(smem + {off_}) + (uint32_t)((int)(flat - r0 * {re}LL) * 4), "
+                           f"(float)res);")
             if (i, i + 1) in ew_fwd:
                 mrp_n = (lp.rows_per_cta * ops[i + 1][2] + 3) // 4 * 4
-                fwd_st = (f"\n        {{ const int lf = (int)(flat - r0 * {re}LL); "
+                fwd_st += (f"\n        {{ const int lf = (int)(flat - r0 * {re}LL); "
                           f"sts1(sA32 + (uint32_t)(((lf % {re}) * {mrp_n} + lf / {re}) * 4), (float)res); }}")
             dec = "\n        ".join(_decompose(nd, ext))
             bl = "\n      ".join(bases)
@@ -393,7 +401,7 @@ def loop_source(lp, ops, name, info=None):
                     step_pre.append("    " + pf[0])
                 t1s = "p.stop" if lp.blk_len else f"{lp.stop}LL"
                 parts.append(_udf_literal(p, i, soff, noise, prefetched=None if pf is None else
-                                          (nz_off, pf[1], lp.step, t1s)))
+                                          (nz_off, pf[1], lp.step, t1s), staged=xu.get(i)))
             else:
                 parts.append(f"""    udf_op(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env, r0, r1, t);""")
         elif kernel == N.RT_K_RNG:
@@ -848,7 +856,7 @@ def _nz_row(p):
     return sum(p.out_count[j] for j in range(p.nout))
 
 
-def _udf_literal(p, op_index, soff, noise, prefetched=False):
+def _udf_literal(p, op_index, soff, noise, prefetched=False, staged=None):
     """Synthetic env body with counts, strides and the row decomposition baked."""
     nd = p.box.nd
     ext = [p.box.ext[j] for j in range(nd)]
@@ -878,7 +886,11 @@ def _udf_literal(p, op_index, soff, noise, prefetched=False):
     for k in range(p.nin):
         v = p.in_[k]
         off = _offset_expr(f"io{k}", v, nd)
-        lines.append(f"  base = base + warp_pairwise_sum((const void*)in{k}, {v.dtype}, {off}, {p.in_count[k]}LL, lane) / {float(p.in_count[k])!r};")
+        if staged and k in staged:
+            lines.append(f"  base = base + warp_pairwise_sum_s(smem_u32(smem + {staged[k][1]}) + (uint32_t)((row - r0) * "
+                         f"{p.in_count[k] * 4}), {p.in_count[k]}, lane) / {float(p.in_count[k])!r};")
+        else:
+            lines.append(f"  base = base + warp_pairwise_sum((const void*)in{k}, {v.dtype}, {off}, {p.in_count[k]}LL, lane) / {float(p.in_count[k])!r};")
     lines.append("  long long nz = nz0 + row * nzr + t * nzs; (void)nz;")
     if prefetched:
         lines.append("  cp_async_wait_all();")
@@ -1075,6 +1087,61 @@ def _gemm_ew_forwards(lp, ops, info):
                    for e in range(re2)):
                 out[i + 1] = (kk, i)
                 break
+    return out
+
+
+def _ew_udf_forwards(lp, ops, info):
+    """{udf op u: {input k: (ew op e, smem offset)}}: elementwise op e < u
+    writes exactly env op u's input k (element j of slab row r at the
+    input's row offset + j); op e also stages its rows in shared memory
+    ([rows][count] floats) and the env op sums them there (the observation
+    and action the synthetic env reads)."""
+    out = {}
+    base = (info or {}).get("xu_off")
+    if not base or not FORWARD_ENABLED or lp.rows_per_cta > 8:
+        return out
+    cur = 0
+    for u, (ku, pu, *_r) in enumerate(ops):
+        if ku != N.RT_K_UDF:
+            continue
+        ndu = pu.box.nd
+        extu = [pu.box.ext[d] for d in range(ndu)]
+
+        def row_off(v, r):
+            o = 0
+            for d in reversed(range(ndu)):
+                o += (r % extu[d]) * v.stride[d]
+                r //= extu[d]
+            return o
+        for k in range(pu.nin):
+            v = pu.in_[k]
+            cnt = pu.in_count[k]
+            if v.dtype != N.RT_F32 or cnt > 128 or cur + 8 * cnt > 512:
+                continue
+            for e in range(u - 1, -1, -1):
+                ke, pe, re, _f, *_s = ops[e]
+                if ke != N.RT_K_EW or pe.f64 or re != cnt or pe.out.dtype != N.RT_F32:
+                    continue
+                o = pe.out
+                if o.ptr != v.ptr or o.off != v.off or \
+                        any(o.off_env[x] != v.off_env[x] for x in range(N.RT_MAXENV)):
+                    continue
+                nd = pe.box.nd
+                ext = [pe.box.ext[d] for d in range(nd)]
+
+                def ew_off(f):
+                    oo = 0
+                    for d in reversed(range(nd)):
+                        oo += (f % ext[d]) * o.stride[d]
+                        f //= ext[d]
+                    return oo
+                rows = lp.rows
+                if all(ew_off(r * re + j) == row_off(v, r) + j
+                       for r in sorted({0, 1, rows // 2, rows - 1}) if 0 <= r < rows
+                       for j in range(cnt)):
+                    out.setdefault(u, {})[k] = (e, base + cur * 4)
+                    cur += 8 * cnt
+                    break
     return out
 
 
