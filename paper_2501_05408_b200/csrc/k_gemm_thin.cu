@@ -18,6 +18,11 @@ namespace {
 constexpr int THREADS = 256;
 constexpr int KT = 64;
 
+RT_DEV float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+RT_DEV double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+RT_DEV float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+RT_DEV double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
 // offset of flat row index `flat` over box b (nd <= 1: flat * s[0])
 RT_DEV int64_t wdec(const rt_gbox& b, int64_t flat, const int64_t* s) {
   if (b.nd <= 1) return flat * s[0];
@@ -100,9 +105,14 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
     const int k = i / R, r = i - k * R;
     ys[i] = k < K ? Y[k * p.Y.s1[0] + r * p.Y.s2[0]] : (T)0;
   }
+  // epilogue 2 (tanh-VJP gate, executor.find_gate_epilogues): C = acc * (1 - h*h)
+  // with h in the bias slot, laid out exactly like C; no bias then
+  const bool gate = p.epilogue == 2;
+  const T* Hg = gate ? (const T*)p.bias.ptr + p.bias.off : nullptr;
   for (int r = threadIdx.x; r < R; r += THREADS)
-    bs[r] = p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + r * p.bias.s2[0])
-                       : (T)0;
+    bs[r] = (p.bias.ptr && !gate)
+                ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + r * p.bias.s2[0])
+                : (T)0;
   const int64_t xk = p.X.s1[0], cr = p.C.s2[0];
   const int64_t ntiles = (p.w + RT - 1) / RT;
   const bool acc_in = p.accumulate != 0, tanh_epi = p.epilogue == 1;
@@ -125,6 +135,27 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
       for (int k = 0; k < KP; ++k) yreg[k] = ys[k * R + r];
       const T b = bs[r];
       T* cbase = Cp + r * cr;
+      if (gate) {
+        // 16 rows per chunk: their h loads are issued together (a load per
+        // output row one at a time left the kernel latency-bound)
+        for (int rr0 = 0; rr0 < nrow; rr0 += 16) {
+          T hv[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            hv[u] = rr0 + u < nrow ? __ldcs(Hg + coff[rr0 + u] + r * cr) : (T)0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            if (rr0 + u >= nrow) break;
+            const int rr = rr0 + u;
+            T a = (T)0;
+#pragma unroll
+            for (int k = 0; k < KP; ++k) a = fma(xs[rr * KP + k], yreg[k], a);
+            // numpy order, no contraction: gy * (1 - h*h)
+            __stcs(cbase + coff[rr], mul_rn(a, sub_rn((T)1, mul_rn(hv[u], hv[u]))));
+          }
+        }
+        continue;
+      }
 #pragma unroll 4
       for (int rr = 0; rr < nrow; ++rr) {
         T a = (T)0;

@@ -378,6 +378,85 @@ def find_gemm_epilogues(g: Graph, pshape, fixed_of, skip, ext=None):
     return res
 
 
+GATE_ENABLED = os.environ.get("RTB200_NO_GATE") != "1"
+
+
+def find_gate_epilogues(g: Graph, pshape, fixed_of, skip, ext):
+    """matmul -> (always-true merges) -> mul(., 1 - h*h): the tanh VJP
+    (reference frontend.py:961-963, `gy * (one - y * y)`) applied to a
+    narrow-K product (d(hidden) = d(head) @ W^T).  One RT_K_THIN variant-2
+    launch computes the product and multiplies by (1 - h*h) in its epilogue
+    (csrc/k_gemm_thin.cu, epilogue 2), so the product never round-trips HBM.
+    Only where that kernel is certain to run (K <= 32, >= 4096 rows, fp32 or
+    fp64 throughout).  Returns {mul id: (matmul id, merges, sub id, inner
+    mul id, edge h -> inner mul)}."""
+    out_ids = {nid for _, nid, _ in g.outputs}
+    res = {}
+    for x in g.sorted_nodes():
+        if x.kind != "matmul" or x.id in skip or x.id in out_ids or x.dtype not in ("f32", "f64"):
+            continue
+        xs = pshape[(x.id, 0)]
+        if len(xs) != 2:
+            continue
+        chain, cur, e = [], x, None
+        while True:
+            e = _single_identity_consumer(g, cur.id, out_ids)
+            if e is None:
+                break
+            nx = g.nodes[e.sink]
+            if nx.kind == "merge" and nx.params["conds"] == (ir.TRUE,) and \
+                    len(g.in_edges(nx.id)) == 1 and nx.dtype == x.dtype and \
+                    pshape[(nx.id, 0)] == xs and nx.id not in skip:
+                chain.append(nx.id)
+                cur = nx
+                continue
+            break
+        if e is None:
+            continue
+        y = g.nodes[e.sink]
+        ins = g.in_edges(y.id)
+        if y.kind != "mul" or y.dtype != x.dtype or len(ins) != 2 or pshape[(y.id, 0)] != xs:
+            continue
+        se = ins[1 - e.iid]
+        sn = g.nodes[se.src]
+        if sn.kind != "sub" or sn.id in skip or not _is_identity(se, sn, y) or \
+                _single_identity_consumer(g, sn.id, out_ids) is None:
+            continue
+        s_in = sorted(g.in_edges(sn.id), key=lambda q: q.iid)
+        if len(s_in) != 2 or _const_scalar(g, s_in[0].src) != 1.0:
+            continue
+        mn = g.nodes[s_in[1].src]
+        if mn.kind != "mul" or mn.id in skip or not _is_identity(s_in[1], mn, sn) or \
+                _single_identity_consumer(g, mn.id, out_ids) is None:
+            continue
+        m_in = g.in_edges(mn.id)
+        if len(m_in) != 2 or m_in[0].src != m_in[1].src or m_in[0].oid != m_in[1].oid:
+            continue
+        h = g.nodes[m_in[0].src]
+        if not all(_is_identity(q, h, mn) for q in m_in) or \
+                pshape[(h.id, m_in[0].oid)] != xs or h.out_dtypes[m_in[0].oid] != x.dtype:
+            continue
+        if len({fixed_of.get(k) for k in (x.id, y.id, sn.id, mn.id)}) != 1:
+            continue
+        # the narrow-K thin kernel must be the one that runs (lower._gemm_smallk)
+        xa = g.in_edges(x.id)
+        xa = [q for q in xa if q.iid == 0]
+        if not xa:
+            continue
+        ashape = pshape[(xa[0].src, xa[0].oid)]
+        k = ashape[-1] if ashape else 0
+        rows = xs[0]
+        for d in y.domain:
+            if d not in (fixed_of.get(y.id) or ()):
+                rows *= ext.get(d, 1)
+        kp = 4 if k <= 4 else 8 if k <= 8 else 16 if k <= 16 else 32
+        esize = 8 if x.dtype == "f64" else 4
+        if not (1 <= k <= 32 and rows >= 4096 and (kp * xs[1] + 64 * kp + xs[1]) * esize <= 48 * 1024):
+            continue
+        res[y.id] = (x.id, tuple(chain), sn.id, mn.id, m_in[0])
+    return res
+
+
 def _const_scalar(g, nid):
     n = g.nodes[nid]
     if n.kind != "const" or n.domain or tuple(n.out_shapes[0]) not in ((), (1,)):
@@ -587,6 +666,11 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
         taken.add(x)
         if t:
             taken.add(g.in_edges(f)[0].src)
+    gates = find_gate_epilogues(g, pshape, fixed_of, taken - alias_nodes, ext) \
+        if fuse and GATE_ENABLED else {}
+    for y_, (x_, _ch, s_, m_, _he) in gates.items():
+        gemm_epi[y_] = (x_, None, ("gate", s_, m_, _he))
+        taken |= {y_, x_, s_, m_}
     gae = find_gae_fusions(g, benv, alias, {nid for _, nid, _ in g.outputs}) if fuse else {}
     for info in gae.values():
         taken |= info["nodes"]
@@ -596,7 +680,9 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
     virtual |= set(fuse_src)
     for f, (x, _b, t) in gemm_epi.items():
         virtual.add(x)
-        if t:
+        if isinstance(t, tuple):
+            virtual |= {t[1], t[2]}
+        elif t:
             virtual.add(g.in_edges(f)[0].src)
     bufs = {}
     for n in g.sorted_nodes():

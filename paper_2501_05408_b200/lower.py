@@ -298,7 +298,9 @@ class Lowering:
             self.virtual |= info["nodes"]          # delta chain formed inside the scan
         for f, (x, _b, t) in self.gemm_epi.items():
             self.virtual.add(x)
-            if t:
+            if isinstance(t, tuple):           # tanh-VJP gate: (1 - h*h) chain
+                self.virtual |= {t[1], t[2]}
+            elif t:
                 self.virtual.add(self.g.in_edges(f)[0].src)
         self.launches_per_kernel = {}
 
@@ -935,7 +937,10 @@ class Lowering:
             return
         if n.id in self.gemm_epi:
             x, bias_e, tanh = self.gemm_epi[n.id]
-            self.k_matmul(ctx, self.g.nodes[x], bias_e, 1 if tanh else 0)
+            if isinstance(tanh, tuple):
+                self.k_matmul(ctx, self.g.nodes[x], None, 2, gate_edge=tanh[3])
+            else:
+                self.k_matmul(ctx, self.g.nodes[x], bias_e, 1 if tanh else 0)
         else:
             fn = getattr(self, f"k_{n.kind}", None)
             if fn is None:
@@ -1618,7 +1623,7 @@ class Lowering:
 
     # ---- matmul
 
-    def k_matmul(self, ctx: Ctx, X=None, bias_edge=None, epilogue=0):
+    def k_matmul(self, ctx: Ctx, X=None, bias_edge=None, epilogue=0, gate_edge=None):
         """GEMM for matmul node X (default: ctx.node) written into ctx.node's
         buffer, optionally with a fused `+ bias` and `tanh` epilogue."""
         n = ctx.node
@@ -1662,8 +1667,26 @@ class Lowering:
             for d, sv in bv.coef.items():
                 bias.off_env[self.slot[d]] += sv
             bias.s2[0] = bv.axes[-1].stride if bv.axes and bv.axes[-1].ext != 1 else 0
+        gate = None
+        if gate_edge is not None:
+            # epilogue 2: C = acc * (1 - h*h) with h laid out exactly like C
+            hv = self.edge_val(ctx, gate_edge)
+            if hv.checks or hv.progs or _ragged(hv) or any(t[0] != 1 for t in Z) or len(hv.axes) != 2:
+                raise LowerError(f"{n.name}: gate operand is not a plain view "
+                                 f"({len(hv.checks)}, {len(hv.progs)}, {_ragged(hv)}, {Z}, {hv.axes})")
+            same = all(hv.coef.get(d, 0) == cdst[d] for d in ctx.slab if self.ext[d] != 1) and \
+                (m == 1 or hv.axes[-2].stride == c_log[nb]) and hv.axes[-1].stride == c_log[nb + 1]
+            if not same:
+                raise LowerError(f"{n.name}: gate operand layout differs from the output's")
+            gate = N.rt_gop()
+            gate.ptr = hv.buf.ptr if hasattr(hv.buf, "ptr") else self.storage(hv.buf.key).ptr
+            gate.dtype = N.DTYPE_CODE[hv.buf.dtype]
+            gate.off = hv.off
+            for d, sv in hv.coef.items():
+                if d in ctx.fixed:
+                    gate.off_env[self.slot[d]] += sv
         self._gemm((A.buf, A.off, env_a), (B.buf, B.off, env_b), (st, 0, env_c),
-                   Z, M, Nn, K, (n.id, n.name), epilogue=epilogue, bias=bias)
+                   Z, M, Nn, K, (n.id, n.name), epilogue=epilogue, bias=bias, gate=gate)
 
     @staticmethod
     def _bstride(axes, i, nb):
@@ -1701,7 +1724,7 @@ class Lowering:
             raise LowerError("matmul output layout mismatch")
         return a_ax, b_ax, batch, m, nn, kk, c_log
 
-    def _gemm(self, A, B, Cc, Z, M, Nn, K, label, accumulate=0, epilogue=0, bias=None):
+    def _gemm(self, A, B, Cc, Z, M, Nn, K, label, accumulate=0, epilogue=0, bias=None, gate=None):
         """Z/M/N/K: lists of (extent, a_stride, b_stride, c_stride).
         A/B/C: (buf, element offset, {env slot: stride})."""
         p = N.rt_gemm_params()
@@ -1749,6 +1772,13 @@ class Lowering:
         p.epilogue = epilogue
         if bias is not None:
             p.bias = bias
+        if gate is not None:
+            # the tanh-VJP gate epilogue exists in the narrow-K thin kernel only
+            # (executor.find_gate_epilogues fuses only where it runs)
+            if self._capture_active() or not self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
+                                                             epilogue, None, gate=gate):
+                raise LowerError(f"{label[1]}: gate epilogue needs the narrow-K thin GEMM")
+            return
         if not self._capture_active() and self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
                                                           epilogue, bias):
             return
@@ -1815,7 +1845,7 @@ class Lowering:
     THIN_MAX_R = 32
     THIN_MIN_K = 4096
 
-    def _gemm_thin(self, p, Z, M, Nn, K, label, accumulate, epilogue, bias):
+    def _gemm_thin(self, p, Z, M, Nn, K, label, accumulate, epilogue, bias, gate=None):
         """Narrow GEMMs -> RT_K_THIN (csrc/k_gemm_thin.cu); False if not one."""
         if p.z != 1 or any(t[0] != 1 for t in Z):
             return False
@@ -1824,6 +1854,10 @@ class Lowering:
         f64 = dt == ["f64"] * 3
         if not (f64 or dt == ["f32"] * 3):
             return False
+        if gate is not None:
+            if nc is None or kc is None or self._gop_dtype(gate) != dt[0]:
+                return False
+            return self._gemm_smallk(p, M, nc, kc, f64, label, accumulate, epilogue, None, gate=gate)
         if nc is not None and kc is not None and self._gemm_rows(p, M, nc, kc, f64, label,
                                                                  accumulate, epilogue, bias):
             return True
@@ -1874,7 +1908,7 @@ class Lowering:
             return True
         return self._gemm_smallk(p, M, nc, kc, f64, label, accumulate, epilogue, bias)
 
-    def _gemm_smallk(self, p, M, nc, kc, f64, label, accumulate, epilogue, bias):
+    def _gemm_smallk(self, p, M, nc, kc, f64, label, accumulate, epilogue, bias, gate=None):
         """K <= 32 products over many rows (the observation layer, dX of a
         narrow head) -> RT_K_THIN variant 2; rows may be a multi-dim box
         (gathered minibatch rows)."""
@@ -1913,6 +1947,9 @@ class Lowering:
         q.C = gop(p.C, [t[3] for t in mdims], [c_n])
         if bias is not None:
             q.bias = gop(bias, [0], [bias.s2[0]])
+        if gate is not None:
+            # epilogue 2: the gate operand walks C's strides (checked in k_matmul)
+            q.bias = gop(gate, [t[3] for t in mdims], [c_n])
         q.accumulate, q.epilogue = accumulate, epilogue
         grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
         self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)

@@ -210,3 +210,26 @@ def test_default_loop_at_8_rows_matches_interpreter(monkeypatch):
     got = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=5)
     for k in ref:
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
+
+
+def test_tanh_vjp_gate_epilogue_matches_unfused(monkeypatch):
+    """The thin GEMM's gate epilogue (d(h2) = d(mu) W3^T times 1 - h2*h2 in
+    one launch, executor.find_gate_epilogues) reproduces the unfused
+    product + elementwise pair at a size where it is chosen (8192 rows)."""
+    from golden_cases import load_graph
+    from paper_2501_05408_b200 import execute, executor as X, get_executable
+    from paper_2501_05408_b200 import native as N
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    bounds = {"I": 1, "B": 128, "T": 64}
+    monkeypatch.setattr(X, "GATE_ENABLED", False)
+    X._CACHE.clear()
+    ref = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=5)
+    monkeypatch.setattr(X, "GATE_ENABLED", True)
+    X._CACHE.clear()
+    g = load_graph("reinforce_mlp_c2")
+    exe, _ = get_executable(g, bounds, mlp_inputs(), 5)
+    assert any(k == N.RT_K_THIN and p.variant == 2 and p.epilogue == 2
+               for k, p in zip(exe.kernels, exe._params))
+    got = execute(g, bounds=bounds, inputs=mlp_inputs(), seed=5)
+    for k in ref:
+        np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)

@@ -256,3 +256,17 @@ def test_gae_delta_fused_into_the_scan():
         scans = [p for (k, p, *_r) in low.recs if k == N.RT_K_SCAN]
         assert any(p.gae for p in scans), name
         assert not any(lab[1] == "delta" for (*_r, lab) in low.recs), name
+
+
+def test_c2_tanh_vjp_gate_fuses_into_the_narrow_head_product():
+    """d(h2) = d(mu) @ W3^T followed by the tanh VJP `gy * (1 - h2*h2)`
+    (reference frontend.py:961-963) lowers to ONE thin variant-2 launch with
+    the gate epilogue (no elementwise launch, no d(h2) buffer); small
+    problems keep the unfused path (the thin kernel would not be chosen)."""
+    g = load_graph("reinforce_mlp_c2")
+    _plan, low, _c, _a = dry_lower(g, {"I": 1, "B": 1024, "T": 1000})
+    gates = [p for (k, p, *_r) in low.recs if k == N.RT_K_THIN and p.variant == 2 and p.epilogue == 2]
+    assert len(gates) == 1 and gates[0].k == 4 and gates[0].r == 256
+    assert any(isinstance(t, tuple) and t[0] == "gate" for (_x, _b, t) in low.gemm_epi.values())
+    _plan, low2, _c, _a = dry_lower(g, {"I": 1, "B": 4, "T": 8})
+    assert not any(isinstance(t, tuple) for (_x, _b, t) in low2.gemm_epi.values())
