@@ -118,15 +118,6 @@ RT_DEV void sts4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
 
-// acc[r] += a[r] * b over a row block.  fp32: packed FFMA2 (fma.rn.f32x2,
-// sm_100+) on row pairs with b broadcast — two IEEE fused multiply-adds per
-// issued instruction, bit-identical to scalar fma; the in-loop GEMM cores
-// are issue bound, so this halves their FMA instruction count.
-RT_DEV void fma2(float& d0, float& d1, float a0, float a1, float b) {
-  asm("{.reg .b64 d, a, bb;\n\tmov.b64 d, {%0,%1};\n\tmov.b64 a, {%2,%3};\n\tmov.b64 bb, {%4,%4};\n\t"
-      "fma.rn.f32x2 d, a, bb, d;\n\tmov.b64 {%0,%1}, d;}"
-      : "+f"(d0), "+f"(d1) : "f"(a0), "f"(a1), "f"(b));
-}
 template <int MRP>
 RT_DEV void fma_rows(float (&acc)[MRP], const float (&a)[MRP], float b) {
   static_assert(MRP % 2 == 0, "row blocks are padded to even counts");
