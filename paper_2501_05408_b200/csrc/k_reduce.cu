@@ -199,15 +199,23 @@ __global__ void __launch_bounds__(256) k_reduce_cols(const __grid_constant__ rt_
   }
 }
 
+// Pass 2: one warp per output; lane l sums splits l, l+32, ... in order,
+// then a fixed xor tree (deterministic; a thread per output walking up to
+// 1024 partials serially took ~90 us per launch)
 __global__ void __launch_bounds__(256) k_reduce_cols_fin(const __grid_constant__ rt_reduce_params p) {
   int64_t idx[RT_MAXD];
   const double* part = (const double*)p.part;
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < p.total;
-       o += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t o = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < p.total;
+       o += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     double acc = 0.0;
-    for (int s = 0; s < p.splits; ++s) acc += part[(int64_t)s * p.total + o];
-    decompose(p.box, o, idx);
-    store_as<double>((void*)p.out.ptr, p.out.dtype, view_off(p.out, p.box.nd, idx), acc);
+    for (int s = lane; s < p.splits; s += 32) acc += part[(int64_t)s * p.total + o];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (lane == 0) {
+      decompose(p.box, o, idx);
+      store_as<double>((void*)p.out.ptr, p.out.dtype, view_off(p.out, p.box.nd, idx), acc);
+    }
   }
 }
 

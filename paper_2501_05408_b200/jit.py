@@ -311,8 +311,7 @@ def loop_source(lp, ops, name, info=None):
             xpf = xpf[:max(0, XPF_SLOTS - n_xpf)]
             if xpf and (info or {}).get("xpf_off") and lp.rows_per_cta * re <= 256 and pair is None:
                 ov = dict(ov or {})
-                t_first = "p.start" if lp.blk_len else f"{lp.start}LL"
-                t_stop = "p.stop" if lp.blk_len else f"{lp.stop}LL"
+                t_first, t_stop = "T0_", "T1_"   # (the op's own `p` shadows the loop's)
                 cmp_ = "<" if lp.step > 0 else ">"
                 for si0, k in enumerate(xpf):
                     si = n_xpf + si0
@@ -399,7 +398,7 @@ def loop_source(lp, ops, name, info=None):
                     _nz_row(p) * 8 * 8 <= (info or {}).get("nz_bytes", 0) else None
                 if pf is not None:
                     step_pre.append("    " + pf[0])
-                t1s = "p.stop" if lp.blk_len else f"{lp.stop}LL"
+                t1s = "T1_"
                 parts.append(_udf_literal(p, i, soff, noise, prefetched=None if pf is None else
                                           (nz_off, pf[1], lp.step, t1s), staged=xu.get(i)))
             else:
@@ -481,6 +480,8 @@ extern "C" __global__ void __launch_bounds__(256, {per_sm}) {name}(const __grid_
 {bias_pro}
 {pair_pro}
   long long c0 = clock64();
+  const long long T0_ = {t0}, T1_ = {t1};   // loop range (ops name their own params `p`)
+  (void)T0_; (void)T1_;
   for (long long t = {t0}; t {cmp} {t1}; t += {lp.step}LL) {{
     env[{lp.slot}] = t;
 {chr(10).join(step_pre)}
@@ -847,8 +848,7 @@ def _udf_prefetch(lp, p, op_index, soff_nz):
             e0 += c
         lines.append("  cp_async_commit(); }")
         return "\n    ".join(lines)
-    t_first = "p.start" if lp.blk_len else f"{lp.start}LL"
-    first = f"if (t == {t_first}) {{\n    {issue('t')}\n    }}"
+    first = f"if (t == T0_) {{\n    {issue('t')}\n    }}"
     return first, issue
 
 

@@ -1418,8 +1418,9 @@ class Lowering:
             p.part = self.alloc(splits * p.total * 8)
             self.add_rec(N.RT_K_REDUCE, p, [ob, splits, 1], [256, 1, 1], 0, (n.id, n.name))
             q = N.rt_reduce_params.from_buffer_copy(p)
-            q.threads_per_out = -1
-            self.add_rec(N.RT_K_REDUCE, q, self.grid1(p.total), [256, 1, 1], 0, (n.id, n.name))
+            q.threads_per_out = -1     # k_reduce_cols_fin: a warp per output
+            self.add_rec(N.RT_K_REDUCE, q, [min((p.total + 7) // 8, 148 * 8), 1, 1], [256, 1, 1], 0,
+                         (n.id, n.name))
             return
         if const_lens and p.total <= 64 and maxlen >= 4096 and p.total * maxlen >= (1 << 18):
             # few outputs, long constant ranges (a head's bias gradient over all
@@ -1429,8 +1430,9 @@ class Lowering:
             p.part = self.alloc(splits * p.total * 8)
             self.add_rec(N.RT_K_REDUCE, p, [1, splits, 1], [256, 1, 1], 0, (n.id, n.name))
             q = N.rt_reduce_params.from_buffer_copy(p)
-            q.threads_per_out = -1
-            self.add_rec(N.RT_K_REDUCE, q, self.grid1(p.total), [256, 1, 1], 0, (n.id, n.name))
+            q.threads_per_out = -1     # k_reduce_cols_fin: a warp per output
+            self.add_rec(N.RT_K_REDUCE, q, [min((p.total + 7) // 8, 148 * 8), 1, 1], [256, 1, 1], 0,
+                         (n.id, n.name))
             return
         if maxlen >= 256 and p.total < 148 * 64:
             tpo = 1024 if maxlen >= 4096 else 256

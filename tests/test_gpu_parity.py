@@ -233,3 +233,22 @@ def test_tanh_vjp_gate_epilogue_matches_unfused(monkeypatch):
     got = execute(g, bounds=bounds, inputs=mlp_inputs(), seed=5)
     for k in ref:
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
+
+
+@pytest.mark.parametrize("bs", [8, 10])
+def test_time_blocked_jit_loop_matches_interpreter(monkeypatch, bs):
+    """Time-blocked acting loop (one persistent launch per block, range from
+    the launch) through the JIT path — staged normals / operands take the
+    block's own start and stop — reproduces the interpreting loop kernel."""
+    from golden_cases import load_graph
+    from paper_2501_05408_b200 import execute, jit
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    bounds = {"I": 1, "B": 64, "T": 40}
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 1 << 40)
+    ref = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=3,
+                  block=("t", bs))
+    monkeypatch.setattr(jit, "JIT_LOOP_MIN", 0)
+    got = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=3,
+                  block=("t", bs))
+    for k in ref:
+        np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
