@@ -21,3 +21,6 @@ for K in ${NCU_KERNELS:-loop_jit k_gemm_tma ew_jit k_thin}; do
 done
 timeout 600 python bench_kernels.py > gpurun_out/bench_kernels_$P.jsonl 2>&1
 tail -2 gpurun_out/pytest_gpu_$P.log
+# multi-rank functional check of the bench's sharded path (2 gloo ranks on one GPU)
+BENCH_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_gloo2_$P.log 2>&1
+BENCH_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --workload c5 --gpus 2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5_gloo2_$P.log 2>&1
