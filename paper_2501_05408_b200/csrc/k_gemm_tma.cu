@@ -201,19 +201,32 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
     for (int kt = 0; kt < ntiles; ++kt) {
       const int s = kt % TM_ST;
       mb_wait(su32(&full[s]), (uint32_t)((kt / TM_ST) & 1));
-      unsigned char* st = smem + s * TM_STAGE;
+      const uint32_t st = sbase + s * TM_STAGE;
       constexpr int NA = TM_A_BYTES / 16, NB = TM_B_BYTES / 16;
+      constexpr int NI = (NA + NB) / TM_CONV;
+      static_assert((NA + NB) % TM_CONV == 0 && NA % TM_CONV == 0, "whole conversion rounds");
+      // explicit shared-space accesses (generic LD/ST.E here were tracked on
+      // the long scoreboard), all of a thread's loads issued before its stores
+      float4 xs[NI];
 #pragma unroll
-      for (int i = tid; i < NA + NB; i += TM_CONV) {
+      for (int j = 0; j < NI; ++j) {
+        const int i = tid + j * TM_CONV;
+        const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(xs[j].x), "=f"(xs[j].y), "=f"(xs[j].z), "=f"(xs[j].w) : "r"(st + off));
+      }
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int i = tid + j * TM_CONV;
         const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
         const uint32_t lo_off = i < NA ? TM_A_BYTES : TM_B_BYTES;
-        float4 x = *(const float4*)(st + off);
+        const float4 x = xs[j];
         uint4 h, l;
         h.x = rna(x.x); h.y = rna(x.y); h.z = rna(x.z); h.w = rna(x.w);
         l.x = rna(x.x - __uint_as_float(h.x)); l.y = rna(x.y - __uint_as_float(h.y));
         l.z = rna(x.z - __uint_as_float(h.z)); l.w = rna(x.w - __uint_as_float(h.w));
-        *(uint4*)(st + off) = h;
-        *(uint4*)(st + off + lo_off) = l;
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off), "r"(h.x), "r"(h.y), "r"(h.z), "r"(h.w));
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off + lo_off), "r"(l.x), "r"(l.y), "r"(l.z), "r"(l.w));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mb_arrive(su32(&conv[s]));
