@@ -136,8 +136,9 @@ def _program_lines(p, T, nd, base=None, chk=None, env="p.h.env", load_override=N
                 off = f"{off} + n{a}"
                 valid = f"(n{b} != 0) && {valid}"
             ct = CT[v.dtype]
-            if o == "LOAD" and load_override and imm in load_override and valid == "true":
-                w(f"v{d} = {load_override[imm]};")
+            if o == "LOAD" and load_override and imm in load_override:
+                w(f"v{d} = {load_override[imm]};" if valid == "true" else
+                  f"v{d} = ({valid}) ? ({T})({load_override[imm]}) : ({T})0;")
                 pc += 2
                 continue
             load = f"(({T})((const {ct}*){pfx}.ptr)[{off}])"
@@ -269,6 +270,10 @@ def loop_source(lp, ops, name, info=None):
     fwd |= ew_fwd
     xfwd = _gemm_ew_forwards(lp, ops, info) if pair is None else {}
     xu = _ew_udf_forwards(lp, ops, info) if pair is None else {}
+    xc = _udf_ew_carries(lp, ops, info) if pair is None else {}
+    xc_src = {}
+    for e_, (k_, u_, j_, off_) in xc.items():
+        xc_src.setdefault(u_, {})[j_] = off_
     xu_src = {}
     for u_, m_ in xu.items():
         for k_, (e_, off_) in m_.items():
@@ -301,6 +306,12 @@ def loop_source(lp, ops, name, info=None):
             if i in xfwd and not p.f64:
                 kx = xfwd[i][0]
                 ov = {kx: f"lds1(smem_u32(smem + {info['xfwd_off']}) + (uint32_t)((int)(flat - r0 * {re}LL) * 4), 0.f)"}
+            if i in xc and not p.f64:
+                kc_, _u, _j, off_c = xc[i]
+                ov = dict(ov or {})
+                offc = _offset_expr(f"b{kc_}", p.in_[kc_], nd)
+                ov[kc_] = (f"(t == T0_ ? ((const float*)p.in[{kc_}].ptr)[{offc}] : lds1(smem_u32(smem + {off_c}) + "
+                           f"(uint32_t)((int)(flat - r0 * {re}LL) * 4), 0.f))")
             # operands no loop op writes (pre-drawn normals): staged one step
             # ahead by cp.async; the first step reads them from global
             pf_pre, pf_post = "", ""
@@ -400,7 +411,8 @@ def loop_source(lp, ops, name, info=None):
                     step_pre.append("    " + pf[0])
                 t1s = "T1_"
                 parts.append(_udf_literal(p, i, soff, noise, prefetched=None if pf is None else
-                                          (nz_off, pf[1], lp.step, t1s), staged=xu.get(i)))
+                                          (nz_off, pf[1], lp.step, t1s), staged=xu.get(i),
+                                          carry=xc_src.get(i)))
             else:
                 parts.append(f"""    udf_op(*(const rt_udf_params*)(smem + {soff}), ops[{i}], env, r0, r1, t);""")
         elif kernel == N.RT_K_RNG:
@@ -856,7 +868,7 @@ def _nz_row(p):
     return sum(p.out_count[j] for j in range(p.nout))
 
 
-def _udf_literal(p, op_index, soff, noise, prefetched=False, staged=None):
+def _udf_literal(p, op_index, soff, noise, prefetched=False, staged=None, carry=None):
     """Synthetic env body with counts, strides and the row decomposition baked."""
     nd = p.box.nd
     ext = [p.box.ext[j] for j in range(nd)]
@@ -910,6 +922,10 @@ def _udf_literal(p, op_index, soff, noise, prefetched=False, staged=None):
             lines.append(pre)
         store = (f"out{j}[{off} + e] = ({expr}) != 0.0;" if v.dtype == N.RT_BOOL
                  else f"out{j}[{off} + e] = ({ct})({expr});")
+        if carry and j in carry and v.dtype == N.RT_F32:
+            # (the value is recomputed: numpy's double -> float32 cast, same rounding)
+            store = (f"{{ const float cv_ = (float)({expr}); out{j}[{off} + e] = cv_; "
+                     f"sts1(smem_u32(smem + {carry[j]}) + (uint32_t)(((row - r0) * {p.out_count[j]} + e) * 4), cv_); }}")
         if prefetched:
             e0 = sum(p.out_count[jj] for jj in range(j))
             lines.append(f"  if (lane < {p.out_count[j]}) {{ const int e = lane; const double z = lds1(smem_u32(smem + "
@@ -1141,6 +1157,66 @@ def _ew_udf_forwards(lp, ops, info):
                        for j in range(cnt)):
                     out.setdefault(u, {})[k] = (e, base + cur * 4)
                     cur += 8 * cnt
+                    break
+    return out
+
+
+def _udf_ew_carries(lp, ops, info):
+    """{ew op e: (input k, udf op u, output j, smem offset)}: elementwise op e
+    reads at step t exactly what env op u wrote as output j at step t - step
+    (the observation carried into the next step's merge).  Op u also stages
+    its fp32 rows in shared memory and op e reads them there (from the second
+    step of a launch on; the first reads global)."""
+    out = {}
+    base = (info or {}).get("xc_off")
+    if not base or not FORWARD_ENABLED or lp.rows_per_cta > 8:
+        return out
+    slot = lp.slot
+    used = 0
+    for u, (ku, pu, *_r) in enumerate(ops):
+        if ku != N.RT_K_UDF:
+            continue
+        ndu = pu.box.nd
+        extu = [pu.box.ext[d] for d in range(ndu)]
+        for j in range(pu.nout):
+            vo = pu.out[j]
+            cnt = pu.out_count[j]
+            if vo.dtype != N.RT_F32 or cnt > 32 or used + 8 * cnt > 256:
+                continue
+            coef = vo.off_env[slot] * lp.step
+            for e in range(len(ops)):
+                ke, pe, re, _f, *_s = ops[e]
+                if ke != N.RT_K_EW or pe.f64 or re != cnt or e >= u:
+                    continue
+                nd = pe.box.nd
+                ext = [pe.box.ext[d] for d in range(nd)]
+                for k in range(pe.nin):
+                    v = pe.in_[k]
+                    if v.dtype != N.RT_F32 or v.ptr != vo.ptr or v.off != vo.off - coef or \
+                            any(v.off_env[x] != vo.off_env[x] for x in range(N.RT_MAXENV)):
+                        continue
+
+                    def ew_off(f, v=v, nd=nd, ext=ext):
+                        oo = 0
+                        for d in reversed(range(nd)):
+                            oo += (f % ext[d]) * v.stride[d]
+                            f //= ext[d]
+                        return oo
+
+                    def u_off(r):
+                        oo = 0
+                        for d in reversed(range(ndu)):
+                            oo += (r % extu[d]) * vo.stride[d]
+                            r //= extu[d]
+                        return oo
+                    rows = lp.rows
+                    if all(ew_off(r * re + q) == u_off(r) + q
+                           for r in sorted({0, 1, rows // 2, rows - 1}) if 0 <= r < rows
+                           for q in range(cnt)):
+                        out[e] = (k, u, j, base + used * 4)
+                        used += 8 * cnt
+                        break
+                if e in out:
                     break
     return out
 

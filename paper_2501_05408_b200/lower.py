@@ -768,7 +768,8 @@ class Lowering:
         xfwd_off = ring_off
         xpf_off = xfwd_off + 8 * 32 * 4
         xu_off = xpf_off + 256 * 4 * 2         # env-op inputs staged by their producers
-        ring_off = (xu_off + 512 * 4 + 127) // 128 * 128
+        xc_off = xu_off + 512 * 4              # env-op outputs carried to the next step
+        ring_off = (xc_off + 256 * 4 + 127) // 128 * 128
         # loop-invariant GEMM biases copied to shared memory once (their
         # per-step global loads sat on each layer's epilogue critical path)
         bias_smem = {}
@@ -860,7 +861,7 @@ class Lowering:
                                "trips_per_launch": min(T, lp.blk_len) if lp.blk_len else T,
                                "ctas_per_sm": 2 if dual else 1, "resident": resident,
                                "hybrid": hybrid, "nz_off": nz_off, "nz_bytes": nz_bytes,
-                               "bias_smem": bias_smem, "xfwd_off": xfwd_off, "xpf_off": xpf_off, "xu_off": xu_off,
+                               "bias_smem": bias_smem, "xfwd_off": xfwd_off, "xpf_off": xpf_off, "xu_off": xu_off, "xc_off": xc_off,
                                "ext_in": ext_in}
         if pair_info is not None:
             self.rec_cluster[idx] = 2
