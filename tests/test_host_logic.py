@@ -270,3 +270,48 @@ def test_c2_tanh_vjp_gate_fuses_into_the_narrow_head_product():
     assert any(isinstance(t, tuple) and t[0] == "gate" for (_x, _b, t) in low.gemm_epi.values())
     _plan, low2, _c, _a = dry_lower(g, {"I": 1, "B": 4, "T": 8})
     assert not any(isinstance(t, tuple) for (_x, _b, t) in low2.gemm_epi.values())
+
+
+def test_c2_acting_loop_kernel_source_builds_for_sm100a():
+    """The JIT-specialised acting loop of C2 carries every on-chip mechanism
+    (W2 in registers + shared memory with the row-split epilogue, normals and
+    eps staged by cp.async, env inputs and the carried observation read from
+    shared memory) and NVRTC compiles it for sm_100a (no GPU needed)."""
+    import ctypes as C
+    from paper_2501_05408_b200 import jit
+    g = load_graph("reinforce_mlp_c2")
+    _p, low, _c, _a = dry_lower(g, {"I": 1, "B": 1024, "T": 1000})
+    subs = list(low.loop_subs.items())
+    assert len(subs) == 1
+    ri, info = subs[0]
+    lp = low.recs[ri][1]
+    assert info["hybrid"] and info["hybrid"]["kr"] == 128 and info["hybrid"]["ncol"] == 2
+    src = jit.loop_source(lp, info["ops"], "loop_jit", info)
+    for needle in ("hyb_core<8, 256, 256, 2, 64, true>",   # W2 on chip, row-split epilogue
+                   "hyb_core<8, 16, 256, 2, 0, true>",     # W1 resident through the same core
+                   "cp_async8", "cp_async4",               # normals / eps one step ahead
+                   "warp_pairwise_sum_s",                  # env inputs from shared memory
+                   "T0_ ?",                                # carried observation / staged eps
+                   "tanh_fast"):
+        assert needle in src, needle
+    lib = N.lib()
+    opts = jit._opts()
+    blob = b"\0".join(opts) + b"\0"
+    size = C.c_uint64(0)
+    rc = lib.rt_jit_cubin(src.encode(), blob, len(opts), None, C.byref(size))
+    assert rc == 0 and size.value > 0
+    # resource usage: the 128 weight registers per thread must not spill
+    import shutil
+    import subprocess
+    import tempfile
+    if shutil.which("cuobjdump"):
+        buf = C.create_string_buffer(size.value)
+        assert lib.rt_jit_cubin(src.encode(), blob, len(opts), buf, C.byref(size)) == 0
+        with tempfile.NamedTemporaryFile(suffix=".cubin") as fh:
+            fh.write(buf.raw[:size.value])
+            fh.flush()
+            res = subprocess.run(["cuobjdump", "--dump-resource-usage", fh.name],
+                                 capture_output=True, text=True).stdout
+        line = [x for x in res.splitlines() if "REG:" in x][0]
+        fields = dict(f.split(":") for f in line.split() if ":" in f and f.split(":")[1].isdigit())
+        assert int(fields["REG"]) <= 255 and int(fields.get("LOCAL", "0")) == 0, line
