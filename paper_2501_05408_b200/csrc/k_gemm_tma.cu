@@ -265,13 +265,33 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
         continue;
       }
       const int64_t rowoff = p.C.off + m * a.c_m;
+      // the 16 bias values of this chunk (the same for every row/thread):
+      // four 16-byte loads when contiguous fp32, not a dtype-dispatched load
+      // per element (the bias+tanh forward GEMM ran ~30% slower than dX)
+      float bv[16];
+      if (p.bias.ptr) {
+        const int64_t b0 = p.bias.off + (n0 + c0) * a.bias_n;
+        const float* bp = (const float*)p.bias.ptr + b0;
+        if (a.bias_n == 1 && p.bias.dtype == RT_F32 && n0 + c0 + 16 <= p.n &&
+            (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bp) + q);
+            bv[4 * q] = b4.x; bv[4 * q + 1] = b4.y; bv[4 * q + 2] = b4.z; bv[4 * q + 3] = b4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            bv[j] = n0 + c0 + j < p.n
+                        ? load_as<float>((const void*)p.bias.ptr, p.bias.dtype, b0 + j * a.bias_n) : 0.f;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int64_t n = n0 + c0 + j;
         if (n >= p.n) break;
         if (p.accumulate) x[j] += Cp[rowoff + n * a.c_n];
-        if (p.bias.ptr)
-          x[j] += load_as<float>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + n * a.bias_n);
+        if (p.bias.ptr) x[j] += bv[j];
         if (p.epilogue == 1) x[j] = tanh_fast(x[j]);
       }
       if (vec && n0 + c0 + 16 <= p.n) {
