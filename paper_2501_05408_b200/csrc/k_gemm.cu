@@ -153,14 +153,22 @@ __global__ void __launch_bounds__(256) k_gemm(const __grid_constant__ rt_gemm_pa
   }
 }
 
+// Split-K reduction.  One warp per output (grid-stride over outputs by
+// warp): lane l sums splits l, l+32, ... in order, then a fixed xor tree —
+// deterministic; a thread walking ~1000 partials serially per output was
+// latency-bound (~90 GB/s on the narrow dW contractions).
 template <typename T>
 __global__ void __launch_bounds__(256) k_splitk(const __grid_constant__ rt_splitk_params p) {
   const int64_t total = p.z * p.m * p.n;
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total;
-       f += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < total; f += nw) {
     const T* part = (const T*)p.part;
     T v = (T)0;
-    for (int s = 0; s < p.splits; ++s) v += part[s * total + f];
+    for (int s = lane; s < p.splits; s += 32) v += part[s * total + f];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane != 0) continue;
     int64_t n = f % p.n, r = f / p.n;
     int64_t m = r % p.m, zi = r / p.m;
     int64_t oc = p.C.off + gdecomp(p.Z, zi, p.C.sz) + gdecomp(p.M, m, p.C.s1) +

@@ -1810,7 +1810,8 @@ class Lowering:
             q.C = p.C
             if bias is not None:
                 q.bias = bias
-            self.add_rec(N.RT_K_SPLITK, q, self.grid1(p.z * p.m * p.n), [256, 1, 1], 0, label)
+            self.add_rec(N.RT_K_SPLITK, q, [int(min((p.z * p.m * p.n + 7) // 8, 148 * 16)), 1, 1], [256, 1, 1], 0,
+                         label)   # k_splitk: a warp per output
         else:
             grid = [(p.m + 63) // 64, (p.n + 63) // 64, p.z]
             self.add_rec(N.RT_K_GEMM, p, grid, [256, 1, 1], 0, label)
@@ -1907,7 +1908,8 @@ class Lowering:
             r.part, r.C = q.part, p.C
             if bias is not None:
                 r.bias = bias
-            self.add_rec(N.RT_K_SPLITK, r, self.grid1(p.m * p.n), [256, 1, 1], 0, label)
+            self.add_rec(N.RT_K_SPLITK, r, [int(min((p.m * p.n + 7) // 8, 148 * 16)), 1, 1], [256, 1, 1], 0,
+                         label)   # k_splitk: a warp per output
             return True
         return self._gemm_smallk(p, M, nc, kc, f64, label, accumulate, epilogue, bias)
 
@@ -2067,7 +2069,8 @@ class Lowering:
             q.C = p.C
             if bias is not None:
                 q.bias = bias
-            self.add_rec(N.RT_K_SPLITK, q, self.grid1(p.z * p.m * p.n), [256, 1, 1], 0, label)
+            self.add_rec(N.RT_K_SPLITK, q, [int(min((p.z * p.m * p.n + 7) // 8, 148 * 16)), 1, 1], [256, 1, 1], 0,
+                         label)   # k_splitk: a warp per output
 
     def k_contract(self, ctx: Ctx, X):
         """sum over full-range slices of a per-point matmul X, never
