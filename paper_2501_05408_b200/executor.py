@@ -1136,6 +1136,7 @@ class Executable:
         for i in range(N.RT_MAXENV):
             self.env[i] = 0
         pc, hook = N.i32(0), N.i32(-1)
+        pending = []
         if pre is not None:
             N.check(self.lib.rt_graph_launch(pre[0], s.cuda_stream), "prefix graph")
             pc = N.i32(pre[1])
@@ -1154,10 +1155,14 @@ class Executable:
             item = ITEMSIZE_OF[h["dtype"]]
             t = _wrap_ptr(torch, h["ptr"] + off * item, h["count"] * item, self.dev)
             t = t.view(_TORCH_DT[h["dtype"]])
+            pending.append(t)
+            if not h.get("flush", True):
+                continue          # lower._bucket_allreduces: a later hook reduces it
             # NCCL orders the collective after torch's *current* stream:
             # make that the stream the program runs on
             with torch.cuda.stream(s):
-                self.comm.allreduce_(t)
+                _allreduce_bucket(self.comm, pending, torch)
+            pending = []
 
     def profile(self, inputs, stream=None):
         """One run with an event pair around every launch: per-record device
@@ -1337,6 +1342,26 @@ class Executable:
 
 _TORCH_DT = None
 ITEMSIZE_OF = {"f64": 8, "f32": 4, "i64": 8, "bool": 1}
+
+
+def _allreduce_bucket(comm, tensors, torch):
+    """Sum all-reduce of several device tensors as one collective per dtype:
+    flatten into one bucket, reduce, scatter back (a lone tensor is reduced
+    in place)."""
+    by_dt = {}
+    for t in tensors:
+        by_dt.setdefault(t.dtype, []).append(t)
+    for ts in by_dt.values():
+        if len(ts) == 1:
+            comm.allreduce_(ts[0])
+            continue
+        flat = torch.cat([t.reshape(-1) for t in ts])
+        comm.allreduce_(flat)
+        off = 0
+        for t in ts:
+            n = t.numel()
+            t.view(-1).copy_(flat[off:off + n])
+            off += n
 
 
 def _u8view(torch, ptr, nbytes, dev):

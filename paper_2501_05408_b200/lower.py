@@ -499,7 +499,39 @@ class Lowering:
             for info in self.loop_subs.values():
                 params += [op[1] for op in info["ops"]]
             adjust_views(params, self.swap, self.bufs, self.slot)
+        self._bucket_allreduces()
         return self
+
+    def _bucket_allreduces(self):
+        """Mark which all-reduce hooks flush.  A hook whose program continues,
+        before any launch that reads an already-reduced buffer, with another
+        all-reduce hook defers its collective; the last one of such a run
+        all-reduces every pending buffer as ONE bucket (per dtype) — one
+        collective per optimizer step, e.g. C2's six gradient
+        sums and its objective.  Loop boundaries and other hooks flush."""
+        from .memplan import touched_ptrs
+        pending = set()
+        for pc, ins in enumerate(self.prog):
+            if ins[0] != N.RT_OP_HOOK:
+                continue
+            h = self.hooks[ins[1]]
+            if h.get("kind", "allreduce") != "allreduce":
+                continue
+            pending.add(h["ptr"])
+            flush = True
+            for j in range(pc + 1, len(self.prog)):
+                nxt = self.prog[j]
+                if nxt[0] == N.RT_OP_LAUNCH:
+                    if touched_ptrs(self.recs[nxt[1]][1]) & pending:
+                        break
+                    continue
+                if nxt[0] == N.RT_OP_HOOK and \
+                        self.hooks[nxt[1]].get("kind", "allreduce") == "allreduce":
+                    flush = False
+                break
+            h["flush"] = flush
+            if flush:
+                pending = set()
 
     def steps(self, steps):
         for s in steps:

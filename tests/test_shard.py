@@ -235,3 +235,30 @@ def test_sharded_run_over_nccl_on_a_side_stream():
     p.join(timeout=60)
     for k, want in full.items():
         np.testing.assert_allclose(res[k], want, rtol=1e-5, atol=1e-6, err_msg=k)
+
+
+def test_gradient_allreduces_bucket_into_one_collective():
+    """The sharded C2 program's seven sum all-reduces (six gradients and the
+    objective) all precede their first consumer, so only the last hook
+    flushes: one collective per optimizer step; PPO flushes
+    once per minibatch update."""
+    g = load_graph("reinforce_mlp_c2")
+    low = _dry(g, {"I": 1, "B": 8, "T": 16}, ShardSpec("b", 0, 2))
+    flags = [h["flush"] for h in low.hooks]
+    assert len(flags) == 7 and flags.count(True) == 1 and flags[-1]
+    lowp = _dry_shard(load_graph("ppo_c3"), {"I": 1, "E": 2, "M": 2, "U": 4, "B": 8, "T": 6},
+                      ShardSpec("b", 1, 2, ("u",)))
+    assert any(h["flush"] for h in lowp.hooks)
+    assert sum(h["flush"] for h in lowp.hooks) < len(lowp.hooks)
+
+
+def test_allreduce_bucket_sums_each_tensor():
+    from paper_2501_05408_b200.executor import _allreduce_bucket
+
+    class Twice:
+        def allreduce_(self, t):
+            t.mul_(2)
+            return t
+    a, b, c = torch.ones(3), torch.arange(4.0), torch.ones(2, dtype=torch.float64)
+    _allreduce_bucket(Twice(), [a, b, c], torch)
+    assert a.tolist() == [2.0] * 3 and b.tolist() == [0.0, 2.0, 4.0, 6.0] and c.tolist() == [2.0, 2.0]
