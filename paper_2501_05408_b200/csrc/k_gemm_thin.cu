@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant
 // variant 2: rows of X (K <= KP values each, zero-padded to KP) times a
 // resident [KP, R] Y; each thread owns output columns, rows stream through
 // a shared-memory tile, stores are coalesced along r.
-template <typename T, int KP>
+// GATE: the epilogue-2 instantiation (its 16-row h prefetch is kept out of
+// the plain kernel's register budget)
+template <typename T, int KP, bool GATE = false>
 __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__ rt_thin_params p) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   constexpr int RT = 64;  // rows per tile
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
   }
   // epilogue 2 (tanh-VJP gate, executor.find_gate_epilogues): C = acc * (1 - h*h)
   // with h in the bias slot, laid out exactly like C; no bias then
-  const bool gate = p.epilogue == 2;
+  constexpr bool gate = GATE;
   const T* Hg = gate ? (const T*)p.bias.ptr + p.bias.off : nullptr;
   for (int r = threadIdx.x; r < R; r += THREADS)
     bs[r] = (p.bias.ptr && !gate)
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
       for (int k = 0; k < KP; ++k) yreg[k] = ys[k * R + r];
       const T b = bs[r];
       T* cbase = Cp + r * cr;
-      if (gate) {
+      if constexpr (GATE) {
         // 16 rows per chunk: their h loads are issued together (a load per
         // output row one at a time left the kernel latency-bound)
         for (int rr0 = 0; rr0 < nrow; rr0 += 16) {
@@ -311,6 +313,19 @@ extern "C" void* rt_kernel_thin_rows(int f64, int r, int k) {
 }
 
 extern "C" void* rt_kernel_thin(int variant, int f64, int r) {
+  if (variant == 4) {
+    // variant 2 with the tanh-VJP gate epilogue (runtime.cu passes 4)
+    if (f64) {
+      if (r <= 4) return (void*)k_thin_smallk<double, 4, true>;
+      if (r <= 8) return (void*)k_thin_smallk<double, 8, true>;
+      if (r <= 16) return (void*)k_thin_smallk<double, 16, true>;
+      return (void*)k_thin_smallk<double, 32, true>;
+    }
+    if (r <= 4) return (void*)k_thin_smallk<float, 4, true>;
+    if (r <= 8) return (void*)k_thin_smallk<float, 8, true>;
+    if (r <= 16) return (void*)k_thin_smallk<float, 16, true>;
+    return (void*)k_thin_smallk<float, 32, true>;
+  }
   if (variant == 2) {
     // r carries K for this variant (see lower.py _gemm_thin)
     if (f64) {

@@ -169,7 +169,9 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_gop(p->C, env, nenv);
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
       if (p->variant == 3) return rt_kernel_thin_rows(p->f64, (int)p->r, (int)p->k);
-      return rt_kernel_thin(p->variant, p->f64, (int)(p->variant == 2 ? p->k : p->r));
+      // variant 2 with epilogue 2 (gate) is a separate instantiation ("4")
+      return rt_kernel_thin(p->variant == 2 && p->epilogue == 2 ? 4 : p->variant, p->f64,
+                            (int)(p->variant == 2 ? p->k : p->r));
     }
     case RT_K_SPLITK: {
       rt_splitk_params* p = (rt_splitk_params*)blk;
