@@ -74,7 +74,9 @@ enum rt_status_code {
   RT_ERR_SLICE_RANGE = 2,   /* index_select rows lo:hi outside (runtime.py:176-177) */
   RT_ERR_CUDA = 3,
   RT_ERR_BAD_ARG = 4,
-  RT_ERR_UNKNOWN_KERNEL = 5
+  RT_ERR_UNKNOWN_KERNEL = 5,
+  RT_ERR_DIV_ZERO = 6       /* index expression // or % by zero (symexpr.py:491-506);
+                               aux = (dividend, 0 for //, 1 for %) */
 };
 
 /* A flat index over a box, decomposed row-major. */

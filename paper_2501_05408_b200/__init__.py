@@ -5,7 +5,9 @@ Drop-in replacement for the reference executor `recten.runtime.reference_execute
 behind a C ABI (include/rtb200.h), driven by a loop-nest planner.
 """
 
-from .executor import OracleError, RuntimeError_, execute, get_executable  # noqa: F401
+from .executor import (EvaluationError, OracleError, RuntimeError_, execute,  # noqa: F401
+                       get_executable)
 from .ir import Graph, from_pdg  # noqa: F401
 
-__all__ = ["execute", "get_executable", "Graph", "from_pdg", "RuntimeError_", "OracleError"]
+__all__ = ["execute", "get_executable", "Graph", "from_pdg", "RuntimeError_", "OracleError",
+           "EvaluationError"]

@@ -20,6 +20,8 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import sys
+from collections import OrderedDict
 import weakref
 
 import os
@@ -42,10 +44,25 @@ class OracleError(RuntimeError_):
     """reference runtime.py:29-30 (kept for drop-in error handling)"""
 
 
+class EvaluationError(Exception):
+    """reference symexpr.py:30 (`EvaluationError(SymExprError)`): an index
+    expression divided by zero on device (symexpr.py:491-506)."""
+
+
 DYN_CAP = 4096  # reference runtime.py:33
 
 _ERR_TEXT = {N.RT_ERR_ROW_RANGE: "row {a} outside 0..{b1}",
              N.RT_ERR_SLICE_RANGE: "rows {a}:{b} outside the folded axis"}
+
+
+def _status_error(g, code, node_id, a, b):
+    """The exception the reference raises for a device status word."""
+    node = g.nodes.get(int(node_id))
+    name = node.name if node else f"n{int(node_id)}"
+    if code == N.RT_ERR_DIV_ZERO:
+        return EvaluationError(f"{'modulo' if b else 'division'} by zero (in {name})")
+    txt = _ERR_TEXT.get(int(code), "device error {a} {b}").format(a=int(a), b=int(b), b1=int(b) - 1)
+    return RuntimeError_(f"{name}: {txt}")
 
 
 def _torch():
@@ -856,7 +873,8 @@ class Executable:
                 ptrs |= memplan.touched_ptrs(op[1])
             rec_ptrs.append({(q >> 44) << 44 for q in ptrs if q >> 44})
         life = memplan.lifetimes(low.prog, rec_ptrs, key_of, pinned,
-                                 fold_slots(self.bufs, low.slot))
+                                 fold_slots(self.bufs, low.slot),
+                                 hook_ptrs=memplan.hook_touches(low.prog, low.hooks))
         for k in roots:
             life.setdefault(k, (-1, -1))   # never touched: still allocated, tiny lifetime
         sizes = {k: max(1, self.bufs[k].nbytes) for k in roots}
@@ -911,8 +929,9 @@ class Executable:
         self.labels = [lab for (*_, lab) in low.recs]
         self.kernels = [k for (k, *_rest) in low.recs]
         from . import jit
-        self.jit_count = jit.specialise(recs, self.kernels, self._params, self.labels,
-                                        self.loop_info)
+        with self.torch.cuda.device(self.dev):
+            self.jit_count = jit.specialise(recs, self.kernels, self._params, self.labels,
+                                            self.loop_info)
         prog = (N.rt_instr * max(1, len(low.prog)))()
         for i, ins in enumerate(low.prog):
             prog[i].op, prog[i].a, prog[i].b, prog[i].c, prog[i].d, prog[i].e = (
@@ -1005,6 +1024,18 @@ class Executable:
     # -- run -------------------------------------------------------------------
 
     def upload_inputs(self, inputs, stream):
+        """Copy the inputs into their arena buffers ON `stream` (the
+        program's stream): the copies, and the events guarding the reused
+        pinned staging buffers, are ordered with the program itself."""
+        torch = self.torch
+        cur = torch.cuda.current_stream(self.dev)
+        if stream != cur and any(isinstance(v, torch.Tensor) and v.is_cuda
+                                 for v in (inputs or {}).values()):
+            stream.wait_stream(cur)       # device inputs produced on the caller's stream
+        with torch.cuda.stream(stream):
+            self._upload(inputs, stream)
+
+    def _upload(self, inputs, stream):
         torch = self.torch
         for n in self.g.sorted_nodes():
             if n.kind != "input":
@@ -1262,11 +1293,7 @@ class Executable:
         st = (N.i32 * 4)()
         N.check(self.lib.rt_status_read(self.status, st, s.cuda_stream), "status read")
         if st[0] != 0:
-            node = self.g.nodes.get(st[1])
-            name = node.name if node else f"n{st[1]}"
-            txt = _ERR_TEXT.get(st[0], "device error {a} {b}").format(a=st[2], b=st[3],
-                                                                      b1=st[3] - 1)
-            raise RuntimeError_(f"{name}: {txt}")
+            raise _status_error(self.g, st[0], st[1], st[2], st[3])
 
     def fetch(self, stream=None):
         """Status word + every output in ONE device->host synchronisation:
@@ -1307,11 +1334,7 @@ class Executable:
 
     def _raise_status(self, st):
         if st[0] != 0:
-            node = self.g.nodes.get(int(st[1]))
-            name = node.name if node else f"n{int(st[1])}"
-            txt = _ERR_TEXT.get(int(st[0]), "device error {a} {b}").format(
-                a=int(st[2]), b=int(st[3]), b1=int(st[3]) - 1)
-            raise RuntimeError_(f"{name}: {txt}")
+            raise _status_error(self.g, st[0], st[1], st[2], st[3])
 
     def outputs(self, device_outputs=False, clone=True):
         torch = self.torch
@@ -1434,6 +1457,8 @@ def _eval_int(e, env):
         return min(vals)
     if k == "max":
         return max(vals)
+    if k in ("floordiv", "mod") and vals[1] == 0:
+        raise EvaluationError(f"{'division' if k == 'floordiv' else 'modulo'} by zero")
     if k == "floordiv":
         q = vals[0] // vals[1]
         if vals[0] % vals[1] != 0 and vals[1] < 0:
@@ -1449,8 +1474,61 @@ def _eval_int(e, env):
 # public API
 
 
-_CACHE: dict = {}
+_CACHE: "OrderedDict" = OrderedDict()
+CACHE_MAX = int(os.environ.get("RTB200_CACHE_MAX", "8"))   # executables kept (LRU)
 _PREP: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _param_sig(v):
+    if isinstance(v, np.ndarray):
+        return ("arr", v.shape, str(v.dtype), hash(v.tobytes()) if v.size <= 65536 else id(v))
+    if isinstance(v, dict):
+        return tuple(sorted((k, _param_sig(x)) for k, x in v.items()))
+    if isinstance(v, (list, tuple)):
+        return tuple(_param_sig(x) for x in v)
+    try:
+        hash(v)
+        return v
+    except TypeError:
+        return repr(v)
+
+
+def _params_sig(params):
+    out = []
+    for k, v in params.items():
+        try:
+            hash(v)
+            out.append((k, v))
+        except TypeError:
+            out.append((k, _param_sig(v)))
+    return tuple(out)
+
+
+def fingerprint(g: Graph):
+    """Structural key of a graph: dims, bindings, nodes (kind, domain,
+    shapes, dtypes, params incl. constant values), edges, outputs.  The
+    reference transforms rewrite a Pdg IN PLACE (vectorize_all, fuse,
+    incrementalize), so the executable cache cannot key on object identity."""
+    nodes = tuple((n.id, n.name, n.kind, n.domain, n.out_shapes, n.out_dtypes, n.nin,
+                   _params_sig(n.params)) for n in g.nodes.values())
+    edges = tuple((e.sink, e.iid, e.phi, e.psi, e.oid, e.src) for e in g.edges)
+    return hash((tuple(g.dim_order), tuple(sorted(g.dim_bound.items())),
+                 tuple(sorted(g.bindings.items(), key=str)), tuple(g.outputs), nodes, edges))
+
+
+_KNOB_NAMES = None
+
+
+def _knobs():
+    """Module-level lowering switches (tests flip them): part of the key."""
+    global _KNOB_NAMES
+    from . import jit
+    mods = (jit, sys.modules[__name__])
+    if _KNOB_NAMES is None:
+        _KNOB_NAMES = [[k for k, v in vars(m).items()
+                        if k.isupper() and isinstance(v, (bool, int, float, str))] for m in mods]
+    return (tuple(getattr(m, k) for m, ks in zip(mods, _KNOB_NAMES) for k in ks),
+            tuple(OPTS.items()))
 
 
 def _bind_bounds(g: Graph, bounds):
@@ -1499,11 +1577,14 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         benv = _resolve_dynamic(graph, benv, dyn, inputs, seed, device)
     dev = torch.cuda.current_device() if device is None else int(device)
     block = tuple(block) if block else None
-    key = (id(g), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs), shard, block,
-           swap)
+    key = (fingerprint(graph), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs),
+           shard, block, swap, _knobs())
     ex = _CACHE.get(key)
-    if ex is not None and ex[0]() is g:
-        return ex[1], benv
+    if ex is not None:
+        _CACHE.move_to_end(key)
+        return ex, benv
+    from .demand import check as demand_check
+    demand_check(graph, benv)      # the reference's out-of-domain OracleError (F5)
     h = copy_graph(graph)
     prepare(h, benv)
     outer_benv = benv
@@ -1515,10 +1596,9 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         comm = TorchComm()
     exe = Executable(h, benv, int(seed), dev, _input_sig(inputs), shard=shard, comm=comm,
                      swap=swap if block else False)
-    try:
-        _CACHE[key] = (weakref.ref(g), exe)
-    except TypeError:
-        pass
+    _CACHE[key] = exe
+    while len(_CACHE) > CACHE_MAX:
+        _CACHE.popitem(last=False)        # frees the least recently used arena
     return exe, outer_benv
 
 

@@ -107,8 +107,10 @@ def _program_lines(p, T, nd, base=None, chk=None, env="p.h.env", load_override=N
         elif o in ("IADD", "ISUB", "IMUL"):
             w(f"n{d} = n{a} {'+-*'[['IADD', 'ISUB', 'IMUL'].index(o)]} n{b};")
         elif o == "IFDIV":
+            w(f"if (n{b} == 0) report(p.h, {N.RT_ERR_DIV_ZERO}, n{a}, 0);")
             w(f"n{d} = euclid_div(n{a}, n{b});")
         elif o == "IMOD":
+            w(f"if (n{b} == 0) report(p.h, {N.RT_ERR_DIV_ZERO}, n{a}, 1);")
             w(f"n{d} = euclid_mod(n{a}, n{b});")
         elif o in ("IMIN", "IMAX"):
             w(f"n{d} = n{a} {'<' if o == 'IMIN' else '>'} n{b} ? n{a} : n{b};")
@@ -1307,8 +1309,12 @@ _HDR_KEY = _headers_key()
 def compile_kernel(src: str, name: str) -> int:
     """CUfunction handle for `name` in `src` (process + on-disk cubin cache)."""
     key = hashlib.sha256((src + name + _HDR_KEY).encode()).hexdigest()
-    if key in _FN_CACHE:
-        return _FN_CACHE[key]
+    # cuModuleLoadData binds the function to the CURRENT context: one handle
+    # per (kernel, device); callers load under torch.cuda.device(dev)
+    import torch
+    dkey = (key, torch.cuda.current_device())
+    if dkey in _FN_CACHE:
+        return _FN_CACHE[dkey]
     lib = N.lib()
     fn = N.u64(0)
     path = os.path.join(CACHE, key + ".cubin")
@@ -1333,7 +1339,7 @@ def compile_kernel(src: str, name: str) -> int:
         except OSError:
             pass
     N.check(lib.rt_jit_load(image, name.encode(), C.byref(fn)), "jit load")
-    _FN_CACHE[key] = fn.value
+    _FN_CACHE[dkey] = fn.value
     return fn.value
 
 

@@ -282,7 +282,7 @@ class Lowering:
         self.absorbed = set(absorbed or ())
         self.virtual |= self.absorbed
         self.persistent = persistent
-        self.use_tc = use_tc
+        self.use_tc = use_tc and os.environ.get("RTB200_GEMM", "") != "simt"
         self.use_tma = os.environ.get("RTB200_GEMM", "") != "tc"
         self.shard = shard
         self.shard_reduce = set(shard_reduce or ())
@@ -1026,9 +1026,21 @@ class Lowering:
                 and e.phi == tuple(("sym", d, "loop") for d in src.domain)
                 and list(self.bufs[(src.id, e.oid)].pshape) == list(out_p))
 
+    ROUND_KINDS = {"add", "sub", "mul", "div", "neg", "exp", "log", "tanh", "sqrt", "pow_const",
+                   "scan"}
+
     def _value(self, ctx: Ctx, n, P: Prog, views: list, out_p, depth):
         """Compile node n's value at the current box element into a value
-        register; single-consumer pointwise producers are inlined."""
+        register; single-consumer pointwise producers are inlined.  An
+        inlined f32 result is rounded to f32 (a no-op unless the fused
+        program computes in f64 because some other operand is f64: numpy
+        rounds every f32 op, e.g. cast(x, f32) * 3 in an f64 program)."""
+        r = self._value_raw(ctx, n, P, views, out_p, depth)
+        if n.dtype == "f32" and n.kind in self.ROUND_KINDS and self._f64:
+            P.emit("VCAST", d=r, a=r, imm=N.RT_F32)
+        return r
+
+    def _value_raw(self, ctx: Ctx, n, P: Prog, views: list, out_p, depth):
         ins = self.g.in_edges(n.id)
         if n.dtype == "f64":
             self._f64 = True
@@ -1054,10 +1066,46 @@ class Lowering:
                 pst = self.bcast(ev, out_p)
             else:
                 pst = mapping(ev)
+            if ev.progs:
+                return gather(ev, pst)
             vi = view_of(ev, pst)
             r = P.vreg()
             P.emit("LOAD", d=r, imm=vi)
             return r
+
+        def gather(ev, pst):
+            """Non-affine φ components (floordiv/mod/min/max of dims,
+            symexpr.py:521-570) evaluated per element on device (Euclidean
+            // and %; a zero divisor sets RT_ERR_DIV_ZERO): row offset
+            sum(c_j(point) * stride_j), the load masked when a component
+            leaves the source's domain (like the affine checks)."""
+            dm = ctx.dimmap()
+            off = P.ireg()
+            P.emit("ICONST", d=off, imm=0)
+            ok = P.ireg()
+            P.emit("ICONST", d=ok, imm=1)
+            for c, S, hi_dom in ev.progs:
+                r = P.int_expr(c, dm)
+                t = P.ireg()
+                P.emit("ICONST", d=t, imm=0)
+                P.emit("IGE", d=t, a=r, b=t)
+                P.emit("IAND", d=ok, a=ok, b=t)
+                P.emit("ICONST", d=t, imm=hi_dom)
+                P.emit("ILT", d=t, a=r, b=t)
+                P.emit("IAND", d=ok, a=ok, b=t)
+                P.emit("ICONST", d=t, imm=S)
+                P.emit("IMUL", d=t, a=t, b=r)
+                P.emit("IADD", d=off, a=off, b=t)
+                P.ifree_(t)
+                P.ifree_(r)
+            plain = EdgeVal(buf=ev.buf, off=ev.off, coef=dict(ev.coef), checks=list(ev.checks),
+                            axes=ev.axes, nslices=ev.nslices, psi=ev.psi)
+            vi = view_of(plain, pst)
+            v = P.vreg()
+            P.emit("LOADX", d=v, a=off, b=ok, imm=vi)
+            P.ifree_(ok)
+            P.ifree_(off)
+            return v
 
         k = n.kind
         if k in ("add", "sub", "mul", "div"):

@@ -56,17 +56,42 @@ def loop_spans(prog):
     return spans
 
 
-def lifetimes(prog, rec_ptrs, key_of_ptr, pinned, folds=None):
+def hook_touches(prog, hooks):
+    """pc -> buffer pointers an all-reduce hook reads and writes there.  A
+    bucketed hook (lower._bucket_allreduces) defers its collective to the
+    flushing hook of its run, so its buffer is touched at that pc too."""
+    out, pending = {}, set()
+    for pc, ins in enumerate(prog):
+        if ins[0] != N.RT_OP_HOOK:
+            continue
+        h = hooks[ins[1]]
+        if h.get("kind", "allreduce") != "allreduce" or "ptr" not in h:
+            continue
+        pending.add(h["ptr"])
+        out.setdefault(pc, set()).add(h["ptr"])
+        if h.get("flush", True):
+            out[pc] |= pending
+            pending = set()
+    return out
+
+
+def lifetimes(prog, rec_ptrs, key_of_ptr, pinned, folds=None, hook_ptrs=None):
     """key -> (first pc, last pc).  A buffer folded along a loop's dim
     (executor.find_folds: produced and consumed within one iteration) is
-    not kept live across that loop's iterations."""
+    not kept live across that loop's iterations.  hook_ptrs (pc -> ptrs,
+    hook_touches) extends buffers to the hooks that all-reduce them."""
     folds = folds or {}
+    hook_ptrs = hook_ptrs or {}
     spans = [s for s in loop_spans(prog) if s[2] > 1]
     touch = {}
     for pc, ins in enumerate(prog):
-        if ins[0] != N.RT_OP_LAUNCH:
+        if ins[0] == N.RT_OP_HOOK:
+            ptrs = {(q >> 44) << 44 for q in hook_ptrs.get(pc, ())}
+        elif ins[0] == N.RT_OP_LAUNCH:
+            ptrs = rec_ptrs[ins[1]]
+        else:
             continue
-        for p in rec_ptrs[ins[1]]:
+        for p in ptrs:
             k = key_of_ptr.get(p)
             if k is None:
                 continue

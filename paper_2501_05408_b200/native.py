@@ -36,6 +36,7 @@ RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK, RT_OP_ENVMOD = 1, 2
 RT_HOOK = 100
 
 RT_ERR_ROW_RANGE, RT_ERR_SLICE_RANGE = 1, 2
+RT_ERR_DIV_ZERO = 6
 
 i32, i64, u64, u32, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_uint32, C.c_double
 

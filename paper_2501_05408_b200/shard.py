@@ -68,8 +68,10 @@ def _check_dim(g: ir.Graph, d: str, env_dim: str, also: tuple, benv) -> set:
             raise ShardError(f"{n.name}: dim {d} is folded into a payload axis")
         if n.kind == "merge" and any(_mentions(c, d) for c in n.params["conds"]):
             raise ShardError(f"{n.name}: branch condition depends on {d}")
-        if n.kind == "eval_symbol" and n.params["symbol"].name == d:
-            raise ShardError(f"{n.name}: reads the value of {d}")
+        if n.kind == "eval_symbol" and n.params["symbol"].name in (d, bound):
+            # the bound too: a shard sees the per-rank extent, so e.g.
+            # sum(x[0:B]) / B would divide the all-reduced sum by the local B
+            raise ShardError(f"{n.name}: reads the value of {n.params['symbol'].name}")
         if n.kind in ("index_select", "window_reduce", "slice_axis", "scan") and \
                 getattr(n.params.get("dim"), "name", None) == d:
             raise ShardError(f"{n.name}: {n.kind} along {d}")

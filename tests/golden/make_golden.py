@@ -160,14 +160,76 @@ def edge_cases():
                    {"program": "ppo_mlp", "edge": True})
 
 
+# Full-width benchmark programs (obs 16, H=256 x 2, act 4 [+ value head]) at
+# sizes where the executor picks the kernels the benchmark runs: the JIT
+# acting loop (forced on by the test), tcgen05 TMA GEMMs with the bias+tanh
+# epilogue, the thin row/small-K/gate kernels and split-K.  (name, kind,
+# dtype, I, B, T, epochs, minibatches)
+FULLWIDTH = (
+    ("fw_mlp_f32_I2B1024T8", "mlp", "f32", 2, 1024, 8, 0, 0),
+    ("fw_mlp_f32_I2B8T32", "mlp", "f32", 2, 8, 32, 0, 0),
+    ("fw_mlp_f64_I2B8T16", "mlp", "f64", 2, 8, 16, 0, 0),
+    ("fw_ppo_f32_I1B1024T8E2M2", "ppo", "f32", 1, 1024, 8, 2, 2),
+    ("fw_ppo_f64_I1B16T8E2M2", "ppo", "f64", 1, 16, 8, 2, 2),
+)
+
+
+def fullwidth_case(spec):
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+    name, kind, dt, I, B, T, ep, mb = spec
+    if kind == "mlp":
+        ctx = P.ctx_reinforce_mlp(B=B, T=T, I=I, dtype=dt)
+        inputs = P.mlp_inputs(dtype=dt)
+    else:
+        ctx = P.ctx_ppo_mlp(B=B, T=T, I=I, epochs=ep, minibatches=mb, dtype=dt)
+        inputs = ppo_inputs(16, 256, 4, dt)
+    g = pdg.build(ctx)
+    pdg.eliminate_dead(g)
+    write_case(name, g, None, inputs, 0,
+               {"program": "reinforce_mlp" if kind == "mlp" else "ppo_mlp", "dtype": dt,
+                "fullwidth": True})
+
+
+def fullwidth_cases():
+    from multiprocessing import Pool
+    with Pool(len(FULLWIDTH)) as pool:
+        pool.map(fullwidth_case, FULLWIDTH)
+
+
+def opset_cases():
+    """The remaining KERNELS kinds (div, log, sqrt, where, cast, reshape,
+    squeeze, identity, eval_symbol, cumsum), the unit-gamma cumsum lift
+    (reference test_transforms.py:223-237), Euclidean index KATs with
+    negative operands and a zero divisor (symexpr.py:491-506)."""
+    dsl, fe, pdg, tr, rt, ps = P.recten()
+    V = variants()
+    for dt in ("f64", "f32"):
+        for vname in ("plain", "vec"):
+            g = pdg.build(P.ctx_opset(dtype=dt))
+            V[vname](g)
+            write_case(f"ops_{dt}_{vname}", g, None, None, 3, {"program": "opset", "variant": vname})
+    for vname in ("plain", "vec"):
+        g = pdg.build(P.ctx_unit_cumsum())
+        V[vname](g)
+        write_case(f"tr_unit_cumsum_{vname}", g, None, None, 1,
+                   {"program": "unit_cumsum", "variant": vname})
+    x = np.arange(9.0) * 1.5 - 2.0
+    g = pdg.build(P.ctx_euclid())
+    write_case("kat_euclid", g, None, {"x": x}, 0, {"program": "euclid"})
+    g = pdg.build(P.ctx_divzero())
+    write_case("kat_divzero", g, None, {"x": np.arange(5.0)}, 0, {"program": "divzero"})
+
+
 def main():
     dsl, fe, pdg, tr, rt, ps = P.recten()
     os.makedirs(CASES, exist_ok=True)
     os.makedirs(GRAPHS, exist_ok=True)
     if "--only" in sys.argv:
         what = sys.argv[sys.argv.index("--only") + 1]
-        return {"ppo": ppo_cases, "kernels": kernel_graphs, "edge": edge_cases}[what]()
+        return {"ppo": ppo_cases, "kernels": kernel_graphs, "edge": edge_cases,
+                "fullwidth": fullwidth_cases, "opset": opset_cases}[what]()
     ppo_cases()
+    opset_cases()
     V = variants()
 
     # corpus x variants x seeds (reference pkg/tests/test_dsl.py:240-248)

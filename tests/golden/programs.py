@@ -229,6 +229,93 @@ def ctx_widesum(T=3, payload=(40, 8)):
     return ctx
 
 
+def ctx_opset(T=5, dtype="f64"):
+    """Every remaining elementwise / layout / control kind of the reference
+    KERNELS table (runtime.py:58-93, 149-150, 239-259) in one program:
+    div, log, sqrt, exp, cmp, where, cast (both ways), reshape, squeeze,
+    unsqueeze, identity, eval_symbol of a loop dim and of a bound, cumsum
+    forward and reverse on a payload axis."""
+    dsl, fe, pdg, tr, rt, ps = recten()
+    ctx = fe.Context()
+    t, Tb = ctx.declare_dim("t", "T")
+    ctx.bind(Tb, T)
+    other = "f32" if dtype == "f64" else "f64"
+    x = ctx.rng("x", (3, 2), dtype, (t,))
+    u = ctx.rng("u", (3, 2), dtype, (t,), dist="uniform")
+    one = ctx.constant(1.0, dtype, (), name="one")
+    half = ctx.constant(0.5, dtype, (), name="half")
+    zero = ctx.constant(0.0, dtype, (), name="zero")
+    lg = ctx.op("log", [ctx.op("exp", [x]) + one], name="lg")
+    sq = ctx.op("sqrt", [u + half], name="sq")
+    q = ctx.op("div", [lg, sq], name="q")
+    pos = ctx.cmp("gt", x, zero)
+    w = ctx.where(pos, x, -x)
+    c1 = ctx.op("cast", [w], {"dtype": other}, name="c1")
+    back = ctx.op("cast", [c1 * ctx.constant(3.0, other, (), name="three")],
+                  {"dtype": dtype}, name="back")
+    rs = ctx.reshape(q, (6,))
+    rs2 = ctx.reshape(rs, (2, 3))
+    uq = ctx.unsqueeze(rs2, 0)
+    sqz = ctx.squeeze(uq, 0)
+    idn = ctx.op("identity", [sqz], name="idn")
+    ev = ctx.eval_symbol(t)
+    evf = ctx.op("cast", [ev], {"dtype": dtype}, name="evf")
+    y = ctx.op("mul", [idn, evf + one], name="y")
+    nT = ctx.op("cast", [ctx.eval_symbol(Tb)], {"dtype": dtype}, name="nT")
+    tot = ctx.sum(y["0:T"], 0)
+    mean = ctx.op("div", [tot, nT], name="mean")
+    csf = ctx.cumsum(back, 0)
+    csr = ctx.cumsum(back, 1, reverse=True)
+    for name, v in (("q", q), ("w", w), ("pos", pos), ("back", back), ("idn", idn),
+                    ("ev", ev), ("y", y), ("mean", mean), ("csf", csf), ("csr", csr)):
+        ctx.mark_output(v, name)
+    return ctx
+
+
+def ctx_unit_cumsum(T=6):
+    """reference pkg/tests/test_transforms.py:223-237: a unit-gamma scan that
+    vectorize_all lifts to a `cumsum` over the time axis."""
+    dsl, fe, pdg, tr, rt, ps = recten()
+    import recten.symexpr as se
+    ctx = fe.Context()
+    t, Tb = ctx.declare_dim("t", "T")
+    ctx.bind(Tb, T)
+    x = ctx.rng("x", (2,), domain=(t,))
+    y = ctx.recurrent("y", (2,), domain=(t,))
+    y.define([(se.eq(se.sym(t), se.cint(0)), x), (None, y["t-1"] + x["t"])])
+    ctx.mark_output(y, "y")
+    return ctx
+
+
+def ctx_euclid(T=9):
+    """Euclidean // and % with negative operands inside device index
+    expressions (reference symexpr.py:491-506; KATs test_symexpr.py:34-49:
+    -t % 4 with t=3 -> 1, -7 // 2 -> -4): y[t] = x[(t - 5) % 4] + x[(t - 7) // 2 + 4]."""
+    dsl, fe, pdg, tr, rt, ps = recten()
+    ctx = fe.Context()
+    t, Tb = ctx.declare_dim("t", "T")
+    ctx.bind(Tb, T)
+    x = ctx.input("x", (), "f64", (t,))
+    y = ctx.op("add", [x["(t - 5) % 4"], x["(t - 7) // 2 + 4"] * 100.0], name="y")
+    z = ctx.op("mul", [x["(-t) % 4"], x["(8 - t) // 3"]], name="z")
+    ctx.mark_output(y, "y")
+    ctx.mark_output(z, "z")
+    return ctx
+
+
+def ctx_divzero(T=5):
+    """An index expression that divides by zero at t = 2: the reference
+    raises EvaluationError (symexpr.py:491-506)."""
+    dsl, fe, pdg, tr, rt, ps = recten()
+    ctx = fe.Context()
+    t, Tb = ctx.declare_dim("t", "T")
+    ctx.bind(Tb, T)
+    x = ctx.input("x", (), "f64", (t,))
+    y = ctx.op("mul", [x["t % (t - 2)"], ctx.constant(2.0, "f64", (), name="two")], name="y")
+    ctx.mark_output(y, "y")
+    return ctx
+
+
 # ---------------------------------------------------------------------------
 # The benchmark workload: REINFORCE with a 2-hidden-layer tanh MLP policy
 # (BASELINE.json configs[1]; SURVEY §8(d) C2), f32 via the Context API.
@@ -337,7 +424,10 @@ def ctx_ppo_mlp(B=4096, T=512, I=1, epochs=4, minibatches=4, d_o=16, H=256, d_a=
     assert B % M == 0
     Bm = B // M
     if lr is None:
-        lr = 0.01 / (Bm * T)
+        # 0.01 / (Bm * T) made the importance ratio exp(lp_new - lp_old)
+        # overflow in the second epoch at full width (weights ~1e14 in the
+        # reference's own run); 1e-3 keeps every epoch finite
+        lr = 1e-3 / (Bm * T)
     ctx = fe.Context()
     i, Ib = ctx.declare_dim("i", "I")
     e, Eb = ctx.declare_dim("e", "E")

@@ -1,6 +1,7 @@
 """Parity of the CUDA executor against the reference (golden fixtures) and
-the oracle port, on a B200.  Tolerances (north_star): integer/bool/index
-results exact; fp64 programs rtol 1e-9; fp32 programs rtol 1e-5."""
+the oracle port, on a B200.  Tolerances (north_star): integer /
+bool / index results exact; fp64 programs rtol 1e-12; fp32 programs rtol
+1e-5."""
 
 import numpy as np
 import pytest
@@ -9,7 +10,7 @@ from golden_cases import all_cases, case_ids, load_case
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"f64": dict(rtol=1e-9, atol=1e-12), "f32": dict(rtol=1e-5, atol=1e-6)}
+TOL = {"f64": dict(rtol=1e-12, atol=1e-13), "f32": dict(rtol=1e-5, atol=1e-6)}
 
 
 def assert_close(got, want, name):
@@ -37,14 +38,38 @@ def test_executor_matches_reference(name):
         assert_close(outs[k], want, k)
 
 
+ERR_CASES = [c for c in case_ids() if load_case(c).error]
+
+
+@pytest.mark.parametrize("name", ERR_CASES)
+def test_executor_fails_like_reference(name):
+    """Graphs the reference itself cannot evaluate raise the same exception
+    class with the same message: the F5 eager-fold hazard (OracleError,
+    runtime.py:352-355, via demand.py) and a zero divisor in a device index
+    expression (EvaluationError, symexpr.py:491-506, via the status word)."""
+    from paper_2501_05408_b200 import execute
+    c = load_case(name)
+    with pytest.raises(Exception) as exc:
+        execute(c.graph(), bounds=c.bounds, inputs=c.inputs, seed=c.seed)
+    kind, msg = c.error.split(": ", 1)
+    assert type(exc.value).__name__ == kind
+    if kind == "OracleError":
+        assert str(exc.value) == msg
+    else:
+        assert str(exc.value).startswith(msg)
+
+
 def test_rng_bit_exact_vs_numpy():
-    """Device SeedSequence->PCG64->ziggurat equals numpy default_rng bit for bit."""
+    """Device SeedSequence -> PCG64 -> ziggurat equals numpy default_rng bit
+    for bit on EVERY draw: 100 000 points x 100 draws = 10 M normals (about
+    2.6 k of them from the ziggurat tail, |x| > r = 3.6541528853610088,
+    rng.cuh's log1p/exp path) and 10 M uniforms."""
     import ctypes as C
     import torch
     from paper_2501_05408_b200 import native as N
-    rows, count = 20000, 7
+    rows, count = 100_000, 100
     rng = np.random.default_rng(0)
-    coords = rng.integers(0, 5000, size=(rows, 3)).astype(np.int64)
+    coords = rng.integers(0, 1 << 20, size=(rows, 3)).astype(np.int64)
     coords[:5] = 0
     prefix = [3, 1]
     for dist in (0, 1):
@@ -54,10 +79,14 @@ def test_rng_bit_exact_vs_numpy():
                                  coords.ctypes.data_as(C.POINTER(N.i64)), 3, rows, count, dist, 0)
         N.check(rc, "rng_fill")
         got = out.cpu().numpy().reshape(rows, count)
-        for r in list(range(0, rows, 997)) + [1, 2, 3, 4]:
+        want = np.empty_like(got)
+        for r in range(rows):
             g = np.random.default_rng(tuple(prefix) + tuple(int(x) for x in coords[r]))
-            want = g.standard_normal(count) if dist == 0 else g.uniform(0.0, 1.0, count)
-            assert np.array_equal(got[r], want), r
+            want[r] = g.standard_normal(count) if dist == 0 else g.uniform(0.0, 1.0, count)
+        bad = np.argwhere(got.view(np.int64) != want.view(np.int64))
+        assert bad.size == 0, (dist, bad[:5])
+        if dist == 0:
+            assert int((np.abs(want) > 3.6541528853610088).sum()) > 1000
 
 
 def test_index_select_error_maps_to_runtime_error():

@@ -15,7 +15,14 @@ from golden_cases import case_ids, load_case
 from oracle.pdg_oracle import OracleError, oracle_execute
 
 
-@pytest.mark.parametrize("name", case_ids())
+# The B=1024 full-width fixtures take the per-point port 40-90 s each; they
+# are reference outputs already and are checked against the CUDA path
+# directly (tests/test_gpu_fullwidth.py).  RTB200_PIN_ALL=1 includes them.
+SLOW = {"fw_mlp_f32_I2B1024T8", "fw_ppo_f32_I1B1024T8E2M2"}
+
+
+@pytest.mark.parametrize("name", [c for c in case_ids()
+                                  if os.environ.get("RTB200_PIN_ALL") or c not in SLOW])
 def test_oracle_port_matches_reference(name):
     c = load_case(name)
     g = c.graph()
