@@ -17,9 +17,11 @@ One step = one call of the program at I=1: roll out, returns/advantages
   e2e   : public API `execute()` with host numpy weights in and updated
           weights + outputs out (H2D/D2H inside the timed region)
 
-`--impl reference` times the reference CPU implementation of the same
-program (the oracle port of reference_execute, oracle/pdg_oracle.py) on a
-bounded sample on the host cores.
+`--impl reference` times the reference's own CPU executor on the same
+program: recten.runtime.reference_execute from the installed reference
+package (baseline/_ref; the oracle port oracle/pdg_oracle.py when it is
+absent) on a bounded sample (the real horizon, fewer envs) on every host
+core.
 """
 
 from __future__ import annotations
@@ -35,6 +37,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 
 
 class Workload:
@@ -182,58 +185,97 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def _oracle_sample():
-    g = load_graph()
-    inputs = WL.inputs()
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _ref_importable():
+    """The reference package itself (`pip install --target baseline/_ref
+    /root/reference`, git-ignored, shipped to the GPU box), else None."""
+    try:
+        import programs as P   # tests/golden/programs.py builds through recten's front end
+        P.recten()
+        return P
+    except Exception:
+        return None
+
+
+def _ref_sample():
+    """A bounded sample of WL's program for the CPU: the REAL horizon (C2:
+    T=1000, so the reference's O(T^2) r[t:T] gather is paid as in the real
+    workload) over fewer envs (envs are independent: the per-point
+    interpreter's cost is linear in them).  PPO: 4 envs x T=128, 4 epochs x
+    4 minibatches.  Returns (kind, graph, inputs, bounds, env-steps per call)."""
+    P = _ref_importable()
     if WL.ppo:
-        B, T = 4, 16
-        bounds = {"I": 1, "E": 2, "M": 2, "U": 2, "B": B, "T": T}
+        B, T = 4, min(WL.T, 128)
+        bounds = {"I": 1, "E": 4, "M": 4, "U": 1, "B": B, "T": T}
     else:
-        B, T = 4, 32
+        B, T = 1, min(WL.T, 1000)
         bounds = {"I": 1, "B": B, "T": T}
-    return g, inputs, bounds, B * T
+    inputs = WL.inputs()
+    if P is not None:
+        dsl, fe, pdg, tr, rt, ps = P.recten()
+        ctx = (P.ctx_ppo_mlp(B=B, T=T, I=1, epochs=4, minibatches=4) if WL.ppo
+               else P.ctx_reinforce_mlp(B=B, T=T, I=1))
+        g = pdg.build(ctx)
+        pdg.eliminate_dead(g)
+        return "reference", g, inputs, None, B * T
+    return "port", load_graph(), inputs, bounds, B * T
 
 
-def _oracle_worker(args):
-    """One host process: run the oracle port on distinct seeds for `seconds`."""
+def _ref_worker(args):
+    """One host process: run the reference executor (recten.runtime.
+    reference_execute on the untransformed graph; else the oracle port) on
+    distinct seeds for `seconds`."""
     wl, seconds, seed0 = args
     global WL
     WL = WORKLOADS[wl]
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    from oracle.pdg_oracle import oracle_execute
-    g, inputs, bounds, per = _oracle_sample()
+    kind, g, inputs, bounds, per = _ref_sample()
+    if kind == "reference":
+        import recten.runtime as rt
+        run = rt.reference_execute
+    else:
+        from oracle.pdg_oracle import oracle_execute as run
     t0 = time.perf_counter()
     n = 0
     while True:
-        oracle_execute(g, bounds=bounds, inputs=inputs, seed=seed0 + n)
+        run(g, bounds=bounds, inputs=inputs, seed=seed0 + n)
         n += 1
         if time.perf_counter() - t0 > seconds:
             break
-    return n * per, time.perf_counter() - t0
+    return kind, n * per, time.perf_counter() - t0
 
 
 def cpu_baseline(seconds=12.0, processes=1):
-    """Oracle port (reference_execute restated, single-threaded Python +
-    numpy) on a bounded sample of the same program at full width (H=256):
-    C2 at E=4 envs x T=32 steps; PPO at E=4 x T=16 with 2 epochs x 2
-    minibatches.  processes > 1 runs that many independent samples in
-    parallel host processes (the reference arm: all host cores)."""
+    """The reference's own CPU executor on a bounded sample of WL's program
+    (_ref_sample), single-threaded Python + numpy per process; processes > 1
+    runs independent samples in parallel host processes (the reference arm:
+    every host core the process may use)."""
     name = [k for k, v in WORKLOADS.items() if v is WL][0]
-    g, inputs, bounds, per = _oracle_sample()
     if processes <= 1:
-        steps, dt = _oracle_worker((name, seconds, 0))
+        kind, steps, dt = _ref_worker((name, seconds, 0))
         value = steps / dt
     else:
         import multiprocessing as mp
         with mp.get_context("spawn").Pool(processes) as pool:
-            res = pool.map(_oracle_worker, [(name, seconds, 100000 * i) for i in range(processes)])
-        steps = sum(r[0] for r in res)
-        dt = max(r[1] for r in res)
-        value = sum(r[0] / r[1] for r in res)
-    return {"value": value, "unit": "env-steps/s", "cores": processes, "kind": "port",
-            "sample": f"{steps // per} x oracle_execute({bounds}, H=256) of the {WL.name} "
-                      f"program over {processes} process(es), {dt:.1f}s each, single-threaded "
-                      f"Python+numpy per process (reference_execute restated)"}
+            res = pool.map(_ref_worker, [(name, seconds, 100000 * i) for i in range(processes)])
+        kind = res[0][0]
+        steps = sum(r[1] for r in res)
+        dt = max(r[2] for r in res)
+        value = sum(r[1] / r[2] for r in res)
+    B, T = (4, min(WL.T, 128)) if WL.ppo else (1, min(WL.T, 1000))
+    what = ("recten.runtime.reference_execute (the reference package, baseline/_ref)"
+            if kind == "reference" else "oracle/pdg_oracle.py (reference_execute restated)")
+    return {"value": value, "unit": "env-steps/s", "cores": processes, "kind": kind,
+            "sample": f"{int(steps // (B * T))} calls of {what} on the untransformed {WL.name} "
+                      f"program at E={B} x T={T} (full width, H=256), {processes} process(es) x "
+                      f"{dt:.1f}s, single-threaded Python+numpy each; host cores available "
+                      f"{_host_cores()}"}
 
 
 def run_reference(args):
@@ -241,8 +283,8 @@ def run_reference(args):
     if rank != 0:
         return
     steps_total = args.warmup + args.steps
-    procs = max(1, min(os.cpu_count() or 1, 64))
-    base = cpu_baseline(seconds=max(5.0, 2.0 * steps_total), processes=procs)
+    procs = max(1, min(_host_cores(), 64))
+    base = cpu_baseline(seconds=max(12.0, 2.0 * steps_total), processes=procs)
     line = {"impl": "reference", "metric": "env-steps/s per train iter",
             "value": base["value"], "unit": "env-steps/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,

@@ -13,9 +13,20 @@
 //                  conflict-free), then the epilogue (TMEM -> global)
 //   warp 9 lane 0  MMA issuer: hi*hi + hi*lo + lo*hi per K=8 step, commit
 //                  releases the stage back to the producer
-// Stage = A(128 x 16) + B(256 x 16) fp32, hi and lo: 48 KB; 4 stages.
+// Stage = A(128 x 16) + B(256 x 16) fp32, hi and lo: 48 KB.
 // Operands must be plain 2-D (collapsed boxes), one unit-stride dim, 16-byte
 // aligned — lower.py checks that, else RT_K_GEMM_TC (generic staging) runs.
+//
+// Accumulation bias.  The tensor core's fp32 accumulation truncates (rounds
+// toward zero) once per MMA, so a long K chain shrinks |C| systematically by
+// about 3e-8 per MMA into the same accumulator (measured, tools/tc_bias.py:
+// -2.1e-5 relative at 2 k MMAs per accumulator, -7.9e-5 at 2.6 k — the C2
+// dW2 contraction — while fp32 SIMT stays unbiased).  Launches whose K per
+// CTA exceeds TM_DRAIN_K therefore run the DRAIN variant: one CTA per SM, two
+// TMEM accumulators; every TM_DRAIN_K of K the MMA issuer switches
+// accumulator and the converter warps drain the finished one into fp32
+// registers (round-to-nearest adds), so no accumulator sees more than
+// 3 * TM_DRAIN_K / 8 = 96 MMAs (bias ~2.4e-6, as the K = 256 row GEMMs).
 #include <cuda.h>
 #include "common.cuh"
 
@@ -23,12 +34,15 @@
 #define TM_BN 256
 #define TM_BK 16
 #define TM_ST 2   // 2 stages: two CTAs per SM, one's epilogue overlaps the other's mainloop
+#define TM_ST_DRAIN 4   // drain variant: one CTA per SM, deeper ring
+#define TM_DRAIN_K 256  // K elements per TMEM accumulation chunk (drain variant)
 #define TM_CONV 256
 #define TM_THREADS (TM_CONV + 64)
 #define TM_A_BYTES (TM_BM * TM_BK * 4)
 #define TM_B_BYTES (TM_BN * TM_BK * 4)
 #define TM_STAGE (2 * TM_A_BYTES + 2 * TM_B_BYTES)
 #define TM_SMEM (TM_ST * TM_STAGE + 1024)
+#define TM_SMEM_DRAIN (TM_ST_DRAIN * TM_STAGE + 1024)
 
 struct tm_args {
   CUtensorMap ta;
@@ -109,9 +123,10 @@ RT_DEV uint64_t op_desc(uint32_t base, int ks, int mn) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constant__ tm_args a) {
+template <int ST, bool DRAIN>
+__device__ __forceinline__ void gemm_tma_body(const tm_args& a) {
   extern __shared__ unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[TM_ST], conv[TM_ST], empty[TM_ST], done;
+  __shared__ __align__(8) uint64_t full[ST], conv[ST], empty[ST], done, accfull[2], accfree[2];
   __shared__ uint32_t tmem_s;
   const rt_gemm_params& p = a.p;
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -127,18 +142,24 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
   const int nbB = a.b_mn ? BN / 32 : 1;
   const uint32_t bytesB = a.b_mn ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
 
+  constexpr uint32_t TCOLS = DRAIN ? 512 : 256;
+  constexpr int KD = TM_DRAIN_K / TM_BK;     // k-tiles per accumulation chunk (DRAIN)
   if (tid == 0) {
-    for (int i = 0; i < TM_ST; ++i) {
+    for (int i = 0; i < ST; ++i) {
       mb_init(su32(&full[i]), 1);
       mb_init(su32(&conv[i]), TM_CONV);
       mb_init(su32(&empty[i]), 1);
     }
     mb_init(su32(&done), 1);
+    for (int i = 0; i < 2; ++i) {
+      mb_init(su32(&accfull[i]), 1);
+      mb_init(su32(&accfree[i]), TM_CONV);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;"
-                 ::"r"(su32(&tmem_s)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(su32(&tmem_s)), "n"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -154,8 +175,8 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
   if (warp == 8) {
     if (lane == 0) {
       for (int kt = 0; kt < ntiles; ++kt) {
-        const int s = kt % TM_ST;
-        if (kt >= TM_ST) mb_wait(su32(&empty[s]), (uint32_t)(((kt / TM_ST) - 1) & 1));
+        const int s = kt % ST;
+        if (kt >= ST) mb_wait(su32(&empty[s]), (uint32_t)(((kt / ST) - 1) & 1));
         const uint32_t st = sbase + s * TM_STAGE;
         const uint32_t fb = su32(&full[s]);
         mb_expect(fb, TM_A_BYTES + bytesB);
@@ -178,8 +199,12 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
                              ((uint32_t)a.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TM_BM >> 4) << 24);
       for (int kt = 0; kt < ntiles; ++kt) {
-        const int s = kt % TM_ST;
-        mb_wait(su32(&conv[s]), (uint32_t)((kt / TM_ST) & 1));
+        const int s = kt % ST;
+        const int c = DRAIN ? kt / KD : 0, kc = DRAIN ? kt - c * KD : kt;
+        const uint32_t acc = tmem + (uint32_t)(256 * (c & 1));
+        if (DRAIN && kc == 0 && c >= 2)   // the converters drained this accumulator
+          mb_wait(su32(&accfree[c & 1]), (uint32_t)(((c >> 1) - 1) & 1));
+        mb_wait(su32(&conv[s]), (uint32_t)((kt / ST) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t st = sbase + s * TM_STAGE;
         const uint32_t ahi = st, alo = st + TM_A_BYTES;
@@ -188,75 +213,118 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
         for (int ks = 0; ks < TM_BK / 8; ++ks) {
           const uint64_t dah = op_desc(ahi, ks, a.a_mn), dal = op_desc(alo, ks, a.a_mn);
           const uint64_t dbh = op_desc(bhi, ks, a.b_mn), dbl = op_desc(blo, ks, a.b_mn);
-          mma_tf32(tmem, dah, dbh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
-          mma_tf32(tmem, dah, dbl, idesc, 1u);
-          mma_tf32(tmem, dal, dbh, idesc, 1u);
+          mma_tf32(acc, dah, dbh, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32(acc, dah, dbl, idesc, 1u);
+          mma_tf32(acc, dal, dbh, idesc, 1u);
         }
         mma_commit(su32(&empty[s]));
+        if (DRAIN && (kc == KD - 1 || kt == ntiles - 1)) mma_commit(su32(&accfull[c & 1]));
       }
       mma_commit(su32(&done));
     }
   } else {
     // converters: hi in place, lo into the twin buffer
+    const int wq = warp & 3, wh = warp >> 2;
+    float racc[DRAIN ? 128 : 1];     // DRAIN: this thread's row, column half wh
+#pragma unroll
+    for (int j = 0; j < (DRAIN ? 128 : 1); ++j) racc[j] = 0.f;
+#define TM_DRAIN(c_)                                                                          \
+  do {                                                                                        \
+    const int cc_ = (c_);                                                                     \
+    mb_wait(su32(&accfull[cc_ & 1]), (uint32_t)((cc_ >> 1) & 1));                             \
+    asm volatile("tcgen05.fence::after_thread_sync;");                                        \
+    const uint32_t base_ = tmem + (uint32_t)(256 * (cc_ & 1)) + ((uint32_t)(wq * 32) << 16) + \
+                           (uint32_t)(128 * wh);                                              \
+    _Pragma("unroll") for (int q = 0; q < (DRAIN ? 8 : 0); ++q) {                             \
+      uint32_t v[16];                                                                         \
+      asm volatile(                                                                           \
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), \
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),       \
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])                                             \
+          : "r"(base_ + 16u * q));                                                            \
+      asm volatile("tcgen05.wait::ld.sync.aligned;");                                         \
+      _Pragma("unroll") for (int j = 0; j < 16; ++j)                                          \
+        racc[(16 * q + j) & (DRAIN ? 127 : 0)] += __uint_as_float(v[j]);                      \
+    }                                                                                         \
+    asm volatile("tcgen05.fence::before_thread_sync;");                                       \
+    mb_arrive(su32(&accfree[cc_ & 1]));                                                       \
+  } while (0)
     for (int kt = 0; kt < ntiles; ++kt) {
-      const int s = kt % TM_ST;
-      mb_wait(su32(&full[s]), (uint32_t)((kt / TM_ST) & 1));
+      const int s = kt % ST;
+      mb_wait(su32(&full[s]), (uint32_t)((kt / ST) & 1));
       const uint32_t st = sbase + s * TM_STAGE;
       constexpr int NA = TM_A_BYTES / 16, NB = TM_B_BYTES / 16;
       constexpr int NI = (NA + NB) / TM_CONV;
       static_assert((NA + NB) % TM_CONV == 0 && NA % TM_CONV == 0, "whole conversion rounds");
       // explicit shared-space accesses (generic LD/ST.E here were tracked on
       // the long scoreboard), all of a thread's loads issued before its stores
-      float4 xs[NI];
+      // (DRAIN: two half batches — the 128 drain accumulators leave 168 - 128
+      // registers, the per-SMSP limit for 10 warps)
+      constexpr int NB_ = DRAIN ? NI / 2 : NI;
 #pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        const int i = tid + j * TM_CONV;
-        const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(xs[j].x), "=f"(xs[j].y), "=f"(xs[j].z), "=f"(xs[j].w) : "r"(st + off));
-      }
+      for (int j0 = 0; j0 < NI; j0 += NB_) {
+        float4 xs[NB_];
 #pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        const int i = tid + j * TM_CONV;
-        const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
-        const uint32_t lo_off = i < NA ? TM_A_BYTES : TM_B_BYTES;
-        const float4 x = xs[j];
-        uint4 h, l;
-        h.x = rna(x.x); h.y = rna(x.y); h.z = rna(x.z); h.w = rna(x.w);
-        l.x = rna(x.x - __uint_as_float(h.x)); l.y = rna(x.y - __uint_as_float(h.y));
-        l.z = rna(x.z - __uint_as_float(h.z)); l.w = rna(x.w - __uint_as_float(h.w));
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off), "r"(h.x), "r"(h.y), "r"(h.z), "r"(h.w));
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off + lo_off), "r"(l.x), "r"(l.y), "r"(l.z), "r"(l.w));
+        for (int jj = 0; jj < NB_; ++jj) {
+          const int i = tid + (j0 + jj) * TM_CONV;
+          const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(xs[jj].x), "=f"(xs[jj].y), "=f"(xs[jj].z), "=f"(xs[jj].w) : "r"(st + off));
+        }
+#pragma unroll
+        for (int jj = 0; jj < NB_; ++jj) {
+          const int i = tid + (j0 + jj) * TM_CONV;
+          const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
+          const uint32_t lo_off = i < NA ? TM_A_BYTES : TM_B_BYTES;
+          const float4 x = xs[jj];
+          uint4 h, l;
+          h.x = rna(x.x); h.y = rna(x.y); h.z = rna(x.z); h.w = rna(x.w);
+          l.x = rna(x.x - __uint_as_float(h.x)); l.y = rna(x.y - __uint_as_float(h.y));
+          l.z = rna(x.z - __uint_as_float(h.z)); l.w = rna(x.w - __uint_as_float(h.w));
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off), "r"(h.x), "r"(h.y), "r"(h.z), "r"(h.w));
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off + lo_off), "r"(l.x), "r"(l.y), "r"(l.z), "r"(l.w));
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mb_arrive(su32(&conv[s]));
+      // DRAIN: the previous chunk, once the first tile of this one is converted
+      if (DRAIN && kt % KD == 0 && kt > 0) TM_DRAIN(kt / KD - 1);
     }
+    if (DRAIN && ntiles > 0) TM_DRAIN((ntiles - 1) / KD);
     // epilogue: warp w reads TMEM lanes 32(w%4).. (= tile rows), column half w/4
     if (ntiles > 0) mb_wait(su32(&done), 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const int wq = warp & 3, wh = warp >> 2;
     const int r = wq * 32 + lane;
     const int64_t m = m0 + r;
-    const int half = ((BN / 2) + 15) / 16 * 16;
-    const int cbeg = wh * half, cend = wh ? BN : (half < BN ? half : BN);
+    const int half = DRAIN ? 128 : ((BN / 2) + 15) / 16 * 16;
+    const int cbeg = wh * half;
+    const int cend = DRAIN ? (cbeg + 128 < BN ? cbeg + 128 : BN) : (wh ? BN : (half < BN ? half : BN));
     float* Cp = (float*)p.C.ptr;
     const bool vec = p.splits == 1 && a.c_n == 1 && ((p.C.ptr + 4 * (p.C.off + m * a.c_m)) & 15) == 0;
-    for (int c0 = cbeg; c0 < cend; c0 += 16) {
-      uint32_t v[16];
-      const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;");
-      if (ntiles == 0)
-        for (int j = 0; j < 16; ++j) v[j] = 0u;
-      if (m >= p.m) continue;
-      float x[16];
+    // (DRAIN: the columns come from racc, so the chunk loop is unrolled
+    // with static indices; the 128-column halves start at 128 * wh)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) x[j] = __uint_as_float(v[j]);
+    for (int qq = 0; qq < (DRAIN ? 8 : 1); ++qq)
+    for (int c0 = DRAIN ? 128 * wh + 16 * qq : cbeg; c0 < (DRAIN ? (128 * wh + 16 * qq + 16 < cend ? 128 * wh + 16 * qq + 16 : cend) : cend); c0 += 16) {
+      float x[16];
+      if constexpr (DRAIN) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = racc[(16 * qq + j) & 127];
+      } else {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = ntiles == 0 ? 0.f : __uint_as_float(v[j]);
+      }
+      if (m >= p.m) continue;
       if (p.splits > 1) {
         float* part = (float*)p.part + ((int64_t)split * p.m + m) * p.n + n0;
 #pragma unroll
@@ -310,7 +378,16 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
+}
+
+__global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constant__ tm_args a) {
+  gemm_tma_body<TM_ST, false>(a);
+}
+// 10 warps, 3 on some SM sub-partition: 16 K registers / 96 threads -> 168
+__global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_constant__ tm_args a) {
+  gemm_tma_body<TM_ST_DRAIN, true>(a);
 }
 
 typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -365,8 +442,12 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
   }
   if (rc) return nullptr;
   memcpy(blk, &a, sizeof a);
-  return (void*)k_gemm_tma;
+  // K per CTA past one accumulation chunk: the draining variant (lower.py
+  // sizes its shared memory with the same rule, TMA_SMEM_DRAIN)
+  const int64_t kper = ((p.k + p.splits - 1) / p.splits + TM_BK - 1) / TM_BK * TM_BK;
+  return kper > TM_DRAIN_K ? (void*)k_gemm_tma_drain : (void*)k_gemm_tma;
 }
 
 extern "C" int rt_gemm_tma_smem() { return TM_SMEM; }
+extern "C" int rt_gemm_tma_smem_drain() { return TM_SMEM_DRAIN; }
 extern "C" int rt_gemm_tma_args_bytes() { return (int)sizeof(tm_args); }

@@ -2125,7 +2125,8 @@ class Lowering:
         tiles = ((p.m + 127) // 128) * ((p.n + 255) // 256) * p.z
         splits = 1
         if tiles < 148 and p.k >= 4096:
-            splits = int(max(1, min(148 * 2 // max(1, tiles), p.k // 2048)))
+            # long-K contractions run the draining TMA variant, one CTA per SM
+            splits = int(max(1, min(148 // max(1, tiles), p.k // 2048)))
         if p.z * splits > 65535 or (p.n + 255) // 256 > 65535:
             raise LowerError("gemm grid too large")
         p.splits = splits
@@ -2134,7 +2135,11 @@ class Lowering:
         # M tiles on grid.x (up to 2^31 - 1: E*T rows), N tiles on grid.y
         grid = [(p.m + 127) // 128, (p.n + 255) // 256, p.z * splits]
         if self.use_tma and self._tma_ok(p):
-            self.add_rec(N.RT_K_GEMM_TMA, p, grid, [320, 1, 1], N.TMA_SMEM, label)
+            # K per CTA beyond one TMEM accumulation chunk -> the draining
+            # variant (csrc/k_gemm_tma.cu, rt_gemm_tma_pack: same rule)
+            kper = (-(-p.k // splits) + 15) // 16 * 16
+            smem = N.TMA_SMEM_DRAIN if kper > N.TMA_DRAIN_K else N.TMA_SMEM
+            self.add_rec(N.RT_K_GEMM_TMA, p, grid, [320, 1, 1], smem, label)
         else:
             self.add_rec(N.RT_K_GEMM_TC, p, grid, [256, 1, 1], N.TC_SMEM, label)
         if splits > 1:

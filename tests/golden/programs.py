@@ -14,11 +14,17 @@ import sys
 
 REF_SRC = "/root/reference/pkg/src"
 REF_PROGRAMS = "/root/reference/pkg/programs"
+# the reference installed by `pip install --target baseline/_ref` (git-ignored;
+# travels to the GPU box, where /root/reference does not exist)
+REF_INSTALLED = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(
+    os.path.abspath(__file__)))), "baseline", "_ref")
 
 
 def recten():
-    if REF_SRC not in sys.path:
-        sys.path.insert(0, REF_SRC)
+    if "recten" not in sys.modules:
+        src = REF_SRC if os.path.isdir(REF_SRC) else REF_INSTALLED
+        if src not in sys.path:
+            sys.path.insert(0, src)
     import recten  # noqa: F401
     from recten import dsl, frontend, pdg, transforms, runtime, polysched
     return dsl, frontend, pdg, transforms, runtime, polysched

@@ -26,6 +26,9 @@ class Case:
         arrs = np.load(path[:-5] + ".npz")
         self.inputs = {k: arrs[f"in_{k}"] for k in doc["inputs"]}
         self.outputs = {k: arrs[f"out_{k}"] for k in doc["outputs"]}
+        # fp32 cases: the same program with float64-accumulated reductions
+        # (make_golden.alt_accumulation): the reference's own rounding noise
+        self.alt_outputs = {k: arrs[f"alt_{k}"] for k in doc.get("alt_outputs", [])}
 
     def graph(self):
         return ir.Graph.from_json(json.dumps(self.graph_doc))

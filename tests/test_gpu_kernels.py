@@ -279,3 +279,20 @@ def test_gae_fused_scan(B, T):
         acc = delta[:, t].astype(np.float64) + (0.99 * 0.95 * acc if t < T - 1 else 0.0)
         want[:, t] = acc
     np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("B", [65536, 1 << 20])
+def test_tcgen05_long_k_contraction_is_unbiased(B):
+    """Long-K tcgen05 contractions drain their TMEM accumulator every 256 K
+    into round-to-nearest fp32 registers (k_gemm_tma_drain): positive
+    operands (no cancellation to hide it) show no systematic shrink.  Before
+    the drain: -2.1e-5 (K=65536) and -7.9e-5 (K=2^20, the C2 dW2 shape)."""
+    K, Nn = 256, 256
+    rng = np.random.default_rng(B)
+    x = rng.random((B, 1, K)).astype(np.float32)
+    gr = rng.random((B, 1, Nn)).astype(np.float32)
+    out = execute(mm_graph(B, K, Nn, contract=True), inputs={"x": x, "gr": gr})["s"]
+    want = np.einsum("bk,bn->kn", x[:, 0].astype(np.float64), gr[:, 0].astype(np.float64))
+    rel = (out.astype(np.float64) - want) / want
+    assert abs(rel.mean()) < 4e-6, rel.mean()
+    assert np.abs(rel).max() < 1e-5, np.abs(rel).max()
