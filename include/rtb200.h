@@ -21,7 +21,12 @@
  *                     pinned cudaMemcpyAsync on a side stream)
  *   rt_rng_fill       runtime.py:50-55, 391-394 per-point
  *                     default_rng((seed, tag, *point)) draws, bit-exact
- *   rt_scan_ref       runtime.py:133-146 discounted_cumsum (standalone)
+ *   rt_pool_*, rt_offload, rt_fetch, rt_block_update, rt_stack
+ *                     SPEC.md:541-561 the runtime's Backend (allocate,
+ *                     deallocate, move-between-tiers, dynamic-update, stack)
+ *                     and MemorySim (device/host live+peak, transfer
+ *                     counters, overflow = hard error) — specified by the
+ *                     reference, implemented nowhere in it
  */
 #ifndef RTB200_H
 #define RTB200_H
@@ -75,8 +80,9 @@ enum rt_status_code {
   RT_ERR_CUDA = 3,
   RT_ERR_BAD_ARG = 4,
   RT_ERR_UNKNOWN_KERNEL = 5,
-  RT_ERR_DIV_ZERO = 6       /* index expression // or % by zero (symexpr.py:491-506);
+  RT_ERR_DIV_ZERO = 6,      /* index expression // or % by zero (symexpr.py:491-506);
                                aux = (dividend, 0 for //, 1 for %) */
+  RT_ERR_OVERFLOW = 7       /* device tier over capacity (SPEC.md:554-557 MemorySim) */
 };
 
 /* A flat index over a box, decomposed row-major. */
@@ -424,6 +430,32 @@ int rt_rng_fill(uint64_t dev_out, const uint32_t* prefix, int32_t nprefix,
                 const int64_t* coords, int32_t ncoord, int64_t rows, int32_t count,
                 int32_t dist, uint64_t stream);
 const char* rt_last_error(void);
+/* ---- Backend + MemorySim ----------
+ * A stream-ordered device pool with the MemorySim's accounting:
+ * stats8 = {capacity, live, peak, host_live, host_peak, offloads, fetches,
+ * bytes_moved}; capacity 0 = unbounded; rt_pool_alloc past capacity fails
+ * with RT_ERR_OVERFLOW. */
+int rt_pool_create(int32_t device, uint64_t capacity, uint64_t* pool_out);
+int rt_pool_destroy(uint64_t pool);
+int rt_pool_alloc(uint64_t pool, uint64_t bytes, uint64_t stream, uint64_t* dev_out);
+int rt_pool_free(uint64_t pool, uint64_t dev, uint64_t stream);
+int rt_pool_host(uint64_t pool, int64_t delta_bytes);    /* host tier live += delta */
+int rt_pool_stats(uint64_t pool, uint64_t* stats8);
+/* move-between-tiers: `height` rows of `width` bytes (height 1: one span) on
+ * `stream` after `after_event` (0: none), recording `done_event` (0: none);
+ * events are caller-owned cudaEvent_t handles. */
+int rt_offload(uint64_t pool, void* host_pinned, uint64_t hpitch, uint64_t dev, uint64_t dpitch,
+               uint64_t width, uint64_t height, uint64_t stream, uint64_t after_event,
+               uint64_t done_event);
+int rt_fetch(uint64_t pool, uint64_t dev, uint64_t dpitch, const void* host_pinned, uint64_t hpitch,
+             uint64_t width, uint64_t height, uint64_t stream, uint64_t after_event,
+             uint64_t done_event);
+/* dynamic-update: block[slot * elem_bytes ..] = src[0 .. elem_bytes) */
+int rt_block_update(uint64_t block, int64_t slot, uint64_t src, uint64_t elem_bytes,
+                    uint64_t stream);
+/* stack: dst[i * elem_bytes ..] = srcs[i][0 .. elem_bytes), i < n */
+int rt_stack(uint64_t dst, const uint64_t* srcs, int32_t n, uint64_t elem_bytes, uint64_t stream);
+int rt_set_error(int code, const char* what);
 #endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus

@@ -1193,7 +1193,19 @@ RT_DEV void sts_cols(uint32_t a, const float (&x)[NC]) {
 // each (part p keeps rows [4p, 4p+4) in acc[j][0..3]) so the epilogue
 // (bias, tanh, stores) runs on all eight warps.  KRP = 0: no register rows
 // (a shared-memory resident layer such as W1 through the same core).
-template <int MRP, int K, int N, int NCOL, int KRP, bool SPLIT = false>
+// NR < MRP: only rows [0, NR) are computed (the CTA's real rows; the FMA
+// pipe time of a step scales with NR, the padding to MRP only feeds the
+// 16-byte row loads).
+template <int MRP, int NR>
+RT_DEV void fma_rows_n(float (&acc)[MRP], const float (&a)[MRP], float b) {
+#pragma unroll
+  for (int r = 0; r < NR; r += 2) {
+    if (r + 1 < NR) fma2(acc[r], acc[r + 1], a[r], a[r + 1], b);
+    else acc[r] = fmaf(a[r], b, acc[r]);
+  }
+}
+
+template <int MRP, int K, int N, int NCOL, int KRP, bool SPLIT = false, int NR = MRP>
 RT_DEV void hyb_core(const float (&w)[NCOL][KRP > 0 ? KRP : 1], uint32_t sB, uint32_t sA, uint32_t red,
                      float (&acc)[NCOL][MRP]) {
   constexpr int P = NCOL, HT = N / NCOL, KP = K / P, KS = KP - KRP;
@@ -1206,7 +1218,7 @@ RT_DEV void hyb_core(const float (&w)[NCOL][KRP > 0 ? KRP : 1], uint32_t sB, uin
     float a[MRP];
     lds_rows<MRP>(a0 + (uint32_t)(kk * MRP * 4), a);
 #pragma unroll
-    for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a, w[j][kk]);
+    for (int j = 0; j < NCOL; ++j) fma_rows_n<MRP, NR>(acc[j], a, w[j][kk]);
   }
   const uint32_t bn = sB + (uint32_t)((part * KS * N + c0) * 4);
 #pragma unroll 4
@@ -1215,7 +1227,7 @@ RT_DEV void hyb_core(const float (&w)[NCOL][KRP > 0 ? KRP : 1], uint32_t sB, uin
     lds_rows<MRP>(a0 + (uint32_t)((KRP + kk) * MRP * 4), a);
     lds_cols<NCOL>(bn + (uint32_t)(kk * N * 4), b);
 #pragma unroll
-    for (int j = 0; j < NCOL; ++j) fma_rows<MRP>(acc[j], a, b[j]);
+    for (int j = 0; j < NCOL; ++j) fma_rows_n<MRP, NR>(acc[j], a, b[j]);
   }
   if constexpr (SPLIT) {
     static_assert(P == 2 && MRP == 8, "row-split finalisation: two parts, 8 rows");

@@ -73,6 +73,9 @@ static int fail(int code, const char* what) {
   return code;
 }
 
+// for the other translation units of the library (backend.cu)
+extern "C" int rt_set_error(int code, const char* what) { return fail(code, what); }
+
 static int cuda_check(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return RT_OK;
   char buf[512];

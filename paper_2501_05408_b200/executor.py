@@ -1522,8 +1522,8 @@ _KNOB_NAMES = None
 def _knobs():
     """Module-level lowering switches (tests flip them): part of the key."""
     global _KNOB_NAMES
-    from . import jit
-    mods = (jit, sys.modules[__name__])
+    from . import jit, jit_mlp
+    mods = (jit, jit_mlp, sys.modules[__name__])
     if _KNOB_NAMES is None:
         _KNOB_NAMES = [[k for k, v in vars(m).items()
                         if k.isupper() and isinstance(v, (bool, int, float, str))] for m in mods]

@@ -1348,8 +1348,21 @@ def specialise(recs, kernels, params, labels, loop_info=None):
     if not ENABLED:
         return 0
     n = 0
+    from . import jit_mlp
     for ri, info in (loop_info or {}).items():
         if params[ri].rows * info["trips"] < JIT_LOOP_MIN:
+            continue
+        m = None if (info.get("pair") or MMA_ENABLED or KS_ENABLED) else \
+            jit_mlp.match(params[ri], info["ops"], info)
+        sm = jit_mlp.smem_bytes(params[ri], m) if m is not None else 0
+        if m is not None and sm <= 227 * 1024:
+            # the six-op MLP acting step: one fused 512-thread kernel (loop_mlp.cuh)
+            src = jit_mlp.source(params[ri], info["ops"], info, m)
+            recs[ri].jit_fn = compile_kernel(src, "loop_mlp")
+            recs[ri].block[0] = jit_mlp.THREADS
+            recs[ri].smem = sm
+            info["mlp"] = dict(m, smem=sm)
+            n += 1
             continue
         src = loop_source(params[ri], info["ops"], "loop_jit", info)
         recs[ri].jit_fn = compile_kernel(src, "loop_jit")

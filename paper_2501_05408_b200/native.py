@@ -39,6 +39,7 @@ RT_HOOK = 100
 
 RT_ERR_ROW_RANGE, RT_ERR_SLICE_RANGE = 1, 2
 RT_ERR_DIV_ZERO = 6
+RT_ERR_OVERFLOW = 7
 
 i32, i64, u64, u32, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_uint32, C.c_double
 
@@ -195,6 +196,17 @@ def lib():
     L.rt_memcpy_h2d_async.argtypes = [u64, C.c_void_p, u64, u64]
     L.rt_memcpy2d_d2h_async.argtypes = [C.c_void_p, u64, u64, u64, u64, u64, u64]
     L.rt_memcpy2d_h2d_async.argtypes = [u64, u64, C.c_void_p, u64, u64, u64, u64]
+    L.rt_pool_create.argtypes = [i32, u64, C.POINTER(u64)]
+    L.rt_pool_destroy.argtypes = [u64]
+    L.rt_pool_alloc.argtypes = [u64, u64, u64, C.POINTER(u64)]
+    L.rt_pool_free.argtypes = [u64, u64, u64]
+    L.rt_pool_host.argtypes = [u64, i64]
+    L.rt_pool_stats.argtypes = [u64, C.POINTER(u64)]
+    L.rt_offload.argtypes = [u64, C.c_void_p, u64, u64, u64, u64, u64, u64, u64, u64]
+    L.rt_fetch.argtypes = [u64, u64, u64, C.c_void_p, u64, u64, u64, u64, u64, u64]
+    L.rt_block_update.argtypes = [u64, i64, u64, u64, u64]
+    L.rt_stack.argtypes = [u64, C.POINTER(u64), i32, u64, u64]
+    L.rt_set_error.argtypes = [i32, C.c_char_p]
     if L.rt_version() != 1:
         raise NativeError("librtb200 ABI version mismatch")
     _lib = L
@@ -206,7 +218,9 @@ EXPORTS = ("rt_version", "rt_launch", "rt_run", "rt_status_alloc", "rt_status_re
            "rt_rng_fill", "rt_last_error", "rt_graph_capture", "rt_graph_launch",
            "rt_graph_destroy", "rt_profile", "rt_graph_capture_ev", "rt_run_segment",
            "rt_jit_compile", "rt_jit_load", "rt_jit_cubin", "rt_memcpy2d_d2h_async",
-           "rt_memcpy2d_h2d_async")
+           "rt_memcpy2d_h2d_async", "rt_pool_create", "rt_pool_destroy", "rt_pool_alloc",
+           "rt_pool_free", "rt_pool_host", "rt_pool_stats", "rt_offload", "rt_fetch",
+           "rt_block_update", "rt_stack", "rt_set_error")
 
 
 def check(rc: int, what: str = ""):

@@ -155,13 +155,20 @@ class SwapRuntime:
             self.geo.append((b.ptr, h.data_ptr(), rows, plan.bs * row, 2 * plan.bs * row,
                              T * row))
         self.host_bytes = sum(h.numel() for h in self.host)
+        # tier moves through the SPEC Backend (backend.py, csrc/backend.cu):
+        # ordered by events, counted by its MemorySim
+        from .backend import Backend
+        dev = exe.dev
+        self.backend = Backend(dev if isinstance(dev, int) else (dev.index or 0))
+        self.backend.host_tier(self.host_bytes)
 
-    def _issue_in(self, k):
-        for dev, host, rows, width, dpitch, hpitch in self.geo:
-            N.check(self.lib.rt_memcpy2d_h2d_async(dev + (k % 2) * width, dpitch,
-                                                    C.c_void_p(host + k * width), hpitch, width,
-                                                    rows, self.side.cuda_stream), "fetch")
-        self.ev_in[k % 2].record(self.side)
+    def _issue_in(self, k, after=None):
+        ev = self.ev_in[k % 2]
+        for i, (dev, host, rows, width, dpitch, hpitch) in enumerate(self.geo):
+            self.backend.fetch(dev + (k % 2) * width, host + k * width, width, rows, dpitch=dpitch,
+                               hpitch=hpitch, stream=self.side.cuda_stream,
+                               after_event=after.cuda_event if (after is not None and i == 0) else 0)
+        ev.record(self.side)
 
     def hook(self, kind, kb, stream):
         torch = self.torch
@@ -170,25 +177,22 @@ class SwapRuntime:
                 stream.wait_event(self.ev_out[kb % 2])
         elif kind == "swap_out":
             ev = torch.cuda.Event()
-            ev.record(stream)
-            self.side.wait_event(ev)
-            for dev, host, rows, width, dpitch, hpitch in self.geo:
-                N.check(self.lib.rt_memcpy2d_d2h_async(C.c_void_p(host + kb * width), hpitch,
-                                                        dev + (kb % 2) * width, dpitch, width,
-                                                        rows, self.side.cuda_stream), "offload")
+            ev.record(stream)          # the block's producer is done with it
+            for i, (dev, host, rows, width, dpitch, hpitch) in enumerate(self.geo):
+                self.backend.offload(host + kb * width, dev + (kb % 2) * width, width, rows,
+                                     hpitch=hpitch, dpitch=dpitch, stream=self.side.cuda_stream,
+                                     after_event=ev.cuda_event if i == 0 else 0)
             self.ev_out[kb % 2].record(self.side)
         elif kind == "swap_in":
             if kb == 0:
                 ev = torch.cuda.Event()
                 ev.record(stream)
-                self.side.wait_event(ev)
-                self._issue_in(0)
+                self._issue_in(0, after=ev)
             stream.wait_event(self.ev_in[kb % 2])
             if kb + 1 < self.plan.DI:
                 ev = torch.cuda.Event()
                 ev.record(stream)      # block kb-1 is done with the other slot
-                self.side.wait_event(ev)
-                self._issue_in(kb + 1)
+                self._issue_in(kb + 1, after=ev)
         else:
             raise ValueError(kind)
 

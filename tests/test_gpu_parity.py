@@ -230,16 +230,22 @@ def test_trace_and_stats_report():
     assert rep["static_estimate"]["G"] == 1 * 4 * 6 * 4
 
 
-def test_default_loop_at_8_rows_matches_interpreter(monkeypatch):
-    """Default in-loop path at 8-row CTAs (E=1024): 2-columns-per-thread core
-    and shared-memory forwarding of h1 -> h2 -> mu (jit._forward_pairs)."""
+@pytest.mark.parametrize("fused", [True, False])
+def test_default_loop_at_8_rows_matches_interpreter(monkeypatch, fused):
+    """JIT acting loop at 7-row CTAs (E=1024) against the interpreting loop
+    kernel: the fused 512-thread MLP step (jit_mlp.py, loop_mlp.cuh; the
+    default) and the op-by-op JIT loop (2-columns-per-thread core,
+    shared-memory forwarding h1 -> h2 -> mu, jit._forward_pairs)."""
     from golden_cases import load_graph
-    from paper_2501_05408_b200 import execute, jit
+    from paper_2501_05408_b200 import execute, get_executable, jit, jit_mlp
     from paper_2501_05408_b200.workloads import mlp_inputs
     bounds = {"I": 1, "B": 1024, "T": 12}
     monkeypatch.setattr(jit, "JIT_LOOP_MIN", 1 << 40)
     ref = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=5)
     monkeypatch.setattr(jit, "JIT_LOOP_MIN", 0)
+    monkeypatch.setattr(jit_mlp, "ENABLED", fused)
+    exe, _ = get_executable(load_graph("reinforce_mlp_c2"), bounds, mlp_inputs(), 5)
+    assert any("mlp" in info for info in exe.loop_info.values()) == fused
     got = execute(load_graph("reinforce_mlp_c2"), bounds=bounds, inputs=mlp_inputs(), seed=5)
     for k in ref:
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)

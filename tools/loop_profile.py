@@ -44,7 +44,20 @@ for ri, info in exe.loop_info.items():
         from paper_2501_05408_b200 import jit as J
         os.makedirs("gpurun_out", exist_ok=True)
         with open(f"gpurun_out/loop_src_{ri}.cu", "w") as fh:
-            fh.write(J.loop_source(params, info["ops"], "loop_jit", info))
+            if info.get("mlp"):
+                from paper_2501_05408_b200 import jit_mlp as JM
+                fh.write(JM.source(params, info["ops"], info, info["mlp"]))
+            else:
+                fh.write(J.loop_source(params, info["ops"], "loop_jit", info))
+    if info.get("mlp"):
+        # fused MLP step (jit_mlp.py): phase probes 0..3, h2 core alone in 6
+        names = ["obs (op 0)", "h1 (op 1)", "h2 (op 2: core + epilogue)", "tail (ops 3-5: head, action, env)"]
+        for nm, c in zip(names, cyc[:4]):
+            print(f"  {nm:40s} cycles/step={c / info['trips']:8.0f} share={100 * c / max(1, tot):5.1f}%")
+        print(f"  {'  of which h2 core (hyb_core)':40s} cycles/step={cyc[6] / info['trips']:8.0f}")
+        print(f"  total cycles/step {sum(cyc[:4]) / info['trips']:.0f}")
+        params.prof = 0
+        continue
     for (k, q, re, f64, noise, *_), c in zip(info["ops"], cyc):
         print(f"  {RF.FAMILY.get(k):6s} row_elems={re:5d} cycles/step={c / info['trips']:10.0f} "
               f"share={100 * c / max(1, tot):5.1f}%")
