@@ -51,6 +51,10 @@ struct tm_args {
   int32_t a_mn, b_mn;      // operand is MN-major (unit stride along M / N)
   int64_t c_m, c_n;        // collapsed C strides
   int64_t bias_n;          // collapsed bias stride along N
+  int64_t g_m, g_n;        // epilogue 2: the gate operand's strides (in p.bias)
+  CUtensorMap tbh, tbl;    // PRESPLIT: B's tf32 hi / lo parts (same geometry as tb)
+  uint64_t b_base, b_span; // PRESPLIT: B element base address and span (elements)
+  int32_t presplit, _pad2;
 };
 
 namespace {
@@ -308,6 +312,22 @@ __device__ __forceinline__ void gemm_tma_body(const tm_args& a) {
     for (int qq = 0; qq < (DRAIN ? 8 : 1); ++qq)
     for (int c0 = DRAIN ? 128 * wh + 16 * qq : cbeg; c0 < (DRAIN ? (128 * wh + 16 * qq + 16 < cend ? 128 * wh + 16 * qq + 16 : cend) : cend); c0 += 16) {
       float x[16];
+      // epilogue 2: this row's 16 gate values, issued before the TMEM read
+      // (four 16-byte loads when contiguous and aligned)
+      float gv[16];
+      if (!DRAIN && p.epilogue == 2 && m < p.m) {   // (the gate runs only with K <= 256)
+        const float* gp = (const float*)p.bias.ptr + p.bias.off + m * a.g_m + (n0 + c0) * a.g_n;
+        if (a.g_n == 1 && n0 + c0 + 16 <= p.n && (reinterpret_cast<uintptr_t>(gp) & 15) == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 g4 = __ldcs(reinterpret_cast<const float4*>(gp) + q);
+            gv[4 * q] = g4.x; gv[4 * q + 1] = g4.y; gv[4 * q + 2] = g4.z; gv[4 * q + 3] = g4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) gv[j] = n0 + c0 + j < p.n ? gp[j * a.g_n] : 0.f;
+        }
+      }
       if constexpr (DRAIN) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) x[j] = racc[(16 * qq + j) & 127];
@@ -337,7 +357,12 @@ __device__ __forceinline__ void gemm_tma_body(const tm_args& a) {
       // four 16-byte loads when contiguous fp32, not a dtype-dispatched load
       // per element (the bias+tanh forward GEMM ran ~30% slower than dX)
       float bv[16];
-      if (p.bias.ptr) {
+      if (!DRAIN && p.epilogue == 2) {
+        // tanh-VJP gate (frontend.py:961-963): x * (1 - h*h), h laid out like
+        // C; each op rounded like numpy's (no contraction into an FMA)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) bv[j] = __fsub_rn(1.f, __fmul_rn(gv[j], gv[j]));
+      } else if (p.bias.ptr) {
         const int64_t b0 = p.bias.off + (n0 + c0) * a.bias_n;
         const float* bp = (const float*)p.bias.ptr + b0;
         if (a.bias_n == 1 && p.bias.dtype == RT_F32 && n0 + c0 + 16 <= p.n &&
@@ -359,6 +384,10 @@ __device__ __forceinline__ void gemm_tma_body(const tm_args& a) {
         const int64_t n = n0 + c0 + j;
         if (n >= p.n) break;
         if (p.accumulate) x[j] += Cp[rowoff + n * a.c_n];
+        if (!DRAIN && p.epilogue == 2) {
+          x[j] = __fmul_rn(x[j], bv[j]);
+          continue;
+        }
         if (p.bias.ptr) x[j] += bv[j];
         if (p.epilogue == 1) x[j] = tanh_fast(x[j]);
       }
@@ -388,6 +417,303 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_gemm_tma(const __grid_constan
 // 10 warps, 3 on some SM sub-partition: 16 K registers / 96 threads -> 168
 __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_constant__ tm_args a) {
   gemm_tma_body<TM_ST_DRAIN, true>(a);
+}
+
+
+// ---------------------------------------------------------------- persistent
+// Warp-specialised persistent variant for launches with one K chunk (K <=
+// TM_DRAIN_K, no split): one CTA per SM loops over the output tiles; TMEM
+// holds two 256-column accumulators so four epilogue warps drain tile i
+// (TMEM -> gate/bias/tanh -> HBM) while the MMA issuer fills tile i+1; the
+// operand ring has 4 stages.  PRESPLIT: B (a weight matrix every M tile
+// reads) was split into tf32 hi / lo arrays once by k_tf32_split for the
+// launch; TMA loads them straight into the stage's hi / lo slots and the
+// converters only split A (the converters' shared-memory traffic bounded
+// the per-tile variant: ncu tensor pipe 29%, smem 31%, long-scoreboard
+// stalls on per-tile prologues).
+#define TP_ST 4
+#define TP_CONV 128  // converter threads (warps 0-3; PRESPLIT leaves them only A)
+#define TP_EPI 8     // epilogue warps 6-13: two per TMEM lane quarter (column halves)
+#define TP_THREADS (TP_CONV + 64 + 32 * TP_EPI)
+#define TP_SMEM (TP_ST * TM_STAGE + 1024)
+
+template <bool PRESPLIT>
+__device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[TP_ST], conv[TP_ST], empty[TP_ST], accfull[2], accfree[2];
+  __shared__ uint32_t tmem_s;
+  const rt_gemm_params& p = a.p;
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = su32(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t mt = (p.m + TM_BM - 1) / TM_BM, nt = (p.n + TM_BN - 1) / TM_BN;
+  const int64_t ntile = mt * nt;
+  const int ktiles = (int)((p.k + TM_BK - 1) / TM_BK);
+  if (tid == 0) {
+    for (int i = 0; i < TP_ST; ++i) {
+      mb_init(su32(&full[i]), 1);
+      mb_init(su32(&conv[i]), TP_CONV);
+      mb_init(su32(&empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mb_init(su32(&accfull[i]), 1);
+      mb_init(su32(&accfree[i]), 32 * TP_EPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 ::"r"(su32(&tmem_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_s;
+  auto tile_bn = [&](int64_t ni) {
+    const int64_t nrem = p.n - ni * TM_BN;
+    return nrem >= TM_BN ? TM_BN
+           : a.b_mn ? (int)((nrem + 31) / 32 * 32) : (int)((nrem + 15) / 16 * 16);
+  };
+
+  if (warp == TP_CONV / 32) {                    // TMA producer
+    if (lane == 0) {
+      int64_t g = 0;
+      for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int64_t mi = tile % mt, ni = tile / mt;
+        const int64_t m0 = mi * TM_BM, n0 = ni * TM_BN;
+        const int BN = tile_bn(ni);
+        const int nbB = a.b_mn ? BN / 32 : 1;
+        const uint32_t bytesB = a.b_mn ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
+        for (int kt = 0; kt < ktiles; ++kt, ++g) {
+          const int s = (int)(g % TP_ST);
+          if (g >= TP_ST) mb_wait(su32(&empty[s]), (uint32_t)(((g / TP_ST) - 1) & 1));
+          const uint32_t st = sbase + s * TM_STAGE;
+          const uint32_t fb = su32(&full[s]);
+          mb_expect(fb, TM_A_BYTES + (PRESPLIT ? 2 : 1) * bytesB);
+          const int32_t k0 = kt * TM_BK;
+          if (a.a_mn)
+            for (int j = 0; j < TM_BM / 32; ++j) tma2d(st + j * 2048, &a.ta, (int32_t)(m0 + 32 * j), k0, fb);
+          else
+            tma2d(st, &a.ta, k0, (int32_t)m0, fb);
+          const uint32_t sb = st + 2 * TM_A_BYTES;
+#pragma unroll
+          for (int part = 0; part < (PRESPLIT ? 2 : 1); ++part) {
+            const CUtensorMap* mb = PRESPLIT ? (part ? &a.tbl : &a.tbh) : &a.tb;
+            const uint32_t dst = sb + part * TM_B_BYTES;
+            if (a.b_mn)
+              for (int j = 0; j < nbB; ++j) tma2d(dst + j * 2048, mb, (int32_t)(n0 + 32 * j), k0, fb);
+            else
+              tma2d(dst, mb, k0, (int32_t)n0, fb);
+          }
+        }
+      }
+    }
+  } else if (warp == TP_CONV / 32 + 1) {         // MMA issuer
+    if (lane == 0) {
+      int64_t g = 0;
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x, ++it) {
+        const int BN = tile_bn(tile / mt);
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a.a_mn << 15) |
+                               ((uint32_t)a.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(TM_BM >> 4) << 24);
+        const int b = it & 1;
+        const uint32_t acc = tmem + (uint32_t)(256 * b);
+        if (it >= 2) mb_wait(su32(&accfree[b]), (uint32_t)(((it >> 1) - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int kt = 0; kt < ktiles; ++kt, ++g) {
+          const int s = (int)(g % TP_ST);
+          mb_wait(su32(&conv[s]), (uint32_t)((g / TP_ST) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t st = sbase + s * TM_STAGE;
+          const uint32_t ahi = st, alo = st + TM_A_BYTES;
+          const uint32_t bhi = st + 2 * TM_A_BYTES, blo = bhi + TM_B_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < TM_BK / 8; ++ks) {
+            const uint64_t dah = op_desc(ahi, ks, a.a_mn), dal = op_desc(alo, ks, a.a_mn);
+            const uint64_t dbh = op_desc(bhi, ks, a.b_mn), dbl = op_desc(blo, ks, a.b_mn);
+            mma_tf32(acc, dah, dbh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(acc, dah, dbl, idesc, 1u);
+            mma_tf32(acc, dal, dbh, idesc, 1u);
+          }
+          mma_commit(su32(&empty[s]));
+        }
+        mma_commit(su32(&accfull[b]));
+      }
+    }
+  } else if (warp < TP_CONV / 32) {              // converters: hi in place, lo into the twin
+    int64_t g = 0;
+    constexpr int NA = TM_A_BYTES / 16, NB = PRESPLIT ? 0 : TM_B_BYTES / 16;
+    constexpr int NI = (NA + NB) / TP_CONV;
+    static_assert((NA + NB) % TP_CONV == 0, "whole conversion rounds");
+    for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+      for (int kt = 0; kt < ktiles; ++kt, ++g) {
+        const int s = (int)(g % TP_ST);
+        mb_wait(su32(&full[s]), (uint32_t)((g / TP_ST) & 1));
+        const uint32_t st = sbase + s * TM_STAGE;
+        float4 xs[NI];
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const int i = tid + j * TP_CONV;
+          const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(xs[j].x), "=f"(xs[j].y), "=f"(xs[j].z), "=f"(xs[j].w) : "r"(st + off));
+        }
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const int i = tid + j * TP_CONV;
+          const uint32_t off = i < NA ? i * 16 : 2 * TM_A_BYTES + (i - NA) * 16;
+          const uint32_t lo_off = i < NA ? TM_A_BYTES : TM_B_BYTES;
+          const float4 x = xs[j];
+          uint4 h, l;
+          h.x = rna(x.x); h.y = rna(x.y); h.z = rna(x.z); h.w = rna(x.w);
+          l.x = rna(x.x - __uint_as_float(h.x)); l.y = rna(x.y - __uint_as_float(h.y));
+          l.z = rna(x.z - __uint_as_float(h.z)); l.w = rna(x.w - __uint_as_float(h.w));
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off), "r"(h.x), "r"(h.y), "r"(h.z), "r"(h.w));
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(st + off + lo_off), "r"(l.x), "r"(l.y), "r"(l.z), "r"(l.w));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mb_arrive(su32(&conv[s]));
+      }
+    }
+  } else {                                       // epilogue warps
+    const int wq = warp & 3;                     // TMEM lane quarter of this warp
+    const int half = (warp - TP_CONV / 32 - 2) >> 2;   // column half of the tile
+    const int r = wq * 32 + lane;
+    float* Cp = (float*)p.C.ptr;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x, ++it) {
+      const int64_t mi = tile % mt, ni = tile / mt;
+      const int64_t m0 = mi * TM_BM, n0 = ni * TM_BN;
+      const int BN = tile_bn(ni);
+      const int hw = ((BN / 2) + 15) / 16 * 16;  // columns of half 0
+      const int cbeg = half * hw, cend = half ? BN : (hw < BN ? hw : BN);
+      const int b = it & 1;
+      const int64_t m = m0 + r;
+      const bool live = m < p.m;
+      const bool gate = p.epilogue == 2 && live;
+      const float* gbase = (const float*)p.bias.ptr + p.bias.off + m * a.g_m + n0 * a.g_n;
+      const bool gvec = a.g_n == 1 && ((reinterpret_cast<uintptr_t>(gbase) & 15) == 0);
+      // this row's gate values one chunk ahead (the HBM latency of chunk c+1
+      // overlaps chunk c; before the first, it overlaps the accumulator wait)
+      float gn[16];
+      auto load_gate = [&](int c0, float (&gv)[16]) {
+        if (!gate || c0 >= cend) return;
+        const float* gp = gbase + c0 * a.g_n;
+        if (gvec && n0 + c0 + 16 <= p.n) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 g4 = __ldcs(reinterpret_cast<const float4*>(gp) + q);
+            gv[4 * q] = g4.x; gv[4 * q + 1] = g4.y; gv[4 * q + 2] = g4.z; gv[4 * q + 3] = g4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) gv[j] = n0 + c0 + j < p.n ? gp[j * a.g_n] : 0.f;
+        }
+      };
+      // two chunks ahead: 2 x 64 B of HBM reads in flight per thread
+      float gn2[16];
+      load_gate(cbeg, gn);
+      load_gate(cbeg + 16, gn2);
+      mb_wait(su32(&accfull[b]), (uint32_t)((it >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const bool vec = a.c_n == 1 && ((p.C.ptr + 4 * (p.C.off + m * a.c_m)) & 15) == 0;
+      const int64_t rowoff = p.C.off + m * a.c_m;
+      for (int c0 = cbeg; c0 < cend; c0 += 16) {
+        float gv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { gv[j] = gn[j]; gn[j] = gn2[j]; }
+        load_gate(c0 + 32, gn2);
+        uint32_t v[16];
+        const uint32_t taddr = tmem + (uint32_t)(256 * b) + ((uint32_t)(wq * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (c0 + 16 >= cend) {     // this warp's reads of the accumulator are done
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mb_arrive(su32(&accfree[b]));
+        }
+        if (!live) continue;
+        float x[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = ktiles == 0 ? 0.f : __uint_as_float(v[j]);
+        if (p.epilogue == 2) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = __fmul_rn(x[j], __fsub_rn(1.f, __fmul_rn(gv[j], gv[j])));
+        } else {
+          float bv[16];
+          if (p.bias.ptr) {
+            const int64_t b0 = p.bias.off + (n0 + c0) * a.bias_n;
+            const float* bp = (const float*)p.bias.ptr + b0;
+            if (a.bias_n == 1 && p.bias.dtype == RT_F32 && n0 + c0 + 16 <= p.n &&
+                (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(bp) + q);
+                bv[4 * q] = b4.x; bv[4 * q + 1] = b4.y; bv[4 * q + 2] = b4.z; bv[4 * q + 3] = b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                bv[j] = n0 + c0 + j < p.n
+                            ? load_as<float>((const void*)p.bias.ptr, p.bias.dtype, b0 + j * a.bias_n) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int64_t n = n0 + c0 + j;
+            if (n >= p.n) break;
+            if (p.accumulate) x[j] += Cp[rowoff + n * a.c_n];
+            if (p.bias.ptr) x[j] += bv[j];
+            if (p.epilogue == 1) x[j] = tanh_fast(x[j]);
+          }
+        }
+        if (vec && n0 + c0 + 16 <= p.n) {
+          float4* dst = (float4*)(Cp + rowoff + n0 + c0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcs(dst + j, make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+        } else {
+          for (int j = 0; j < 16; ++j) {
+            const int64_t n = n0 + c0 + j;
+            if (n >= p.n) break;
+            Cp[rowoff + n * a.c_n] = x[j];
+          }
+        }
+      }
+      if (cbeg >= cend) {          // (a half with no columns still frees its share)
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mb_arrive(su32(&accfree[b]));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+__global__ void __launch_bounds__(TP_THREADS, 1) k_gemm_tmap(const __grid_constant__ tm_args a) {
+  gemm_tmap_body<false>(a);
+}
+__global__ void __launch_bounds__(TP_THREADS, 1) k_gemm_tmap_split(const __grid_constant__ tm_args a) {
+  gemm_tmap_body<true>(a);
+}
+
+// B -> tf32 hi / lo arrays over its whole element span (same offsets)
+__global__ void k_tf32_split(const float* __restrict__ x, float* __restrict__ hi,
+                             float* __restrict__ lo, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    const uint32_t h = rna(v);
+    hi[i] = __uint_as_float(h);
+    lo[i] = __uint_as_float(rna(v - __uint_as_float(h)));
+  }
 }
 
 typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -423,6 +749,8 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
   a.c_m = p.C.s1[0];
   a.c_n = p.C.s2[0];
   a.bias_n = p.bias.s2[0];
+  a.g_m = p.bias.s1[0];
+  a.g_n = p.bias.s2[0];
   const uint64_t abase = p.A.ptr + 4 * (uint64_t)p.A.off, bbase = p.B.ptr + 4 * (uint64_t)p.B.off;
   int rc;
   if (a_k == 1 || p.k == 1) {
@@ -445,9 +773,46 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
   // K per CTA past one accumulation chunk: the draining variant (lower.py
   // sizes its shared memory with the same rule, TMA_SMEM_DRAIN)
   const int64_t kper = ((p.k + p.splits - 1) / p.splits + TM_BK - 1) / TM_BK * TM_BK;
-  return kper > TM_DRAIN_K ? (void*)k_gemm_tma_drain : (void*)k_gemm_tma;
+  if (kper > TM_DRAIN_K && p.epilogue == 2) return nullptr;   // no gate in the drain variant
+  if (kper > TM_DRAIN_K) return (void*)k_gemm_tma_drain;
+  if (p.splits != 1 || !p.part) return (void*)k_gemm_tma;      // per-tile variant
+  // persistent (lower.py launches TP_THREADS x min(tiles, SMs) when it set
+  // `part`: the hi/lo scratch of B, 2 x span floats, or ~0 for no presplit)
+  if (p.part != ~0ull) {
+    const uint64_t span = a.b_mn ? (uint64_t)(p.k - 1) * (uint64_t)b_k + (uint64_t)p.n
+                                 : (uint64_t)(p.n - 1) * (uint64_t)b_n + (uint64_t)p.k;
+    const uint64_t hbase = p.part, lbase = p.part + 4 * span;
+    a.b_base = bbase;
+    a.b_span = span;
+    a.presplit = 1;
+    if (a.b_mn) {
+      rc = tm_encode(enc, &a.tbh, hbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      rc |= tm_encode(enc, &a.tbl, lbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    } else {
+      rc = tm_encode(enc, &a.tbh, hbase, p.k, p.n, b_n, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
+      rc |= tm_encode(enc, &a.tbl, lbase, p.k, p.n, b_n, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
+    }
+    if (rc) return nullptr;
+    memcpy(blk, &a, sizeof a);
+    return (void*)k_gemm_tmap_split;
+  }
+  memcpy(blk, &a, sizeof a);
+  return (void*)k_gemm_tmap;
+}
+
+// launched before a PRESPLIT GEMM on the same stream (runtime.cu launch_one)
+extern "C" int rt_gemm_tma_prepass(const void* blk, void* stream) {
+  const tm_args* a = (const tm_args*)blk;
+  if (!a->presplit) return 0;
+  float* hi = (float*)a->p.part;
+  float* lo = hi + a->b_span;
+  const int64_t n = (int64_t)a->b_span;
+  const int grid = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+  k_tf32_split<<<grid > 0 ? grid : 1, 256, 0, (cudaStream_t)stream>>>((const float*)a->b_base, hi, lo, n);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 extern "C" int rt_gemm_tma_smem() { return TM_SMEM; }
+extern "C" int rt_gemm_tma_smem_persist() { return TP_SMEM; }
 extern "C" int rt_gemm_tma_smem_drain() { return TM_SMEM_DRAIN; }
 extern "C" int rt_gemm_tma_args_bytes() { return (int)sizeof(tm_args); }

@@ -28,6 +28,7 @@ extern "C" void* rt_kernel_scan_tile(int f64);
 extern "C" void* rt_kernel_scan_pipe(int f64, int step_major);
 extern "C" void* rt_kernel_scan_gae(int f64);
 extern "C" void* rt_gemm_tma_pack(void* blk, void* encode);
+extern "C" int rt_gemm_tma_prepass(const void* blk, void* stream);
 
 static thread_local std::string g_err;
 
@@ -217,6 +218,10 @@ static int launch_one(const rt_launch_rec* rec, const int64_t* env, int nenv, cu
   void* fn = prepare(rec->kernel, blk, env, nenv);
   if (!fn) return fail(RT_ERR_UNKNOWN_KERNEL, "unknown kernel family");
   if (rec->grid[0] <= 0) return RT_OK;  // empty box
+  // a persistent TMA GEMM whose weight operand is split into tf32 hi/lo once
+  // per launch: the split pass first, on the same stream
+  if (rec->kernel == RT_K_GEMM_TMA && rt_gemm_tma_prepass(blk, (void*)s) != 0)
+    return fail(RT_ERR_CUDA, "tf32 split pass");
   void* args[1] = {blk};
   dim3 g(rec->grid[0], rec->grid[1] > 0 ? rec->grid[1] : 1, rec->grid[2] > 0 ? rec->grid[2] : 1);
   dim3 b(rec->block[0], rec->block[1] > 0 ? rec->block[1] : 1, rec->block[2] > 0 ? rec->block[2] : 1);

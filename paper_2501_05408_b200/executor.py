@@ -401,11 +401,11 @@ GATE_ENABLED = os.environ.get("RTB200_NO_GATE") != "1"
 def find_gate_epilogues(g: Graph, pshape, fixed_of, skip, ext):
     """matmul -> (always-true merges) -> mul(., 1 - h*h): the tanh VJP
     (reference frontend.py:961-963, `gy * (one - y * y)`) applied to a
-    narrow-K product (d(hidden) = d(head) @ W^T).  One RT_K_THIN variant-2
-    launch computes the product and multiplies by (1 - h*h) in its epilogue
-    (csrc/k_gemm_thin.cu, epilogue 2), so the product never round-trips HBM.
-    Only where that kernel is certain to run (K <= 32, >= 4096 rows, fp32 or
-    fp64 throughout).  Returns {mul id: (matmul id, merges, sub id, inner
+    product (d(hidden) = d(next) @ W^T).  One GEMM launch computes the product
+    and multiplies by (1 - h*h) in its epilogue, so the product never
+    round-trips HBM: the narrow-K RT_K_THIN variant 2 (K <= 32, >= 4096 rows,
+    fp32 or fp64) or the tcgen05 TMA GEMM (fp32, K >= 64, a real
+    contraction; csrc/k_gemm_tma.cu epilogue 2).  Returns {mul id: (matmul id, merges, sub id, inner
     mul id, edge h -> inner mul)}."""
     out_ids = {nid for _, nid, _ in g.outputs}
     res = {}
@@ -468,7 +468,12 @@ def find_gate_epilogues(g: Graph, pshape, fixed_of, skip, ext):
                 rows *= ext.get(d, 1)
         kp = 4 if k <= 4 else 8 if k <= 8 else 16 if k <= 16 else 32
         esize = 8 if x.dtype == "f64" else 4
-        if not (1 <= k <= 32 and rows >= 4096 and (kp * xs[1] + 64 * kp + xs[1]) * esize <= 48 * 1024):
+        thin = 1 <= k <= 32 and rows >= 4096 and (kp * xs[1] + 64 * kp + xs[1]) * esize <= 48 * 1024
+        # or the tcgen05 TMA GEMM (epilogue 2 in csrc/k_gemm_tma.cu): fp32, a
+        # real contraction (lower.TC_MIN_MACS), one K pass (no split-K)
+        tma = x.dtype == "f32" and k >= 64 and rows >= 64 and xs[1] >= 16 and \
+            rows * xs[1] * k >= (1 << 26) and k <= 256     # one TMEM chunk (no drain)
+        if not (thin or tma):
             continue
         res[y.id] = (x.id, tuple(chain), sn.id, mn.id, m_in[0])
     return res

@@ -113,6 +113,8 @@ OPC = {"ICOORD": 1, "IENV": 2, "ICONST": 3, "IADD": 4, "ISUB": 5, "IMUL": 6, "IF
        "VGT": 48, "VGE": 49, "VWHERE": 50, "VCAST": 51, "VMOV": 52, "VTOI": 53,
        "VALID": 54, "STORE": 60, "ERROR": 62, "ISTORE": 63}
 
+TMA_PERSIST = os.environ.get("RTB200_GEMM_PERSIST", "1") != "0"
+
 IBIN = {"add": "IADD", "sub": "ISUB", "mul": "IMUL", "floordiv": "IFDIV", "mod": "IMOD",
         "eq": "IEQ", "lt": "ILT", "le": "ILE", "gt": "IGT", "ge": "IGE", "and": "IAND",
         "or": "IOR"}
@@ -1856,12 +1858,20 @@ class Lowering:
         if bias is not None:
             p.bias = bias
         if gate is not None:
-            # the tanh-VJP gate epilogue exists in the narrow-K thin kernel only
-            # (executor.find_gate_epilogues fuses only where it runs)
-            if self._capture_active() or not self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
-                                                             epilogue, None, gate=gate):
-                raise LowerError(f"{label[1]}: gate epilogue needs the narrow-K thin GEMM")
-            return
+            # the tanh-VJP gate epilogue: the narrow-K thin kernel or the
+            # tcgen05 TMA GEMM (executor.find_gate_epilogues fuses only there)
+            if not self._capture_active() and self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
+                                                              epilogue, None, gate=gate):
+                return
+            if not self._capture_active() and self.use_tc and self._tc_ok(p, A, B, Cc) and \
+                    self.use_tma and self._tma_ok(p) and p.k <= N.TMA_DRAIN_K and not accumulate:
+                g = N.rt_gop()
+                C.memmove(C.addressof(g), C.addressof(gate), C.sizeof(g))
+                g.s1[0], g.s2[0] = p.C.s1[0], p.C.s2[0]     # laid out like C (k_matmul)
+                p.bias = g
+                p.epilogue = 2
+                return self._gemm_tc(p, label, accumulate, 2, None)
+            raise LowerError(f"{label[1]}: gate epilogue needs the thin or the TMA GEMM")
         if not self._capture_active() and self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
                                                           epilogue, bias):
             return
@@ -2106,6 +2116,14 @@ class Lowering:
         return self._capture is not None
 
     @staticmethod
+    def _tma_b_span(p):
+        """Elements of B's storage a 2-D TMA view covers (k_gemm_tma.cu pack)."""
+        b_k, b_n = p.B.s1[0], p.B.s2[0]
+        if b_k == 1 or p.k == 1:
+            return (p.n - 1) * b_n + p.k
+        return (p.k - 1) * b_k + p.n
+
+    @staticmethod
     def _tma_ok(p):
         """Plain 2-D f32 operands with a unit-stride dim and 16-byte aligned
         rows: eligible for the TMA-fed pipeline (csrc/k_gemm_tma.cu)."""
@@ -2136,10 +2154,24 @@ class Lowering:
         grid = [(p.m + 127) // 128, (p.n + 255) // 256, p.z * splits]
         if self.use_tma and self._tma_ok(p):
             # K per CTA beyond one TMEM accumulation chunk -> the draining
-            # variant (csrc/k_gemm_tma.cu, rt_gemm_tma_pack: same rule)
+            # variant (csrc/k_gemm_tma.cu, rt_gemm_tma_pack: same rule);
+            # one chunk, no split -> the persistent warp-specialised variant
+            # (p.part = scratch for B's tf32 hi/lo split when B is a small
+            # operand every M tile reads, else ~0)
             kper = (-(-p.k // splits) + 15) // 16 * 16
-            smem = N.TMA_SMEM_DRAIN if kper > N.TMA_DRAIN_K else N.TMA_SMEM
-            self.add_rec(N.RT_K_GEMM_TMA, p, grid, [320, 1, 1], smem, label)
+            if kper > N.TMA_DRAIN_K:
+                self.add_rec(N.RT_K_GEMM_TMA, p, grid, [320, 1, 1], N.TMA_SMEM_DRAIN, label)
+            elif splits == 1 and TMA_PERSIST:
+                b_span = self._tma_b_span(p)
+                mtiles = (p.m + 127) // 128
+                if b_span * 4 <= (16 << 20) and mtiles >= 16:
+                    p.part = self.alloc(2 * b_span * 4)
+                else:
+                    p.part = (1 << 64) - 1
+                g = [int(min(tiles, 148)), 1, 1]
+                self.add_rec(N.RT_K_GEMM_TMA, p, g, [N.TMA_THREADS_P, 1, 1], N.TMA_SMEM_P, label)
+            else:
+                self.add_rec(N.RT_K_GEMM_TMA, p, grid, [320, 1, 1], N.TMA_SMEM, label)
         else:
             self.add_rec(N.RT_K_GEMM_TC, p, grid, [256, 1, 1], N.TC_SMEM, label)
         if splits > 1:

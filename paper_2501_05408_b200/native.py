@@ -32,6 +32,8 @@ RT_K_GEMM_TMA = 12
 TMA_SMEM = 2 * 48 * 1024 + 1024
 TMA_SMEM_DRAIN = 4 * 48 * 1024 + 1024   # k_gemm_tma_drain: 4 stages, one CTA per SM
 TMA_DRAIN_K = 256                        # K per TMEM accumulation chunk
+TMA_SMEM_P = 4 * 48 * 1024 + 1024       # k_gemm_tmap: persistent, 4 stages, one CTA per SM
+TMA_THREADS_P = 128 + 64 + 256
 TC_SMEM = 2 * (2 * 128 * 32 * 4 + 2 * 256 * 32 * 4)
 
 RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK, RT_OP_ENVMOD = 1, 2, 3, 4, 6, 7
