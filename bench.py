@@ -419,6 +419,14 @@ def main():
                  "ms_per_launch": kms, "launches_per_step": dom["count"],
                  "share_of_step": dom["ms"] / max(1e-9, sum(r["ms"] for r in prof)),
                  "peak_source": src})
+    # whole-step roofline: sum over launches of max(bytes / HBM,
+    # flops / compute ceiling) against the measured step time
+    floor = sum(RF.floor_ms(r["kernel"], r["params"], exe.loop_info.get(r["rec"]), hbm, tfl,
+                            FP32_SIMT_TFLOPS) * max(1, r["count"]) for r in prof)
+    whole = {"floor_ms_per_step": round(floor, 4), "measured_ms_per_step": round(ms, 4),
+             "frac": floor / ms if ms > 0 else None,
+             "ceilings": {"hbm_gbs": hbm, "tensor_3xtf32_tflops": tfl / 6.0,
+                          "fp32_simt_tflops": FP32_SIMT_TFLOPS}}
     top = []
     for r in rows[:8]:
         b_, f_ = RF.cost(r["kernel"], r["params"], exe.loop_info.get(r["rec"]))
@@ -474,6 +482,7 @@ def main():
                 "time_block": exe.swap_plan.bs},
             "naive_hbm_bytes": exe.naive_bytes,
             "roofline": roof,
+            "roofline_step": whole,
             "breakdown": {"family_ms_per_step": {k: round(v, 3) for k, v in fam_ms.items()},
                           "top": top},
             "clocks": clk}

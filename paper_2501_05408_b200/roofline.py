@@ -70,12 +70,15 @@ def cost(kernel, p, loop_info=None):
         ea = _gop_elems(p.A, p.Z, p.M, p.K, 0) * ITEM.get(p.A.dtype, 4)
         eb = _gop_elems(p.B, p.Z, p.K, p.N, 1) * ITEM.get(p.B.dtype, 4)
         ec = p.z * p.m * p.n * ITEM.get(p.C.dtype, 4)
+        if kernel == N.RT_K_GEMM_TMA and p.epilogue == 2:   # tanh-VJP gate operand (m x n)
+            ec += p.z * p.m * p.n * ITEM.get(p.bias.dtype, 4)
         return ea + eb + ec, fl
     if kernel == N.RT_K_THIN:
         it = 8 if p.f64 else 4
         if p.variant == 1:   # stream X[k, w], Y[k, r]; partials out
             return (p.k * (p.w + p.r) + p.splits * p.w * p.r) * it, 2 * p.w * p.r * p.k
-        return (p.w * p.k + p.k * p.r + p.w * p.r * (2 if p.accumulate else 1)) * it, \
+        gate = p.w * p.r if (p.variant == 2 and p.epilogue == 2) else 0   # gate operand read
+        return (p.w * p.k + p.k * p.r + p.w * p.r * (2 if p.accumulate else 1) + gate) * it, \
             2 * p.w * p.r * p.k
     if kernel == N.RT_K_RNG:
         return p.total * p.count * ITEM.get(p.out.dtype, 4), 0
@@ -90,3 +93,21 @@ def cost(kernel, p, loop_info=None):
         it = 8 if p.f64 else 4
         return p.z * p.m * p.n * it * (p.splits + 1), p.z * p.m * p.n * p.splits
     return 0, 0
+
+
+# per-family compute ceilings for the whole-step roofline (TFLOP/s): the
+# tcgen05 GEMMs run 3xTF32 (three tf32 MMAs per fp32 product: the dense bf16
+# peak / 2 / 3), everything else computes on the FP32 SIMT pipes
+def compute_peak_tflops(family, bf16_tflops, fp32_simt_tflops):
+    if family in ("gemm_tma", "gemm_tc"):
+        return bf16_tflops / 2.0 / 3.0
+    return fp32_simt_tflops
+
+
+def floor_ms(kernel, p, loop_info, hbm_gbs, bf16_tflops, fp32_simt_tflops):
+    """Roofline time of one launch: max(algorithmic bytes / HBM, flops /
+    the family's compute ceiling), in ms."""
+    b, f = cost(kernel, p, loop_info)
+    t_mem = b / (hbm_gbs * 1e9)
+    t_cmp = f / (compute_peak_tflops(FAMILY.get(kernel, ""), bf16_tflops, fp32_simt_tflops) * 1e12)
+    return 1e3 * max(t_mem, t_cmp)
