@@ -1570,7 +1570,7 @@ def _input_sig(inputs):
 
 
 def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None, comm=None,
-                   block=None, swap=False):
+                   block=None, swap=False, theta=None, memops=None):
     global _TORCH_DT
     torch = _torch()
     if _TORCH_DT is None:
@@ -1587,6 +1587,8 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
     ex = _CACHE.get(key)
     if ex is not None:
         _CACHE.move_to_end(key)
+        if theta is not None or memops is not None:
+            attach_plan_report(ex, theta, memops)
         return ex, benv
     from .demand import check as demand_check
     demand_check(graph, benv)      # the reference's out-of-domain OracleError (F5)
@@ -1601,6 +1603,9 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         comm = TorchComm()
     exe = Executable(h, benv, int(seed), dev, _input_sig(inputs), shard=shard, comm=comm,
                      swap=swap if block else False)
+    exe.plan_report = None
+    if theta is not None or memops is not None:
+        attach_plan_report(exe, theta, memops)
     _CACHE[key] = exe
     while len(_CACHE) > CACHE_MAX:
         _CACHE.popitem(last=False)        # frees the least recently used arena
@@ -1650,8 +1655,21 @@ def _resolve_dynamic(g: Graph, benv, dyn, inputs, seed, device):
     return benv
 
 
+def attach_plan_report(exe, theta, memops):
+    """polysched's plan (reference polysched.py: ScheduleFn, MemOpSet) checked
+    against the executor's own (plancheck.py); raises PlanError on an unsafe
+    free, keeps the report in exe.plan_report."""
+    from . import plancheck
+    prog = [(exe.prog[i].op, exe.prog[i].a) for i in range(exe.nprog)]
+    swapped = exe.swap_plan.keys if exe.swap_plan is not None else ()
+    exe.plan_report = plancheck.check(exe.g, exe.bufs, exe.labels, prog, exe.lifetimes,
+                                      plancheck.fused_map(exe), theta, memops, swapped)
+    return exe.plan_report
+
+
 def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=None,
-            device_outputs=False, stream=None, shard=None, comm=None, block=None, swap=False):
+            device_outputs=False, stream=None, shard=None, comm=None, block=None, swap=False,
+            theta=None, memops=None):
     """Drop-in for reference `reference_execute` (runtime.py:460-475).
 
     shard=ShardSpec(dim, rank, world): this process runs envs
@@ -1663,8 +1681,16 @@ def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=
     swap=True (with block): activations of the acting recurrence keep two
     time blocks in HBM and are offloaded to / fetched from pinned host
     memory per block (swap.py); an int is the swap threshold in bytes
-    (default 64 MiB, the reference's polysched.py:28)."""
-    exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm, block, swap)
+    (default 64 MiB, the reference's polysched.py:28).
+
+    theta / memops: polysched's ScheduleFn and MemOpSet for this graph
+    (reference polysched.py:92-143, 842-859; `memops` may carry the
+    donation_analysis dict as `.donations`).  The executor runs its own plan;
+    these are checked against it (plancheck.py: deallocation never before
+    polysched's last consumer, swap set, donations) and the report is kept
+    on the executable (get_executable(...)[0].plan_report)."""
+    exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm, block, swap,
+                               theta, memops)
     exe.run(inputs or {}, stream)
     if device_outputs:
         exe.check_status(stream)
