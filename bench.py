@@ -333,10 +333,15 @@ def main():
     host = WL.inputs()
     params = WL.params()
     dev_in = {k: torch.from_numpy(v).cuda() for k, v in host.items()}
-    shard = None
+    shard, comm = None, None
     if world > 1:
         shard = WL.shard(rank, world)     # envs [rank*B, (rank+1)*B) of B*world
-    exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard, block=WL.block,
+        if dist.get_backend() == "nccl":
+            # the library's own NCCL communicator: gradient all-reduces run
+            # inside the program (RT_OP_COLL), one CUDA graph per step
+            from paper_2501_05408_b200.shard import NcclComm
+            comm = NcclComm()
+    exe, _ = get_executable(g, bounds, dev_in, seed=0, shard=shard, comm=comm, block=WL.block,
                             swap=WL.swap)
 
     def step_dev(inp, graph=None):
@@ -439,16 +444,16 @@ def main():
     # e2e through the public API with host buffers
     hin = host
     for w in range(max(1, args.warmup)):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block,
-                       swap=WL.swap)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, comm=comm,
+                       block=WL.block, swap=WL.swap)
         hin = next_inputs(outs, params)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for s in range(args.steps):
-        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, block=WL.block,
-                       swap=WL.swap)
+        outs = execute(g, bounds=bounds, inputs=hin, seed=0, shard=shard, comm=comm,
+                       block=WL.block, swap=WL.swap)
         hin = next_inputs(outs, params)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     h2d = sum(v.nbytes for v in host.values())
@@ -472,6 +477,8 @@ def main():
             "e2e": {"value": e2e, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": exe.launch_count * args.steps,
+            "in_graph_collectives_per_step": 0 if exe.colls is None else len(exe.colls),
+            "host_hooks_per_step": len(exe.hooks),
             "peak_hbm_bytes": exe.peak_bytes,
             "peak_hbm_allocated_bytes": int(torch.cuda.max_memory_allocated()),
             "swap": None if exe.swap_rt is None else {

@@ -21,6 +21,10 @@
  *                     pinned cudaMemcpyAsync on a side stream)
  *   rt_rng_fill       runtime.py:50-55, 391-394 per-point
  *                     default_rng((seed, tag, *point)) draws, bit-exact
+ *   rt_nccl_*, rt_set_collectives, rt_coll_exec
+ *                     the gradient all-reduce of an env-sharded
+ *                     run (no reference counterpart: the reference is
+ *                     single-process), issued from the program itself
  *   rt_pool_*, rt_offload, rt_fetch, rt_block_update, rt_stack
  *                     SPEC.md:541-561 the runtime's Backend (allocate,
  *                     deallocate, move-between-tiers, dynamic-update, stack)
@@ -359,8 +363,24 @@ enum rt_op {
   RT_OP_HOOK = 6,      /* host hook a (e.g. an NCCL all-reduce of a slab,   */
                        /* a swap copy): rt_run_segment returns RT_HOOK      */
                        /* with the next pc                                  */
-  RT_OP_ENVMOD = 7     /* env[a] = env[b] mod c (ring slot of a time block) */
+  RT_OP_ENVMOD = 7,    /* env[a] = env[b] mod c (ring slot of a time block) */
+  RT_OP_COLL = 8       /* in-program collective a (rt_set_collectives): sum
+                          all-reduce of its slab on the program's stream;
+                          captured into CUDA graphs like a launch */
 };
+
+/* A sum all-reduce of a slab of one buffer (a gradient summed over the
+ * env-sharded dim): element offset off0 + sum_e env[e] *
+ * off_env[e] from ptr, count elements.  flush = 0: joins a bucket that the
+ * next flushing collective reduces as one NCCL group. */
+typedef struct {
+  uint64_t ptr;
+  int64_t off0;
+  int64_t off_env[RT_MAXENV];
+  int64_t count;
+  int32_t dtype;
+  int32_t flush;
+} rt_coll;
 
 #define RT_HOOK 100
 
@@ -456,6 +476,16 @@ int rt_block_update(uint64_t block, int64_t slot, uint64_t src, uint64_t elem_by
 /* stack: dst[i * elem_bytes ..] = srcs[i][0 .. elem_bytes), i < n */
 int rt_stack(uint64_t dst, const uint64_t* srcs, int32_t n, uint64_t elem_bytes, uint64_t stream);
 int rt_set_error(int code, const char* what);
+/* ---- NCCL (in-program collectives, csrc/coll.cu) -----------------------
+ * The library's own communicator (NCCL resolved with dlopen): rank 0 makes
+ * a unique id, every rank joins with it; rt_set_collectives registers the
+ * RT_OP_COLL table of the program about to run (per calling thread). */
+int rt_nccl_unique_id(unsigned char* out128);
+int rt_nccl_comm_init(int32_t nranks, int32_t rank, const unsigned char* id128, uint64_t* comm_out);
+int rt_nccl_comm_destroy(uint64_t comm);
+int rt_nccl_allreduce(uint64_t comm, uint64_t ptr, uint64_t count, int32_t dtype, uint64_t stream);
+int rt_set_collectives(uint64_t comm, const rt_coll* colls, int32_t ncoll);
+int rt_coll_exec(int32_t idx, const int64_t* env, int32_t nenv, uint64_t stream);
 #endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus

@@ -29,6 +29,7 @@ extern "C" void* rt_kernel_scan_pipe(int f64, int step_major);
 extern "C" void* rt_kernel_scan_gae(int f64);
 extern "C" void* rt_gemm_tma_pack(void* blk, void* encode);
 extern "C" int rt_gemm_tma_prepass(const void* blk, void* stream);
+extern "C" int rt_coll_exec(int32_t idx, const int64_t* env, int32_t nenv, uint64_t stream);
 
 static thread_local std::string g_err;
 
@@ -333,6 +334,12 @@ extern "C" int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* 
         ++pc;
         break;
       }
+      case RT_OP_COLL: {
+        int rc = rt_coll_exec(in.a, env, nenv, stream);
+        if (rc) return rc;
+        ++pc;
+        break;
+      }
       case RT_OP_HOOK:
         return fail(RT_ERR_BAD_ARG, "program has host hooks: use rt_run_segment");
       default:
@@ -374,6 +381,12 @@ extern "C" int rt_run_segment(const rt_instr* prog, int32_t nprog, const rt_laun
         env[in.a] = env[in.b] % in.c;
         ++pc;
         break;
+      case RT_OP_COLL: {
+        int rc = rt_coll_exec(in.a, env, nenv, stream);
+        if (rc) return rc;
+        ++pc;
+        break;
+      }
       case RT_OP_HOOK:
         *pc_io = pc + 1;
         *hook_out = in.a;
@@ -561,6 +574,10 @@ extern "C" int rt_profile(const rt_instr* prog, int32_t nprog, const rt_launch_r
     } else if (in.op == RT_OP_ENVMOD) {
       if (in.c > 0 && in.a >= 0 && in.a < nenv && in.b >= 0 && in.b < nenv)
         env[in.a] = env[in.b] % in.c;
+      ++pc;
+    } else if (in.op == RT_OP_COLL) {
+      int rc = rt_coll_exec(in.a, env, nenv, stream);
+      if (rc) return rc;
       ++pc;
     } else {
       ++pc;

@@ -909,6 +909,9 @@ class Executable:
                        shard_reduce=self.shard_reduce,
                        persistent=OPTS["persistent"], swap=self.swap_plan).lower()
         self.hooks = low.hooks
+        self.colls = None
+        if getattr(comm, "native", False):
+            self._native_collectives(low)
         self.slot_of = dict(low.slot)
         self.fixed_of = plan_fixed(self.plan.steps)
         self.swap_rt = None
@@ -949,6 +952,40 @@ class Executable:
         self.graph_failed = False
         self._stage_in, self._stage_ev, self._stage_out = {}, {}, None
         self._pgraph, self._pgraph_failed = None, False
+
+    def _native_collectives(self, low):
+        """All-reduce hooks -> in-program RT_OP_COLL instructions (csrc/coll.cu)
+        on the library's NCCL communicator: no host hook is left, so the whole
+        sharded program runs (and is captured) like an unsharded one."""
+        colls = []
+        for pc, ins in enumerate(low.prog):
+            if ins[0] != N.RT_OP_HOOK:
+                continue
+            h = low.hooks[ins[1]]
+            if h.get("kind", "allreduce") != "allreduce":
+                continue
+            c = N.rt_coll()
+            c.ptr = h["ptr"]
+            c.off0 = h["off0"]
+            for k, v in h["off_env"].items():
+                c.off_env[k] = v
+            c.count = h["count"]
+            c.dtype = N.DTYPE_CODE[h["dtype"]]
+            c.flush = 1 if h.get("flush", True) else 0
+            low.prog[pc] = (N.RT_OP_COLL, len(colls), 0, 0, 0, 0)
+            colls.append(c)
+        if colls:
+            arr = (N.rt_coll * len(colls))()
+            for i, c in enumerate(colls):
+                arr[i] = c
+            self.colls = arr
+        self.hooks = [h for h in low.hooks if h.get("kind", "allreduce") != "allreduce"] \
+            if not any(ins[0] == N.RT_OP_HOOK for ins in low.prog) else low.hooks
+
+    def _set_colls(self):
+        if self.colls is not None:
+            N.check(self.lib.rt_set_collectives(self.comm.handle, self.colls, len(self.colls)),
+                    "set collectives")
 
     def _upload_loops(self, low):
         """Persistent-loop sub-op descriptors live in HBM: one blob per loop
@@ -1106,6 +1143,7 @@ class Executable:
             s = stream or torch.cuda.current_stream(self.dev)
             self.upload_inputs(inputs, s)
             N.check(self.lib.rt_status_clear(self.status, s.cuda_stream), "status clear")
+            self._set_colls()
             if self.hooks:
                 return self._run_with_hooks(s)
             if graph and not events and self.launch_count >= self.GRAPH_MIN_LAUNCHES:
@@ -1212,6 +1250,7 @@ class Executable:
                 self.env[i] = 0
             ms = (N.f64 * max(1, self.nrec))()
             cnt = (N.i64 * max(1, self.nrec))()
+            self._set_colls()
             N.check(self.lib.rt_profile(self.prog, self.nprog, self.recs, self.nrec, self.env,
                                         N.RT_MAXENV, s.cuda_stream, ms, cnt), "rt_profile")
         out = []
@@ -1268,6 +1307,7 @@ class Executable:
             for i in range(N.RT_MAXENV):
                 self.env[i] = 0
             out = N.u64()
+            self._set_colls()
             N.check(self.lib.rt_graph_capture_ev(prog, len(ins), self.recs, self.nrec, self.env,
                                                  N.RT_MAXENV, cap.cuda_stream, ev_arr,
                                                  len(events), C.byref(out)), "capture")

@@ -37,6 +37,7 @@ TMA_THREADS_P = 128 + 64 + 256
 TC_SMEM = 2 * (2 * 128 * 32 * 4 + 2 * 256 * 32 * 4)
 
 RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK, RT_OP_ENVMOD = 1, 2, 3, 4, 6, 7
+RT_OP_COLL = 8
 RT_HOOK = 100
 
 RT_ERR_ROW_RANGE, RT_ERR_SLICE_RANGE = 1, 2
@@ -153,6 +154,11 @@ class rt_instr(C.Structure):
                 ("_pad", i32)]
 
 
+class rt_coll(C.Structure):
+    _fields_ = [("ptr", u64), ("off0", i64), ("off_env", i64 * RT_MAXENV), ("count", i64),
+                ("dtype", i32), ("flush", i32)]
+
+
 class NativeError(RuntimeError):
     pass
 
@@ -209,6 +215,12 @@ def lib():
     L.rt_block_update.argtypes = [u64, i64, u64, u64, u64]
     L.rt_stack.argtypes = [u64, C.POINTER(u64), i32, u64, u64]
     L.rt_set_error.argtypes = [i32, C.c_char_p]
+    L.rt_nccl_unique_id.argtypes = [C.c_char_p]
+    L.rt_nccl_comm_init.argtypes = [i32, i32, C.c_char_p, C.POINTER(u64)]
+    L.rt_nccl_comm_destroy.argtypes = [u64]
+    L.rt_nccl_allreduce.argtypes = [u64, u64, u64, i32, u64]
+    L.rt_set_collectives.argtypes = [u64, C.POINTER(rt_coll), i32]
+    L.rt_coll_exec.argtypes = [i32, C.POINTER(i64), i32, u64]
     if L.rt_version() != 1:
         raise NativeError("librtb200 ABI version mismatch")
     _lib = L
@@ -222,7 +234,9 @@ EXPORTS = ("rt_version", "rt_launch", "rt_run", "rt_status_alloc", "rt_status_re
            "rt_jit_compile", "rt_jit_load", "rt_jit_cubin", "rt_memcpy2d_d2h_async",
            "rt_memcpy2d_h2d_async", "rt_pool_create", "rt_pool_destroy", "rt_pool_alloc",
            "rt_pool_free", "rt_pool_host", "rt_pool_stats", "rt_offload", "rt_fetch",
-           "rt_block_update", "rt_stack", "rt_set_error")
+           "rt_block_update", "rt_stack", "rt_set_error", "rt_nccl_unique_id",
+           "rt_nccl_comm_init", "rt_nccl_comm_destroy", "rt_nccl_allreduce",
+           "rt_set_collectives", "rt_coll_exec")
 
 
 def check(rc: int, what: str = ""):

@@ -17,6 +17,8 @@ shards into contiguous blocks of B/G per rank with:
 
 from __future__ import annotations
 
+import ctypes as C
+
 from dataclasses import dataclass
 
 from . import ir
@@ -130,3 +132,50 @@ class TorchComm:
     def allreduce_(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
+
+
+class NcclComm:
+    """The library's own NCCL communicator (csrc/coll.cu): the sharded
+    program's gradient all-reduces become in-program collectives (RT_OP_COLL)
+    issued by the interpreter on the program's stream, so a whole step --
+    rollout, backward, all-reduces, updates -- is one CUDA graph.  The unique
+    id travels through torch.distributed (any backend) once at setup."""
+
+    native = True
+
+    def __init__(self, rank=None, world=None, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import native as N
+        self.lib = N.lib()
+        rank = dist.get_rank(group) if rank is None else rank
+        world = dist.get_world_size(group) if world is None else world
+        buf = bytearray(128)
+        if rank == 0:
+            cid = C.create_string_buffer(128)
+            N.check(self.lib.rt_nccl_unique_id(cid), "nccl unique id")
+            buf = bytearray(cid.raw[:128])
+        t = torch.tensor(list(buf), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=0, group=group)
+        idb = bytes(t.cpu().tolist())
+        h = N.u64()
+        N.check(self.lib.rt_nccl_comm_init(int(world), int(rank), idb, C.byref(h)), "nccl init")
+        self.handle = h.value
+        self.rank, self.world = rank, world
+
+    def allreduce_(self, t):
+        """(host-side fallback path: one tensor, on torch's current stream)"""
+        import torch
+        from . import native as N
+        code = {torch.float64: N.RT_F64, torch.float32: N.RT_F32, torch.int64: N.RT_I64}[t.dtype]
+        N.check(self.lib.rt_nccl_allreduce(self.handle, t.data_ptr(), t.numel(), code,
+                                           torch.cuda.current_stream().cuda_stream), "allreduce")
+        return t
+
+    def close(self):
+        if getattr(self, "handle", 0):
+            from . import native as N
+            N.check(self.lib.rt_nccl_comm_destroy(self.handle), "nccl destroy")
+            self.handle = 0

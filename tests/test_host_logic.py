@@ -38,7 +38,7 @@ def test_struct_layouts_match_header(tmp_path):
     src = tmp_path / "sz.c"
     names = ["rt_box", "rt_view", "rt_hdr", "rt_ew_params", "rt_reduce_params",
              "rt_scan_params", "rt_gemm_params", "rt_splitk_params", "rt_rng_params",
-             "rt_udf_params", "rt_launch_rec", "rt_instr", "rt_gop", "rt_thin_params"]
+             "rt_udf_params", "rt_launch_rec", "rt_instr", "rt_gop", "rt_thin_params", "rt_coll"]
     src.write_text('#include <stdio.h>\n#include "rtb200.h"\nint main(){' +
                    "".join(f'printf("%zu\\n", sizeof({n}));' for n in names) + "}")
     exe = tmp_path / "sz"
