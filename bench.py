@@ -116,7 +116,7 @@ def peaks():
 FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 # kernel family -> the kernel name in the committed ncu --set full capture
-_NCU_NAME = {"loop": "loop_jit", "gemm_tma": "k_gemm_tma", "ew": "ew_jit", "scan": "k_scan"}
+_NCU_NAME = {"loop": "loop_mlp", "gemm_tma": "k_gemm_tmap", "ew": "ew_jit", "scan": "k_scan"}
 
 
 def ncu_traffic(family):
