@@ -177,13 +177,14 @@ typedef struct {
   rt_view out;
   /* window form: y[j] = S[lo(j)] - gamma^(hi-lo) * S[hi(j)], unused if win=0 */
   int32_t win;
-  int32_t tile;        /* 1: tiled kernel (64 contiguous lines per CTA, 16-B I/O) */
+  int32_t tile;        /* 2: cp.async ring, line-major; 3: the same, step-major;
+                        * 4: bulk-copy pipeline per line (chunk = elements per stage) */
   /* gae != 0: the scanned value is the TD residual computed on the fly,
    * x[j] = in[j] + gae_c * (j+1 < L ? in2[j+1] : gae_vb) - in2[j]
    * (GAE(lambda): delta = r + gamma V[t+1] - V, bootstrap gae_vb at T-1),
    * so delta never round-trips through HBM. */
   int32_t gae;
-  int32_t _pad3;
+  int32_t stages;      /* tile 4: shared-memory stages per line */
   double gae_c, gae_vb;
   rt_view in2;
 } rt_scan_params;

@@ -115,14 +115,6 @@ __global__ void __launch_bounds__(256) k_scan_thread(const __grid_constant__ rt_
   }
 }
 
-// Line-contiguous lines, tiled: a CTA of 64 threads owns 64 lines and
-// walks them chunk by chunk (TC elements, in processing order).  Each chunk
-// arrives as 16-byte loads coalesced along the lines (prefetched into
-// registers while the previous chunk is scanned), is transposed through
-// shared memory so that thread i scans line i sequentially (one fp64 FMA per
-// element, no shuffles), and leaves as 16-byte coalesced stores.  Needs
-// in/out of type T, every line start and the line length a multiple of the
-// vector width (host checks, lower.py _scan_launch).
 template <typename T> struct svec;
 template <> struct svec<float> { using V = float4; static constexpr int W = 4; };
 template <> struct svec<double> { using V = double2; static constexpr int W = 2; };
@@ -131,101 +123,8 @@ RT_DEV void sunpack(const float4& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = 
 RT_DEV void sunpack(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
 RT_DEV float4 spack(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
 RT_DEV double2 spack(const double* o) { return make_double2(o[0], o[1]); }
-RT_DEV void szero(float4& v) { v = make_float4(0.f, 0.f, 0.f, 0.f); }
-RT_DEV void szero(double2& v) { v = make_double2(0.0, 0.0); }
 
 #define SCAN_LB 64
-
-template <typename T>
-__global__ void __launch_bounds__(SCAN_LB) k_scan_tile(const __grid_constant__ rt_scan_params p) {
-  using V = typename svec<T>::V;
-  constexpr int VW = svec<T>::W;
-  constexpr int TC = 16 * VW;                 // elements per line per chunk
-  constexpr int VPL = TC / VW;                // vectors per line per chunk (16)
-  constexpr int NV = SCAN_LB * VPL / SCAN_LB; // vectors per thread per chunk (16)
-  __shared__ T tile[SCAN_LB][TC + 1];
-  __shared__ int64_t ib[SCAN_LB], ob[SCAN_LB];
-  const int tid = threadIdx.x;
-  const double g = p.gamma;
-  const T* X = (const T*)p.in.ptr;
-  T* Y = (T*)p.out.ptr;
-  const int64_t L = p.box.ext[p.sdim];
-  const int64_t nch = (L + TC - 1) / TC;
-  for (int64_t blk = blockIdx.x; blk * SCAN_LB < p.total_lines; blk += gridDim.x) {
-    const int64_t nl = p.total_lines - blk * SCAN_LB < SCAN_LB ? p.total_lines - blk * SCAN_LB
-                                                               : SCAN_LB;
-    {
-      int64_t i0, o0, si, so, LL;
-      line_base(p, blk * SCAN_LB + (tid < nl ? tid : 0), &i0, &o0, &si, &so, &LL);
-      ib[tid] = i0;
-      ob[tid] = o0;
-    }
-    __syncthreads();
-    // memory range of chunk c: [j0, j0 + cnt)
-    auto chunk = [&](int64_t c, int64_t& j0, int& cnt) {
-      const int64_t a = c * TC, b = (c + 1) * TC < L ? (c + 1) * TC : L;
-      cnt = (int)(b - a);
-      j0 = p.reverse ? L - b : a;
-    };
-    V r[NV];
-    auto load = [&](int64_t c) {
-      int64_t j0;
-      int cnt;
-      chunk(c, j0, cnt);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int f = tid + SCAN_LB * v, ln = f / VPL, pc = f - ln * VPL;
-        if (ln < nl && pc * VW < cnt)
-          r[v] = __ldcs(reinterpret_cast<const V*>(X + ib[ln] + j0 + pc * VW));
-        else
-          szero(r[v]);
-      }
-    };
-    load(0);
-    double acc = 0.0;
-    for (int64_t c = 0; c < nch; ++c) {
-      int64_t j0;
-      int cnt;
-      chunk(c, j0, cnt);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int f = tid + SCAN_LB * v, ln = f / VPL, pc = f - ln * VPL;
-        T e[VW];
-        sunpack(r[v], e);
-#pragma unroll
-        for (int q = 0; q < VW; ++q) tile[ln][pc * VW + q] = e[q];
-      }
-      __syncthreads();
-      if (c + 1 < nch) load(c + 1);
-      if (p.reverse) {
-        for (int k = cnt - 1; k >= 0; --k) {
-          const double x = (double)tile[tid][k];
-          acc = (c == 0 && k == cnt - 1) ? x : x + g * acc;
-          tile[tid][k] = (T)acc;
-        }
-      } else {
-#pragma unroll 8
-        for (int k = 0; k < cnt; ++k) {
-          const double x = (double)tile[tid][k];
-          acc = (c == 0 && k == 0) ? x : x + g * acc;
-          tile[tid][k] = (T)acc;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int f = tid + SCAN_LB * v, ln = f / VPL, pc = f - ln * VPL;
-        if (ln < nl && pc * VW < cnt) {
-          T e[VW];
-#pragma unroll
-          for (int q = 0; q < VW; ++q) e[q] = tile[ln][pc * VW + q];
-          __stcs(reinterpret_cast<V*>(Y + ob[ln] + j0 + pc * VW), spack(e));
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
 
 // Pipelined tiled scan: the same 64-line CTA tiles, but chunks land in a
 // 3-stage shared-memory ring through cp.async 16-byte copies (two chunks in
@@ -501,10 +400,6 @@ extern "C" void* rt_kernel_scan_gae(int f64) {
   return f64 ? (void*)k_scan_gae<double> : (void*)k_scan_gae<float>;
 }
 
-extern "C" void* rt_kernel_scan_tile(int f64) {
-  return f64 ? (void*)k_scan_tile<double> : (void*)k_scan_tile<float>;
-}
-
 // tile == 2: pipelined line-major, tile == 3: pipelined step-major
 extern "C" void* rt_kernel_scan_pipe(int f64, int step_major) {
   if (step_major) return f64 ? (void*)k_scan_pipe<double, true> : (void*)k_scan_pipe<float, true>;
@@ -515,3 +410,4 @@ extern "C" void* rt_kernel_scan(int f64, int warp) {
   if (warp) return f64 ? (void*)k_scan_warp<double> : (void*)k_scan_warp<float>;
   return f64 ? (void*)k_scan_thread<double> : (void*)k_scan_thread<float>;
 }
+

@@ -24,7 +24,7 @@ extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
 extern "C" void* rt_kernel_thin_rows(int f64, int r, int k);
-extern "C" void* rt_kernel_scan_tile(int f64);
+extern "C" void* rt_scan_tma_pack(void* blk, void* encode);
 extern "C" void* rt_kernel_scan_pipe(int f64, int step_major);
 extern "C" void* rt_kernel_scan_gae(int f64);
 extern "C" void* rt_gemm_tma_pack(void* blk, void* encode);
@@ -132,11 +132,13 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       rt_scan_params* p = (rt_scan_params*)blk;
       fold_view(p->in, env, nenv);
       fold_view(p->out, env, nenv);
-      if (p->gae) {
-        fold_view(p->in2, env, nenv);
-        return rt_kernel_scan_gae(p->f64);
+      if (p->gae) fold_view(p->in2, env, nenv);
+      if (p->tile == 4) {
+        DriverApi& D = drv();
+        if (!D.ok) return nullptr;
+        return rt_scan_tma_pack(blk, D.tensorMapEncodeTiled);
       }
-      if (p->tile == 1) return rt_kernel_scan_tile(p->f64);
+      if (p->gae) return rt_kernel_scan_gae(p->f64);
       if (p->tile >= 2) return rt_kernel_scan_pipe(p->f64, p->tile == 3);
       int warp = p->in.stride[p->sdim] == 1 && p->out.stride[p->sdim] == 1;
       return rt_kernel_scan(p->f64, warp);

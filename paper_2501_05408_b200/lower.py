@@ -1644,9 +1644,62 @@ class Lowering:
                     any(v.off_env[e] % vw for e in range(N.RT_MAXENV)) or \
                     any(v.stride[d] % vw for d in range(p.box.nd) if d != p.sdim and box[d] > 1):
                 raise LowerError("GAE scan operands are not line-major and 16-B aligned")
+        if self._scan_bulk(p, 2, (n.id, n.name)):
+            return
         smem = 2 * self.SCAN_STAGES * 64 * 8 * 16 + 3 * 64 * 8      # k_scan_gae: 8 vectors/line
         self.add_rec(N.RT_K_SCAN, p, [-(-p.total_lines // 64), 1, 1], [64, 1, 1], smem,
                      (n.id, n.name))
+
+    SCAN_TMA = os.environ.get("RTB200_SCAN_TMA", "1") != "0"
+
+    def _scan_bulk(self, p, nin, label):
+        """TMA scan (csrc/k_scan_tma.cu, tile 4): one warp per 32 lines,
+        128-byte x 32-line boxes per operand and stage.  Needs every
+        operand 2-D: unit stride along the scan dim, the other dims
+        collapsing to one line stride (a multiple of 16 bytes), 16-byte
+        aligned bases.  The stage count is chosen so that every CTA of the
+        launch is resident at once (no tail wave): one SM's shared memory
+        (228 KB, 1 KB reserved per CTA) split over the CTAs it must hold,
+        at most 4 (the r2t sweep: 2 -> 53%, 4 -> 75%, 8 -> 54% of HBM with
+        a tail wave); RTB200_SCAN_STAGES overrides for measurements."""
+        if not self.SCAN_TMA or p.total_lines >= (1 << 31):
+            return False
+        esize = 8 if p.f64 else 4
+        nd, sd = p.box.nd, p.sdim
+        L = p.box.ext[sd]
+        if L >= (1 << 31) or L % (16 // esize):
+            return False
+        views = [p.in_, p.out] + ([p.in2] if nin == 2 else [])
+        for v in views:
+            if v.stride[sd] != 1 or (v.ptr + esize * v.off) % 16 or \
+                    any(v.off_env[e] % (16 // esize) for e in range(N.RT_MAXENV)):
+                return False
+            st, span = None, 1
+            for d in reversed(range(nd)):
+                if d == sd or p.box.ext[d] <= 1:
+                    continue
+                if st is None:
+                    st = v.stride[d]
+                elif v.stride[d] != st * span:
+                    return False
+                span *= p.box.ext[d]
+            if st is not None and p.total_lines > 1 and (st * esize) % 16:
+                return False
+        ctas = -(-p.total_lines // 32)
+        per_sm = min(32, -(-ctas // 148))
+        budget = (228 * 1024) // per_sm - 1024
+        ns = min(4, (budget - 1024 - 64) // (nin * 4096))   # 4 measured best (r2t sweep)
+        env_s = os.environ.get("RTB200_SCAN_STAGES")
+        if env_s:
+            ns = int(env_s)
+        if ns < 2:
+            return False
+        smem = ns * nin * 4096 + 8 * ns + 1024
+        if smem > 227 * 1024:
+            return False
+        p.tile, p.chunk, p.stages = 4, 128 // esize, ns
+        self.add_rec(N.RT_K_SCAN, p, [ctas, 1, 1], [32, 1, 1], smem, label)
+        return True
 
     def _scan_launch(self, p, label):
         """Pick the scan kernel (csrc/k_scan.cu): tiled 64-line CTAs with
@@ -1674,6 +1727,8 @@ class Lowering:
         nblk = -(-p.total_lines // 64)
         if contig and same_t and L % vw == 0 and aligned(p.in_) and aligned(p.out) \
                 and nblk < (1 << 31):
+            if self._scan_bulk(p, 1, label):
+                return
             p.tile = 2
             self.add_rec(N.RT_K_SCAN, p, [nblk, 1, 1], [64, 1, 1], smem, label)
         elif (same_t and inner is not None and p.in_.stride[inner] == 1

@@ -83,7 +83,7 @@ class rt_scan_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("box", rt_box), ("total_lines", i64), ("sdim", i32),
                 ("reverse", i32), ("gamma", f64), ("f64", i32), ("chunk", i32),
                 ("in_", rt_view), ("out", rt_view), ("win", i32), ("tile", i32),
-                ("gae", i32), ("_pad3", i32), ("gae_c", f64), ("gae_vb", f64),
+                ("gae", i32), ("stages", i32), ("gae_c", f64), ("gae_vb", f64),
                 ("in2", rt_view)]
 
 

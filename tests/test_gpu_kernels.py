@@ -235,6 +235,86 @@ def test_scan_kernels_layouts(layout, dt, forward, n_env, T):
     np.testing.assert_allclose(out, want, rtol=tol, atol=tol * 10)
 
 
+def _scan_tiles(g, inputs, bounds=None):
+    from paper_2501_05408_b200 import get_executable, native as N
+    exe, _ = get_executable(g, bounds or {}, inputs, 0)
+    return [(p.tile, p.stages) for k, p in zip(exe.kernels, exe._params) if k == N.RT_K_SCAN]
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+@pytest.mark.parametrize("stages", [2, 3, 5, 8])
+@pytest.mark.parametrize("forward", [False, True])
+@pytest.mark.parametrize("n_env,T", [(300, 212), (32, 8), (1, 1000)])
+def test_scan_tma_configs(dt, stages, forward, n_env, T, monkeypatch):
+    """The TMA scan (k_scan_tma: 32-line x 128-byte boxes on a stage ring,
+    TMA stores) at several stage counts, on line counts that are not a
+    multiple of the 32-line CTA and lengths that are not a multiple of the
+    box width (zero-filled loads, clipped stores), vs a float64 scan; the
+    lowering must have picked it (tile 4)."""
+    from paper_2501_05408_b200 import executor as X
+    monkeypatch.setenv("RTB200_SCAN_STAGES", str(stages))
+    X._CACHE.clear()
+    npd = np.float32 if dt == "f32" else np.float64
+    r = np.random.default_rng(T + stages).standard_normal((n_env, T)).astype(npd)
+    g = _scan_graph("bt", n_env, T, dt, forward)
+    assert _scan_tiles(g, {"r": r}) == [(4, stages)]
+    out = execute(g, inputs={"r": r})["G"]
+    x = r.astype(np.float64)
+    want = np.zeros_like(x)
+    acc = np.zeros(n_env)
+    order = range(T) if forward else reversed(range(T))
+    for i, t in enumerate(order):
+        acc = x[:, t] + (0.97 * acc if i else 0.0)
+        want[:, t] = acc
+    tol = 1e-5 if dt == "f32" else 1e-12
+    np.testing.assert_allclose(out, want, rtol=tol, atol=tol * 10)
+    X._CACHE.clear()
+
+
+@pytest.mark.parametrize("stages", [2, 3, 6])
+@pytest.mark.parametrize("B,T", [(4096, 512), (33, 100), (7, 4)])
+def test_gae_tma_scan(stages, B, T, monkeypatch):
+    """GAE residual formed inside the TMA scan (r and V boxes on one stage
+    barrier, V[t+1] carried across boxes in reverse order), ragged boxes."""
+    from golden_cases import load_graph
+    from paper_2501_05408_b200 import executor as X
+    monkeypatch.setenv("RTB200_SCAN_STAGES", str(stages))
+    X._CACHE.clear()
+    rng = np.random.default_rng(B + T + stages)
+    r = rng.standard_normal((B, T)).astype(np.float32)
+    V = rng.standard_normal((B, T)).astype(np.float32)
+    g = load_graph("k_gae_bt")
+    assert _scan_tiles(g, {"r": r, "V": V}, {"B": B, "T": T}) == [(4, stages)]
+    out = execute(g, bounds={"B": B, "T": T}, inputs={"r": r, "V": V})["A"]
+    Vn = np.concatenate([V[:, 1:], np.zeros((B, 1), np.float32)], axis=1)
+    delta = (r + Vn * np.float32(0.99)) - V
+    want = np.zeros((B, T))
+    acc = np.zeros(B)
+    for t in reversed(range(T)):
+        acc = delta[:, t].astype(np.float64) + (0.99 * 0.95 * acc if t < T - 1 else 0.0)
+        want[:, t] = acc
+    np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-5)
+    X._CACHE.clear()
+
+
+def test_scan_pipe_fallback_still_exact(monkeypatch):
+    """RTB200_SCAN_TMA=0 keeps the cp.async ring (k_scan_pipe, tile 2)."""
+    from paper_2501_05408_b200 import executor as X, lower
+    monkeypatch.setattr(lower.Lowering, "SCAN_TMA", False)
+    X._CACHE.clear()
+    r = np.random.default_rng(5).standard_normal((256, 300)).astype(np.float32)
+    g = _scan_graph("bt", 256, 300, "f32", False)
+    assert [t for t, _ in _scan_tiles(g, {"r": r})] == [2]
+    out = execute(g, inputs={"r": r})["G"]
+    want = np.zeros((256, 300))
+    acc = np.zeros(256)
+    for i, t in enumerate(reversed(range(300))):
+        acc = r[:, t] + (0.97 * acc if i else 0.0)
+        want[:, t] = acc
+    np.testing.assert_allclose(out, want, rtol=1e-5, atol=1e-4)
+    X._CACHE.clear()
+
+
 @pytest.mark.parametrize("K,N,dt", [(16, 256, "f32"), (16, 64, "f64"), (7, 33, "f32")])
 def test_gathered_rows_small_k_gemm(K, N, dt):
     """y[j,u,t] = x[u*M + j, t] @ W: minibatch rows gathered by a symbolic
