@@ -70,7 +70,7 @@ enum rt_kernel {
   RT_K_RNG = 5,      /* SeedSequence->PCG64->{normal,uniform} per point       */
   RT_K_UDF = 6,      /* synthetic environment (dsl.py:288-307) per point      */
   RT_K_SPLITK = 7,   /* split-K partial reduction for RT_K_GEMM               */
-  RT_K_POLICY = 8,   /* reserved                                              */
+  RT_K_MEMCPY = 8,   /* stream-ordered tier move of a swapped buffer (rt_memcpy_params) */
   RT_K_LOOP = 9,     /* persistent kernel running a whole row-local loop      */
   RT_K_GEMM_TC = 10, /* RT_K_GEMM on tcgen05 (3xTF32, TMEM accumulators)      */
   RT_K_THIN = 11,    /* HBM-bound skinny GEMMs (narrow contraction / small K)  */
@@ -188,6 +188,21 @@ typedef struct {
   double gae_c, gae_vb;
   rt_view in2;
 } rt_scan_params;
+
+/* RT_K_MEMCPY: one stream-ordered copy of `bytes` from src to dst
+ * (cudaMemcpyAsync, kind inferred from the addresses: device <-> pinned host).
+ * The general swap (swap.py plan_gap_swap) offloads a swap-managed buffer
+ * after its last touch before an idle gap and fetches it back before its next
+ * touch; as a launch record it is ordered, profiled and graph-captured like a
+ * kernel. */
+typedef struct {
+  rt_hdr h;
+  uint64_t dst;
+  uint64_t src;
+  int64_t bytes;
+  int32_t dir;         /* 0 offload (device -> host), 1 fetch (host -> device) */
+  int32_t _pad;
+} rt_memcpy_params;
 
 /* RT_K_GEMM: for z in Z, C[z,m,n] (+)= sum_k A[z,m,k] * B[z,k,n].
  * Each of Z, M, N, K is a flat index decomposed over its own small box;

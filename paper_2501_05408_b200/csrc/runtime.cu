@@ -19,7 +19,6 @@ extern "C" void* rt_kernel_splitk(int f64);
 extern "C" void* rt_kernel_rng();
 extern "C" void* rt_kernel_udf();
 extern "C" void* rt_kernel_rng_fill();
-extern "C" void* rt_kernel_policy(const void* params);
 extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
@@ -107,6 +106,8 @@ static void fold_gop(rt_gop& g, const int64_t* env, int nenv) {
 static void patch_env(rt_hdr* h, const int64_t* env, int nenv) {
   for (int e = 0; e < RT_MAXENV; ++e) h->env[e] = e < nenv ? env[e] : 0;
 }
+
+static char rt_memcpy_marker;
 
 // Fold the launch's env into a private copy of the parameter block and pick
 // the kernel variant.  Returns the kernel function or null.
@@ -197,8 +198,8 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       for (int i = 0; i < p->nout; ++i) fold_view(p->out[i], env, nenv);
       return rt_kernel_udf();
     }
-    case RT_K_POLICY:
-      return rt_kernel_policy(blk);
+    case RT_K_MEMCPY:
+      return (void*)&rt_memcpy_marker;   // not a kernel: launch_one copies
     case RT_K_LOOP: {
       rt_loop_params* p = (rt_loop_params*)blk;
       if (p->blk_len > 0) {
@@ -215,6 +216,15 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
 
 static int launch_one(const rt_launch_rec* rec, const int64_t* env, int nenv, cudaStream_t s) {
   alignas(128) static thread_local unsigned char blk[32768];
+  if (rec->kernel == RT_K_MEMCPY) {
+    rt_memcpy_params m;
+    if (rec->param_bytes != (int)sizeof m) return fail(RT_ERR_BAD_ARG, "memcpy record size");
+    memcpy(&m, (const void*)rec->params, sizeof m);
+    if (m.bytes <= 0) return RT_OK;
+    return cuda_check(cudaMemcpyAsync((void*)m.dst, (const void*)m.src, (size_t)m.bytes,
+                                      cudaMemcpyDefault, s),
+                      m.dir ? "swap fetch (cudaMemcpyAsync)" : "swap offload (cudaMemcpyAsync)");
+  }
   if (rec->param_bytes <= 0 || rec->param_bytes > (int)sizeof blk)
     return fail(RT_ERR_BAD_ARG, "parameter block size out of range");
   memcpy(blk, (const void*)rec->params, rec->param_bytes);

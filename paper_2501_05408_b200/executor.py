@@ -883,10 +883,37 @@ class Executable:
         for k in roots:
             life.setdefault(k, (-1, -1))   # never touched: still allocated, tiny lifetime
         sizes = {k: max(1, self.bufs[k].nbytes) for k in roots}
+        # general swapping across idle gaps (swap.plan_gap_swap): swap-managed
+        # buffers offloaded after their last touch before a gap and fetched
+        # back before the next, kept when that lowers the arena
+        self.gap_swaps = []
+        if swap and not any(ins[0] == N.RT_OP_HOOK for ins in low.prog):
+            from .swap import DEFAULT_SWAP_THRESHOLD, plan_gap_swap
+            thr = DEFAULT_SWAP_THRESHOLD if swap is True else int(swap)
+            ring = set(self.swap_plan.keys) if self.swap_plan is not None else set()
+            managed = [k for k in roots if k not in pinned and k not in ring and
+                       len(g.nodes[k[0]].domain) > 1 and sizes[k] >= thr]
+            folds = fold_slots(self.bufs, low.slot)
+
+            def lifetimes_of(p, ptrs):
+                lf = memplan.lifetimes(p, ptrs, key_of, pinned, folds,
+                                       hook_ptrs=memplan.hook_touches(p, low.hooks))
+                for k in roots:
+                    lf.setdefault(k, (-1, -1))
+                return lf
+
+            if managed:
+                chosen, _p, _r, glife = plan_gap_swap(low.prog, rec_ptrs, key_of, managed, sizes,
+                                                      life, memplan.assign, lifetimes_of)
+                if chosen:
+                    self.gap_swaps, life = chosen, glife
+                    self._gap_nrec = len(low.recs)
         offs, arena = memplan.assign(sizes, life)
         self.arena_bytes = arena
         self.naive_bytes = sum(sizes.values())
-        self.lifetimes = life
+        self.life_intervals = life
+        self.lifetimes = {k: (memplan._ivals(v)[0][0], memplan._ivals(v)[-1][1])
+                          for k, v in life.items()}
         self.trace_names = {k: g.nodes[k[0]].name for k in roots}
         with torch.cuda.device(self.dev):
             self.arena = torch.empty(max(1, arena), dtype=torch.uint8, device=self.dev)
@@ -908,6 +935,8 @@ class Executable:
                        absorbed=self.absorbed, shard=shard,
                        shard_reduce=self.shard_reduce,
                        persistent=OPTS["persistent"], swap=self.swap_plan).lower()
+        if self.gap_swaps:
+            self._apply_gap_swaps(low)
         self.hooks = low.hooks
         self.colls = None
         if getattr(comm, "native", False):
@@ -947,11 +976,39 @@ class Executable:
         self.prog = prog
         self.nprog = len(low.prog)
         self.env = (N.i64 * N.RT_MAXENV)()
+        self._low_kinds = [k for (k, *_r) in low.recs]
         self.launch_count = self._count_launches(low.prog)
         self.graph_exec = None
         self.graph_failed = False
         self._stage_in, self._stage_ev, self._stage_out = {}, {}, None
         self._pgraph, self._pgraph_failed = None, False
+
+    def _apply_gap_swaps(self, low):
+        """The chosen gap swaps on the real program: pinned host copies and
+        RT_K_MEMCPY records (offload, fetch per buffer, numbered as in the
+        planning pass) inserted at the planned top-level positions."""
+        from .swap import insert_instrs
+        torch = self.torch
+        if len(low.recs) != self._gap_nrec:
+            raise RuntimeError("gap swap: lowering passes disagree on the launch records")
+        self.gap_host = []
+        inserts = {}
+        for k, a, b in self.gap_swaps:
+            buf = self.bufs[k]
+            h = torch.empty(max(1, buf.nbytes), dtype=torch.uint8, pin_memory=True)
+            self.gap_host.append(h)
+            name = self.g.nodes[k[0]].name
+            for pos, d in ((a, 0), (b, 1)):
+                mp = N.rt_memcpy_params()
+                mp.h.status = self.status
+                mp.h.node = int(k[0])
+                mp.dst, mp.src = (h.data_ptr(), buf.ptr) if d == 0 else (buf.ptr, h.data_ptr())
+                mp.bytes, mp.dir = buf.nbytes, d
+                low.recs.append((N.RT_K_MEMCPY, mp, [1, 1, 1], [1, 1, 1], 0,
+                                 (-1, f"{name}:{'fetch' if d else 'offload'}")))
+                inserts.setdefault(pos, []).append((N.RT_OP_LAUNCH, len(low.recs) - 1, 0, 0, 0, 0))
+        low.prog = insert_instrs(low.prog, inserts)
+        self.gap_host_bytes = sum(h.numel() for h in self.gap_host)
 
     def _native_collectives(self, low):
         """All-reduce hooks -> in-program RT_OP_COLL instructions (csrc/coll.cu)
@@ -1047,7 +1104,7 @@ class Executable:
                 stack.append(trip)
             elif ins[0] == N.RT_OP_END:
                 stack.pop()
-            elif ins[0] == N.RT_OP_LAUNCH:
+            elif ins[0] == N.RT_OP_LAUNCH and self._low_kinds[ins[1]] != N.RT_K_MEMCPY:
                 total += prod(stack)
         return total
 
@@ -1642,7 +1699,7 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         from .shard import TorchComm
         comm = TorchComm()
     exe = Executable(h, benv, int(seed), dev, _input_sig(inputs), shard=shard, comm=comm,
-                     swap=swap if block else False)
+                     swap=swap)
     exe.plan_report = None
     if theta is not None or memops is not None:
         attach_plan_report(exe, theta, memops)
@@ -1701,7 +1758,8 @@ def attach_plan_report(exe, theta, memops):
     free, keeps the report in exe.plan_report."""
     from . import plancheck
     prog = [(exe.prog[i].op, exe.prog[i].a) for i in range(exe.nprog)]
-    swapped = exe.swap_plan.keys if exe.swap_plan is not None else ()
+    swapped = list(exe.swap_plan.keys) if exe.swap_plan is not None else []
+    swapped += [k for k, _, _ in getattr(exe, "gap_swaps", ())]
     exe.plan_report = plancheck.check(exe.g, exe.bufs, exe.labels, prog, exe.lifetimes,
                                       plancheck.fused_map(exe), theta, memops, swapped)
     return exe.plan_report
@@ -1718,10 +1776,14 @@ def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=
     (default: torch.distributed).
 
     block=(dim, bs): time-block the backward along dim (blocking.block_dim);
-    swap=True (with block): activations of the acting recurrence keep two
-    time blocks in HBM and are offloaded to / fetched from pinned host
-    memory per block (swap.py); an int is the swap threshold in bytes
-    (default 64 MiB, the reference's polysched.py:28).
+    swap=True: polysched's swap-managed tensors (multi-dim domain, at least
+    the threshold's bytes) move to pinned host memory where that lowers
+    peak HBM (swap.py): with block, activations of the acting recurrence
+    keep two time blocks in HBM and are offloaded / fetched per block; any
+    other such tensor is offloaded across an idle gap between its touches
+    and fetched back before its next reader (swap.plan_gap_swap).  An int
+    is the swap threshold in bytes (default 64 MiB, the reference's
+    polysched.py:28).
 
     theta / memops: polysched's ScheduleFn and MemOpSet for this graph
     (reference polysched.py:92-143, 842-859; `memops` may carry the

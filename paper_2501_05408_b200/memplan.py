@@ -113,16 +113,23 @@ def lifetimes(prog, rec_ptrs, key_of_ptr, pinned, folds=None, hook_ptrs=None):
     return out
 
 
+def _ivals(x):
+    """A lifetime: (lo, hi), or a list of them (a buffer swapped out across
+    an idle gap, swap.plan_gap_swap, is live in two intervals)."""
+    return [x] if isinstance(x, tuple) else list(x)
+
+
 def assign(sizes: dict, life: dict):
-    """Best-fit offsets for intervals; returns (offsets, arena bytes)."""
-    order = sorted(sizes, key=lambda k: (-sizes[k], life[k][0]))
-    placed = []   # (off, size, lo, hi)
+    """Best-fit offsets for interval lists; returns (offsets, arena bytes)."""
+    order = sorted(sizes, key=lambda k: (-sizes[k], _ivals(life[k])[0][0]))
+    placed = []   # (off, size, [(lo, hi)])
     offs = {}
     top = 0
     for k in order:
         sz = (sizes[k] + ALIGN - 1) // ALIGN * ALIGN
-        lo, hi = life[k]
-        busy = sorted((o, s) for (o, s, a, b) in placed if not (b < lo or hi < a))
+        mine = _ivals(life[k])
+        busy = sorted((o, s) for (o, s, iv) in placed
+                      if any(not (b < lo or hi < a) for lo, hi in mine for a, b in iv))
         best, cur = None, 0
         for o, s in busy:
             if o - cur >= sz and (best is None or (o - cur) < best[1]):
@@ -130,6 +137,6 @@ def assign(sizes: dict, life: dict):
             cur = max(cur, o + s)
         off = best[0] if best else cur
         offs[k] = off
-        placed.append((off, sz, lo, hi))
+        placed.append((off, sz, mine))
         top = max(top, off + sz)
     return offs, top

@@ -23,7 +23,7 @@ RT_KONST = 32
 RT_F64, RT_F32, RT_I64, RT_BOOL = 0, 1, 2, 3
 DTYPE_CODE = {"f64": RT_F64, "f32": RT_F32, "i64": RT_I64, "bool": RT_BOOL}
 
-RT_K_EW, RT_K_REDUCE, RT_K_SCAN, RT_K_GEMM, RT_K_RNG, RT_K_UDF, RT_K_SPLITK, RT_K_POLICY = \
+RT_K_EW, RT_K_REDUCE, RT_K_SCAN, RT_K_GEMM, RT_K_RNG, RT_K_UDF, RT_K_SPLITK, RT_K_MEMCPY = \
     1, 2, 3, 4, 5, 6, 7, 8
 RT_K_LOOP = 9
 RT_K_GEMM_TC = 10
@@ -85,6 +85,11 @@ class rt_scan_params(C.Structure):
                 ("in_", rt_view), ("out", rt_view), ("win", i32), ("tile", i32),
                 ("gae", i32), ("stages", i32), ("gae_c", f64), ("gae_vb", f64),
                 ("in2", rt_view)]
+
+
+class rt_memcpy_params(C.Structure):
+    _fields_ = [("h", rt_hdr), ("dst", u64), ("src", u64), ("bytes", i64), ("dir", i32),
+                ("_pad", i32)]
 
 
 class rt_gbox(C.Structure):

@@ -9,7 +9,7 @@ from . import native as N
 ITEM = {N.RT_F64: 8, N.RT_F32: 4, N.RT_I64: 8, N.RT_BOOL: 1}
 FAMILY = {N.RT_K_EW: "ew", N.RT_K_REDUCE: "reduce", N.RT_K_SCAN: "scan", N.RT_K_GEMM: "gemm",
           N.RT_K_RNG: "rng", N.RT_K_UDF: "udf", N.RT_K_SPLITK: "splitk",
-          N.RT_K_POLICY: "policy", N.RT_K_LOOP: "loop", N.RT_K_GEMM_TC: "gemm_tc",
+          N.RT_K_MEMCPY: "memcpy", N.RT_K_LOOP: "loop", N.RT_K_GEMM_TC: "gemm_tc",
           N.RT_K_THIN: "thin", N.RT_K_GEMM_TMA: "gemm_tma"}
 
 
@@ -36,6 +36,8 @@ def _gop_elems(o, Z, M, N_, role):
 
 def cost(kernel, p, loop_info=None):
     """(bytes, flops) for one launch of record params p."""
+    if kernel == N.RT_K_MEMCPY:
+        return int(p.bytes), 0
     if kernel == N.RT_K_LOOP:
         if not loop_info:
             return 0, 0

@@ -202,3 +202,157 @@ def N_prod(xs):
     for x in xs:
         out *= int(x)
     return out
+
+
+# ---------------------------------------------------------------------------
+# General swapping across idle gaps (polysched
+# `_swap_managed` :876-877, `augment_memory_ops` :936-1105).
+#
+# Any swap-managed buffer (a multi-dim domain and at least the threshold's
+# bytes, not an input/output) whose touches in the lowered program leave an
+# idle gap -- launches in between that neither read nor write it -- can be
+# moved to pinned host memory after its last touch before the gap (OFFLOAD)
+# and brought back before its next touch (FETCH).  Its arena range is then
+# free for other buffers during the gap, so the memory plan (memplan.assign
+# over interval LISTS) can place them there.  The copies are RT_K_MEMCPY
+# launch records on the program's stream: stream order IS polysched's `mem`
+# level (fetch < exec < offload < dealloc, `schedule_memory` :1116-1137), and
+# the program still captures into one CUDA graph.  A gap swap is kept only
+# if it lowers the arena (peak HBM); the cost is 2 x bytes over PCIe.
+
+
+def _segments(prog, touches):
+    """Top-level touch segments: a touch inside a loop counts as the whole
+    span of its outermost loop (insertion points must be at depth 0)."""
+    outer, stack = [], []
+    for pc, ins in enumerate(prog):
+        if ins[0] == N.RT_OP_FOR:
+            stack.append(pc)
+        elif ins[0] == N.RT_OP_END:
+            a = stack.pop()
+            if not stack:
+                outer.append((a, pc))
+    segs = set()
+    for pc in touches:
+        lo = hi = pc
+        for a, b in outer:
+            if a <= pc <= b:
+                lo, hi = a, b
+                break
+        segs.add((lo, hi))
+    out = []
+    for lo, hi in sorted(segs):
+        if out and lo <= out[-1][1] + 1:
+            out[-1] = (out[-1][0], max(out[-1][1], hi))
+        else:
+            out.append((lo, hi))
+    return out
+
+
+def key_touches(prog, rec_ptrs, key_of, hook_ptrs=None):
+    """key -> sorted pcs of the launches (and all-reduce hooks) touching it."""
+    hook_ptrs = hook_ptrs or {}
+    out = {}
+    for pc, ins in enumerate(prog):
+        if ins[0] == N.RT_OP_LAUNCH:
+            ptrs = rec_ptrs[ins[1]]
+        elif ins[0] == N.RT_OP_HOOK:
+            ptrs = {(q >> 44) << 44 for q in hook_ptrs.get(pc, ())}
+        else:
+            continue
+        for p in ptrs:
+            k = key_of.get(p)
+            if k is not None:
+                out.setdefault(k, []).append(pc)
+    return out
+
+
+def gap_candidates(prog, touches, managed):
+    """[(key, off_pos, fetch_pos)]: for each managed key, its largest idle
+    gap between two top-level touch segments that contains a launch.
+    off_pos / fetch_pos are instruction positions in `prog` (the offload is
+    inserted before off_pos, i.e. right after the earlier segment; the fetch
+    before fetch_pos, the start of the later one)."""
+    launches = [pc for pc, ins in enumerate(prog) if ins[0] == N.RT_OP_LAUNCH]
+    out = []
+    for k in managed:
+        segs = _segments(prog, touches.get(k, ()))
+        best = None
+        for (a0, a1), (b0, b1) in zip(segs, segs[1:]):
+            inside = sum(1 for pc in launches if a1 < pc < b0)
+            if inside and (best is None or b0 - a1 > best[1] - best[0]):
+                best = (a1 + 1, b0)
+        if best is not None:
+            out.append((k, best[0], best[1]))
+    return out
+
+
+def insert_instrs(prog, inserts):
+    """Insert instructions at top-level positions: inserts = {pos: [instr]}
+    (before the instruction at old position pos; pos == len(prog) appends).
+    FOR.e (pc after its END) and END.a (pc of its FOR) are remapped."""
+    shift, acc = [], 0
+    for pc in range(len(prog) + 1):
+        acc += len(inserts.get(pc, ()))
+        shift.append(acc)
+
+    def new(pc):            # new position of old instruction pc
+        return pc + shift[pc]
+
+    def target(pc):         # jump target: the first instruction inserted at pc, if any
+        return pc + (shift[pc - 1] if pc > 0 else 0)
+
+    out = []
+    for pc, ins in enumerate(prog):
+        out.extend(inserts.get(pc, ()))
+        ins = tuple(ins)
+        if ins[0] == N.RT_OP_FOR:
+            ins = ins[:5] + (target(ins[5]),)
+        elif ins[0] == N.RT_OP_END:
+            ins = (ins[0], new(ins[1])) + ins[2:]
+        out.append(ins)
+    out.extend(inserts.get(len(prog), ()))
+    return out
+
+
+def plan_gap_swap(prog, rec_ptrs, key_of, managed, sizes, base_life, assign, lifetimes_of):
+    """Greedy choice of gap swaps that lower the arena.  `lifetimes_of(prog,
+    rec_ptrs)` recomputes key -> (lo, hi) on a rewritten program; returns
+    (chosen [(key, off_pos, fetch_pos)], program, rec_ptrs, lifetimes) with
+    the chosen copies inserted as launch records numbered after the
+    existing ones (offload, fetch per key, in `chosen` order)."""
+    touches = key_touches(prog, rec_ptrs, key_of)
+    cands = gap_candidates(prog, touches, managed)
+    cands.sort(key=lambda c: -sizes[c[0]])
+    fake = {v: k for k, v in key_of.items()}
+    chosen = []
+
+    def build(sel):
+        inserts, ptrs = {}, list(rec_ptrs)
+        for k, a, b in sel:
+            ptrs.append({fake[k]})
+            inserts.setdefault(a, []).append((N.RT_OP_LAUNCH, len(ptrs) - 1, 0, 0, 0, 0))
+            ptrs.append({fake[k]})
+            inserts.setdefault(b, []).append((N.RT_OP_LAUNCH, len(ptrs) - 1, 0, 0, 0, 0))
+        p2 = insert_instrs(prog, inserts)
+        life = lifetimes_of(p2, ptrs)
+        # split lifetimes: live up to its offload, and again from its fetch
+        tl = key_touches(p2, ptrs, key_of)
+        for i, (k, a, b) in enumerate(sel):
+            off_rec, fetch_rec = len(rec_ptrs) + 2 * i, len(rec_ptrs) + 2 * i + 1
+            off_pc = [pc for pc, x in enumerate(p2) if x[0] == N.RT_OP_LAUNCH and x[1] == off_rec][0]
+            fe_pc = [pc for pc, x in enumerate(p2) if x[0] == N.RT_OP_LAUNCH and x[1] == fetch_rec][0]
+            lo, hi = life[k]
+            assert min(tl[k]) <= off_pc < fe_pc <= max(tl[k])
+            life[k] = [(lo, off_pc), (fe_pc, hi)]
+        return p2, ptrs, life
+
+    _, best = assign(sizes, base_life)
+    cur = (prog, rec_ptrs, base_life)
+    for c in cands:
+        trial = chosen + [c]
+        p2, ptrs, life = build(trial)
+        _, arena = assign(sizes, life)
+        if arena < best:
+            chosen, best, cur = trial, arena, (p2, ptrs, life)
+    return chosen, cur[0], cur[1], cur[2]

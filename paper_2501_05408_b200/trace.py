@@ -71,6 +71,12 @@ def trace(exe, max_lines=100000):
         elif op == N.RT_OP_ENVMOD:
             env[a] = env[b] % c
             pc += 1
+        elif op == N.RT_OP_LAUNCH and exe.kernels[a] == N.RT_K_MEMCPY:
+            # a gap swap (swap.plan_gap_swap): the whole buffer moves
+            name, what = exe.labels[a][1].rsplit(":", 1)
+            k = next(k for k in exe.trace_names if exe.trace_names[k] == name)
+            out.append(f"{'FETCH' if what == 'fetch' else 'OFFLOAD'} {name} {_full_points(exe, k)}")
+            pc += 1
         elif op == N.RT_OP_LAUNCH:
             label = exe.labels[a]
             nid = label[0]
@@ -125,14 +131,17 @@ def stats(exe):
     lines = trace(exe, max_lines=1 << 62) if exe.launch_count < 200000 else []
     n_exec = exe.launch_count
     swap = exe.swap_rt
+    gaps = getattr(exe, "gap_swaps", [])
+    gap_host = getattr(exe, "gap_host_bytes", 0)
     rep = {
         "peak_device_bytes": int(exe.peak_bytes),
         "arena_bytes": int(exe.arena_bytes),
         "naive_device_bytes": int(exe.naive_bytes),
-        "peak_host_bytes": int(swap.host_bytes) if swap else 0,
-        "offloads": (exe.swap_plan.DI * len(exe.swap_plan.keys)) if swap else 0,
-        "fetches": (exe.swap_plan.DI * len(exe.swap_plan.keys)) if swap else 0,
-        "bytes_moved": (2 * swap.host_bytes) if swap else 0,
+        "peak_host_bytes": (int(swap.host_bytes) if swap else 0) + int(gap_host),
+        "offloads": (exe.swap_plan.DI * len(exe.swap_plan.keys) if swap else 0) + len(gaps),
+        "fetches": (exe.swap_plan.DI * len(exe.swap_plan.keys) if swap else 0) + len(gaps),
+        "bytes_moved": (2 * swap.host_bytes if swap else 0) + 2 * int(gap_host),
+        "gap_swaps": [exe.trace_names[k] for k, _, _ in gaps],
         "execute_events": int(n_exec),
         "deallocations": sum(1 for x in lines if x.startswith("DEALLOC")),
         "static_estimate": static_estimate(exe),
