@@ -380,9 +380,11 @@ enum rt_op {
                        /* a swap copy): rt_run_segment returns RT_HOOK      */
                        /* with the next pc                                  */
   RT_OP_ENVMOD = 7,    /* env[a] = env[b] mod c (ring slot of a time block) */
-  RT_OP_COLL = 8       /* in-program collective a (rt_set_collectives): sum
+  RT_OP_COLL = 8,      /* in-program collective a (rt_set_collectives): sum
                           all-reduce of its slab on the program's stream;
                           captured into CUDA graphs like a launch */
+  RT_OP_ENVADD = 9     /* env[a] += b (a skewed schedule's lag around the
+                          lagged nodes of a band, planner.skew_steps)      */
 };
 
 /* A sum all-reduce of a slab of one buffer (a gradient summed over the

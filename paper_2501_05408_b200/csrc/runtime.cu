@@ -346,6 +346,12 @@ extern "C" int rt_run(const rt_instr* prog, int32_t nprog, const rt_launch_rec* 
         ++pc;
         break;
       }
+      case RT_OP_ENVADD: {
+        if (in.a < 0 || in.a >= nenv) return fail(RT_ERR_BAD_ARG, "bad envadd");
+        env[in.a] += in.b;
+        ++pc;
+        break;
+      }
       case RT_OP_COLL: {
         int rc = rt_coll_exec(in.a, env, nenv, stream);
         if (rc) return rc;
@@ -391,6 +397,11 @@ extern "C" int rt_run_segment(const rt_instr* prog, int32_t nprog, const rt_laun
         if (in.a < 0 || in.a >= nenv || in.b < 0 || in.b >= nenv || in.c <= 0)
           return fail(RT_ERR_BAD_ARG, "bad envmod");
         env[in.a] = env[in.b] % in.c;
+        ++pc;
+        break;
+      case RT_OP_ENVADD:
+        if (in.a < 0 || in.a >= nenv) return fail(RT_ERR_BAD_ARG, "bad envadd");
+        env[in.a] += in.b;
         ++pc;
         break;
       case RT_OP_COLL: {
@@ -586,6 +597,9 @@ extern "C" int rt_profile(const rt_instr* prog, int32_t nprog, const rt_launch_r
     } else if (in.op == RT_OP_ENVMOD) {
       if (in.c > 0 && in.a >= 0 && in.a < nenv && in.b >= 0 && in.b < nenv)
         env[in.a] = env[in.b] % in.c;
+      ++pc;
+    } else if (in.op == RT_OP_ENVADD) {
+      if (in.a >= 0 && in.a < nenv) env[in.a] += in.b;
       ++pc;
     } else if (in.op == RT_OP_COLL) {
       int rc = rt_coll_exec(in.a, env, nenv, stream);

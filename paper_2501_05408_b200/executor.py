@@ -669,14 +669,23 @@ OPTS = {"fuse": os.environ.get("RTB200_NOFUSE") != "1",
         "persistent": os.environ.get("RTB200_NOPERSIST") != "1"}
 
 
-def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
+def analyze(g: Graph, benv, pshape, fuse=True, fold=True, skew=None):
     """Plan the loop nest and decide aliases, contractions and fusions
-    (device-independent; the CPU tests run this directly)."""
+    (device-independent; the CPU tests run this directly).  skew = (dim,
+    {nid: lag}) from a polysched band schedule (schedule.band_lags) pipelines
+    the lagged nodes into the band's loop (planner.skew_steps)."""
     ext = {d: benv[g.dim_bound[d]] for d in g.dim_order}
     contract = find_contractions(g)
     virtual = set(contract.values())
     alias = find_aliases(g, pshape)
-    plan = Planner(g, benv).plan(getattr(g, "block_dims", ()))
+    planner = Planner(g, benv)
+    plan = planner.plan(getattr(g, "block_dims", ()))
+    lag_of = {}
+    if skew is not None:
+        from .planner import skew_steps
+        plan.steps = skew_steps(planner, plan.steps, skew[0], dict(skew[1]))
+        lag_of = getattr(planner, "lags", {})
+    plan.lags = lag_of
     fixed_of = plan_fixed(plan.steps)
     alias_nodes = {k[0] for k in alias}
     absorbed = find_absorbed_layouts(g, virtual | alias_nodes, set(contract.values())) \
@@ -713,14 +722,15 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True):
             bufs[key] = Buf(key, n.domain, tuple(ext[d] for d in n.domain), pshape[key],
                             n.out_dtypes[oid], alias.get(key))
     if fold:
-        for key, dims in find_folds(g, bufs, fixed_of, virtual, ext).items():
+        for key, dims in find_folds(g, bufs, fixed_of, virtual, ext, lag_of).items():
             bufs[key].folded = dims
     return {"contract": contract, "alias": alias, "plan": plan, "gemm_epi": gemm_epi,
             "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs, "absorbed": absorbed,
             "gae": gae}
 
 
-def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, depth=0):
+def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, depth=0,
+                       lag_of=None):
     """Edge e reads the producer's value made in the same iteration of the
     loop over d: the consumer's loops down to d are the producer's (same
     order), and it reads at its own index along every one of them (a read
@@ -730,6 +740,8 @@ def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, dept
     fixed_c = fixed_of.get(snk.id, ())
     if d not in fixed_c:
         return False
+    if lag_of and lag_of.get(snk.id, 0) != lag_of.get(e.src, 0):
+        return False          # a skewed consumer reads it in a later iteration
     k = fixed_c.index(d) + 1
     if tuple(fixed_p[:k]) != tuple(fixed_c[:k]):
         return False
@@ -748,12 +760,12 @@ def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, dept
         if depth > 32:
             return False
         return all(_read_in_iteration(g, f, d, fixed_p, snk.domain, fixed_of, virtual,
-                                      depth + 1)
+                                      depth + 1, lag_of)
                    for f in g.out_edges(snk.id))
     return True
 
 
-def find_folds(g: Graph, bufs, fixed_of, virtual, ext):
+def find_folds(g: Graph, bufs, fixed_of, virtual, ext, lag_of=None):
     """Storage contraction: a buffer whose every value is produced and
     consumed within one iteration of an enclosing loop over d keeps a
     single slot along d (the deallocate-after-last-use of
@@ -779,7 +791,8 @@ def find_folds(g: Graph, bufs, fixed_of, virtual, ext):
             for e in g.out_edges(m[0]):
                 if e.oid == m[1]:
                     ok = {d for d in ok if _read_in_iteration(
-                        g, e, d, fixed_of.get(r[0], ()), n.domain, fixed_of, virtual)}
+                        g, e, d, fixed_of.get(r[0], ()), n.domain, fixed_of, virtual,
+                        lag_of=lag_of)}
         if ok:
             for m in mem:
                 folds[m] = frozenset(ok)
@@ -809,7 +822,7 @@ def payload_shapes(g: Graph, benv):
 
 class Executable:
     def __init__(self, g: Graph, benv: dict, seed: int, device: int, input_sig, fuse=True,
-                 shard=None, comm=None, swap=False):
+                 shard=None, comm=None, swap=False, skew=None):
         torch = _torch()
         self.torch = torch
         self.g = g
@@ -830,7 +843,8 @@ class Executable:
         if shard is not None:
             from .shard import check_shardable
             self.shard_reduce = check_shardable(g, shard.dim, shard.also, benv)
-        an = analyze(g, benv, pshape, fuse and OPTS["fuse"], OPTS["fold"])
+        an = analyze(g, benv, pshape, fuse and OPTS["fuse"], OPTS["fold"], skew=skew)
+        self.skew = skew
         self.contract, self.plan, self.gemm_epi, self.fuse_src = (
             an["contract"], an["plan"], an["gemm_epi"], an["fuse_src"])
         self.absorbed = an["absorbed"]
@@ -1679,8 +1693,10 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         benv = _resolve_dynamic(graph, benv, dyn, inputs, seed, device)
     dev = torch.cuda.current_device() if device is None else int(device)
     block = tuple(block) if block else None
+    from .schedule import band_lags
+    skew = band_lags(theta, graph) if not block and shard is None else None
     key = (fingerprint(graph), tuple(sorted(benv.items())), int(seed), dev, _input_sig(inputs),
-           shard, block, swap, _knobs())
+           shard, block, swap, skew, _knobs())
     ex = _CACHE.get(key)
     if ex is not None:
         _CACHE.move_to_end(key)
@@ -1699,7 +1715,7 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
         from .shard import TorchComm
         comm = TorchComm()
     exe = Executable(h, benv, int(seed), dev, _input_sig(inputs), shard=shard, comm=comm,
-                     swap=swap)
+                     swap=swap, skew=skew)
     exe.plan_report = None
     if theta is not None or memops is not None:
         attach_plan_report(exe, theta, memops)
@@ -1787,10 +1803,13 @@ def execute(g, bounds=None, inputs=None, seed=0, return_bounds=False, *, device=
 
     theta / memops: polysched's ScheduleFn and MemOpSet for this graph
     (reference polysched.py:92-143, 842-859; `memops` may carry the
-    donation_analysis dict as `.donations`).  The executor runs its own plan;
-    these are checked against it (plancheck.py: deallocation never before
-    polysched's last consumer, swap set, donations) and the report is kept
-    on the executable (get_executable(...)[0].plan_report)."""
+    donation_analysis dict as `.donations`).  A band schedule with constant
+    skews (e.g. nstep targets at t + n - 1) is realised as a software
+    pipeline (schedule.band_lags, planner.skew_steps); otherwise the
+    executor runs its own plan.  Either way the plan is checked against
+    them (plancheck.py: deallocation never before polysched's last
+    consumer, swap set, donations) and the report is kept on the executable
+    (get_executable(...)[0].plan_report)."""
     exe, benv = get_executable(g, bounds, inputs, seed, device, shard, comm, block, swap,
                                theta, memops)
     exe.run(inputs or {}, stream)

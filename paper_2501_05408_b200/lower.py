@@ -25,7 +25,7 @@ import numpy as np
 
 from . import ir
 from . import native as N
-from .planner import INF, Bulk, Loop, interval, subst_bounds
+from .planner import INF, Bulk, Loop, Shift, interval, subst_bounds
 
 
 class LowerError(Exception):
@@ -539,8 +539,18 @@ class Lowering:
         for s in steps:
             if isinstance(s, Bulk):
                 self.bulk(s)
+            elif isinstance(s, Shift):
+                self.shift(s)
             else:
                 self.loop(s)
+
+    def shift(self, s: Shift):
+        """Lagged nodes of a skewed band (planner.skew_steps): the loop
+        index minus k while they launch (launches fold env when issued)."""
+        slot = self.slot[s.dim]
+        self.prog.append((N.RT_OP_ENVADD, slot, -s.k, 0, 0, 0))
+        self.steps(s.body)
+        self.prog.append((N.RT_OP_ENVADD, slot, s.k, 0, 0, 0))
 
     # -- persistent loops ------------------------------------------------------
 

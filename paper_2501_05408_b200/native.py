@@ -37,6 +37,7 @@ TMA_THREADS_P = 128 + 64 + 256
 TC_SMEM = 2 * (2 * 128 * 32 * 4 + 2 * 256 * 32 * 4)
 
 RT_OP_LAUNCH, RT_OP_FOR, RT_OP_END, RT_OP_EVENT, RT_OP_HOOK, RT_OP_ENVMOD = 1, 2, 3, 4, 6, 7
+RT_OP_ENVADD = 9
 RT_OP_COLL = 8
 RT_HOOK = 100
 

@@ -54,11 +54,12 @@ def check(g, bufs, labels, prog, lifetimes, fused_into, theta=None, memops=None,
     pcs = _node_launch_pcs(prog, labels, g, fused_into)
     rep = {}
     if theta is not None:
-        lv = []
-        for lev in theta.levels:
-            lv.append(lev[0] if lev[0] != "band" else f"band({getattr(lev[1], 'name', lev[1])})")
-        rep["theta_levels"] = lv
-        rep["theta_nodes"] = len(theta.rows)
+        from .schedule import _levels, _rows, band_lags
+        rep["theta_levels"] = [lev[0] if lev[0] != "band" else f"band({lev[1]})"
+                               for lev in _levels(theta)]
+        rep["theta_nodes"] = len(_rows(theta))
+        sk = band_lags(theta, g)
+        rep["theta_skew"] = {names.get(k, str(k)): c for k, c in sk[1] if c} if sk else {}
     if memops is None:
         return rep
     root = {}

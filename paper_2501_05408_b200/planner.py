@@ -165,6 +165,15 @@ class Loop:
 
 
 @dataclass
+class Shift:
+    """Inside a loop over `dim`: evaluate `body` at dim = (loop index) - k
+    (a skewed schedule's lag; lowered as env adds around the body)."""
+    dim: str
+    k: int
+    body: list = field(default_factory=list)
+
+
+@dataclass
 class Plan:
     graph: Graph
     benv: dict            # bound name -> int
@@ -451,6 +460,10 @@ def group_block_loop(steps, g: Graph, kb: str):
 def describe(steps, g: Graph, indent=0) -> str:
     out = []
     for s in steps:
+        if isinstance(s, Shift):
+            out.append("  " * indent + f"at {s.dim} - {s.k}:")
+            out.append(describe(s.body, g, indent + 1))
+            continue
         if isinstance(s, Bulk):
             n = g.nodes[s.nid]
             free = [d for d in n.domain if d not in s.fixed]
@@ -460,3 +473,105 @@ def describe(steps, g: Graph, indent=0) -> str:
             out.append("  " * indent + f"for {s.dim} {'asc' if s.step > 0 else 'desc'}{rng}:")
             out.append(describe(s.body, g, indent + 1))
     return "\n".join(out)
+
+
+# ---------------------------------------------------------------------------
+# skewed pipelines (a polysched band schedule with constant skews)
+
+
+def _max_ahead(planner: "Planner", e, d: str):
+    """Largest src_d - snk_d an edge reads (None: vacuous).  Interval
+    arithmetic loses the correlation in windows like r[t : min(t+2, T)]
+    (it gives 7 at T = 8), so the loop dim is enumerated point by point
+    when its extent is small."""
+    dist = planner.distance(e, d)
+    if dist is None or dist[1] <= 0:
+        return None if dist is None else dist[1]
+    src, snk = planner.g.nodes[e.src], planner.g.nodes[e.sink]
+    box = planner.sink_box(e)
+    if box is None or d not in snk.domain or d not in src.domain or \
+            box[d][1] - box[d][0] > (1 << 16):
+        return dist[1]
+    c = subst_bounds(e.phi[src.domain.index(d)], planner.benv)
+    hi_e = ("sub", c[2], ("int", 1)) if c[0] == "slice" else c
+    best = None
+    for t in range(int(box[d][0]), int(box[d][1]) + 1):
+        b2 = dict(box)
+        b2[d] = (t, t)
+        v = interval(("sub", hi_e, ("sym", d, "loop")), b2)[1]
+        best = v if best is None else max(best, v)
+    return best
+
+
+def skew_steps(planner: "Planner", steps, d: str, lags: dict):
+    """Realise a band schedule over d with constant skews (reference
+    polysched.py:546-612; e.g. nstep2: s, r at t and the window target g, d
+    at t + 1): the top-level recurrence loop over d and
+    the bulk steps after it whose nodes the schedule places in the same band
+    at d + c (c = lags[nid] >= 0) become ONE loop over the band index tau in
+    [0, T + K): the recurrence body at d = tau (tau < T), then every lagged
+    node at d = tau - c (0 <= tau - c < T) in plan order.  The steady range
+    tau in [K, T) is one loop; the first and last K iterations are peeled
+    (the SPEC's "window skew guard peeled for first n iterations",
+    SPEC.md:494, 503).  Valid when every dependence of a lagged node on the
+    band's nodes reads at most c - c_src ahead along d; else the steps are
+    returned unchanged (the executor's own dependence order)."""
+    g, ext = planner.g, planner.ext
+    T = ext.get(d, 0)
+    idx = [i for i, st in enumerate(steps) if isinstance(st, Loop) and st.dim == d and
+           not st.fixed and st.lo is None and st.step == 1]
+    if not idx or T <= 0:
+        return steps
+    i = idx[0]
+    L = steps[i]
+    band = dict.fromkeys(_step_nodes(L), 0)
+    if any(lags.get(v, 0) != 0 for v in band if d in g.nodes[v].domain):
+        return steps
+    cands, late, rest = [], set(), []
+    for st in steps[i + 1:]:
+        nodes = _step_nodes(st)
+        ins = [e for v in nodes for e in g.in_edges(v)]
+        if isinstance(st, Bulk) and d in g.nodes[st.nid].domain and st.nid in lags and \
+                lags[st.nid] >= 0 and not any(e.src in late for e in ins):
+            c = lags[st.nid]
+            ok = True
+            for e in ins:
+                if e.src in band:
+                    ahead = _max_ahead(planner, e, d)
+                    if ahead is not None and ahead > c - band[e.src]:
+                        ok = False
+                        break
+            if ok:
+                band[st.nid] = c
+                cands.append(st)
+                continue
+        late |= nodes
+        rest.append(st)
+    if not cands or not any(band[st.nid] > 0 for st in cands):
+        return steps
+    K = max(band[st.nid] for st in cands)
+
+    def items(tau):
+        out = list(L.body) if tau is None or tau < T else []
+        for st in cands:
+            c = band[st.nid]
+            if tau is not None and not (0 <= tau - c < T):
+                continue
+            b = Bulk(st.nid, (d,))
+            if c == 0:
+                out.append(b)
+            elif out and isinstance(out[-1], Shift) and out[-1].k == c:
+                out[-1].body.append(b)
+            else:
+                out.append(Shift(d, c, [b]))
+        return out
+
+    loops = []
+    for tau in range(0, min(K, T)):
+        loops.append(Loop(d, 1, items(tau), (), tau, tau + 1))
+    if K < T:
+        loops.append(Loop(d, 1, items(None), (), K, T))
+    for tau in range(max(K, T), T + K):
+        loops.append(Loop(d, 1, items(tau), (), tau, tau + 1))
+    planner.lags = dict(band)
+    return steps[:i] + loops + rest

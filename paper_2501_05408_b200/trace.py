@@ -71,6 +71,9 @@ def trace(exe, max_lines=100000):
         elif op == N.RT_OP_ENVMOD:
             env[a] = env[b] % c
             pc += 1
+        elif op == N.RT_OP_ENVADD:
+            env[a] += b
+            pc += 1
         elif op == N.RT_OP_LAUNCH and exe.kernels[a] == N.RT_K_MEMCPY:
             # a gap swap (swap.plan_gap_swap): the whole buffer moves
             name, what = exe.labels[a][1].rsplit(":", 1)
