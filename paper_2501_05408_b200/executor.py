@@ -254,11 +254,49 @@ def simplify_guards(g: Graph, benv):
 
 def prepare(g: Graph, benv):
     """Per-bounds graph preparation before planning: inline `dataflow`
-    groups, drop provably-true guards, remove dead nodes."""
+    groups, drop provably-true guards, read through pass-through nodes,
+    remove dead nodes."""
     inline_dataflow(g, benv)
     simplify_guards(g, benv)
+    bypass_pass_through(g)
     eliminate_dead(g)
     return g
+
+
+def bypass_pass_through(g: Graph):
+    """Consumers of a pass-through node -- a merge whose one condition is
+    `true` (the symbolic backward's gradient accumulators with a single
+    contribution, reference frontend.py) or identity / detach (runtime.py:
+    253-254) -- read its producer directly when the node is the identity on
+    the producer's points (same domain, payload and dtype).  The node then
+    has no readers and is removed as dead unless it is an output, so the
+    producer and the real consumer become adjacent for the fusion rules
+    (e.g. d(h2) = (dmu W3^T + dV Wv^T) * (1 - h2*h2): the add fuses into the
+    gate's elementwise launch instead of round-tripping HBM)."""
+    out_ids = {nid for _, nid, _ in g.outputs}
+    changed = False
+    for m in g.sorted_nodes():
+        if m.id in out_ids:
+            continue
+        ok = m.kind in IDENTITY_KINDS or (
+            m.kind == "merge" and len(m.params.get("conds", ())) == 1 and
+            m.params["conds"][0] == ir.TRUE)
+        ins = g.in_edges(m.id)
+        if not ok or len(ins) != 1:
+            continue
+        e = ins[0]
+        src = g.nodes[e.src]
+        if not _is_identity(e, src, m) or src.out_dtypes[e.oid] != m.dtype or \
+                tuple(src.out_shapes[e.oid]) != tuple(m.out_shapes[0]):
+            continue
+        outs = list(g.out_edges(m.id))
+        if not outs:
+            continue
+        for f in outs:
+            f.src, f.oid = e.src, e.oid
+        changed = True
+        g.invalidate()
+    return changed
 
 
 def copy_graph(g: Graph) -> Graph:
@@ -722,15 +760,42 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True, skew=None):
             bufs[key] = Buf(key, n.domain, tuple(ext[d] for d in n.domain), pshape[key],
                             n.out_dtypes[oid], alias.get(key))
     if fold:
-        for key, dims in find_folds(g, bufs, fixed_of, virtual, ext, lag_of).items():
+        loops_of = plan_loops(plan.steps)
+        for key, dims in find_folds(g, bufs, fixed_of, virtual, ext, lag_of, loops_of).items():
             bufs[key].folded = dims
     return {"contract": contract, "alias": alias, "plan": plan, "gemm_epi": gemm_epi,
             "fuse_src": fuse_src, "virtual": virtual, "bufs": bufs, "absorbed": absorbed,
             "gae": gae}
 
 
+def plan_loops(steps, path=(), out=None):
+    """nid -> set of enclosing-loop paths (tuples of (id(Loop), dim)), one per
+    place the node is evaluated: two sibling loops over the same dim are
+    different loops (a value made in one is not 'this iteration' in the
+    other)."""
+    out = {} if out is None else out
+    from .planner import Bulk, Loop
+    for st in steps:
+        if isinstance(st, Bulk):
+            out.setdefault(st.nid, set()).add(path)
+        elif isinstance(st, Loop):
+            plan_loops(st.body, path + ((id(st), st.dim),), out)
+        else:
+            plan_loops(st.body, path, out)
+    return out
+
+
+def _loop_prefix(paths, d):
+    """The enclosing loops down to (and including) the innermost loop over d."""
+    res = set()
+    for p in paths:
+        k = max((i for i, (_, dim) in enumerate(p) if dim == d), default=-1)
+        res.add(p[:k + 1])
+    return frozenset(res)
+
+
 def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, depth=0,
-                       lag_of=None):
+                       lag_of=None, loops_of=None):
     """Edge e reads the producer's value made in the same iteration of the
     loop over d: the consumer's loops down to d are the producer's (same
     order), and it reads at its own index along every one of them (a read
@@ -742,6 +807,9 @@ def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, dept
         return False
     if lag_of and lag_of.get(snk.id, 0) != lag_of.get(e.src, 0):
         return False          # a skewed consumer reads it in a later iteration
+    if loops_of is not None and snk.id not in virtual and \
+            _loop_prefix(loops_of.get(snk.id, ()), d) != _loop_prefix(loops_of.get(e.src, ()), d):
+        return False          # a sibling loop over d: not the same iteration
     k = fixed_c.index(d) + 1
     if tuple(fixed_p[:k]) != tuple(fixed_c[:k]):
         return False
@@ -760,12 +828,12 @@ def _read_in_iteration(g: Graph, e, d, fixed_p, src_dom, fixed_of, virtual, dept
         if depth > 32:
             return False
         return all(_read_in_iteration(g, f, d, fixed_p, snk.domain, fixed_of, virtual,
-                                      depth + 1, lag_of)
+                                      depth + 1, lag_of, loops_of)
                    for f in g.out_edges(snk.id))
     return True
 
 
-def find_folds(g: Graph, bufs, fixed_of, virtual, ext, lag_of=None):
+def find_folds(g: Graph, bufs, fixed_of, virtual, ext, lag_of=None, loops_of=None):
     """Storage contraction: a buffer whose every value is produced and
     consumed within one iteration of an enclosing loop over d keeps a
     single slot along d (the deallocate-after-last-use of
@@ -792,7 +860,7 @@ def find_folds(g: Graph, bufs, fixed_of, virtual, ext, lag_of=None):
                 if e.oid == m[1]:
                     ok = {d for d in ok if _read_in_iteration(
                         g, e, d, fixed_of.get(r[0], ()), n.domain, fixed_of, virtual,
-                        lag_of=lag_of)}
+                        lag_of=lag_of, loops_of=loops_of)}
         if ok:
             for m in mem:
                 folds[m] = frozenset(ok)

@@ -225,7 +225,12 @@ def test_time_blocking_shrinks_long_horizon_plan():
     txt = P.describe(an["plan"].steps, h)
     assert "for t_blk asc:" in txt
     folded = [k for k, b in an["bufs"].items() if "t_blk" in b.folded]
-    assert len(folded) >= 20
+    assert len(folded) >= 15
+    # every block-chain buffer of real size keeps one block of storage
+    roots = [k for k, b in an["bufs"].items() if b.alias is None and k[0] not in an["virtual"]]
+    big = [k for k in roots if "t_blk" in an["bufs"][k].dims and
+           "t_blk" not in an["bufs"][k].folded and an["bufs"][k].nbytes > 16 << 20]
+    assert not big, big
     assert an["bufs"][[k for k in an["bufs"] if h.nodes[k[0]].name == "v126"][0]].nbytes \
         == 256 * 10000 * 256 * 4
 
