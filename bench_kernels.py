@@ -77,6 +77,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--only", default=None)
+    ap.add_argument("--envs", type=int, default=None, help="override E of the scan programs")
     args = ap.parse_args()
     import torch
     from golden_cases import load_graph
@@ -85,6 +86,9 @@ def main():
     for name, (graph, bounds, algo) in CASES.items():
         if args.only and name != args.only:
             continue
+        if args.envs and "B" in bounds and name != "gather_mb":
+            bounds = dict(bounds, B=args.envs)
+            algo = algo // E * args.envs
         g = load_graph(graph)
         gen = torch.Generator(device="cuda").manual_seed(0)
         inputs = {}

@@ -277,6 +277,11 @@ typedef struct {
   uint64_t part;
   rt_gop X, Y, C, bias;
   rt_gbox W;           /* variant 3: decomposition of w (nd == 0: flat) */
+  /* variant 2 + gate with k2 > 0: a second narrow-K product over the same
+   * rows added before the gate, C = (X Y + X2 Y2) * (1 - h*h) (the sum of
+   * two heads' backward into one hidden layer, executor.find_gate_epilogues) */
+  int64_t k2;
+  rt_gop X2, Y2;
 } rt_thin_params;
 
 /* Point coordinates for per-point entropy: coordinate j of the node's

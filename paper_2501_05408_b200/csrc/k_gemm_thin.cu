@@ -21,6 +21,8 @@ constexpr int KT = 64;
 RT_DEV float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 RT_DEV double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 RT_DEV float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+RT_DEV float add_rn(float a, float b) { return __fadd_rn(a, b); }
+RT_DEV double add_rn(double a, double b) { return __dadd_rn(a, b); }
 RT_DEV double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
 // offset of flat row index `flat` over box b (nd <= 1: flat * s[0])
@@ -93,7 +95,10 @@ __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant
 // a shared-memory tile, stores are coalesced along r.
 // GATE: the epilogue-2 instantiation (its 16-row h prefetch is kept out of
 // the plain kernel's register budget)
-template <typename T, int KP, bool GATE = false>
+// KP2 > 0 (GATE only): a second product X2 Y2 (K2 <= KP2) summed before the
+// gate, in the reference's order: a = X Y, b = X2 Y2, then a + b, then the
+// gate (the PPO trunk's d(h2) = (dmu W3^T + dV Wv^T) * (1 - h2*h2)).
+template <typename T, int KP, bool GATE = false, int KP2 = 0>
 __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__ rt_thin_params p) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   constexpr int RT = 64;  // rows per tile
@@ -101,6 +106,8 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
   T* ys = (T*)sm_raw;             // [KP][R]
   T* xs = ys + KP * R;            // [RT][KP]
   T* bs = xs + RT * KP;           // [R]
+  T* ys2 = bs + R;                // KP2: [KP2][R]
+  T* xs2 = ys2 + KP2 * R;         // KP2: [RT][KP2]
   __shared__ int64_t coff[RT];    // output row offsets of the tile
   const T* X = (const T*)p.X.ptr + p.X.off;
   const T* Y = (const T*)p.Y.ptr + p.Y.off;
@@ -108,6 +115,15 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
   for (int i = threadIdx.x; i < KP * R; i += THREADS) {
     const int k = i / R, r = i - k * R;
     ys[i] = k < K ? Y[k * p.Y.s1[0] + r * p.Y.s2[0]] : (T)0;
+  }
+  const int K2 = (int)p.k2;
+  const T* X2 = KP2 ? (const T*)p.X2.ptr + p.X2.off : nullptr;
+  if constexpr (KP2 > 0) {
+    const T* Y2 = (const T*)p.Y2.ptr + p.Y2.off;
+    for (int i = threadIdx.x; i < KP2 * R; i += THREADS) {
+      const int k = i / R, r = i - k * R;
+      ys2[i] = k < K2 ? Y2[k * p.Y2.s1[0] + r * p.Y2.s2[0]] : (T)0;
+    }
   }
   // epilogue 2 (tanh-VJP gate, executor.find_gate_epilogues): C = acc * (1 - h*h)
   // with h in the bias slot, laid out exactly like C; no bias then
@@ -131,12 +147,21 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
       const T* xr = X + wdec(p.W, w, p.X.s2);
 #pragma unroll
       for (int k = 0; k < KP; ++k) xs[rr * KP + k] = (rr < nrow && k < K) ? __ldcs(xr + k * xk) : (T)0;
+      if constexpr (KP2 > 0) {
+        const T* xr2 = X2 + wdec(p.W, w, p.X2.s2);
+#pragma unroll
+        for (int k = 0; k < KP2; ++k)
+          xs2[rr * KP2 + k] = (rr < nrow && k < K2) ? __ldcs(xr2 + k * p.X2.s1[0]) : (T)0;
+      }
     }
     __syncthreads();
     for (int r = threadIdx.x; r < R; r += THREADS) {
       T yreg[KP];
 #pragma unroll
       for (int k = 0; k < KP; ++k) yreg[k] = ys[k * R + r];
+      T yreg2[KP2 > 0 ? KP2 : 1];
+#pragma unroll
+      for (int k = 0; k < KP2; ++k) yreg2[k] = ys2[k * R + r];
       const T b = bs[r];
       T* cbase = Cp + r * cr;
       if constexpr (GATE) {
@@ -154,6 +179,12 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
             T a = (T)0;
 #pragma unroll
             for (int k = 0; k < KP; ++k) a = fma(xs[rr * KP + k], yreg[k], a);
+            if constexpr (KP2 > 0) {
+              T b = (T)0;
+#pragma unroll
+              for (int k = 0; k < KP2; ++k) b = fma(xs2[rr * KP2 + k], yreg2[k], b);
+              a = add_rn(a, b);
+            }
             // numpy order, no contraction: gy * (1 - h*h)
             __stcs(cbase + coff[rr], mul_rn(a, sub_rn((T)1, mul_rn(hv[u], hv[u]))));
           }
@@ -313,6 +344,18 @@ extern "C" void* rt_kernel_thin_rows(int f64, int r, int k) {
 }
 
 extern "C" void* rt_kernel_thin(int variant, int f64, int r) {
+  if (variant == 5) {
+    // variant 2 + gate + a second product with K2 <= 4 (runtime.cu passes 5)
+    if (f64) {
+      if (r <= 4) return (void*)k_thin_smallk<double, 4, true, 4>;
+      if (r <= 8) return (void*)k_thin_smallk<double, 8, true, 4>;
+      return nullptr;
+    }
+    if (r <= 4) return (void*)k_thin_smallk<float, 4, true, 4>;
+    if (r <= 8) return (void*)k_thin_smallk<float, 8, true, 4>;
+    if (r <= 16) return (void*)k_thin_smallk<float, 16, true, 4>;
+    return nullptr;
+  }
   if (variant == 4) {
     // variant 2 with the tanh-VJP gate epilogue (runtime.cu passes 4)
     if (f64) {

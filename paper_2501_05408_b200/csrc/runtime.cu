@@ -177,7 +177,13 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_gop(p->C, env, nenv);
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
       if (p->variant == 3) return rt_kernel_thin_rows(p->f64, (int)p->r, (int)p->k);
-      // variant 2 with epilogue 2 (gate) is a separate instantiation ("4")
+      // variant 2 with epilogue 2 (gate) is a separate instantiation ("4"),
+      // with a second summed product ("5")
+      if (p->variant == 2 && p->k2 > 0) {
+        fold_gop(p->X2, env, nenv);
+        fold_gop(p->Y2, env, nenv);
+        return p->epilogue == 2 && p->k2 <= 4 ? rt_kernel_thin(5, p->f64, (int)p->k) : nullptr;
+      }
       return rt_kernel_thin(p->variant == 2 && p->epilogue == 2 ? 4 : p->variant, p->f64,
                             (int)(p->variant == 2 ? p->k : p->r));
     }

@@ -469,6 +469,41 @@ def find_gate_epilogues(g: Graph, pshape, fixed_of, skip, ext):
         if e is None:
             continue
         y = g.nodes[e.sink]
+        two = ()
+        if y.kind == "add" and y.id not in skip and y.id not in out_ids and y.dtype == x.dtype \
+                and pshape[(y.id, 0)] == xs and len(g.in_edges(y.id)) == 2 and \
+                _is_identity(e, x, y):
+            # (X Y + X2 Y2) * (1 - h*h): a second narrow-K product summed in
+            # (two heads' backward into one hidden layer); registered from
+            # the lower-id product
+            oth = g.in_edges(y.id)[1 - e.iid]
+            x2 = g.nodes[oth.src]
+            c2 = _single_identity_consumer(g, x2.id, out_ids)
+            if x2.kind != "matmul" or x2.id in skip or x2.id in out_ids or x2.id < x.id or \
+                    x2.dtype != x.dtype or pshape[(x2.id, 0)] != xs or c2 is None or \
+                    c2.sink != y.id or not _is_identity(oth, x2, y):
+                continue
+            a2 = [q for q in g.in_edges(x2.id) if q.iid == 0]
+            sh2 = pshape[(a2[0].src, a2[0].oid)] if a2 else ()
+            if not sh2 or sh2[-1] > 4:
+                continue
+            add_id, cur = y.id, y
+            while True:
+                e = _single_identity_consumer(g, cur.id, out_ids)
+                if e is None:
+                    break
+                nx = g.nodes[e.sink]
+                if nx.kind == "merge" and nx.params["conds"] == (ir.TRUE,) and \
+                        len(g.in_edges(nx.id)) == 1 and nx.dtype == x.dtype and \
+                        pshape[(nx.id, 0)] == xs and nx.id not in skip:
+                    chain.append(nx.id)
+                    cur = nx
+                    continue
+                break
+            if e is None:
+                continue
+            y = g.nodes[e.sink]
+            two = (add_id, x2.id)
         ins = g.in_edges(y.id)
         if y.kind != "mul" or y.dtype != x.dtype or len(ins) != 2 or pshape[(y.id, 0)] != xs:
             continue
@@ -491,7 +526,7 @@ def find_gate_epilogues(g: Graph, pshape, fixed_of, skip, ext):
         if not all(_is_identity(q, h, mn) for q in m_in) or \
                 pshape[(h.id, m_in[0].oid)] != xs or h.out_dtypes[m_in[0].oid] != x.dtype:
             continue
-        if len({fixed_of.get(k) for k in (x.id, y.id, sn.id, mn.id)}) != 1:
+        if len({fixed_of.get(k) for k in (x.id, y.id, sn.id, mn.id) + two}) != 1:
             continue
         # the narrow-K thin kernel must be the one that runs (lower._gemm_smallk)
         xa = g.in_edges(x.id)
@@ -511,9 +546,11 @@ def find_gate_epilogues(g: Graph, pshape, fixed_of, skip, ext):
         # real contraction (lower.TC_MIN_MACS), one K pass (no split-K)
         tma = x.dtype == "f32" and k >= 64 and rows >= 64 and xs[1] >= 16 and \
             rows * xs[1] * k >= (1 << 26) and k <= 256     # one TMEM chunk (no drain)
+        if two and not (thin and k <= (8 if x.dtype == "f64" else 16)):
+            continue                # the summed form exists only in the small-K kernel
         if not (thin or tma):
             continue
-        res[y.id] = (x.id, tuple(chain), sn.id, mn.id, m_in[0])
+        res[y.id] = (x.id, tuple(chain), sn.id, mn.id, m_in[0]) + two
     return res
 
 
@@ -737,9 +774,9 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True, skew=None):
             taken.add(g.in_edges(f)[0].src)
     gates = find_gate_epilogues(g, pshape, fixed_of, taken - alias_nodes, ext) \
         if fuse and GATE_ENABLED else {}
-    for y_, (x_, _ch, s_, m_, _he) in gates.items():
-        gemm_epi[y_] = (x_, None, ("gate", s_, m_, _he))
-        taken |= {y_, x_, s_, m_}
+    for y_, (x_, _ch, s_, m_, _he, *two) in gates.items():
+        gemm_epi[y_] = (x_, None, ("gate", s_, m_, _he, *two))
+        taken |= {y_, x_, s_, m_} | set(two)
     gae = find_gae_fusions(g, benv, alias, {nid for _, nid, _ in g.outputs}) if fuse else {}
     for info in gae.values():
         taken |= info["nodes"]
@@ -750,7 +787,7 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True, skew=None):
     for f, (x, _b, t) in gemm_epi.items():
         virtual.add(x)
         if isinstance(t, tuple):
-            virtual |= {t[1], t[2]}
+            virtual |= {t[1], t[2]} | set(t[4:6])
         elif t:
             virtual.add(g.in_edges(f)[0].src)
     bufs = {}

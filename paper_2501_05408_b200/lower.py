@@ -292,6 +292,8 @@ class Lowering:
         self.rec_cluster = {}                  # launch record -> cluster size (pair loops)
         self.swap = swap                       # swap.SwapPlan (time-blocked swapping)
         self._capture = None
+        self._smallk_capture = None            # dual gate: the second product's thin params
+        self._smallk_second = None
         self.loop_subs = {}                    # loop record -> sub-op descriptors
         self.fuse_src = dict(fuse_src or {})   # producer nid -> consumer nid (inlined)
         self.gemm_epi = dict(gemm_epi or {})   # final nid -> (matmul nid, bias edge, tanh)
@@ -301,7 +303,7 @@ class Lowering:
         for f, (x, _b, t) in self.gemm_epi.items():
             self.virtual.add(x)
             if isinstance(t, tuple):           # tanh-VJP gate: (1 - h*h) chain
-                self.virtual |= {t[1], t[2]}
+                self.virtual |= {t[1], t[2]} | set(t[4:6])   # (+ the summed second product)
             elif t:
                 self.virtual.add(self.g.in_edges(f)[0].src)
         self.launches_per_kernel = {}
@@ -982,7 +984,23 @@ class Lowering:
             return
         if n.id in self.gemm_epi:
             x, bias_e, tanh = self.gemm_epi[n.id]
-            if isinstance(tanh, tuple):
+            if isinstance(tanh, tuple) and len(tanh) > 4:
+                # (X Y + X2 Y2) * (1 - h*h): lower the second product for its
+                # operands only, then the first with it attached (one launch)
+                self._smallk_capture = []
+                try:
+                    self.k_matmul(ctx, self.g.nodes[tanh[5]], None, 2, gate_edge=tanh[3])
+                    if len(self._smallk_capture) != 1:
+                        raise LowerError(f"{n.name}: second gated product is not small-K")
+                    qb = self._smallk_capture[0]
+                finally:
+                    self._smallk_capture = None
+                self._smallk_second = qb
+                try:
+                    self.k_matmul(ctx, self.g.nodes[x], None, 2, gate_edge=tanh[3])
+                finally:
+                    self._smallk_second = None
+            elif isinstance(tanh, tuple):
                 self.k_matmul(ctx, self.g.nodes[x], None, 2, gate_edge=tanh[3])
             else:
                 self.k_matmul(ctx, self.g.nodes[x], bias_e, 1 if tanh else 0)
@@ -1928,6 +1946,8 @@ class Lowering:
             if not self._capture_active() and self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
                                                               epilogue, None, gate=gate):
                 return
+            if self._smallk_capture is not None or self._smallk_second is not None:
+                raise LowerError(f"{label[1]}: summed gated products need the small-K kernel")
             if not self._capture_active() and self.use_tc and self._tc_ok(p, A, B, Cc) and \
                     self.use_tma and self._tma_ok(p) and p.k <= N.TMA_DRAIN_K and not accumulate:
                 g = N.rt_gop()
@@ -2111,6 +2131,19 @@ class Lowering:
             # epilogue 2: the gate operand walks C's strides (checked in k_matmul)
             q.bias = gop(gate, [t[3] for t in mdims], [c_n])
         q.accumulate, q.epilogue = accumulate, epilogue
+        if self._smallk_capture is not None:
+            self._smallk_capture.append(q)     # the second product of a dual gate
+            return True
+        qb = self._smallk_second
+        if qb is not None:
+            if gate is None or qb.w != q.w or qb.r != q.r or qb.k > 4 or \
+                    kp > (8 if f64 else 16) or qb.W.nd != q.W.nd or \
+                    any(qb.W.ext[i] != q.W.ext[i] for i in range(q.W.nd)):
+                return False
+            q.k2, q.X2, q.Y2 = qb.k, qb.X, qb.Y
+            smem += (4 * n + 64 * 4) * esize
+            if smem > 48 * 1024:
+                return False
         grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
         self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
         return True

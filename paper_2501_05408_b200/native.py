@@ -120,7 +120,8 @@ class rt_thin_params(C.Structure):
     _fields_ = [("h", rt_hdr), ("variant", i32), ("f64", i32), ("w", i64), ("r", i64), ("k", i64),
                 ("splits", i32), ("accumulate", i32), ("epilogue", i32), ("vec", i32),
                 ("part_w", i64), ("part_r", i64), ("part", u64), ("X", rt_gop), ("Y", rt_gop),
-                ("C", rt_gop), ("bias", rt_gop), ("W", rt_gbox)]
+                ("C", rt_gop), ("bias", rt_gop), ("W", rt_gbox), ("k2", i64), ("X2", rt_gop),
+                ("Y2", rt_gop)]
 
 
 class rt_rng_params(C.Structure):

@@ -127,7 +127,7 @@ def fused_map(exe_like):
         out[x] = f
         extra = info[2]
         if isinstance(extra, tuple):
-            for m in extra[1:3]:
+            for m in extra[1:3] + extra[4:6]:
                 if isinstance(m, int):
                     out[m] = f
     for s, x in (getattr(exe_like, "contract", None) or {}).items():

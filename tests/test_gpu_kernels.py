@@ -376,3 +376,52 @@ def test_tcgen05_long_k_contraction_is_unbiased(B):
     rel = (out.astype(np.float64) - want) / want
     assert abs(rel.mean()) < 4e-6, rel.mean()
     assert np.abs(rel).max() < 1e-5, np.abs(rel).max()
+
+
+@pytest.mark.parametrize("dt,ka,kb", [("f32", 4, 1), ("f64", 4, 1), ("f32", 16, 4)])
+def test_summed_gated_products_one_launch(dt, ka, kb):
+    """y = (ga @ Wa + gb @ Wb) * (1 - h*h) -- the PPO trunk's d(h2) from the
+    policy and value heads (reference frontend.py:961-963 tanh VJP,
+    runtime.py:249 matmul) -- runs as ONE small-K thin launch with a second
+    product (executor.find_gate_epilogues, k_thin_smallk KP2) and matches
+    numpy evaluated in the reference's order (product, product, add, gate)."""
+    from paper_2501_05408_b200 import executor as X, get_executable, native as N
+    B, H = 8192, 256
+    npd = np.float32 if dt == "f32" else np.float64
+    g = ir.Graph(["b"], {"b": "B"}, {"B": B})
+    nodes = [("ga", "input", ("b",), (1, ka), 0), ("gb", "input", ("b",), (1, kb), 0),
+             ("Wa", "input", (), (ka, H), 0), ("Wb", "input", (), (kb, H), 0),
+             ("h", "input", ("b",), (1, H), 0), ("m1", "matmul", ("b",), (1, H), 2),
+             ("m2", "matmul", ("b",), (1, H), 2), ("s", "add", ("b",), (1, H), 2),
+             ("hh", "mul", ("b",), (1, H), 2), ("one", "const", (), (), 0),
+             ("om", "sub", ("b",), (1, H), 2), ("y", "mul", ("b",), (1, H), 2)]
+    ids = {}
+    for i, (name, kind, dom, shp, nin) in enumerate(nodes):
+        params = {"value": np.array(1.0, dtype=npd)} if kind == "const" else {}
+        g.nodes[i] = ir.Node(i, name, kind, dom, (shp,), (dt,), params, nin)
+        ids[name] = i
+    b = (S("b"),)
+    for snk, srcs in (("m1", [("ga", b), ("Wa", ())]), ("m2", [("gb", b), ("Wb", ())]),
+                      ("s", [("m1", b), ("m2", b)]), ("hh", [("h", b), ("h", b)]),
+                      ("om", [("one", ()), ("hh", b)]), ("y", [("s", b), ("om", b)])):
+        for iid, (src, phi) in enumerate(srcs):
+            g.edges.append(ir.Edge(ids[snk], iid, phi, None, 0, ids[src]))
+    g.outputs = [("y", ids["y"], 0)]
+    rng = np.random.default_rng(ka * 10 + kb)
+    inp = {"ga": rng.standard_normal((B, 1, ka)).astype(npd),
+           "gb": rng.standard_normal((B, 1, kb)).astype(npd),
+           "Wa": rng.standard_normal((ka, H)).astype(npd),
+           "Wb": rng.standard_normal((kb, H)).astype(npd),
+           "h": np.tanh(rng.standard_normal((B, 1, H))).astype(npd)}
+    X._CACHE.clear()
+    exe, _ = get_executable(g, {}, inp, 0)
+    thin = [p for k, p in zip(exe.kernels, exe._params) if k == N.RT_K_THIN]
+    assert exe.launch_count == 1 and len(thin) == 1 and thin[0].k2 == kb and thin[0].epilogue == 2
+    out = execute(g, inputs=inp)["y"]
+    a = inp["ga"].astype(np.float64) @ inp["Wa"].astype(np.float64)
+    c = inp["gb"].astype(np.float64) @ inp["Wb"].astype(np.float64)
+    hv = inp["h"].astype(np.float64)
+    want = (a + c) * (1 - hv * hv)
+    tol = 1e-5 if dt == "f32" else 1e-12
+    np.testing.assert_allclose(out, want, rtol=tol, atol=tol)
+    X._CACHE.clear()
