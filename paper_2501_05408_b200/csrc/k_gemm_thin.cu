@@ -29,6 +29,18 @@ RT_DEV double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 RT_DEV int64_t wdec(const rt_gbox& b, int64_t flat, const int64_t* s) {
   if (b.nd <= 1) return flat * s[0];
   int64_t o = 0;
+  if (flat < (1ll << 32)) {
+    // 32-bit divisions (a 64-bit division is a ~100-instruction call):
+    // gathered minibatch rows decompose every row of every tile
+    uint32_t f = (uint32_t)flat;
+    for (int d = b.nd - 1; d >= 0; --d) {
+      const uint32_t e = (uint32_t)b.ext[d];
+      const uint32_t q = f / e;
+      o += (int64_t)(f - q * e) * s[d];
+      f = q;
+    }
+    return o;
+  }
   for (int d = b.nd - 1; d >= 0; --d) {
     const int64_t e = b.ext[d];
     const int64_t q = flat / e;
@@ -206,6 +218,137 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallk(const __grid_constant__
   }
 }
 
+// variant 2, vectorised (p.vec != 0): a thread owns VW adjacent output
+// columns (one 16-byte store per row) and walks every RL-th row of the tile
+// (RL = 256 / (R / VW) row lanes), with its Y columns in registers; the
+// K-chain per output is the scalar kernel's (fma from 0 in k order, FFMA2 on
+// column pairs: bit-identical), so only the instruction count changes (the
+// scalar form issued ~45 instructions per output of the tanh layer over
+// gathered minibatch rows, 1.9 TB/s; here the x loads and the address math
+// are shared by VW outputs).  Needs R % VW == 0, 256 % (R / VW) == 0, C (and
+// the gate operand) 16-byte aligned rows; lower.py _gemm_smallk checks.
+template <typename T> struct svec2;
+template <> struct svec2<float> { using V = float4; static constexpr int W = 4; };
+template <> struct svec2<double> { using V = double2; static constexpr int W = 2; };
+RT_DEV void v_unpack(const float4& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+RT_DEV void v_unpack(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
+RT_DEV float4 v_pack(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
+RT_DEV double2 v_pack(const double* o) { return make_double2(o[0], o[1]); }
+
+template <int VW>
+RT_DEV void vfma(float (&acc)[VW], const float (&y)[VW], float x) {
+#pragma unroll
+  for (int j = 0; j + 1 < VW; j += 2) fma2(acc[j], acc[j + 1], y[j], y[j + 1], x);
+}
+template <int VW>
+RT_DEV void vfma(double (&acc)[VW], const double (&y)[VW], double x) {
+#pragma unroll
+  for (int j = 0; j < VW; ++j) acc[j] = fma(x, y[j], acc[j]);
+}
+
+template <typename T, int KP, bool GATE = false, int KP2 = 0>
+__global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__ rt_thin_params p) {
+  using V = typename svec2<T>::V;
+  constexpr int VW = svec2<T>::W;
+  constexpr int RT = 64;  // rows per tile
+  __shared__ __align__(16) T xs[RT * KP];
+  __shared__ __align__(16) T xs2[RT * (KP2 > 0 ? KP2 : 1)];
+  __shared__ int64_t coff[RT];
+  const int K = (int)p.k, R = (int)p.r, K2 = (int)p.k2;
+  const int G = R / VW, RL = THREADS / G;
+  const int cg = (int)threadIdx.x % G, rl = (int)threadIdx.x / G;
+  const T* X = (const T*)p.X.ptr + p.X.off;
+  const T* Y = (const T*)p.Y.ptr + p.Y.off;
+  T* Cp = (T*)p.C.ptr + p.C.off;
+  const T* Hg = GATE ? (const T*)p.bias.ptr + p.bias.off : nullptr;
+  const int c0 = cg * VW;
+  T yreg[KP][VW], breg[VW];
+#pragma unroll
+  for (int k = 0; k < KP; ++k)
+#pragma unroll
+    for (int j = 0; j < VW; ++j)
+      yreg[k][j] = k < K ? Y[k * p.Y.s1[0] + (c0 + j) * p.Y.s2[0]] : (T)0;
+  T yreg2[KP2 > 0 ? KP2 : 1][VW];
+  if constexpr (KP2 > 0) {
+    const T* Y2 = (const T*)p.Y2.ptr + p.Y2.off;
+#pragma unroll
+    for (int k = 0; k < KP2; ++k)
+#pragma unroll
+      for (int j = 0; j < VW; ++j)
+        yreg2[k][j] = k < K2 ? Y2[k * p.Y2.s1[0] + (c0 + j) * p.Y2.s2[0]] : (T)0;
+  }
+#pragma unroll
+  for (int j = 0; j < VW; ++j)
+    breg[j] = (p.bias.ptr && !GATE)
+                  ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + (c0 + j) * p.bias.s2[0])
+                  : (T)0;
+  const T* X2 = KP2 ? (const T*)p.X2.ptr + p.X2.off : nullptr;
+  const int64_t xk = p.X.s1[0];
+  const int64_t ntiles = (p.w + RT - 1) / RT;
+  const bool acc_in = p.accumulate != 0, tanh_epi = p.epilogue == 1;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t w0 = tile * RT;
+    const int nrow = (int)(p.w - w0 < RT ? p.w - w0 : RT);
+    __syncthreads();
+    if (threadIdx.x < RT) {
+      const int rr = threadIdx.x;
+      const int64_t w = w0 + (rr < nrow ? rr : 0);
+      coff[rr] = wdec(p.W, w, p.C.s1);
+      const T* xr = X + wdec(p.W, w, p.X.s2);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) xs[rr * KP + k] = (rr < nrow && k < K) ? __ldcs(xr + k * xk) : (T)0;
+      if constexpr (KP2 > 0) {
+        const T* xr2 = X2 + wdec(p.W, w, p.X2.s2);
+#pragma unroll
+        for (int k = 0; k < KP2; ++k)
+          xs2[rr * KP2 + k] = (rr < nrow && k < K2) ? __ldcs(xr2 + k * p.X2.s1[0]) : (T)0;
+      }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int rr = rl; rr < nrow; rr += RL) {
+      const int64_t co = coff[rr] + c0;
+      V hv;
+      if constexpr (GATE) hv = __ldcs(reinterpret_cast<const V*>(Hg + co));
+      T a[VW];
+#pragma unroll
+      for (int j = 0; j < VW; ++j) a[j] = (T)0;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) vfma<VW>(a, yreg[k], xs[rr * KP + k]);
+      if constexpr (KP2 > 0) {
+        T b[VW];
+#pragma unroll
+        for (int j = 0; j < VW; ++j) b[j] = (T)0;
+#pragma unroll
+        for (int k = 0; k < KP2; ++k) vfma<VW>(b, yreg2[k], xs2[rr * KP2 + k]);
+#pragma unroll
+        for (int j = 0; j < VW; ++j) a[j] = add_rn(a[j], b[j]);
+      }
+      if constexpr (GATE) {
+        T h[VW];
+        v_unpack(hv, h);
+        // numpy order, no contraction: gy * (1 - h*h)
+#pragma unroll
+        for (int j = 0; j < VW; ++j) a[j] = mul_rn(a[j], sub_rn((T)1, mul_rn(h[j], h[j])));
+      } else {
+        if (acc_in) {
+          T o[VW];
+          v_unpack(*reinterpret_cast<const V*>(Cp + co), o);
+#pragma unroll
+          for (int j = 0; j < VW; ++j) a[j] += o[j];
+        }
+#pragma unroll
+        for (int j = 0; j < VW; ++j) a[j] += breg[j];
+        if (tanh_epi) {
+#pragma unroll
+          for (int j = 0; j < VW; ++j) a[j] = epi_tanh<T>(a[j]);
+        }
+      }
+      __stcs(reinterpret_cast<V*>(Cp + co), v_pack(a));
+    }
+  }
+}
+
 // variant 3: narrow-N row products C[w, 0:R] = X[w, 0:K] @ Y[0:K, 0:R].
 // One warp per RW (4 or 8) rows per iteration; lane l owns k in {l*VW + 32*VW*i}
 // for i < KI, with the matching Y rows held in registers for the whole
@@ -341,6 +484,24 @@ extern "C" void* rt_kernel_thin_rows(int f64, int r, int k) {
   }
 #undef RT_ROWS
   return nullptr;
+}
+
+// vectorised variant 2 (p.vec): mode 0 plain/tanh/accumulate, 1 gate, 2
+// gate + a second product (K2 <= 4); k = K (KP <= 16 fp32, <= 8 fp64)
+extern "C" void* rt_kernel_thin_vec(int mode, int f64, int k) {
+#define SV(T, KP)                                                              \
+  (mode == 0 ? (void*)k_thin_smallv<T, KP> : mode == 1 ? (void*)k_thin_smallv<T, KP, true> \
+                                                         : (void*)k_thin_smallv<T, KP, true, 4>)
+  if (f64) {
+    if (k <= 4) return SV(double, 4);
+    if (k <= 8) return SV(double, 8);
+    return nullptr;
+  }
+  if (k <= 4) return SV(float, 4);
+  if (k <= 8) return SV(float, 8);
+  if (k <= 16) return SV(float, 16);
+  return nullptr;
+#undef SV
 }
 
 extern "C" void* rt_kernel_thin(int variant, int f64, int r) {

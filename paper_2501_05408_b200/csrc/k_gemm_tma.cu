@@ -81,6 +81,12 @@ RT_DEV void mb_expect(uint32_t bar, uint32_t bytes) {
 RT_DEV void mb_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// L2 prefetch of a TMA box (no shared memory, no barrier): the A operand
+// tile a few stages ahead, so the stage's TMA load is an L2 hit
+RT_DEV void tma2d_prefetch(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+               ::"l"((uint64_t)map), "r"(c0), "r"(c1) : "memory");
+}
 RT_DEV void tma2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
@@ -432,6 +438,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_c
 // the per-tile variant: ncu tensor pipe 29%, smem 31%, long-scoreboard
 // stalls on per-tile prologues).
 #define TP_ST 4
+#ifndef TP_PF
+#define TP_PF 0      // A-tile L2 prefetch distance (stages; 8 measured slower: h2_n 0.56 -> 0.74 ms)
+#endif
 #define TP_CONV 128  // converter threads (warps 0-3; PRESPLIT leaves them only A)
 #define TP_EPI 8     // epilogue warps 6-13: two per TMEM lane quarter (column halves)
 #define TP_THREADS (TP_CONV + 64 + 32 * TP_EPI)
@@ -478,6 +487,19 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
 
   if (warp == TP_CONV / 32) {                    // TMA producer
     if (lane == 0) {
+      // A tiles TP_PF stages ahead are prefetched into L2 (the ring holds
+      // only TP_ST - 1 stages of HBM latency; B is L2-resident anyway)
+      auto prefetch_a = [&](int64_t gg) {
+        const int64_t lt = gg / ktiles, tile2 = blockIdx.x + lt * gridDim.x;
+        if (tile2 >= ntile) return;
+        const int64_t m2 = (tile2 % mt) * TM_BM;
+        const int32_t k2 = (int32_t)((gg % ktiles) * TM_BK);
+        if (a.a_mn)
+          for (int j = 0; j < TM_BM / 32; ++j) tma2d_prefetch(&a.ta, (int32_t)(m2 + 32 * j), k2);
+        else
+          tma2d_prefetch(&a.ta, k2, (int32_t)m2);
+      };
+      for (int64_t q = 0; q < TP_PF; ++q) prefetch_a(q);
       int64_t g = 0;
       for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
         const int64_t mi = tile % mt, ni = tile / mt;
@@ -486,6 +508,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
         const int nbB = a.b_mn ? BN / 32 : 1;
         const uint32_t bytesB = a.b_mn ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
         for (int kt = 0; kt < ktiles; ++kt, ++g) {
+          if (TP_PF > 0) prefetch_a(g + TP_PF);
           const int s = (int)(g % TP_ST);
           if (g >= TP_ST) mb_wait(su32(&empty[s]), (uint32_t)(((g / TP_ST) - 1) & 1));
           const uint32_t st = sbase + s * TM_STAGE;

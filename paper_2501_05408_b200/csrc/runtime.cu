@@ -22,6 +22,7 @@ extern "C" void* rt_kernel_rng_fill();
 extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
+extern "C" void* rt_kernel_thin_vec(int mode, int f64, int k);
 extern "C" void* rt_kernel_thin_rows(int f64, int r, int k);
 extern "C" void* rt_scan_tma_pack(void* blk, void* encode);
 extern "C" void* rt_kernel_scan_pipe(int f64, int step_major);
@@ -182,8 +183,11 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       if (p->variant == 2 && p->k2 > 0) {
         fold_gop(p->X2, env, nenv);
         fold_gop(p->Y2, env, nenv);
-        return p->epilogue == 2 && p->k2 <= 4 ? rt_kernel_thin(5, p->f64, (int)p->k) : nullptr;
+        if (p->epilogue != 2 || p->k2 > 4) return nullptr;
+        return p->vec ? rt_kernel_thin_vec(2, p->f64, (int)p->k) : rt_kernel_thin(5, p->f64, (int)p->k);
       }
+      if (p->variant == 2 && p->vec)
+        return rt_kernel_thin_vec(p->epilogue == 2 ? 1 : 0, p->f64, (int)p->k);
       return rt_kernel_thin(p->variant == 2 && p->epilogue == 2 ? 4 : p->variant, p->f64,
                             (int)(p->variant == 2 ? p->k : p->r));
     }

@@ -2144,8 +2144,32 @@ class Lowering:
             smem += (4 * n + 64 * 4) * esize
             if smem > 48 * 1024:
                 return False
+        if self.THIN_VEC and self._smallk_vec_ok(q, kp, f64, gate is not None):
+            q.vec, smem = 1, 0           # k_thin_smallv: static shared memory
         grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
         self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
+        return True
+
+    THIN_VEC = os.environ.get("RTB200_THIN_VEC", "1") != "0"
+
+    @staticmethod
+    def _smallk_vec_ok(q, kp, f64, gate):
+        """k_thin_smallv: VW = 16 / itemsize output columns per thread with
+        16-byte stores (and 16-byte gate loads): every C row start (base,
+        row strides, env offsets) a multiple of VW elements, unit column
+        stride, R a multiple of VW with R / VW dividing 256."""
+        vw = 2 if f64 else 4
+        es = 8 if f64 else 4
+        R = q.r
+        if kp > (8 if f64 else 16) or R % vw or R // vw > 256 or 256 % (R // vw) or \
+                q.C.s2[0] != 1 or q.accumulate and q.epilogue == 2:
+            return False
+        ops = [q.C] + ([q.bias] if gate else [])
+        for g in ops:
+            if (g.ptr + es * g.off) % 16 or any(g.off_env[e] % vw for e in range(N.RT_MAXENV)):
+                return False
+            if any(g.s1[i] % vw for i in range(max(1, q.W.nd))):
+                return False
         return True
 
     ROWS_MAX_R = 4

@@ -425,3 +425,48 @@ def test_summed_gated_products_one_launch(dt, ka, kb):
     tol = 1e-5 if dt == "f32" else 1e-12
     np.testing.assert_allclose(out, want, rtol=tol, atol=tol)
     X._CACHE.clear()
+
+
+@pytest.mark.parametrize("K,Nc,dt,epi", [(16, 256, "f32", "tanh"), (8, 64, "f64", "plain"),
+                                         (4, 256, "f32", "plain"), (8, 128, "f64", "tanh"),
+                                         (3, 256, "f32", "tanh")])
+def test_vectorised_small_k_is_bit_identical(K, Nc, dt, epi, monkeypatch):
+    """k_thin_smallv (VW columns per thread, 16-byte stores) computes every
+    output with the scalar kernel's operation sequence: bit-identical results
+    on gathered minibatch rows, with and without the bias + tanh epilogue."""
+    from paper_2501_05408_b200 import executor as X, get_executable, lower, native as N
+    Mb, U, T = 4, 256, 24
+    B = Mb * U
+    npd = np.float32 if dt == "f32" else np.float64
+    g = ir.Graph(["j", "u", "b", "t"], {"j": "M", "u": "U", "b": "B", "t": "T"},
+                 {"M": Mb, "U": U, "B": B, "T": T})
+    g.nodes[0] = ir.Node(0, "x", "input", ("b", "t"), ((1, K),), (dt,))
+    g.nodes[1] = ir.Node(1, "W", "input", (), ((K, Nc),), (dt,))
+    g.nodes[2] = ir.Node(2, "y", "matmul", ("j", "u", "t"), ((1, Nc),), (dt,), {}, 2)
+    bidx = ("add", ("mul", S("u"), S("M", "bound")), S("j"))
+    g.edges += [ir.Edge(2, 0, (bidx, S("t")), None, 0, 0), ir.Edge(2, 1, (), None, 0, 1)]
+    out_id = 2
+    if epi == "tanh":
+        g.nodes[3] = ir.Node(3, "bb", "input", (), ((1, Nc),), (dt,))
+        g.nodes[4] = ir.Node(4, "z", "add", ("j", "u", "t"), ((1, Nc),), (dt,), {}, 2)
+        g.nodes[5] = ir.Node(5, "h", "tanh", ("j", "u", "t"), ((1, Nc),), (dt,), {}, 1)
+        jut = (S("j"), S("u"), S("t"))
+        g.edges += [ir.Edge(4, 0, jut, None, 0, 2), ir.Edge(4, 1, (), None, 0, 3),
+                    ir.Edge(5, 0, jut, None, 0, 4)]
+        out_id = 5
+    g.outputs = [("out", out_id, 0)]
+    rng = np.random.default_rng(K * Nc)
+    inp = {"x": rng.standard_normal((B, T, 1, K)).astype(npd),
+           "W": rng.standard_normal((K, Nc)).astype(npd)}
+    if epi == "tanh":
+        inp["bb"] = rng.standard_normal((1, Nc)).astype(npd)
+    res = {}
+    for vec in (False, True):
+        monkeypatch.setattr(lower.Lowering, "THIN_VEC", vec)
+        X._CACHE.clear()
+        exe, _ = get_executable(g, {}, inp, 0)
+        thin = [p for k, p in zip(exe.kernels, exe._params) if k == N.RT_K_THIN]
+        assert len(thin) == 1 and thin[0].vec == int(vec), (vec, [t.vec for t in thin])
+        res[vec] = execute(g, inputs=inp)["out"]
+    np.testing.assert_array_equal(res[True], res[False])
+    X._CACHE.clear()
