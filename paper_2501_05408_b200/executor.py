@@ -1518,39 +1518,33 @@ class Executable:
 
     def fetch(self, stream=None):
         """Status word + every output in ONE device->host synchronisation:
-        outputs are copied (asynchronously) into one reused pinned staging
-        buffer, then into fresh numpy arrays.  Raises like check_status."""
+        each output is copied (asynchronously, on the program's stream) into
+        its own freshly allocated pinned host tensor -- torch's caching host
+        allocator recycles them once the caller drops the arrays -- and
+        returned as a numpy view of it (no host-side copy).  Raises like
+        check_status."""
         torch = self.torch
         s = stream or torch.cuda.current_stream(self.dev)
         if self._stage_out is None:
-            total = 16 + sum((self.bufs[(nid, oid)].nbytes + 255) // 256 * 256
-                             for _, nid, oid in self.g.outputs)
-            self._stage_out = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+            self._stage_out = torch.empty(16, dtype=torch.uint8, pin_memory=True)
         st = self._stage_out
         views = self.outputs(device_outputs=True, clone=False)
+        hosts = {}
         with torch.cuda.device(self.dev):
             with torch.cuda.stream(s):
-                st[:16].copy_(_u8view(torch, self.status, 16, self.dev), non_blocking=True)
-                off, spans = 16, {}
+                st.copy_(_u8view(torch, self.status, 16, self.dev), non_blocking=True)
                 for name, nid, oid in self.g.outputs:
                     t = views[name]
-                    nb = t.numel() * t.element_size()
-                    if nb:
-                        src = t.contiguous().reshape(-1).view(torch.uint8)
-                        st[off:off + nb].copy_(src, non_blocking=True)
-                    spans[name] = (off, nb, t.shape, t.dtype)
-                    off += (nb + 255) // 256 * 256
+                    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+                    if t.numel():
+                        h.copy_(t, non_blocking=True)
+                    hosts[name] = h
             s.synchronize()
-        hostst = st[:16].numpy().view(np.int32)
-        self._raise_status(hostst)
+        self._raise_status(st.numpy().view(np.int32))
         res = {}
-        buf = st.numpy()
         for name, nid, oid in self.g.outputs:
-            off, nb, shape, tdt = spans[name]
             b = self.bufs[(nid, oid)]
-            npdt = DTYPES[b.dtype]
-            a = np.array(buf[off:off + nb].view(npdt).reshape(tuple(shape)), copy=True)
-            res[name] = a
+            res[name] = hosts[name].numpy().view(DTYPES[b.dtype])
         return res
 
     def _raise_status(self, st):

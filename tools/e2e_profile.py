@@ -31,9 +31,8 @@ for _ in range(n):
     t1 = time.perf_counter()
     exe.run(hin)          # (uploads again inside run: measured separately above)
     t2 = time.perf_counter()
-    exe.check_status()
     t3 = time.perf_counter()
-    outs = exe.outputs()
+    outs = exe.fetch()
     t4 = time.perf_counter()
     hin = next_inputs(outs, WL.params())
     T["upload"] += t1 - t0
