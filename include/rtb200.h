@@ -282,6 +282,14 @@ typedef struct {
    * two heads' backward into one hidden layer, executor.find_gate_epilogues) */
   int64_t k2;
   rt_gop X2, Y2;
+  /* variant 1 with ones != 0: a column of ones appended to Y -- the bias
+   * gradient sum_k X[k,w] of the same contraction (executor.find_ones_bias),
+   * per-split partials into part2[s, w] (reduced by a second RT_K_SPLITK) */
+  int32_t ones;
+  int32_t colsum;      /* variant 2 vectorised: fp64 column sums of C over the rows
+                        * into part2[blockIdx, r] (a bias gradient of the output,
+                        * executor.find_colsum_epilogues; RT_K_SPLITK finishes) */
+  uint64_t part2;
 } rt_thin_params;
 
 /* Point coordinates for per-point entropy: coordinate j of the node's

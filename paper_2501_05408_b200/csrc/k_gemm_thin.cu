@@ -51,7 +51,7 @@ RT_DEV int64_t wdec(const rt_gbox& b, int64_t flat, const int64_t* s) {
 }
 
 
-template <typename T, int R>
+template <typename T, int R, bool ONES = false>
 __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant__ rt_thin_params p) {
   // 256-row Y chunks when they fit in 16 KB: 4x fewer barrier + Y-latency
   // exposures per split than 64-row chunks
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant
   T acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = (T)0;
+  T acc1 = (T)0;   // ONES: the sum of X over k (a column of ones in Y)
   for (int64_t kb = k0; kb < k1; kb += KT) {
     const int nk = (int)(k1 - kb < KT ? k1 - kb : KT);
     __syncthreads();
@@ -86,16 +87,19 @@ __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant
       for (int kk = 0; kk < KT; ++kk) {
         const T x = __ldcs(xb + kk * xk);
         fma_bcast<R>(acc, ys[kk], x);
+        if constexpr (ONES) acc1 += x;
       }
     } else {
       for (int kk = 0; kk < nk; ++kk) {
         const T x = __ldcs(xb + kk * xk);
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = fma(x, ys[kk][r], acc[r]);
+        if constexpr (ONES) acc1 += x;
       }
     }
   }
   if (!wok) return;
+  if constexpr (ONES) ((T*)p.part2)[(int64_t)s * p.w + w] = acc1;
   T* part = (T*)p.part + (int64_t)s * p.w * p.r;
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -254,8 +258,13 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__
   __shared__ __align__(16) T xs[RT * KP];
   __shared__ __align__(16) T xs2[RT * (KP2 > 0 ? KP2 : 1)];
   __shared__ int64_t coff[RT];
+  __shared__ double csum[THREADS * VW];   // colsum: per-lane column partials
   const int K = (int)p.k, R = (int)p.r, K2 = (int)p.k2;
   const int G = R / VW, RL = THREADS / G;
+  double cs[VW];
+#pragma unroll
+  for (int j = 0; j < VW; ++j) cs[j] = 0.0;
+  const bool colsum = p.colsum != 0;
   const int cg = (int)threadIdx.x % G, rl = (int)threadIdx.x / G;
   const T* X = (const T*)p.X.ptr + p.X.off;
   const T* Y = (const T*)p.Y.ptr + p.Y.off;
@@ -345,6 +354,22 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__
         }
       }
       __stcs(reinterpret_cast<V*>(Cp + co), v_pack(a));
+      if (colsum) {     // fp64 per row: the sum keeps the reference's accuracy
+#pragma unroll
+        for (int j = 0; j < VW; ++j) cs[j] += (double)a[j];
+      }
+    }
+  }
+  if (colsum) {
+    // this CTA's column sums: lanes rl = 0.. RL-1 in order (deterministic)
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < VW; ++j) csum[rl * R + c0 + j] = cs[j];
+    __syncthreads();
+    for (int c = (int)threadIdx.x; c < R; c += THREADS) {
+      double t = 0.0;
+      for (int l = 0; l < RL; ++l) t += csum[l * R + c];
+      ((double*)p.part2)[(int64_t)blockIdx.x * R + c] = t;
     }
   }
 }
@@ -505,6 +530,19 @@ extern "C" void* rt_kernel_thin_vec(int mode, int f64, int k) {
 }
 
 extern "C" void* rt_kernel_thin(int variant, int f64, int r) {
+  if (variant == 6) {
+    // variant 1 with the ones column (bias gradient of the same contraction)
+    if (f64) {
+      if (r <= 4) return (void*)k_thin_contract<double, 4, true>;
+      if (r <= 8) return (void*)k_thin_contract<double, 8, true>;
+      if (r <= 16) return (void*)k_thin_contract<double, 16, true>;
+      return (void*)k_thin_contract<double, 32, true>;
+    }
+    if (r <= 4) return (void*)k_thin_contract<float, 4, true>;
+    if (r <= 8) return (void*)k_thin_contract<float, 8, true>;
+    if (r <= 16) return (void*)k_thin_contract<float, 16, true>;
+    return (void*)k_thin_contract<float, 32, true>;
+  }
   if (variant == 5) {
     // variant 2 + gate + a second product with K2 <= 4 (runtime.cu passes 5)
     if (f64) {

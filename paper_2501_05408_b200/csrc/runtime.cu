@@ -186,6 +186,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
         if (p->epilogue != 2 || p->k2 > 4) return nullptr;
         return p->vec ? rt_kernel_thin_vec(2, p->f64, (int)p->k) : rt_kernel_thin(5, p->f64, (int)p->k);
       }
+      if (p->variant == 1 && p->ones) return rt_kernel_thin(6, p->f64, (int)p->r);
       if (p->variant == 2 && p->vec)
         return rt_kernel_thin_vec(p->epilogue == 2 ? 1 : 0, p->f64, (int)p->k);
       return rt_kernel_thin(p->variant == 2 && p->epilogue == 2 ? 4 : p->variant, p->f64,

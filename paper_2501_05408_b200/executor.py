@@ -334,6 +334,95 @@ def find_aliases(g: Graph, pshape):
     return alias
 
 
+ONES_BIAS = os.environ.get("RTB200_ONES_BIAS", "1") != "0"
+
+
+def out_ids_of(g):
+    return {nid for _, nid, _ in g.outputs}
+
+
+def find_colsum_epilogues(g: Graph, gemm_epi, pshape, fixed_of, skip, ext):
+    """A full-range sum over the rows of a gate-fused small-K product's
+    output (d(hidden) and its bias gradient: the reference VJP of `+ b`
+    sums the same values) -> column sums accumulated by the producing
+    launch (k_thin_smallv `colsum`).  Returns {producer y: sum node}; the
+    lowering falls back to the separate reduction when the vectorised
+    kernel does not run."""
+    out = {}
+    for y, (_x, _b, t) in gemm_epi.items():
+        if not isinstance(t, tuple):
+            continue
+        yn = g.nodes[y]
+        for e in g.out_edges(y):
+            r = g.nodes[e.sink]
+            if r.kind != "sum" or r.id in skip or e.psi is not None or e.oid != 0 or \
+                    len(g.in_edges(r.id)) != 1:
+                continue
+            kept = [d for d, c in zip(yn.domain, e.phi) if c == ("sym", d, "loop")]
+            sl = [d for d, c in zip(yn.domain, e.phi)
+                  if c[0] == "slice" and c[1] == ("int", 0) and c[2] == ("sym", g.dim_bound[d], "bound")]
+            if len(kept) + len(sl) != len(yn.domain) or not sl or tuple(kept) != tuple(r.domain) or \
+                    tuple(r.params.get("dims", ())) != tuple(range(len(sl))) or \
+                    pshape[(r.id, 0)] != pshape[(y, 0)] or r.dtype != yn.dtype or \
+                    fixed_of.get(r.id) != fixed_of.get(y) or \
+                    any(d not in fixed_of.get(y, ()) and ext.get(d, 1) != 1 for d in kept):
+                continue
+            out[y] = r.id
+            break
+    return out
+
+
+
+def find_ones_bias(g: Graph, contract, pshape, ext, skip):
+    """Bias gradient + weight gradient of one layer in one pass: for a
+    contraction s = sum(matmul(a, P)[kept, 0:B, 0:T]) (dW = a^T dP over the
+    points, a narrow: K_a <= 32 rows of a column operand) and a reduction
+    R = sum(P[kept, 0:B, 0:T]) over the SAME points (db = sum of dP,
+    reference frontend.py VJP of `+ b`), R is the contraction of P with a
+    column of ones: the thin contraction computes it alongside (RT_K_THIN
+    variant 1, `ones`), P is streamed once.  Returns {s: R}."""
+    out_ids = {nid for _, nid, _ in g.outputs}
+    by_src = {}
+    for sid, xid in contract.items():
+        x = g.nodes[xid]
+        ins = sorted(g.in_edges(xid), key=lambda e: e.iid)
+        if len(ins) != 2:
+            continue
+        ea, eb = ins
+        sa, sb = pshape.get((ea.src, ea.oid), ()), pshape.get((eb.src, eb.oid), ())
+        if len(sa) != 2 or len(sb) != 2 or sa[1] != 1 or sb[0] != 1 or not (1 <= sa[0] <= 32) \
+                or sb[1] <= 32 or x.dtype not in ("f32", "f64"):
+            continue
+        if not _is_identity(eb, g.nodes[eb.src], x):
+            continue
+        (es,) = g.in_edges(sid)
+        by_src.setdefault((eb.src, eb.oid), []).append((sid, es.phi, x))
+    res = {}
+    for r in g.sorted_nodes():
+        if r.kind != "sum" or r.id in skip or r.id in contract:
+            continue
+        ins = g.in_edges(r.id)
+        if len(ins) != 1 or ins[0].psi is not None:
+            continue
+        e = ins[0]
+        if e.src in skip:
+            continue
+        for sid, phi, x in by_src.get((e.src, e.oid), ()):
+            if sid in res or e.phi != phi or g.nodes[sid].domain != r.domain or \
+                    tuple(r.params.get("dims", ())) != tuple(g.nodes[sid].params.get("dims", ())) or \
+                    r.dtype != x.dtype or pshape[(r.id, 0)] != (1, pshape[(e.src, e.oid)][1]):
+                continue
+            pts = 1
+            for d, c in zip(g.nodes[e.src].domain, e.phi):
+                if c[0] == "slice":
+                    pts *= ext.get(d, 1)
+            if pts < 4096:
+                continue
+            res[sid] = r.id
+            break
+    return res
+
+
 def find_contractions(g: Graph):
     """sum(matmul(...)[kept dims, 0:B, 0:T]) -> one GEMM over the points."""
     out_ids = {nid for _, nid, _ in g.outputs}
@@ -784,6 +873,27 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True, skew=None):
     plan.gae = gae
     fuse_src = find_ew_fusions(g, pshape, taken) if fuse else {}
     virtual |= set(fuse_src)
+    ones = find_ones_bias(g, contract, pshape, ext, virtual) if fuse and ONES_BIAS else {}
+    if ones:
+        # plan order of the steps (both in the same loops)
+        order = {}
+        def walk(steps):
+            for st in steps:
+                if hasattr(st, "nid"):
+                    order.setdefault(st.nid, len(order))
+                else:
+                    walk(st.body)
+        walk(plan.steps)
+        for sid, rid in list(ones.items()):
+            # the contraction launches at its own place and writes the sum:
+            # every reader of the sum must come after it
+            readers = [e.sink for e in g.out_edges(rid)]
+            if fixed_of.get(sid) != fixed_of.get(rid) or any(
+                    order.get(c, -1) <= order.get(sid, 1 << 30) for c in readers):
+                del ones[sid]
+    plan.ones_bias = ones      # the bias sums stay materialised: the contraction writes them
+    plan.colsum = find_colsum_epilogues(g, gemm_epi, pshape, fixed_of, virtual | set(ones.values()),
+                                        ext) if fuse else {}
     for f, (x, _b, t) in gemm_epi.items():
         virtual.add(x)
         if isinstance(t, tuple):

@@ -300,6 +300,12 @@ class Lowering:
         self.virtual |= set(self.fuse_src)
         for info in getattr(plan, "gae", {}).values():
             self.virtual |= info["nodes"]          # delta chain formed inside the scan
+        self.ones_bias = dict(getattr(plan, "ones_bias", {}) or {})   # contraction -> bias sum
+        self.ones_targets = {r: s_ for s_, r in self.ones_bias.items()}   # bias sum -> contraction
+        self._ones_done = set()
+        self.colsum = dict(getattr(plan, "colsum", {}) or {})   # gate product -> its row sum
+        self._colsum_done = set()
+        self._colsum_req = None
         for f, (x, _b, t) in self.gemm_epi.items():
             self.virtual.add(x)
             if isinstance(t, tuple):           # tanh-VJP gate: (1 - h*h) chain
@@ -979,7 +985,23 @@ class Lowering:
             return  # aliases and leaves need no kernel
         if n.id in self.virtual:
             return  # fused into its consumer
+        if n.id in self.ones_targets:
+            return    # a bias sum written by its contraction's launch (ones column)
+        if n.id in self._colsum_done:
+            self._colsum_done.discard(n.id)   # (per plan instance: its producer ran just before)
+            return    # summed by its producer's launch (k_thin_smallv colsum)
         ctx = Ctx(self, n, s.fixed)
+        if n.id in self.colsum and self._capture is None:
+            rkey = (self.colsum[n.id], 0)
+            sr = self.storage(rkey)
+            rdst = {d: sr.strides[j] for j, d in enumerate(self.bufs[rkey].dims)}
+            g_ = N.rt_gop()
+            g_.ptr, g_.dtype, g_.off = sr.ptr, N.DTYPE_CODE[sr.dtype], 0
+            for d in ctx.fixed:
+                if d in rdst:
+                    g_.off_env[self.slot[d]] += rdst[d]
+            g_.s2[0] = sr.strides[-1]
+            self._colsum_req = (rkey[0], g_)
         if any(e == 0 for e in ctx.slab_ext):
             return
         if n.id in self.gemm_epi:
@@ -1011,6 +1033,7 @@ class Lowering:
                     raise LowerError(f"no kernel for op kind {n.kind!r}")
                 fn = self.ew
             fn(ctx)
+        self._colsum_req = None
         if n.id in self.shard_reduce:
             self._hook_allreduce(ctx, (n.id, 0))
 
@@ -1892,7 +1915,8 @@ class Lowering:
             raise LowerError("matmul output layout mismatch")
         return a_ax, b_ax, batch, m, nn, kk, c_log
 
-    def _gemm(self, A, B, Cc, Z, M, Nn, K, label, accumulate=0, epilogue=0, bias=None, gate=None):
+    def _gemm(self, A, B, Cc, Z, M, Nn, K, label, accumulate=0, epilogue=0, bias=None, gate=None,
+              ones=None):
         """Z/M/N/K: lists of (extent, a_stride, b_stride, c_stride).
         A/B/C: (buf, element offset, {env slot: stride})."""
         p = N.rt_gemm_params()
@@ -1958,8 +1982,10 @@ class Lowering:
                 return self._gemm_tc(p, label, accumulate, 2, None)
             raise LowerError(f"{label[1]}: gate epilogue needs the thin or the TMA GEMM")
         if not self._capture_active() and self._gemm_thin(p, Z, M, Nn, K, label, accumulate,
-                                                          epilogue, bias):
+                                                          epilogue, bias, ones=ones):
             return
+        if ones is not None:
+            raise LowerError(f"{label[1]}: the bias-gradient column needs the thin contraction")
         if self.use_tc and self._tc_ok(p, A, B, Cc):
             return self._gemm_tc(p, label, accumulate, epilogue, bias)
         tiles = ((p.m + 63) // 64) * ((p.n + 63) // 64) * p.z
@@ -2024,7 +2050,14 @@ class Lowering:
     THIN_MAX_R = 32
     THIN_MIN_K = 4096
 
-    def _gemm_thin(self, p, Z, M, Nn, K, label, accumulate, epilogue, bias, gate=None):
+    def ones_bias_label(self, label):
+        return self.ones_bias.get(label[0], label[0])
+
+    def ones_bias_name(self, label):
+        r = self.ones_bias.get(label[0])
+        return self.g.nodes[r].name if r is not None else label[1]
+
+    def _gemm_thin(self, p, Z, M, Nn, K, label, accumulate, epilogue, bias, gate=None, ones=None):
         """Narrow GEMMs -> RT_K_THIN (csrc/k_gemm_thin.cu); False if not one."""
         if p.z != 1 or any(t[0] != 1 for t in Z):
             return False
@@ -2064,6 +2097,8 @@ class Lowering:
                                       or m <= self.THIN_MAX_R < n and b_n == 1):
             q.variant = 1
             if n <= self.THIN_MAX_R and a_m == 1:
+                if ones is not None:
+                    return False
                 q.w, q.r = m, n
                 q.X, q.Y = gop(p.A, a_k, a_m), gop(p.B, b_k, b_n)
                 q.part_w, q.part_r = n, 1
@@ -2085,6 +2120,19 @@ class Lowering:
                 r.bias = bias
             self.add_rec(N.RT_K_SPLITK, r, [int(min((p.m * p.n + 7) // 8, 148 * 16)), 1, 1], [256, 1, 1], 0,
                          label)   # k_splitk: a warp per output
+            if ones is not None:
+                # the ones column: sum_k X[k, w] per split -> part2 -> the bias sum
+                q.ones, q.part2 = 1, self.alloc(q.splits * q.w * esize)
+                r2 = N.rt_splitk_params()
+                r2.Z.nd = r2.M.nd = 1
+                r2.Z.ext[0] = r2.M.ext[0] = 1
+                r2.N.nd = 1
+                r2.N.ext[0] = q.w
+                r2.z, r2.m, r2.n = 1, 1, q.w
+                r2.splits, r2.f64 = q.splits, q.f64
+                r2.part, r2.C = q.part2, ones
+                self.add_rec(N.RT_K_SPLITK, r2, [int(min((q.w + 7) // 8, 148 * 16)), 1, 1],
+                             [256, 1, 1], 0, (self.ones_bias_label(label), self.ones_bias_name(label)))
             return True
         return self._gemm_smallk(p, M, nc, kc, f64, label, accumulate, epilogue, bias)
 
@@ -2147,7 +2195,24 @@ class Lowering:
         if self.THIN_VEC and self._smallk_vec_ok(q, kp, f64, gate is not None):
             q.vec, smem = 1, 0           # k_thin_smallv: static shared memory
         grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
+        req = self._colsum_req
+        if req is not None and q.vec and gate is not None and not accumulate:
+            # the row sum of this output (its bias gradient) from the same launch
+            q.colsum, q.part2 = 1, self.alloc(grid[0] * q.r * 8)
         self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
+        if q.colsum:
+            rid, gc = req
+            r2 = N.rt_splitk_params()
+            r2.Z.nd = r2.M.nd = r2.N.nd = 1
+            r2.Z.ext[0] = r2.M.ext[0] = 1
+            r2.N.ext[0] = q.r
+            r2.z, r2.m, r2.n = 1, 1, q.r
+            r2.splits, r2.f64 = grid[0], 1          # fp64 partials, stored in C's dtype
+            r2.part, r2.C = q.part2, gc
+            self.add_rec(N.RT_K_SPLITK, r2, [int(min((q.r + 7) // 8, 148 * 16)), 1, 1],
+                         [256, 1, 1], 0, (rid, self.g.nodes[rid].name))
+            self._colsum_done.add(rid)
+            self._colsum_req = None
         return True
 
     THIN_VEC = os.environ.get("RTB200_THIN_VEC", "1") != "0"
@@ -2345,8 +2410,23 @@ class Lowering:
         env_a = {self.slot[d]: s for d, s in A.coef.items() if d in ctx.fixed}
         env_b = {self.slot[d]: s for d, s in B.coef.items() if d in ctx.fixed}
         env_c = {self.slot[d]: cdst[d] for d in ctx.fixed if d in cdst}
+        ones = None
+        if S.id in self.ones_bias:
+            # the bias gradient sum(P) of the same points, as a ones column
+            rkey = (self.ones_bias[S.id], 0)
+            sr = self.storage(rkey)
+            rdst = {d: sr.strides[j] for j, d in enumerate(self.bufs[rkey].dims)}
+            if any(self.ext[d] != 1 for d in ctx.slab):
+                raise LowerError(f"{S.name}: bias-gradient column over a batched contraction")
+            g_ = N.rt_gop()
+            g_.ptr, g_.dtype, g_.off = sr.ptr, N.DTYPE_CODE[sr.dtype], 0
+            for d in ctx.fixed:
+                if d in rdst:
+                    g_.off_env[self.slot[d]] += rdst[d]
+            g_.s2[0] = sr.strides[-1]
+            ones = g_
         self._gemm((A.buf, A.off, env_a), (B.buf, B.off, env_b), (st, 0, env_c),
-                   Z, M, Nn, K, (S.id, S.name))
+                   Z, M, Nn, K, (S.id, S.name), ones=ones)
 
     # ---- rng / udf
 

@@ -132,6 +132,9 @@ def fused_map(exe_like):
                     out[m] = f
     for s, x in (getattr(exe_like, "contract", None) or {}).items():
         out[x] = s
+    plan = getattr(exe_like, "plan", None)
+    for s, r in (getattr(plan, "ones_bias", None) or {}).items():
+        out[r] = s        # the bias sum computed by its contraction's launch
     # chains (a fused producer of a fused producer) end at a launched node
     for v in list(out):
         seen, r = {v}, out[v]

@@ -470,3 +470,90 @@ def test_vectorised_small_k_is_bit_identical(K, Nc, dt, epi, monkeypatch):
         res[vec] = execute(g, inputs=inp)["out"]
     np.testing.assert_array_equal(res[True], res[False])
     X._CACHE.clear()
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_bias_gradient_rides_the_weight_contraction(dt):
+    """db = sum(dP over the points) and dW = sum(a^T dP) of one layer
+    (reference frontend.py VJPs of `+ b` and matmul) in ONE pass over dP:
+    the thin contraction carries a column of ones (find_ones_bias), the
+    separate column reduction is gone; both match float64 numpy."""
+    from paper_2501_05408_b200 import executor as X, get_executable, native as N
+    B, K, Nc = 16384, 16, 256
+    g = ir.Graph(["b"], {"b": "B"}, {"B": B})
+    g.nodes[0] = ir.Node(0, "a", "input", ("b",), ((1, K),), (dt,))
+    g.nodes[1] = ir.Node(1, "P", "input", ("b",), ((1, Nc),), (dt,))
+    g.nodes[2] = ir.Node(2, "at", "permute", ("b",), ((K, 1),), (dt,), {"order": (1, 0)}, 1)
+    g.nodes[3] = ir.Node(3, "x", "matmul", ("b",), ((K, Nc),), (dt,), {}, 2)
+    g.nodes[4] = ir.Node(4, "dW", "sum", (), ((K, Nc),), (dt,), {"dims": (0,)}, 1)
+    g.nodes[5] = ir.Node(5, "db", "sum", (), ((1, Nc),), (dt,), {"dims": (0,)}, 1)
+    full = (("slice", ("int", 0), S("B", "bound")),)
+    g.edges += [ir.Edge(2, 0, (S("b"),), None, 0, 0),
+                ir.Edge(3, 0, (S("b"),), None, 0, 2), ir.Edge(3, 1, (S("b"),), None, 0, 1),
+                ir.Edge(4, 0, full, None, 0, 3), ir.Edge(5, 0, full, None, 0, 1)]
+    g.outputs = [("dW", 4, 0), ("db", 5, 0)]
+    npd = np.float32 if dt == "f32" else np.float64
+    rng = np.random.default_rng(7)
+    inp = {"a": rng.standard_normal((B, 1, K)).astype(npd),
+           "P": rng.standard_normal((B, 1, Nc)).astype(npd)}
+    X._CACHE.clear()
+    exe, _ = get_executable(g, {}, inp, 0)
+    thin = [p for k, p in zip(exe.kernels, exe._params) if k == N.RT_K_THIN]
+    assert len(thin) == 1 and thin[0].ones == 1
+    assert N.RT_K_REDUCE not in exe.kernels
+    out = execute(g, inputs=inp)
+    a64, p64 = inp["a"][:, 0].astype(np.float64), inp["P"][:, 0].astype(np.float64)
+    # fp32 sums of 16 k terms of size ~1: absolute error ~1e-4 where they cancel
+    tol = dict(rtol=1e-5, atol=2e-3) if dt == "f32" else dict(rtol=1e-12, atol=1e-10)
+    np.testing.assert_allclose(out["dW"], a64.T @ p64, **tol)
+    np.testing.assert_allclose(out["db"], p64.sum(axis=0, keepdims=True), **tol)
+    X._CACHE.clear()
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_bias_gradient_summed_by_the_gate_launch(dt):
+    """d(hidden) = (g @ W) * (1 - h*h) and its bias gradient sum(d(hidden))
+    over the points from ONE launch: the vectorised gate kernel accumulates
+    fp64 column sums per CTA (colsum), a split-K pass finishes them; no
+    separate column reduction; both match float64 numpy."""
+    from paper_2501_05408_b200 import executor as X, get_executable, native as N
+    B, K, H = 16384, 4, 256
+    g = ir.Graph(["b"], {"b": "B"}, {"B": B})
+    nodes = [("gz", "input", ("b",), (1, K), 0), ("W", "input", (), (K, H), 0),
+             ("h", "input", ("b",), (1, H), 0), ("m", "matmul", ("b",), (1, H), 2),
+             ("hh", "mul", ("b",), (1, H), 2), ("one", "const", (), (), 0),
+             ("om", "sub", ("b",), (1, H), 2), ("y", "mul", ("b",), (1, H), 2),
+             ("db", "sum", (), (1, H), 1)]
+    ids = {}
+    npd = np.float32 if dt == "f32" else np.float64
+    for i, (name, kind, dom, shp, nin) in enumerate(nodes):
+        params = {"value": np.array(1.0, dtype=npd)} if kind == "const" else \
+            ({"dims": (0,)} if kind == "sum" else {})
+        g.nodes[i] = ir.Node(i, name, kind, dom, (shp,), (dt,), params, nin)
+        ids[name] = i
+    b = (S("b"),)
+    for snk, srcs in (("m", [("gz", b), ("W", ())]), ("hh", [("h", b), ("h", b)]),
+                      ("om", [("one", ()), ("hh", b)]), ("y", [("m", b), ("om", b)]),
+                      ("db", [("y", (("slice", ("int", 0), S("B", "bound")),))])):
+        for iid, (src, phi) in enumerate(srcs):
+            g.edges.append(ir.Edge(ids[snk], iid, phi, None, 0, ids[src]))
+    g.outputs = [("y", ids["y"], 0), ("db", ids["db"], 0)]
+    rng = np.random.default_rng(3)
+    inp = {"gz": rng.standard_normal((B, 1, K)).astype(npd),
+           "W": rng.standard_normal((K, H)).astype(npd),
+           "h": np.tanh(rng.standard_normal((B, 1, H))).astype(npd)}
+    X._CACHE.clear()
+    exe, _ = get_executable(g, {}, inp, 0)
+    thin = [p for k, p in zip(exe.kernels, exe._params) if k == N.RT_K_THIN]
+    assert len(thin) == 1 and thin[0].colsum == 1 and thin[0].vec == 1
+    assert N.RT_K_REDUCE not in exe.kernels
+    out = execute(g, inputs=inp)
+    y = (inp["gz"][:, 0].astype(np.float64) @ inp["W"].astype(np.float64)) * \
+        (1 - inp["h"][:, 0].astype(np.float64) ** 2)
+    tol = dict(rtol=1e-5, atol=1e-4) if dt == "f32" else dict(rtol=1e-12, atol=1e-10)
+    np.testing.assert_allclose(out["y"][:, 0], y, **tol)
+    # db sums the kernel's own (rounded) y values in fp64
+    np.testing.assert_allclose(out["db"], out["y"][:, 0].astype(np.float64).sum(0, keepdims=True),
+                               rtol=1e-6 if dt == "f32" else 1e-13, atol=1e-6 if dt == "f32" else 1e-11)
+    np.testing.assert_allclose(out["db"], y.sum(0, keepdims=True), **tol)
+    X._CACHE.clear()
