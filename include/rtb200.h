@@ -290,6 +290,12 @@ typedef struct {
                         * into part2[blockIdx, r] (a bias gradient of the output,
                         * executor.find_colsum_epilogues; RT_K_SPLITK finishes) */
   uint64_t part2;
+  /* variant 2 vectorised + gate, dw != 0: also the weight gradient of the
+   * product's first operand against the gate operand, sum_rows h[w,c] X[w,k]
+   * (dW of the head whose backward this is: dW3 = h2^T dmu), fp64 partials
+   * per CTA into part3[blockIdx, c, k]; dw2: the same for X2 into part4 */
+  int32_t dw, dw2;
+  uint64_t part3, part4;
 } rt_thin_params;
 
 /* Point coordinates for per-point entropy: coordinate j of the node's

@@ -265,6 +265,17 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__
 #pragma unroll
   for (int j = 0; j < VW; ++j) cs[j] = 0.0;
   const bool colsum = p.colsum != 0;
+  // dw (GATE): sum_rows h[c] * x[k] -- the first operand's weight gradient
+  constexpr int DK = GATE ? KP : 1, DK2 = GATE ? (KP2 > 0 ? KP2 : 1) : 1;
+  T dwa[VW][DK], dwb[VW][DK2];
+#pragma unroll
+  for (int j = 0; j < VW; ++j) {
+#pragma unroll
+    for (int k = 0; k < DK; ++k) dwa[j][k] = (T)0;
+#pragma unroll
+    for (int k = 0; k < DK2; ++k) dwb[j][k] = (T)0;
+  }
+  const bool dw = GATE && p.dw != 0, dw2 = GATE && KP2 > 0 && p.dw2 != 0;
   const int cg = (int)threadIdx.x % G, rl = (int)threadIdx.x / G;
   const T* X = (const T*)p.X.ptr + p.X.off;
   const T* Y = (const T*)p.Y.ptr + p.Y.off;
@@ -314,11 +325,24 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__
       }
     }
     __syncthreads();
-#pragma unroll 2
-    for (int rr = rl; rr < nrow; rr += RL) {
+    // GATE: the h rows of HB row steps are loaded together (one 16-byte load
+    // per row in flight per thread left the kernel latency-bound, ~3 TB/s)
+    constexpr int HB = GATE ? 8 : 1;
+    for (int rb = rl; rb < nrow; rb += HB * RL) {
+    V hvb[HB];
+    if constexpr (GATE) {
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+        const int rr = rb + u * RL;
+        if (rr < nrow) hvb[u] = __ldcs(reinterpret_cast<const V*>(Hg + coff[rr] + c0));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < HB; ++u) {
+      const int rr = rb + u * RL;
+      if (rr >= nrow) break;
       const int64_t co = coff[rr] + c0;
-      V hv;
-      if constexpr (GATE) hv = __ldcs(reinterpret_cast<const V*>(Hg + co));
+      V hv = hvb[u];
       T a[VW];
 #pragma unroll
       for (int j = 0; j < VW; ++j) a[j] = (T)0;
@@ -336,6 +360,24 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__
       if constexpr (GATE) {
         T h[VW];
         v_unpack(hv, h);
+        if (dw) {
+#pragma unroll
+          for (int k = 0; k < DK; ++k) {
+            const T xk_ = xs[rr * KP + k];
+#pragma unroll
+            for (int j = 0; j < VW; ++j) dwa[j][k] = fma(h[j], xk_, dwa[j][k]);
+          }
+        }
+        if constexpr (KP2 > 0) {
+          if (dw2) {
+#pragma unroll
+            for (int k = 0; k < DK2; ++k) {
+              const T xk_ = xs2[rr * KP2 + k];
+#pragma unroll
+              for (int j = 0; j < VW; ++j) dwb[j][k] = fma(h[j], xk_, dwb[j][k]);
+            }
+          }
+        }
         // numpy order, no contraction: gy * (1 - h*h)
 #pragma unroll
         for (int j = 0; j < VW; ++j) a[j] = mul_rn(a[j], sub_rn((T)1, mul_rn(h[j], h[j])));
@@ -357,6 +399,32 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__
       if (colsum) {     // fp64 per row: the sum keeps the reference's accuracy
 #pragma unroll
         for (int j = 0; j < VW; ++j) cs[j] += (double)a[j];
+      }
+    }
+    }
+  }
+  if (dw || dw2) {
+    // this CTA's weight-gradient partials: row lanes in order, fp64
+    for (int which = 0; which < 2; ++which) {
+      const int KK = which ? K2 : K;
+      if (which ? !dw2 : !dw) continue;
+      for (int k = 0; k < KK; ++k) {
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < VW; ++j) {
+          T v = (T)0;
+#pragma unroll
+          for (int kk = 0; kk < (DK > DK2 ? DK : DK2); ++kk)
+            if (kk == k) v = which ? (kk < DK2 ? dwb[j][kk < DK2 ? kk : 0] : (T)0)
+                                   : (kk < DK ? dwa[j][kk < DK ? kk : 0] : (T)0);
+          csum[rl * R + c0 + j] = (double)v;
+        }
+        __syncthreads();
+        for (int c = (int)threadIdx.x; c < R; c += THREADS) {
+          double t = 0.0;
+          for (int l = 0; l < RL; ++l) t += csum[l * R + c];
+          ((double*)(which ? p.part4 : p.part3))[((int64_t)blockIdx.x * R + c) * KK + k] = t;
+        }
       }
     }
   }
@@ -466,18 +534,36 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
             for (int r = 0; r < R; ++r) acc[rr][r] = fma(x, y[i][j][r], acc[rr][r]);
           }
     }
-    T mine = (T)0;
+    // the RW x R dot products across the warp by recursive halving: at each
+    // level a lane keeps half of its values and receives the partner's copy
+    // of that half (NV - 1 + 5 - log2 NV shuffles instead of 5 NV)
+    constexpr int NV = RW * R;
+    constexpr int LG = NV >= 32 ? 5 : NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : NV >= 2 ? 1 : 0;
+    static_assert((1 << LG) == NV, "power-of-two row x output count");
+    T v[NV];
 #pragma unroll
     for (int rr = 0; rr < RW; ++rr)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        T v = acc[rr][r];
+      for (int r = 0; r < R; ++r) v[rr * R + r] = acc[rr][r];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == rr * R + r) mine = v;
+    for (int sl = 0; sl < LG; ++sl) {
+      const int n = NV >> sl, o = 16 >> sl;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        const T send = up ? v[i] : v[i + n / 2];
+        const T keep = up ? v[i + n / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
-    if (lane < RW * R) {
-      const int rr = lane / R, r = lane - rr * R;
+    }
+#pragma unroll
+    for (int o = 16 >> LG; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    const T mine = v[0];
+    int idx = 0;
+#pragma unroll
+    for (int sl = 0; sl < LG; ++sl) idx |= ((lane >> (4 - sl)) & 1) << (LG - 1 - sl);
+    if ((lane & ((1 << (5 - LG)) - 1)) == 0) {
+      const int rr = idx / R, r = idx - rr * R;
       const int64_t w = w0 + rr;
       if (w < p.w && r < p.r) {
         T* cptr = Cp + wdec(p.W, w, p.C.s1) + r * p.C.s2[0];

@@ -337,6 +337,103 @@ def find_aliases(g: Graph, pshape):
 ONES_BIAS = os.environ.get("RTB200_ONES_BIAS", "1") != "0"
 
 
+DW_EPI = os.environ.get("RTB200_DW_EPI", "1") != "0"
+
+
+def pshape_k(g, e):
+    """Contraction length of a per-point matmul operand edge (its last
+    payload extent), from the node's declared shape (ints only)."""
+    shp = g.nodes[e.src].out_shapes[e.oid]
+    try:
+        return int(shp[-1]) if shp else 1
+    except (TypeError, ValueError):
+        return 1 << 30
+
+
+def _plan_order(steps):
+    order = {}
+
+    def walk(sts):
+        for st in sts:
+            if hasattr(st, "nid"):
+                order.setdefault(st.nid, len(order))
+            else:
+                walk(st.body)
+    walk(steps)
+    return order
+
+
+def find_dw_epilogues(g: Graph, gemm_epi, contract, fixed_of, ext, steps, skip):
+    """The head's weight gradient from the launch of its backward product:
+    for a gate-fused small-K product y = (gz @ W^T [+ gz2 @ W2^T]) * (1-h*h)
+    (the VJP into a tanh layer h from narrow heads), a contraction
+    S = sum(matmul(permute(h), gz)[kept, 0:B, 0:T]) -- dW = h^T gz over the
+    same rows, reference frontend.py:984-989 -- is accumulated by the same
+    launch, which already holds h (the gate) and gz (its operand) per row
+    (k_thin_smallv dw / dw2).  Returns {y: [(S, 0 | 1 for gz / gz2)]}; the
+    lowering falls back to the separate contraction when the vectorised
+    kernel does not run."""
+    order = _plan_order(steps)
+    idx = {}
+    for sid, xid in contract.items():
+        if sid in skip:
+            continue
+        x = g.nodes[xid]
+        ins = sorted(g.in_edges(xid), key=lambda e: e.iid)
+        if len(ins) != 2:
+            continue
+        ea, eb = ins
+        pm = g.nodes[ea.src]
+        if pm.kind != "permute" or tuple(pm.params.get("order", ())) != (1, 0):
+            continue
+        pin = g.in_edges(pm.id)
+        if len(pin) != 1 or not _is_identity(ea, pm, x) or \
+                not _is_identity(pin[0], g.nodes[pin[0].src], pm) or \
+                not _is_identity(eb, g.nodes[eb.src], x):
+            continue
+        (es,) = g.in_edges(sid)
+        idx[(pin[0].src, pin[0].oid, eb.src, eb.oid)] = (sid, x, es)
+    out = {}
+    for y, (x, _b, t) in gemm_epi.items():
+        if not isinstance(t, tuple) or t[0] != "gate":
+            continue
+        he = t[3]
+        prods = [x] + ([t[5]] if len(t) > 5 else [])
+        ax = [e for e in g.in_edges(x) if e.iid == 0]
+        if not ax or pshape_k(g, ax[0]) > 16:
+            continue      # only the small-K (vectorised thin) product carries it
+        res = []
+        for which, xp in enumerate(prods):
+            a = [e for e in g.in_edges(xp) if e.iid == 0]
+            if not a:
+                continue
+            hit = idx.get((he.src, he.oid, a[0].src, a[0].oid))
+            if hit is None:
+                continue
+            sid, xs_, es = hit
+            if xs_.domain != g.nodes[y].domain:
+                continue
+            kept = [d for d, c in zip(xs_.domain, es.phi) if c == ("sym", d, "loop")]
+            sl = [d for d, c in zip(xs_.domain, es.phi)
+                  if c[0] == "slice" and c[1] == ("int", 0) and c[2] == ("sym", g.dim_bound[d], "bound")]
+            if len(kept) + len(sl) != len(xs_.domain) or not sl or \
+                    tuple(kept) != tuple(g.nodes[sid].domain) or \
+                    fixed_of.get(sid) != fixed_of.get(y) or \
+                    any(d not in fixed_of.get(y, ()) and ext.get(d, 1) != 1 for d in kept):
+                continue
+            # S is computed by y's launch: earlier than its own place (safe) or
+            # later, then no reader may sit in between
+            # (a reader placed before S's own place reads an earlier iteration's
+            # value: only readers between S's place and y's can see it early)
+            os_, oy = order.get(sid, -1), order.get(y, 1 << 30)
+            if oy > os_ and any(os_ < order.get(e.sink, -1) <= oy for e in g.out_edges(sid)):
+                continue
+            res.append((sid, which))
+        if res:
+            out[y] = res
+    return out
+
+
 def out_ids_of(g):
     return {nid for _, nid, _ in g.outputs}
 
@@ -887,13 +984,18 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True, skew=None):
         for sid, rid in list(ones.items()):
             # the contraction launches at its own place and writes the sum:
             # every reader of the sum must come after it
+            # (computed at the contraction's place: earlier than the sum's own
+            # place is safe, later needs every reader after it)
             readers = [e.sink for e in g.out_edges(rid)]
-            if fixed_of.get(sid) != fixed_of.get(rid) or any(
-                    order.get(c, -1) <= order.get(sid, 1 << 30) for c in readers):
+            orr, osd = order.get(rid, -1), order.get(sid, 1 << 30)
+            if fixed_of.get(sid) != fixed_of.get(rid) or osd > orr and any(
+                    orr < order.get(c, -1) <= osd for c in readers):
                 del ones[sid]
     plan.ones_bias = ones      # the bias sums stay materialised: the contraction writes them
     plan.colsum = find_colsum_epilogues(g, gemm_epi, pshape, fixed_of, virtual | set(ones.values()),
                                         ext) if fuse else {}
+    plan.dw_epi = find_dw_epilogues(g, gemm_epi, contract, fixed_of, ext, plan.steps,
+                                    set(ones)) if fuse and DW_EPI else {}
     for f, (x, _b, t) in gemm_epi.items():
         virtual.add(x)
         if isinstance(t, tuple):

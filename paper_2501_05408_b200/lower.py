@@ -306,6 +306,8 @@ class Lowering:
         self.colsum = dict(getattr(plan, "colsum", {}) or {})   # gate product -> its row sum
         self._colsum_done = set()
         self._colsum_req = None
+        self.dw_epi = dict(getattr(plan, "dw_epi", {}) or {})   # gate product -> [(dW sum, which)]
+        self._dw_req = None
         for f, (x, _b, t) in self.gemm_epi.items():
             self.virtual.add(x)
             if isinstance(t, tuple):           # tanh-VJP gate: (1 - h*h) chain
@@ -989,8 +991,22 @@ class Lowering:
             return    # a bias sum written by its contraction's launch (ones column)
         if n.id in self._colsum_done:
             self._colsum_done.discard(n.id)   # (per plan instance: its producer ran just before)
-            return    # summed by its producer's launch (k_thin_smallv colsum)
+            return    # summed by its producer's launch (k_thin_smallv colsum / dw)
         ctx = Ctx(self, n, s.fixed)
+        if n.id in self.dw_epi and self._capture is None:
+            reqs = []
+            for sid, which in self.dw_epi[n.id]:
+                skey = (sid, 0)
+                ss = self.storage(skey)
+                sdst = {d: ss.strides[j] for j, d in enumerate(self.bufs[skey].dims)}
+                g_ = N.rt_gop()
+                g_.ptr, g_.dtype, g_.off = ss.ptr, N.DTYPE_CODE[ss.dtype], 0
+                for d in ctx.fixed:
+                    if d in sdst:
+                        g_.off_env[self.slot[d]] += sdst[d]
+                g_.s1[0], g_.s2[0] = ss.strides[-2], ss.strides[-1]
+                reqs.append((sid, which, g_))
+            self._dw_req = reqs
         if n.id in self.colsum and self._capture is None:
             rkey = (self.colsum[n.id], 0)
             sr = self.storage(rkey)
@@ -1034,6 +1050,7 @@ class Lowering:
                 fn = self.ew
             fn(ctx)
         self._colsum_req = None
+        self._dw_req = None
         if n.id in self.shard_reduce:
             self._hook_allreduce(ctx, (n.id, 0))
 
@@ -2195,11 +2212,34 @@ class Lowering:
         if self.THIN_VEC and self._smallk_vec_ok(q, kp, f64, gate is not None):
             q.vec, smem = 1, 0           # k_thin_smallv: static shared memory
         grid = [int(min((m + 63) // 64, 148 * 8)), 1, 1]
+        self._dw_recs = []
         req = self._colsum_req
         if req is not None and q.vec and gate is not None and not accumulate:
             # the row sum of this output (its bias gradient) from the same launch
             q.colsum, q.part2 = 1, self.alloc(grid[0] * q.r * 8)
         self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
+        for sid, which, gd in (self._dw_req or []) if (q.vec and gate is not None) else []:
+            kk = q.k2 if which else q.k
+            if which and not q.k2:
+                continue
+            part = self.alloc(grid[0] * q.r * kk * 8)
+            if which:
+                q.dw2, q.part4 = 1, part
+            else:
+                q.dw, q.part3 = 1, part
+            r3 = N.rt_splitk_params()
+            r3.Z.nd = r3.M.nd = r3.N.nd = 1
+            r3.Z.ext[0] = 1
+            r3.M.ext[0], r3.N.ext[0] = q.r, kk
+            r3.z, r3.m, r3.n = 1, q.r, kk
+            r3.splits, r3.f64 = grid[0], 1          # fp64 partials, stored in C's dtype
+            r3.part, r3.C = part, gd
+            self._dw_recs.append((r3, [int(min((q.r * kk + 7) // 8, 148 * 16)), 1, 1],
+                                  (sid, self.g.nodes[sid].name)))
+            self._colsum_done.add(sid)
+        for r3, g3, lab in self._dw_recs:
+            self.add_rec(N.RT_K_SPLITK, r3, g3, [256, 1, 1], 0, lab)
+        self._dw_recs = []
         if q.colsum:
             rid, gc = req
             r2 = N.rt_splitk_params()

@@ -512,8 +512,8 @@ def test_bias_gradient_rides_the_weight_contraction(dt):
 
 @pytest.mark.parametrize("dt", ["f32", "f64"])
 def test_bias_gradient_summed_by_the_gate_launch(dt):
-    """d(hidden) = (g @ W) * (1 - h*h) and its bias gradient sum(d(hidden))
-    over the points from ONE launch: the vectorised gate kernel accumulates
+    """d(hidden) = (g @ W) * (1 - h*h), its bias gradient sum(d(hidden)) and
+    the head's weight gradient sum(h^T g) over the points from ONE launch: the vectorised gate kernel accumulates
     fp64 column sums per CTA (colsum), a split-K pass finishes them; no
     separate column reduction; both match float64 numpy."""
     from paper_2501_05408_b200 import executor as X, get_executable, native as N
@@ -523,21 +523,24 @@ def test_bias_gradient_summed_by_the_gate_launch(dt):
              ("h", "input", ("b",), (1, H), 0), ("m", "matmul", ("b",), (1, H), 2),
              ("hh", "mul", ("b",), (1, H), 2), ("one", "const", (), (), 0),
              ("om", "sub", ("b",), (1, H), 2), ("y", "mul", ("b",), (1, H), 2),
-             ("db", "sum", (), (1, H), 1)]
+             ("db", "sum", (), (1, H), 1), ("ht", "permute", ("b",), (H, 1), 1),
+             ("xw", "matmul", ("b",), (H, K), 2), ("dW", "sum", (), (H, K), 1)]
     ids = {}
     npd = np.float32 if dt == "f32" else np.float64
     for i, (name, kind, dom, shp, nin) in enumerate(nodes):
         params = {"value": np.array(1.0, dtype=npd)} if kind == "const" else \
-            ({"dims": (0,)} if kind == "sum" else {})
+            ({"dims": (0,)} if kind == "sum" else ({"order": (1, 0)} if kind == "permute" else {}))
         g.nodes[i] = ir.Node(i, name, kind, dom, (shp,), (dt,), params, nin)
         ids[name] = i
     b = (S("b"),)
     for snk, srcs in (("m", [("gz", b), ("W", ())]), ("hh", [("h", b), ("h", b)]),
                       ("om", [("one", ()), ("hh", b)]), ("y", [("m", b), ("om", b)]),
-                      ("db", [("y", (("slice", ("int", 0), S("B", "bound")),))])):
+                      ("db", [("y", (("slice", ("int", 0), S("B", "bound")),))]),
+                      ("ht", [("h", b)]), ("xw", [("ht", b), ("gz", b)]),
+                      ("dW", [("xw", (("slice", ("int", 0), S("B", "bound")),))])):
         for iid, (src, phi) in enumerate(srcs):
             g.edges.append(ir.Edge(ids[snk], iid, phi, None, 0, ids[src]))
-    g.outputs = [("y", ids["y"], 0), ("db", ids["db"], 0)]
+    g.outputs = [("y", ids["y"], 0), ("db", ids["db"], 0), ("dW", ids["dW"], 0)]
     rng = np.random.default_rng(3)
     inp = {"gz": rng.standard_normal((B, 1, K)).astype(npd),
            "W": rng.standard_normal((K, H)).astype(npd),
@@ -545,7 +548,9 @@ def test_bias_gradient_summed_by_the_gate_launch(dt):
     X._CACHE.clear()
     exe, _ = get_executable(g, {}, inp, 0)
     thin = [p for k, p in zip(exe.kernels, exe._params) if k == N.RT_K_THIN]
-    assert len(thin) == 1 and thin[0].colsum == 1 and thin[0].vec == 1
+    # one launch: d(hidden), its bias gradient (colsum) and the head's weight
+    # gradient h^T gz (dw); only split-K finishes after it
+    assert len(thin) == 1 and thin[0].colsum == 1 and thin[0].vec == 1 and thin[0].dw == 1
     assert N.RT_K_REDUCE not in exe.kernels
     out = execute(g, inputs=inp)
     y = (inp["gz"][:, 0].astype(np.float64) @ inp["W"].astype(np.float64)) * \
@@ -556,4 +561,6 @@ def test_bias_gradient_summed_by_the_gate_launch(dt):
     np.testing.assert_allclose(out["db"], out["y"][:, 0].astype(np.float64).sum(0, keepdims=True),
                                rtol=1e-6 if dt == "f32" else 1e-13, atol=1e-6 if dt == "f32" else 1e-11)
     np.testing.assert_allclose(out["db"], y.sum(0, keepdims=True), **tol)
+    dW = inp["h"][:, 0].astype(np.float64).T @ inp["gz"][:, 0].astype(np.float64)
+    np.testing.assert_allclose(out["dW"], dW, **(dict(rtol=1e-5, atol=2e-3) if dt == "f32" else tol))
     X._CACHE.clear()
