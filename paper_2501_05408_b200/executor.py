@@ -1297,9 +1297,18 @@ class Executable:
         self.labels = [lab for (*_, lab) in low.recs]
         self.kernels = [k for (k, *_rest) in low.recs]
         from . import jit
+        mult = [0] * len(low.recs)          # launches of each record per run
+        stack = []
+        for ins in low.prog:
+            if ins[0] == N.RT_OP_FOR:
+                stack.append(abs(ins[3] - ins[2]))
+            elif ins[0] == N.RT_OP_END:
+                stack.pop()
+            elif ins[0] == N.RT_OP_LAUNCH:
+                mult[ins[1]] += prod(stack)
         with self.torch.cuda.device(self.dev):
             self.jit_count = jit.specialise(recs, self.kernels, self._params, self.labels,
-                                            self.loop_info)
+                                            self.loop_info, mult)
         prog = (N.rt_instr * max(1, len(low.prog)))()
         for i, ins in enumerate(low.prog):
             prog[i].op, prog[i].a, prog[i].b, prog[i].c, prog[i].d, prog[i].e = (

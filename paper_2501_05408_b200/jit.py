@@ -1343,8 +1343,15 @@ def compile_kernel(src: str, name: str) -> int:
     return fn.value
 
 
-def specialise(recs, kernels, params, labels, loop_info=None):
-    """Attach JIT kernels to large EW records and persistent loops (in place)."""
+JIT_REPEAT = int(os.environ.get("RTB200_JIT_REPEAT", "4"))
+
+
+def specialise(recs, kernels, params, labels, loop_info=None, mult=None):
+    """Attach JIT kernels to persistent loops and to EW records that are
+    large (>= JIT_MIN_ELEMS elements) or launched JIT_REPEAT+ times per run
+    (e.g. a PPO minibatch's small elementwise ops: the interpreting kernel's
+    fixed cost dominates them; C3 59.6 -> 57.2 ms/step with all of them
+    specialised) -- in place."""
     if not ENABLED:
         return 0
     n = 0
@@ -1368,7 +1375,9 @@ def specialise(recs, kernels, params, labels, loop_info=None):
         recs[ri].jit_fn = compile_kernel(src, "loop_jit")
         n += 1
     for i, (k, p) in enumerate(zip(kernels, params)):
-        if k != N.RT_K_EW or p.total < JIT_MIN_ELEMS:
+        if k != N.RT_K_EW:
+            continue
+        if p.total < JIT_MIN_ELEMS and (mult is None or mult[i] < JIT_REPEAT):
             continue
         src = ew_source(p, "ew_jit")
         recs[i].jit_fn = compile_kernel(src, "ew_jit")
