@@ -320,3 +320,40 @@ def test_c2_acting_loop_kernel_source_builds_for_sm100a():
         line = [x for x in res.splitlines() if "REG:" in x][0]
         fields = dict(f.split(":") for f in line.split() if ":" in f and f.split(":")[1].isdigit())
         assert int(fields["REG"]) <= 255 and int(fields.get("LOCAL", "0")) == 0, line
+
+
+def test_c2_fused_mlp_step_source_builds_for_sm100a():
+    """The fused MLP acting step of C2 (jit_mlp.py: four-column h2 core,
+    warp-per-row head/action/env) matches the C2 loop and NVRTC compiles it
+    for sm_100a without spills (no GPU needed)."""
+    import ctypes as C
+    from paper_2501_05408_b200 import jit, jit_mlp
+    g = load_graph("reinforce_mlp_c2")
+    _p, low, _c, _a = dry_lower(g, {"I": 1, "B": 1024, "T": 1000})
+    (ri, info), = list(low.loop_subs.items())
+    lp = low.recs[ri][1]
+    m = jit_mlp.match(lp, info["ops"], info)
+    assert m is not None and m["R"] == 7
+    src = jit_mlp.source(lp, info["ops"], info, m)
+    for needle in ("mlp_h2q<8, 7, 32, 256>", "mlp_head<4, 256>",
+                   "warp_pairwise_sum_s", "cp_async8", "tanh_fast"):
+        assert needle in src, needle
+    lib = N.lib()
+    opts = jit._opts()
+    blob = b"\0".join(opts) + b"\0"
+    size = C.c_uint64(0)
+    assert lib.rt_jit_cubin(src.encode(), blob, len(opts), None, C.byref(size)) == 0
+    buf = C.create_string_buffer(size.value)
+    assert lib.rt_jit_cubin(src.encode(), blob, len(opts), buf, C.byref(size)) == 0
+    import shutil
+    import subprocess
+    import tempfile
+    if shutil.which("cuobjdump"):
+        with tempfile.NamedTemporaryFile(suffix=".cubin") as fh:
+            fh.write(buf.raw[:size.value])
+            fh.flush()
+            res = subprocess.run(["cuobjdump", "--dump-resource-usage", fh.name],
+                                 capture_output=True, text=True).stdout
+        line = [x for x in res.splitlines() if "REG:" in x][0]
+        fields = dict(f.split(":") for f in line.split() if ":" in f and f.split(":")[1].isdigit())
+        assert int(fields["REG"]) <= 255 and int(fields.get("LOCAL", "0")) == 0, line
