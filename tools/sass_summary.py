@@ -21,6 +21,16 @@ KEYS = ("UTCHMMA", "UTCQMMA", "UTCMMA", "LDTM", "STTM", "UTMALDG", "UTMASTG", "U
         "HMMA", "FFMA2", "FFMA", "DFMA", "LDS", "STS", "BAR", "SYNCS")
 
 
+def _demangle(fn):
+    """cu++filt, with the anonymous-namespace and parameter noise removed."""
+    try:
+        out = subprocess.run(["cu++filt", fn], capture_output=True, text=True).stdout.strip()
+    except OSError:
+        return fn
+    out = re.sub(r"\(anonymous namespace\)::", "", out or fn)
+    return re.sub(r"\((rt_|tm_|scan_)\w+\)$", "", out)
+
+
 def summarize(sass_text):
     out = OrderedDict()
     cur = None
@@ -48,7 +58,8 @@ def emit(title, counts):
     for fn, c in counts.items():
         if not any(c.values()):
             continue
-        short = fn if len(fn) < 60 else fn[:57] + "..."
+        short = _demangle(fn)
+        short = short if len(short) < 72 else short[:69] + "..."
         print(f"  {short:60s} " + " ".join(f"{k}={c[k]}" for k in KEYS if c[k]))
 
 
