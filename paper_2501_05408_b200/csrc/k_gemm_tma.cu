@@ -438,6 +438,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_c
 // the per-tile variant: ncu tensor pipe 29%, smem 31%, long-scoreboard
 // stalls on per-tile prologues).
 #define TP_ST 4
+#ifndef TM_PASSES
+#define TM_PASSES 3  // 3xTF32 (hi*hi + hi*lo + lo*hi); fewer only for bound experiments (wrong results)
+#endif
 #ifndef TP_PF
 #define TP_PF 0      // A-tile L2 prefetch distance (stages; 8 measured slower: h2_n 0.56 -> 0.74 ms)
 #endif
@@ -557,8 +560,12 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
             const uint64_t dah = op_desc(ahi, ks, a.a_mn), dal = op_desc(alo, ks, a.a_mn);
             const uint64_t dbh = op_desc(bhi, ks, a.b_mn), dbl = op_desc(blo, ks, a.b_mn);
             mma_tf32(acc, dah, dbh, idesc, (kt > 0 || ks > 0) ? 1u : 0u);
+#if TM_PASSES >= 2
             mma_tf32(acc, dah, dbl, idesc, 1u);
+#endif
+#if TM_PASSES >= 3
             mma_tf32(acc, dal, dbh, idesc, 1u);
+#endif
           }
           mma_commit(su32(&empty[s]));
         }
