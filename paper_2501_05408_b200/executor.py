@@ -335,6 +335,7 @@ def find_aliases(g: Graph, pshape):
 
 
 ONES_BIAS = os.environ.get("RTB200_ONES_BIAS", "1") != "0"
+REMAT = os.environ.get("RTB200_REMAT", "1") != "0"
 
 
 DW_EPI = os.environ.get("RTB200_DW_EPI", "1") != "0"
@@ -2030,6 +2031,11 @@ def get_executable(g, bounds=None, inputs=None, seed=0, device=None, shard=None,
     outer_benv = benv
     if block:
         from .blocking import block_dim
+        if swap and REMAT:
+            # the backward recomputes the loop's tanh layers from the kept
+            # observation instead of swapping them (remat.py)
+            from .remat import remat_chains
+            remat_chains(h, block[0])
         benv = block_dim(h, benv, block[0], int(block[1]))
     if shard is not None and comm is None:
         from .shard import TorchComm
