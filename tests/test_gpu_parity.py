@@ -291,3 +291,30 @@ def test_time_blocked_jit_loop_matches_interpreter(monkeypatch, bs):
                   block=("t", bs))
     for k in ref:
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6, err_msg=k)
+
+
+@pytest.mark.parametrize("B,T,bs", [(128, 400, 100), (32, 250, 64)])
+def test_rematerialised_backward_matches_swapped_layers(B, T, bs, monkeypatch):
+    """Long-horizon mode: the backward recomputing the loop's tanh layers
+    per time block (remat.py) gives the gradients of the run that swaps the
+    loop's own layers to the host and back, to the fp32 tolerance (the
+    recomputation rounds like the learner GEMMs, the loop like its FMA
+    chain: ~1e-7 relative per activation)."""
+    from golden_cases import load_graph
+    from paper_2501_05408_b200 import execute, executor as X
+    from paper_2501_05408_b200.workloads import mlp_inputs
+    g = load_graph("reinforce_mlp_c2")
+    bounds = {"I": 1, "B": B, "T": T}
+    inp = mlp_inputs()
+    X._CACHE.clear()
+    monkeypatch.setattr(X, "REMAT", False)
+    ref = execute(g, bounds=bounds, inputs=inp, seed=4, block=("t", bs), swap=1)
+    X._CACHE.clear()
+    monkeypatch.setattr(X, "REMAT", True)
+    got = execute(g, bounds=bounds, inputs=inp, seed=4, block=("t", bs), swap=1)
+    exe, _ = X.get_executable(g, bounds, inp, 4, block=("t", bs), swap=1)
+    assert exe.swap_plan is not None and \
+        sorted(exe.trace_names[k] for k in exe.swap_plan.keys) == ["a", "mu"]
+    for k in ref:
+        np.testing.assert_allclose(got[k], ref[k], rtol=2e-5, atol=1e-5, err_msg=k)
+    X._CACHE.clear()
