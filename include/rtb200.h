@@ -296,6 +296,11 @@ typedef struct {
    * per CTA into part3[blockIdx, c, k]; dw2: the same for X2 into part4 */
   int32_t dw, dw2;
   uint64_t part3, part4;
+  /* variant 3 with r2 > 0: a sibling head over the same rows, outputs
+   * r - r2 .. r - 1 from the weights Y2 (+ bias2) into C2 (the policy and
+   * value heads reading the trunk once, executor.find_sibling_rows) */
+  int64_t r2;
+  rt_gop C2, bias2;
 } rt_thin_params;
 
 /* Point coordinates for per-point entropy: coordinate j of the node's

@@ -470,6 +470,9 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
   const T* Y = (const T*)p.Y.ptr + p.Y.off;
   T* Cp = (T*)p.C.ptr + p.C.off;
   const int64_t xk = p.X.s1[0];
+  // outputs r < r1 from (Y, bias, C); r1 <= r < r from the sibling (Y2, bias2, C2)
+  const int r1 = (int)(p.r - p.r2);
+  const T* Y2 = (const T*)p.Y2.ptr + p.Y2.off;
   T y[KI][VW][R];
 #pragma unroll
   for (int i = 0; i < KI; ++i)
@@ -478,14 +481,18 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
       const int k = (i * 32 + lane) * VW + j;
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        y[i][j][r] = (k < K && r < p.r) ? Y[k * p.Y.s1[0] + r * p.Y.s2[0]] : (T)0;
+        y[i][j][r] = !(k < K && r < p.r) ? (T)0
+                     : r < r1 ? Y[k * p.Y.s1[0] + r * p.Y.s2[0]]
+                              : Y2[k * p.Y2.s1[0] + (r - r1) * p.Y2.s2[0]];
     }
   T bias[R];
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    bias[r] = (p.bias.ptr && r < p.r)
-                  ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype, p.bias.off + r * p.bias.s2[0])
-                  : (T)0;
+    bias[r] = r < r1 ? (p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
+                                                 p.bias.off + r * p.bias.s2[0]) : (T)0)
+            : r < p.r ? (p.bias2.ptr ? load_as<T>((const void*)p.bias2.ptr, p.bias2.dtype,
+                                                   p.bias2.off + (r - r1) * p.bias2.s2[0]) : (T)0)
+                      : (T)0;
   const int64_t gw = (int64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * (THREADS / 32);
   for (int64_t w0 = gw * RW; w0 < p.w; w0 += nw * RW) {
@@ -566,7 +573,8 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
       const int rr = idx / R, r = idx - rr * R;
       const int64_t w = w0 + rr;
       if (w < p.w && r < p.r) {
-        T* cptr = Cp + wdec(p.W, w, p.C.s1) + r * p.C.s2[0];
+        T* cptr = r < r1 ? Cp + wdec(p.W, w, p.C.s1) + r * p.C.s2[0]
+                         : (T*)p.C2.ptr + p.C2.off + wdec(p.W, w, p.C2.s1) + (r - r1) * p.C2.s2[0];
         T a = mine;
         if (p.accumulate) a += *cptr;
         a += bias[r];
@@ -589,9 +597,9 @@ extern "C" void* rt_kernel_thin_rows(int f64, int r, int k) {
     return (void*)k_thin_rows<T, R, 8>;                          \
   }
   if (f64) {
-    RT_ROWS(double, 1) RT_ROWS(double, 2) RT_ROWS(double, 4)
+    RT_ROWS(double, 1) RT_ROWS(double, 2) RT_ROWS(double, 4) RT_ROWS(double, 8)
   } else {
-    RT_ROWS(float, 1) RT_ROWS(float, 2) RT_ROWS(float, 4)
+    RT_ROWS(float, 1) RT_ROWS(float, 2) RT_ROWS(float, 4) RT_ROWS(float, 8)
   }
 #undef RT_ROWS
   return nullptr;

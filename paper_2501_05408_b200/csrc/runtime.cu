@@ -177,7 +177,14 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
       fold_gop(p->Y, env, nenv);
       fold_gop(p->C, env, nenv);
       if (p->bias.ptr) fold_gop(p->bias, env, nenv);
-      if (p->variant == 3) return rt_kernel_thin_rows(p->f64, (int)p->r, (int)p->k);
+      if (p->variant == 3) {
+        if (p->r2 > 0) {
+          fold_gop(p->Y2, env, nenv);
+          fold_gop(p->C2, env, nenv);
+          if (p->bias2.ptr) fold_gop(p->bias2, env, nenv);
+        }
+        return rt_kernel_thin_rows(p->f64, (int)p->r, (int)p->k);
+      }
       // variant 2 with epilogue 2 (gate) is a separate instantiation ("4"),
       // with a second summed product ("5")
       if (p->variant == 2 && p->k2 > 0) {

@@ -339,6 +339,44 @@ REMAT = os.environ.get("RTB200_REMAT", "1") != "0"
 
 
 DW_EPI = os.environ.get("RTB200_DW_EPI", "1") != "0"
+SIBLING = os.environ.get("RTB200_SIBLING", "1") != "0"
+
+
+def find_sibling_rows(g: Graph, gemm_epi, fixed_of, skip):
+    """Two narrow heads over the same rows (matmul + bias of one operand,
+    e.g. the policy head mu = h2 W3 + b3 and the value head V = h2 Wv + bv,
+    reference frontend.py matmul/add): one row-stream launch reads the shared
+    operand once and writes both (RT_K_THIN variant 3 with a sibling).
+    Returns {first head: second head}; the lowering falls back to two
+    launches when the row kernel does not run."""
+    groups = {}
+    for y, (x, _b, t) in gemm_epi.items():
+        if t or y in skip:
+            continue
+        ins = [e for e in g.in_edges(x) if e.iid == 0]
+        if not ins:
+            continue
+        e = ins[0]
+        xn = g.nodes[x]
+        if not _is_identity(e, g.nodes[e.src], xn) or xn.dtype not in ("f32", "f64"):
+            continue
+        shp = xn.out_shapes[0]
+        try:
+            nout = int(shp[-1])
+        except (TypeError, ValueError):
+            continue
+        if nout > 4:
+            continue
+        groups.setdefault((e.src, e.oid, fixed_of.get(y), g.nodes[y].domain), []).append((y, nout))
+    out = {}
+    for members in groups.values():
+        members.sort()
+        while len(members) >= 2:
+            (y1, n1), (y2, n2) = members[0], members[1]
+            members = members[2:]
+            if n1 + n2 <= 8:
+                out[y1] = y2
+    return out
 
 
 def pshape_k(g, e):
@@ -995,6 +1033,7 @@ def analyze(g: Graph, benv, pshape, fuse=True, fold=True, skew=None):
     plan.ones_bias = ones      # the bias sums stay materialised: the contraction writes them
     plan.colsum = find_colsum_epilogues(g, gemm_epi, pshape, fixed_of, virtual | set(ones.values()),
                                         ext) if fuse else {}
+    plan.sibling = find_sibling_rows(g, gemm_epi, fixed_of, virtual) if fuse and SIBLING else {}
     plan.dw_epi = find_dw_epilogues(g, gemm_epi, contract, fixed_of, ext, plan.steps,
                                     set(ones)) if fuse and DW_EPI else {}
     for f, (x, _b, t) in gemm_epi.items():

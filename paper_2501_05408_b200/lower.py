@@ -308,6 +308,10 @@ class Lowering:
         self._colsum_req = None
         self.dw_epi = dict(getattr(plan, "dw_epi", {}) or {})   # gate product -> [(dW sum, which)]
         self._dw_req = None
+        self.sibling = dict(getattr(plan, "sibling", {}) or {})  # head -> sibling head
+        self._rows_capture = None
+        self._rows_second = None
+        self._sibling_done = set()
         for f, (x, _b, t) in self.gemm_epi.items():
             self.virtual.add(x)
             if isinstance(t, tuple):           # tanh-VJP gate: (1 - h*h) chain
@@ -992,7 +996,24 @@ class Lowering:
         if n.id in self._colsum_done:
             self._colsum_done.discard(n.id)   # (per plan instance: its producer ran just before)
             return    # summed by its producer's launch (k_thin_smallv colsum / dw)
+        if n.id in self._sibling_done:
+            self._sibling_done.discard(n.id)
+            return    # written by its sibling head's launch
         ctx = Ctx(self, n, s.fixed)
+        if n.id in self.sibling and self._capture is None:
+            # the sibling head first, captured (its operands only)
+            y2 = self.g.nodes[self.sibling[n.id]]
+            x2, b2, _t2 = self.gemm_epi[y2.id]
+            self._rows_capture = []
+            try:
+                self.k_matmul(Ctx(self, y2, s.fixed), self.g.nodes[x2], b2, 0)
+                cap = self._rows_capture
+            except LowerError:
+                cap = []
+            finally:
+                self._rows_capture = None
+            if len(cap) == 1:
+                self._rows_second = (y2.id, cap[0])
         if n.id in self.dw_epi and self._capture is None:
             reqs = []
             for sid, which in self.dw_epi[n.id]:
@@ -1051,6 +1072,7 @@ class Lowering:
             fn(ctx)
         self._colsum_req = None
         self._dw_req = None
+        self._rows_second = None
         if n.id in self.shard_reduce:
             self._hook_allreduce(ctx, (n.id, 0))
 
@@ -2323,6 +2345,24 @@ class Lowering:
         q.vec = int(k % vw == 0 and (A.ptr + esize * A.off) % 16 == 0
                     and all(t[1] % vw == 0 for t in mdims)
                     and all(A.off_env[e] % vw == 0 for e in range(N.RT_MAXENV)))
+        if self._rows_capture is not None:
+            self._rows_capture.append(q)        # a sibling head, merged by its partner
+            return True
+        sec = self._rows_second
+        if sec is not None:
+            sid, q2 = sec
+            same_x = q2.X.ptr == q.X.ptr and q2.X.off == q.X.off and \
+                all(q2.X.off_env[e] == q.X.off_env[e] for e in range(N.RT_MAXENV)) and \
+                all(q2.X.s2[i] == q.X.s2[i] for i in range(4))
+            if same_x and q2.w == q.w and q2.k == q.k and q2.f64 == q.f64 and \
+                    q.r + q2.r <= 8 and ki * vw * 8 <= 64 and not accumulate and \
+                    not q2.accumulate and q.epilogue == 0 and q2.epilogue == 0 and \
+                    q2.W.nd == q.W.nd and all(q2.W.ext[i] == q.W.ext[i] for i in range(q.W.nd)):
+                q.r2 = q2.r
+                q.r = q.r + q2.r
+                q.Y2, q.C2, q.bias2 = q2.Y, q2.C, q2.bias
+                self._sibling_done.add(sid)
+            self._rows_second = None
         rows_per_cta = 8 * 8
         grid = [int(max(1, min(-(-m // rows_per_cta), 148 * 16))), 1, 1]
         self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], 0, label)

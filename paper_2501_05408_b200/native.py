@@ -122,7 +122,8 @@ class rt_thin_params(C.Structure):
                 ("part_w", i64), ("part_r", i64), ("part", u64), ("X", rt_gop), ("Y", rt_gop),
                 ("C", rt_gop), ("bias", rt_gop), ("W", rt_gbox), ("k2", i64), ("X2", rt_gop),
                 ("Y2", rt_gop), ("ones", i32), ("colsum", i32), ("part2", u64), ("dw", i32),
-                ("dw2", i32), ("part3", u64), ("part4", u64)]
+                ("dw2", i32), ("part3", u64), ("part4", u64), ("r2", i64),
+                ("C2", rt_gop), ("bias2", rt_gop)]
 
 
 class rt_rng_params(C.Structure):

@@ -564,3 +564,45 @@ def test_bias_gradient_summed_by_the_gate_launch(dt):
     dW = inp["h"][:, 0].astype(np.float64).T @ inp["gz"][:, 0].astype(np.float64)
     np.testing.assert_allclose(out["dW"], dW, **(dict(rtol=1e-5, atol=2e-3) if dt == "f32" else tol))
     X._CACHE.clear()
+
+
+@pytest.mark.parametrize("dt,n1,n2", [("f32", 4, 1), ("f64", 4, 1), ("f32", 2, 2)])
+def test_sibling_heads_share_one_row_stream(dt, n1, n2):
+    """mu = h @ W3 + b3 and V = h @ Wv + bv over the same rows (the PPO
+    policy and value heads, reference frontend.py matmul/add) from ONE
+    row-stream launch that reads h once (find_sibling_rows), vs numpy."""
+    from paper_2501_05408_b200 import executor as X, get_executable, native as N
+    B, K = 20000, 256
+    npd = np.float32 if dt == "f32" else np.float64
+    g = ir.Graph(["b"], {"b": "B"}, {"B": B})
+    nodes = [("h", "input", ("b",), (1, K), 0), ("W3", "input", (), (K, n1), 0),
+             ("b3", "input", (), (1, n1), 0), ("Wv", "input", (), (K, n2), 0),
+             ("bv", "input", (), (1, n2), 0), ("m3", "matmul", ("b",), (1, n1), 2),
+             ("mu", "add", ("b",), (1, n1), 2), ("mv", "matmul", ("b",), (1, n2), 2),
+             ("V", "add", ("b",), (1, n2), 2)]
+    ids = {}
+    for i, (name, kind, dom, shp, nin) in enumerate(nodes):
+        g.nodes[i] = ir.Node(i, name, kind, dom, (shp,), (dt,), {}, nin)
+        ids[name] = i
+    b = (S("b"),)
+    for snk, srcs in (("m3", [("h", b), ("W3", ())]), ("mu", [("m3", b), ("b3", ())]),
+                      ("mv", [("h", b), ("Wv", ())]), ("V", [("mv", b), ("bv", ())])):
+        for iid, (src, phi) in enumerate(srcs):
+            g.edges.append(ir.Edge(ids[snk], iid, phi, None, 0, ids[src]))
+    g.outputs = [("mu", ids["mu"], 0), ("V", ids["V"], 0)]
+    rng = np.random.default_rng(n1 * 10 + n2)
+    inp = {"h": np.tanh(rng.standard_normal((B, 1, K))).astype(npd),
+           "W3": (rng.standard_normal((K, n1)) / 16).astype(npd),
+           "b3": rng.standard_normal((1, n1)).astype(npd),
+           "Wv": (rng.standard_normal((K, n2)) / 16).astype(npd),
+           "bv": rng.standard_normal((1, n2)).astype(npd)}
+    X._CACHE.clear()
+    exe, _ = get_executable(g, {}, inp, 0)
+    thin = [p for k, p in zip(exe.kernels, exe._params) if k == N.RT_K_THIN]
+    assert len(thin) == 1 and thin[0].variant == 3 and thin[0].r2 == n2 and exe.launch_count == 1
+    out = execute(g, inputs=inp)
+    h64 = inp["h"][:, 0].astype(np.float64)
+    tol = 1e-5 if dt == "f32" else 1e-12
+    np.testing.assert_allclose(out["mu"][:, 0], h64 @ inp["W3"] + inp["b3"], rtol=tol, atol=tol)
+    np.testing.assert_allclose(out["V"][:, 0], h64 @ inp["Wv"] + inp["bv"], rtol=tol, atol=tol)
+    X._CACHE.clear()

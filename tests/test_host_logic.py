@@ -201,14 +201,17 @@ def test_ppo_env_shard_co_shards_minibatch_envs():
 
 def test_ppo_heads_use_row_stream_gemm():
     """mu_n (N=4) and V_n (N=1) over a minibatch's (u,t) rows are narrow-N
-    row streams (thin variant 3), not 128x256 tensor-core tiles."""
+    row streams (thin variant 3), not 128x256 tensor-core tiles -- and ONE
+    launch per minibatch writes both (find_sibling_rows: the trunk's h2_n
+    is read once)."""
     g = load_graph("ppo_c3")
     plan, low, _, _ = dry_lower(g, PPO_BOUNDS)
     fam = {}
     for (k, p, *_r, lab) in low.recs:
         if lab[1] in ("mu_n", "V_n", "V"):
-            fam.setdefault(lab[1], set()).add((k, getattr(p, "variant", None)))
-    assert fam["mu_n"] == {(N.RT_K_THIN, 3)} and fam["V_n"] == {(N.RT_K_THIN, 3)}
+            fam.setdefault(lab[1], set()).add((k, getattr(p, "variant", None),
+                                               getattr(p, "r", None), getattr(p, "r2", None)))
+    assert fam["mu_n"] == {(N.RT_K_THIN, 3, 5, 1)} and "V_n" not in fam
 
 
 def test_time_blocking_shrinks_long_horizon_plan():
