@@ -54,7 +54,8 @@ struct tm_args {
   int64_t g_m, g_n;        // epilogue 2: the gate operand's strides (in p.bias)
   CUtensorMap tbh, tbl;    // PRESPLIT: B's tf32 hi / lo parts (same geometry as tb)
   uint64_t b_base, b_span; // PRESPLIT: B element base address and span (elements)
-  int32_t presplit, _pad2;
+  int32_t presplit, _pad2; // 1: B split in place; 2: split AND transposed to K-major
+  int64_t b_ld, b_kk, b_nn; // presplit 2: the MN-major source's row stride, K, N
 };
 
 namespace {
@@ -438,6 +439,20 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_c
 // the per-tile variant: ncu tensor pipe 29%, smem 31%, long-scoreboard
 // stalls on per-tile prologues).
 #define TP_ST 4
+#ifndef TM_TRACE
+#define TM_TRACE 0
+#endif
+#if TM_TRACE
+// per-role timestamps of CTA 0 (globaltimer ns): [role][event]
+__device__ long long g_tm_trace[8][512];
+#define TM_TS(role, idx) do { if (blockIdx.x == 0 && (idx) < 512) { long long t_; \
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_tm_trace[role][idx] = t_; } } while (0)
+#else
+#define TM_TS(role, idx) do {} while (0)
+#endif
+#ifndef TM_NO_B
+#define TM_NO_B 0
+#endif
 #ifndef TM_PASSES
 #define TM_PASSES 3  // 3xTF32 (hi*hi + hi*lo + lo*hi); fewer only for bound experiments (wrong results)
 #endif
@@ -516,13 +531,21 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
           if (g >= TP_ST) mb_wait(su32(&empty[s]), (uint32_t)(((g / TP_ST) - 1) & 1));
           const uint32_t st = sbase + s * TM_STAGE;
           const uint32_t fb = su32(&full[s]);
+#if TM_NO_B   // bound experiment only: B never reloaded (wrong results)
+          mb_expect(fb, TM_A_BYTES + ((g < TP_ST) ? (PRESPLIT ? 2 : 1) * bytesB : 0));
+#else
           mb_expect(fb, TM_A_BYTES + (PRESPLIT ? 2 : 1) * bytesB);
+#endif
           const int32_t k0 = kt * TM_BK;
           if (a.a_mn)
             for (int j = 0; j < TM_BM / 32; ++j) tma2d(st + j * 2048, &a.ta, (int32_t)(m0 + 32 * j), k0, fb);
           else
             tma2d(st, &a.ta, k0, (int32_t)m0, fb);
+            TM_TS(0, g);
           const uint32_t sb = st + 2 * TM_A_BYTES;
+#if TM_NO_B
+          if (g >= TP_ST) continue;
+#endif
 #pragma unroll
           for (int part = 0; part < (PRESPLIT ? 2 : 1); ++part) {
             const CUtensorMap* mb = PRESPLIT ? (part ? &a.tbl : &a.tbh) : &a.tb;
@@ -551,6 +574,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
         for (int kt = 0; kt < ktiles; ++kt, ++g) {
           const int s = (int)(g % TP_ST);
           mb_wait(su32(&conv[s]), (uint32_t)((g / TP_ST) & 1));
+          TM_TS(2, g);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = sbase + s * TM_STAGE;
           const uint32_t ahi = st, alo = st + TM_A_BYTES;
@@ -568,6 +592,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
 #endif
           }
           mma_commit(su32(&empty[s]));
+          TM_TS(3, g);
         }
         mma_commit(su32(&accfull[b]));
       }
@@ -581,6 +606,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
       for (int kt = 0; kt < ktiles; ++kt, ++g) {
         const int s = (int)(g % TP_ST);
         mb_wait(su32(&full[s]), (uint32_t)((g / TP_ST) & 1));
+        if (tid == 0) TM_TS(1, g);
         const uint32_t st = sbase + s * TM_STAGE;
         float4 xs[NI];
 #pragma unroll
@@ -605,6 +631,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mb_arrive(su32(&conv[s]));
+        if (tid == 0) TM_TS(4, g);
       }
     }
   } else {                                       // epilogue warps
@@ -647,6 +674,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
       load_gate(cbeg, gn);
       load_gate(cbeg + 16, gn2);
       mb_wait(su32(&accfull[b]), (uint32_t)((it >> 1) & 1));
+      if (warp == TP_CONV / 32 + 2 && lane == 0) TM_TS(5, it);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const bool vec = a.c_n == 1 && ((p.C.ptr + 4 * (p.C.off + m * a.c_m)) & 15) == 0;
       const int64_t rowoff = p.C.off + m * a.c_m;
@@ -746,6 +774,28 @@ __global__ void k_tf32_split(const float* __restrict__ x, float* __restrict__ hi
   }
 }
 
+// split + transpose an MN-major [K][N] (row stride ld) fp32 operand into
+// K-major [N][K] tf32 hi / lo arrays (32 x 32 tiles through shared memory)
+__global__ void k_tf32_split_t(const float* __restrict__ x, int64_t ld, int64_t K, int64_t N,
+                               float* __restrict__ hi, float* __restrict__ lo) {
+  __shared__ float t[32][33];
+  const int64_t n0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t k = k0 + r, n = n0 + threadIdx.x;
+    t[r][threadIdx.x] = (k < K && n < N) ? x[k * ld + n] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t n = n0 + r, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      const float v = t[threadIdx.x][r];
+      const uint32_t h = rna(v);
+      hi[n * K + k] = __uint_as_float(h);
+      lo[n * K + k] = __uint_as_float(rna(v - __uint_as_float(h)));
+    }
+  }
+}
+
 typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                 CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -816,8 +866,17 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
     a.b_span = span;
     a.presplit = 1;
     if (a.b_mn) {
-      rc = tm_encode(enc, &a.tbh, hbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-      rc |= tm_encode(enc, &a.tbl, lbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      // MN-major weights: the split pass also transposes them to K-major, so
+      // a stage of B is ONE 64-byte-row box per part instead of eight 32-wide
+      // MN groups (per-stage TMA issue bounded the kernel: ~1 us per stage,
+      // tools/gemm_trace.py)
+      a.presplit = 2;
+      a.b_ld = b_k;
+      a.b_kk = p.k;
+      a.b_nn = p.n;
+      a.b_mn = 0;
+      rc = tm_encode(enc, &a.tbh, hbase, p.k, p.n, p.k, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
+      rc |= tm_encode(enc, &a.tbl, lbase, p.k, p.n, p.k, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
     } else {
       rc = tm_encode(enc, &a.tbh, hbase, p.k, p.n, b_n, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
       rc |= tm_encode(enc, &a.tbl, lbase, p.k, p.n, b_n, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -836,6 +895,12 @@ extern "C" int rt_gemm_tma_prepass(const void* blk, void* stream) {
   if (!a->presplit) return 0;
   float* hi = (float*)a->p.part;
   float* lo = hi + a->b_span;
+  if (a->presplit == 2) {
+    dim3 grid((unsigned)((a->b_nn + 31) / 32), (unsigned)((a->b_kk + 31) / 32));
+    k_tf32_split_t<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>((const float*)a->b_base, a->b_ld,
+                                                                   a->b_kk, a->b_nn, hi, lo);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   const int64_t n = (int64_t)a->b_span;
   const int grid = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
   k_tf32_split<<<grid > 0 ? grid : 1, 256, 0, (cudaStream_t)stream>>>((const float*)a->b_base, hi, lo, n);
@@ -846,3 +911,12 @@ extern "C" int rt_gemm_tma_smem() { return TM_SMEM; }
 extern "C" int rt_gemm_tma_smem_persist() { return TP_SMEM; }
 extern "C" int rt_gemm_tma_smem_drain() { return TM_SMEM_DRAIN; }
 extern "C" int rt_gemm_tma_args_bytes() { return (int)sizeof(tm_args); }
+
+extern "C" int rt_gemm_tma_trace(long long* out, int n) {
+#if TM_TRACE
+  return cudaMemcpyFromSymbol(out, g_tm_trace, sizeof(long long) * (n < 8 * 512 ? n : 8 * 512)) == cudaSuccess ? 0 : -1;
+#else
+  (void)out; (void)n;
+  return -1;
+#endif
+}

@@ -1,0 +1,48 @@
+"""Per-role stage timeline of the persistent tcgen05 GEMM (CTA 0), from a
+build with -DTM_TRACE=1 (RTB200_NVCC_EXTRA): producer issue, converter sees
+the stage, converter done, MMA start, MMA commit; epilogue accumulator-ready
+per tile.  python tools/gemm_trace.py [rows]"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+from test_gpu_kernels import mm_graph  # noqa: E402
+from paper_2501_05408_b200 import execute, native as N  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 524288
+rng = np.random.default_rng(0)
+x = torch.from_numpy(rng.standard_normal((B, 1, 256)).astype(np.float32)).cuda()
+W = torch.from_numpy((rng.standard_normal((256, 256)) / 16).astype(np.float32)).cuda()
+g = mm_graph(B, 256, 256)
+for _ in range(3):
+    execute(g, inputs={"x": x, "W": W}, device_outputs=True)
+torch.cuda.synchronize()
+t0 = torch.cuda.Event(enable_timing=True)
+t1 = torch.cuda.Event(enable_timing=True)
+t0.record()
+execute(g, inputs={"x": x, "W": W}, device_outputs=True)
+t1.record()
+torch.cuda.synchronize()
+print("call ms", t0.elapsed_time(t1))
+buf = (C.c_longlong * (8 * 512))()
+lib = N.lib()
+assert lib.rt_gemm_tma_trace(buf, 8 * 512) == 0, "build with -DTM_TRACE=1"
+tr = np.array(buf[:], dtype=np.int64).reshape(8, 512)
+base = tr[0, 0]
+names = ["issue", "conv_sees", "mma_start", "mma_commit", "conv_done"]
+print("stage  " + "  ".join(f"{n:>10s}" for n in names))
+for gidx in list(range(0, 20)) + list(range(200, 216)):
+    print(f"{gidx:5d}  " + "  ".join(f"{(tr[r, gidx] - base) / 1e3:10.2f}" for r in range(5)))
+acc = tr[5, :40]
+print("epilogue acc ready (us):", [round((a - base) / 1e3, 1) for a in acc[:20] if a])
+d = np.diff(tr[2, 16:400]) / 1e3
+print("MMA start spacing us: median", np.median(d), "mean", d.mean())
+lat = (tr[1, :400] - tr[0, :400]) / 1e3
+print("issue -> converter sees (us): median", np.median(lat), "p90", np.percentile(lat, 90))
+wait = (tr[0, 4:400] - tr[3, :396]) / 1e3
+print("commit(g) -> issue(g+4) (us): median", np.median(wait))
