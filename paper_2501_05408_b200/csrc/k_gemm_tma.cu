@@ -56,6 +56,8 @@ struct tm_args {
   uint64_t b_base, b_span; // PRESPLIT: B element base address and span (elements)
   int32_t presplit, _pad2; // 1: B split in place; 2: split AND transposed to K-major
   int64_t b_ld, b_kk, b_nn; // presplit 2: the MN-major source's row stride, K, N
+  CUtensorMap tc;           // persistent epilogue: C as 16-col x 32-row boxes (SWIZZLE_64B)
+  int32_t c_tma, _pad3;     // 1: the epilogue stores C through shared memory + TMA
 };
 
 namespace {
@@ -87,6 +89,11 @@ RT_DEV void mb_arrive(uint32_t bar) {
 RT_DEV void tma2d_prefetch(const CUtensorMap* map, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
                ::"l"((uint64_t)map), "r"(c0), "r"(c1) : "memory");
+}
+RT_DEV void tma2d_store(const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"((uint64_t)map), "r"(c0), "r"(c1), "r"(src) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 RT_DEV void tma2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar) {
   asm volatile(
@@ -439,6 +446,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_c
 // the per-tile variant: ncu tensor pipe 29%, smem 31%, long-scoreboard
 // stalls on per-tile prologues).
 #define TP_ST 4
+#ifndef TP_TMA_STORE
+#define TP_TMA_STORE 1   // persistent epilogue: C through shared memory + TMA store
+#endif
 #ifndef TM_TRACE
 #define TM_TRACE 0
 #endif
@@ -462,7 +472,8 @@ __device__ long long g_tm_trace[8][512];
 #define TP_CONV 128  // converter threads (warps 0-3; PRESPLIT leaves them only A)
 #define TP_EPI 8     // epilogue warps 6-13: two per TMEM lane quarter (column halves)
 #define TP_THREADS (TP_CONV + 64 + 32 * TP_EPI)
-#define TP_SMEM (TP_ST * TM_STAGE + 1024)
+#define TP_STAGE_EPI (2 * 32 * 16 * 4)   // per epilogue warp: two C chunks of 32 rows x 16 cols
+#define TP_SMEM (TP_ST * TM_STAGE + 1024 + TP_EPI * TP_STAGE_EPI)
 
 template <bool PRESPLIT>
 __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
@@ -637,6 +648,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
   } else {                                       // epilogue warps
     const int wq = warp & 3;                     // TMEM lane quarter of this warp
     const int half = (warp - TP_CONV / 32 - 2) >> 2;   // column half of the tile
+    const uint32_t estage = sbase + TP_ST * TM_STAGE;  // the epilogue warps' C chunks
     const int r = wq * 32 + lane;
     float* Cp = (float*)p.C.ptr;
     int it = 0;
@@ -696,7 +708,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
           asm volatile("tcgen05.fence::before_thread_sync;");
           mb_arrive(su32(&accfree[b]));
         }
-        if (!live) continue;
+        if (!live && !a.c_tma) continue;   // (TMA stores clip the rows past M)
         float x[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) x[j] = ktiles == 0 ? 0.f : __uint_as_float(v[j]);
@@ -731,7 +743,26 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
             if (p.epilogue == 1) x[j] = tanh_fast(x[j]);
           }
         }
-        if (vec && n0 + c0 + 16 <= p.n) {
+        if (a.c_tma) {
+          // the warp's 32 rows x 16 columns through shared memory, one TMA
+          // store per chunk (row-per-lane 16-byte stores hit 32 rows per
+          // instruction); SWIZZLE_64B: 16-byte chunk q of row l sits at
+          // q ^ ((l >> 1) & 3), so the lanes' writes are conflict-free
+          const int ew = warp - TP_CONV / 32 - 2;
+          const uint32_t buf = estage + (uint32_t)ew * TP_STAGE_EPI +
+                               (uint32_t)((((c0 - cbeg) >> 4) & 1) * 2048);
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t sa = buf + (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) * 16));
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(sa), "f"(x[4 * q]),
+                         "f"(x[4 * q + 1]), "f"(x[4 * q + 2]), "f"(x[4 * q + 3]) : "memory");
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma2d_store(&a.tc, (int32_t)(n0 + c0), (int32_t)(m0 + wq * 32), buf);
+        } else if (vec && n0 + c0 + 16 <= p.n) {
           float4* dst = (float4*)(Cp + rowoff + n0 + c0);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -749,6 +780,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
         mb_arrive(su32(&accfree[b]));
       }
     }
+    if (a.c_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -858,6 +890,15 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
   if (p.splits != 1 || !p.part) return (void*)k_gemm_tma;      // per-tile variant
   // persistent (lower.py launches TP_THREADS x min(tiles, SMs) when it set
   // `part`: the hi/lo scratch of B, 2 x span floats, or ~0 for no presplit)
+  {
+    // the epilogue stores C with TMA when C is a plain row-major 2-D tile
+    const uint64_t cbase = p.C.ptr + 4 * (uint64_t)p.C.off;
+    a.c_tma = 0;
+    if (TP_TMA_STORE && !p.accumulate && a.c_n == 1 && (cbase & 15) == 0 &&
+        ((a.c_m * 4) & 15) == 0 && a.c_m >= p.n && p.C.dtype == RT_F32)
+      a.c_tma = tm_encode(enc, &a.tc, cbase, p.n, p.m, a.c_m, 16, 32,
+                          CU_TENSOR_MAP_SWIZZLE_64B) == 0;
+  }
   if (p.part != ~0ull) {
     const uint64_t span = a.b_mn ? (uint64_t)(p.k - 1) * (uint64_t)b_k + (uint64_t)p.n
                                  : (uint64_t)(p.n - 1) * (uint64_t)b_n + (uint64_t)p.k;

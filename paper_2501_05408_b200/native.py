@@ -32,7 +32,7 @@ RT_K_GEMM_TMA = 12
 TMA_SMEM = 2 * 48 * 1024 + 1024
 TMA_SMEM_DRAIN = 4 * 48 * 1024 + 1024   # k_gemm_tma_drain: 4 stages, one CTA per SM
 TMA_DRAIN_K = 256                        # K per TMEM accumulation chunk
-TMA_SMEM_P = 4 * 48 * 1024 + 1024       # k_gemm_tmap: persistent, 4 stages, one CTA per SM
+TMA_SMEM_P = 4 * 48 * 1024 + 1024 + 8 * 4096   # k_gemm_tmap: persistent, 4 stages + epilogue C chunks
 TMA_THREADS_P = 128 + 64 + 256
 TC_SMEM = 2 * (2 * 128 * 32 * 4 + 2 * 256 * 32 * 4)
 

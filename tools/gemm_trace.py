@@ -15,17 +15,32 @@ from test_gpu_kernels import mm_graph  # noqa: E402
 from paper_2501_05408_b200 import execute, native as N  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 524288
+TANH = "--tanh" in sys.argv
 rng = np.random.default_rng(0)
 x = torch.from_numpy(rng.standard_normal((B, 1, 256)).astype(np.float32)).cuda()
 W = torch.from_numpy((rng.standard_normal((256, 256)) / 16).astype(np.float32)).cuda()
-g = mm_graph(B, 256, 256)
+inp = {"x": x, "W": W}
+if TANH:
+    # y = tanh(x @ W + b): the bias + tanh epilogue of the learner's forward
+    from paper_2501_05408_b200 import ir
+    g = mm_graph(B, 256, 256)
+    S = ("sym", "b", "loop")
+    g.nodes[3] = ir.Node(3, "bb", "input", (), ((1, 256),), ("f32",))
+    g.nodes[4] = ir.Node(4, "z", "add", ("b",), ((1, 256),), ("f32",), {}, 2)
+    g.nodes[5] = ir.Node(5, "h", "tanh", ("b",), ((1, 256),), ("f32",), {}, 1)
+    g.edges += [ir.Edge(4, 0, (S,), None, 0, 2), ir.Edge(4, 1, (), None, 0, 3),
+                ir.Edge(5, 0, (S,), None, 0, 4)]
+    g.outputs = [("h", 5, 0)]
+    inp["bb"] = torch.zeros((1, 256), device="cuda")
+else:
+    g = mm_graph(B, 256, 256)
 for _ in range(3):
-    execute(g, inputs={"x": x, "W": W}, device_outputs=True)
+    execute(g, inputs=inp, device_outputs=True)
 torch.cuda.synchronize()
 t0 = torch.cuda.Event(enable_timing=True)
 t1 = torch.cuda.Event(enable_timing=True)
 t0.record()
-execute(g, inputs={"x": x, "W": W}, device_outputs=True)
+execute(g, inputs=inp, device_outputs=True)
 t1.record()
 torch.cuda.synchronize()
 print("call ms", t0.elapsed_time(t1))
