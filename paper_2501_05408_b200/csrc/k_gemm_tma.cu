@@ -58,6 +58,7 @@ struct tm_args {
   int64_t b_ld, b_kk, b_nn; // presplit 2: the MN-major source's row stride, K, N
   CUtensorMap tc;           // persistent epilogue: C as 16-col x 32-row boxes (SWIZZLE_64B)
   int32_t c_tma, _pad3;     // 1: the epilogue stores C through shared memory + TMA
+  int32_t a3d, b3d;         // MN-major operand as ONE 3-D box (32-wide groups on dim 2)
 };
 
 namespace {
@@ -94,6 +95,12 @@ RT_DEV void tma2d_store(const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                ::"l"((uint64_t)map), "r"(c0), "r"(c1), "r"(src) : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+RT_DEV void tma3d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                  uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
 }
 RT_DEV void tma2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar) {
   asm volatile(
@@ -158,7 +165,7 @@ __device__ __forceinline__ void gemm_tma_body(const tm_args& a) {
   const int BN = nrem >= TM_BN ? TM_BN
                : a.b_mn ? (int)((nrem + 31) / 32 * 32) : (int)((nrem + 15) / 16 * 16);
   const int nbB = a.b_mn ? BN / 32 : 1;
-  const uint32_t bytesB = a.b_mn ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
+  const uint32_t bytesB = a.b_mn && !a.b3d ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
 
   constexpr uint32_t TCOLS = DRAIN ? 512 : 256;
   constexpr int KD = TM_DRAIN_K / TM_BK;     // k-tiles per accumulation chunk (DRAIN)
@@ -199,13 +206,17 @@ __device__ __forceinline__ void gemm_tma_body(const tm_args& a) {
         const uint32_t fb = su32(&full[s]);
         mb_expect(fb, TM_A_BYTES + bytesB);
         const int32_t k0 = (int32_t)(kbeg + (int64_t)kt * TM_BK);
-        if (a.a_mn)
+        if (a.a_mn && a.a3d)
+          tma3d(st, &a.ta, 0, k0, (int32_t)(m0 / 32), fb);
+        else if (a.a_mn)
           for (int j = 0; j < TM_BM / 32; ++j)
             tma2d(st + j * 2048, &a.ta, (int32_t)(m0 + 32 * j), k0, fb);
         else
           tma2d(st, &a.ta, k0, (int32_t)m0, fb);
         const uint32_t sb = st + 2 * TM_A_BYTES;
-        if (a.b_mn)
+        if (a.b_mn && a.b3d)
+          tma3d(sb, &a.tb, 0, k0, (int32_t)(n0 / 32), fb);
+        else if (a.b_mn)
           for (int j = 0; j < nbB; ++j) tma2d(sb + j * 2048, &a.tb, (int32_t)(n0 + 32 * j), k0, fb);
         else
           tma2d(sb, &a.tb, k0, (int32_t)n0, fb);
@@ -446,6 +457,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_c
 // the per-tile variant: ncu tensor pipe 29%, smem 31%, long-scoreboard
 // stalls on per-tile prologues).
 #define TP_ST 4
+#ifndef TM_3D
+#define TM_3D 1   // MN-major operands as one 3-D TMA box per stage
+#endif
 #ifndef TP_TMA_STORE
 #define TP_TMA_STORE 1   // persistent epilogue: C through shared memory + TMA store
 #endif
@@ -535,7 +549,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
         const int64_t m0 = mi * TM_BM, n0 = ni * TM_BN;
         const int BN = tile_bn(ni);
         const int nbB = a.b_mn ? BN / 32 : 1;
-        const uint32_t bytesB = a.b_mn ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
+        const uint32_t bytesB = a.b_mn && !a.b3d ? nbB * 32 * TM_BK * 4 : TM_B_BYTES;
         for (int kt = 0; kt < ktiles; ++kt, ++g) {
           if (TP_PF > 0) prefetch_a(g + TP_PF);
           const int s = (int)(g % TP_ST);
@@ -548,7 +562,9 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
           mb_expect(fb, TM_A_BYTES + (PRESPLIT ? 2 : 1) * bytesB);
 #endif
           const int32_t k0 = kt * TM_BK;
-          if (a.a_mn)
+          if (a.a_mn && a.a3d)
+            tma3d(st, &a.ta, 0, k0, (int32_t)(m0 / 32), fb);
+          else if (a.a_mn)
             for (int j = 0; j < TM_BM / 32; ++j) tma2d(st + j * 2048, &a.ta, (int32_t)(m0 + 32 * j), k0, fb);
           else
             tma2d(st, &a.ta, k0, (int32_t)m0, fb);
@@ -561,7 +577,9 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
           for (int part = 0; part < (PRESPLIT ? 2 : 1); ++part) {
             const CUtensorMap* mb = PRESPLIT ? (part ? &a.tbl : &a.tbh) : &a.tb;
             const uint32_t dst = sb + part * TM_B_BYTES;
-            if (a.b_mn)
+            if (a.b_mn && a.b3d && !PRESPLIT)
+              tma3d(dst, mb, 0, k0, (int32_t)(n0 / 32), fb);
+            else if (a.b_mn)
               for (int j = 0; j < nbB; ++j) tma2d(dst + j * 2048, mb, (int32_t)(n0 + 32 * j), k0, fb);
             else
               tma2d(dst, mb, k0, (int32_t)n0, fb);
@@ -834,6 +852,22 @@ typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, v
                                 CUtensorMapFloatOOBfill);
 
 // 2-D fp32 map over (inner, outer) with unit inner stride.
+// an MN-major operand [K][MN] (row stride ld) as dims {32, K, MN/32}: one
+// box of {32, TM_BK, groups} fills `groups` 2 KB group slots of a stage in a
+// single TMA instruction (the 2-D map needed one per 32-wide group: 12 per
+// stage of the contraction GEMMs)
+static int tm_encode3_mn(encode_fn_t enc, CUtensorMap* map, uint64_t addr, uint64_t mn, uint64_t k,
+                         uint64_t ld, uint32_t groups) {
+  cuuint64_t dims[3] = {32, k, mn / 32};
+  cuuint64_t strides[2] = {ld * 4, 128};
+  cuuint32_t box[3] = {32, TM_BK, groups};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)addr, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
 static int tm_encode(encode_fn_t enc, CUtensorMap* map, uint64_t addr, uint64_t inner, uint64_t outer,
                      uint64_t outer_stride_elems, uint32_t box_inner, uint32_t box_outer,
                      CUtensorMapSwizzle sw) {
@@ -870,7 +904,10 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
     rc = tm_encode(enc, &a.ta, abase, p.k, p.m, a_m, TM_BK, TM_BM, CU_TENSOR_MAP_SWIZZLE_64B);
   } else {
     a.a_mn = 1;
-    rc = tm_encode(enc, &a.ta, abase, p.m, p.k, a_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    a.a3d = TM_3D && p.m % 32 == 0 && (abase & 127) == 0 &&
+            tm_encode3_mn(enc, &a.ta, abase, p.m, p.k, a_k, TM_BM / 32) == 0;
+    rc = a.a3d ? 0 : tm_encode(enc, &a.ta, abase, p.m, p.k, a_k, 32, TM_BK,
+                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
   if (rc) return nullptr;
   if (b_k == 1 || p.k == 1) {
@@ -878,7 +915,10 @@ extern "C" void* rt_gemm_tma_pack(void* blk, void* encode) {
     rc = tm_encode(enc, &a.tb, bbase, p.k, p.n, b_n, TM_BK, TM_BN, CU_TENSOR_MAP_SWIZZLE_64B);
   } else {
     a.b_mn = 1;
-    rc = tm_encode(enc, &a.tb, bbase, p.n, p.k, b_k, 32, TM_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    a.b3d = TM_3D && p.n % 32 == 0 && (bbase & 127) == 0 &&
+            tm_encode3_mn(enc, &a.tb, bbase, p.n, p.k, b_k, TM_BN / 32) == 0;
+    rc = a.b3d ? 0 : tm_encode(enc, &a.tb, bbase, p.n, p.k, b_k, 32, TM_BK,
+                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
   if (rc) return nullptr;
   memcpy(blk, &a, sizeof a);
