@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_gemm_tma_drain(const __grid_c
 #endif
 #if TM_TRACE
 // per-role timestamps of CTA 0 (globaltimer ns): [role][event]
-__device__ long long g_tm_trace[8][512];
+__device__ long long g_tm_trace[10][512];
 #define TM_TS(role, idx) do { if (blockIdx.x == 0 && (idx) < 512) { long long t_; \
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_tm_trace[role][idx] = t_; } } while (0)
 #else
@@ -686,7 +686,29 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
       // overlaps chunk c; before the first, it overlaps the accumulator wait)
       float gn[16];
       auto load_gate = [&](int c0, float (&gv)[16]) {
-        if (!gate || c0 >= cend) return;
+        if (c0 >= cend) return;
+        if (p.epilogue != 2) {
+          // no gate: prefetch this chunk's bias instead (row-independent; a
+          // load after the accumulator read exposed ~1 us per chunk)
+          if (!p.bias.ptr) return;
+          const int64_t b0 = p.bias.off + (n0 + c0) * a.bias_n;
+          const float* bp = (const float*)p.bias.ptr + b0;
+          if (a.bias_n == 1 && p.bias.dtype == RT_F32 && n0 + c0 + 16 <= p.n &&
+              (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bp) + q);
+              gv[4 * q] = b4.x; gv[4 * q + 1] = b4.y; gv[4 * q + 2] = b4.z; gv[4 * q + 3] = b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              gv[j] = n0 + c0 + j < p.n
+                          ? load_as<float>((const void*)p.bias.ptr, p.bias.dtype, b0 + j * a.bias_n) : 0.f;
+          }
+          return;
+        }
+        if (!gate) return;
         const float* gp = gbase + c0 * a.g_n;
         if (gvec && n0 + c0 + 16 <= p.n) {
 #pragma unroll
@@ -722,6 +744,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
               "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (warp == TP_CONV / 32 + 2 && lane == 0) TM_TS(6, it * 16 + ((c0 - cbeg) >> 4));
         if (c0 + 16 >= cend) {     // this warp's reads of the accumulator are done
           asm volatile("tcgen05.fence::before_thread_sync;");
           mb_arrive(su32(&accfree[b]));
@@ -734,24 +757,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) x[j] = __fmul_rn(x[j], __fsub_rn(1.f, __fmul_rn(gv[j], gv[j])));
         } else {
-          float bv[16];
-          if (p.bias.ptr) {
-            const int64_t b0 = p.bias.off + (n0 + c0) * a.bias_n;
-            const float* bp = (const float*)p.bias.ptr + b0;
-            if (a.bias_n == 1 && p.bias.dtype == RT_F32 && n0 + c0 + 16 <= p.n &&
-                (reinterpret_cast<uintptr_t>(bp) & 15) == 0) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(bp) + q);
-                bv[4 * q] = b4.x; bv[4 * q + 1] = b4.y; bv[4 * q + 2] = b4.z; bv[4 * q + 3] = b4.w;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                bv[j] = n0 + c0 + j < p.n
-                            ? load_as<float>((const void*)p.bias.ptr, p.bias.dtype, b0 + j * a.bias_n) : 0.f;
-            }
-          }
+          const float* bv = gv;      // the prefetched bias chunk (load_gate)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int64_t n = n0 + c0 + j;
@@ -769,8 +775,10 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
           const int ew = warp - TP_CONV / 32 - 2;
           const uint32_t buf = estage + (uint32_t)ew * TP_STAGE_EPI +
                                (uint32_t)((((c0 - cbeg) >> 4) & 1) * 2048);
+          if (warp == TP_CONV / 32 + 2 && lane == 0) TM_TS(8, it * 16 + ((c0 - cbeg) >> 4));
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncwarp();
+          if (warp == TP_CONV / 32 + 2 && lane == 0) TM_TS(9, it * 16 + ((c0 - cbeg) >> 4));
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint32_t sa = buf + (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) * 16));
@@ -780,6 +788,7 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) tma2d_store(&a.tc, (int32_t)(n0 + c0), (int32_t)(m0 + wq * 32), buf);
+          if (warp == TP_CONV / 32 + 2 && lane == 0) TM_TS(7, it * 16 + ((c0 - cbeg) >> 4));
         } else if (vec && n0 + c0 + 16 <= p.n) {
           float4* dst = (float4*)(Cp + rowoff + n0 + c0);
 #pragma unroll
@@ -995,7 +1004,7 @@ extern "C" int rt_gemm_tma_args_bytes() { return (int)sizeof(tm_args); }
 
 extern "C" int rt_gemm_tma_trace(long long* out, int n) {
 #if TM_TRACE
-  return cudaMemcpyFromSymbol(out, g_tm_trace, sizeof(long long) * (n < 8 * 512 ? n : 8 * 512)) == cudaSuccess ? 0 : -1;
+  return cudaMemcpyFromSymbol(out, g_tm_trace, sizeof(long long) * (n < 10 * 512 ? n : 10 * 512)) == cudaSuccess ? 0 : -1;
 #else
   (void)out; (void)n;
   return -1;
