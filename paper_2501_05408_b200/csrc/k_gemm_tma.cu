@@ -404,17 +404,27 @@ __device__ __forceinline__ void gemm_tma_body(const tm_args& a) {
                         ? load_as<float>((const void*)p.bias.ptr, p.bias.dtype, b0 + j * a.bias_n) : 0.f;
         }
       }
+      // every column unconditionally (the stores below are guarded): the 16
+      // independent epilogue chains unroll and interleave
+      if (p.accumulate) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int64_t n = n0 + c0 + j;
-        if (n >= p.n) break;
-        if (p.accumulate) x[j] += Cp[rowoff + n * a.c_n];
-        if (!DRAIN && p.epilogue == 2) {
-          x[j] = __fmul_rn(x[j], bv[j]);
-          continue;
+        for (int j = 0; j < 16; ++j) {
+          const int64_t n = n0 + c0 + j;
+          if (n < p.n) x[j] += Cp[rowoff + n * a.c_n];
         }
-        if (p.bias.ptr) x[j] += bv[j];
-        if (p.epilogue == 1) x[j] = tanh_fast(x[j]);
+      }
+      if (!DRAIN && p.epilogue == 2) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = __fmul_rn(x[j], bv[j]);
+      } else {
+        if (p.bias.ptr) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] += bv[j];
+        }
+        if (p.epilogue == 1) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = tanh_fast(x[j]);
+        }
       }
       if (vec && n0 + c0 + 16 <= p.n) {
         float4* dst = (float4*)(Cp + rowoff + n0 + c0);
@@ -758,13 +768,23 @@ __device__ __forceinline__ void gemm_tmap_body(const tm_args& a) {
           for (int j = 0; j < 16; ++j) x[j] = __fmul_rn(x[j], __fsub_rn(1.f, __fmul_rn(gv[j], gv[j])));
         } else {
           const float* bv = gv;      // the prefetched bias chunk (load_gate)
+          // all 16 columns unconditionally (past N: clipped by the store), so
+          // the 16 independent bias + tanh chains unroll and interleave (a
+          // per-column `break` kept them one at a time: ~1.7 us per chunk)
+          if (p.accumulate) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int64_t n = n0 + c0 + j;
-            if (n >= p.n) break;
-            if (p.accumulate) x[j] += Cp[rowoff + n * a.c_n];
-            if (p.bias.ptr) x[j] += bv[j];
-            if (p.epilogue == 1) x[j] = tanh_fast(x[j]);
+            for (int j = 0; j < 16; ++j) {
+              const int64_t n = n0 + c0 + j;
+              if (n < p.n) x[j] += Cp[rowoff + n * a.c_n];
+            }
+          }
+          if (p.bias.ptr) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] += bv[j];
+          }
+          if (p.epilogue == 1) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] = tanh_fast(x[j]);
           }
         }
         if (a.c_tma) {
