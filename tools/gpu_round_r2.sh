@@ -2,7 +2,7 @@
 # C3, C4, reference arm), ncu launch lists (C2, C3), ncu --set full of the top
 # kernels, kernel roofline bench.
 mkdir -p gpurun_out
-P=${PROFILE_TAG:-r2b}
+P=${PROFILE_TAG:-r2d}
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$P.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$P.log
 tail -3 gpurun_out/pytest_gpu_$P.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke_$P.log 2>&1
@@ -32,5 +32,13 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sc
   -o gpurun_out/full_${P}_k_scan_tma python bench_kernels.py --only returns_bt --reps 1 \
   > gpurun_out/ncu_full_${P}_k_scan_tma.log 2>&1
 timeout 600 python bench_kernels.py > gpurun_out/bench_kernels_$P.jsonl 2>&1
+# keep the copy-back under 64 MiB: raw-page CSV exports instead of the reports,
+# a per-kernel summary instead of the C3 launch list
+for f in gpurun_out/full_${P}_*.ncu-rep; do
+  ncu -i "$f" --page raw --csv > "${f%.ncu-rep}_raw.csv" 2>/dev/null && rm -f "$f"
+done
+python tools/launch_summary.py gpurun_out/launches_$P.csv gpurun_out/launches_c3_$P.csv > gpurun_out/launches_summary_$P.txt 2>&1
+rm -f gpurun_out/launches_c3_$P.csv gpurun_out/loop_src_*.cu
+du -sh gpurun_out
 timeout 300 python tools/loop_profile.py c2 > gpurun_out/loop_profile_$P.txt 2>&1
 for f in gpurun_out/bench_*_$P.json; do echo "$f"; tail -c 400 "$f"; echo; done
