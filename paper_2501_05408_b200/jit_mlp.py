@@ -32,6 +32,9 @@ from .jit import (_decompose, _env_fold, _env_terms, _ew_udf_forwards, _forward_
 ENABLED = os.environ.get("RTB200_LOOP_MLP", "1") != "0"
 THREADS = 256
 KR = 32   # W2 rows per K quarter (and column) held in registers (mlp_h2q)
+# op 0 (observation merge) of step t + 1 computed by the env step's lanes
+# instead of a separate phase behind its own CTA barrier
+FOLD_OBS = os.environ.get("RTB200_MLP_FOLD_OBS", "1") != "0"
 
 
 def match(lp, ops, info):
@@ -130,6 +133,16 @@ def smem_bytes(lp, m):
     return _layout(lp, m)["total"]
 
 
+def _vec_ok(q, lp, w):
+    """Loop GEMM q's output rows take w-float vector stores: one contiguous
+    column dim and every offset term (base, row strides, per-step env
+    offsets) a multiple of w floats on a 16-byte aligned buffer."""
+    if q.N.nd != 1 or q.C.s2[0] != 1 or q.C.dtype != N.RT_F32 or q.C.ptr % 16:
+        return False
+    terms = [q.C.off] + [q.C.s1[d] for d in range(q.M.nd)] + [q.C.off_env[e] for e in range(N.RT_MAXENV)]
+    return all(t % w == 0 for t in terms)
+
+
 def _gemm_io(q, soff, name):
     """Pointer/offset lines and C/bias index expressions of loop GEMM q."""
     env_c = _env_terms([q.C.off_env[e] for e in range(N.RT_MAXENV)])
@@ -186,15 +199,25 @@ def source(lp, ops, info, m, name="loop_mlp"):
         "p.out.off", [e0.out.off_env[e] for e in range(N.RT_MAXENV)]) + ";")
     kc = m["k_carry"]
     offc = _offset_expr(f"b{kc}", e0.in_[kc], nd0)
-    ov = {kc: (f"(t == T0_ ? ((const float*)p.in[{kc}].ptr)[{offc}] : "
-               f"lds1({S['carry']} + (uint32_t)(lf * 4), 0.f))")}
-    lines0 = _program_lines(e0, "float", nd0, base=lambda k: f"b{k}", chk=lambda k, c: f"c{k}_{c}",
-                            env="env", load_override=ov)
-    op0 = f"""    {{  // op 0: observation (elementwise, generic body)
+
+    def op0_src(tag, fold):
+        """op 0's generic body: over the CTA's (row, e) elements (flat loop),
+        or folded into the env step (fold: lane e of the row's warp computes
+        observation t + 1 from the env output cv_ in its register)."""
+        if fold:
+            ov = {kc: "cv_"}
+        else:
+            ov = {kc: (f"(t == T0_ ? ((const float*)p.in[{kc}].ptr)[{offc}] : "
+                       f"lds1({S['carry']} + (uint32_t)(lf * 4), 0.f))")}
+        lines0 = _program_lines(e0, "float", nd0, base=lambda k: f"b{k}", chk=lambda k, c: f"c{k}_{c}",
+                                env="env", load_override=ov)
+        head = (f"{{ const long long flat = row * {DO}LL + e; const int lf = r * {DO} + e;" if fold else
+                f"for (long long flat = r0 * {DO}LL + tid; flat < r1 * {DO}LL; flat += {THREADS}) {{\n"
+                f"        const int lf = (int)(flat - r0 * {DO}LL);")
+        src = f"""    {{  // op 0: observation (elementwise, generic body)
       const rt_ew_params& p = *(const rt_ew_params*)(smem + {soff[0]});
       {chr(10).join('      ' + b for b in bases).strip()}
-      for (long long flat = r0 * {DO}LL + tid; flat < r1 * {DO}LL; flat += {THREADS}) {{
-        const int lf = (int)(flat - r0 * {DO}LL);
+      {head}
         {chr(10).join('        ' + x for x in _decompose(nd0, ext0)).strip()}
         float v0, v1, v2, v3, v4, v5, v6, v7;
         long long n0, n1, n2, n3, n4, n5, n6, n7;
@@ -207,8 +230,10 @@ def source(lp, ops, info, m, name="loop_mlp"):
         sts1({S['so']} + (uint32_t)((((lf % {DO}) * {MRP}) + lf / {DO}) * 4), res);
       }}
     }}"""
-    op0 = op0.replace("goto Lend;", "goto Lend0;").replace("Lend:", "Lend0:")
-    op0 = _rename_labels(op0.replace("goto L", "goto X0L").replace("goto X0Lend0", "goto Lend0"), 0)
+        src = src.replace("goto Lend;", f"goto Lend{tag};").replace("Lend:", f"Lend{tag}:")
+        return _rename_labels(src.replace("goto L", f"goto X{tag}L").replace(f"goto X{tag}Lend{tag}", f"goto Lend{tag}"), tag)
+    op0 = op0_src(0, False)
+    op0f = op0_src(9, True).replace("\n", "\n    ") if FOLD_OBS else ""
 
     # ---- op 4 (action) body: mu and eps from registers ----------------------
     nd4 = e4.box.nd
@@ -240,6 +265,35 @@ def source(lp, ops, info, m, name="loop_mlp"):
     dec4 = "\n          ".join(x.replace("unsigned int r =", "unsigned int ar =").replace("(r %", "(ar %")
                                .replace("r /=", "ar /=").replace("(long long)r;", "(long long)ar;")
                                for x in _decompose(nd4, ext4, flat="f4"))
+
+    # h1 / h2 rows to global: 8- / 16-byte stores when the columns are
+    # contiguous and every row start is aligned (else one store per element)
+    if _vec_ok(g1, lp, 2):
+        h1_store = (f"#pragma unroll\n      for (int rr = 0; rr < {HR}; ++rr) {{ if (hh * {HR} + rr < mr) {{ "
+                    f"const long long m = r0 + hh * {HR} + rr, n = c0; "
+                    f"*reinterpret_cast<float2*>(C1 + co1 + {_c1m} + {_c1n}) = make_float2(v[0][rr], v[1][rr]); }} }}")
+    else:
+        h1_store = (f"#pragma unroll\n      for (int j = 0; j < 2; ++j)\n      #pragma unroll\n"
+                    f"      for (int rr = 0; rr < {HR}; ++rr) {{ if (hh * {HR} + rr < mr) {{ "
+                    f"const long long m = r0 + hh * {HR} + rr, n = c0 + j; C1[co1 + {_c1m} + {_c1n}] = v[j][rr]; }} }}")
+    if _vec_ok(g2, lp, 4):
+        h2_store = (f"{{ const long long n = qc; *reinterpret_cast<float4*>(C2 + co2 + {_c2m} + {_c2n}) = "
+                    f"make_float4(v[0], v[1], v[2], v[3]); }}")
+    else:
+        h2_store = (f"#pragma unroll\n          for (int j = 0; j < 4; ++j) {{ const long long n = qc + j; "
+                    f"C2[co2 + {_c2m} + {_c2n}] = v[j]; }}")
+
+    if FOLD_OBS:
+        # op 0 of step T0_ before the loop, op 0 of step t + 1 in the env step
+        prologue_op0 = (f"  if (T0_ < T1_) {{\n    const long long t = T0_;\n    env[{lp.slot}] = t;\n"
+                        f"{op0}\n  }}\n  __syncthreads();\n")
+        loop_op0 = ""
+        carry_or_fold = (f"if (t + 1LL < T1_) {{\n            env[{lp.slot}] = t + 1LL;\n"
+                         + op0f.replace("\n", "\n        ") + "\n          }")
+    else:
+        prologue_op0 = ""
+        loop_op0 = op0 + "\n    __syncthreads();\n    MLP_PROF(0)"
+        carry_or_fold = f"sts1({S['carry']} + (uint32_t)((r * {DO} + e) * 4), cv_);"
 
     # ---- the kernel ---------------------------------------------------------
     src = f"""#include "loop_mlp.cuh"
@@ -287,27 +341,22 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
   const long long nz_row = ops[5].noise_row, nz_step = ops[5].noise_step;
   long long c0_ = clock64();
 #define MLP_PROF(i) if (p.prof && blockIdx.x == 0 && tid == 0) {{ const long long c1_ = clock64(); ((long long*)p.prof)[i] += c1_ - c0_; c0_ = c1_; }}
-  for (long long t = T0_; t < T1_; t += 1LL) {{
+{prologue_op0}  for (long long t = T0_; t < T1_; t += 1LL) {{
     env[{lp.slot}] = t;
-{op0}
-    __syncthreads();
-    MLP_PROF(0)
+{loop_op0}
     {{  // op 1: h1 = tanh(o W1 + b1): rows [hh*{HR}, +{HR}) of columns c0, c0+1
       {chr(10).join('      ' + x for x in _l1).strip()}
       float acc[2][{HR}];
       mlp_h1<{MRP}, {DO}, {H}>({S['so']}, {S['w1']}, c0, hh, acc);
+      float v[2][{HR}];
       #pragma unroll
       for (int j = 0; j < 2; ++j) {{
-        const long long n = c0 + j;
         const float bias = lds1({S['b1']} + 4u * (c0 + j), 0.f);
-        float v[{HR}];
         #pragma unroll
-        for (int rr = 0; rr < {HR}; ++rr) {{ const float x_ = {tanh}(acc[j][rr] + bias); v[rr] = hh * {HR} + rr < mr ? x_ : 0.f; }}
-        #pragma unroll
-        for (int rr = 0; rr < {HR}; ++rr) {{ if (hh * {HR} + rr >= mr) break; const long long m = r0 + hh * {HR} + rr;
-          C1[co1 + {_c1m} + {_c1n}] = v[rr]; }}
-        sts4({S['x1']} + (uint32_t)(((c0 + j) * {MRP} + hh * {HR}) * 4), make_float4(v[0], v[1], v[2], v[3]));
+        for (int rr = 0; rr < {HR}; ++rr) {{ const float x_ = {tanh}(acc[j][rr] + bias); v[j][rr] = hh * {HR} + rr < mr ? x_ : 0.f; }}
+        sts4({S['x1']} + (uint32_t)(((c0 + j) * {MRP} + hh * {HR}) * 4), make_float4(v[j][0], v[j][1], v[j][2], v[j][3]));
       }}
+      {h1_store}
     }}
     __syncthreads();
     MLP_PROF(1)
@@ -329,8 +378,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
         sts4({S['h2']} + (uint32_t)((r * {H} + qc) * 4), make_float4(v[0], v[1], v[2], v[3]));
         if (r < mr) {{
           const long long m = r0 + r;
-          #pragma unroll
-          for (int j = 0; j < 4; ++j) {{ const long long n = qc + j; C2[co2 + {_c2m} + {_c2n}] = v[j]; }}
+          {h2_store}
         }}
       }}
     }}
@@ -342,6 +390,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
       {chr(10).join('      ' + x for x in _l3).strip()}
       float mu[{DA}];
       mlp_head<{DA}, {H}>({S['h2']} + (uint32_t)(r * {H} * 4), {S['w3t']}, lane, mu);
+      MLP_PROF(4)
       const rt_ew_params& p4 = *(const rt_ew_params*)(smem + {soff[4]});
       {chr(10).join('      ' + b for b in bases4).strip()}
       if (t != T0_) cp_async_wait_all();     // this lane's eps / normals of step t
@@ -367,6 +416,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
                                      (const float*)p4.in[{ke}].ptr + ({eps_off} + {eps_step}LL));
       }}
       __syncwarp();
+      MLP_PROF(5)
       {{  // op 5: env (make_udf_fn body: numpy pairwise means in fp64)
         const rt_udf_params& q5 = *(const rt_udf_params*)(smem + {soff[5]});
         float* out5 = (float*)q5.out[0].ptr; const long long oo5 = q5.out[0].off{env_o};
@@ -380,7 +430,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
                                     : lds1({S['nz']} + (uint32_t)((r * {DO} + e) * 8), 0.0);
           const float cv_ = (float)tanh(base + 0.3 * z);
           out5[{out5} + e] = cv_;
-          sts1({S['carry']} + (uint32_t)((r * {DO} + e) * 4), cv_);
+          {carry_or_fold}
           if (t + 1LL < T1_) cp_async8({S['nz']} + (uint32_t)((r * {DO} + e) * 8),
                                        nz_base + row * nz_row + (t + 1LL) * nz_step + e);
         }}

@@ -15,3 +15,4 @@ for w in ("c2","c3"):
     except Exception as e: print(w, "ERR", e)
 PY
 head -25 gpurun_out/records_c3_$T.txt
+timeout 300 python tools/loop_profile.py c2 > gpurun_out/loop_profile_$T.txt 2>&1; head -12 gpurun_out/loop_profile_$T.txt

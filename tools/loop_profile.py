@@ -51,11 +51,15 @@ for ri, info in exe.loop_info.items():
                 fh.write(J.loop_source(params, info["ops"], "loop_jit", info))
     if info.get("mlp"):
         # fused MLP step (jit_mlp.py): phase probes 0..3, h2 core alone in 6
-        names = ["obs (op 0)", "h1 (op 1)", "h2 (op 2: core + epilogue)", "tail (ops 3-5: head, action, env)"]
-        for nm, c in zip(names, cyc[:4]):
-            print(f"  {nm:40s} cycles/step={c / info['trips']:8.0f} share={100 * c / max(1, tot):5.1f}%")
-        print(f"  {'  of which h2 core (hyb_core)':40s} cycles/step={cyc[6] / info['trips']:8.0f}")
-        print(f"  total cycles/step {sum(cyc[:4]) / info['trips']:.0f}")
+        # (probe k charges the cycles since the previous probe: 6 = h2 core,
+        # 2 = h2 epilogue, 4 = head, 5 = action, 3 = env (+ folded op 0))
+        names = [(0, "obs (op 0; 0 when folded into the env step)"), (1, "h1 (op 1)"),
+                 (6, "h2 core (mlp_h2q)"), (2, "h2 epilogue"), (4, "head (op 3)"),
+                 (5, "action (op 4)"), (3, "env (op 5 [+ op 0 of t+1])")]
+        tot = sum(cyc[k] for k, _ in names)
+        for k, nm in names:
+            print(f"  {nm:46s} cycles/step={cyc[k] / info['trips']:8.0f} share={100 * cyc[k] / max(1, tot):5.1f}%")
+        print(f"  total cycles/step {tot / info['trips']:.0f}")
         params.prof = 0
         continue
     for (k, q, re, f64, noise, *_), c in zip(info["ops"], cyc):
