@@ -606,3 +606,42 @@ def test_sibling_heads_share_one_row_stream(dt, n1, n2):
     np.testing.assert_allclose(out["mu"][:, 0], h64 @ inp["W3"] + inp["b3"], rtol=tol, atol=tol)
     np.testing.assert_allclose(out["V"][:, 0], h64 @ inp["Wv"] + inp["bv"], rtol=tol, atol=tol)
     X._CACHE.clear()
+
+
+@pytest.mark.gpu
+def test_tanh_fast_flush_to_zero_forms_are_bit_identical():
+    """tanh_fast (common.cuh) uses ex2/rcp.approx.ftz; over EVERY fp32 bit
+    pattern it returns the bits of the __expf/__fdividef formulation it
+    replaced (tanh_fast_ref), compiled both with -fmad=false (the JIT loop
+    kernels) and with contraction on (the nvcc-built kernels)."""
+    import ctypes as C
+    import torch
+    from paper_2501_05408_b200 import jit
+    src = r'''#include "common.cuh"
+extern "C" __global__ void tanh_cmp(unsigned long long* bad, unsigned* first) {
+  const unsigned long long n = 1ull << 32;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const float x = __uint_as_float((unsigned)i);
+    const unsigned a = __float_as_uint(tanh_fast(x)), b = __float_as_uint(tanh_fast_ref(x));
+    const bool nan = x != x;
+    if (!nan && a != b) { atomicAdd(bad, 1ull); atomicMin(first, (unsigned)i); }
+  }
+}'''
+    cu = C.CDLL("libcuda.so.1")
+    torch.zeros(1, device="cuda")
+    for fmad in (False, True):
+        opts = jit._opts
+        try:
+            if fmad:
+                jit._opts = lambda: [o for o in opts() if o != b"-fmad=false"] + [b"-fmad=true"]
+            fn = jit.compile_kernel(src + f"\n// fmad={fmad}\n", "tanh_cmp")
+        finally:
+            jit._opts = opts
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        first = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+        args = [C.c_void_p(bad.data_ptr()), C.c_void_p(first.data_ptr())]
+        ptrs = (C.c_void_p * 2)(*[C.cast(C.byref(a), C.c_void_p) for a in args])
+        assert cu.cuLaunchKernel(C.c_void_p(fn), 148 * 8, 1, 1, 256, 1, 1, 0, None, ptrs, None) == 0
+        torch.cuda.synchronize()
+        assert int(bad.item()) == 0, (fmad, int(bad.item()), hex(int(first.item()) & 0xffffffff))
