@@ -125,6 +125,7 @@ def _layout(lp, m):
     put("eps", MRP * DA * 4)                 # eps of the next step (cp.async)
     put("nz", MRP * DO * 8)                  # env normals of the next step (cp.async)
     put("carry", MRP * DO * 4)               # env output -> next step's observation
+    put("prof", 64)                          # phase probe accumulators (profiling runs)
     lay["total"] = cur
     return lay
 
@@ -339,8 +340,15 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
   const long long T0_ = {t0}, T1_ = {t1};
   const double* nz_base = (const double*)ops[5].noise + ops[5].noise_off;
   const long long nz_row = ops[5].noise_row, nz_step = ops[5].noise_step;
+  // phase probes (tools/loop_profile.py): CTA 0 / thread 0 accumulates the
+  // clock deltas in shared memory (a global read-modify-write per probe put a
+  // memory round trip on warp 0's path) and writes them out at the end
+  const bool prof_on = p.prof && blockIdx.x == 0 && tid == 0;
+  if (prof_on)
+    for (int i = 0; i < 8; ++i) sts1({S['prof']} + 8u * i, 0.0);
   long long c0_ = clock64();
-#define MLP_PROF(i) if (p.prof && blockIdx.x == 0 && tid == 0) {{ const long long c1_ = clock64(); ((long long*)p.prof)[i] += c1_ - c0_; c0_ = c1_; }}
+#define MLP_PROF(i) if (prof_on) {{ const long long c1_ = clock64(); \
+    sts1({S['prof']} + 8u * (i), lds1({S['prof']} + 8u * (i), 0.0) + (double)(c1_ - c0_)); c0_ = c1_; }}
 {prologue_op0}  for (long long t = T0_; t < T1_; t += 1LL) {{
     env[{lp.slot}] = t;
 {loop_op0}
@@ -440,6 +448,8 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
     __syncthreads();
     MLP_PROF(3)
   }}
+  if (prof_on)
+    for (int i = 0; i < 8; ++i) ((long long*)p.prof)[i] += (long long)lds1({S['prof']} + 8u * i, 0.0);
 }}
 """
     return src

@@ -1,9 +1,9 @@
 # ncu --set full of the C3 learner's thin kernels (raw CSV exports only)
 mkdir -p gpurun_out
 P=${PROFILE_TAG:-r2e}
-for K in "k_thin_smallv<float, 4, 1, 4>:smallv_gate" "k_thin_contract:contract" "k_thin_rows:rows"; do
+for K in "k_thin_smallv<float, 4, 1, 4>:smallv_gate" "k_thin_contract<float, 16, 1>:contract" "k_thin_rows<float, 8, 2>:rows"; do
   RX=${K%%:*}; NM=${K##*:}
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${RX%%<*}" \
+  timeout 900 ncu --set full --clock-control none --import-source on \
     --kernel-name-base demangled -k "regex:$(echo "$RX" | sed 's/[<>, ]/./g')" -c 1 \
     -o gpurun_out/full_${P}_c3_$NM python bench.py --workload c3 --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_full_${P}_c3_$NM.log 2>&1
