@@ -495,27 +495,6 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
                       : (T)0;
   const int64_t gw = (int64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * (THREADS / 32);
-  // vectorised rows with a small register tile: the next iteration's rows are
-  // loaded before this one's FMAs (one 4-row batch in flight per warp left
-  // the kernel at ~3.3 TB/s: too few bytes in flight for HBM latency)
-  constexpr bool PF = RW * KI <= 8;
-  auto load_rows = [&](int64_t w0_, V (&xv_)[RW][KI]) {
-#pragma unroll
-    for (int rr = 0; rr < RW; ++rr) {
-      const int64_t w = w0_ + rr < p.w ? w0_ + rr : p.w - 1;
-      const int64_t xo_ = wdec(p.W, w, p.X.s2);
-#pragma unroll
-      for (int i = 0; i < KI; ++i) {
-        const int k = (i * 32 + lane) * VW;
-        if (k < K) xv_[rr][i] = __ldcs(reinterpret_cast<const V*>(X + xo_ + k));
-        else unpack_zero(xv_[rr][i]);
-      }
-    }
-  };
-  V xnext[PF ? RW : 1][PF ? KI : 1];
-  if constexpr (PF) {
-    if (p.vec && gw * RW < p.w) load_rows(gw * RW, xnext);
-  }
   for (int64_t w0 = gw * RW; w0 < p.w; w0 += nw * RW) {
     T acc[RW][R];
 #pragma unroll
@@ -526,19 +505,18 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
 #pragma unroll
     for (int rr = 0; rr < RW; ++rr) {
       const int64_t w = w0 + rr < p.w ? w0 + rr : p.w - 1;
-      xo[rr] = PF && p.vec ? 0 : wdec(p.W, w, p.X.s2);
+      xo[rr] = wdec(p.W, w, p.X.s2);
     }
     if (p.vec) {
       V xv[RW][KI];
-      if constexpr (PF) {
 #pragma unroll
-        for (int rr = 0; rr < RW; ++rr)
+      for (int rr = 0; rr < RW; ++rr)
 #pragma unroll
-          for (int i = 0; i < KI; ++i) xv[rr][i] = xnext[rr][i];
-        if (w0 + nw * RW < p.w) load_rows(w0 + nw * RW, xnext);
-      } else {
-        load_rows(w0, xv);
-      }
+        for (int i = 0; i < KI; ++i) {
+          const int k = (i * 32 + lane) * VW;
+          if (k < K) xv[rr][i] = __ldcs(reinterpret_cast<const V*>(X + xo[rr] + k));
+          else unpack_zero(xv[rr][i]);
+        }
 #pragma unroll
       for (int rr = 0; rr < RW; ++rr)
 #pragma unroll
