@@ -396,6 +396,10 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
       const int r = warp;
       const long long row = r0 + r;
       {chr(10).join('      ' + x for x in _l3).strip()}
+      // the env's observation mean depends only on step t's observation:
+      // issued ahead of the head so its loads / shuffles overlap the head's
+      const double sobs_ = warp_pairwise_sum_s({S['obs']} + (uint32_t)(r * {DO * 4}), {DO}, lane);
+      float actv_ = 0.f;
       float mu[{DA}];
       mlp_head<{DA}, {H}>({S['h2']} + (uint32_t)(r * {H} * 4), {S['w3t']}, lane, mu);
       MLP_PROF(4)
@@ -419,7 +423,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
         {body4}
       Lend4:
         {st4}
-        sts1({S['act']} + (uint32_t)((r * {DA} + lane) * 4), res);
+        actv_ = res;
         if (t + 1LL < T1_) cp_async4({S['eps']} + (uint32_t)((r * {DA} + lane) * 4),
                                      (const float*)p4.in[{ke}].ptr + ({eps_off} + {eps_step}LL));
       }}
@@ -430,8 +434,13 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
         float* out5 = (float*)q5.out[0].ptr; const long long oo5 = q5.out[0].off{env_o};
         {dec5}
         double base = {repr(float(u5.salt))};
-        base = base + warp_pairwise_sum_s({S['obs']} + (uint32_t)(r * {DO * 4}), {DO}, lane) / {float(DO)!r};
-        base = base + warp_pairwise_sum_s({S['act']} + (uint32_t)(r * {DA * 4}), {DA}, lane) / {float(DA)!r};
+        base = base + sobs_ / {float(DO)!r};
+        // the action mean: lane 0's serial fp64 sum of warp_pairwise_sum_s
+        // (n < 8), read from the action lanes' registers by every lane
+        double sact_ = 0.0;
+        #pragma unroll
+        for (int i_ = 0; i_ < {DA}; ++i_) sact_ += (double)__shfl_sync(0xffffffffu, actv_, i_);
+        base = base + sact_ / {float(DA)!r};
         if (lane < {DO}) {{
           const int e = lane;
           const double z = t == T0_ ? nz_base[row * nz_row + t * nz_step + e]
