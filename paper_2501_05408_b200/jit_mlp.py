@@ -35,6 +35,10 @@ KR = 32   # W2 rows per K quarter (and column) held in registers (mlp_h2q)
 # op 0 (observation merge) of step t + 1 computed by the env step's lanes
 # instead of a separate phase behind its own CTA barrier
 FOLD_OBS = os.environ.get("RTB200_MLP_FOLD_OBS", "1") != "0"
+# h1 computed per K quarter of the h2 core: the 64 threads of part p produce
+# the h1 columns [64p, 64p + 64) their own core reads, so h1 -> core is a
+# 64-thread named barrier per part instead of a CTA barrier
+PART_BAR = os.environ.get("RTB200_MLP_PART_BAR", "1") != "0"
 
 
 def match(lp, ops, info):
@@ -306,7 +310,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
   const long long r0 = (long long)blockIdx.x * {R}LL;
   const long long r1 = r0 + {R}LL < {lp.rows}LL ? r0 + {R}LL : {lp.rows}LL;
   if (r0 >= r1) return;
-  const int tid = (int)threadIdx.x, hh = tid >> 7, c0 = 2 * (tid & 127), warp = tid >> 5, lane = tid & 31;
+  const int tid = (int)threadIdx.x, {"hh = (tid >> 5) & 1, c0 = 64 * (tid >> 6) + 2 * (tid & 31)" if PART_BAR else "hh = tid >> 7, c0 = 2 * (tid & 127)"}, warp = tid >> 5, lane = tid & 31;
   const int mr = (int)(r1 - r0);
   const rt_loop_op* ops = (const rt_loop_op*)p.ops;
   for (int i = 0; i < p.nops; ++i) {{
@@ -366,7 +370,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1) {name}(const __grid_c
       }}
       {h1_store}
     }}
-    __syncthreads();
+    {"asm volatile(\"bar.sync %0, 64;\" :: \"r\"(1 + (tid >> 6)) : \"memory\");" if PART_BAR else "__syncthreads();"}
     MLP_PROF(1)
     {{  // op 2: h2 = tanh(h1 W2 + b2): K quarters, 4 columns per thread (mlp_h2q)
       {chr(10).join('      ' + x for x in _l2).strip()}
