@@ -106,6 +106,131 @@ __global__ void __launch_bounds__(THREADS) k_thin_contract(const __grid_constant
     if (r < nr) part[w * p.part_w + r * p.part_r] = acc[r];
 }
 
+// variant 1, bulk-streamed (p.vec, fp32): the same per-thread sums as
+// k_thin_contract -- thread (blockIdx.x, tid) owns column w of X and sums
+// x[k] * y[k, r] over its split's rows in k order -- but the rows arrive by
+// cp.async.bulk into a 3-stage shared-memory ring (32 rows of the block's
+// 256-column slice of X + the rows' Y per stage, one mbarrier each) instead
+// of per-thread 4-byte loads behind a Y-tile barrier: the bulk engine keeps
+// ~200 KB per SM in flight (2 CTAs), and the splits are sized to one wave.
+// Requires 16-byte aligned rows (X columns contiguous, w % 4 == 0, Y
+// columns contiguous, r % 4 == 0); the lowering checks and otherwise keeps
+// k_thin_contract.
+constexpr int BK_SR = 32, BK_ST = 3;
+
+RT_DEV uint32_t bk_su32(const void* q) { return (uint32_t)__cvta_generic_to_shared(q); }
+RT_DEV void bk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+RT_DEV void bk_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+  }
+}
+
+template <int R, bool ONES>
+__global__ void __launch_bounds__(THREADS, 2) k_thin_contract_bulk(const __grid_constant__ rt_thin_params p) {
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  float* xs = (float*)sm_raw;                          // [ST][SR][256]
+  float* ys = xs + BK_ST * BK_SR * THREADS;            // [ST][SR][R]
+  uint64_t* bars = (uint64_t*)(ys + BK_ST * BK_SR * R);
+  const int tid = (int)threadIdx.x, lane = tid & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * THREADS;
+  const int W = (int)(p.w - w0 < THREADS ? p.w - w0 : THREADS);
+  const int s = blockIdx.y;
+  const int64_t per = (p.k + p.splits - 1) / p.splits;
+  const int64_t k0 = (int64_t)s * per;
+  const int64_t k1 = k0 + per < p.k ? k0 + per : p.k;
+  const int nst = k1 > k0 ? (int)((k1 - k0 + BK_SR - 1) / BK_SR) : 0;
+  const float* X = (const float*)p.X.ptr + p.X.off + w0;
+  const float* Y = (const float*)p.Y.ptr + p.Y.off;
+  const int64_t xk = p.X.s1[0], yk = p.Y.s1[0];
+  const int nr = (int)p.r;
+  const bool xdense = xk == W && W == THREADS, ydense = yk == R && nr == R;
+  if (tid == 0) {
+    for (int i = 0; i < BK_ST; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bk_su32(bars + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // warp 0 fills stage st with rows [kb, kb + n)
+  auto issue = [&](int it, int st) {
+    const int64_t kb = k0 + (int64_t)it * BK_SR;
+    const int n = (int)(k1 - kb < BK_SR ? k1 - kb : BK_SR);
+    const uint32_t bar = bk_su32(bars + st);
+    float* xd = xs + st * BK_SR * THREADS;
+    float* yd = ys + st * BK_SR * R;
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                   ::"r"(bar), "r"((uint32_t)(n * (W + nr) * 4)) : "memory");
+    __syncwarp();
+    if (xdense) {
+      if (lane == 0) bk_copy(bk_su32(xd), X + kb * xk, (uint32_t)(n * W * 4), bar);
+    } else {
+      for (int i = lane; i < n; i += 32) bk_copy(bk_su32(xd + i * THREADS), X + (kb + i) * xk, (uint32_t)(W * 4), bar);
+    }
+    if (ydense) {
+      if (lane == 0) bk_copy(bk_su32(yd), Y + kb * yk, (uint32_t)(n * R * 4), bar);
+    } else {
+      for (int i = lane; i < n; i += 32) bk_copy(bk_su32(yd + i * R), Y + (kb + i) * yk, (uint32_t)(nr * 4), bar);
+    }
+  };
+  if (tid < 32)
+    for (int it = 0; it < BK_ST && it < nst; ++it) issue(it, it);
+  float acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.f;
+  float acc1 = 0.f;
+  for (int it = 0; it < nst; ++it) {
+    const int st = it % BK_ST;
+    bk_wait(bk_su32(bars + st), (uint32_t)((it / BK_ST) & 1));
+    const int64_t kb = k0 + (int64_t)it * BK_SR;
+    const int n = (int)(k1 - kb < BK_SR ? k1 - kb : BK_SR);
+    const float* xr = xs + st * BK_SR * THREADS + tid;
+    const float4* yr = (const float4*)(ys + st * BK_SR * R);
+    if (tid < W) {
+      if (n == BK_SR) {
+#pragma unroll 8
+        for (int kk = 0; kk < BK_SR; ++kk) {
+          const float x = xr[kk * THREADS];
+          float y[R];
+#pragma unroll
+          for (int q = 0; q < R / 4; ++q) {
+            const float4 v = yr[kk * (R / 4) + q];
+            y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
+          }
+          fma_bcast<R>(acc, y, x);
+          if constexpr (ONES) acc1 += x;
+        }
+      } else {
+        for (int kk = 0; kk < n; ++kk) {
+          const float x = xr[kk * THREADS];
+          float y[R];
+#pragma unroll
+          for (int q = 0; q < R / 4; ++q) {
+            const float4 v = yr[kk * (R / 4) + q];
+            y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
+          }
+          fma_bcast<R>(acc, y, x);
+          if constexpr (ONES) acc1 += x;
+        }
+      }
+    }
+    __syncthreads();   // every thread is done with stage st
+    if (tid < 32 && it + BK_ST < nst) issue(it + BK_ST, st);
+  }
+  if (tid >= W) return;
+  const int64_t w = w0 + tid;
+  if constexpr (ONES) ((float*)p.part2)[(int64_t)s * p.w + w] = acc1;
+  float* part = (float*)p.part + (int64_t)s * p.w * p.r;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r < nr) part[w * p.part_w + r * p.part_r] = acc[r];
+}
+
 // variant 2: rows of X (K <= KP values each, zero-padded to KP) times a
 // resident [KP, R] Y; each thread owns output columns, rows stream through
 // a shared-memory tile, stores are coalesced along r.
@@ -621,6 +746,15 @@ extern "C" void* rt_kernel_thin_vec(int mode, int f64, int k) {
   if (k <= 16) return SV(float, 16);
   return nullptr;
 #undef SV
+}
+
+extern "C" void* rt_kernel_thin_bulk(int r, int ones) {
+#define BK(R) (ones ? (void*)k_thin_contract_bulk<R, true> : (void*)k_thin_contract_bulk<R, false>)
+  if (r <= 4) return BK(4);
+  if (r <= 8) return BK(8);
+  if (r <= 16) return BK(16);
+  return BK(32);
+#undef BK
 }
 
 extern "C" void* rt_kernel_thin(int variant, int f64, int r) {

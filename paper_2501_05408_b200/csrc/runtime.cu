@@ -22,6 +22,7 @@ extern "C" void* rt_kernel_rng_fill();
 extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
+extern "C" void* rt_kernel_thin_bulk(int r, int ones);
 extern "C" void* rt_kernel_thin_vec(int mode, int f64, int k);
 extern "C" void* rt_kernel_thin_rows(int f64, int r, int k);
 extern "C" void* rt_scan_tma_pack(void* blk, void* encode);
@@ -193,6 +194,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
         if (p->epilogue != 2 || p->k2 > 4) return nullptr;
         return p->vec ? rt_kernel_thin_vec(2, p->f64, (int)p->k) : rt_kernel_thin(5, p->f64, (int)p->k);
       }
+      if (p->variant == 1 && p->vec) return p->f64 ? nullptr : rt_kernel_thin_bulk((int)p->r, p->ones);
       if (p->variant == 1 && p->ones) return rt_kernel_thin(6, p->f64, (int)p->r);
       if (p->variant == 2 && p->vec)
         return rt_kernel_thin_vec(p->epilogue == 2 ? 1 : 0, p->f64, (int)p->k);

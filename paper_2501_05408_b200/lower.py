@@ -2147,9 +2147,17 @@ class Lowering:
                 q.part_w, q.part_r = 1, n
             q.k = k
             gx = (q.w + 255) // 256
-            q.splits = int(max(1, min(k // 256, (148 * 8) // gx, 65535)))
+            smem = 0
+            if self._thin_bulk_ok(q):
+                # k_thin_contract_bulk: 2 CTAs per SM, the splits one wave
+                q.vec = 1
+                q.splits = int(max(1, min(296 // gx, -(-k // 32), 65535)))
+                rp = 4 if q.r <= 4 else 8 if q.r <= 8 else 16 if q.r <= 16 else 32
+                smem = 3 * 32 * (256 + rp) * 4 + 3 * 8      # BK_ST x BK_SR rows + mbarriers
+            else:
+                q.splits = int(max(1, min(k // 256, (148 * 8) // gx, 65535)))
             q.part = self.alloc(q.splits * m * n * esize)
-            self.add_rec(N.RT_K_THIN, q, [gx, q.splits, 1], [256, 1, 1], 0, label)
+            self.add_rec(N.RT_K_THIN, q, [gx, q.splits, 1], [256, 1, 1], smem, label)
             r = N.rt_splitk_params()
             r.Z, r.M, r.N = p.Z, p.M, p.N
             r.z, r.m, r.n = p.z, p.m, p.n
@@ -2174,6 +2182,20 @@ class Lowering:
                              [256, 1, 1], 0, (self.ones_bias_label(label), self.ones_bias_name(label)))
             return True
         return self._gemm_smallk(p, M, nc, kc, f64, label, accumulate, epilogue, bias)
+
+    THIN_BULK = os.environ.get("RTB200_THIN_BULK", "1") != "0"
+
+    def _thin_bulk_ok(self, q):
+        """Variant 1 can stream its rows by cp.async.bulk (k_thin_contract_bulk):
+        fp32, contiguous 16-byte-aligned X and Y rows at every env offset."""
+        if not self.THIN_BULK or q.f64 or q.r > 32 or q.w % 4 or q.r % 4:
+            return False
+        for g in (q.X, q.Y):
+            if g.s2[0] != 1 or g.s1[0] % 4 or g.off % 4 or (g.ptr + 4 * g.off) % 16:
+                return False
+            if any(g.off_env[e] % 4 for e in range(N.RT_MAXENV)):
+                return False
+        return True
 
     def _gemm_smallk(self, p, M, nc, kc, f64, label, accumulate, epilogue, bias, gate=None):
         """K <= 32 products over many rows (the observation layer, dX of a

@@ -107,6 +107,24 @@ def test_thin_contraction(K, N, dt):
     np.testing.assert_allclose(out, want.astype(npdt), rtol=tol, atol=tol * np.sqrt(B) * 10)
 
 
+@pytest.mark.parametrize("K,N,B", [(16, 600, 30011), (8, 1000, 4099), (16, 256, 70001), (4, 64, 4100)])
+def test_thin_contraction_bulk(K, N, B):
+    """Variant 1 streamed by cp.async.bulk (k_thin_contract_bulk): column
+    slices of several CTAs (N > 256, ragged last slice), per-row and whole-
+    stage copies, a ragged last stage, fewer rows than stages; fp64 numpy."""
+    from paper_2501_05408_b200 import get_executable, native as NN
+    rng = np.random.default_rng(K * 7 + N + B)
+    x = rng.standard_normal((B, 1, K)).astype(np.float32)
+    gr = rng.standard_normal((B, 1, N)).astype(np.float32)
+    g = mm_graph(B, K, N, contract=True)
+    exe, _ = get_executable(g, None, {"x": x, "gr": gr}, seed=0)
+    assert any(k == NN.RT_K_THIN and p.variant == 1 and p.vec
+               for k, p in zip(exe.kernels, exe._params)), "bulk contraction not lowered"
+    out = execute(g, inputs={"x": x, "gr": gr})["s"]
+    want = np.einsum("bk,bn->kn", x[:, 0].astype(np.float64), gr[:, 0].astype(np.float64))
+    np.testing.assert_allclose(out, want.astype(np.float32), rtol=1e-5, atol=1e-5 * np.sqrt(B) * 10)
+
+
 @pytest.mark.parametrize("K,N", [(4, 256), (16, 300), (1, 64)])
 def test_thin_small_k_rows(K, N):
     """y[b] = x[b] @ W with K <= 32 (write-bound): RT_K_THIN variant 2."""
