@@ -180,55 +180,79 @@ __global__ void __launch_bounds__(THREADS, 2) k_thin_contract_bulk(const __grid_
   };
   if (tid < 32)
     for (int it = 0; it < BK_ST && it < nst; ++it) issue(it, it);
-  float acc[R];
+  // thread (g, c4): columns c4 .. c4 + 3 of the slice over the stage rows
+  // kk = g, g + 4, ...; the four row groups' sums are added in group order
+  // at the end.  (Four columns per thread: the broadcast Y row is read once
+  // per 4 columns -- with one column per thread the Y reads were 4/5 of the
+  // shared-memory wavefronts and paced the kernel.)
+  const int g = tid >> 6, c4 = 4 * (tid & 63);
+  const bool cok = c4 < W;                   // W % 4 == 0
+  float acc[4][R], acc1[4];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = 0.f;
-  float acc1 = 0.f;
+  for (int j = 0; j < 4; ++j) {
+    acc1[j] = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[j][r] = 0.f;
+  }
   for (int it = 0; it < nst; ++it) {
     const int st = it % BK_ST;
     bk_wait(bk_su32(bars + st), (uint32_t)((it / BK_ST) & 1));
     const int64_t kb = k0 + (int64_t)it * BK_SR;
     const int n = (int)(k1 - kb < BK_SR ? k1 - kb : BK_SR);
-    const float* xr = xs + st * BK_SR * THREADS + tid;
+    const float* xr = xs + st * BK_SR * THREADS + c4;
     const float4* yr = (const float4*)(ys + st * BK_SR * R);
-    if (tid < W) {
-      if (n == BK_SR) {
-#pragma unroll 8
-        for (int kk = 0; kk < BK_SR; ++kk) {
-          const float x = xr[kk * THREADS];
-          float y[R];
+    if (cok) {
+#pragma unroll 2
+      for (int kk = g; kk < n; kk += 4) {
+        const float4 x = *(const float4*)(xr + kk * THREADS);
+        float y[R];
 #pragma unroll
-          for (int q = 0; q < R / 4; ++q) {
-            const float4 v = yr[kk * (R / 4) + q];
-            y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
-          }
-          fma_bcast<R>(acc, y, x);
-          if constexpr (ONES) acc1 += x;
+        for (int q = 0; q < R / 4; ++q) {
+          const float4 v = yr[kk * (R / 4) + q];
+          y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
         }
-      } else {
-        for (int kk = 0; kk < n; ++kk) {
-          const float x = xr[kk * THREADS];
-          float y[R];
-#pragma unroll
-          for (int q = 0; q < R / 4; ++q) {
-            const float4 v = yr[kk * (R / 4) + q];
-            y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
-          }
-          fma_bcast<R>(acc, y, x);
-          if constexpr (ONES) acc1 += x;
-        }
+        fma_bcast<R>(acc[0], y, x.x);
+        fma_bcast<R>(acc[1], y, x.y);
+        fma_bcast<R>(acc[2], y, x.z);
+        fma_bcast<R>(acc[3], y, x.w);
+        if constexpr (ONES) { acc1[0] += x.x; acc1[1] += x.y; acc1[2] += x.z; acc1[3] += x.w; }
       }
     }
     __syncthreads();   // every thread is done with stage st
     if (tid < 32 && it + BK_ST < nst) issue(it + BK_ST, st);
   }
-  if (tid >= W) return;
-  const int64_t w = w0 + tid;
-  if constexpr (ONES) ((float*)p.part2)[(int64_t)s * p.w + w] = acc1;
+  // row groups -> one sum per column, RC outputs at a time through the
+  // (now idle) ring: red[g][rc][256]
+  constexpr int RC = R < 8 ? R : 8;
+  float* red = xs;
   float* part = (float*)p.part + (int64_t)s * p.w * p.r;
+  const int64_t w = w0 + tid;
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (r < nr) part[w * p.part_w + r * p.part_r] = acc[r];
+  for (int rb = 0; rb < R; rb += RC) {
+    if (cok)
+#pragma unroll
+      for (int r = 0; r < RC; ++r)
+        *(float4*)(red + (g * RC + r) * THREADS + c4) =
+            make_float4(acc[0][rb + r], acc[1][rb + r], acc[2][rb + r], acc[3][rb + r]);
+    if (ONES && rb == 0 && cok)
+      *(float4*)(red + 4 * RC * THREADS + g * THREADS + c4) = make_float4(acc1[0], acc1[1], acc1[2], acc1[3]);
+    __syncthreads();
+    if (tid < W) {
+#pragma unroll
+      for (int r = 0; r < RC; ++r) {
+        if (rb + r >= nr) break;
+        float v = red[r * THREADS + tid];
+#pragma unroll
+        for (int gg = 1; gg < 4; ++gg) v += red[(gg * RC + r) * THREADS + tid];
+        part[w * p.part_w + (rb + r) * p.part_r] = v;
+      }
+      if (ONES && rb == 0) {
+        const float* r1 = red + 4 * RC * THREADS;
+        ((float*)p.part2)[(int64_t)s * p.w + w] = ((r1[tid] + r1[THREADS + tid]) + r1[2 * THREADS + tid]) + r1[3 * THREADS + tid];
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // variant 2: rows of X (K <= KP values each, zero-padded to KP) times a
@@ -753,7 +777,7 @@ extern "C" void* rt_kernel_thin_bulk(int r, int ones) {
   if (r <= 4) return BK(4);
   if (r <= 8) return BK(8);
   if (r <= 16) return BK(16);
-  return BK(32);
+  return nullptr;   // r > 16: k_thin_contract (4 x 32 accumulators would spill)
 #undef BK
 }
 

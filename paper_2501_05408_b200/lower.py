@@ -2152,7 +2152,7 @@ class Lowering:
                 # k_thin_contract_bulk: 2 CTAs per SM, the splits one wave
                 q.vec = 1
                 q.splits = int(max(1, min(296 // gx, -(-k // 32), 65535)))
-                rp = 4 if q.r <= 4 else 8 if q.r <= 8 else 16 if q.r <= 16 else 32
+                rp = 4 if q.r <= 4 else 8 if q.r <= 8 else 16
                 smem = 3 * 32 * (256 + rp) * 4 + 3 * 8      # BK_ST x BK_SR rows + mbarriers
             else:
                 q.splits = int(max(1, min(k // 256, (148 * 8) // gx, 65535)))
@@ -2188,7 +2188,7 @@ class Lowering:
     def _thin_bulk_ok(self, q):
         """Variant 1 can stream its rows by cp.async.bulk (k_thin_contract_bulk):
         fp32, contiguous 16-byte-aligned X and Y rows at every env offset."""
-        if not self.THIN_BULK or q.f64 or q.r > 32 or q.w % 4 or q.r % 4:
+        if not self.THIN_BULK or q.f64 or q.r > 16 or q.w % 4 or q.r % 4:
             return False
         for g in (q.X, q.Y):
             if g.s2[0] != 1 or g.s1[0] % 4 or g.off % 4 or (g.ptr + 4 * g.off) % 16:
