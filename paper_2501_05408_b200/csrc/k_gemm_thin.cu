@@ -400,7 +400,7 @@ RT_DEV void vfma(double (&acc)[VW], const double (&y)[VW], double x) {
 }
 
 template <typename T, int KP, bool GATE = false, int KP2 = 0>
-__global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__ rt_thin_params p) {
+__global__ void __launch_bounds__(THREADS, KP2 > 0 ? 2 : 1) k_thin_smallv(const __grid_constant__ rt_thin_params p) {
   using V = typename svec2<T>::V;
   constexpr int VW = svec2<T>::W;
   constexpr int RT = 64;  // rows per tile
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_smallv(const __grid_constant__
     __syncthreads();
     // GATE: the h rows of HB row steps are loaded together (one 16-byte load
     // per row in flight per thread left the kernel latency-bound, ~3 TB/s)
-    constexpr int HB = GATE ? 8 : 1;
+    constexpr int HB = GATE ? (KP2 > 0 ? 4 : 8) : 1;   // KP2: 2 CTAs per SM in 128 registers
     for (int rb = rl; rb < nrow; rb += HB * RL) {
     V hvb[HB];
     if constexpr (GATE) {
