@@ -2,7 +2,7 @@
 # C3, C4, reference arm), ncu launch lists (C2, C3), ncu --set full of the top
 # kernels, kernel roofline bench.
 mkdir -p gpurun_out
-P=${PROFILE_TAG:-r2d}
+P=${PROFILE_TAG:-r2f}
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$P.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$P.log
 tail -3 gpurun_out/pytest_gpu_$P.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke_$P.log 2>&1
@@ -17,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv \
   --log-file gpurun_out/launches_c3_$P.csv python bench.py --workload c3 --steps 1 --warmup 3 --no-cpu-baseline \
   > gpurun_out/bench_c3_under_ncu_$P.log 2>&1
-for K in ${NCU_KERNELS:-loop_mlp k_gemm_tmap k_thin_small}; do
+for K in ${NCU_KERNELS:-loop_mlp k_gemm_tmap k_thin_small k_thin_contract_bulk}; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -c 1 \
     -o gpurun_out/full_${P}_$K python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_full_${P}_$K.log 2>&1
@@ -28,6 +28,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ge
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_thin_smallv -c 1 \
   -o gpurun_out/full_${P}_c3_smallv python bench.py --workload c3 --steps 1 --warmup 3 --no-cpu-baseline \
   > gpurun_out/ncu_full_${P}_c3_smallv.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k "regex:smallv<float, .int.4, .bool.1, .int.4>" -c 1 \
+  -o gpurun_out/full_${P}_c3_sumgate python bench.py --workload c3 --steps 1 --warmup 3 --no-cpu-baseline \
+  > gpurun_out/ncu_full_${P}_c3_sumgate.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_scan_tma -c 1 \
   -o gpurun_out/full_${P}_k_scan_tma python bench_kernels.py --only returns_bt --reps 1 \
   > gpurun_out/ncu_full_${P}_k_scan_tma.log 2>&1
