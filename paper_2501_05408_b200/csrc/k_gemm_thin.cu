@@ -672,10 +672,9 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
         for (int i = 0; i < KI; ++i) {
           T xs[VW];
           unpack<T>(xv[rr][i], xs);
+          // acc[rr][r] = fma(x, y[r], acc[rr][r]) per r (FFMA2 on r pairs)
 #pragma unroll
-          for (int j = 0; j < VW; ++j)
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[rr][r] = fma(xs[j], y[i][j][r], acc[rr][r]);
+          for (int j = 0; j < VW; ++j) fma_bcast<R>(acc[rr], y[i][j], xs[j]);
         }
     } else {
 #pragma unroll
@@ -686,8 +685,7 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
           for (int j = 0; j < VW; ++j) {
             const int k = (i * 32 + lane) * VW + j;
             const T x = k < K ? __ldcs(X + xo[rr] + k * xk) : (T)0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[rr][r] = fma(x, y[i][j][r], acc[rr][r]);
+            fma_bcast<R>(acc[rr], y[i][j], x);
           }
     }
     // the RW x R dot products across the warp by recursive halving: at each
