@@ -133,7 +133,7 @@ RT_DEV void bk_wait(uint32_t bar, uint32_t phase) {
 
 template <int R, bool ONES>
 __global__ void __launch_bounds__(THREADS, 2) k_thin_contract_bulk(const __grid_constant__ rt_thin_params p) {
-  extern __shared__ __align__(128) unsigned char sm_raw[];
+  extern __shared__ __align__(16) unsigned char sm_raw[];
   float* xs = (float*)sm_raw;                          // [ST][SR][256]
   float* ys = xs + BK_ST * BK_SR * THREADS;            // [ST][SR][R]
   uint64_t* bars = (uint64_t*)(ys + BK_ST * BK_SR * R);
@@ -608,6 +608,54 @@ template <> RT_DEV void unpack<double>(const double2& v, double* o) { o[0] = v.x
 RT_DEV void unpack_zero(float4& v) { v = make_float4(0.f, 0.f, 0.f, 0.f); }
 RT_DEV void unpack_zero(double2& v) { v = make_double2(0.0, 0.0); }
 
+// the RW x R dot products of a warp (lane partials in acc) reduced and
+// stored with the bias / accumulate / tanh epilogue (k_thin_rows)
+template <typename T, int R, int RW>
+RT_DEV void rows_reduce_store(const rt_thin_params& p, int64_t w0, T (&acc)[RW][R], const T (&bias)[R],
+                              int lane, int r1, T* Cp, int64_t wlim) {
+    // the RW x R dot products across the warp by recursive halving: at each
+    // level a lane keeps half of its values and receives the partner's copy
+    // of that half (NV - 1 + 5 - log2 NV shuffles instead of 5 NV)
+    constexpr int NV = RW * R;
+    constexpr int LG = NV >= 32 ? 5 : NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : NV >= 2 ? 1 : 0;
+    static_assert((1 << LG) == NV, "power-of-two row x output count");
+    T v[NV];
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[rr * R + r] = acc[rr][r];
+#pragma unroll
+    for (int sl = 0; sl < LG; ++sl) {
+      const int n = NV >> sl, o = 16 >> sl;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        const T send = up ? v[i] : v[i + n / 2];
+        const T keep = up ? v[i + n / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+#pragma unroll
+    for (int o = 16 >> LG; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    const T mine = v[0];
+    int idx = 0;
+#pragma unroll
+    for (int sl = 0; sl < LG; ++sl) idx |= ((lane >> (4 - sl)) & 1) << (LG - 1 - sl);
+    if ((lane & ((1 << (5 - LG)) - 1)) == 0) {
+      const int rr = idx / R, r = idx - rr * R;
+      const int64_t w = w0 + rr;
+      if (w < wlim && r < p.r) {
+        T* cptr = r < r1 ? Cp + wdec(p.W, w, p.C.s1) + r * p.C.s2[0]
+                         : (T*)p.C2.ptr + p.C2.off + wdec(p.W, w, p.C2.s1) + (r - r1) * p.C2.s2[0];
+        T a = mine;
+        if (p.accumulate) a += *cptr;
+        a += bias[r];
+        if (p.epilogue == 1) a = epi_tanh<T>(a);
+        *cptr = a;
+      }
+    }
+}
+
 template <typename T, int R, int KI>
 __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ rt_thin_params p) {
   using V = typename vec16<T>::V;
@@ -688,51 +736,121 @@ __global__ void __launch_bounds__(THREADS) k_thin_rows(const __grid_constant__ r
             fma_bcast<R>(acc[rr], y[i][j], x);
           }
     }
-    // the RW x R dot products across the warp by recursive halving: at each
-    // level a lane keeps half of its values and receives the partner's copy
-    // of that half (NV - 1 + 5 - log2 NV shuffles instead of 5 NV)
-    constexpr int NV = RW * R;
-    constexpr int LG = NV >= 32 ? 5 : NV >= 16 ? 4 : NV >= 8 ? 3 : NV >= 4 ? 2 : NV >= 2 ? 1 : 0;
-    static_assert((1 << LG) == NV, "power-of-two row x output count");
-    T v[NV];
-#pragma unroll
-    for (int rr = 0; rr < RW; ++rr)
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[rr * R + r] = acc[rr][r];
-#pragma unroll
-    for (int sl = 0; sl < LG; ++sl) {
-      const int n = NV >> sl, o = 16 >> sl;
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < n / 2; ++i) {
-        const T send = up ? v[i] : v[i + n / 2];
-        const T keep = up ? v[i + n / 2] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
-#pragma unroll
-    for (int o = 16 >> LG; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-    const T mine = v[0];
-    int idx = 0;
-#pragma unroll
-    for (int sl = 0; sl < LG; ++sl) idx |= ((lane >> (4 - sl)) & 1) << (LG - 1 - sl);
-    if ((lane & ((1 << (5 - LG)) - 1)) == 0) {
-      const int rr = idx / R, r = idx - rr * R;
-      const int64_t w = w0 + rr;
-      if (w < p.w && r < p.r) {
-        T* cptr = r < r1 ? Cp + wdec(p.W, w, p.C.s1) + r * p.C.s2[0]
-                         : (T*)p.C2.ptr + p.C2.off + wdec(p.W, w, p.C2.s1) + (r - r1) * p.C2.s2[0];
-        T a = mine;
-        if (p.accumulate) a += *cptr;
-        a += bias[r];
-        if (p.epilogue == 1) a = epi_tanh<T>(a);
-        *cptr = a;
-      }
-    }
+    rows_reduce_store<T, R, RW>(p, w0, acc, bias, lane, r1, Cp, p.w);
   }
 }
 
 }  // namespace
+
+// variant 3 with its rows streamed by cp.async.bulk (p.vec == 2, fp32,
+// K <= 256 contiguous 16-byte-aligned floats per row): the per-warp
+// 16-byte row loads of k_thin_rows left the kernel memory-latency bound
+// (ncu: 41% of DRAM peak, 128 registers for the loads in flight).  CTA s
+// takes a contiguous range of rows; a stage is 8 warps x RW rows, copied
+// one row per lane of warp 0 into a 3-stage mbarrier ring; every warp then
+// runs k_thin_rows' arithmetic on its RW rows from shared memory (same
+// fma order, same reduction: bit-identical outputs).
+template <int R, int KI>
+__global__ void __launch_bounds__(THREADS, 2) k_thin_rows_bulk(const __grid_constant__ rt_thin_params p) {
+  using T = float;
+  using V = float4;
+  constexpr int VW = 4, KP = KI * 32 * VW;
+  constexpr int RW = (R * KI * VW >= 16) ? 4 : 8;
+  constexpr int SR = (THREADS / 32) * RW;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  float* xs = (float*)sm_raw;                          // [ST][SR][KP]
+  uint64_t* bars = (uint64_t*)(xs + BK_ST * SR * KP);
+  const int tid = (int)threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const int K = (int)p.k;
+  const T* X = (const T*)p.X.ptr + p.X.off;
+  const T* Y = (const T*)p.Y.ptr + p.Y.off;
+  T* Cp = (T*)p.C.ptr + p.C.off;
+  const int r1 = (int)(p.r - p.r2);
+  const T* Y2 = (const T*)p.Y2.ptr + p.Y2.off;
+  T y[KI][VW][R];
+#pragma unroll
+  for (int i = 0; i < KI; ++i)
+#pragma unroll
+    for (int j = 0; j < VW; ++j) {
+      const int k = (i * 32 + lane) * VW + j;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        y[i][j][r] = !(k < K && r < p.r) ? (T)0
+                     : r < r1 ? Y[k * p.Y.s1[0] + r * p.Y.s2[0]]
+                              : Y2[k * p.Y2.s1[0] + (r - r1) * p.Y2.s2[0]];
+    }
+  T bias[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    bias[r] = r < r1 ? (p.bias.ptr ? load_as<T>((const void*)p.bias.ptr, p.bias.dtype,
+                                                 p.bias.off + r * p.bias.s2[0]) : (T)0)
+            : r < p.r ? (p.bias2.ptr ? load_as<T>((const void*)p.bias2.ptr, p.bias2.dtype,
+                                                   p.bias2.off + (r - r1) * p.bias2.s2[0]) : (T)0)
+                      : (T)0;
+  const int64_t per = (p.w + gridDim.x - 1) / gridDim.x;
+  const int64_t q0 = (int64_t)blockIdx.x * per;
+  const int64_t q1 = q0 + per < p.w ? q0 + per : p.w;
+  const int nst = q1 > q0 ? (int)((q1 - q0 + SR - 1) / SR) : 0;
+  if (tid == 0) {
+    for (int i = 0; i < BK_ST; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bk_su32(bars + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int it, int st) {       // warp 0: one row per lane
+    const int64_t wb = q0 + (int64_t)it * SR;
+    const int n = (int)(q1 - wb < SR ? q1 - wb : SR);
+    const uint32_t bar = bk_su32(bars + st);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                   ::"r"(bar), "r"((uint32_t)(n * K * 4)) : "memory");
+    __syncwarp();
+    for (int i = lane; i < n; i += 32)
+      bk_copy(bk_su32(xs + (st * SR + i) * KP), X + wdec(p.W, wb + i, p.X.s2), (uint32_t)(K * 4), bar);
+  };
+  if (tid < 32)
+    for (int it = 0; it < BK_ST && it < nst; ++it) issue(it, it);
+  for (int it = 0; it < nst; ++it) {
+    const int st = it % BK_ST;
+    bk_wait(bk_su32(bars + st), (uint32_t)((it / BK_ST) & 1));
+    const int64_t w0 = q0 + (int64_t)it * SR + wp * RW;
+    if (w0 < q1) {
+      T acc[RW][R];
+#pragma unroll
+      for (int rr = 0; rr < RW; ++rr)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[rr][r] = (T)0;
+#pragma unroll
+      for (int rr = 0; rr < RW; ++rr) {
+        const float* xr = xs + (st * SR + wp * RW + rr) * KP;
+#pragma unroll
+        for (int i = 0; i < KI; ++i) {
+          const int k = (i * 32 + lane) * VW;
+          // rows past q1 hold stale data: their outputs are not stored
+          V xv;
+          if (k < K) xv = *reinterpret_cast<const V*>(xr + k);
+          else unpack_zero(xv);
+          T xv_[VW];
+          unpack<T>(xv, xv_);
+#pragma unroll
+          for (int j = 0; j < VW; ++j) fma_bcast<R>(acc[rr], y[i][j], xv_[j]);
+        }
+      }
+      // rows in [q1, p.w) belong to the next CTA: stored only below q1
+      rows_reduce_store<T, R, RW>(p, w0, acc, bias, lane, r1, Cp, q1);
+    }
+    __syncthreads();
+    if (tid < 32 && it + BK_ST < nst) issue(it + BK_ST, st);
+  }
+}
+
+extern "C" void* rt_kernel_thin_rows_bulk(int r, int k) {
+  if (k > 256) return nullptr;
+#define RB(R) if (r <= R) return k <= 128 ? (void*)k_thin_rows_bulk<R, 1> : (void*)k_thin_rows_bulk<R, 2>;
+  RB(1) RB(2) RB(4) RB(8)
+#undef RB
+  return nullptr;
+}
 
 extern "C" void* rt_kernel_thin_rows(int f64, int r, int k) {
 #define RT_ROWS(T, R)                                            \

@@ -23,6 +23,7 @@ extern "C" void* rt_kernel_loop();
 extern "C" void* rt_kernel_gemm_tc();
 extern "C" void* rt_kernel_thin(int variant, int f64, int r);
 extern "C" void* rt_kernel_thin_bulk(int r, int ones);
+extern "C" void* rt_kernel_thin_rows_bulk(int r, int k);
 extern "C" void* rt_kernel_thin_vec(int mode, int f64, int k);
 extern "C" void* rt_kernel_thin_rows(int f64, int r, int k);
 extern "C" void* rt_scan_tma_pack(void* blk, void* encode);
@@ -184,6 +185,7 @@ static void* prepare(int kernel, void* blk, const int64_t* env, int nenv) {
           fold_gop(p->C2, env, nenv);
           if (p->bias2.ptr) fold_gop(p->bias2, env, nenv);
         }
+        if (p->vec == 2) return p->f64 ? nullptr : rt_kernel_thin_rows_bulk((int)p->r, (int)p->k);
         return rt_kernel_thin_rows(p->f64, (int)p->r, (int)p->k);
       }
       // variant 2 with epilogue 2 (gate) is a separate instantiation ("4"),

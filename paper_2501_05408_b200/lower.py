@@ -2387,8 +2387,19 @@ class Lowering:
             self._rows_second = None
         rows_per_cta = 8 * 8
         grid = [int(max(1, min(-(-m // rows_per_cta), 148 * 16))), 1, 1]
-        self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], 0, label)
+        smem = 0
+        if self.ROWS_BULK and q.vec and not f64 and k <= 256:
+            # k_thin_rows_bulk: rows by cp.async.bulk, 2 CTAs per SM
+            rp = 1 if q.r <= 1 else 2 if q.r <= 2 else 4 if q.r <= 4 else 8
+            kin = 1 if k <= 128 else 2
+            rw = 4 if rp * kin * 4 >= 16 else 8
+            q.vec = 2
+            grid = [296, 1, 1]
+            smem = 3 * (8 * rw) * (kin * 128) * 4 + 3 * 8    # BK_ST stages x SR rows x KP
+        self.add_rec(N.RT_K_THIN, q, grid, [256, 1, 1], smem, label)
         return True
+
+    ROWS_BULK = os.environ.get("RTB200_ROWS_BULK", "1") != "0"
 
     @staticmethod
     def _gop_dtype(g):

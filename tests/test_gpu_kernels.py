@@ -211,6 +211,36 @@ def test_narrow_head_rows_gemm(N, K, dt):
     np.testing.assert_allclose(out, want, rtol=tol, atol=tol)
 
 
+@pytest.mark.parametrize("N,K,B", [(4, 256, 20011), (1, 128, 9001), (2, 100, 4099), (3, 256, 70003)])
+def test_narrow_head_rows_bulk_bit_identical(N, K, B):
+    """Variant 3 with rows streamed by cp.async.bulk (k_thin_rows_bulk) gives
+    the bits of the register-load kernel (same fma order and reduction), on
+    ragged row counts (CTA ranges not multiples of a stage), and matches
+    fp64 numpy."""
+    from paper_2501_05408_b200 import executor as X, get_executable, lower as L, native as NN
+    rng = np.random.default_rng(N * 1000 + K + B)
+    x = rng.standard_normal((B, 1, K)).astype(np.float32)
+    W = (rng.standard_normal((K, N)) / 16).astype(np.float32)
+    g = mm_graph(B, K, N)
+    outs = {}
+    cls = [c for c in vars(L).values() if isinstance(c, type) and hasattr(c, "ROWS_BULK")][0]
+    saved = cls.ROWS_BULK
+    try:
+        for bulk in (True, False):
+            cls.ROWS_BULK = bulk
+            X._CACHE.clear()
+            exe, _ = get_executable(g, None, {"x": x, "W": W}, seed=0)
+            thin = [p for k, p in zip(exe.kernels, exe._params) if k == NN.RT_K_THIN]
+            assert thin and thin[0].variant == 3 and (thin[0].vec == 2) == bulk
+            outs[bulk] = execute(g, inputs={"x": x, "W": W})["y"]
+    finally:
+        cls.ROWS_BULK = saved
+        X._CACHE.clear()
+    assert np.array_equal(outs[True], outs[False])
+    want = x[:, 0].astype(np.float64) @ W.astype(np.float64)
+    np.testing.assert_allclose(outs[True][:, 0], want, rtol=1e-5, atol=1e-5)
+
+
 def _scan_graph(layout, n_env, T, dt, forward):
     """G = dsum over a suffix r[t:T] (reverse scan) or, forward, the
     reversed-weight prefix dsum r[0:t+1] (reference runtime.py:108-122),
