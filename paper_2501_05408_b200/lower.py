@@ -2388,11 +2388,14 @@ class Lowering:
         rows_per_cta = 8 * 8
         grid = [int(max(1, min(-(-m // rows_per_cta), 148 * 16))), 1, 1]
         smem = 0
-        if self.ROWS_BULK and q.vec and not f64 and k <= 256:
-            # k_thin_rows_bulk: rows by cp.async.bulk, 2 CTAs per SM
-            rp = 1 if q.r <= 1 else 2 if q.r <= 2 else 4 if q.r <= 4 else 8
-            kin = 1 if k <= 128 else 2
-            rw = 4 if rp * kin * 4 >= 16 else 8
+        rp = 1 if q.r <= 1 else 2 if q.r <= 2 else 4 if q.r <= 4 else 8
+        kin = 1 if k <= 128 else 2
+        rw = 4 if rp * kin * 4 >= 16 else 8
+        # k_thin_rows_bulk: rows by cp.async.bulk, 2 CTAs per SM -- only when
+        # its 3-stage ring fits twice in shared memory (8-row warps over
+        # 256-wide rows would need 192 KB: one CTA per SM, two waves; the
+        # register-load kernel streams those single-output rows at ~6.5 TB/s)
+        if self.ROWS_BULK and q.vec and not f64 and k <= 256 and 3 * (8 * rw) * (kin * 128) * 4 <= 100 * 1024:
             q.vec = 2
             grid = [296, 1, 1]
             smem = 3 * (8 * rw) * (kin * 128) * 4 + 3 * 8    # BK_ST stages x SR rows x KP

@@ -2,7 +2,7 @@
 # C3, C4, reference arm), ncu launch lists (C2, C3), ncu --set full of the top
 # kernels, kernel roofline bench.
 mkdir -p gpurun_out
-P=${PROFILE_TAG:-r2g}
+P=${PROFILE_TAG:-r2h}
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$P.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$P.log
 tail -3 gpurun_out/pytest_gpu_$P.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke_$P.log 2>&1
